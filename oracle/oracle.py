@@ -1,0 +1,339 @@
+"""ctypes bindings for the CPU oracle (liboracle.so) and oracle/_ref.
+
+TEST INFRASTRUCTURE: imported only by tests/, __graft_entry__.smoke() and
+bench.py's cpu-baseline / --impl reference leg. Never part of the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liboracle.so")
+REF_PATH = os.path.join(HERE, "_ref", "libsphemu_ref.so")
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_u8 = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+
+VARIANTS = {"dp": 0, "dpsp": 1, "dpsphp": 2, "dphp": 3}
+
+
+class CholConfig(C.Structure):
+    _fields_ = [("variant", C.c_int), ("tile_size", C.c_int), ("band_width_dp", C.c_int),
+                ("sp_fraction", C.c_double), ("workers", C.c_int), ("hp_format", C.c_int)]
+
+
+class Counters(C.Structure):
+    _fields_ = [("demotions_sp", C.c_int64), ("demotions_hp", C.c_int64),
+                ("half_saturations", C.c_int64)]
+
+
+class CholStats(C.Structure):
+    _fields_ = [("n", C.c_int), ("tile_size", C.c_int), ("n_tiles", C.c_int), ("workers", C.c_int),
+                ("variant", C.c_int), ("tasks_potrf", C.c_int64), ("tasks_trsm", C.c_int64),
+                ("tasks_syrk", C.c_int64), ("tasks_gemm", C.c_int64), ("tiles_dp", C.c_int64),
+                ("tiles_sp", C.c_int64), ("tiles_hp", C.c_int64), ("bytes_dp", C.c_int64),
+                ("bytes_sp", C.c_int64), ("bytes_hp", C.c_int64), ("conv", Counters),
+                ("wall_seconds", C.c_double)]
+
+    def as_dict(self) -> dict:
+        names = ["dp", "dpsp", "dpsphp", "dphp"]
+        return {
+            "n": self.n, "tile_size": self.tile_size, "n_tiles": self.n_tiles,
+            "workers": self.workers, "variant": names[self.variant],
+            "tasks": {"potrf": self.tasks_potrf, "trsm": self.tasks_trsm, "syrk": self.tasks_syrk,
+                      "gemm": self.tasks_gemm,
+                      "total": self.tasks_potrf + self.tasks_trsm + self.tasks_syrk + self.tasks_gemm},
+            "tiles": {"dp": self.tiles_dp, "sp": self.tiles_sp, "hp": self.tiles_hp},
+            "bytes": {"dp": self.bytes_dp, "sp": self.bytes_sp, "hp": self.bytes_hp,
+                      "total": self.bytes_dp + self.bytes_sp + self.bytes_hp},
+            "conversions": {"to_sp": self.conv.demotions_sp, "to_hp": self.conv.demotions_hp,
+                            "half_saturations": self.conv.half_saturations},
+            "wall_seconds": self.wall_seconds,
+        }
+
+
+class NotPositiveDefinite(RuntimeError):
+    def __init__(self, tile_index: int):
+        super().__init__(f"diagonal tile {tile_index} has a non-positive pivot")
+        self.tile_index = tile_index
+
+
+def build(force: bool = False) -> None:
+    """Compile liboracle.so (and oracle/_ref when /root/reference is present)."""
+    if force or not os.path.exists(LIB_PATH) or _stale():
+        subprocess.run(["make", "-s", "-C", HERE], check=True)
+    if os.path.isdir(os.environ.get("SPHEMU_REFERENCE", "/root/reference/proj")) and (
+            force or not os.path.exists(REF_PATH)):
+        subprocess.run([os.path.join(HERE, "ref", "build_ref.sh")], check=True)
+
+
+def _stale() -> bool:
+    t = os.path.getmtime(LIB_PATH)
+    return any(os.path.getmtime(os.path.join(HERE, f)) > t for f in os.listdir(HERE)
+               if f.endswith((".c", ".h")))
+
+
+_lib = None
+_ref = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = C.CDLL(LIB_PATH)
+        L.so_rng_normals.argtypes = [C.c_uint64, C.c_int64, _dp]
+        L.so_quantize_half.argtypes = [C.c_double, C.POINTER(C.c_longlong)]
+        L.so_quantize_half.restype = C.c_double
+        L.so_quantize_bf16.argtypes = [C.c_double, C.POINTER(C.c_longlong)]
+        L.so_quantize_bf16.restype = C.c_double
+        L.so_quantize_tile.argtypes = [_dp, C.c_int64, C.c_int, C.c_int, C.POINTER(Counters)]
+        L.so_assign_precisions.argtypes = [C.c_int, C.POINTER(CholConfig), _u8]
+        L.so_task_count.argtypes = [C.c_int]
+        L.so_task_count.restype = C.c_int64
+        L.so_task_graph.restype = C.c_int64
+        L.so_tiled_cholesky_dense.argtypes = [_dp, C.c_int, C.POINTER(CholConfig), _dp,
+                                              C.POINTER(CholStats), C.POINTER(C.c_int)]
+        L.so_make_spd.argtypes = [C.c_int, C.c_uint64, _dp]
+        L.so_make_spd_factors.argtypes = [C.c_int, C.c_uint64, _dp, _dp]
+        L.so_dense_cholesky.argtypes = [_dp, C.c_int, _dp]
+        L.so_relative_residual.argtypes = [_dp, _dp, C.c_int, C.c_int]
+        L.so_relative_residual.restype = C.c_double
+        L.so_use_blas.argtypes = [C.c_char_p]
+        L.so_i_integral.argtypes = [C.c_longlong, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.so_wigner_build.argtypes = [C.c_int, C.c_size_t]
+        L.so_wigner_build.restype = C.c_void_p
+        L.so_wigner_free.argtypes = [C.c_void_p]
+        L.so_wigner_d.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
+        L.so_wigner_d.restype = C.c_double
+        L.so_wigner_q.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
+        L.so_wigner_q.restype = C.c_double
+        L.so_wigner_renorm_warnings.argtypes = [C.c_void_p]
+        L.so_wigner_bytes.argtypes = [C.c_int]
+        L.so_wigner_bytes.restype = C.c_size_t
+        L.so_wigner_brute.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.so_wigner_brute.restype = C.c_double
+        L.so_plan_build.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.so_plan_build.restype = C.c_void_p
+        L.so_plan_free.argtypes = [C.c_void_p]
+        L.so_forward_sht_batch.argtypes = [C.c_void_p, _dp, C.c_int64, _dp, C.c_int]
+        L.so_inverse_sht_batch.argtypes = [C.c_void_p, _dp, C.c_int64, _dp, C.c_int]
+        L.so_normalized_legendre_all.argtypes = [C.c_int, C.c_double, _dp]
+        L.so_synth_bandlimited.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp]
+        L.so_draw_random_coefficients.argtypes = [C.c_int, C.c_uint64, _dp]
+        L.so_field_energy_quadrature.argtypes = [_dp, C.c_int, C.c_int]
+        L.so_field_energy_quadrature.restype = C.c_double
+        L.so_parseval_energy.argtypes = [_dp, C.c_int]
+        L.so_parseval_energy.restype = C.c_double
+        L.so_dft.argtypes = [C.c_int, C.c_int, _dp, _dp]
+        L.so_estimate_innovation_covariance.argtypes = [
+            _dp, C.c_int64, C.c_int, C.POINTER(CholConfig), C.c_int, _dp, _dp,
+            C.POINTER(C.c_double), C.POINTER(CholStats)]
+        L.so_emulate.argtypes = [C.c_void_p, _dp, C.c_int, _dp, C.c_int, _dp, _dp, _dp, C.c_int,
+                                 C.c_uint64, C.c_int, C.c_int, _dp]
+        _lib = L
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_PATH)
+
+
+def ref():
+    """The reference's own wigner/grid/sht/half/rng code (oracle/_ref)."""
+    global _ref
+    if _ref is None:
+        R = C.CDLL(REF_PATH)
+        R.ref_quantize_half.argtypes = [C.c_double, C.POINTER(C.c_longlong)]
+        R.ref_quantize_half.restype = C.c_double
+        R.ref_rng_normals.argtypes = [C.c_uint64, C.c_int64, _dp]
+        R.ref_rng_uniforms.argtypes = [C.c_uint64, C.c_int64, _dp]
+        R.ref_i_integral.argtypes = [C.c_longlong, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        R.ref_wigner_dump.argtypes = [C.c_int, _dp, _dp, C.POINTER(C.c_int)]
+        R.ref_wigner_check_cap.argtypes = [C.c_int, C.c_size_t]
+        R.ref_wigner_brute.argtypes = [C.c_int, C.c_int, C.c_int]
+        R.ref_wigner_brute.restype = C.c_double
+        R.ref_forward_sht_batch.argtypes = [C.c_int, C.c_int, C.c_int, _dp, C.c_int64, _dp, C.c_int]
+        R.ref_inverse_sht_batch.argtypes = [C.c_int, C.c_int, C.c_int, _dp, C.c_int64, _dp, C.c_int]
+        R.ref_forward_sht_via_weights.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp]
+        R.ref_draw_random_coefficients.argtypes = [C.c_int, C.c_uint64, _dp]
+        R.ref_synth_bandlimited.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp]
+        R.ref_normalized_legendre_all.argtypes = [C.c_int, C.c_double, _dp]
+        R.ref_field_energy_quadrature.argtypes = [_dp, C.c_int, C.c_int]
+        R.ref_field_energy_quadrature.restype = C.c_double
+        _ref = R
+    return _ref
+
+
+# ----------------------------------------------------------------------------
+# numpy-level helpers
+# ----------------------------------------------------------------------------
+
+def config(variant="dp", tile_size=128, band_width_dp=1, sp_fraction=0.05, workers=1,
+           hp_format="fp16") -> CholConfig:
+    return CholConfig(VARIANTS[variant] if isinstance(variant, str) else variant, tile_size,
+                      band_width_dp, sp_fraction, workers, 1 if hp_format == "bf16" else 0)
+
+
+def normals(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n)
+    lib().so_rng_normals(seed, n, out)
+    return out
+
+
+def make_spd(n: int, seed: int = 1) -> np.ndarray:
+    a = np.empty((n, n))
+    lib().so_make_spd(n, seed, a)
+    return a
+
+
+def spd_factors(n: int, seed: int = 1):
+    d = np.empty(n)
+    pw = np.empty(n)
+    lib().so_make_spd_factors(n, seed, d, pw)
+    return d, pw
+
+
+def assign_precisions(n_tiles: int, **kw) -> np.ndarray:
+    out = np.empty(n_tiles * (n_tiles + 1) // 2, dtype=np.uint8)
+    rc = lib().so_assign_precisions(n_tiles, C.byref(config(**kw)), out)
+    if rc:
+        raise ValueError("invalid configuration")
+    return out
+
+
+def task_graph(n_tiles: int):
+    cnt = lib().so_task_count(n_tiles)
+    kind = np.empty(cnt, dtype=np.uint8)
+    ti, tj, tk, indeg = (np.empty(cnt, dtype=np.int32) for _ in range(4))
+    off = np.empty(cnt + 1, dtype=np.int64)
+    cap = 8 * cnt + 16
+    succ = np.empty(cap, dtype=np.int32)
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)
+    lib().so_task_graph.argtypes = [C.c_int] + [C.c_void_p] * 7 + [C.c_int64]
+    edges = lib().so_task_graph(n_tiles, ptr(kind), ptr(ti), ptr(tj), ptr(tk), ptr(off),
+                                ptr(succ), ptr(indeg), cap)
+    return dict(kind=kind, i=ti, j=tj, k=tk, succ_off=off, succ=succ[:edges], indegree=indeg)
+
+
+def quantize(x: np.ndarray, prec: int, hp_format="fp16"):
+    y = np.ascontiguousarray(x, dtype=np.float64).copy()
+    c = Counters()
+    lib().so_quantize_tile(y, y.size, prec, 1 if hp_format == "bf16" else 0, C.byref(c))
+    return y, c
+
+
+def tiled_cholesky(a: np.ndarray, variant="dp", tile_size=128, workers=1, band_width_dp=1,
+                   sp_fraction=0.05, hp_format="fp16"):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    n = a.shape[0]
+    out = np.empty_like(a)
+    st = CholStats()
+    failed = C.c_int(-1)
+    cfg = config(variant, tile_size, band_width_dp, sp_fraction, workers, hp_format)
+    rc = lib().so_tiled_cholesky_dense(a, n, C.byref(cfg), out, C.byref(st), C.byref(failed))
+    if rc == 1:
+        raise NotPositiveDefinite(failed.value)
+    if rc:
+        raise ValueError("invalid configuration")
+    return out, st.as_dict()
+
+
+def dense_cholesky(a: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    out = np.empty_like(a)
+    if lib().so_dense_cholesky(a, a.shape[0], out):
+        raise RuntimeError("matrix is not positive definite")
+    return out
+
+
+def relative_residual(a: np.ndarray, l: np.ndarray, threads: int = 0) -> float:
+    threads = threads or os.cpu_count() or 1
+    return lib().so_relative_residual(np.ascontiguousarray(a), np.ascontiguousarray(l),
+                                      a.shape[0], threads)
+
+
+class Wigner:
+    def __init__(self, band_limit: int, cap: int = 2 << 30):
+        self.L = band_limit
+        self.h = lib().so_wigner_build(band_limit, cap)
+        if not self.h:
+            raise ValueError("Wigner tables over the memory cap")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().so_wigner_free(self.h)
+
+    def d(self, l, m2, m):
+        return lib().so_wigner_d(self.h, l, m2, m)
+
+    def q(self, l, m, m2):
+        return lib().so_wigner_q(self.h, l, m, m2)
+
+    @property
+    def renorm_warnings(self):
+        return lib().so_wigner_renorm_warnings(self.h)
+
+
+class Plan:
+    def __init__(self, n_theta: int, n_phi: int, band_limit: int):
+        self.n_theta, self.n_phi, self.L = n_theta, n_phi, band_limit
+        self.h = lib().so_plan_build(n_theta, n_phi, band_limit, None)
+        if not self.h:
+            raise ValueError(f"grid {n_theta}x{n_phi} does not resolve band limit {band_limit}")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().so_plan_free(self.h)
+
+    def forward(self, fields: np.ndarray, threads: int = 1) -> np.ndarray:
+        f = np.ascontiguousarray(fields, dtype=np.float64).reshape(-1, self.n_theta * self.n_phi)
+        out = np.empty((f.shape[0], self.L * self.L))
+        lib().so_forward_sht_batch(self.h, f, f.shape[0], out, threads)
+        return out
+
+    def inverse(self, coeffs: np.ndarray, threads: int = 1) -> np.ndarray:
+        c = np.ascontiguousarray(coeffs, dtype=np.float64).reshape(-1, self.L * self.L)
+        out = np.empty((c.shape[0], self.n_theta, self.n_phi))
+        lib().so_inverse_sht_batch(self.h, c, c.shape[0], out, threads)
+        return out
+
+
+def draw_random_coefficients(band_limit: int, seed: int) -> np.ndarray:
+    out = np.empty(band_limit * band_limit)
+    lib().so_draw_random_coefficients(band_limit, seed, out)
+    return out
+
+
+def emulate(plan: Plan, v, phi, means, sigma, v2, t_out, seed, r_len=1, threads=1):
+    d = v.shape[0]
+    order = 0 if phi is None else phi.shape[0]
+    phi_a = np.ascontiguousarray(phi if order else np.zeros((1, d)), dtype=np.float64)
+    out = np.empty((r_len, t_out, plan.n_theta, plan.n_phi))
+    lib().so_emulate(plan.h, np.ascontiguousarray(v), d, phi_a, order,
+                     np.ascontiguousarray(means), np.ascontiguousarray(sigma),
+                     np.ascontiguousarray(v2), t_out, seed, r_len, threads, out)
+    return out
+
+
+def stats_json(stats: dict) -> str:
+    return json.dumps(stats, indent=2) + "\n"
+
+
+def find_openblas():
+    """scipy's bundled OpenBLAS: the oracle's stand-in for Eigen's tile BLAS."""
+    try:
+        import scipy  # noqa: F401
+        d = os.path.join(os.path.dirname(os.path.dirname(scipy.__file__)), "scipy.libs")
+        for f in sorted(os.listdir(d)):
+            if f.startswith("libscipy_openblas") and f.endswith(".so"):
+                return os.path.join(d, f)
+    except Exception:
+        pass
+    return None
