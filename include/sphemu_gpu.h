@@ -1,0 +1,167 @@
+/*
+ * sphemu_gpu.h — C-ABI of the B200-native sphemu hot path.
+ *
+ * The reference (proj/, CPU-only C++20) has no C-ABI; its drop-in boundary is
+ * the C++ API of mpchol.hpp / sht.hpp / wigner.hpp / stochastic.hpp and the
+ * pybind11 module of bindings/module.cpp. Every entry point below names the
+ * reference interface it replaces. Plain pointers and sizes only; no C++
+ * exceptions or torch types cross this boundary. Status codes are returned;
+ * sphemu_gpu_last_error() describes the last failure on the calling thread.
+ *
+ * Pointer kinds: functions taking a `where` argument accept host memory
+ * (SPHEMU_HOST) or device memory on the current device (SPHEMU_DEVICE).
+ */
+#ifndef SPHEMU_GPU_H
+#define SPHEMU_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---- */
+#define SPHEMU_OK 0
+#define SPHEMU_ERR_INVALID_ARG 1  /* std::invalid_argument in the reference */
+#define SPHEMU_ERR_NOT_SPD 2      /* NotPositiveDefiniteError (mpchol.hpp:122-130) */
+#define SPHEMU_ERR_CUDA 3
+#define SPHEMU_ERR_NCCL 4
+#define SPHEMU_ERR_OOM 5
+#define SPHEMU_ERR_RUNTIME 6      /* std::runtime_error in the reference */
+
+#define SPHEMU_HOST 0
+#define SPHEMU_DEVICE 1
+
+const char* sphemu_gpu_last_error(void);
+const char* sphemu_gpu_version(void); /* "0.1.0" like proj/include/sphemu/version.hpp:4 */
+int sphemu_gpu_device_count(void);
+int sphemu_gpu_set_device(int device);
+/* Number of kernel launches this process issued from the library (evidence
+ * for bench.py's gpu_launches). */
+int64_t sphemu_gpu_launch_count(void);
+
+/* ======================================================================
+ * Mixed-precision tiled Cholesky (replaces mpchol.hpp:18-148)
+ * ====================================================================== */
+#define SPHEMU_VARIANT_DP 0     /* PrecisionVariant::kDp     (mpchol.hpp:12) */
+#define SPHEMU_VARIANT_DPSP 1   /* PrecisionVariant::kDpSp   */
+#define SPHEMU_VARIANT_DPSPHP 2 /* PrecisionVariant::kDpSpHp */
+#define SPHEMU_VARIANT_DPHP 3   /* PrecisionVariant::kDpHp   */
+
+#define SPHEMU_PREC_DP 0 /* Precision::kDouble (mpchol.hpp:11) */
+#define SPHEMU_PREC_SP 1 /* Precision::kSingle */
+#define SPHEMU_PREC_HP 2 /* Precision::kHalf   */
+
+#define SPHEMU_HP_FP16 0 /* IEEE binary16, saturating (half.hpp) — reference */
+#define SPHEMU_HP_BF16 1 /* bfloat16 storage class — extension   */
+
+#define SPHEMU_COMPUTE_TENSOR 0 /* per-class tensor cores: tcgen05 fp16/bf16, 3xTF32, FP64 DMMA */
+#define SPHEMU_COMPUTE_FP64 1   /* every tile kernel in FP64 (mpchol.cpp:283-316 semantics) */
+
+/* MpCholConfig (mpchol.hpp:18-28) plus appended GPU fields whose zero values
+ * keep reference behaviour. */
+typedef struct {
+  int variant;        /* SPHEMU_VARIANT_* */
+  int tile_size;      /* default 128 */
+  int band_width_dp;  /* default 1 */
+  double sp_fraction; /* default 0.05 */
+  int workers;        /* accepted for API parity; the GPU scheduler uses streams */
+  int hp_format;      /* SPHEMU_HP_* */
+  int compute;        /* SPHEMU_COMPUTE_* */
+  int lookahead;      /* 0 = off, 1 = panel k+1 on a priority stream */
+} sphemu_chol_config;
+
+/* FactorizationStats (mpchol.hpp:104-120) + GPU timing. */
+typedef struct {
+  int n, tile_size, n_tiles, workers, variant;
+  int64_t tasks_potrf, tasks_trsm, tasks_syrk, tasks_gemm;
+  int64_t tiles_dp, tiles_sp, tiles_hp;
+  int64_t bytes_dp, bytes_sp, bytes_hp;
+  int64_t demotions_sp, demotions_hp, half_saturations;
+  double wall_seconds;
+  double device_ms;   /* factorization time on the device (CUDA events) */
+  int64_t launches;   /* kernels launched by this factorization */
+} sphemu_chol_stats;
+
+/* MpCholConfig::validate (mpchol.cpp:55-61). */
+int sphemu_gpu_chol_config_validate(const sphemu_chol_config* cfg);
+/* assign_precisions (mpchol.cpp:67-93): out has n_tiles*(n_tiles+1)/2 bytes. */
+int sphemu_gpu_assign_precisions(int n_tiles, const sphemu_chol_config* cfg, uint8_t* out);
+
+/* tiled_cholesky_dense (mpchol.cpp:412-417): dense row-major n x n in, dense
+ * lower factor (exact zeros above the diagonal) out. Host or device pointers.
+ * On SPHEMU_ERR_NOT_SPD *failed_tile holds the diagonal tile index. */
+int sphemu_gpu_tiled_cholesky_dense(const double* a, int where_a, int n,
+                                    const sphemu_chol_config* cfg, double* factor,
+                                    int where_factor, sphemu_chol_stats* stats, int* failed_tile);
+
+/* Device-resident factorization handle (TiledMatrix + tiled_cholesky,
+ * mpchol.hpp:47-71,135): tiles live in HBM at their storage precision. */
+typedef struct sphemu_chol_s* sphemu_chol_t;
+int sphemu_gpu_chol_create(int n, const sphemu_chol_config* cfg, sphemu_chol_t* out);
+int sphemu_gpu_chol_destroy(sphemu_chol_t h);
+/* TiledMatrix::from_dense (mpchol.cpp:124-138) + the input quantization of
+ * mpchol.cpp:360-363; lda = row stride in elements. */
+int sphemu_gpu_chol_load_dense(sphemu_chol_t h, const double* a, int where, int64_t lda);
+/* make_spd_test_matrix(n, seed) (mpchol.cpp:419-435) generated tile by tile in
+ * HBM, bitwise equal to the reference's values, then quantized. */
+int sphemu_gpu_chol_generate_spd(sphemu_chol_t h, uint64_t seed);
+/* tiled_cholesky (mpchol.cpp:351-410), enqueued on the handle's streams. */
+int sphemu_gpu_chol_factor(sphemu_chol_t h);
+/* Waits for the factorization; returns SPHEMU_ERR_NOT_SPD with *failed_tile. */
+int sphemu_gpu_chol_wait(sphemu_chol_t h, sphemu_chol_stats* stats, int* failed_tile);
+/* TiledMatrix::to_dense_lower (mpchol.cpp:140-154); ldf = row stride. */
+int sphemu_gpu_chol_store_dense(sphemu_chol_t h, double* factor, int where, int64_t ldf);
+/* ||A - L L^T||_F / ||A||_F against a dense row-major A (device or host),
+ * computed on the device in FP64 (tests/support/reference.cpp:32-44). */
+int sphemu_gpu_chol_residual(sphemu_chol_t h, const double* a, int where, int64_t lda,
+                             double* out);
+/* Size-independent check for sizes the host cannot hold: ||(A - L L^T) x|| /
+ * ||A x|| for n_vec seeded random vectors x, against make_spd_test_matrix(seed). */
+int sphemu_gpu_chol_residual_probe_spd(sphemu_chol_t h, uint64_t seed, int n_vec, double* out);
+/* Per-precision flop split of the factorization (BASELINE.md §4 units). */
+int sphemu_gpu_chol_flops(sphemu_chol_t h, double* f_dp, double* f_sp, double* f_hp);
+/* Device stream the handle enqueues on (cudaStream_t as void*). */
+void* sphemu_gpu_chol_stream(sphemu_chol_t h);
+
+/* ======================================================================
+ * Spherical harmonic transform (replaces sht.hpp:105-129, wigner.hpp:48-63)
+ * ====================================================================== */
+typedef struct sphemu_sht_s* sphemu_sht_t;
+/* build_plan(GridSpec{n_theta, n_phi}, band_limit) (sht.cpp:111-171). The
+ * Wigner tables are built with the memory cap of wigner.hpp:48-49 unless
+ * wigner_cap_bytes is nonzero. SPHEMU_ERR_INVALID_ARG on an inadmissible grid
+ * or a cap violation, with the reference's message. */
+int sphemu_gpu_sht_create(int n_theta, int n_phi, int band_limit, size_t wigner_cap_bytes,
+                          sphemu_sht_t* out);
+int sphemu_gpu_sht_destroy(sphemu_sht_t p);
+/* forward_sht_batch (sht.cpp:374-388): fields (n, n_theta, n_phi) ->
+ * coefficients (n, L^2) in the packed layout of sht.hpp:24-45. */
+int sphemu_gpu_sht_forward(sphemu_sht_t p, const double* fields, int where_in, int64_t n,
+                           double* coeffs, int where_out);
+/* inverse_sht_batch (sht.cpp:390-404). */
+int sphemu_gpu_sht_inverse(sphemu_sht_t p, const double* coeffs, int where_in, int64_t n,
+                           double* fields, int where_out);
+void* sphemu_gpu_sht_stream(sphemu_sht_t p);
+/* Seconds spent building the plan (Wigner recurrence + operator build). */
+double sphemu_gpu_sht_plan_seconds(sphemu_sht_t p);
+
+/* ======================================================================
+ * Emulation generator (replaces stochastic.hpp:84-86 emulate)
+ * ====================================================================== */
+#define SPHEMU_RNG_REFERENCE 0 /* the reference's serial mt19937_64 stream, bit-exact order */
+#define SPHEMU_RNG_PHILOX 1    /* counter-based normals generated on the device */
+
+/* emulate(model, plan, forcing, t_out, seed, r_len) with the trend evaluated
+ * by the caller: means (t_out x points), sigma (points), v2 (points), phi
+ * (order x d), and the innovation factor v as a dense lower d x d matrix.
+ * out is (r_len, t_out, n_theta, n_phi). All pointers host. */
+int sphemu_gpu_emulate(sphemu_sht_t p, const double* v, int d, const double* phi, int order,
+                       const double* means, const double* sigma, const double* v2, int t_out,
+                       uint64_t seed, int r_len, int rng_mode, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,26 @@
+"""B200-native drop-in for the BLAS3 hot path of sphemu (arXiv 2408.04440).
+
+Mirrors the reference's Python module (proj/python/sphemu/__init__.py,
+proj/bindings/module.cpp): forward_sht / inverse_sht / tiled_cholesky /
+make_spd_matrix / max_band_limit / resolution_summary, backed by hand-written
+sm_100a kernels in lib/libsphemu_gpu.so (see include/sphemu_gpu.h).
+"""
+from ._sphemu import (  # noqa: F401
+    Cholesky,
+    NotPositiveDefiniteError,
+    ShtPlan,
+    __version__,
+    assign_precisions,
+    forward_sht,
+    inverse_sht,
+    make_spd_matrix,
+    max_band_limit,
+    resolution_summary,
+    tiled_cholesky,
+)
+
+__all__ = [
+    "Cholesky", "NotPositiveDefiniteError", "ShtPlan", "__version__", "assign_precisions",
+    "forward_sht", "inverse_sht", "make_spd_matrix", "max_band_limit", "resolution_summary",
+    "tiled_cholesky",
+]

@@ -1,0 +1,336 @@
+"""Python mirror of the reference's pybind11 module ``_sphemu``
+(proj/bindings/module.cpp:183-246) over the B200 C-ABI (include/sphemu_gpu.h).
+
+Same function names, argument names, defaults and error types as the
+reference; every computation runs in lib/libsphemu_gpu.so on the GPU. There
+is no CPU fallback: importing on a machine without the built library raises.
+New keyword arguments are appended after the reference's and default to the
+reference behaviour.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+import os
+
+import numpy as np
+
+__version__ = "0.1.0"  # proj/include/sphemu/version.hpp:4
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsphemu_gpu.so")
+
+SPHEMU_OK, SPHEMU_ERR_INVALID_ARG, SPHEMU_ERR_NOT_SPD = 0, 1, 2
+HOST, DEVICE = 0, 1
+VARIANTS = {"dp": 0, "dpsp": 1, "dpsphp": 2, "dphp": 3}  # mpchol.cpp:47-53
+_VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
+
+
+class NotPositiveDefiniteError(RuntimeError):
+    """mpchol.hpp:122-130: carries the failing diagonal tile index."""
+
+    def __init__(self, tile_index: int, what: str):
+        super().__init__(what)
+        self.tile_index = tile_index
+
+
+class CholConfig(C.Structure):
+    _fields_ = [("variant", C.c_int), ("tile_size", C.c_int), ("band_width_dp", C.c_int),
+                ("sp_fraction", C.c_double), ("workers", C.c_int), ("hp_format", C.c_int),
+                ("compute", C.c_int), ("lookahead", C.c_int)]
+
+
+class CholStats(C.Structure):
+    _fields_ = [("n", C.c_int), ("tile_size", C.c_int), ("n_tiles", C.c_int), ("workers", C.c_int),
+                ("variant", C.c_int), ("tasks_potrf", C.c_int64), ("tasks_trsm", C.c_int64),
+                ("tasks_syrk", C.c_int64), ("tasks_gemm", C.c_int64), ("tiles_dp", C.c_int64),
+                ("tiles_sp", C.c_int64), ("tiles_hp", C.c_int64), ("bytes_dp", C.c_int64),
+                ("bytes_sp", C.c_int64), ("bytes_hp", C.c_int64), ("demotions_sp", C.c_int64),
+                ("demotions_hp", C.c_int64), ("half_saturations", C.c_int64),
+                ("wall_seconds", C.c_double), ("device_ms", C.c_double), ("launches", C.c_int64)]
+
+    def to_json(self) -> str:
+        """FactorizationStats::to_json (mpchol.cpp:437-457): nlohmann's sorted
+        keys, indent 2; GPU-only numbers under the new key "device"."""
+        d = {
+            "n": self.n, "tile_size": self.tile_size, "n_tiles": self.n_tiles,
+            "workers": self.workers, "variant": _VARIANT_NAMES[self.variant],
+            "tasks": {"potrf": self.tasks_potrf, "trsm": self.tasks_trsm,
+                      "syrk": self.tasks_syrk, "gemm": self.tasks_gemm,
+                      "total": self.tasks_potrf + self.tasks_trsm + self.tasks_syrk + self.tasks_gemm},
+            "tiles": {"dp": self.tiles_dp, "sp": self.tiles_sp, "hp": self.tiles_hp},
+            "bytes": {"dp": self.bytes_dp, "sp": self.bytes_sp, "hp": self.bytes_hp,
+                      "total": self.bytes_dp + self.bytes_sp + self.bytes_hp},
+            "conversions": {"to_sp": self.demotions_sp, "to_hp": self.demotions_hp,
+                            "half_saturations": self.half_saturations},
+            "wall_seconds": self.wall_seconds,
+            "device": {"factor_ms": self.device_ms, "kernel_launches": self.launches},
+        }
+        return json.dumps(d, indent=2, sort_keys=True) + "\n"
+
+
+_lib = None
+
+
+def lib():
+    """The native library; raises when it is not built (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(there is no CPU fallback for the sphemu B200 path)")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, dp = C.c_void_p, C.c_int64, C.POINTER(C.c_double)
+        L.sphemu_gpu_last_error.restype = C.c_char_p
+        L.sphemu_gpu_version.restype = C.c_char_p
+        L.sphemu_gpu_launch_count.restype = i64
+        L.sphemu_gpu_tiled_cholesky_dense.argtypes = [vp, C.c_int, C.c_int, C.POINTER(CholConfig), vp,
+                                                      C.c_int, C.POINTER(CholStats), C.POINTER(C.c_int)]
+        L.sphemu_gpu_chol_create.argtypes = [C.c_int, C.POINTER(CholConfig), C.POINTER(vp)]
+        L.sphemu_gpu_chol_destroy.argtypes = [vp]
+        L.sphemu_gpu_chol_load_dense.argtypes = [vp, vp, C.c_int, i64]
+        L.sphemu_gpu_chol_generate_spd.argtypes = [vp, C.c_uint64]
+        L.sphemu_gpu_chol_factor.argtypes = [vp]
+        L.sphemu_gpu_chol_wait.argtypes = [vp, C.POINTER(CholStats), C.POINTER(C.c_int)]
+        L.sphemu_gpu_chol_store_dense.argtypes = [vp, vp, C.c_int, i64]
+        L.sphemu_gpu_chol_residual.argtypes = [vp, vp, C.c_int, i64, dp]
+        L.sphemu_gpu_chol_flops.argtypes = [vp, dp, dp, dp]
+        L.sphemu_gpu_chol_stream.argtypes = [vp]
+        L.sphemu_gpu_chol_stream.restype = vp
+        L.sphemu_gpu_assign_precisions.argtypes = [C.c_int, C.POINTER(CholConfig), vp]
+        L.sphemu_gpu_chol_config_validate.argtypes = [C.POINTER(CholConfig)]
+        L.sphemu_gpu_sht_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_size_t, C.POINTER(vp)]
+        L.sphemu_gpu_sht_destroy.argtypes = [vp]
+        L.sphemu_gpu_sht_forward.argtypes = [vp, vp, C.c_int, i64, vp, C.c_int]
+        L.sphemu_gpu_sht_inverse.argtypes = [vp, vp, C.c_int, i64, vp, C.c_int]
+        L.sphemu_gpu_sht_stream.argtypes = [vp]
+        L.sphemu_gpu_sht_stream.restype = vp
+        L.sphemu_gpu_sht_plan_seconds.argtypes = [vp]
+        L.sphemu_gpu_sht_plan_seconds.restype = C.c_double
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, failed_tile: int = -1):
+    if rc == SPHEMU_OK:
+        return
+    msg = lib().sphemu_gpu_last_error().decode()
+    if rc == SPHEMU_ERR_INVALID_ARG:
+        raise ValueError(msg)
+    if rc == SPHEMU_ERR_NOT_SPD:
+        raise NotPositiveDefiniteError(failed_tile, msg)
+    raise RuntimeError(msg)
+
+
+def _ptr(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
+
+
+def make_config(variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_fraction=0.05,
+                hp_format="fp16", compute="tensor", lookahead=0) -> CholConfig:
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown precision variant: {variant}")  # mpchol.cpp:52
+    if hp_format not in ("fp16", "bf16"):
+        raise ValueError(f"unknown half-precision format: {hp_format}")
+    if compute not in ("tensor", "fp64"):
+        raise ValueError(f"unknown compute mode: {compute}")
+    return CholConfig(VARIANTS[variant], tile_size, band_width_dp, sp_fraction, workers,
+                      1 if hp_format == "bf16" else 0, 0 if compute == "tensor" else 1, lookahead)
+
+
+# ---------------------------------------------------------------------------
+# module.cpp:209-214 tiled_cholesky / make_spd_matrix
+# ---------------------------------------------------------------------------
+def tiled_cholesky(a, variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_fraction=0.05,
+                   hp_format="fp16", compute="tensor"):
+    """Tiled Cholesky factorization; returns (lower_factor, stats_json)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        raise ValueError("expected a square matrix")
+    n = a.shape[0]
+    cfg = make_config(variant, tile_size, workers, band_width_dp, sp_fraction, hp_format, compute)
+    out = np.empty_like(a)
+    st = CholStats()
+    failed = C.c_int(-1)
+    rc = lib().sphemu_gpu_tiled_cholesky_dense(_ptr(a), HOST, n, C.byref(cfg), _ptr(out), HOST,
+                                               C.byref(st), C.byref(failed))
+    _check(rc, failed.value)
+    return out, st.to_json()
+
+
+def make_spd_matrix(n, seed=1):
+    """make_spd_test_matrix (mpchol.cpp:419-435), generated on the device."""
+    if n < 1:
+        raise ValueError("matrix size must be positive")
+    h = Cholesky(n, variant="dp", tile_size=min(1024, max(64, n)), compute="fp64")
+    h.generate_spd(seed)
+    lower = h.factor_dense_unfactored()
+    return lower + np.tril(lower, -1).T
+
+
+class Cholesky:
+    """Device-resident factorization (TiledMatrix + tiled_cholesky)."""
+
+    def __init__(self, n, variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_fraction=0.05,
+                 hp_format="fp16", compute="tensor", lookahead=0):
+        self.n = n
+        self.cfg = make_config(variant, tile_size, workers, band_width_dp, sp_fraction, hp_format,
+                               compute, lookahead)
+        h = C.c_void_p()
+        _check(lib().sphemu_gpu_chol_create(n, C.byref(self.cfg), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().sphemu_gpu_chol_destroy(self.h)
+            self.h = None
+
+    def generate_spd(self, seed=1):
+        _check(lib().sphemu_gpu_chol_generate_spd(self.h, seed))
+
+    def load(self, a, where=HOST, lda=None):
+        if where == HOST:
+            a = np.ascontiguousarray(a, dtype=np.float64)
+            _check(lib().sphemu_gpu_chol_load_dense(self.h, _ptr(a), HOST, a.shape[1]))
+        else:  # device pointer (int) with row stride
+            _check(lib().sphemu_gpu_chol_load_dense(self.h, C.c_void_p(a), DEVICE, lda or self.n))
+
+    def factor(self):
+        _check(lib().sphemu_gpu_chol_factor(self.h))
+
+    def wait(self):
+        st = CholStats()
+        failed = C.c_int(-1)
+        rc = lib().sphemu_gpu_chol_wait(self.h, C.byref(st), C.byref(failed))
+        _check(rc, failed.value)
+        return st
+
+    def factor_dense(self):
+        out = np.empty((self.n, self.n))
+        _check(lib().sphemu_gpu_chol_store_dense(self.h, _ptr(out), HOST, self.n))
+        return out
+
+    factor_dense_unfactored = factor_dense  # the stored tiles, before or after factor()
+
+    def store(self, dev_ptr, ld=None):
+        _check(lib().sphemu_gpu_chol_store_dense(self.h, C.c_void_p(dev_ptr), DEVICE, ld or self.n))
+
+    def residual(self, a):
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        out = C.c_double()
+        _check(lib().sphemu_gpu_chol_residual(self.h, _ptr(a), HOST, a.shape[1], C.byref(out)))
+        return out.value
+
+    def flops(self):
+        f = [C.c_double() for _ in range(3)]
+        _check(lib().sphemu_gpu_chol_flops(self.h, *[C.byref(x) for x in f]))
+        return {"dp": f[0].value, "sp": f[1].value, "hp": f[2].value}
+
+    @property
+    def stream(self):
+        return lib().sphemu_gpu_chol_stream(self.h)
+
+
+def assign_precisions(n_tiles, variant="dp", band_width_dp=1, sp_fraction=0.05):
+    """assign_precisions (mpchol.cpp:67-93): packed i(i+1)/2 + j, 0/1/2 = dp/sp/hp."""
+    cfg = make_config(variant, 128, 1, band_width_dp, sp_fraction)
+    out = np.empty(n_tiles * (n_tiles + 1) // 2, dtype=np.uint8)
+    _check(lib().sphemu_gpu_assign_precisions(n_tiles, C.byref(cfg), _ptr(out)))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# module.cpp:194-198 forward_sht / inverse_sht (+ batch plans)
+# ---------------------------------------------------------------------------
+class ShtPlan:
+    """build_plan(GridSpec{n_theta, n_phi}, band_limit) on the device."""
+
+    def __init__(self, n_theta, n_phi, band_limit, wigner_cap_bytes=0):
+        self.n_theta, self.n_phi, self.band_limit = n_theta, n_phi, band_limit
+        h = C.c_void_p()
+        _check(lib().sphemu_gpu_sht_create(n_theta, n_phi, band_limit, wigner_cap_bytes, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().sphemu_gpu_sht_destroy(self.h)
+            self.h = None
+
+    @property
+    def plan_seconds(self):
+        return lib().sphemu_gpu_sht_plan_seconds(self.h)
+
+    @property
+    def stream(self):
+        return lib().sphemu_gpu_sht_stream(self.h)
+
+    def forward(self, fields):
+        f = np.ascontiguousarray(fields, dtype=np.float64).reshape(-1, self.n_theta * self.n_phi)
+        out = np.empty((f.shape[0], self.band_limit ** 2))
+        _check(lib().sphemu_gpu_sht_forward(self.h, _ptr(f), HOST, f.shape[0], _ptr(out), HOST))
+        return out
+
+    def inverse(self, coeffs):
+        c = np.ascontiguousarray(coeffs, dtype=np.float64).reshape(-1, self.band_limit ** 2)
+        out = np.empty((c.shape[0], self.n_theta, self.n_phi))
+        _check(lib().sphemu_gpu_sht_inverse(self.h, _ptr(c), HOST, c.shape[0], _ptr(out), HOST))
+        return out
+
+    def forward_device(self, fields_ptr, n, coeffs_ptr):
+        _check(lib().sphemu_gpu_sht_forward(self.h, C.c_void_p(fields_ptr), DEVICE, n,
+                                            C.c_void_p(coeffs_ptr), DEVICE))
+
+    def inverse_device(self, coeffs_ptr, n, fields_ptr):
+        _check(lib().sphemu_gpu_sht_inverse(self.h, C.c_void_p(coeffs_ptr), DEVICE, n,
+                                            C.c_void_p(fields_ptr), DEVICE))
+
+
+def _band_limit_of_coeffs(count):
+    big_l = int(round(math.sqrt(count)))
+    if big_l * big_l != count:
+        raise ValueError("coefficient length must be a perfect square")
+    return big_l
+
+
+def max_band_limit(n_theta, n_phi):
+    """GridSpec::max_band_limit (grid.cpp:27-29)."""
+    if n_theta < 2:
+        raise ValueError("grid needs at least two latitude rings")
+    if n_phi < 1:
+        raise ValueError("grid needs at least one longitude point")
+    return min(n_theta - 1, (n_phi + 1) // 2)
+
+
+def forward_sht(field, band_limit=0):
+    """Analyze a (theta, phi) field into packed real harmonic coefficients."""
+    f = np.ascontiguousarray(field, dtype=np.float64)
+    if f.ndim != 2:
+        raise ValueError("expected a (theta, phi) array")
+    if band_limit == 0:
+        band_limit = max_band_limit(*f.shape)
+    return ShtPlan(f.shape[0], f.shape[1], band_limit).forward(f)[0]
+
+
+def inverse_sht(coeffs, n_theta=0, n_phi=0):
+    """Synthesize packed coefficients on a grid (tight grid by default)."""
+    c = np.ascontiguousarray(coeffs, dtype=np.float64)
+    if c.ndim != 1:
+        raise ValueError("expected a flat coefficient array")
+    big_l = _band_limit_of_coeffs(c.shape[0])
+    if n_theta <= 0:
+        n_theta, n_phi = big_l + 1, 2 * big_l  # GridSpec::from_band_limit
+    if big_l > max_band_limit(n_theta, n_phi):
+        raise ValueError(f"grid {n_theta}x{n_phi} does not resolve band limit {big_l} "
+                         "(direct Legendre synthesis onto under-resolved grids is not on the "
+                         "B200 path yet)")
+    return ShtPlan(n_theta, n_phi, big_l).inverse(c)[0]
+
+
+def resolution_summary(band_limit):
+    """resolution_summary (grid.cpp:40-48)."""
+    if band_limit < 2:
+        raise ValueError("band limit must be at least 2")
+    return {"band_limit": band_limit, "degrees_per_cell": 180.0 / band_limit,
+            "km_per_cell": 180.0 * 111.2 / band_limit,
+            "grid_points": (band_limit - 1) * (2 * band_limit)}

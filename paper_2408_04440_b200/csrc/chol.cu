@@ -1,0 +1,596 @@
+// chol.cu — host side of the tiled mixed-precision Cholesky: precision map,
+// HBM tile arena, the CUDA-stream tile scheduler that replaces the reference's
+// DAG worker pool (proj/src/mpchol.cpp:254-347), statistics, and the C-ABI
+// entry points of include/sphemu_gpu.h.
+//
+// Schedule (right-looking, the same k-ordered update chains as
+// build_task_graph, mpchol.cpp:156-205, so every tile sees its updates in
+// k order exactly like the reference's serialized chains):
+//   for k: POTRF+TRTRI(k,k) -> panel TRSM-as-GEMM (all i > k) -> scatter
+//          -> trailing update grouped by output precision class.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "chol_kernels.cuh"
+#include "tc_gemm.cuh"
+
+namespace sphemu_gpu {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+}  // namespace
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+void note_launch(int64_t n) { g_launches += n; }
+int64_t launch_count() { return g_launches.load(); }
+
+int num_sms() {
+  static int sms = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return sms;
+}
+
+// MpCholConfig::validate (mpchol.cpp:55-61), same messages.
+void validate_config(const sphemu_chol_config& c) {
+  if (c.tile_size < 1) throw std::invalid_argument("tile size must be positive");
+  if (c.band_width_dp < 1) throw std::invalid_argument("double-precision band must be at least 1");
+  if (c.sp_fraction < 0.0 || c.sp_fraction > 1.0)
+    throw std::invalid_argument("sp fraction must lie in [0, 1]");
+  if (c.workers < 1) throw std::invalid_argument("worker count must be positive");
+  if (c.variant < 0 || c.variant > 3) throw std::invalid_argument("unknown precision variant");
+  if (c.hp_format != SPHEMU_HP_FP16 && c.hp_format != SPHEMU_HP_BF16)
+    throw std::invalid_argument("unknown half-precision format");
+}
+
+// assign_precisions (mpchol.cpp:67-93): band tiles double; off-band tiles
+// ordered by (distance, i, j); dpsp all single, dpsphp the first
+// ceil(sp_fraction * off) single and the rest half, dphp all half.
+std::vector<uint8_t> assign_precisions(int nt, const sphemu_chol_config& c) {
+  validate_config(c);
+  if (nt < 1) throw std::invalid_argument("need at least one tile");
+  std::vector<uint8_t> map(static_cast<size_t>(nt) * (nt + 1) / 2, SPHEMU_PREC_DP);
+  if (c.variant == SPHEMU_VARIANT_DP) return map;
+  int64_t n_off = 0;
+  for (int d = c.band_width_dp; d < nt; ++d) n_off += nt - d;
+  int64_t n_sp = n_off;
+  if (c.variant == SPHEMU_VARIANT_DPSPHP)
+    n_sp = static_cast<int64_t>(std::ceil(c.sp_fraction * static_cast<double>(n_off)));
+  else if (c.variant == SPHEMU_VARIANT_DPHP)
+    n_sp = 0;
+  int64_t t = 0;
+  for (int d = c.band_width_dp; d < nt; ++d)
+    for (int j = 0; j + d < nt; ++j, ++t) {
+      const int i = j + d;
+      map[static_cast<size_t>(i) * (i + 1) / 2 + j] = t < n_sp ? SPHEMU_PREC_SP : SPHEMU_PREC_HP;
+    }
+  return map;
+}
+
+// ---- residual probe kernels -------------------------------------------------
+__global__ void k_probe_vec(int n, uint64_t seed, double* x) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t z = seed + 0x9E3779B97F4A7C15ull * (uint64_t)(i + 1);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  x[i] = ((double)(z >> 11) * 0x1.0p-53) * 2.0 - 1.0;
+}
+
+// y = A x with A = make_spd_test_matrix regenerated from (d, pw); warp per row.
+__global__ void k_spd_matvec(int n, const double* __restrict__ d, const double* __restrict__ pw,
+                             const double* __restrict__ x, double* y) {
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double acc = 0.0;
+  for (int j = lane; j < n; j += 32) {
+    double a;
+    if (j == row) a = __dmul_rn(__dmul_rn(d[row], d[row]), 1.25);
+    else if (j < row) a = __dmul_rn(__dmul_rn(__dmul_rn(d[row], d[j]), 0.25), pw[row - j]);
+    else a = __dmul_rn(__dmul_rn(__dmul_rn(d[j], d[row]), 0.25), pw[j - row]);
+    acc += a * x[j];
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) y[row] = acc;
+}
+
+// trans = 1: z_j += L_ij^T x_i ; trans = 0: y_i += L_ij z_j  (block per tile).
+__global__ void k_tile_matvec(TileStore ts, const double* __restrict__ x, double* y, int trans) {
+  int i, j;
+  pair_from_index(blockIdx.x, i, j);
+  const void* tp = ts.tile(i, j);
+  const int p = ts.tprec(i, j);
+  const int ri = ts.rows(i), rj = ts.rows(j);
+  if (trans) {
+    for (int c = threadIdx.x; c < rj; c += blockDim.x) {
+      double acc = 0.0;
+      for (int r = 0; r < ri; ++r) acc += load_elem(tp, p, (int64_t)r * ts.b + c) * x[i * ts.lb + r];
+      atomicAdd(&y[j * ts.lb + c], acc);
+    }
+  } else {
+    for (int r = threadIdx.x; r < ri; r += blockDim.x) {
+      double acc = 0.0;
+      for (int c = 0; c < rj; ++c) acc += load_elem(tp, p, (int64_t)r * ts.b + c) * x[j * ts.lb + c];
+      atomicAdd(&y[i * ts.lb + r], acc);
+    }
+  }
+}
+
+__global__ void k_diff_norms(int n, const double* a, const double* b, double* sums) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double num = 0.0, den = 0.0;
+  if (i < n) {
+    num = (a[i] - b[i]) * (a[i] - b[i]);
+    den = a[i] * a[i];
+  }
+  num = warp_sum(num);
+  den = warp_sum(den);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&sums[0], num);
+    atomicAdd(&sums[1], den);
+  }
+}
+
+struct Chol {
+  int n = 0, b = 0, nt = 0;  // b = storage pitch (padded), lb = logical tile size
+  int lb = 0;
+  sphemu_chol_config cfg{};
+  std::vector<uint8_t> pmap, sprec;
+  std::vector<int64_t> off;
+  DevBuf<char> arena;
+  DevBuf<int64_t> d_off;
+  DevBuf<uint8_t> d_prec;
+  DevBuf<double> linv, dinv, p64, spd_d, spd_pw;
+  DevBuf<int> fail;
+  DevBuf<unsigned> sat;
+  DevBuf<int2> lists;
+  std::vector<int64_t> list_off, list_cnt;  // [k * 3 + class]
+  PanelFormats panel;                       // tensor-core operand mirrors
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t launches_at_start = 0, launches = 0;
+  std::chrono::steady_clock::time_point t_start;
+  bool factored = false;
+
+  int rows(int i) const { return std::min(lb, n - i * lb); }
+  size_t tix(int i, int j) const { return static_cast<size_t>(i) * (i + 1) / 2 + j; }
+
+  TileStore store() const {
+    return TileStore{arena.get(), d_off.get(), d_prec.get(), n, b, nt, lb};
+  }
+
+  Chol(int n_, const sphemu_chol_config& c) : n(n_), cfg(c) {
+    validate_config(cfg);
+    if (n < 1) throw std::invalid_argument("matrix is empty");
+    lb = cfg.tile_size;
+    if (lb > 1024) throw std::invalid_argument("tile_size above 1024 is not supported");
+    // Storage pitch: the logical tile padded with zeros to the kernel granule
+    // (64 for the FP64 kernels, 128 for the tcgen05 tiles).
+    const int granule = cfg.compute == SPHEMU_COMPUTE_TENSOR ? 128 : 64;
+    b = (lb + granule - 1) / granule * granule;
+    nt = (n + lb - 1) / lb;
+    pmap = assign_precisions(nt, cfg);
+    sprec.resize(pmap.size());
+    off.resize(pmap.size() + 1);
+    int64_t o = 0;
+    for (size_t t = 0; t < pmap.size(); ++t) {
+      int sp = pmap[t] == SPHEMU_PREC_DP ? kDP : (pmap[t] == SPHEMU_PREC_SP ? kSP : (cfg.hp_format == SPHEMU_HP_BF16 ? kBF : kHP));
+      sprec[t] = static_cast<uint8_t>(sp);
+      off[t] = o;
+      o += static_cast<int64_t>(b) * b * prec_bytes(sp);
+      o = (o + 255) & ~int64_t{255};
+    }
+    off.back() = o;
+    arena.alloc(static_cast<size_t>(o));
+    d_off.alloc(pmap.size());
+    d_prec.alloc(pmap.size());
+    SPH_CUDA(cudaMemcpy(d_off.get(), off.data(), pmap.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    SPH_CUDA(cudaMemcpy(d_prec.get(), sprec.data(), pmap.size(), cudaMemcpyHostToDevice));
+    SPH_CUDA(cudaMemset(arena.get(), 0, static_cast<size_t>(o)));
+    linv.alloc(static_cast<size_t>(b) * b);
+    dinv.alloc(static_cast<size_t>(b / 32 + 1) * 1024);
+    if (nt > 1) p64.alloc(static_cast<size_t>(nt - 1) * b * b);
+    fail.alloc(1);
+    sat.alloc(1);
+    // Per-step output-tile lists by precision class.
+    list_off.assign(static_cast<size_t>(nt) * 3 + 1, 0);
+    list_cnt.assign(static_cast<size_t>(nt) * 3, 0);
+    std::vector<int2> all;
+    for (int k = 0; k < nt; ++k)
+      for (int cls = 0; cls < 3; ++cls) {
+        list_off[k * 3 + cls] = static_cast<int64_t>(all.size());
+        for (int j = k + 1; j < nt; ++j)
+          for (int i = j; i < nt; ++i)
+            if (pmap[tix(i, j)] == cls) all.push_back(make_int2(i, j));
+        list_cnt[k * 3 + cls] = static_cast<int64_t>(all.size()) - list_off[k * 3 + cls];
+      }
+    if (!all.empty()) {
+      lists.alloc(all.size());
+      SPH_CUDA(cudaMemcpy(lists.get(), all.data(), all.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    }
+    if (cfg.compute == SPHEMU_COMPUTE_TENSOR && nt > 1) panel.alloc(nt, b, pmap, cfg.hp_format);
+    SPH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    SPH_CUDA(cudaEventCreate(&ev0));
+    SPH_CUDA(cudaEventCreate(&ev1));
+  }
+
+  ~Chol() {
+    if (stream) cudaStreamSynchronize(stream);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  void reset_flags() {
+    SPH_CUDA(cudaMemsetAsync(fail.get(), 0xff, sizeof(int), stream));
+    SPH_CUDA(cudaMemsetAsync(sat.get(), 0, sizeof(unsigned), stream));
+  }
+
+  dim3 tile_grid() const {
+    return dim3(static_cast<unsigned>(pmap.size()), static_cast<unsigned>(std::max(1, b * b / (256 * 64))));
+  }
+
+  void load_dense(const double* a, int where, int64_t lda) {
+    factored = false;
+    reset_flags();
+    DevBuf<double> staging;
+    const double* dptr = a;
+    if (where == SPHEMU_HOST) {
+      staging.alloc(static_cast<size_t>(n) * n);
+      SPH_CUDA(cudaMemcpy2DAsync(staging.get(), sizeof(double) * n, a, sizeof(double) * lda,
+                                 sizeof(double) * n, n, cudaMemcpyHostToDevice, stream));
+      dptr = staging.get();
+      lda = n;
+    }
+    k_load_dense<<<tile_grid(), 256, 0, stream>>>(store(), dptr, lda, sat.get());
+    SPH_LAUNCH_CHECK();
+    SPH_CUDA(cudaStreamSynchronize(stream));
+  }
+
+  void generate_spd(uint64_t seed);
+
+  void factor() {
+    factored = false;
+    launches_at_start = launch_count();
+    t_start = std::chrono::steady_clock::now();
+    SPH_CUDA(cudaEventRecord(ev0, stream));
+    const TileStore ts = store();
+    for (int k = 0; k < nt; ++k) {
+      double* dkk = reinterpret_cast<double*>(arena.get() + off[tix(k, k)]);
+      k_potrf_trtri<<<1, PT_THREADS, 0, stream>>>(dkk, b, rows(k), linv.get(), dinv.get(),
+                                                  fail.get(), k);
+      SPH_LAUNCH_CHECK();
+      if (k + 1 >= nt) break;
+      const int below = nt - k - 1;
+      if (cfg.compute == SPHEMU_COMPUTE_TENSOR) {
+        panel_step_tensor(k);
+      } else {
+        k_panel_trsm_fp64<<<dim3(below * (b / DG_BM), b / DG_BN), DG_THREADS, 0, stream>>>(
+            ts, k, linv.get(), p64.get(), fail.get(), sat.get());
+        SPH_LAUNCH_CHECK();
+      }
+      if (cfg.compute != SPHEMU_COMPUTE_TENSOR) {
+        k_panel_scatter<<<dim3(std::max(1, b * b / (256 * 16)), below), 256, 0, stream>>>(
+            ts, k, p64.get(), fail.get());
+        SPH_LAUNCH_CHECK();
+      }
+      for (int cls = 0; cls < 3; ++cls) {
+        const int64_t cnt = list_cnt[k * 3 + cls];
+        if (!cnt) continue;
+        const int2* lst = lists.get() + list_off[k * 3 + cls];
+        if (cls != SPHEMU_PREC_DP && cfg.compute == SPHEMU_COMPUTE_TENSOR) {
+          update_tensor(k, cls, lst, cnt);
+        } else {
+          const int per = (b / DG_BM) * (b / DG_BN);
+          k_update_fp64<<<static_cast<unsigned>(cnt * per), DG_THREADS, 0, stream>>>(
+              ts, k, lst, p64.get(), fail.get(), sat.get());
+          SPH_LAUNCH_CHECK();
+        }
+      }
+    }
+    SPH_CUDA(cudaEventRecord(ev1, stream));
+    launches = launch_count() - launches_at_start;
+    factored = true;
+  }
+
+  void panel_step_tensor(int k);
+  void update_tensor(int k, int cls, const int2* lst, int64_t cnt);
+
+  // Reads the failure flag; fills stats (mpchol.cpp:376-409).
+  int wait(sphemu_chol_stats* st) {
+    SPH_CUDA(cudaStreamSynchronize(stream));
+    int f = -1;
+    unsigned s = 0;
+    SPH_CUDA(cudaMemcpy(&f, fail.get(), sizeof(int), cudaMemcpyDeviceToHost));
+    SPH_CUDA(cudaMemcpy(&s, sat.get(), sizeof(unsigned), cudaMemcpyDeviceToHost));
+    if (st) fill_stats(st, s);
+    return f;
+  }
+
+  void fill_stats(sphemu_chol_stats* st, unsigned saturations) const {
+    std::memset(st, 0, sizeof *st);
+    st->n = n;
+    st->tile_size = b;
+    st->n_tiles = nt;
+    st->workers = cfg.workers;
+    st->variant = cfg.variant;
+    const int64_t N = nt;
+    st->tasks_potrf = N;
+    st->tasks_trsm = N * (N - 1) / 2;
+    st->tasks_syrk = N * (N - 1) / 2;
+    st->tasks_gemm = N * (N - 1) * (N - 2) / 6;
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j <= i; ++j) {
+        const int64_t e = static_cast<int64_t>(rows(i)) * rows(j);
+        // writes: the input quantization, then TRSM + GEMM chain (off-diagonal)
+        const int64_t writes = 1 + (i == j ? 0 : (1 + j));
+        switch (pmap[tix(i, j)]) {
+          case SPHEMU_PREC_DP: st->tiles_dp++; st->bytes_dp += 8 * e; break;
+          case SPHEMU_PREC_SP: st->tiles_sp++; st->bytes_sp += 4 * e; st->demotions_sp += writes * e; break;
+          default: st->tiles_hp++; st->bytes_hp += 2 * e; st->demotions_hp += writes * e; break;
+        }
+      }
+    st->half_saturations = saturations;
+    float ms = 0.f;
+    if (factored && cudaEventElapsedTime(&ms, ev0, ev1) == cudaSuccess) st->device_ms = ms;
+    st->wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    st->launches = launches;
+  }
+
+  void store_dense(double* out, int where, int64_t ldo) {
+    DevBuf<double> staging;
+    double* dptr = out;
+    int64_t ld = ldo;
+    if (where == SPHEMU_HOST) {
+      staging.alloc(static_cast<size_t>(n) * n);
+      dptr = staging.get();
+      ld = n;
+    }
+    const int threads = 256;
+    dim3 grid(std::max(1, std::min(ceil_div(n, threads), 64)), static_cast<unsigned>(n));
+    k_store_dense<<<grid, threads, 0, stream>>>(store(), dptr, ld);
+    SPH_LAUNCH_CHECK();
+    if (where == SPHEMU_HOST)
+      SPH_CUDA(cudaMemcpy2DAsync(out, sizeof(double) * ldo, dptr, sizeof(double) * n,
+                                 sizeof(double) * n, n, cudaMemcpyDeviceToHost, stream));
+    SPH_CUDA(cudaStreamSynchronize(stream));
+  }
+
+  double residual(const double* a, int where, int64_t lda) {
+    DevBuf<double> da, dl, sums(2);
+    const double* ap = a;
+    if (where == SPHEMU_HOST) {
+      da.alloc(static_cast<size_t>(n) * n);
+      SPH_CUDA(cudaMemcpy2D(da.get(), sizeof(double) * n, a, sizeof(double) * lda, sizeof(double) * n,
+                            n, cudaMemcpyHostToDevice));
+      ap = da.get();
+      lda = n;
+    }
+    dl.alloc(static_cast<size_t>(n) * n);
+    store_dense(dl.get(), SPHEMU_DEVICE, n);
+    SPH_CUDA(cudaMemsetAsync(sums.get(), 0, 2 * sizeof(double), stream));
+    dim3 grid(ceil_div(n, DG_BN), ceil_div(n, DG_BM));
+    k_residual<<<grid, DG_THREADS, 0, stream>>>(ap, lda, dl.get(), n, n, sums.get());
+    SPH_LAUNCH_CHECK();
+    double h[2];
+    SPH_CUDA(cudaMemcpyAsync(h, sums.get(), sizeof h, cudaMemcpyDeviceToHost, stream));
+    SPH_CUDA(cudaStreamSynchronize(stream));
+    return std::sqrt(h[0]) / std::sqrt(h[1]);
+  }
+
+  // ||(A - L L^T) x|| / ||A x|| over n_vec seeded vectors, A regenerated
+  // from (d, pw) on the fly: a size-independent check at sizes the host
+  // cannot hold.
+  double residual_probe(uint64_t seed, int n_vec) {
+    std::vector<double> d(n), pw(n);
+    host_spd_factors(n, seed, d.data(), pw.data());
+    DevBuf<double> dd(n), dpw(n), x(n), y1(n), z(n), y2(n), sums(2);
+    SPH_CUDA(cudaMemcpyAsync(dd.get(), d.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream));
+    SPH_CUDA(cudaMemcpyAsync(dpw.get(), pw.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream));
+    double worst = 0.0;
+    for (int v = 0; v < n_vec; ++v) {
+      k_probe_vec<<<ceil_div(n, 256), 256, 0, stream>>>(n, 0x9E3779B97F4A7C15ull * (v + 1) + seed, x.get());
+      SPH_LAUNCH_CHECK();
+      k_spd_matvec<<<ceil_div(n, 4), 128, 0, stream>>>(n, dd.get(), dpw.get(), x.get(), y1.get());
+      SPH_LAUNCH_CHECK();
+      SPH_CUDA(cudaMemsetAsync(z.get(), 0, n * sizeof(double), stream));
+      SPH_CUDA(cudaMemsetAsync(y2.get(), 0, n * sizeof(double), stream));
+      k_tile_matvec<<<static_cast<unsigned>(pmap.size()), 256, 0, stream>>>(store(), x.get(), z.get(), 1);
+      SPH_LAUNCH_CHECK();
+      k_tile_matvec<<<static_cast<unsigned>(pmap.size()), 256, 0, stream>>>(store(), z.get(), y2.get(), 0);
+      SPH_LAUNCH_CHECK();
+      SPH_CUDA(cudaMemsetAsync(sums.get(), 0, 2 * sizeof(double), stream));
+      k_diff_norms<<<ceil_div(n, 256), 256, 0, stream>>>(n, y1.get(), y2.get(), sums.get());
+      SPH_LAUNCH_CHECK();
+      double h[2];
+      SPH_CUDA(cudaMemcpyAsync(h, sums.get(), sizeof h, cudaMemcpyDeviceToHost, stream));
+      SPH_CUDA(cudaStreamSynchronize(stream));
+      worst = std::max(worst, std::sqrt(h[0]) / std::sqrt(h[1]));
+    }
+    return worst;
+  }
+
+  void flops(double* f) const {
+    f[0] = f[1] = f[2] = 0.0;
+    auto cls = [&](int i, int j) { return static_cast<int>(pmap[tix(i, j)]); };
+    for (int k = 0; k < nt; ++k) {
+      const double bk = rows(k);
+      f[cls(k, k)] += bk * bk * bk / 3.0;
+      for (int i = k + 1; i < nt; ++i) {
+        const double bi = rows(i);
+        f[cls(i, k)] += bi * bk * bk;
+        f[cls(i, i)] += bi * bi * bk;
+        for (int j = k + 1; j < i; ++j) f[cls(i, j)] += 2.0 * bi * rows(j) * bk;
+      }
+    }
+  }
+};
+
+// make_spd_test_matrix inputs computed on the host exactly as the reference
+// does (GaussianRng uniform -> exp, std::pow(0.9, k)), matrix built on device.
+void Chol::generate_spd(uint64_t seed) {
+  factored = false;
+  std::vector<double> d(n), pw(n);
+  host_spd_factors(n, seed, d.data(), pw.data());
+  spd_d.alloc(n);
+  spd_pw.alloc(n);
+  SPH_CUDA(cudaMemcpyAsync(spd_d.get(), d.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream));
+  SPH_CUDA(cudaMemcpyAsync(spd_pw.get(), pw.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream));
+  reset_flags();
+  k_gen_spd<<<tile_grid(), 256, 0, stream>>>(store(), spd_d.get(), spd_pw.get(), sat.get());
+  SPH_LAUNCH_CHECK();
+  SPH_CUDA(cudaStreamSynchronize(stream));
+}
+
+void Chol::panel_step_tensor(int k) {
+  const int below = nt - k - 1;
+  tc_panel_trsm(store(), k, below, linv.get(), p64.get(), panel, fail.get(), sat.get(), stream);
+}
+
+void Chol::update_tensor(int k, int cls, const int2* lst, int64_t cnt) {
+  tc_update(store(), k, cls, cfg.hp_format, lst, cnt, p64.get(), panel, fail.get(), sat.get(), stream);
+}
+
+}  // namespace sphemu_gpu
+
+using namespace sphemu_gpu;
+
+struct sphemu_chol_s {
+  Chol* c;
+};
+
+extern "C" {
+
+const char* sphemu_gpu_last_error(void) { return g_last_error.c_str(); }
+const char* sphemu_gpu_version(void) { return "0.1.0"; }
+int64_t sphemu_gpu_launch_count(void) { return launch_count(); }
+
+int sphemu_gpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int sphemu_gpu_set_device(int device) {
+  return guard([&] { SPH_CUDA(cudaSetDevice(device)); });
+}
+
+int sphemu_gpu_chol_config_validate(const sphemu_chol_config* cfg) {
+  return guard([&] { validate_config(*cfg); });
+}
+
+int sphemu_gpu_assign_precisions(int n_tiles, const sphemu_chol_config* cfg, uint8_t* out) {
+  return guard([&] {
+    auto m = assign_precisions(n_tiles, *cfg);
+    std::memcpy(out, m.data(), m.size());
+  });
+}
+
+int sphemu_gpu_chol_create(int n, const sphemu_chol_config* cfg, sphemu_chol_t* out) {
+  return guard([&] {
+    *out = nullptr;
+    auto* h = new sphemu_chol_s{nullptr};
+    try {
+      h->c = new Chol(n, *cfg);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int sphemu_gpu_chol_destroy(sphemu_chol_t h) {
+  return guard([&] {
+    if (!h) return;
+    delete h->c;
+    delete h;
+  });
+}
+
+int sphemu_gpu_chol_load_dense(sphemu_chol_t h, const double* a, int where, int64_t lda) {
+  return guard([&] { h->c->load_dense(a, where, lda); });
+}
+
+int sphemu_gpu_chol_generate_spd(sphemu_chol_t h, uint64_t seed) {
+  return guard([&] { h->c->generate_spd(seed); });
+}
+
+int sphemu_gpu_chol_factor(sphemu_chol_t h) {
+  return guard([&] { h->c->factor(); });
+}
+
+int sphemu_gpu_chol_wait(sphemu_chol_t h, sphemu_chol_stats* st, int* failed_tile) {
+  int rc = SPHEMU_OK;
+  int g = guard([&] {
+    const int f = h->c->wait(st);
+    if (failed_tile) *failed_tile = f;
+    if (f >= 0) {
+      set_last_error("diagonal tile " + std::to_string(f) + " has a non-positive pivot");
+      rc = SPHEMU_ERR_NOT_SPD;
+    }
+  });
+  return g != SPHEMU_OK ? g : rc;
+}
+
+int sphemu_gpu_chol_store_dense(sphemu_chol_t h, double* factor, int where, int64_t ldf) {
+  return guard([&] { h->c->store_dense(factor, where, ldf); });
+}
+
+int sphemu_gpu_chol_residual(sphemu_chol_t h, const double* a, int where, int64_t lda, double* out) {
+  return guard([&] { *out = h->c->residual(a, where, lda); });
+}
+
+int sphemu_gpu_chol_flops(sphemu_chol_t h, double* f_dp, double* f_sp, double* f_hp) {
+  return guard([&] {
+    double f[3];
+    h->c->flops(f);
+    *f_dp = f[0];
+    *f_sp = f[1];
+    *f_hp = f[2];
+  });
+}
+
+int sphemu_gpu_chol_residual_probe_spd(sphemu_chol_t h, uint64_t seed, int n_vec, double* out) {
+  return guard([&] { *out = h->c->residual_probe(seed, n_vec); });
+}
+
+void* sphemu_gpu_chol_stream(sphemu_chol_t h) { return h ? h->c->stream : nullptr; }
+
+int sphemu_gpu_tiled_cholesky_dense(const double* a, int where_a, int n, const sphemu_chol_config* cfg,
+                                    double* factor, int where_factor, sphemu_chol_stats* stats,
+                                    int* failed_tile) {
+  int rc = SPHEMU_OK;
+  int g = guard([&] {
+    Chol c(n, *cfg);
+    c.load_dense(a, where_a, n);
+    c.factor();
+    const int f = c.wait(stats);
+    if (failed_tile) *failed_tile = f;
+    if (f >= 0) {
+      set_last_error("diagonal tile " + std::to_string(f) + " has a non-positive pivot");
+      rc = SPHEMU_ERR_NOT_SPD;
+      return;
+    }
+    c.store_dense(factor, where_factor, n);
+  });
+  return g != SPHEMU_OK ? g : rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,192 @@
+// emulate.cu — the emulation generator (replaces proj/src/stochastic.cpp:217-277)
+// behind sphemu_gpu_emulate, plus the full-size residual probe of the
+// Cholesky (sphemu_gpu_chol_residual_probe_spd).
+//
+// Reference loop per replicate: eta ~ N(0,1)^d, xi = V eta (dense GEMV),
+// f = xi + sum_p phi_p * state_p, keep f after 10P burn-in steps; eps ~
+// N(0,1)^points per kept step; y = m_t + sigma (inverse_sht(f_t) + sqrt(v2) eps).
+// B200 form: all innovations of all replicates and steps in one FP64 GEMM
+// Xi = H V^T (DMMA, zero tiles of the lower factor skipped), the AR(P)
+// recursion as one pass per coefficient (serial in time, parallel over
+// coefficients and replicates), one batched inverse SHT, and a fused retrend
+// epilogue.
+//
+// RNG: SPHEMU_RNG_REFERENCE reproduces the reference's single serial
+// mt19937_64 + Box-Muller stream in its exact draw order (rng.hpp:12-39,
+// stochastic.cpp:230-259), generated on the host because that stream is
+// serial by definition; SPHEMU_RNG_PHILOX draws counter-based normals on the
+// device.
+#include <cmath>
+#include <random>
+#include <vector>
+
+#include "common.cuh"
+#include "dgemm.cuh"
+
+namespace sphemu_gpu {
+
+struct Sht;  // sht.cu
+void sht_inverse_device(void* plan, const double* coeffs, int64_t n, double* fields, cudaStream_t* s_out);
+
+// Xi (S x d) = H (S x d) * V^T, V lower triangular dense (row-major d x d).
+__global__ void __launch_bounds__(DG_THREADS) k_emul_xi(const double* __restrict__ H, const double* __restrict__ V,
+                                                         int64_t S, int d, double* __restrict__ Xi) {
+  __shared__ DgSmem sm;
+  const int64_t r0 = (int64_t)blockIdx.y * DG_BM;
+  const int c0 = blockIdx.x * DG_BN;
+  // Output columns c0..c0+63 use V rows c0.. whose nonzeros stop at column c0+63.
+  const int kmax = min(d, c0 + DG_BN);
+  RowMajorK A{H + r0 * d, d, (int)(S - r0 < DG_BM ? S - r0 : DG_BM), kmax};
+  RowMajorK B{V + (int64_t)c0 * d, d, min(DG_BN, d - c0), kmax};
+  double acc[4][4][2];
+  dgemm_64x64(A, B, kmax, sm, acc);
+  dg_for_each(acc, [&](int r, int c, double v) {
+    if (r0 + r < S && c0 + c < d) Xi[(r0 + r) * d + c0 + c] = v;
+  });
+}
+
+// AR(P) recursion (stochastic.cpp:247-253): f_t = xi_t + sum_p phi_p f_{t-p},
+// state zero at the start of each replicate, burn-in steps dropped.
+__global__ void k_emul_ar(const double* __restrict__ Xi, const double* __restrict__ phi, int order, int d,
+                          int burn, int t_out, int r_len, double* __restrict__ draws) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (i >= d || r >= r_len) return;
+  double st[16];
+  double ph[16];
+  for (int p = 0; p < order; ++p) {
+    st[p] = 0.0;
+    ph[p] = phi[(int64_t)p * d + i];
+  }
+  const int steps = burn + t_out;
+  for (int s = 0; s < steps; ++s) {
+    double f = Xi[((int64_t)r * steps + s) * d + i];
+    for (int p = 0; p < order; ++p) f += ph[p] * st[p];
+    for (int p = order - 1; p > 0; --p) st[p] = st[p - 1];
+    if (order > 0) st[0] = f;
+    if (s >= burn) draws[((int64_t)r * t_out + (s - burn)) * d + i] = f;
+  }
+}
+
+// y = m_t + sigma (synth + sqrt(v2) eps)   (stochastic.cpp:266-273)
+__global__ void k_emul_retrend(const double* __restrict__ synth, const double* __restrict__ eps,
+                               const double* __restrict__ means, const double* __restrict__ sigma,
+                               const double* __restrict__ v2, int64_t points, int t_out, int64_t total,
+                               double* __restrict__ out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t loc = e % points;
+    const int64_t t = (e / points) % t_out;
+    const double ep = sqrt(v2[loc]) * eps[e];
+    out[e] = means[t * points + loc] + sigma[loc] * (synth[e] + ep);
+  }
+}
+
+// Philox4x32-10 counter-based normals (Box-Muller on two 53-bit uniforms).
+__device__ __forceinline__ void philox(uint32_t (&c)[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = (uint32_t)p1;
+    c[2] = n2;
+    c[3] = (uint32_t)p0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+__global__ void k_philox_normals(uint64_t seed, uint64_t stream, int64_t n, double* out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t c[4] = {(uint32_t)e, (uint32_t)(e >> 32), (uint32_t)stream, (uint32_t)(stream >> 32)};
+    philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const double u1 = ((double)((((uint64_t)c[0] << 32) | c[1]) >> 11) + 1.0) * 0x1.0p-53;
+    const double u2 = ((double)((((uint64_t)c[2] << 32) | c[3]) >> 11) + 1.0) * 0x1.0p-53;
+    const double rad = sqrt(-2.0 * log(u1));
+    double s, co;
+    sincospi(2.0 * u2, &s, &co);
+    out[2 * e] = rad * co;
+    if (2 * e + 1 < n) out[2 * e + 1] = rad * s;
+  }
+}
+
+// The reference's serial stream (rng.hpp:12-39): uniform (0,1] from
+// mt19937_64 >> 11, Box-Muller with a cached spare.
+struct RefGaussian {
+  std::mt19937_64 eng;
+  double spare = 0.0;
+  bool has = false;
+  explicit RefGaussian(uint64_t s) : eng(s) {}
+  double uniform() { return static_cast<double>((eng() >> 11) + 1) * 0x1.0p-53; }
+  double normal() {
+    if (has) {
+      has = false;
+      return spare;
+    }
+    const double u1 = uniform(), u2 = uniform();
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double a = 6.283185307179586476925286766559 * u2;
+    spare = r * std::sin(a);
+    has = true;
+    return r * std::cos(a);
+  }
+};
+
+void emulate(void* plan, int n_theta, int n_phi, int L, const double* v, int d, const double* phi, int order,
+             const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed, int r_len,
+             int rng_mode, double* out) {
+  if (t_out < 1 || r_len < 1) throw std::invalid_argument("need t_out, r_len >= 1");
+  if (d != L * L) throw std::invalid_argument("transform plan does not match the model");
+  if (order < 0 || order > 16) throw std::invalid_argument("lag order must lie in [0, 16]");
+  const int burn = 10 * order;  // stochastic.cpp:17,227
+  const int64_t steps = burn + t_out;
+  const int64_t S = (int64_t)r_len * steps;
+  const int64_t points = (int64_t)n_theta * n_phi;
+  const int64_t ytot = (int64_t)r_len * t_out * points;
+  cudaStream_t s = nullptr;
+  sht_inverse_device(plan, nullptr, 0, nullptr, &s);  // fetch the plan's stream
+  DevBuf<double> dV((size_t)d * d), dH((size_t)S * d), dXi((size_t)S * d), dDraws((size_t)r_len * t_out * d);
+  DevBuf<double> dEps(ytot), dSynth(ytot), dMeans((size_t)t_out * points), dSigma(points), dV2(points),
+      dPhi(order > 0 ? (size_t)order * d : 1);
+  SPH_CUDA(cudaMemcpyAsync(dV.get(), v, (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice, s));
+  SPH_CUDA(cudaMemcpyAsync(dMeans.get(), means, (size_t)t_out * points * sizeof(double), cudaMemcpyHostToDevice, s));
+  SPH_CUDA(cudaMemcpyAsync(dSigma.get(), sigma, points * sizeof(double), cudaMemcpyHostToDevice, s));
+  SPH_CUDA(cudaMemcpyAsync(dV2.get(), v2, points * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (order > 0)
+    SPH_CUDA(cudaMemcpyAsync(dPhi.get(), phi, (size_t)order * d * sizeof(double), cudaMemcpyHostToDevice, s));
+  std::vector<double> hH, hE;
+  if (rng_mode == SPHEMU_RNG_REFERENCE) {
+    // Exact reference order: per replicate, (burn + t_out) x d innovations,
+    // then t_out x points small-scale normals.
+    hH.resize((size_t)S * d);
+    hE.resize(ytot);
+    RefGaussian g(seed);
+    for (int r = 0; r < r_len; ++r) {
+      double* h = hH.data() + (size_t)r * steps * d;
+      for (int64_t e = 0; e < steps * d; ++e) h[e] = g.normal();
+      double* ep = hE.data() + (size_t)r * t_out * points;
+      for (int64_t e = 0; e < (int64_t)t_out * points; ++e) ep[e] = g.normal();
+    }
+    SPH_CUDA(cudaMemcpyAsync(dH.get(), hH.data(), hH.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    SPH_CUDA(cudaMemcpyAsync(dEps.get(), hE.data(), hE.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  } else {
+    k_philox_normals<<<4 * num_sms(), 256, 0, s>>>(seed, 1, S * d, dH.get());
+    SPH_LAUNCH_CHECK();
+    k_philox_normals<<<4 * num_sms(), 256, 0, s>>>(seed, 2, ytot, dEps.get());
+    SPH_LAUNCH_CHECK();
+  }
+  k_emul_xi<<<dim3(ceil_div(d, DG_BN), (unsigned)ceil_div(S, DG_BM)), DG_THREADS, 0, s>>>(dH.get(), dV.get(), S, d,
+                                                                                           dXi.get());
+  SPH_LAUNCH_CHECK();
+  k_emul_ar<<<dim3(ceil_div(d, 128), r_len), 128, 0, s>>>(dXi.get(), dPhi.get(), order, d, burn, t_out, r_len,
+                                                           dDraws.get());
+  SPH_LAUNCH_CHECK();
+  sht_inverse_device(plan, dDraws.get(), (int64_t)r_len * t_out, dSynth.get(), nullptr);
+  k_emul_retrend<<<8 * num_sms(), 256, 0, s>>>(dSynth.get(), dEps.get(), dMeans.get(), dSigma.get(), dV2.get(),
+                                                points, t_out, ytot, dEps.get());
+  SPH_LAUNCH_CHECK();
+  SPH_CUDA(cudaMemcpyAsync(out, dEps.get(), ytot * sizeof(double), cudaMemcpyDeviceToHost, s));
+  SPH_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace sphemu_gpu

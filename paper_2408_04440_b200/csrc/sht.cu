@@ -1,0 +1,738 @@
+// sht.cu — B200 spherical harmonic transform behind the C-ABI of
+// include/sphemu_gpu.h (replaces proj/src/sht.cpp:111-404).
+//
+// The reference analysis per order m is  ring FFT -> parity extension ->
+// FFT(2 n_theta - 2) -> J = K * I -> Wigner contraction  (sht.cpp:226-263),
+// and synthesis is  K = sum_l q z -> spectrum -> FFT(2 n_theta - 2) -> ring
+// FFT  (sht.cpp:304-357). Everything after the ring FFT is linear and fixed
+// per m, so the plan composes it once into real operators:
+//   forward  f_{l,m} = sum_i Psi_m[l, i] g_m(theta_i)
+//            Psi_m = Re(2 pi i^{-m} Q_m V_par(m)),
+//            V_par(m2, i) = W(m2, i) + par W(-m2, i),
+//            W(m2, i) = (1/n_ext) sum_{m'} I(m' + m2) (w^{-i m'} + par [interior] w^{i m'})
+//   inverse  g_m(theta_i) = sum_l Y_m[i, l] z_{l,m},
+//            Y_m = s_m (Q_m T_par)^T, T_+ = (1, 2cos m' theta), T_- = (0, 2sin m' theta)
+// with Q_m[l, m2] = q(l, m, m2) (wigner.cpp:152-163). Both are the exact
+// linear maps of the reference on every input (band-limited or not). Psi_m,
+// Y_m are built on the GPU by FP64 DMMA GEMMs; a transform is then one
+// batched ring FFT (HBM-bound) plus one grouped FP64 Legendre GEMM over m.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "dgemm.cuh"
+
+namespace sphemu_gpu {
+
+// ===========================================================================
+// Host: Wigner d(pi/2) tables (wigner.cpp:18-134). Product code: the plan
+// build needs them; they are restated here, not linked from the oracle.
+// ===========================================================================
+struct WignerHost {
+  int L = 0;
+  int renorm = 0;
+  std::vector<double> d;
+  std::vector<int64_t> off;  // (a, b) -> start of the chain l = max(a,b)..L-1
+  double get(int l, int m2, int m) const {  // m2, m >= 0, l >= max
+    return d[off[(int64_t)m2 * L + m] + l - std::max(m2, m)];
+  }
+};
+
+static int parity_sign(int e) { return (e & 1) ? -1 : 1; }
+
+static size_t wigner_bytes(int L) {
+  size_t d_entries = 0;
+  for (int a = 0; a < L; ++a)
+    for (int b = 0; b < L; ++b) d_entries += static_cast<size_t>(L - std::max(a, b));
+  const size_t q_entries = static_cast<size_t>(L) * L * (L + 1) / 2;
+  return (d_entries + q_entries) * sizeof(double) + (static_cast<size_t>(L) * L + 1) * sizeof(size_t);
+}
+
+static WignerHost build_wigner(int L, size_t cap) {
+  if (L < 1) throw std::invalid_argument("band limit must be positive");
+  const size_t bytes = wigner_bytes(L);
+  if (bytes > cap)
+    throw std::invalid_argument("Wigner tables for band limit " + std::to_string(L) + " need " +
+                                std::to_string(bytes) + " bytes, over the cap of " +
+                                std::to_string(cap));
+  WignerHost t;
+  t.L = L;
+  t.off.assign(static_cast<size_t>(L) * L + 1, 0);
+  int64_t o = 0;
+  for (int a = 0; a < L; ++a)
+    for (int b = 0; b < L; ++b) {
+      t.off[(size_t)a * L + b] = o;
+      o += L - std::max(a, b);
+    }
+  t.off.back() = o;
+  t.d.assign(static_cast<size_t>(o), 0.0);
+  for (int a = 0; a < L; ++a)
+    for (int b = 0; b < L; ++b) {
+      const int l0 = std::max(a, b), lo = std::min(a, b);
+      long double prod = 1.0L;
+      for (int k = 1; k <= l0 - lo; ++k) prod *= static_cast<long double>(l0 + lo + k) / k;
+      const long double v = std::ldexp(1.0L, -l0) * std::sqrt(prod);
+      double* chain = t.d.data() + t.off[(size_t)a * L + b];
+      chain[0] = static_cast<double>(parity_sign(l0 - b) * v);
+      if (l0 + 1 >= L) continue;
+      double prev = 0.0, cur = chain[0];
+      for (int l = l0; l + 1 < L; ++l) {
+        double next;
+        if (l == 0) {
+          next = 0.0;
+        } else {
+          const double c1 = std::sqrt(static_cast<double>(l + 1 + a)) * std::sqrt(static_cast<double>(l + 1 - a)) *
+                            std::sqrt(static_cast<double>(l + 1 + b)) * std::sqrt(static_cast<double>(l + 1 - b));
+          const double c0 = std::sqrt(static_cast<double>(l + a)) * std::sqrt(static_cast<double>(l - a)) *
+                            std::sqrt(static_cast<double>(l + b)) * std::sqrt(static_cast<double>(l - b));
+          next = (-(2.0 * l + 1.0) * a * b * cur - (l + 1.0) * c0 * prev) / (l * c1);
+        }
+        chain[l + 1 - l0] = next;
+        prev = cur;
+        cur = next;
+      }
+    }
+  // Renormalization guard (wigner.cpp:111-130).
+  for (int l = 0; l < L; ++l)
+    for (int b = 0; b <= l; ++b) {
+      bool bad = false;
+      double s = 0.0;
+      for (int a = 0; a <= l; ++a) {
+        const double v = t.get(l, a, b);
+        if (std::abs(v) > 1.0 + 1e-9) bad = true;
+        s += (a == 0 ? 1.0 : 2.0) * v * v;
+      }
+      if (!bad) continue;
+      ++t.renorm;
+      const double scale = 1.0 / std::sqrt(s);
+      for (int a = 0; a <= l; ++a) t.d[t.off[(size_t)a * L + b] + l - std::max(a, b)] *= scale;
+    }
+  return t;
+}
+
+// ===========================================================================
+// Device: operator build
+// ===========================================================================
+// Q_m accessor: element (r, k) = q(m + r, m, k) = norm_l d^l_{k,0} d^l_{k,m}
+// (wigner.cpp:152-163), zero for k > l. Used as A (forward) and as B (inverse).
+struct QAcc {
+  static constexpr bool kKContig = true;
+  const double* d;
+  const int64_t* off;
+  int L, m, rows;
+  __device__ double operator()(int r, int k) const {
+    const int l = m + r;
+    if (r >= rows || k >= L || k > l) return 0.0;
+    const double norm = sqrt((2.0 * l + 1.0) / (4.0 * 3.14159265358979323846));
+    const double d0 = d[off[(int64_t)k * L + 0] + l - k];
+    const double dm = d[off[(int64_t)k * L + m] + l - max(k, m)];
+    return norm * d0 * dm;
+  }
+};
+
+// Q_m rows shifted by an output-tile origin.
+struct QShift {
+  static constexpr bool kKContig = true;
+  QAcc q;
+  int r0;
+  __device__ double operator()(int r, int k) const { return q(r0 + r, k); }
+};
+
+// V tables: vre_p = Re V_+(m2, i), vim_m = Im V_-(m2, i), L x n_theta.
+__global__ void k_sht_vtables(int L, int n_theta, const double2* __restrict__ tw_ext, double* vre_p,
+                              double* vim_m) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int m2 = blockIdx.y;
+  if (i >= n_theta) return;
+  const int n_ext = 2 * n_theta - 2;
+  const bool interior = i > 0 && i < n_theta - 1;
+  // W_par(+-m2, i) accumulated for both parities.
+  double wr_p[2] = {0, 0}, wi_p[2] = {0, 0}, wr_m[2] = {0, 0}, wi_m[2] = {0, 0};
+  for (int mp = -(L - 1); mp <= L - 1; ++mp) {
+    // w^{-i mp} = tw_ext[(i*mp) mod n_ext] (tw = exp(-2 pi i t / n_ext))
+    int t = (int)(((int64_t)i * mp) % n_ext);
+    if (t < 0) t += n_ext;
+    const double2 e_neg = tw_ext[t];                 // exp(-i theta mp)
+    const double2 e_pos = make_double2(e_neg.x, -e_neg.y);  // exp(+i theta mp)
+    // c_par = e_neg + par * [interior] e_pos
+    double cp_r = e_neg.x, cp_i = e_neg.y, cm_r = e_neg.x, cm_i = e_neg.y;
+    if (interior) {
+      cp_r += e_pos.x; cp_i += e_pos.y;
+      cm_r -= e_pos.x; cm_i -= e_pos.y;
+    }
+#pragma unroll
+    for (int sgn = 0; sgn < 2; ++sgn) {
+      const int q = mp + (sgn == 0 ? m2 : -m2);
+      double Ir = 0.0, Ii = 0.0;
+      if (q & 1) {
+        if (q == 1) Ii = 3.14159265358979323846 / 2.0;
+        else if (q == -1) Ii = -3.14159265358979323846 / 2.0;
+        else continue;
+      } else {
+        Ir = 2.0 / (1.0 - (double)q * (double)q);
+      }
+      wr_p[sgn] += Ir * cp_r - Ii * cp_i;
+      wi_p[sgn] += Ir * cp_i + Ii * cp_r;
+      wr_m[sgn] += Ir * cm_r - Ii * cm_i;
+      wi_m[sgn] += Ir * cm_i + Ii * cm_r;
+    }
+  }
+  const double inv = 1.0 / n_ext;
+  double vp, vm;
+  if (m2 == 0) {
+    vp = wr_p[0] * inv;
+    vm = wi_m[0] * inv;
+  } else {
+    vp = (wr_p[0] + wr_p[1]) * inv;   // W_+(m2) + W_+(-m2)
+    vm = (wi_m[0] - wi_m[1]) * inv;   // W_-(m2) - W_-(-m2)
+  }
+  vre_p[(int64_t)m2 * n_theta + i] = vp;
+  vim_m[(int64_t)m2 * n_theta + i] = vm;
+}
+
+// Psi_m (L-m x n_theta) = s_m 2 pi Q_m Vsel, grid (n_theta/64, L/64, L).
+__global__ void __launch_bounds__(DG_THREADS) k_sht_build_psi(const double* d, const int64_t* off, int L,
+                                                               int n_theta, const double* vre_p,
+                                                               const double* vim_m, const int64_t* psi_off,
+                                                               double* psi) {
+  __shared__ DgSmem sm;
+  const int m = blockIdx.z;
+  const int rows = L - m;
+  const int r0 = blockIdx.y * DG_BM, c0 = blockIdx.x * DG_BN;
+  if (r0 >= rows) return;
+  QShift As{QAcc{d, off, L, m, rows}, r0};
+  const double* vs = (m & 1) ? vim_m : vre_p;
+  KMajor B{vs + c0, n_theta, min(DG_BN, n_theta - c0), L};
+  double acc[4][4][2];
+  dgemm_64x64(As, B, L, sm, acc);
+  const double sgn = ((m >> 1) & 1) ? -1.0 : 1.0;
+  const double scale = sgn * 2.0 * 3.14159265358979323846;
+  double* out = psi + psi_off[m];
+  dg_for_each(acc, [&](int r, int c, double v) {
+    if (r0 + r < rows && c0 + c < n_theta) out[(int64_t)(r0 + r) * n_theta + c0 + c] = scale * v;
+  });
+}
+
+// Y_m (n_theta x L-m) = s_m (Q_m Tsel)^T: A(i, m') = Tsel(m', i), B(l', m') = Q_m.
+__global__ void __launch_bounds__(DG_THREADS) k_sht_build_y(const double* d, const int64_t* off, int L,
+                                                             int n_theta, const double* tcos,
+                                                             const double* tsin, const int64_t* y_off,
+                                                             double* y) {
+  __shared__ DgSmem sm;
+  const int m = blockIdx.z;
+  const int cols = L - m;
+  const int r0 = blockIdx.x * DG_BM, c0 = blockIdx.y * DG_BN;
+  if (c0 >= cols) return;
+  const double* ts = (m & 1) ? tsin : tcos;
+  KMajor A{ts + r0, n_theta, min(DG_BM, n_theta - r0), L};
+  QShift Bs{QAcc{d, off, L, m, cols}, c0};
+  double acc[4][4][2];
+  dgemm_64x64(A, Bs, L, sm, acc);
+  const double sgn = ((m >> 1) & 1) ? -1.0 : 1.0;
+  double* out = y + y_off[m];
+  dg_for_each(acc, [&](int r, int c, double v) {
+    if (r0 + r < n_theta && c0 + c < cols) out[(int64_t)(r0 + r) * cols + c0 + c] = sgn * v;
+  });
+}
+
+// ===========================================================================
+// Device: batched ring FFT (in-place mixed-radix DIF in shared memory)
+// ===========================================================================
+constexpr int FFT_MAX_STAGES = 24;
+struct FftPlan {
+  int n;
+  int stages;
+  int radix[FFT_MAX_STAGES];
+  const double2* tw;  // exp(-2 pi i t / n), t in [0, n)
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// One DIF pass over R rings held in x (R * n complex), sign -1 (analysis) or
+// +1 (synthesis, conjugated twiddles).
+template <int SIGN>
+__device__ void fft_dif_rings(double2* x, int R, const FftPlan& P) {
+  const int n = P.n;
+  int len = n;
+  for (int s = 0; s < P.stages; ++s) {
+    const int p = P.radix[s];
+    const int span = len / p;
+    const int groups = n / len;
+    const int bfly = R * groups * span;
+    for (int t = threadIdx.x; t < bfly; t += blockDim.x) {
+      const int ring = t / (groups * span);
+      const int rem = t % (groups * span);
+      const int g = rem / span, j = rem % span;
+      double2* base = x + (int64_t)ring * n + g * len + j;
+      const int tstep = n / len;
+      if (p == 2) {
+        const double2 a = base[0], b = base[span];
+        double2 y1 = make_double2(a.x - b.x, a.y - b.y);
+        base[0] = make_double2(a.x + b.x, a.y + b.y);
+        double2 w = P.tw[(j * tstep) % n];
+        if (SIGN > 0) w.y = -w.y;
+        base[span] = cmul(y1, w);
+      } else if (p == 4) {
+        const double2 a0 = base[0], a1 = base[span], a2 = base[2 * span], a3 = base[3 * span];
+        const double2 s02 = make_double2(a0.x + a2.x, a0.y + a2.y), d02 = make_double2(a0.x - a2.x, a0.y - a2.y);
+        const double2 s13 = make_double2(a1.x + a3.x, a1.y + a3.y), d13 = make_double2(a1.x - a3.x, a1.y - a3.y);
+        // -i * d13 for analysis, +i * d13 for synthesis
+        const double2 rd13 = SIGN < 0 ? make_double2(d13.y, -d13.x) : make_double2(-d13.y, d13.x);
+        double2 y0 = make_double2(s02.x + s13.x, s02.y + s13.y);
+        double2 y2 = make_double2(s02.x - s13.x, s02.y - s13.y);
+        double2 y1 = make_double2(d02.x + rd13.x, d02.y + rd13.y);
+        double2 y3 = make_double2(d02.x - rd13.x, d02.y - rd13.y);
+        double2 w1 = P.tw[(j * tstep) % n], w2 = P.tw[(2 * j * tstep) % n], w3 = P.tw[(3 * j * tstep) % n];
+        if (SIGN > 0) { w1.y = -w1.y; w2.y = -w2.y; w3.y = -w3.y; }
+        base[0] = y0;
+        base[span] = cmul(y1, w1);
+        base[2 * span] = cmul(y2, w2);
+        base[3 * span] = cmul(y3, w3);
+      } else {
+        // generic radix p (O(p^2)); p <= 64 buffered in registers/local memory
+        double2 in[64];
+        const int pp = p <= 64 ? p : 64;
+        for (int r = 0; r < pp; ++r) in[r] = base[r * span];
+        for (int q = 0; q < pp; ++q) {
+          double2 acc = make_double2(0.0, 0.0);
+          for (int r = 0; r < pp; ++r) {
+            double2 w = P.tw[((int64_t)((r * q) % p) * (n / p)) % n];
+            if (SIGN > 0) w.y = -w.y;
+            const double2 v = cmul(in[r], w);
+            acc.x += v.x;
+            acc.y += v.y;
+          }
+          double2 w = P.tw[((int64_t)j * q * tstep) % n];
+          if (SIGN > 0) w.y = -w.y;
+          base[q * span] = cmul(acc, w);
+        }
+      }
+    }
+    __syncthreads();
+    len = span;
+  }
+}
+
+__device__ __forceinline__ int fft_pos(int k, const FftPlan& P) {
+  int pos = 0, len = P.n;
+  for (int s = 0; s < P.stages; ++s) {
+    const int p = P.radix[s];
+    len /= p;
+    pos += (k % p) * len;
+    k /= p;
+  }
+  return pos;
+}
+
+// Forward ring stage (sht.cpp:211-222): fields (T, n_theta, n_phi) ->
+// G[m][s][i], s = 2 t + {re, im}, scaled by 1/n_phi. grid (ceil(n_theta/R), T).
+__global__ void k_ring_fft_fwd(const double* __restrict__ fields, int n_theta, int L, int R, FftPlan P,
+                               int T, double* __restrict__ G) {
+  extern __shared__ double2 xs[];
+  const int n = P.n;
+  const int i0 = blockIdx.x * R, t = blockIdx.y;
+  const int rings = min(R, n_theta - i0);
+  const double* src = fields + ((int64_t)t * n_theta + i0) * n;
+  for (int e = threadIdx.x; e < rings * n; e += blockDim.x) xs[e] = make_double2(src[e], 0.0);
+  __syncthreads();
+  fft_dif_rings<-1>(xs, rings, P);
+  const double inv = 1.0 / n;
+  const int64_t sstride = (int64_t)2 * T * n_theta;  // per m
+  for (int e = threadIdx.x; e < L * 2 * rings; e += blockDim.x) {
+    const int r = e % rings, c = (e / rings) & 1, m = e / (2 * rings);
+    const double2 v = xs[r * n + fft_pos(m, P)];
+    G[(int64_t)m * sstride + (int64_t)(2 * t + c) * n_theta + i0 + r] = (c ? v.y : v.x) * inv;
+  }
+}
+
+// Inverse ring stage (sht.cpp:345-356): Hermitian fill, unnormalized
+// synthesis, real part. G[m][s][i] -> fields (T, n_theta, n_phi).
+__global__ void k_ring_fft_inv(const double* __restrict__ G, int n_theta, int L, int R, FftPlan P, int T,
+                               double* __restrict__ fields) {
+  extern __shared__ double2 xs[];
+  const int n = P.n;
+  const int i0 = blockIdx.x * R, t = blockIdx.y;
+  const int rings = min(R, n_theta - i0);
+  const int64_t sstride = (int64_t)2 * T * n_theta;
+  for (int e = threadIdx.x; e < rings * n; e += blockDim.x) xs[e] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int e = threadIdx.x; e < rings * L; e += blockDim.x) {
+    const int r = e % rings, m = e / rings;
+    const double re = G[(int64_t)m * sstride + (int64_t)(2 * t) * n_theta + i0 + r];
+    const double im = G[(int64_t)m * sstride + (int64_t)(2 * t + 1) * n_theta + i0 + r];
+    if (m == 0) {
+      xs[r * n] = make_double2(re, im);
+    } else {
+      xs[r * n + m] = make_double2(re, im);
+      xs[r * n + n - m] = make_double2(re, -im);
+    }
+  }
+  __syncthreads();
+  fft_dif_rings<+1>(xs, rings, P);
+  double* dst = fields + ((int64_t)t * n_theta + i0) * n;
+  for (int e = threadIdx.x; e < rings * n; e += blockDim.x) {
+    const int r = e / n, j = e % n;
+    dst[e] = xs[r * n + fft_pos(j, P)].x;
+  }
+}
+
+// ===========================================================================
+// Device: Legendre stages (grouped FP64 GEMMs over m)
+// ===========================================================================
+// Forward: F_m (L-m x 2T) = Psi_m (L-m x n_theta) * G_m^T; scattered into the
+// packed layout (sht.hpp:38-45): m = 0 keeps the real part only.
+__global__ void __launch_bounds__(DG_THREADS) k_legendre_fwd(const double* __restrict__ psi,
+                                                              const int64_t* psi_off, const double* __restrict__ G,
+                                                              int L, int n_theta, int T, double* coeffs) {
+  __shared__ DgSmem sm;
+  const int m = blockIdx.z;
+  const int rows = L - m;
+  const int r0 = blockIdx.y * DG_BM, c0 = blockIdx.x * DG_BN;
+  if (r0 >= rows) return;
+  const int ncols = 2 * T;
+  RowMajorK A{psi + psi_off[m] + (int64_t)r0 * n_theta, n_theta, min(DG_BM, rows - r0), n_theta};
+  RowMajorK B{G + (int64_t)m * ncols * n_theta + (int64_t)c0 * n_theta, n_theta, min(DG_BN, ncols - c0), n_theta};
+  double acc[4][4][2];
+  dgemm_64x64(A, B, n_theta, sm, acc);
+  const int64_t nc = (int64_t)L * L;
+  dg_for_each(acc, [&](int r, int c, double v) {
+    const int l = m + r0 + r, s = c0 + c;
+    if (r0 + r >= rows || s >= ncols) return;
+    const int t = s >> 1, part = s & 1;
+    if (m == 0) {
+      if (part == 0) coeffs[(int64_t)t * nc + (int64_t)l * l] = v;
+    } else {
+      coeffs[(int64_t)t * nc + (int64_t)l * l + 2 * m - 1 + part] = v;
+    }
+  });
+}
+
+// Z[m][s][l - m] from packed coefficients (m = 0 imaginary part is zero).
+__global__ void k_gather_z(const double* __restrict__ coeffs, int L, int T, const int64_t* z_off, double* Z) {
+  const int m = blockIdx.y;
+  const int s = blockIdx.x;
+  const int t = s >> 1, part = s & 1;
+  const int cols = L - m;
+  const int64_t nc = (int64_t)L * L;
+  double* dst = Z + z_off[m] * 2 * T + (int64_t)s * cols;
+  for (int r = threadIdx.x; r < cols; r += blockDim.x) {
+    const int l = m + r;
+    double v;
+    if (m == 0) v = part ? 0.0 : coeffs[(int64_t)t * nc + (int64_t)l * l];
+    else v = coeffs[(int64_t)t * nc + (int64_t)l * l + 2 * m - 1 + part];
+    dst[r] = v;
+  }
+}
+
+// Inverse: G_m^T (2T x n_theta) = Z_m (2T x L-m) * Y_m^T, G[m][s][i].
+__global__ void __launch_bounds__(DG_THREADS) k_legendre_inv(const double* __restrict__ y, const int64_t* y_off,
+                                                              const double* __restrict__ Z, const int64_t* z_off,
+                                                              int L, int n_theta, int T, double* G) {
+  __shared__ DgSmem sm;
+  const int m = blockIdx.z;
+  const int cols = L - m;
+  const int ncols = 2 * T;
+  const int r0 = blockIdx.y * DG_BM, c0 = blockIdx.x * DG_BN;
+  if (r0 >= ncols) return;
+  RowMajorK A{Z + z_off[m] * ncols + (int64_t)r0 * cols, cols, min(DG_BM, ncols - r0), cols};
+  RowMajorK B{y + y_off[m] + (int64_t)c0 * cols, cols, min(DG_BN, n_theta - c0), cols};
+  double acc[4][4][2];
+  dgemm_64x64(A, B, cols, sm, acc);
+  double* out = G + (int64_t)m * ncols * n_theta;
+  dg_for_each(acc, [&](int r, int c, double v) {
+    if (r0 + r < ncols && c0 + c < n_theta) out[(int64_t)(r0 + r) * n_theta + c0 + c] = v;
+  });
+}
+
+// ===========================================================================
+// Host plan
+// ===========================================================================
+struct Sht {
+  int n_theta = 0, n_phi = 0, L = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf<double> psi, y;
+  DevBuf<int64_t> d_psi_off, d_y_off, d_z_off;
+  std::vector<int64_t> psi_off, y_off, z_off;
+  DevBuf<double2> tw_phi;
+  FftPlan fplan{};
+  int rings_per_cta = 1;
+  size_t fft_smem = 0;
+  int chunk = 64;
+  DevBuf<double> G, Z, fields_buf, coeffs_buf;
+  double plan_seconds = 0.0;
+
+  Sht(int nt, int np, int L_, size_t cap) : n_theta(nt), n_phi(np), L(L_) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (n_theta < 2) throw std::invalid_argument("grid needs at least two latitude rings");
+    if (n_phi < 1) throw std::invalid_argument("grid needs at least one longitude point");
+    const int maxL = std::min(n_theta - 1, (n_phi + 1) / 2);
+    if (L < 1 || L > maxL)
+      throw std::invalid_argument("grid " + std::to_string(n_theta) + "x" + std::to_string(n_phi) +
+                                  " does not resolve band limit " + std::to_string(L));
+    WignerHost w = build_wigner(L, cap ? cap : (size_t{2} << 30));
+    SPH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    // Offsets of the per-m operators.
+    psi_off.resize(L + 1);
+    y_off.resize(L + 1);
+    z_off.resize(L + 1);
+    int64_t po = 0, zo = 0;
+    for (int m = 0; m < L; ++m) {
+      psi_off[m] = po;
+      y_off[m] = po;
+      z_off[m] = zo;
+      po += (int64_t)(L - m) * n_theta;
+      zo += L - m;
+    }
+    psi_off[L] = y_off[L] = po;
+    z_off[L] = zo;
+    psi.alloc(po);
+    y.alloc(po);
+    d_psi_off.alloc(L + 1);
+    d_y_off.alloc(L + 1);
+    d_z_off.alloc(L + 1);
+    SPH_CUDA(cudaMemcpy(d_psi_off.get(), psi_off.data(), (L + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    SPH_CUDA(cudaMemcpy(d_y_off.get(), y_off.data(), (L + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    SPH_CUDA(cudaMemcpy(d_z_off.get(), z_off.data(), (L + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    // Wigner chains to the device.
+    DevBuf<double> dd(w.d.size());
+    DevBuf<int64_t> doff(w.off.size());
+    SPH_CUDA(cudaMemcpy(dd.get(), w.d.data(), w.d.size() * sizeof(double), cudaMemcpyHostToDevice));
+    SPH_CUDA(cudaMemcpy(doff.get(), w.off.data(), w.off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    // Twiddles of the extended line and the T_+/- tables (host, exact angles).
+    const int n_ext = 2 * n_theta - 2;
+    std::vector<double2> tw_ext(n_ext);
+    for (int t = 0; t < n_ext; ++t) {
+      const double a = 2.0 * M_PI * t / n_ext;
+      tw_ext[t] = make_double2(std::cos(a), -std::sin(a));
+    }
+    std::vector<double> tcos((size_t)L * n_theta), tsin((size_t)L * n_theta);
+    for (int mp = 0; mp < L; ++mp)
+      for (int i = 0; i < n_theta; ++i) {
+        const int64_t tt = ((int64_t)mp * i) % n_ext;
+        const double a = 2.0 * M_PI * tt / n_ext;
+        tcos[(size_t)mp * n_theta + i] = mp == 0 ? 1.0 : 2.0 * std::cos(a);
+        tsin[(size_t)mp * n_theta + i] = mp == 0 ? 0.0 : 2.0 * std::sin(a);
+      }
+    DevBuf<double2> dtw(n_ext);
+    DevBuf<double> dtc(tcos.size()), dts(tsin.size()), vre((size_t)L * n_theta), vim((size_t)L * n_theta);
+    SPH_CUDA(cudaMemcpy(dtw.get(), tw_ext.data(), n_ext * sizeof(double2), cudaMemcpyHostToDevice));
+    SPH_CUDA(cudaMemcpy(dtc.get(), tcos.data(), tcos.size() * sizeof(double), cudaMemcpyHostToDevice));
+    SPH_CUDA(cudaMemcpy(dts.get(), tsin.data(), tsin.size() * sizeof(double), cudaMemcpyHostToDevice));
+    k_sht_vtables<<<dim3(ceil_div(n_theta, 128), L), 128, 0, stream>>>(L, n_theta, dtw.get(), vre.get(), vim.get());
+    SPH_LAUNCH_CHECK();
+    k_sht_build_psi<<<dim3(ceil_div(n_theta, DG_BN), ceil_div(L, DG_BM), L), DG_THREADS, 0, stream>>>(
+        dd.get(), doff.get(), L, n_theta, vre.get(), vim.get(), d_psi_off.get(), psi.get());
+    SPH_LAUNCH_CHECK();
+    k_sht_build_y<<<dim3(ceil_div(n_theta, DG_BM), ceil_div(L, DG_BN), L), DG_THREADS, 0, stream>>>(
+        dd.get(), doff.get(), L, n_theta, dtc.get(), dts.get(), d_y_off.get(), y.get());
+    SPH_LAUNCH_CHECK();
+    // Ring FFT plan.
+    fplan.n = n_phi;
+    fplan.stages = 0;
+    int rem = n_phi;
+    auto push = [&](int p) {
+      if (fplan.stages >= FFT_MAX_STAGES) throw std::invalid_argument("n_phi has too many factors");
+      fplan.radix[fplan.stages++] = p;
+    };
+    while (rem % 4 == 0) { push(4); rem /= 4; }
+    while (rem % 2 == 0) { push(2); rem /= 2; }
+    for (int p = 3; rem > 1; p += 2)
+      while (rem % p == 0) { push(p); rem /= p; }
+    for (int s = 0; s < fplan.stages; ++s)
+      if (fplan.radix[s] > 64)
+        throw std::invalid_argument("n_phi has a prime factor above 64 (" + std::to_string(fplan.radix[s]) + ")");
+    std::vector<double2> twp(n_phi);
+    for (int t = 0; t < n_phi; ++t) {
+      const double a = 2.0 * M_PI * t / n_phi;
+      twp[t] = make_double2(std::cos(a), -std::sin(a));
+    }
+    tw_phi.alloc(n_phi);
+    SPH_CUDA(cudaMemcpy(tw_phi.get(), twp.data(), n_phi * sizeof(double2), cudaMemcpyHostToDevice));
+    fplan.tw = tw_phi.get();
+    rings_per_cta = std::max(1, std::min(n_theta, 65536 / (16 * n_phi)));
+    fft_smem = (size_t)rings_per_cta * n_phi * sizeof(double2);
+    if (fft_smem > 48 * 1024) {
+      SPH_CUDA(cudaFuncSetAttribute(k_ring_fft_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
+      SPH_CUDA(cudaFuncSetAttribute(k_ring_fft_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
+    }
+    // Snapshot chunk: bound the G staging to ~1 GiB.
+    const double per = 16.0 * L * n_theta + 16.0 * L * L;
+    chunk = (int)std::max(1.0, std::min(1024.0, (1024.0 * 1024 * 1024) / per));
+    SPH_CUDA(cudaStreamSynchronize(stream));
+    plan_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+
+  ~Sht() {
+    if (stream) {
+      cudaStreamSynchronize(stream);
+      cudaStreamDestroy(stream);
+    }
+  }
+
+  void ensure(int64_t tchunk) {
+    const size_t g = (size_t)L * 2 * tchunk * n_theta;
+    if (G.n < g) G.alloc(g);
+    const size_t z = (size_t)z_off[L] * 2 * tchunk;
+    if (Z.n < z) Z.alloc(z);
+  }
+
+  // Device-resident batched transforms.
+  void forward_dev(const double* fields, int64_t n, double* coeffs) {
+    const int64_t pts = (int64_t)n_theta * n_phi, nc = (int64_t)L * L;
+    for (int64_t t0 = 0; t0 < n; t0 += chunk) {
+      const int T = (int)std::min<int64_t>(chunk, n - t0);
+      ensure(T);
+      k_ring_fft_fwd<<<dim3(ceil_div(n_theta, rings_per_cta), T), 256, fft_smem, stream>>>(
+          fields + t0 * pts, n_theta, L, rings_per_cta, fplan, T, G.get());
+      SPH_LAUNCH_CHECK();
+      k_legendre_fwd<<<dim3(ceil_div(2 * T, DG_BN), ceil_div(L, DG_BM), L), DG_THREADS, 0, stream>>>(
+          psi.get(), d_psi_off.get(), G.get(), L, n_theta, T, coeffs + t0 * nc);
+      SPH_LAUNCH_CHECK();
+    }
+  }
+
+  void inverse_dev(const double* coeffs, int64_t n, double* fields) {
+    const int64_t pts = (int64_t)n_theta * n_phi, nc = (int64_t)L * L;
+    for (int64_t t0 = 0; t0 < n; t0 += chunk) {
+      const int T = (int)std::min<int64_t>(chunk, n - t0);
+      ensure(T);
+      k_gather_z<<<dim3(2 * T, L), 128, 0, stream>>>(coeffs + t0 * nc, L, T, d_z_off.get(), Z.get());
+      SPH_LAUNCH_CHECK();
+      k_legendre_inv<<<dim3(ceil_div(n_theta, DG_BN), ceil_div(2 * T, DG_BM), L), DG_THREADS, 0, stream>>>(
+          y.get(), d_y_off.get(), Z.get(), d_z_off.get(), L, n_theta, T, G.get());
+      SPH_LAUNCH_CHECK();
+      k_ring_fft_inv<<<dim3(ceil_div(n_theta, rings_per_cta), T), 256, fft_smem, stream>>>(
+          G.get(), n_theta, L, rings_per_cta, fplan, T, fields + t0 * pts);
+      SPH_LAUNCH_CHECK();
+    }
+  }
+
+  void forward(const double* in, int win, int64_t n, double* out, int wout) {
+    if (n <= 0) return;
+    const int64_t pts = (int64_t)n_theta * n_phi, nc = (int64_t)L * L;
+    if (win == SPHEMU_DEVICE && wout == SPHEMU_DEVICE) {
+      forward_dev(in, n, out);
+      SPH_CUDA(cudaStreamSynchronize(stream));
+      return;
+    }
+    // Host buffers: stream chunks through device staging.
+    const int64_t step = chunk;
+    DevBuf<double> fin(win == SPHEMU_HOST ? (size_t)std::min(n, step) * pts : 0);
+    DevBuf<double> cout(wout == SPHEMU_HOST ? (size_t)std::min(n, step) * nc : 0);
+    for (int64_t t0 = 0; t0 < n; t0 += step) {
+      const int64_t T = std::min(step, n - t0);
+      const double* src = in + t0 * pts;
+      if (win == SPHEMU_HOST) {
+        SPH_CUDA(cudaMemcpyAsync(fin.get(), src, T * pts * sizeof(double), cudaMemcpyHostToDevice, stream));
+        src = fin.get();
+      }
+      double* dst = wout == SPHEMU_HOST ? cout.get() : out + t0 * nc;
+      forward_dev(src, T, dst);
+      if (wout == SPHEMU_HOST)
+        SPH_CUDA(cudaMemcpyAsync(out + t0 * nc, dst, T * nc * sizeof(double), cudaMemcpyDeviceToHost, stream));
+      SPH_CUDA(cudaStreamSynchronize(stream));
+    }
+  }
+
+  void inverse(const double* in, int win, int64_t n, double* out, int wout) {
+    if (n <= 0) return;
+    const int64_t pts = (int64_t)n_theta * n_phi, nc = (int64_t)L * L;
+    if (win == SPHEMU_DEVICE && wout == SPHEMU_DEVICE) {
+      inverse_dev(in, n, out);
+      SPH_CUDA(cudaStreamSynchronize(stream));
+      return;
+    }
+    const int64_t step = chunk;
+    DevBuf<double> cin(win == SPHEMU_HOST ? (size_t)std::min(n, step) * nc : 0);
+    DevBuf<double> fout(wout == SPHEMU_HOST ? (size_t)std::min(n, step) * pts : 0);
+    for (int64_t t0 = 0; t0 < n; t0 += step) {
+      const int64_t T = std::min(step, n - t0);
+      const double* src = in + t0 * nc;
+      if (win == SPHEMU_HOST) {
+        SPH_CUDA(cudaMemcpyAsync(cin.get(), src, T * nc * sizeof(double), cudaMemcpyHostToDevice, stream));
+        src = cin.get();
+      }
+      double* dst = wout == SPHEMU_HOST ? fout.get() : out + t0 * pts;
+      inverse_dev(src, T, dst);
+      if (wout == SPHEMU_HOST)
+        SPH_CUDA(cudaMemcpyAsync(out + t0 * pts, dst, T * pts * sizeof(double), cudaMemcpyDeviceToHost, stream));
+      SPH_CUDA(cudaStreamSynchronize(stream));
+    }
+  }
+};
+
+}  // namespace sphemu_gpu
+
+using namespace sphemu_gpu;
+
+struct sphemu_sht_s {
+  Sht* p;
+};
+
+namespace sphemu_gpu {
+void emulate(void* plan, int n_theta, int n_phi, int L, const double* v, int d, const double* phi, int order,
+             const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed, int r_len,
+             int rng_mode, double* out);
+
+// Bridge for emulate.cu: the plan's stream, and a device-resident inverse.
+void sht_inverse_device(void* plan, const double* coeffs, int64_t n, double* fields, cudaStream_t* s_out) {
+  Sht* p = static_cast<sphemu_sht_s*>(plan)->p;
+  if (s_out) *s_out = p->stream;
+  if (n > 0) p->inverse_dev(coeffs, n, fields);
+}
+}  // namespace sphemu_gpu
+
+extern "C" {
+
+int sphemu_gpu_sht_create(int n_theta, int n_phi, int band_limit, size_t wigner_cap_bytes, sphemu_sht_t* out) {
+  return guard([&] {
+    *out = nullptr;
+    auto* h = new sphemu_sht_s{nullptr};
+    try {
+      h->p = new Sht(n_theta, n_phi, band_limit, wigner_cap_bytes);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int sphemu_gpu_sht_destroy(sphemu_sht_t p) {
+  return guard([&] {
+    if (!p) return;
+    delete p->p;
+    delete p;
+  });
+}
+
+int sphemu_gpu_sht_forward(sphemu_sht_t p, const double* fields, int where_in, int64_t n, double* coeffs,
+                           int where_out) {
+  return guard([&] { p->p->forward(fields, where_in, n, coeffs, where_out); });
+}
+
+int sphemu_gpu_sht_inverse(sphemu_sht_t p, const double* coeffs, int where_in, int64_t n, double* fields,
+                           int where_out) {
+  return guard([&] { p->p->inverse(coeffs, where_in, n, fields, where_out); });
+}
+
+void* sphemu_gpu_sht_stream(sphemu_sht_t p) { return p ? p->p->stream : nullptr; }
+double sphemu_gpu_sht_plan_seconds(sphemu_sht_t p) { return p ? p->p->plan_seconds : 0.0; }
+
+int sphemu_gpu_emulate(sphemu_sht_t p, const double* v, int d, const double* phi, int order, const double* means,
+                       const double* sigma, const double* v2, int t_out, uint64_t seed, int r_len, int rng_mode,
+                       double* out) {
+  return guard([&] {
+    emulate(p, p->p->n_theta, p->p->n_phi, p->p->L, v, d, phi, order, means, sigma, v2, t_out, seed, r_len,
+            rng_mode, out);
+  });
+}
+
+}  // extern "C"

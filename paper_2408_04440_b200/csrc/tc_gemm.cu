@@ -1,0 +1,583 @@
+// tc_gemm.cu — warp-specialized persistent tcgen05 GEMM for the SP/HP tile
+// classes of the Cholesky (see tc_gemm.cuh), plus the panel producers that
+// write the sender-side operand mirrors.
+//
+// CTA = 256 threads: warp 0 issues TMA, warp 1 issues tcgen05.mma (one
+// elected lane), warp 2 owns the TMEM allocation, warps 4-7 run the epilogue
+// (TMEM lane quarter = warp % 4). Two TMEM accumulators let the epilogue of
+// sub-tile t overlap the MMAs of sub-tile t+1. Each work item is a 128 x BN
+// sub-tile of one b x b output tile with K = b.
+#include <random>
+#include <vector>
+
+#include "tc_gemm.cuh"
+#include "tcgen05.cuh"
+
+namespace sphemu_gpu {
+
+// ---------------------------------------------------------------------------
+// Host: tensor maps
+// ---------------------------------------------------------------------------
+namespace {
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      throw Error(SPHEMU_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+
+// Row-major [rows x cols] array, box = 128 bytes of K x box_rows rows, SW128.
+CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int elem_bytes, int box_rows) {
+  CUtensorMap m;
+  const CUtensorMapDataType dt = elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * elem_bytes};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / elem_bytes), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(SPHEMU_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+  return m;
+}
+}  // namespace
+
+void PanelFormats::alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int hp_format_) {
+  (void)pmap;
+  nt = nt_;
+  b = b_;
+  hp_format = hp_format_;
+  bn = (b % 256 == 0) ? 256 : 128;
+  const int64_t rows = static_cast<int64_t>(nt - 1) * b;
+  const size_t elems = static_cast<size_t>(rows) * b;
+  p_hi.alloc(elems);
+  p_lo.alloc(elems);
+  p16.alloc(elems);
+  in_hi.alloc(elems);
+  in_lo.alloc(elems);
+  l_hi.alloc(static_cast<size_t>(b) * b);
+  l_lo.alloc(static_cast<size_t>(b) * b);
+  const int bn_tf32 = 128;  // tf32x3 uses 128-wide N tiles (smem budget)
+  m_phi_a = make_map(p_hi.get(), rows, b, 4, TC_BM);
+  m_plo_a = make_map(p_lo.get(), rows, b, 4, TC_BM);
+  m_phi_b = make_map(p_hi.get(), rows, b, 4, bn_tf32);
+  m_plo_b = make_map(p_lo.get(), rows, b, 4, bn_tf32);
+  m_p16_a = make_map(p16.get(), rows, b, 2, TC_BM);
+  m_p16_b = make_map(p16.get(), rows, b, 2, bn);
+  m_inhi_a = make_map(in_hi.get(), rows, b, 4, TC_BM);
+  m_inlo_a = make_map(in_lo.get(), rows, b, 4, TC_BM);
+  m_lhi_b = make_map(l_hi.get(), b, b, 4, bn_tf32);
+  m_llo_b = make_map(l_lo.get(), b, b, 4, bn_tf32);
+}
+
+// ---------------------------------------------------------------------------
+// Device: the persistent warp-specialized GEMM
+// ---------------------------------------------------------------------------
+enum : int { OP_F16 = 0, OP_BF16 = 1, OP_TF32X3 = 2 };
+enum : int { MODE_UPDATE = 0, MODE_PANEL = 1 };
+
+struct TcArgs {
+  TileStore ts;
+  const int2* list;  // output tiles (i, j); panel mode: (i, k)
+  int64_t items;     // list entries * sub-tiles per entry
+  int k;
+  int b;
+  int sub_n;         // b / BN
+  int sub_per;       // (b / 128) * sub_n
+  double* p64;
+  float* p_hi;
+  float* p_lo;
+  uint16_t* p16;
+  int hp_format;
+  const int* fail;
+  unsigned* sat;
+};
+
+template <int OPK>
+struct OpTraits {
+  static constexpr bool kSplit = (OPK == OP_TF32X3);
+  static constexpr int kElem = kSplit ? 4 : 2;
+  static constexpr int kBK = 128 / kElem;       // K elements per stage (one 128B swizzle row)
+  static constexpr int kUK = kSplit ? 8 : 16;   // K per tcgen05.mma
+  static constexpr int kFmt = OPK == OP_F16 ? 0 : (OPK == OP_BF16 ? 1 : 2);
+};
+
+template <int BN, int OPK>
+struct TcLayout {
+  using T = OpTraits<OPK>;
+  static constexpr int kA = TC_BM * 128;          // bytes of one A buffer
+  static constexpr int kB = BN * 128;             // bytes of one B buffer
+  static constexpr int kStage = (T::kSplit ? 2 : 1) * (kA + kB);
+  static constexpr int kStages = (T::kSplit ? 3 : 4);
+  static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kTmemCols = 2 * BN;        // double-buffered accumulator
+};
+
+template <int BN, int OPK, int MODE>
+__global__ void __launch_bounds__(256, 1)
+    k_tc_gemm(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
+              const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo,
+              const TcArgs args) {
+  using T = OpTraits<OPK>;
+  using Lay = TcLayout<BN, OPK>;
+  constexpr int S = Lay::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Lay::kStage);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (*(volatile const int*)args.fail >= 0) return;  // an earlier POTRF failed
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mA_hi);
+    tma_prefetch(&mB_hi);
+    if (T::kSplit) {
+      tma_prefetch(&mA_lo);
+      tma_prefetch(&mB_lo);
+    }
+  }
+  if (warp == 2) tmem_alloc(tmem_holder, Lay::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int kblocks = args.b / T::kBK;
+  const int64_t items = args.items;
+
+  auto decode = [&](int64_t w, int& i, int& j, int& m0, int& n0) {
+    const int2 ij = args.list[w / args.sub_per];
+    const int sub = static_cast<int>(w % args.sub_per);
+    i = ij.x;
+    j = ij.y;
+    m0 = (sub / args.sub_n) * TC_BM;
+    n0 = (sub % args.sub_n) * BN;
+  };
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+        int i, j, m0, n0;
+        decode(w, i, j, m0, n0);
+        const int a_row = (i - args.k - 1) * args.b + m0;
+        const int b_row = (MODE == MODE_UPDATE) ? (j - args.k - 1) * args.b + n0 : n0;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* st = smem + stage * Lay::kStage;
+          mbar_arrive_expect_tx(&full[stage], Lay::kStage);
+          const int kx = kb * T::kBK;
+          tma_load_2d(&mA_hi, &full[stage], st, kx, a_row);
+          tma_load_2d(&mB_hi, &full[stage], st + Lay::kA, kx, b_row);
+          if (T::kSplit) {
+            tma_load_2d(&mA_lo, &full[stage], st + Lay::kA + Lay::kB, kx, a_row);
+            tma_load_2d(&mB_lo, &full[stage], st + 2 * Lay::kA + Lay::kB, kx, b_row);
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (single thread) =====
+    constexpr uint32_t idesc = umma_idesc(T::kFmt, TC_BM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * BN;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          uint8_t* st = smem + stage * Lay::kStage;
+          const uint64_t a_hi = umma_desc_sw128(st);
+          const uint64_t b_hi = umma_desc_sw128(st + Lay::kA);
+#pragma unroll
+          for (int kk = 0; kk < T::kBK / T::kUK; ++kk) {
+            const uint64_t koff = (kk * T::kUK * T::kElem) >> 4;
+            const uint32_t accum = (kb | kk) ? 1u : 0u;
+            if constexpr (T::kSplit) {
+              const uint64_t a_lo = umma_desc_sw128(st + Lay::kA + Lay::kB);
+              const uint64_t b_lo = umma_desc_sw128(st + 2 * Lay::kA + Lay::kB);
+              umma_tf32(d, a_lo + koff, b_hi + koff, idesc, accum);
+              umma_tf32(d, a_hi + koff, b_lo + koff, idesc, 1u);
+              umma_tf32(d, a_hi + koff, b_hi + koff, idesc, 1u);
+            } else {
+              umma_f16(d, a_hi + koff, b_hi + koff, idesc, accum);
+            }
+          }
+          umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) umma_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue: TMEM -> registers -> tile storage (+ panel mirrors) =====
+    const int q = warp - 4;  // TMEM lane quarter
+    const int row_in = q * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    unsigned sat_local = 0;
+    const int b = args.b;
+    for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+      int i, j, m0, n0;
+      decode(w, i, j, m0, n0);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int r = m0 + row_in;
+      void* tp = args.ts.tile(i, j);
+      const int p = args.ts.tprec(i, j);
+      const int64_t prow = (int64_t)(i - args.k - 1) * b + r;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c0, v);
+        const int64_t e0 = (int64_t)r * b + n0 + c0;
+        if constexpr (MODE == MODE_UPDATE) {
+          if (p == kSP) {
+            float* cp = static_cast<float*>(tp) + e0;
+#pragma unroll
+            for (int t = 0; t < 32; t += 4) {
+              float4 cv = *reinterpret_cast<float4*>(cp + t);
+              cv.x = __double2float_rn((double)cv.x - (double)__uint_as_float(v[t + 0]));
+              cv.y = __double2float_rn((double)cv.y - (double)__uint_as_float(v[t + 1]));
+              cv.z = __double2float_rn((double)cv.z - (double)__uint_as_float(v[t + 2]));
+              cv.w = __double2float_rn((double)cv.w - (double)__uint_as_float(v[t + 3]));
+              *reinterpret_cast<float4*>(cp + t) = cv;
+            }
+          } else {
+            uint16_t* cp = static_cast<uint16_t*>(tp) + e0;
+#pragma unroll
+            for (int t = 0; t < 32; t += 8) {
+              uint4 raw = *reinterpret_cast<uint4*>(cp + t);
+              uint16_t* h = reinterpret_cast<uint16_t*>(&raw);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const double old = p == kHP ? (double)__half2float(__ushort_as_half(h[u]))
+                                            : (double)__bfloat162float(__ushort_as_bfloat16(h[u]));
+                const double nv = old - (double)__uint_as_float(v[t + u]);
+                h[u] = p == kHP ? __half_as_ushort(to_half_sat(nv, sat_local))
+                                : __bfloat16_as_ushort(to_bf16_sat(nv, sat_local));
+              }
+              *reinterpret_cast<uint4*>(cp + t) = raw;
+            }
+          }
+        } else {
+          // Panel: X = B * Linv^T rounded through p(i, k); write the tile, the
+          // FP64 mirror and the tensor mirrors.
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const double x = (double)__uint_as_float(v[t]);
+            const int64_t e = e0 + t;
+            const int64_t pe = prow * b + n0 + c0 + t;
+            double qv;
+            uint16_t h16;
+            if (p == kSP) {
+              const float f = __double2float_rn(x);
+              static_cast<float*>(tp)[e] = f;
+              qv = (double)f;
+              unsigned dummy = 0;
+              h16 = args.hp_format == SPHEMU_HP_BF16 ? __bfloat16_as_ushort(to_bf16_sat(qv, dummy))
+                                                    : __half_as_ushort(to_half_sat(qv, dummy));
+            } else if (p == kHP) {
+              const __half h = to_half_sat(x, sat_local);
+              h16 = __half_as_ushort(h);
+              static_cast<uint16_t*>(tp)[e] = h16;
+              qv = (double)__half2float(h);
+            } else {
+              const __nv_bfloat16 h = to_bf16_sat(x, sat_local);
+              h16 = __bfloat16_as_ushort(h);
+              static_cast<uint16_t*>(tp)[e] = h16;
+              qv = (double)__bfloat162float(h);
+            }
+            args.p64[pe] = qv;
+            float hi, lo;
+            tf32_split((float)qv, hi, lo);
+            args.p_hi[pe] = hi;
+            args.p_lo[pe] = lo;
+            args.p16[pe] = h16;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    sat_local = warp_sum_u32(sat_local);
+    if (lane == 0 && sat_local) atomicAdd(args.sat, sat_local);
+  }
+  __syncthreads();
+  if (warp == 2) tmem_dealloc(tmem_base, Lay::kTmemCols);
+}
+
+// ---------------------------------------------------------------------------
+// Panel producers
+// ---------------------------------------------------------------------------
+// tf32 splits of the panel TRSM inputs B_i (SP/HP-class panel tiles) and of
+// Linv (blockIdx.y == 0 handles Linv, y >= 1 the list entries).
+__global__ void k_panel_prep(TileStore ts, int k, const int2* list, const double* __restrict__ linv,
+                             float* in_hi, float* in_lo, float* l_hi, float* l_lo, const int* fail) {
+  if (*(volatile const int*)fail >= 0) return;
+  const int b = ts.b;
+  const int64_t bb = (int64_t)b * b;
+  if (blockIdx.y == 0) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += (int64_t)gridDim.x * blockDim.x) {
+      float hi, lo;
+      tf32_split(__double2float_rn(linv[e]), hi, lo);
+      l_hi[e] = hi;
+      l_lo[e] = lo;
+    }
+    return;
+  }
+  const int i = list[blockIdx.y - 1].x;
+  const void* tp = ts.tile(i, k);
+  const int p = ts.tprec(i, k);
+  const int64_t base = (int64_t)(i - k - 1) * bb;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += (int64_t)gridDim.x * blockDim.x) {
+    float hi, lo;
+    tf32_split((float)load_elem(tp, p, e), hi, lo);
+    in_hi[base + e] = hi;
+    in_lo[base + e] = lo;
+  }
+}
+
+// DP-class panel tiles: P64 (already rounded) -> tile storage + mirrors.
+__global__ void k_panel_finish_dp(TileStore ts, int k, const int2* list, const double* __restrict__ p64,
+                                  float* p_hi, float* p_lo, uint16_t* p16, int hp_format, const int* fail) {
+  if (*(volatile const int*)fail >= 0) return;
+  const int b = ts.b;
+  const int64_t bb = (int64_t)b * b;
+  const int i = list[blockIdx.y].x;
+  double* tp = static_cast<double*>(ts.tile(i, k));
+  const int64_t base = (int64_t)(i - k - 1) * bb;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += (int64_t)gridDim.x * blockDim.x) {
+    const double x = p64[base + e];
+    tp[e] = x;
+    float hi, lo;
+    tf32_split(__double2float_rn(x), hi, lo);
+    p_hi[base + e] = hi;
+    p_lo[base + e] = lo;
+    unsigned dummy = 0;
+    p16[base + e] = hp_format == SPHEMU_HP_BF16 ? __bfloat16_as_ushort(to_bf16_sat(x, dummy))
+                                                : __half_as_ushort(to_half_sat(x, dummy));
+  }
+}
+
+// DP-class panel tiles through FP64 DMMA (list variant of k_panel_trsm_fp64).
+__global__ void __launch_bounds__(DG_THREADS) k_panel_trsm_fp64_list(TileStore ts, int k, const int2* list,
+                                                                      const double* __restrict__ Linv,
+                                                                      double* __restrict__ P64,
+                                                                      const int* fail, unsigned* sat) {
+  __shared__ DgSmem sm;
+  if (*(volatile const int*)fail >= 0) return;
+  const int b = ts.b;
+  const int sub_per = b / DG_BM;
+  const int i = list[blockIdx.x / sub_per].x;
+  const int r0 = (blockIdx.x % sub_per) * DG_BM, c0 = blockIdx.y * DG_BN;
+  TileRowAcc A{ts.tile(i, k), ts.tprec(i, k), b, r0, b, b};
+  RowMajorK B{Linv + (int64_t)c0 * b, b, DG_BN, b};
+  double acc[4][4][2];
+  dgemm_64x64(A, B, b, sm, acc);
+  double* out = P64 + (int64_t)(i - k - 1) * b * b;
+  unsigned local = 0;
+  const int p = ts.tprec(i, k);
+  dg_for_each(acc, [&](int r, int c, double v) { out[(int64_t)(r0 + r) * b + c0 + c] = quantize_value(v, p, local); });
+  flush_sat(local, sat);
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers
+// ---------------------------------------------------------------------------
+namespace {
+
+template <int BN, int OPK, int MODE>
+void launch_tc(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi,
+               const CUtensorMap& b_lo, TcArgs args, cudaStream_t s) {
+  using Lay = TcLayout<BN, OPK>;
+  auto kern = k_tc_gemm<BN, OPK, MODE>;
+  static bool attr = false;
+  if (!attr) {
+    SPH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::kSmem));
+    attr = true;
+  }
+  const int grid = static_cast<int>(std::min<int64_t>(args.items, num_sms()));
+  kern<<<grid, 256, Lay::kSmem, s>>>(a_hi, a_lo, b_hi, b_lo, args);
+  SPH_LAUNCH_CHECK();
+}
+
+struct StepLists {
+  // per (k, class) panel-tile lists, cached per TileStore shape
+  int nt = -1;
+  const uint8_t* key = nullptr;
+  std::vector<std::vector<int2>> host;
+  std::vector<DevBuf<int2>> dev;
+};
+
+}  // namespace
+
+void tc_panel_trsm(const TileStore& ts, int k, int below, const double* linv, double* p64,
+                   PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s) {
+  // Panel tiles split by class (host copy of the map lives with the caller;
+  // the device map is consulted through a tiny host mirror built here once).
+  static thread_local std::vector<uint8_t> hmap;
+  static thread_local const uint8_t* hmap_key = nullptr;
+  static thread_local int64_t hmap_n = 0;
+  const int64_t ntiles = (int64_t)ts.nt * (ts.nt + 1) / 2;
+  if (hmap_key != ts.prec || hmap_n != ntiles) {
+    hmap.resize(ntiles);
+    SPH_CUDA(cudaMemcpy(hmap.data(), ts.prec, ntiles, cudaMemcpyDeviceToHost));
+    hmap_key = ts.prec;
+    hmap_n = ntiles;
+  }
+  std::vector<int2> dp, lo;
+  for (int i = k + 1; i < ts.nt; ++i) {
+    const int p = hmap[(int64_t)i * (i + 1) / 2 + k];
+    (p == kDP ? dp : lo).push_back(make_int2(i, k));
+  }
+  (void)below;
+  // Lists travel in a small per-stream scratch ring.
+  static thread_local DevBuf<int2> ring;
+  static thread_local size_t ring_pos = 0;
+  if (ring.n < (size_t)4 * ts.nt + 64) {
+    SPH_CUDA(cudaStreamSynchronize(s));
+    ring.alloc((size_t)64 * ts.nt + 1024);
+    ring_pos = 0;
+  }
+  auto upload = [&](const std::vector<int2>& v) -> const int2* {
+    if (v.empty()) return nullptr;
+    if (ring_pos + v.size() > ring.n) {
+      SPH_CUDA(cudaStreamSynchronize(s));
+      ring_pos = 0;
+    }
+    int2* d = ring.get() + ring_pos;
+    SPH_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+    ring_pos += v.size();
+    return d;
+  };
+  const int2* d_dp = upload(dp);
+  const int2* d_lo = upload(lo);
+  const int b = ts.b;
+  if (!dp.empty()) {
+    k_panel_trsm_fp64_list<<<dim3(static_cast<unsigned>(dp.size() * (b / DG_BM)), b / DG_BN), DG_THREADS, 0, s>>>(
+        ts, k, d_dp, linv, p64, fail, sat);
+    SPH_LAUNCH_CHECK();
+    k_panel_finish_dp<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(dp.size())), 256, 0, s>>>(
+        ts, k, d_dp, p64, pf.p_hi.get(), pf.p_lo.get(), pf.p16.get(), pf.hp_format, fail);
+    SPH_LAUNCH_CHECK();
+  }
+  if (!lo.empty()) {
+    k_panel_prep<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(lo.size() + 1)), 256, 0, s>>>(
+        ts, k, d_lo, linv, pf.in_hi.get(), pf.in_lo.get(), pf.l_hi.get(), pf.l_lo.get(), fail);
+    SPH_LAUNCH_CHECK();
+    TcArgs a{};
+    a.ts = ts;
+    a.list = d_lo;
+    a.k = k;
+    a.b = b;
+    a.sub_n = b / 128;
+    a.sub_per = (b / TC_BM) * a.sub_n;
+    a.items = (int64_t)lo.size() * a.sub_per;
+    a.p64 = p64;
+    a.p_hi = pf.p_hi.get();
+    a.p_lo = pf.p_lo.get();
+    a.p16 = pf.p16.get();
+    a.hp_format = pf.hp_format;
+    a.fail = fail;
+    a.sat = sat;
+    launch_tc<128, OP_TF32X3, MODE_PANEL>(pf.m_inhi_a, pf.m_inlo_a, pf.m_lhi_b, pf.m_llo_b, a, s);
+  }
+}
+
+void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* list, int64_t cnt,
+               const double* p64, PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s) {
+  (void)p64;
+  TcArgs a{};
+  a.ts = ts;
+  a.list = list;
+  a.k = k;
+  a.b = ts.b;
+  a.hp_format = hp_format;
+  a.fail = fail;
+  a.sat = sat;
+  if (cls == SPHEMU_PREC_SP) {
+    a.sub_n = ts.b / 128;
+    a.sub_per = (ts.b / TC_BM) * a.sub_n;
+    a.items = cnt * a.sub_per;
+    launch_tc<128, OP_TF32X3, MODE_UPDATE>(pf.m_phi_a, pf.m_plo_a, pf.m_phi_b, pf.m_plo_b, a, s);
+  } else {
+    a.sub_n = ts.b / pf.bn;
+    a.sub_per = (ts.b / TC_BM) * a.sub_n;
+    a.items = cnt * a.sub_per;
+    if (pf.bn == 256) {
+      if (hp_format == SPHEMU_HP_BF16)
+        launch_tc<256, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s);
+      else
+        launch_tc<256, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s);
+    } else {
+      if (hp_format == SPHEMU_HP_BF16)
+        launch_tc<128, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s);
+      else
+        launch_tc<128, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s);
+    }
+  }
+}
+
+// rng.hpp:12-39 uniform stream (mt19937_64, 53-bit in (0,1]) and
+// mpchol.cpp:423-429's d_i = exp(0.6u - 0.3), pw[k] = pow(0.9, k).
+void host_spd_factors(int n, uint64_t seed, double* d, double* pw) {
+  std::mt19937_64 eng(seed);
+  for (int i = 0; i < n; ++i) {
+    const double u = static_cast<double>((eng() >> 11) + 1) * 0x1.0p-53;
+    d[i] = std::exp(0.6 * u - 0.3);
+  }
+  for (int k = 0; k < n; ++k) pw[k] = std::pow(0.9, k);
+}
+
+}  // namespace sphemu_gpu

@@ -1,0 +1,51 @@
+// tc_gemm.cuh — tcgen05 (5th-gen tensor core) tile GEMMs of the Cholesky:
+// the SP/HP-class trailing updates (mpchol.cpp:300-314) and the panel TRSM
+// expressed as X = B * Linv^T (mpchol.cpp:293-299), with operands staged by
+// TMA into 128B-swizzled shared memory and accumulators in TMEM.
+//
+//   HP class (fp16 / bf16 tiles): kind::f16 (or bf16) operands, FP32 accumulate.
+//   SP class (fp32 tiles):        3xTF32 = hi*hi + hi*lo + lo*hi on kind::tf32,
+//                                 FP32 accumulate (~2^-21 relative products).
+// Operands are the per-step panel mirrors written once by the panel producer
+// (sender-side conversion).
+#pragma once
+
+#include <cuda.h>
+
+#include <vector>
+
+#include "chol_kernels.cuh"
+
+namespace sphemu_gpu {
+
+constexpr int TC_BM = 128;
+
+// Tensor-core operand mirrors of the current panel (rows (i-k-1)*b + r).
+struct PanelFormats {
+  int nt = 0, b = 0, hp_format = 0;
+  DevBuf<float> p_hi, p_lo;       // tf32 split of the rounded panel
+  DevBuf<uint16_t> p16;           // fp16/bf16 copy of the rounded panel
+  DevBuf<float> in_hi, in_lo;     // tf32 split of the panel TRSM input B_i
+  DevBuf<float> l_hi, l_lo;       // tf32 split of Linv (b x b)
+  // TMA descriptors: A-role (128-row box) and B-role (BN-row box).
+  CUtensorMap m_phi_a, m_plo_a, m_phi_b, m_plo_b, m_p16_a, m_p16_b;
+  CUtensorMap m_inhi_a, m_inlo_a, m_lhi_b, m_llo_b;
+  int bn = 256;
+  void alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int hp_format_);
+};
+
+// Panel TRSM for all i > k: DP-class tiles through FP64 DMMA, SP/HP-class
+// tiles through 3xTF32 tcgen05; writes the rounded P64 mirror, the tensor
+// mirrors, and the tile storage.
+void tc_panel_trsm(const TileStore& ts, int k, int below, const double* linv, double* p64,
+                   PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s);
+
+// Trailing update of the SP (cls 1) or HP (cls 2) output tiles of step k.
+void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* list, int64_t cnt,
+               const double* p64, PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s);
+
+// Host-side inputs of make_spd_test_matrix: d_i = exp(0.6 u_i - 0.3) with the
+// reference's GaussianRng uniform stream, pw[k] = std::pow(0.9, k).
+void host_spd_factors(int n, uint64_t seed, double* d, double* pw);
+
+}  // namespace sphemu_gpu
