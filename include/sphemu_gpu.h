@@ -122,6 +122,13 @@ int sphemu_gpu_chol_residual(sphemu_chol_t h, const double* a, int where, int64_
 int sphemu_gpu_chol_residual_probe_spd(sphemu_chol_t h, uint64_t seed, int n_vec, double* out);
 /* Per-precision flop split of the factorization (BASELINE.md §4 units). */
 int sphemu_gpu_chol_flops(sphemu_chol_t h, double* f_dp, double* f_sp, double* f_hp);
+/* Phase profiling (CUDA events around every phase; off by default). Phases:
+ * 0 POTRF+TRTRI, 1 panel TRSM, 2/3/4 trailing update of the DP/SP/HP
+ * classes, 5 tile load. ms/counts have 6 entries. */
+int sphemu_gpu_chol_set_profiling(sphemu_chol_t h, int on);
+int sphemu_gpu_chol_phase_times(sphemu_chol_t h, double* ms, int64_t* counts, int reset);
+/* Trailing-update flops by output class (2 b_i b_j b_k per GEMM, b_i^2 b_k per SYRK). */
+int sphemu_gpu_chol_update_flops(sphemu_chol_t h, double* f_dp, double* f_sp, double* f_hp);
 /* Device stream the handle enqueues on (cudaStream_t as void*). */
 void* sphemu_gpu_chol_stream(sphemu_chol_t h);
 

@@ -108,6 +108,12 @@ def lib():
         L.sphemu_gpu_sht_stream.restype = vp
         L.sphemu_gpu_sht_plan_seconds.argtypes = [vp]
         L.sphemu_gpu_sht_plan_seconds.restype = C.c_double
+        L.sphemu_gpu_chol_set_profiling.argtypes = [vp, C.c_int]
+        L.sphemu_gpu_chol_phase_times.argtypes = [vp, vp, vp, C.c_int]
+        L.sphemu_gpu_chol_update_flops.argtypes = [vp, dp, dp, dp]
+        L.sphemu_gpu_chol_residual_probe_spd.argtypes = [vp, C.c_uint64, C.c_int, dp]
+        L.sphemu_gpu_emulate.argtypes = [vp, vp, C.c_int, vp, C.c_int, vp, vp, vp, C.c_int, C.c_uint64,
+                                         C.c_int, C.c_int, vp]
         _lib = L
     return _lib
 
@@ -230,6 +236,48 @@ class Cholesky:
     @property
     def stream(self):
         return lib().sphemu_gpu_chol_stream(self.h)
+
+    PHASES = ("potrf", "panel", "update_dp", "update_sp", "update_hp", "load")
+
+    def set_profiling(self, on=True):
+        _check(lib().sphemu_gpu_chol_set_profiling(self.h, 1 if on else 0))
+
+    def phase_times(self, reset=False):
+        ms = np.zeros(6)
+        cnt = np.zeros(6, dtype=np.int64)
+        _check(lib().sphemu_gpu_chol_phase_times(self.h, _ptr(ms), _ptr(cnt), 1 if reset else 0))
+        return {p: {"ms": float(ms[i]), "launches": int(cnt[i])} for i, p in enumerate(self.PHASES)}
+
+    def reset_phase_times(self):
+        self.phase_times(reset=True)
+
+    def class_update_flops(self):
+        f = [C.c_double() for _ in range(3)]
+        _check(lib().sphemu_gpu_chol_update_flops(self.h, *[C.byref(x) for x in f]))
+        return {"dp": f[0].value, "sp": f[1].value, "hp": f[2].value}
+
+    def residual_probe(self, seed=1, n_vec=2):
+        out = C.c_double()
+        _check(lib().sphemu_gpu_chol_residual_probe_spd(self.h, seed, n_vec, C.byref(out)))
+        return out.value
+
+
+def emulate(plan, v, phi, means, sigma, v2, t_out, seed=1, r_len=1, rng="reference"):
+    """emulate (stochastic.cpp:217-277) with the trend evaluated by the caller
+    (means: t_out x points, sigma/v2: points). rng="reference" reproduces the
+    reference's serial mt19937_64 stream; "philox" draws on the device."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    d = v.shape[0]
+    phi = np.zeros((0, d)) if phi is None else np.ascontiguousarray(phi, dtype=np.float64).reshape(-1, d)
+    phi_a = phi if phi.shape[0] else np.zeros((1, d))
+    means = np.ascontiguousarray(means, dtype=np.float64)
+    sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+    v2 = np.ascontiguousarray(v2, dtype=np.float64)
+    out = np.empty((r_len, t_out, plan.n_theta, plan.n_phi))
+    mode = {"reference": 0, "philox": 1}[rng]
+    _check(lib().sphemu_gpu_emulate(plan.h, _ptr(v), d, _ptr(phi_a), phi.shape[0], _ptr(means), _ptr(sigma),
+                                    _ptr(v2), t_out, seed, r_len, mode, _ptr(out)))
+    return out
 
 
 def assign_precisions(n_tiles, variant="dp", band_width_dp=1, sp_fraction=0.05):

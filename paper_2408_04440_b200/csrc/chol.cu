@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "chol_kernels.cuh"
+#include "potrf_coop.cuh"
 #include "tc_gemm.cuh"
 
 namespace sphemu_gpu {
@@ -158,10 +159,44 @@ struct Chol {
   DevBuf<unsigned> sat;
   DevBuf<int2> lists;
   std::vector<int64_t> list_off, list_cnt;  // [k * 3 + class]
+  DevBuf<int2> plists;                      // panel tiles per step: DP class, then SP/HP
+  std::vector<int64_t> plist_off, plist_dp, plist_lo;
   PanelFormats panel;                       // tensor-core operand mirrors
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches_at_start = 0, launches = 0;
+  // Phase profiling (tracing subsystem): CUDA events around every phase
+  // launch, folded into per-phase totals at wait().
+  enum Phase { kPotrf = 0, kPanel = 1, kUpdDp = 2, kUpdSp = 3, kUpdHp = 4, kLoad = 5, kNumPhases = 6 };
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_marks;  // (phase, start event index)
+  double phase_ms[kNumPhases] = {0};
+  int64_t phase_n[kNumPhases] = {0};
+  int prof_begin(int phase) {
+    if (!profiling) return -1;
+    const size_t idx = ev_marks.size() * 2;
+    while (ev_pool.size() < idx + 2) {
+      cudaEvent_t e;
+      SPH_CUDA(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    ev_marks.push_back({phase, static_cast<int>(idx)});
+    SPH_CUDA(cudaEventRecord(ev_pool[idx], stream));
+    return static_cast<int>(idx);
+  }
+  void prof_end(int idx) {
+    if (idx >= 0) SPH_CUDA(cudaEventRecord(ev_pool[idx + 1], stream));
+  }
+  void prof_fold() {
+    for (auto& m : ev_marks) {
+      float ms = 0.f;
+      SPH_CUDA(cudaEventElapsedTime(&ms, ev_pool[m.second], ev_pool[m.second + 1]));
+      phase_ms[m.first] += ms;
+      phase_n[m.first] += 1;
+    }
+    ev_marks.clear();
+  }
   std::chrono::steady_clock::time_point t_start;
   bool factored = false;
 
@@ -201,7 +236,7 @@ struct Chol {
     SPH_CUDA(cudaMemcpy(d_prec.get(), sprec.data(), pmap.size(), cudaMemcpyHostToDevice));
     SPH_CUDA(cudaMemset(arena.get(), 0, static_cast<size_t>(o)));
     linv.alloc(static_cast<size_t>(b) * b);
-    dinv.alloc(static_cast<size_t>(b / 32 + 1) * 1024);
+    dinv.alloc(static_cast<size_t>(b / PC_BLK + 1) * PC_BLK * PC_BLK);
     if (nt > 1) p64.alloc(static_cast<size_t>(nt - 1) * b * b);
     fail.alloc(1);
     sat.alloc(1);
@@ -221,6 +256,23 @@ struct Chol {
       lists.alloc(all.size());
       SPH_CUDA(cudaMemcpy(lists.get(), all.data(), all.size() * sizeof(int2), cudaMemcpyHostToDevice));
     }
+    plist_off.assign(nt, 0);
+    plist_dp.assign(nt, 0);
+    plist_lo.assign(nt, 0);
+    std::vector<int2> pl;
+    for (int k = 0; k < nt; ++k) {
+      plist_off[k] = static_cast<int64_t>(pl.size());
+      for (int i = k + 1; i < nt; ++i)
+        if (pmap[tix(i, k)] == SPHEMU_PREC_DP) pl.push_back(make_int2(i, k));
+      plist_dp[k] = static_cast<int64_t>(pl.size()) - plist_off[k];
+      for (int i = k + 1; i < nt; ++i)
+        if (pmap[tix(i, k)] != SPHEMU_PREC_DP) pl.push_back(make_int2(i, k));
+      plist_lo[k] = static_cast<int64_t>(pl.size()) - plist_off[k] - plist_dp[k];
+    }
+    if (!pl.empty()) {
+      plists.alloc(pl.size());
+      SPH_CUDA(cudaMemcpy(plists.get(), pl.data(), pl.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    }
     if (cfg.compute == SPHEMU_COMPUTE_TENSOR && nt > 1) panel.alloc(nt, b, pmap, cfg.hp_format);
     SPH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     SPH_CUDA(cudaEventCreate(&ev0));
@@ -229,6 +281,7 @@ struct Chol {
 
   ~Chol() {
     if (stream) cudaStreamSynchronize(stream);
+    for (auto e : ev_pool) cudaEventDestroy(e);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -255,8 +308,10 @@ struct Chol {
       dptr = staging.get();
       lda = n;
     }
+    const int pl = prof_begin(kLoad);
     k_load_dense<<<tile_grid(), 256, 0, stream>>>(store(), dptr, lda, sat.get());
     SPH_LAUNCH_CHECK();
+    prof_end(pl);
     SPH_CUDA(cudaStreamSynchronize(stream));
   }
 
@@ -269,12 +324,14 @@ struct Chol {
     SPH_CUDA(cudaEventRecord(ev0, stream));
     const TileStore ts = store();
     for (int k = 0; k < nt; ++k) {
-      double* dkk = reinterpret_cast<double*>(arena.get() + off[tix(k, k)]);
-      k_potrf_trtri<<<1, PT_THREADS, 0, stream>>>(dkk, b, rows(k), linv.get(), dinv.get(),
-                                                  fail.get(), k);
-      SPH_LAUNCH_CHECK();
+      {
+        const int pe = prof_begin(kPotrf);
+        launch_potrf(k);
+        prof_end(pe);
+      }
       if (k + 1 >= nt) break;
       const int below = nt - k - 1;
+      const int pp = prof_begin(kPanel);
       if (cfg.compute == SPHEMU_COMPUTE_TENSOR) {
         panel_step_tensor(k);
       } else {
@@ -287,10 +344,12 @@ struct Chol {
             ts, k, p64.get(), fail.get());
         SPH_LAUNCH_CHECK();
       }
+      prof_end(pp);
       for (int cls = 0; cls < 3; ++cls) {
         const int64_t cnt = list_cnt[k * 3 + cls];
         if (!cnt) continue;
         const int2* lst = lists.get() + list_off[k * 3 + cls];
+        const int pu = prof_begin(kUpdDp + cls);
         if (cls != SPHEMU_PREC_DP && cfg.compute == SPHEMU_COMPUTE_TENSOR) {
           update_tensor(k, cls, lst, cnt);
         } else {
@@ -299,6 +358,7 @@ struct Chol {
               ts, k, lst, p64.get(), fail.get(), sat.get());
           SPH_LAUNCH_CHECK();
         }
+        prof_end(pu);
       }
     }
     SPH_CUDA(cudaEventRecord(ev1, stream));
@@ -307,6 +367,26 @@ struct Chol {
   }
 
   void panel_step_tensor(int k);
+
+  // Diagonal tile factor + inverse on a cooperative grid (potrf_coop.cuh).
+  void launch_potrf(int k) {
+    static bool attr = false;
+    const size_t smem = potrf_coop_smem();
+    if (!attr) {
+      SPH_CUDA(cudaFuncSetAttribute(k_potrf_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    const int nblk = (rows(k) + PC_BLK - 1) / PC_BLK;
+    const int G = std::max(1, std::min(32, nblk * (nblk + 1) / 2));
+    double* dkk = reinterpret_cast<double*>(arena.get() + off[tix(k, k)]);
+    int bk = rows(k), kk = k, bb = b;
+    double* lp = linv.get();
+    double* dp = dinv.get();
+    int* fp = fail.get();
+    void* args[] = {&dkk, &bb, &bk, &lp, &dp, &fp, &kk};
+    SPH_CUDA(cudaLaunchCooperativeKernel((void*)k_potrf_coop, dim3(G), dim3(DG_THREADS), args, smem, stream));
+    note_launch();
+  }
   void update_tensor(int k, int cls, const int2* lst, int64_t cnt);
 
   // Reads the failure flag; fills stats (mpchol.cpp:376-409).
@@ -316,6 +396,7 @@ struct Chol {
     unsigned s = 0;
     SPH_CUDA(cudaMemcpy(&f, fail.get(), sizeof(int), cudaMemcpyDeviceToHost));
     SPH_CUDA(cudaMemcpy(&s, sat.get(), sizeof(unsigned), cudaMemcpyDeviceToHost));
+    prof_fold();
     if (st) fill_stats(st, s);
     return f;
   }
@@ -423,6 +504,15 @@ struct Chol {
     return worst;
   }
 
+  // Trailing-update flops by output class (the tcgen05/DMMA update kernels).
+  void update_flops(double* f) const {
+    f[0] = f[1] = f[2] = 0.0;
+    for (int k = 0; k < nt; ++k)
+      for (int j = k + 1; j < nt; ++j)
+        for (int i = j; i < nt; ++i)
+          f[pmap[tix(i, j)]] += (i == j ? 1.0 : 2.0) * rows(i) * rows(j) * rows(k);
+  }
+
   void flops(double* f) const {
     f[0] = f[1] = f[2] = 0.0;
     auto cls = [&](int i, int j) { return static_cast<int>(pmap[tix(i, j)]); };
@@ -456,8 +546,9 @@ void Chol::generate_spd(uint64_t seed) {
 }
 
 void Chol::panel_step_tensor(int k) {
-  const int below = nt - k - 1;
-  tc_panel_trsm(store(), k, below, linv.get(), p64.get(), panel, fail.get(), sat.get(), stream);
+  const int2* base = plists.get() + plist_off[k];
+  tc_panel_trsm(store(), k, base, plist_dp[k], base + plist_dp[k], plist_lo[k], linv.get(), p64.get(), panel,
+                fail.get(), sat.get(), stream);
 }
 
 void Chol::update_tensor(int k, int cls, const int2* lst, int64_t cnt) {
@@ -569,6 +660,33 @@ int sphemu_gpu_chol_flops(sphemu_chol_t h, double* f_dp, double* f_sp, double* f
 
 int sphemu_gpu_chol_residual_probe_spd(sphemu_chol_t h, uint64_t seed, int n_vec, double* out) {
   return guard([&] { *out = h->c->residual_probe(seed, n_vec); });
+}
+
+int sphemu_gpu_chol_set_profiling(sphemu_chol_t h, int on) {
+  return guard([&] { h->c->profiling = on != 0; });
+}
+
+int sphemu_gpu_chol_phase_times(sphemu_chol_t h, double* ms, int64_t* counts, int reset) {
+  return guard([&] {
+    for (int p = 0; p < Chol::kNumPhases; ++p) {
+      if (ms) ms[p] = h->c->phase_ms[p];
+      if (counts) counts[p] = h->c->phase_n[p];
+      if (reset) {
+        h->c->phase_ms[p] = 0.0;
+        h->c->phase_n[p] = 0;
+      }
+    }
+  });
+}
+
+int sphemu_gpu_chol_update_flops(sphemu_chol_t h, double* f_dp, double* f_sp, double* f_hp) {
+  return guard([&] {
+    double f[3];
+    h->c->update_flops(f);
+    *f_dp = f[0];
+    *f_sp = f[1];
+    *f_hp = f[2];
+  });
 }
 
 void* sphemu_gpu_chol_stream(sphemu_chol_t h) { return h ? h->c->stream : nullptr; }

@@ -308,38 +308,53 @@ __global__ void __launch_bounds__(256, 1)
           }
         } else {
           // Panel: X = B * Linv^T rounded through p(i, k); write the tile, the
-          // FP64 mirror and the tensor mirrors.
+          // FP64 mirror and the tensor mirrors, 8 columns (>= 32 B) per store.
 #pragma unroll
-          for (int t = 0; t < 32; ++t) {
-            const double x = (double)__uint_as_float(v[t]);
+          for (int t = 0; t < 32; t += 8) {
             const int64_t e = e0 + t;
             const int64_t pe = prow * b + n0 + c0 + t;
-            double qv;
-            uint16_t h16;
-            if (p == kSP) {
-              const float f = __double2float_rn(x);
-              static_cast<float*>(tp)[e] = f;
-              qv = (double)f;
-              unsigned dummy = 0;
-              h16 = args.hp_format == SPHEMU_HP_BF16 ? __bfloat16_as_ushort(to_bf16_sat(qv, dummy))
-                                                    : __half_as_ushort(to_half_sat(qv, dummy));
-            } else if (p == kHP) {
-              const __half h = to_half_sat(x, sat_local);
-              h16 = __half_as_ushort(h);
-              static_cast<uint16_t*>(tp)[e] = h16;
-              qv = (double)__half2float(h);
-            } else {
-              const __nv_bfloat16 h = to_bf16_sat(x, sat_local);
-              h16 = __bfloat16_as_ushort(h);
-              static_cast<uint16_t*>(tp)[e] = h16;
-              qv = (double)__bfloat162float(h);
+            double qv[8];
+            uint16_t h16[8];
+            float fq[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const double x = (double)__uint_as_float(v[t + u]);
+              if (p == kSP) {
+                fq[u] = __double2float_rn(x);
+                qv[u] = (double)fq[u];
+                unsigned dummy = 0;
+                h16[u] = args.hp_format == SPHEMU_HP_BF16 ? __bfloat16_as_ushort(to_bf16_sat(qv[u], dummy))
+                                                         : __half_as_ushort(to_half_sat(qv[u], dummy));
+              } else if (p == kHP) {
+                const __half hv = to_half_sat(x, sat_local);
+                h16[u] = __half_as_ushort(hv);
+                qv[u] = (double)__half2float(hv);
+              } else {
+                const __nv_bfloat16 hv = to_bf16_sat(x, sat_local);
+                h16[u] = __bfloat16_as_ushort(hv);
+                qv[u] = (double)__bfloat162float(hv);
+              }
             }
-            args.p64[pe] = qv;
-            float hi, lo;
-            tf32_split((float)qv, hi, lo);
-            args.p_hi[pe] = hi;
-            args.p_lo[pe] = lo;
-            args.p16[pe] = h16;
+            if (p == kSP) {
+              float4* tf = reinterpret_cast<float4*>(static_cast<float*>(tp) + e);
+              tf[0] = make_float4(fq[0], fq[1], fq[2], fq[3]);
+              tf[1] = make_float4(fq[4], fq[5], fq[6], fq[7]);
+            } else {
+              *reinterpret_cast<uint4*>(static_cast<uint16_t*>(tp) + e) = *reinterpret_cast<const uint4*>(h16);
+            }
+            double2* pd = reinterpret_cast<double2*>(args.p64 + pe);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pd[u] = make_double2(qv[2 * u], qv[2 * u + 1]);
+            float hi[8], lo[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) tf32_split((float)qv[u], hi[u], lo[u]);
+            float4* ph = reinterpret_cast<float4*>(args.p_hi + pe);
+            float4* pl = reinterpret_cast<float4*>(args.p_lo + pe);
+            ph[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+            ph[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
+            pl[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+            pl[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
+            *reinterpret_cast<uint4*>(args.p16 + pe) = *reinterpret_cast<const uint4*>(h16);
           }
         }
       }
@@ -462,58 +477,20 @@ struct StepLists {
 
 }  // namespace
 
-void tc_panel_trsm(const TileStore& ts, int k, int below, const double* linv, double* p64,
-                   PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s) {
-  // Panel tiles split by class (host copy of the map lives with the caller;
-  // the device map is consulted through a tiny host mirror built here once).
-  static thread_local std::vector<uint8_t> hmap;
-  static thread_local const uint8_t* hmap_key = nullptr;
-  static thread_local int64_t hmap_n = 0;
-  const int64_t ntiles = (int64_t)ts.nt * (ts.nt + 1) / 2;
-  if (hmap_key != ts.prec || hmap_n != ntiles) {
-    hmap.resize(ntiles);
-    SPH_CUDA(cudaMemcpy(hmap.data(), ts.prec, ntiles, cudaMemcpyDeviceToHost));
-    hmap_key = ts.prec;
-    hmap_n = ntiles;
-  }
-  std::vector<int2> dp, lo;
-  for (int i = k + 1; i < ts.nt; ++i) {
-    const int p = hmap[(int64_t)i * (i + 1) / 2 + k];
-    (p == kDP ? dp : lo).push_back(make_int2(i, k));
-  }
-  (void)below;
-  // Lists travel in a small per-stream scratch ring.
-  static thread_local DevBuf<int2> ring;
-  static thread_local size_t ring_pos = 0;
-  if (ring.n < (size_t)4 * ts.nt + 64) {
-    SPH_CUDA(cudaStreamSynchronize(s));
-    ring.alloc((size_t)64 * ts.nt + 1024);
-    ring_pos = 0;
-  }
-  auto upload = [&](const std::vector<int2>& v) -> const int2* {
-    if (v.empty()) return nullptr;
-    if (ring_pos + v.size() > ring.n) {
-      SPH_CUDA(cudaStreamSynchronize(s));
-      ring_pos = 0;
-    }
-    int2* d = ring.get() + ring_pos;
-    SPH_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
-    ring_pos += v.size();
-    return d;
-  };
-  const int2* d_dp = upload(dp);
-  const int2* d_lo = upload(lo);
+void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, const int2* d_lo,
+                   int64_t n_lo, const double* linv, double* p64, PanelFormats& pf, const int* fail,
+                   unsigned* sat, cudaStream_t s) {
   const int b = ts.b;
-  if (!dp.empty()) {
-    k_panel_trsm_fp64_list<<<dim3(static_cast<unsigned>(dp.size() * (b / DG_BM)), b / DG_BN), DG_THREADS, 0, s>>>(
+  if (n_dp) {
+    k_panel_trsm_fp64_list<<<dim3(static_cast<unsigned>(n_dp * (b / DG_BM)), b / DG_BN), DG_THREADS, 0, s>>>(
         ts, k, d_dp, linv, p64, fail, sat);
     SPH_LAUNCH_CHECK();
-    k_panel_finish_dp<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(dp.size())), 256, 0, s>>>(
+    k_panel_finish_dp<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(n_dp)), 256, 0, s>>>(
         ts, k, d_dp, p64, pf.p_hi.get(), pf.p_lo.get(), pf.p16.get(), pf.hp_format, fail);
     SPH_LAUNCH_CHECK();
   }
-  if (!lo.empty()) {
-    k_panel_prep<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(lo.size() + 1)), 256, 0, s>>>(
+  if (n_lo) {
+    k_panel_prep<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(n_lo + 1)), 256, 0, s>>>(
         ts, k, d_lo, linv, pf.in_hi.get(), pf.in_lo.get(), pf.l_hi.get(), pf.l_lo.get(), fail);
     SPH_LAUNCH_CHECK();
     TcArgs a{};
@@ -523,7 +500,7 @@ void tc_panel_trsm(const TileStore& ts, int k, int below, const double* linv, do
     a.b = b;
     a.sub_n = b / 128;
     a.sub_per = (b / TC_BM) * a.sub_n;
-    a.items = (int64_t)lo.size() * a.sub_per;
+    a.items = n_lo * a.sub_per;
     a.p64 = p64;
     a.p_hi = pf.p_hi.get();
     a.p_lo = pf.p_lo.get();

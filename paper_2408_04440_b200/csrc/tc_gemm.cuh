@@ -37,8 +37,9 @@ struct PanelFormats {
 // Panel TRSM for all i > k: DP-class tiles through FP64 DMMA, SP/HP-class
 // tiles through 3xTF32 tcgen05; writes the rounded P64 mirror, the tensor
 // mirrors, and the tile storage.
-void tc_panel_trsm(const TileStore& ts, int k, int below, const double* linv, double* p64,
-                   PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s);
+void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, const int2* d_lo,
+                   int64_t n_lo, const double* linv, double* p64, PanelFormats& pf, const int* fail,
+                   unsigned* sat, cudaStream_t s);
 
 // Trailing update of the SP (cls 1) or HP (cls 2) output tiles of step k.
 void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* list, int64_t cnt,
