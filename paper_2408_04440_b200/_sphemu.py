@@ -149,13 +149,13 @@ def make_config(variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_frac
 # module.cpp:209-214 tiled_cholesky / make_spd_matrix
 # ---------------------------------------------------------------------------
 def tiled_cholesky(a, variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_fraction=0.05,
-                   hp_format="fp16", compute="tensor"):
+                   hp_format="fp16", compute="tensor", lookahead=1):
     """Tiled Cholesky factorization; returns (lower_factor, stats_json)."""
     a = np.ascontiguousarray(a, dtype=np.float64)
     if a.ndim != 2 or a.shape[0] != a.shape[1]:
         raise ValueError("expected a square matrix")
     n = a.shape[0]
-    cfg = make_config(variant, tile_size, workers, band_width_dp, sp_fraction, hp_format, compute)
+    cfg = make_config(variant, tile_size, workers, band_width_dp, sp_fraction, hp_format, compute, lookahead)
     out = np.empty_like(a)
     st = CholStats()
     failed = C.c_int(-1)
@@ -179,7 +179,7 @@ class Cholesky:
     """Device-resident factorization (TiledMatrix + tiled_cholesky)."""
 
     def __init__(self, n, variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_fraction=0.05,
-                 hp_format="fp16", compute="tensor", lookahead=0):
+                 hp_format="fp16", compute="tensor", lookahead=1):
         self.n = n
         self.cfg = make_config(variant, tile_size, workers, band_width_dp, sp_fraction, hp_format,
                                compute, lookahead)

@@ -154,15 +154,21 @@ struct Chol {
   DevBuf<char> arena;
   DevBuf<int64_t> d_off;
   DevBuf<uint8_t> d_prec;
-  DevBuf<double> linv, dinv, p64, spd_d, spd_pw;
+  DevBuf<double> linv_[2], p64_[2];  // double-buffered by step parity (lookahead)
+  DevBuf<double> dinv, spd_d, spd_pw;
   DevBuf<int> fail;
   DevBuf<unsigned> sat;
   DevBuf<int2> lists;
-  std::vector<int64_t> list_off, list_cnt;  // [k * 3 + class]
+  // Update lists per (step k, part, class): part 0 = next column (k+1, the
+  // critical chain), part 1 = the rest (columns >= k+2, the bulk).
+  std::vector<int64_t> list_off, list_cnt;  // [(k * 2 + part) * 3 + class]
   DevBuf<int2> plists;                      // panel tiles per step: DP class, then SP/HP
   std::vector<int64_t> plist_off, plist_dp, plist_lo;
-  PanelFormats panel;                       // tensor-core operand mirrors
-  cudaStream_t stream = nullptr;
+  PanelFormats panel_[2];                   // tensor-core operand mirrors per parity
+  cudaStream_t stream = nullptr;            // main stream: bulk trailing updates
+  cudaStream_t pstream = nullptr;           // high-priority stream: POTRF + panel chain
+  std::vector<cudaEvent_t> ev_panel, ev_bulk;
+  cudaEvent_t ev_start_p = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches_at_start = 0, launches = 0;
   // Phase profiling (tracing subsystem): CUDA events around every phase
@@ -173,7 +179,8 @@ struct Chol {
   std::vector<std::pair<int, int>> ev_marks;  // (phase, start event index)
   double phase_ms[kNumPhases] = {0};
   int64_t phase_n[kNumPhases] = {0};
-  int prof_begin(int phase) {
+  int prof_begin(int phase, cudaStream_t s = nullptr) {
+    if (!s) s = stream;
     if (!profiling) return -1;
     const size_t idx = ev_marks.size() * 2;
     while (ev_pool.size() < idx + 2) {
@@ -182,11 +189,12 @@ struct Chol {
       ev_pool.push_back(e);
     }
     ev_marks.push_back({phase, static_cast<int>(idx)});
-    SPH_CUDA(cudaEventRecord(ev_pool[idx], stream));
+    SPH_CUDA(cudaEventRecord(ev_pool[idx], s));
     return static_cast<int>(idx);
   }
-  void prof_end(int idx) {
-    if (idx >= 0) SPH_CUDA(cudaEventRecord(ev_pool[idx + 1], stream));
+  void prof_end(int idx, cudaStream_t s = nullptr) {
+    if (!s) s = stream;
+    if (idx >= 0) SPH_CUDA(cudaEventRecord(ev_pool[idx + 1], s));
   }
   void prof_fold() {
     for (auto& m : ev_marks) {
@@ -235,23 +243,27 @@ struct Chol {
     SPH_CUDA(cudaMemcpy(d_off.get(), off.data(), pmap.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     SPH_CUDA(cudaMemcpy(d_prec.get(), sprec.data(), pmap.size(), cudaMemcpyHostToDevice));
     SPH_CUDA(cudaMemset(arena.get(), 0, static_cast<size_t>(o)));
-    linv.alloc(static_cast<size_t>(b) * b);
+    for (int p = 0; p < 2; ++p) linv_[p].alloc(static_cast<size_t>(b) * b);
     dinv.alloc(static_cast<size_t>(b / PC_BLK + 1) * PC_BLK * PC_BLK);
-    if (nt > 1) p64.alloc(static_cast<size_t>(nt - 1) * b * b);
+    if (nt > 1)
+      for (int p = 0; p < 2; ++p) p64_[p].alloc(static_cast<size_t>(nt - 1) * b * b);
     fail.alloc(1);
     sat.alloc(1);
     // Per-step output-tile lists by precision class.
-    list_off.assign(static_cast<size_t>(nt) * 3 + 1, 0);
-    list_cnt.assign(static_cast<size_t>(nt) * 3, 0);
+    list_off.assign(static_cast<size_t>(nt) * 6 + 1, 0);
+    list_cnt.assign(static_cast<size_t>(nt) * 6, 0);
     std::vector<int2> all;
     for (int k = 0; k < nt; ++k)
-      for (int cls = 0; cls < 3; ++cls) {
-        list_off[k * 3 + cls] = static_cast<int64_t>(all.size());
-        for (int j = k + 1; j < nt; ++j)
-          for (int i = j; i < nt; ++i)
-            if (pmap[tix(i, j)] == cls) all.push_back(make_int2(i, j));
-        list_cnt[k * 3 + cls] = static_cast<int64_t>(all.size()) - list_off[k * 3 + cls];
-      }
+      for (int part = 0; part < 2; ++part)
+        for (int cls = 0; cls < 3; ++cls) {
+          const size_t slot = (static_cast<size_t>(k) * 2 + part) * 3 + cls;
+          list_off[slot] = static_cast<int64_t>(all.size());
+          const int j_lo = part == 0 ? k + 1 : k + 2, j_hi = part == 0 ? std::min(k + 2, nt) : nt;
+          for (int j = j_lo; j < j_hi; ++j)
+            for (int i = j; i < nt; ++i)
+              if (pmap[tix(i, j)] == cls) all.push_back(make_int2(i, j));
+          list_cnt[slot] = static_cast<int64_t>(all.size()) - list_off[slot];
+        }
     if (!all.empty()) {
       lists.alloc(all.size());
       SPH_CUDA(cudaMemcpy(lists.get(), all.data(), all.size() * sizeof(int2), cudaMemcpyHostToDevice));
@@ -273,15 +285,31 @@ struct Chol {
       plists.alloc(pl.size());
       SPH_CUDA(cudaMemcpy(plists.get(), pl.data(), pl.size() * sizeof(int2), cudaMemcpyHostToDevice));
     }
-    if (cfg.compute == SPHEMU_COMPUTE_TENSOR && nt > 1) panel.alloc(nt, b, pmap, cfg.hp_format);
-    SPH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    if (cfg.compute == SPHEMU_COMPUTE_TENSOR && nt > 1)
+      for (int p = 0; p < 2; ++p) panel_[p].alloc(nt, b, pmap, cfg.hp_format);
+    int prio_lo = 0, prio_hi = 0;
+    SPH_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    SPH_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, prio_lo));
+    SPH_CUDA(cudaStreamCreateWithPriority(&pstream, cudaStreamNonBlocking, prio_hi));
+    ev_panel.resize(nt);
+    ev_bulk.resize(nt);
+    for (int k = 0; k < nt; ++k) {
+      SPH_CUDA(cudaEventCreateWithFlags(&ev_panel[k], cudaEventDisableTiming));
+      SPH_CUDA(cudaEventCreateWithFlags(&ev_bulk[k], cudaEventDisableTiming));
+    }
+    SPH_CUDA(cudaEventCreateWithFlags(&ev_start_p, cudaEventDisableTiming));
     SPH_CUDA(cudaEventCreate(&ev0));
     SPH_CUDA(cudaEventCreate(&ev1));
   }
 
   ~Chol() {
     if (stream) cudaStreamSynchronize(stream);
+    if (pstream) cudaStreamSynchronize(pstream);
     for (auto e : ev_pool) cudaEventDestroy(e);
+    for (auto e : ev_panel) cudaEventDestroy(e);
+    for (auto e : ev_bulk) cudaEventDestroy(e);
+    if (ev_start_p) cudaEventDestroy(ev_start_p);
+    if (pstream) cudaStreamDestroy(pstream);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -317,59 +345,99 @@ struct Chol {
 
   void generate_spd(uint64_t seed);
 
+  // ---- the per-step operations, on a given stream and panel buffer set ----
+  void op_potrf(int k, cudaStream_t s) {
+    const int pe = prof_begin(kPotrf, s);
+    launch_potrf(k, s);
+    prof_end(pe, s);
+  }
+
+  void op_panel(int k, cudaStream_t s) {
+    const int set = k & 1;
+    const int pp = prof_begin(kPanel, s);
+    if (cfg.compute == SPHEMU_COMPUTE_TENSOR) {
+      const int2* base = plists.get() + plist_off[k];
+      tc_panel_trsm(store(), k, base, plist_dp[k], base + plist_dp[k], plist_lo[k], linv_[set].get(),
+                    p64_[set].get(), panel_[set], fail.get(), sat.get(), s);
+    } else {
+      const int below = nt - k - 1;
+      k_panel_trsm_fp64<<<dim3(below * (b / DG_BM), b / DG_BN), DG_THREADS, 0, s>>>(
+          store(), k, linv_[set].get(), p64_[set].get(), fail.get(), sat.get());
+      SPH_LAUNCH_CHECK();
+      k_panel_scatter<<<dim3(std::max(1, b * b / (256 * 16)), below), 256, 0, s>>>(store(), k, p64_[set].get(),
+                                                                                    fail.get());
+      SPH_LAUNCH_CHECK();
+    }
+    prof_end(pp, s);
+  }
+
+  void op_update(int k, int part, cudaStream_t s, int max_ctas) {
+    const int set = k & 1;
+    for (int cls = 0; cls < 3; ++cls) {
+      const size_t slot = (static_cast<size_t>(k) * 2 + part) * 3 + cls;
+      const int64_t cnt = list_cnt[slot];
+      if (!cnt) continue;
+      const int2* lst = lists.get() + list_off[slot];
+      const int pu = prof_begin(kUpdDp + cls, s);
+      if (cls != SPHEMU_PREC_DP && cfg.compute == SPHEMU_COMPUTE_TENSOR) {
+        tc_update(store(), k, cls, cfg.hp_format, lst, cnt, p64_[set].get(), panel_[set], fail.get(), sat.get(), s,
+                  max_ctas);
+      } else {
+        const int per = (b / DG_BM) * (b / DG_BN);
+        k_update_fp64<<<static_cast<unsigned>(cnt * per), DG_THREADS, 0, s>>>(store(), k, lst, p64_[set].get(),
+                                                                               fail.get(), sat.get());
+        SPH_LAUNCH_CHECK();
+      }
+      prof_end(pu, s);
+    }
+  }
+
+  // tiled_cholesky (mpchol.cpp:351-410). Without lookahead every operation is
+  // serialized on one stream. With lookahead the critical chain (update of
+  // column k+1 -> POTRF(k+1) -> panel(k+1)) runs on a high-priority stream
+  // while the bulk update of step k (columns >= k+2) runs on the main stream;
+  // the two touch disjoint tiles, panel buffers alternate by step parity, and
+  // every tile still receives its updates in k order (results are bitwise
+  // identical with and without lookahead).
   void factor() {
     factored = false;
     launches_at_start = launch_count();
     t_start = std::chrono::steady_clock::now();
     SPH_CUDA(cudaEventRecord(ev0, stream));
-    const TileStore ts = store();
-    for (int k = 0; k < nt; ++k) {
-      {
-        const int pe = prof_begin(kPotrf);
-        launch_potrf(k);
-        prof_end(pe);
+    const int reserve = 32;  // SMs left to the chain while the bulk runs
+    if (!cfg.lookahead || nt == 1) {
+      for (int k = 0; k < nt; ++k) {
+        op_potrf(k, stream);
+        if (k + 1 >= nt) break;
+        op_panel(k, stream);
+        op_update(k, 0, stream, 0);
+        op_update(k, 1, stream, 0);
       }
-      if (k + 1 >= nt) break;
-      const int below = nt - k - 1;
-      const int pp = prof_begin(kPanel);
-      if (cfg.compute == SPHEMU_COMPUTE_TENSOR) {
-        panel_step_tensor(k);
-      } else {
-        k_panel_trsm_fp64<<<dim3(below * (b / DG_BM), b / DG_BN), DG_THREADS, 0, stream>>>(
-            ts, k, linv.get(), p64.get(), fail.get(), sat.get());
-        SPH_LAUNCH_CHECK();
+    } else {
+      SPH_CUDA(cudaEventRecord(ev_start_p, stream));
+      SPH_CUDA(cudaStreamWaitEvent(pstream, ev_start_p, 0));
+      op_potrf(0, pstream);
+      op_panel(0, pstream);
+      SPH_CUDA(cudaEventRecord(ev_panel[0], pstream));
+      for (int k = 0; k + 1 < nt; ++k) {
+        if (k > 0) SPH_CUDA(cudaStreamWaitEvent(pstream, ev_bulk[k - 1], 0));
+        op_update(k, 0, pstream, 0);
+        op_potrf(k + 1, pstream);
+        if (k + 2 < nt) op_panel(k + 1, pstream);
+        SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
+        SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k], 0));
+        op_update(k, 1, stream, std::max(1, num_sms() - reserve));
+        SPH_CUDA(cudaEventRecord(ev_bulk[k], stream));
       }
-      if (cfg.compute != SPHEMU_COMPUTE_TENSOR) {
-        k_panel_scatter<<<dim3(std::max(1, b * b / (256 * 16)), below), 256, 0, stream>>>(
-            ts, k, p64.get(), fail.get());
-        SPH_LAUNCH_CHECK();
-      }
-      prof_end(pp);
-      for (int cls = 0; cls < 3; ++cls) {
-        const int64_t cnt = list_cnt[k * 3 + cls];
-        if (!cnt) continue;
-        const int2* lst = lists.get() + list_off[k * 3 + cls];
-        const int pu = prof_begin(kUpdDp + cls);
-        if (cls != SPHEMU_PREC_DP && cfg.compute == SPHEMU_COMPUTE_TENSOR) {
-          update_tensor(k, cls, lst, cnt);
-        } else {
-          const int per = (b / DG_BM) * (b / DG_BN);
-          k_update_fp64<<<static_cast<unsigned>(cnt * per), DG_THREADS, 0, stream>>>(
-              ts, k, lst, p64.get(), fail.get(), sat.get());
-          SPH_LAUNCH_CHECK();
-        }
-        prof_end(pu);
-      }
+      SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[nt - 1], 0));
     }
     SPH_CUDA(cudaEventRecord(ev1, stream));
     launches = launch_count() - launches_at_start;
     factored = true;
   }
 
-  void panel_step_tensor(int k);
-
   // Diagonal tile factor + inverse on a cooperative grid (potrf_coop.cuh).
-  void launch_potrf(int k) {
+  void launch_potrf(int k, cudaStream_t s) {
     static bool attr = false;
     const size_t smem = potrf_coop_smem();
     if (!attr) {
@@ -380,17 +448,17 @@ struct Chol {
     const int G = std::max(1, std::min(32, nblk * (nblk + 1) / 2));
     double* dkk = reinterpret_cast<double*>(arena.get() + off[tix(k, k)]);
     int bk = rows(k), kk = k, bb = b;
-    double* lp = linv.get();
+    double* lp = linv_[k & 1].get();
     double* dp = dinv.get();
     int* fp = fail.get();
     void* args[] = {&dkk, &bb, &bk, &lp, &dp, &fp, &kk};
-    SPH_CUDA(cudaLaunchCooperativeKernel((void*)k_potrf_coop, dim3(G), dim3(DG_THREADS), args, smem, stream));
+    SPH_CUDA(cudaLaunchCooperativeKernel((void*)k_potrf_coop, dim3(G), dim3(DG_THREADS), args, smem, s));
     note_launch();
   }
-  void update_tensor(int k, int cls, const int2* lst, int64_t cnt);
 
   // Reads the failure flag; fills stats (mpchol.cpp:376-409).
   int wait(sphemu_chol_stats* st) {
+    SPH_CUDA(cudaStreamSynchronize(pstream));
     SPH_CUDA(cudaStreamSynchronize(stream));
     int f = -1;
     unsigned s = 0;
@@ -543,16 +611,6 @@ void Chol::generate_spd(uint64_t seed) {
   k_gen_spd<<<tile_grid(), 256, 0, stream>>>(store(), spd_d.get(), spd_pw.get(), sat.get());
   SPH_LAUNCH_CHECK();
   SPH_CUDA(cudaStreamSynchronize(stream));
-}
-
-void Chol::panel_step_tensor(int k) {
-  const int2* base = plists.get() + plist_off[k];
-  tc_panel_trsm(store(), k, base, plist_dp[k], base + plist_dp[k], plist_lo[k], linv.get(), p64.get(), panel,
-                fail.get(), sat.get(), stream);
-}
-
-void Chol::update_tensor(int k, int cls, const int2* lst, int64_t cnt) {
-  tc_update(store(), k, cls, cfg.hp_format, lst, cnt, p64.get(), panel, fail.get(), sat.get(), stream);
 }
 
 }  // namespace sphemu_gpu

@@ -25,96 +25,142 @@ struct PcSmallSmem {
   int bad;
 };
 
-// Warp-level Cholesky-Crout of T[o:o+32, o:o+32] (lane = row) and inverse
-// into Di[o:o+32, o:o+32] (lane = column). Returns false on a bad pivot.
-__device__ bool pc_factor32(PcSmallSmem& s, int o, int w, int lane) {
-  for (int c = 0; c < 32; ++c) {
-    double v = s.T[o + lane][o + c];
-    for (int t = 0; t < c; ++t) v -= s.T[o + lane][o + t] * s.T[o + c][o + t];
-    const double piv = __shfl_sync(0xffffffffu, v, c);
-    if (c < w && !(piv > 0.0)) return false;
-    const double l = sqrt(piv);
-    if (lane == c) s.T[o + c][o + c] = l;
-    else if (lane > c) s.T[o + lane][o + c] = v / l;
-    __syncwarp();
+// 16 x 16 base case in registers (warp 0; lanes 0..15 own the rows):
+// right-looking Cholesky with one rsqrt per column, then the inverse by
+// right-looking forward substitution (lane j owns column j). Small unrolled
+// code (the 32-wide version thrashed the instruction cache).
+__device__ void pc_base16(PcSmallSmem& s, int o, int w, int lane) {
+  constexpr unsigned FULL = 0xffffffffu;
+  const int row = lane & 15;
+  double a[16], rl[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) a[t] = s.T[o + row][o + t];
+  bool ok = true;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    const double piv = __shfl_sync(FULL, a[c], c);
+    if (c < w && !(piv > 0.0)) ok = false;
+    rl[c] = rsqrt(piv);
+    const double lrc = (row == c) ? piv * rl[c] : a[c] * rl[c];
+    a[c] = lrc;
+#pragma unroll
+    for (int j = c + 1; j < 16; ++j) a[j] -= lrc * __shfl_sync(FULL, lrc, j);
   }
-  for (int r = 0; r < 32; ++r) {
-    if (r == lane) {
-      s.Di[o + r][o + lane] = 1.0 / s.T[o + r][o + r];
-    } else if (r > lane) {
-      double acc = 0.0;
-      for (int t = lane; t < r; ++t) acc += s.T[o + r][o + t] * s.Di[o + t][o + lane];
-      s.Di[o + r][o + lane] = -acc / s.T[o + r][o + r];
-    } else {
-      s.Di[o + r][o + lane] = 0.0;
-    }
-    __syncwarp();
+  if (!ok) {
+    if (lane == 0) s.bad = 1;
+    return;
   }
-  return true;
+  if (lane < 16)
+#pragma unroll
+    for (int t = 0; t < 16; ++t) s.T[o + lane][o + t] = t <= lane ? a[t] : 0.0;
+  double x[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = (i == row) ? 1.0 : 0.0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    x[r] *= rl[r];
+#pragma unroll
+    for (int i = r + 1; i < 16; ++i) x[i] -= __shfl_sync(FULL, a[r], i) * x[r];
+  }
+  if (lane < 16)
+#pragma unroll
+    for (int r = 0; r < 16; ++r) s.Di[o + r][o + lane] = x[r];
+}
+
+// out(r, c, sum_t a(r, t) b(t, c)) for an N x N product on the whole CTA
+// (128 threads); each thread keeps one row of a in registers. All reads
+// finish (barrier) before any write, so in-place updates are safe.
+template <int N, class FA, class FB, class FO>
+__device__ __forceinline__ void pc_mm(FA fa, FB fb, FO fo) {
+  constexpr int OUT = N * N / 128, PER_ROW = N / OUT;
+  const int r = threadIdx.x / PER_ROW, cb = (threadIdx.x % PER_ROW) * OUT;
+  double row[N], acc[OUT];
+#pragma unroll
+  for (int t = 0; t < N; ++t) row[t] = fa(r, t);
+#pragma unroll
+  for (int u = 0; u < OUT; ++u) {
+    double v = 0.0;
+#pragma unroll
+    for (int t = 0; t < N; ++t) v += row[t] * fb(t, cb + u);
+    acc[u] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < OUT; ++u) fo(r, cb + u, acc[u]);
+  __syncthreads();
+}
+
+// Cholesky + inverse of the H x H block at (o, o) of s.T into s.T / s.Di by
+// 2 x 2 recursion: L11, inv11 | L21 = A21 inv11^T | A22 -= L21 L21^T |
+// L22, inv22 | inv21 = -inv22 (L21 inv11).
+template <int H>
+__device__ void pc_chol_inv(PcSmallSmem& s, int o, int w) {
+  if constexpr (H == 16) {
+    if ((threadIdx.x >> 5) == 0) pc_base16(s, o, w, threadIdx.x & 31);
+    __syncthreads();
+  } else {
+    constexpr int N = H / 2;
+    pc_chol_inv<N>(s, o, min(w, N));
+    if (s.bad) return;
+    pc_mm<N>([&](int r, int t) { return s.T[o + N + r][o + t]; },
+             [&](int t, int c) { return s.Di[o + c][o + t]; },
+             [&](int r, int c, double v) { s.T[o + N + r][o + c] = v; });
+    pc_mm<N>([&](int r, int t) { return s.T[o + N + r][o + t]; },
+             [&](int t, int c) { return s.T[o + N + c][o + t]; },
+             [&](int r, int c, double v) {
+               if (c <= r) s.T[o + N + r][o + N + c] -= v;
+             });
+    pc_chol_inv<N>(s, o + N, max(0, w - N));
+    if (s.bad) return;
+    // M = L21 inv11 (after the recursion above: s.M is shared scratch).
+    pc_mm<N>([&](int r, int t) { return s.T[o + N + r][o + t]; },
+             [&](int t, int c) { return s.Di[o + t][o + c]; },
+             [&](int r, int c, double v) { s.M[r][c] = v; });
+    pc_mm<N>([&](int r, int t) { return s.Di[o + N + r][o + N + t]; },
+             [&](int t, int c) { return s.M[t][c]; },
+             [&](int r, int c, double v) {
+               s.Di[o + N + r][o + c] = -v;
+               s.Di[o + r][o + N + c] = 0.0;
+             });
+  }
 }
 
 // Factor + invert the 64 x 64 diagonal block at (j0, j0) (w valid rows).
+// Returns false on a bad pivot (not > 0, or NaN) among the first w columns.
 __device__ bool pc_small(double* A, int b, int j0, int w, double* dinv_out, PcSmallSmem& s) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   for (int e = tid; e < 64 * 64; e += blockDim.x) {
     const int r = e >> 6, c = e & 63;
     s.T[r][c] = (r < w && c <= r) ? A[(int64_t)(j0 + r) * b + j0 + c] : (r == c ? 1.0 : 0.0);
   }
   if (tid == 0) s.bad = 0;
   __syncthreads();
-  if (warp == 0 && !pc_factor32(s, 0, min(w, 32), lane)) s.bad = 1;
+  pc_chol_inv<64>(s, 0, w);
   __syncthreads();
   if (s.bad) return false;
-  // L21 = A21 * Di11^T (registers first: in place)
-  {
-    const int r = tid >> 2, cb = (tid & 3) * 8;
-    double x[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      double acc = 0.0;
-      for (int t = 0; t <= cb + u; ++t) acc += s.T[32 + r][t] * s.Di[cb + u][t];
-      x[u] = acc;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s.T[32 + r][cb + u] = x[u];
-  }
-  __syncthreads();
-  // A22 -= L21 L21^T (lower)
-  for (int e = tid; e < 32 * 32; e += blockDim.x) {
-    const int r = e >> 5, c = e & 31;
-    if (c > r) continue;
-    double acc = 0.0;
-    for (int t = 0; t < 32; ++t) acc += s.T[32 + r][t] * s.T[32 + c][t];
-    s.T[32 + r][32 + c] -= acc;
-  }
-  __syncthreads();
-  if (warp == 0 && !pc_factor32(s, 32, max(0, w - 32), lane)) s.bad = 1;
-  __syncthreads();
-  if (s.bad) return false;
-  // Di21 = -Di22 (L21 Di11):  M = L21 Di11, then Di21 = -Di22 M
-  for (int e = tid; e < 32 * 32; e += blockDim.x) {
-    const int r = e >> 5, c = e & 31;
-    double acc = 0.0;
-    for (int t = c; t < 32; ++t) acc += s.T[32 + r][t] * s.Di[t][c];
-    s.M[r][c] = acc;
-  }
-  __syncthreads();
-  for (int e = tid; e < 32 * 32; e += blockDim.x) {
-    const int r = e >> 5, c = e & 31;
-    double acc = 0.0;
-    for (int t = 0; t <= r; ++t) acc += s.Di[32 + r][32 + t] * s.M[t][c];
-    s.Di[32 + r][c] = -acc;
-    s.Di[r][32 + c] = 0.0;
-  }
-  __syncthreads();
   for (int e = tid; e < 64 * 64; e += blockDim.x) {
-    const int r = e >> 6, c = e & 63;
-    if (r < w && c <= r) A[(int64_t)(j0 + r) * b + j0 + c] = s.T[r][c];
-    dinv_out[e] = s.Di[r][c];
+    const int rr = e >> 6, c = e & 63;
+    if (rr < w && c <= rr) A[(int64_t)(j0 + rr) * b + j0 + c] = s.T[rr][c];
+    dinv_out[e] = s.Di[rr][c];
   }
   return true;
 }
+
+#ifdef SPHEMU_POTRF_TRACE
+__device__ unsigned long long* g_potrf_trace;
+#define PTRACE(slot)                                                                         \
+  do {                                                                                       \
+    if (threadIdx.x == 0 && g_potrf_trace) {                                                 \
+      unsigned long long t__;                                                                \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t__));                                \
+      g_potrf_trace[blockIdx.x * 64 + (slot)] = t__;                                         \
+    }                                                                                        \
+  } while (0)
+#else
+#define PTRACE(slot) \
+  do {               \
+  } while (0)
+#endif
 
 __device__ __forceinline__ double* blk(double* A, int b, int r, int c) {
   return A + (int64_t)r * PC_BLK * b + (int64_t)c * PC_BLK;
@@ -143,9 +189,12 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
     const int r = (int)(e / b), c = (int)(e % b);
     Linv[e] = (r == c && r < bk) ? 1.0 : 0.0;
   }
+  PTRACE(0);
   if (cta == 0 && !pc_small(A, b, 0, rows_of(0), dinv_all, ss) && threadIdx.x == 0) atomicCAS(fail, -1, k);
+  PTRACE(1);
   __threadfence();
   grid.sync();
+  PTRACE(2);
   for (int s = 0; s < nblk; ++s) {
     if (*(volatile int*)fail >= 0) return;
     const int w = rows_of(s);
@@ -176,8 +225,10 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
       }
       __syncthreads();
     }
+    PTRACE(3 + 4 * s);
     __threadfence();
     grid.sync();
+    PTRACE(4 + 4 * s);
     // ---- phase B ----
     if (cta == 0) {
       if (s + 1 < nblk) {
@@ -227,8 +278,10 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
         __syncthreads();
       }
     }
+    PTRACE(5 + 4 * s);
     __threadfence();
     grid.sync();
+    PTRACE(6 + 4 * s);
   }
   // Strict upper part to zero (potrf_tile's final loop).
   for (int64_t e = (int64_t)cta * blockDim.x + threadIdx.x; e < (int64_t)b * b; e += (int64_t)G * blockDim.x) {

@@ -295,6 +295,38 @@ __device__ void fft_dif_rings(double2* x, int R, const FftPlan& P) {
         base[span] = cmul(y1, w1);
         base[2 * span] = cmul(y2, w2);
         base[3 * span] = cmul(y3, w3);
+      } else if (p == 3) {
+        // W3 = exp(-+2 pi i / 3): y1,2 = a0 - (a1+a2)/2 -+ i s (sqrt3/2)(a1-a2)
+        const double2 a0 = base[0], a1 = base[span], a2 = base[2 * span];
+        const double2 t = make_double2(a1.x + a2.x, a1.y + a2.y), d = make_double2(a1.x - a2.x, a1.y - a2.y);
+        const double h = 0.86602540378443864676 * (SIGN < 0 ? 1.0 : -1.0);
+        const double2 m = make_double2(a0.x - 0.5 * t.x, a0.y - 0.5 * t.y);
+        const double2 rd = make_double2(h * d.y, -h * d.x);  // -i s (sqrt3/2) d
+        double2 w1 = P.tw[(j * tstep) % n], w2 = P.tw[(2 * j * tstep) % n];
+        if (SIGN > 0) { w1.y = -w1.y; w2.y = -w2.y; }
+        base[0] = make_double2(a0.x + t.x, a0.y + t.y);
+        base[span] = cmul(make_double2(m.x + rd.x, m.y + rd.y), w1);
+        base[2 * span] = cmul(make_double2(m.x - rd.x, m.y - rd.y), w2);
+      } else if (p == 5) {
+        const double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;
+        const double s1 = 0.95105651629515357212 * (SIGN < 0 ? 1.0 : -1.0);
+        const double s2 = 0.58778525229247312917 * (SIGN < 0 ? 1.0 : -1.0);
+        const double2 a0 = base[0], a1 = base[span], a2 = base[2 * span], a3 = base[3 * span], a4 = base[4 * span];
+        const double2 b1 = make_double2(a1.x + a4.x, a1.y + a4.y), b2 = make_double2(a2.x + a3.x, a2.y + a3.y);
+        const double2 d1 = make_double2(a1.x - a4.x, a1.y - a4.y), d2 = make_double2(a2.x - a3.x, a2.y - a3.y);
+        const double2 r1 = make_double2(a0.x + c1 * b1.x + c2 * b2.x, a0.y + c1 * b1.y + c2 * b2.y);
+        const double2 r2 = make_double2(a0.x + c2 * b1.x + c1 * b2.x, a0.y + c2 * b1.y + c1 * b2.y);
+        const double2 e1 = make_double2(s1 * d1.x + s2 * d2.x, s1 * d1.y + s2 * d2.y);
+        const double2 e2 = make_double2(s2 * d1.x - s1 * d2.x, s2 * d1.y - s1 * d2.y);
+        // -i e = (e.y, -e.x)
+        double2 w1 = P.tw[(j * tstep) % n], w2 = P.tw[(2 * j * tstep) % n], w3 = P.tw[(3 * j * tstep) % n],
+                w4 = P.tw[(4 * j * tstep) % n];
+        if (SIGN > 0) { w1.y = -w1.y; w2.y = -w2.y; w3.y = -w3.y; w4.y = -w4.y; }
+        base[0] = make_double2(a0.x + b1.x + b2.x, a0.y + b1.y + b2.y);
+        base[span] = cmul(make_double2(r1.x + e1.y, r1.y - e1.x), w1);
+        base[4 * span] = cmul(make_double2(r1.x - e1.y, r1.y + e1.x), w4);
+        base[2 * span] = cmul(make_double2(r2.x + e2.y, r2.y - e2.x), w2);
+        base[3 * span] = cmul(make_double2(r2.x - e2.y, r2.y + e2.x), w3);
       } else {
         // generic radix p (O(p^2)); p <= 64 buffered in registers/local memory
         double2 in[64];

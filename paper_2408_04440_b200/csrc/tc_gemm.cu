@@ -454,7 +454,7 @@ namespace {
 
 template <int BN, int OPK, int MODE>
 void launch_tc(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi,
-               const CUtensorMap& b_lo, TcArgs args, cudaStream_t s) {
+               const CUtensorMap& b_lo, TcArgs args, cudaStream_t s, int max_ctas = 0) {
   using Lay = TcLayout<BN, OPK>;
   auto kern = k_tc_gemm<BN, OPK, MODE>;
   static bool attr = false;
@@ -462,7 +462,8 @@ void launch_tc(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorM
     SPH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::kSmem));
     attr = true;
   }
-  const int grid = static_cast<int>(std::min<int64_t>(args.items, num_sms()));
+  const int cap = max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms();
+  const int grid = static_cast<int>(std::min<int64_t>(args.items, cap));
   kern<<<grid, 256, Lay::kSmem, s>>>(a_hi, a_lo, b_hi, b_lo, args);
   SPH_LAUNCH_CHECK();
 }
@@ -513,7 +514,8 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
 }
 
 void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* list, int64_t cnt,
-               const double* p64, PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s) {
+               const double* p64, PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s,
+               int max_ctas) {
   (void)p64;
   TcArgs a{};
   a.ts = ts;
@@ -527,21 +529,21 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
     a.sub_n = ts.b / 128;
     a.sub_per = (ts.b / TC_BM) * a.sub_n;
     a.items = cnt * a.sub_per;
-    launch_tc<128, OP_TF32X3, MODE_UPDATE>(pf.m_phi_a, pf.m_plo_a, pf.m_phi_b, pf.m_plo_b, a, s);
+    launch_tc<128, OP_TF32X3, MODE_UPDATE>(pf.m_phi_a, pf.m_plo_a, pf.m_phi_b, pf.m_plo_b, a, s, max_ctas);
   } else {
     a.sub_n = ts.b / pf.bn;
     a.sub_per = (ts.b / TC_BM) * a.sub_n;
     a.items = cnt * a.sub_per;
     if (pf.bn == 256) {
       if (hp_format == SPHEMU_HP_BF16)
-        launch_tc<256, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s);
+        launch_tc<256, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s, max_ctas);
       else
-        launch_tc<256, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s);
+        launch_tc<256, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s, max_ctas);
     } else {
       if (hp_format == SPHEMU_HP_BF16)
-        launch_tc<128, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s);
+        launch_tc<128, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s, max_ctas);
       else
-        launch_tc<128, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s);
+        launch_tc<128, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s, max_ctas);
     }
   }
 }

@@ -165,3 +165,26 @@ def test_full_size_c2_probe(sph):
     rc = sph._sphemu.lib().sphemu_gpu_chol_residual_probe_spd(h.h, 1, 3, C.byref(out))
     assert rc == 0 and out.value < 5e-6, out.value
     assert st.half_saturations == 0
+
+
+@pytest.mark.parametrize("compute", MODES)
+@pytest.mark.parametrize("variant", ["dp", "dpsp", "dpsphp"])
+def test_lookahead_is_bitwise_identical(sph, O, compute, variant):
+    """The two-stream lookahead schedule reorders operations across tiles only;
+    each tile sees its k-ordered updates exactly as without lookahead."""
+    a = O.make_spd(2300, 4)
+    f0, j0 = sph.tiled_cholesky(a, variant, tile_size=256, compute=compute, lookahead=0)
+    f1, j1 = sph.tiled_cholesky(a, variant, tile_size=256, compute=compute, lookahead=1)
+    assert np.array_equal(f0, f1)
+    assert json.loads(j0)["conversions"] == json.loads(j1)["conversions"]
+
+
+def test_repeat_factorizations_are_deterministic(sph):
+    h = sph.Cholesky(6000, "dpsphp", tile_size=512)
+    outs = []
+    for _ in range(2):
+        h.generate_spd(3)
+        h.factor()
+        h.wait()
+        outs.append(h.factor_dense())
+    assert np.array_equal(outs[0], outs[1])
