@@ -383,9 +383,21 @@ struct Chol {
         tc_update(store(), k, cls, cfg.hp_format, lst, cnt, p64_[set].get(), panel_[set], fail.get(), sat.get(), s,
                   max_ctas);
       } else {
-        const int per = (b / DG_BM) * (b / DG_BN);
-        k_update_fp64<<<static_cast<unsigned>(cnt * per), DG_THREADS, 0, s>>>(store(), k, lst, p64_[set].get(),
-                                                                               fail.get(), sat.get());
+        if (b % D2_BM == 0) {
+          static bool attr = false;
+          if (!attr) {
+            SPH_CUDA(cudaFuncSetAttribute(k_update_fp64_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sizeof(D2Smem)));
+            attr = true;
+          }
+          const int per = (b / D2_BM) * (b / D2_BN);
+          k_update_fp64_v2<<<static_cast<unsigned>(cnt * per), D2_THREADS, sizeof(D2Smem), s>>>(
+              store(), k, lst, p64_[set].get(), fail.get(), sat.get());
+        } else {
+          const int per = (b / DG_BM) * (b / DG_BN);
+          k_update_fp64<<<static_cast<unsigned>(cnt * per), DG_THREADS, 0, s>>>(store(), k, lst, p64_[set].get(),
+                                                                                 fail.get(), sat.get());
+        }
         SPH_LAUNCH_CHECK();
       }
       prof_end(pu, s);

@@ -7,6 +7,7 @@
 
 #include "common.cuh"
 #include "dgemm.cuh"
+#include "dgemm2.cuh"
 
 namespace sphemu_gpu {
 
@@ -384,6 +385,51 @@ static __global__ void __launch_bounds__(DG_THREADS) k_update_fp64(TileStore ts,
     const double cur = load_elem(tp, p, e);
     store_elem(tp, p, e, cur - v, local);
   });
+  flush_sat(local, sat);
+}
+
+// Same update on 128 x 64 sub-tiles with the cp.async DGEMM (dgemm2.cuh);
+// needs b % 128 == 0. Sub-tiles strictly above the diagonal of SYRK tiles are
+// skipped.
+static __global__ void __launch_bounds__(D2_THREADS) k_update_fp64_v2(TileStore ts, int k,
+                                                                      const int2* __restrict__ list,
+                                                                      const double* __restrict__ P64,
+                                                                      const int* fail, unsigned* sat) {
+  extern __shared__ __align__(16) uint8_t d2_smem[];
+  D2Smem& sm = *reinterpret_cast<D2Smem*>(d2_smem);
+  if (*(volatile const int*)fail >= 0) return;
+  const int b = ts.b;
+  const int sm_n = b / D2_BN, per = (b / D2_BM) * sm_n;
+  const int2 ij = list[blockIdx.x / per];
+  const int sub = blockIdx.x % per;
+  const int r0 = (sub / sm_n) * D2_BM, c0 = (sub % sm_n) * D2_BN;
+  const int i = ij.x, j = ij.y;
+  if (i == j && c0 >= r0 + D2_BM) return;
+  const double* Pi = P64 + (int64_t)(i - k - 1) * b * b;
+  const double* Pj = P64 + (int64_t)(j - k - 1) * b * b;
+  D2Op A{Pi + (int64_t)r0 * b, b, D2_BM, b};
+  D2Op B{Pj + (int64_t)c0 * b, b, D2_BN, b};
+  double acc[4][4][2];
+  dgemm2_128x64<D2B::kNT, true>(A, B, b, sm, acc);
+  void* tp = ts.tile(i, j);
+  const int p = ts.tprec(i, j);
+  unsigned local = 0;
+  if (p == kDP) {
+    double* C = static_cast<double*>(tp);
+    d2_for_each(acc, [&](int r, int c, double v0, double v1) {
+      double2* q = reinterpret_cast<double2*>(C + (int64_t)(r0 + r) * b + c0 + c);
+      double2 cur = *q;
+      cur.x -= v0;
+      cur.y -= v1;
+      *q = cur;
+    });
+  } else {
+    d2_for_each(acc, [&](int r, int c, double v0, double v1) {
+      const int64_t e = (int64_t)(r0 + r) * b + c0 + c;
+      store_elem(tp, p, e, load_elem(tp, p, e) - v0, local);
+      store_elem(tp, p, e + 1, load_elem(tp, p, e + 1) - v1, local);
+    });
+  }
   flush_sat(local, sat);
 }
 

@@ -22,26 +22,30 @@
 
 #include "common.cuh"
 #include "dgemm.cuh"
+#include "dgemm2.cuh"
 
 namespace sphemu_gpu {
 
 struct Sht;  // sht.cu
 void sht_inverse_device(void* plan, const double* coeffs, int64_t n, double* fields, cudaStream_t* s_out);
 
-// Xi (S x d) = H (S x d) * V^T, V lower triangular dense (row-major d x d).
-__global__ void __launch_bounds__(DG_THREADS) k_emul_xi(const double* __restrict__ H, const double* __restrict__ V,
+// Xi (S x d) = H (S x d) * V^T, V lower triangular dense (row-major d x d):
+// output columns c0..c0+63 need V rows whose nonzeros stop at column c0+63.
+__global__ void __launch_bounds__(D2_THREADS) k_emul_xi(const double* __restrict__ H, const double* __restrict__ V,
                                                          int64_t S, int d, double* __restrict__ Xi) {
-  __shared__ DgSmem sm;
-  const int64_t r0 = (int64_t)blockIdx.y * DG_BM;
-  const int c0 = blockIdx.x * DG_BN;
-  // Output columns c0..c0+63 use V rows c0.. whose nonzeros stop at column c0+63.
-  const int kmax = min(d, c0 + DG_BN);
-  RowMajorK A{H + r0 * d, d, (int)(S - r0 < DG_BM ? S - r0 : DG_BM), kmax};
-  RowMajorK B{V + (int64_t)c0 * d, d, min(DG_BN, d - c0), kmax};
+  extern __shared__ __align__(16) uint8_t d2_smem[];
+  D2Smem& sm = *reinterpret_cast<D2Smem*>(d2_smem);
+  const int64_t r0 = (int64_t)blockIdx.y * D2_BM;
+  const int c0 = blockIdx.x * D2_BN;
+  const int kmax = min(d, c0 + D2_BN);
+  D2Op A{H + r0 * d, d, (int)(S - r0 < D2_BM ? S - r0 : D2_BM), kmax};
+  D2Op B{V + (int64_t)c0 * d, d, min(D2_BN, d - c0), kmax};
   double acc[4][4][2];
-  dgemm_64x64(A, B, kmax, sm, acc);
-  dg_for_each(acc, [&](int r, int c, double v) {
-    if (r0 + r < S && c0 + c < d) Xi[(r0 + r) * d + c0 + c] = v;
+  dgemm2_128x64<D2B::kNT, false>(A, B, kmax, sm, acc);
+  d2_for_each(acc, [&](int r, int c, double v0, double v1) {
+    if (r0 + r >= S) return;
+    if (c0 + c < d) Xi[(r0 + r) * d + c0 + c] = v0;
+    if (c0 + c + 1 < d) Xi[(r0 + r) * d + c0 + c + 1] = v1;
   });
 }
 
@@ -175,8 +179,9 @@ void emulate(void* plan, int n_theta, int n_phi, int L, const double* v, int d, 
     k_philox_normals<<<4 * num_sms(), 256, 0, s>>>(seed, 2, ytot, dEps.get());
     SPH_LAUNCH_CHECK();
   }
-  k_emul_xi<<<dim3(ceil_div(d, DG_BN), (unsigned)ceil_div(S, DG_BM)), DG_THREADS, 0, s>>>(dH.get(), dV.get(), S, d,
-                                                                                           dXi.get());
+  SPH_CUDA(cudaFuncSetAttribute(k_emul_xi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(D2Smem)));
+  k_emul_xi<<<dim3(ceil_div(d, D2_BN), (unsigned)ceil_div(S, D2_BM)), D2_THREADS, sizeof(D2Smem), s>>>(
+      dH.get(), dV.get(), S, d, dXi.get());
   SPH_LAUNCH_CHECK();
   k_emul_ar<<<dim3(ceil_div(d, 128), r_len), 128, 0, s>>>(dXi.get(), dPhi.get(), order, d, burn, t_out, r_len,
                                                            dDraws.get());

@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "dgemm.cuh"
+#include "dgemm2.cuh"
 
 namespace sphemu_gpu {
 
@@ -420,28 +421,33 @@ __global__ void k_ring_fft_inv(const double* __restrict__ G, int n_theta, int L,
 // ===========================================================================
 // Forward: F_m (L-m x 2T) = Psi_m (L-m x n_theta) * G_m^T; scattered into the
 // packed layout (sht.hpp:38-45): m = 0 keeps the real part only.
-__global__ void __launch_bounds__(DG_THREADS) k_legendre_fwd(const double* __restrict__ psi,
+__global__ void __launch_bounds__(D2_THREADS) k_legendre_fwd(const double* __restrict__ psi,
                                                               const int64_t* psi_off, const double* __restrict__ G,
                                                               int L, int n_theta, int T, double* coeffs) {
-  __shared__ DgSmem sm;
+  extern __shared__ __align__(16) uint8_t d2_smem[];
+  D2Smem& sm = *reinterpret_cast<D2Smem*>(d2_smem);
   const int m = blockIdx.z;
   const int rows = L - m;
-  const int r0 = blockIdx.y * DG_BM, c0 = blockIdx.x * DG_BN;
+  const int r0 = blockIdx.y * D2_BM, c0 = blockIdx.x * D2_BN;
   if (r0 >= rows) return;
   const int ncols = 2 * T;
-  RowMajorK A{psi + psi_off[m] + (int64_t)r0 * n_theta, n_theta, min(DG_BM, rows - r0), n_theta};
-  RowMajorK B{G + (int64_t)m * ncols * n_theta + (int64_t)c0 * n_theta, n_theta, min(DG_BN, ncols - c0), n_theta};
+  D2Op A{psi + psi_off[m] + (int64_t)r0 * n_theta, n_theta, min(D2_BM, rows - r0), n_theta};
+  D2Op B{G + (int64_t)m * ncols * n_theta + (int64_t)c0 * n_theta, n_theta, min(D2_BN, ncols - c0), n_theta};
   double acc[4][4][2];
-  dgemm_64x64(A, B, n_theta, sm, acc);
+  dgemm2_128x64<D2B::kNT, false>(A, B, n_theta, sm, acc);
   const int64_t nc = (int64_t)L * L;
-  dg_for_each(acc, [&](int r, int c, double v) {
-    const int l = m + r0 + r, s = c0 + c;
+  d2_for_each(acc, [&](int r, int c, double v0, double v1) {
+    const int l = m + r0 + r, s = c0 + c;  // s even: (re, im) of snapshot s/2
     if (r0 + r >= rows || s >= ncols) return;
-    const int t = s >> 1, part = s & 1;
+    const int t = s >> 1;
     if (m == 0) {
-      if (part == 0) coeffs[(int64_t)t * nc + (int64_t)l * l] = v;
+      coeffs[(int64_t)t * nc + (int64_t)l * l] = v0;
     } else {
-      coeffs[(int64_t)t * nc + (int64_t)l * l + 2 * m - 1 + part] = v;
+      double2* q = reinterpret_cast<double2*>(coeffs + (int64_t)t * nc + (int64_t)l * l + 2 * m - 1);
+      // l*l + 2m - 1 is even when l*l is odd; use scalar stores to stay aligned-agnostic
+      double* qq = reinterpret_cast<double*>(q);
+      qq[0] = v0;
+      qq[1] = v1;
     }
   });
 }
@@ -464,22 +470,25 @@ __global__ void k_gather_z(const double* __restrict__ coeffs, int L, int T, cons
 }
 
 // Inverse: G_m^T (2T x n_theta) = Z_m (2T x L-m) * Y_m^T, G[m][s][i].
-__global__ void __launch_bounds__(DG_THREADS) k_legendre_inv(const double* __restrict__ y, const int64_t* y_off,
+__global__ void __launch_bounds__(D2_THREADS) k_legendre_inv(const double* __restrict__ y, const int64_t* y_off,
                                                               const double* __restrict__ Z, const int64_t* z_off,
                                                               int L, int n_theta, int T, double* G) {
-  __shared__ DgSmem sm;
+  extern __shared__ __align__(16) uint8_t d2_smem[];
+  D2Smem& sm = *reinterpret_cast<D2Smem*>(d2_smem);
   const int m = blockIdx.z;
   const int cols = L - m;
   const int ncols = 2 * T;
-  const int r0 = blockIdx.y * DG_BM, c0 = blockIdx.x * DG_BN;
+  const int r0 = blockIdx.y * D2_BM, c0 = blockIdx.x * D2_BN;
   if (r0 >= ncols) return;
-  RowMajorK A{Z + z_off[m] * ncols + (int64_t)r0 * cols, cols, min(DG_BM, ncols - r0), cols};
-  RowMajorK B{y + y_off[m] + (int64_t)c0 * cols, cols, min(DG_BN, n_theta - c0), cols};
+  D2Op A{Z + z_off[m] * ncols + (int64_t)r0 * cols, cols, min(D2_BM, ncols - r0), cols};
+  D2Op B{y + y_off[m] + (int64_t)c0 * cols, cols, min(D2_BN, n_theta - c0), cols};
   double acc[4][4][2];
-  dgemm_64x64(A, B, cols, sm, acc);
+  dgemm2_128x64<D2B::kNT, false>(A, B, cols, sm, acc);
   double* out = G + (int64_t)m * ncols * n_theta;
-  dg_for_each(acc, [&](int r, int c, double v) {
-    if (r0 + r < ncols && c0 + c < n_theta) out[(int64_t)(r0 + r) * n_theta + c0 + c] = v;
+  d2_for_each(acc, [&](int r, int c, double v0, double v1) {
+    if (r0 + r >= ncols) return;
+    if (c0 + c < n_theta) out[(int64_t)(r0 + r) * n_theta + c0 + c] = v0;
+    if (c0 + c + 1 < n_theta) out[(int64_t)(r0 + r) * n_theta + c0 + c + 1] = v1;
   });
 }
 
@@ -594,6 +603,8 @@ struct Sht {
       SPH_CUDA(cudaFuncSetAttribute(k_ring_fft_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
       SPH_CUDA(cudaFuncSetAttribute(k_ring_fft_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
     }
+    SPH_CUDA(cudaFuncSetAttribute(k_legendre_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(D2Smem)));
+    SPH_CUDA(cudaFuncSetAttribute(k_legendre_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(D2Smem)));
     // Snapshot chunk: bound the G staging to ~1 GiB.
     const double per = 16.0 * L * n_theta + 16.0 * L * L;
     chunk = (int)std::max(1.0, std::min(1024.0, (1024.0 * 1024 * 1024) / per));
@@ -624,7 +635,7 @@ struct Sht {
       k_ring_fft_fwd<<<dim3(ceil_div(n_theta, rings_per_cta), T), 256, fft_smem, stream>>>(
           fields + t0 * pts, n_theta, L, rings_per_cta, fplan, T, G.get());
       SPH_LAUNCH_CHECK();
-      k_legendre_fwd<<<dim3(ceil_div(2 * T, DG_BN), ceil_div(L, DG_BM), L), DG_THREADS, 0, stream>>>(
+      k_legendre_fwd<<<dim3(ceil_div(2 * T, D2_BN), ceil_div(L, D2_BM), L), D2_THREADS, sizeof(D2Smem), stream>>>(
           psi.get(), d_psi_off.get(), G.get(), L, n_theta, T, coeffs + t0 * nc);
       SPH_LAUNCH_CHECK();
     }
@@ -637,7 +648,7 @@ struct Sht {
       ensure(T);
       k_gather_z<<<dim3(2 * T, L), 128, 0, stream>>>(coeffs + t0 * nc, L, T, d_z_off.get(), Z.get());
       SPH_LAUNCH_CHECK();
-      k_legendre_inv<<<dim3(ceil_div(n_theta, DG_BN), ceil_div(2 * T, DG_BM), L), DG_THREADS, 0, stream>>>(
+      k_legendre_inv<<<dim3(ceil_div(n_theta, D2_BN), ceil_div(2 * T, D2_BM), L), D2_THREADS, sizeof(D2Smem), stream>>>(
           y.get(), d_y_off.get(), Z.get(), d_z_off.get(), L, n_theta, T, G.get());
       SPH_LAUNCH_CHECK();
       k_ring_fft_inv<<<dim3(ceil_div(n_theta, rings_per_cta), T), 256, fft_smem, stream>>>(
