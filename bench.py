@@ -198,7 +198,7 @@ def run_ours(args, world, rank, local):
     n, b = args.n, args.tile
     # Dense FP64 input resident in HBM (the tiled_cholesky_dense input form).
     a_dev = torch.empty((n, n), dtype=torch.float64, device="cuda")
-    h = sph.Cholesky(n, VARIANT, tile_size=b, lookahead=args.lookahead)
+    h = sph.Cholesky(n, VARIANT, tile_size=b, lookahead=args.lookahead, sp_compute=args.sp_compute)
     h.generate_spd(1)
     h.store(a_dev.data_ptr())          # lower triangle
     a_dev += torch.tril(a_dev, -1).T   # symmetric dense A, bitwise the reference's values
@@ -236,14 +236,23 @@ def run_ours(args, world, rank, local):
     peaks = load_peaks()
     own = peaks.get("own", {})
     p_dp = own.get("fp64_dgemm_tflops", 35.5)
-    p_sp = own.get("tf32x3_effective_tflops", 244.7)
+    # SP class runs on the pipe of the chosen split: fp16 hi+lo (3 kind::f16
+    # MMAs) -> cuBLAS FP16 / 3; 3xTF32 -> cuBLAS TF32 / 3.
+    if args.sp_compute == "fp16x3":
+        p_sp = own.get("fp16_tflops", 1546.6) / 3
+        sp_src = "cuBLAS FP16 GEMM measured on this pool / 3 (3 kind::f16 MMAs per product; profiles/peaks_r01.json)"
+        sp_kernel = "k_tc_gemm<128, F16x3, UPDATE> (SP-class trailing update, row-scaled fp16 hi+lo)"
+    else:
+        p_sp = own.get("tf32x3_effective_tflops", 244.7)
+        sp_src = "cuBLAS TF32 GEMM measured on this pool / 3 (profiles/peaks_r01.json)"
+        sp_kernel = "k_tc_gemm<128, TF32x3, UPDATE> (SP-class trailing update)"
     p_hp = peaks.get("bf16_tflops", 1692.6)
     sp_update_flops = h.class_update_flops()["sp"]
     t_sp = phases["update_sp"]["ms"] / args.steps
-    dom = {"kernel": "k_tc_gemm<128, TF32x3, UPDATE> (SP-class trailing update)",
+    dom = {"kernel": sp_kernel,
            "bound": "tensor", "achieved": sp_update_flops / (t_sp * 1e-3) / 1e12 if t_sp > 0 else None,
            "peak": p_sp, "unit": "TFLOP/s",
-           "peak_source": "cuBLAS TF32 GEMM measured on this pool / 3 (profiles/peaks_r01.json)",
+           "peak_source": sp_src,
            "traffic": None}
     dom["frac"] = dom["achieved"] / p_sp if dom["achieved"] else None
     t_roof = fl["dp"] / (p_dp * 1e12) + fl["sp"] / (p_sp * 1e12) + fl["hp"] / (p_hp * 1e12)
@@ -256,7 +265,7 @@ def run_ours(args, world, rank, local):
         a_host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
         a_host.copy_(a_dev)
         f_host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-        cfg = sph._sphemu.make_config(VARIANT, b, lookahead=args.lookahead)
+        cfg = sph._sphemu.make_config(VARIANT, b, lookahead=args.lookahead, sp_compute=args.sp_compute)
         stats = sph._sphemu.CholStats()
         failed = C.c_int(-1)
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
@@ -343,6 +352,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--lookahead", type=int, default=1)
+    ap.add_argument("--sp-compute", default="fp16x3", choices=["fp16x3", "tf32x3"])
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":

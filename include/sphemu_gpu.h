@@ -59,6 +59,9 @@ int64_t sphemu_gpu_launch_count(void);
 #define SPHEMU_COMPUTE_TENSOR 0 /* per-class tensor cores: tcgen05 fp16/bf16, 3xTF32, FP64 DMMA */
 #define SPHEMU_COMPUTE_FP64 1   /* every tile kernel in FP64 (mpchol.cpp:283-316 semantics) */
 
+#define SPHEMU_SP_F16X3 0  /* SP-class updates: fp16 hi+lo split of row-scaled operands, kind::f16 */
+#define SPHEMU_SP_TF32X3 1 /* SP-class updates: 3xTF32 on kind::tf32 */
+
 /* MpCholConfig (mpchol.hpp:18-28) plus appended GPU fields whose zero values
  * keep reference behaviour. */
 typedef struct {
@@ -70,6 +73,7 @@ typedef struct {
   int hp_format;      /* SPHEMU_HP_* */
   int compute;        /* SPHEMU_COMPUTE_* */
   int lookahead;      /* 0 = off, 1 = panel k+1 on a priority stream */
+  int sp_compute;     /* SPHEMU_SP_* (tensor mode only) */
 } sphemu_chol_config;
 
 /* FactorizationStats (mpchol.hpp:104-120) + GPU timing. */
@@ -127,6 +131,11 @@ int sphemu_gpu_chol_flops(sphemu_chol_t h, double* f_dp, double* f_sp, double* f
  * classes, 5 tile load. ms/counts have 6 entries. */
 int sphemu_gpu_chol_set_profiling(sphemu_chol_t h, int on);
 int sphemu_gpu_chol_phase_times(sphemu_chol_t h, double* ms, int64_t* counts, int reset);
+/* Timeline of the last profiled factorization: one span per phase launch
+ * (phase as above; stream 0 = main/bulk, 1 = high-priority chain), times in
+ * ms from the factorization's start. Writes min(count, cap) entries. */
+int sphemu_gpu_chol_timeline(sphemu_chol_t h, int* phase, int* stream, double* t0, double* t1, int cap,
+                             int* count);
 /* Trailing-update flops by output class (2 b_i b_j b_k per GEMM, b_i^2 b_k per SYRK). */
 int sphemu_gpu_chol_update_flops(sphemu_chol_t h, double* f_dp, double* f_sp, double* f_hp);
 /* Device stream the handle enqueues on (cudaStream_t as void*). */

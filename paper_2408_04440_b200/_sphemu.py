@@ -38,7 +38,7 @@ class NotPositiveDefiniteError(RuntimeError):
 class CholConfig(C.Structure):
     _fields_ = [("variant", C.c_int), ("tile_size", C.c_int), ("band_width_dp", C.c_int),
                 ("sp_fraction", C.c_double), ("workers", C.c_int), ("hp_format", C.c_int),
-                ("compute", C.c_int), ("lookahead", C.c_int)]
+                ("compute", C.c_int), ("lookahead", C.c_int), ("sp_compute", C.c_int)]
 
 
 class CholStats(C.Structure):
@@ -111,6 +111,7 @@ def lib():
         L.sphemu_gpu_chol_set_profiling.argtypes = [vp, C.c_int]
         L.sphemu_gpu_chol_phase_times.argtypes = [vp, vp, vp, C.c_int]
         L.sphemu_gpu_chol_update_flops.argtypes = [vp, dp, dp, dp]
+        L.sphemu_gpu_chol_timeline.argtypes = [vp, vp, vp, vp, vp, C.c_int, C.POINTER(C.c_int)]
         L.sphemu_gpu_chol_residual_probe_spd.argtypes = [vp, C.c_uint64, C.c_int, dp]
         L.sphemu_gpu_emulate.argtypes = [vp, vp, C.c_int, vp, C.c_int, vp, vp, vp, C.c_int, C.c_uint64,
                                          C.c_int, C.c_int, vp]
@@ -134,28 +135,32 @@ def _ptr(a: np.ndarray) -> C.c_void_p:
 
 
 def make_config(variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_fraction=0.05,
-                hp_format="fp16", compute="tensor", lookahead=0) -> CholConfig:
+                hp_format="fp16", compute="tensor", lookahead=0, sp_compute="fp16x3") -> CholConfig:
     if variant not in VARIANTS:
         raise ValueError(f"unknown precision variant: {variant}")  # mpchol.cpp:52
     if hp_format not in ("fp16", "bf16"):
         raise ValueError(f"unknown half-precision format: {hp_format}")
     if compute not in ("tensor", "fp64"):
         raise ValueError(f"unknown compute mode: {compute}")
+    if sp_compute not in ("fp16x3", "tf32x3"):
+        raise ValueError(f"unknown single-precision compute: {sp_compute}")
     return CholConfig(VARIANTS[variant], tile_size, band_width_dp, sp_fraction, workers,
-                      1 if hp_format == "bf16" else 0, 0 if compute == "tensor" else 1, lookahead)
+                      1 if hp_format == "bf16" else 0, 0 if compute == "tensor" else 1, lookahead,
+                      0 if sp_compute == "fp16x3" else 1)
 
 
 # ---------------------------------------------------------------------------
 # module.cpp:209-214 tiled_cholesky / make_spd_matrix
 # ---------------------------------------------------------------------------
 def tiled_cholesky(a, variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_fraction=0.05,
-                   hp_format="fp16", compute="tensor", lookahead=1):
+                   hp_format="fp16", compute="tensor", lookahead=1, sp_compute="fp16x3"):
     """Tiled Cholesky factorization; returns (lower_factor, stats_json)."""
     a = np.ascontiguousarray(a, dtype=np.float64)
     if a.ndim != 2 or a.shape[0] != a.shape[1]:
         raise ValueError("expected a square matrix")
     n = a.shape[0]
-    cfg = make_config(variant, tile_size, workers, band_width_dp, sp_fraction, hp_format, compute, lookahead)
+    cfg = make_config(variant, tile_size, workers, band_width_dp, sp_fraction, hp_format, compute, lookahead,
+                      sp_compute)
     out = np.empty_like(a)
     st = CholStats()
     failed = C.c_int(-1)
@@ -179,10 +184,10 @@ class Cholesky:
     """Device-resident factorization (TiledMatrix + tiled_cholesky)."""
 
     def __init__(self, n, variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_fraction=0.05,
-                 hp_format="fp16", compute="tensor", lookahead=1):
+                 hp_format="fp16", compute="tensor", lookahead=1, sp_compute="fp16x3"):
         self.n = n
         self.cfg = make_config(variant, tile_size, workers, band_width_dp, sp_fraction, hp_format,
-                               compute, lookahead)
+                               compute, lookahead, sp_compute)
         h = C.c_void_p()
         _check(lib().sphemu_gpu_chol_create(n, C.byref(self.cfg), C.byref(h)))
         self.h = h
@@ -247,6 +252,17 @@ class Cholesky:
         cnt = np.zeros(6, dtype=np.int64)
         _check(lib().sphemu_gpu_chol_phase_times(self.h, _ptr(ms), _ptr(cnt), 1 if reset else 0))
         return {p: {"ms": float(ms[i]), "launches": int(cnt[i])} for i, p in enumerate(self.PHASES)}
+
+    def timeline(self, cap=100000):
+        """[(phase, stream, t0_ms, t1_ms)] of the last profiled factorization."""
+        ph = np.zeros(cap, dtype=np.int32)
+        st = np.zeros(cap, dtype=np.int32)
+        t0 = np.zeros(cap)
+        t1 = np.zeros(cap)
+        n = C.c_int()
+        _check(lib().sphemu_gpu_chol_timeline(self.h, _ptr(ph), _ptr(st), _ptr(t0), _ptr(t1), cap, C.byref(n)))
+        k = min(n.value, cap)
+        return [(self.PHASES[ph[i]], int(st[i]), float(t0[i]), float(t1[i])) for i in range(k)]
 
     def reset_phase_times(self):
         self.phase_times(reset=True)

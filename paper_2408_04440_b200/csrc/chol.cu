@@ -79,6 +79,23 @@ std::vector<uint8_t> assign_precisions(int nt, const sphemu_chol_config& c) {
   return map;
 }
 
+// Row scale exponents for the FP16x3 path: |L_rj| <= sqrt(A_rr), so with
+// sqrt(A_rr) = m 2^E (m in [0.5, 1)) every operand of row r times 2^(14-E)
+// stays below 2^14 in magnitude.
+__global__ void k_rowexp(TileStore ts, int* rowexp) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= ts.n) return;
+  const int t = r / ts.lb, o = r % ts.lb;
+  const double a = load_elem(ts.tile(t, t), ts.tprec(t, t), (int64_t)o * ts.b + o);
+  int e = 0;
+  if (a > 0.0 && a < INFINITY) {
+    int E;
+    frexp(sqrt(a), &E);
+    e = 14 - E;
+  }
+  rowexp[r] = e;
+}
+
 // ---- residual probe kernels -------------------------------------------------
 __global__ void k_probe_vec(int n, uint64_t seed, double* x) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -156,6 +173,7 @@ struct Chol {
   DevBuf<uint8_t> d_prec;
   DevBuf<double> linv_[2], p64_[2];  // double-buffered by step parity (lookahead)
   DevBuf<double> dinv, spd_d, spd_pw;
+  DevBuf<int> rowexp;  // per-row power-of-two operand scale (FP16x3 SP path)
   DevBuf<int> fail;
   DevBuf<unsigned> sat;
   DevBuf<int2> lists;
@@ -177,6 +195,11 @@ struct Chol {
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, int>> ev_marks;  // (phase, start event index)
+  struct Span {
+    int phase, stream;
+    double t0, t1;  // ms since the factorization's start event
+  };
+  std::vector<Span> timeline;  // last factorization
   double phase_ms[kNumPhases] = {0};
   int64_t phase_n[kNumPhases] = {0};
   int prof_begin(int phase, cudaStream_t s = nullptr) {
@@ -188,7 +211,7 @@ struct Chol {
       SPH_CUDA(cudaEventCreate(&e));
       ev_pool.push_back(e);
     }
-    ev_marks.push_back({phase, static_cast<int>(idx)});
+    ev_marks.push_back({phase | (s == pstream ? 0x100 : 0), static_cast<int>(idx)});
     SPH_CUDA(cudaEventRecord(ev_pool[idx], s));
     return static_cast<int>(idx);
   }
@@ -197,11 +220,16 @@ struct Chol {
     if (idx >= 0) SPH_CUDA(cudaEventRecord(ev_pool[idx + 1], s));
   }
   void prof_fold() {
+    if (!ev_marks.empty()) timeline.clear();
     for (auto& m : ev_marks) {
-      float ms = 0.f;
+      float ms = 0.f, a = 0.f, z = 0.f;
+      const int phase = m.first & 0xff;
       SPH_CUDA(cudaEventElapsedTime(&ms, ev_pool[m.second], ev_pool[m.second + 1]));
-      phase_ms[m.first] += ms;
-      phase_n[m.first] += 1;
+      if (factored && cudaEventElapsedTime(&a, ev0, ev_pool[m.second]) == cudaSuccess &&
+          cudaEventElapsedTime(&z, ev0, ev_pool[m.second + 1]) == cudaSuccess)
+        timeline.push_back({phase, (m.first >> 8) & 1, a, z});
+      phase_ms[phase] += ms;
+      phase_n[phase] += 1;
     }
     ev_marks.clear();
   }
@@ -285,8 +313,11 @@ struct Chol {
       plists.alloc(pl.size());
       SPH_CUDA(cudaMemcpy(plists.get(), pl.data(), pl.size() * sizeof(int2), cudaMemcpyHostToDevice));
     }
+    rowexp.alloc(n);
+    SPH_CUDA(cudaMemset(rowexp.get(), 0, n * sizeof(int)));
     if (cfg.compute == SPHEMU_COMPUTE_TENSOR && nt > 1)
-      for (int p = 0; p < 2; ++p) panel_[p].alloc(nt, b, pmap, cfg.hp_format);
+      for (int p = 0; p < 2; ++p)
+        panel_[p].alloc(nt, b, pmap, cfg.hp_format, cfg.sp_compute == SPHEMU_SP_F16X3, rowexp.get());
     int prio_lo = 0, prio_hi = 0;
     SPH_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     SPH_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, prio_lo));
@@ -338,6 +369,8 @@ struct Chol {
     }
     const int pl = prof_begin(kLoad);
     k_load_dense<<<tile_grid(), 256, 0, stream>>>(store(), dptr, lda, sat.get());
+    SPH_LAUNCH_CHECK();
+    k_rowexp<<<ceil_div(n, 256), 256, 0, stream>>>(store(), rowexp.get());
     SPH_LAUNCH_CHECK();
     prof_end(pl);
     SPH_CUDA(cudaStreamSynchronize(stream));
@@ -622,6 +655,8 @@ void Chol::generate_spd(uint64_t seed) {
   reset_flags();
   k_gen_spd<<<tile_grid(), 256, 0, stream>>>(store(), spd_d.get(), spd_pw.get(), sat.get());
   SPH_LAUNCH_CHECK();
+  k_rowexp<<<ceil_div(n, 256), 256, 0, stream>>>(store(), rowexp.get());
+  SPH_LAUNCH_CHECK();
   SPH_CUDA(cudaStreamSynchronize(stream));
 }
 
@@ -746,6 +781,21 @@ int sphemu_gpu_chol_phase_times(sphemu_chol_t h, double* ms, int64_t* counts, in
         h->c->phase_n[p] = 0;
       }
     }
+  });
+}
+
+int sphemu_gpu_chol_timeline(sphemu_chol_t h, int* phase, int* stream, double* t0, double* t1, int cap,
+                             int* count) {
+  return guard([&] {
+    const auto& tl = h->c->timeline;
+    const int n = static_cast<int>(tl.size());
+    for (int i = 0; i < n && i < cap; ++i) {
+      phase[i] = tl[i].phase;
+      stream[i] = tl[i].stream;
+      t0[i] = tl[i].t0;
+      t1[i] = tl[i].t1;
+    }
+    *count = n;
   });
 }
 

@@ -53,8 +53,11 @@ CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int elem_byte
 }
 }  // namespace
 
-void PanelFormats::alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int hp_format_) {
+void PanelFormats::alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int hp_format_, bool f16x3_,
+                         const int* rowexp_) {
   (void)pmap;
+  f16x3 = f16x3_;
+  rowexp = rowexp_;
   nt = nt_;
   b = b_;
   hp_format = hp_format_;
@@ -79,12 +82,20 @@ void PanelFormats::alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int 
   m_inlo_a = make_map(in_lo.get(), rows, b, 4, TC_BM);
   m_lhi_b = make_map(l_hi.get(), b, b, 4, bn_tf32);
   m_llo_b = make_map(l_lo.get(), b, b, 4, bn_tf32);
+  if (f16x3) {
+    h_hi.alloc(elems);
+    h_lo.alloc(elems);
+    m_hhi_a = make_map(h_hi.get(), rows, b, 2, TC_BM);
+    m_hlo_a = make_map(h_lo.get(), rows, b, 2, TC_BM);
+    m_hhi_b = make_map(h_hi.get(), rows, b, 2, 128);
+    m_hlo_b = make_map(h_lo.get(), rows, b, 2, 128);
+  }
 }
 
 // ---------------------------------------------------------------------------
 // Device: the persistent warp-specialized GEMM
 // ---------------------------------------------------------------------------
-enum : int { OP_F16 = 0, OP_BF16 = 1, OP_TF32X3 = 2 };
+enum : int { OP_F16 = 0, OP_BF16 = 1, OP_TF32X3 = 2, OP_F16X3 = 3 };
 enum : int { MODE_UPDATE = 0, MODE_PANEL = 1 };
 
 struct TcArgs {
@@ -99,6 +110,10 @@ struct TcArgs {
   float* p_hi;
   float* p_lo;
   uint16_t* p16;
+  uint16_t* h_hi;    // fp16 split of the row-scaled panel (FP16x3 path)
+  uint16_t* h_lo;
+  const int* rowexp; // per global row: power-of-two scale exponent
+  int lb;            // logical tile size (global row = tile * lb + local row)
   int hp_format;
   const int* fail;
   unsigned* sat;
@@ -106,11 +121,12 @@ struct TcArgs {
 
 template <int OPK>
 struct OpTraits {
-  static constexpr bool kSplit = (OPK == OP_TF32X3);
-  static constexpr int kElem = kSplit ? 4 : 2;
+  static constexpr bool kSplit = (OPK == OP_TF32X3 || OPK == OP_F16X3);
+  static constexpr bool kTf32 = (OPK == OP_TF32X3);
+  static constexpr int kElem = kTf32 ? 4 : 2;
   static constexpr int kBK = 128 / kElem;       // K elements per stage (one 128B swizzle row)
-  static constexpr int kUK = kSplit ? 8 : 16;   // K per tcgen05.mma
-  static constexpr int kFmt = OPK == OP_F16 ? 0 : (OPK == OP_BF16 ? 1 : 2);
+  static constexpr int kUK = kTf32 ? 8 : 16;    // K per tcgen05.mma
+  static constexpr int kFmt = (OPK == OP_F16 || OPK == OP_F16X3) ? 0 : (OPK == OP_BF16 ? 1 : 2);
 };
 
 template <int BN, int OPK>
@@ -230,12 +246,18 @@ __global__ void __launch_bounds__(256, 1)
           for (int kk = 0; kk < T::kBK / T::kUK; ++kk) {
             const uint64_t koff = (kk * T::kUK * T::kElem) >> 4;
             const uint32_t accum = (kb | kk) ? 1u : 0u;
-            if constexpr (T::kSplit) {
+            if constexpr (T::kTf32) {
               const uint64_t a_lo = umma_desc_sw128(st + Lay::kA + Lay::kB);
               const uint64_t b_lo = umma_desc_sw128(st + 2 * Lay::kA + Lay::kB);
               umma_tf32(d, a_lo + koff, b_hi + koff, idesc, accum);
               umma_tf32(d, a_hi + koff, b_lo + koff, idesc, 1u);
               umma_tf32(d, a_hi + koff, b_hi + koff, idesc, 1u);
+            } else if constexpr (T::kSplit) {
+              const uint64_t a_lo = umma_desc_sw128(st + Lay::kA + Lay::kB);
+              const uint64_t b_lo = umma_desc_sw128(st + 2 * Lay::kA + Lay::kB);
+              umma_f16(d, a_lo + koff, b_hi + koff, idesc, accum);
+              umma_f16(d, a_hi + koff, b_lo + koff, idesc, 1u);
+              umma_f16(d, a_hi + koff, b_hi + koff, idesc, 1u);
             } else {
               umma_f16(d, a_hi + koff, b_hi + koff, idesc, accum);
             }
@@ -266,42 +288,84 @@ __global__ void __launch_bounds__(256, 1)
     for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
       int i, j, m0, n0;
       decode(w, i, j, m0, n0);
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
       const int r = m0 + row_in;
       void* tp = args.ts.tile(i, j);
       const int p = args.ts.tprec(i, j);
       const int64_t prow = (int64_t)(i - args.k - 1) * b + r;
-#pragma unroll 1
+      // Update mode: fetch this thread's C row segment (BN values) before the
+      // accumulator is ready, so the HBM latency hides under the MMAs.
+      // uint4 words per row segment: fp32 C for the split (SP) kinds, fp16 C otherwise
+      constexpr int kCWords = (MODE == MODE_UPDATE) ? (T::kSplit ? BN / 4 : BN / 8) : 1;
+      uint4 cpre[kCWords];
+      if constexpr (MODE == MODE_UPDATE) {
+        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const char*>(tp) +
+                                                          ((int64_t)r * b + n0) * prec_bytes(p));
+        const int words = T::kSplit ? BN / 4 : BN / 8;
+#pragma unroll
+        for (int u = 0; u < kCWords; ++u)
+          if (u < words) cpre[u] = src[u];
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll(MODE == MODE_UPDATE ? BN / 32 : 1)
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t v[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c0, v);
         const int64_t e0 = (int64_t)r * b + n0 + c0;
         if constexpr (MODE == MODE_UPDATE) {
-          if (p == kSP) {
-            float* cp = static_cast<float*>(tp) + e0;
+          // C = round_p(C - acc): one correctly rounded fp32 subtraction per
+          // element (== the FP64 subtract + round of mpchol.cpp:311-312 up to
+          // the rare double-rounding tie), then the storage rounding.
+          if constexpr (OPK == OP_F16X3) {
+            // operands were scaled by 2^e_row: undo exactly (powers of two)
+            const int er = args.rowexp[min(i * args.lb + r, args.ts.n - 1)];
+            const int cbase = j * args.lb + n0 + c0;
+            const float rs = __int_as_float((127 - er) << 23);
 #pragma unroll
-            for (int t = 0; t < 32; t += 4) {
-              float4 cv = *reinterpret_cast<float4*>(cp + t);
-              cv.x = __double2float_rn((double)cv.x - (double)__uint_as_float(v[t + 0]));
-              cv.y = __double2float_rn((double)cv.y - (double)__uint_as_float(v[t + 1]));
-              cv.z = __double2float_rn((double)cv.z - (double)__uint_as_float(v[t + 2]));
-              cv.w = __double2float_rn((double)cv.w - (double)__uint_as_float(v[t + 3]));
-              *reinterpret_cast<float4*>(cp + t) = cv;
+            for (int t = 0; t < 32; ++t) {
+              const int ec = __ldg(args.rowexp + min(cbase + t, args.ts.n - 1));
+              v[t] = __float_as_uint(__uint_as_float(v[t]) * (rs * __int_as_float((127 - ec) << 23)));
+            }
+          }
+          if (p == kSP) {
+            float4* cp = reinterpret_cast<float4*>(static_cast<float*>(tp) + e0);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              const uint4 pre = cpre[(MODE == MODE_UPDATE) ? (c0 / 4 + t) % kCWords : 0];
+              float4 cv = make_float4(__uint_as_float(pre.x), __uint_as_float(pre.y), __uint_as_float(pre.z),
+                                      __uint_as_float(pre.w));
+              cv.x = __fsub_rn(cv.x, __uint_as_float(v[4 * t + 0]));
+              cv.y = __fsub_rn(cv.y, __uint_as_float(v[4 * t + 1]));
+              cv.z = __fsub_rn(cv.z, __uint_as_float(v[4 * t + 2]));
+              cv.w = __fsub_rn(cv.w, __uint_as_float(v[4 * t + 3]));
+              cp[t] = cv;
             }
           } else {
             uint16_t* cp = static_cast<uint16_t*>(tp) + e0;
 #pragma unroll
             for (int t = 0; t < 32; t += 8) {
-              uint4 raw = *reinterpret_cast<uint4*>(cp + t);
+              uint4 raw = cpre[(MODE == MODE_UPDATE) ? ((c0 + t) / 8) % kCWords : 0];
               uint16_t* h = reinterpret_cast<uint16_t*>(&raw);
 #pragma unroll
               for (int u = 0; u < 8; ++u) {
-                const double old = p == kHP ? (double)__half2float(__ushort_as_half(h[u]))
-                                            : (double)__bfloat162float(__ushort_as_bfloat16(h[u]));
-                const double nv = old - (double)__uint_as_float(v[t + u]);
-                h[u] = p == kHP ? __half_as_ushort(to_half_sat(nv, sat_local))
-                                : __bfloat16_as_ushort(to_bf16_sat(nv, sat_local));
+                if (p == kHP) {
+                  const float nv = __fsub_rn(__half2float(__ushort_as_half(h[u])), __uint_as_float(v[t + u]));
+                  __half hv = __float2half_rn(nv);
+                  if (__hisinf(hv)) {
+                    ++sat_local;
+                    hv = __ushort_as_half(nv < 0.f ? (unsigned short)0xfbffu : (unsigned short)0x7bffu);
+                  }
+                  h[u] = __half_as_ushort(hv);
+                } else {
+                  const float nv =
+                      __fsub_rn(__bfloat162float(__ushort_as_bfloat16(h[u])), __uint_as_float(v[t + u]));
+                  __nv_bfloat16 hv = __float2bfloat16_rn(nv);
+                  if (__hisinf(hv)) {
+                    ++sat_local;
+                    hv = __ushort_as_bfloat16(nv < 0.f ? (unsigned short)0xff7fu : (unsigned short)0x7f7fu);
+                  }
+                  h[u] = __bfloat16_as_ushort(hv);
+                }
               }
               *reinterpret_cast<uint4*>(cp + t) = raw;
             }
@@ -355,6 +419,14 @@ __global__ void __launch_bounds__(256, 1)
             pl[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
             pl[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
             *reinterpret_cast<uint4*>(args.p16 + pe) = *reinterpret_cast<const uint4*>(h16);
+            if (args.h_hi) {
+              const int er = args.rowexp[min(i * args.lb + r, args.ts.n - 1)];
+              uint16_t hh[8], hl[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) f16_split(qv[u], er, hh[u], hl[u]);
+              *reinterpret_cast<uint4*>(args.h_hi + pe) = *reinterpret_cast<const uint4*>(hh);
+              *reinterpret_cast<uint4*>(args.h_lo + pe) = *reinterpret_cast<const uint4*>(hl);
+            }
           }
         }
       }
@@ -405,7 +477,8 @@ __global__ void k_panel_prep(TileStore ts, int k, const int2* list, const double
 
 // DP-class panel tiles: P64 (already rounded) -> tile storage + mirrors.
 __global__ void k_panel_finish_dp(TileStore ts, int k, const int2* list, const double* __restrict__ p64,
-                                  float* p_hi, float* p_lo, uint16_t* p16, int hp_format, const int* fail) {
+                                  float* p_hi, float* p_lo, uint16_t* p16, int hp_format, const int* fail,
+                                  uint16_t* h_hi, uint16_t* h_lo, const int* rowexp) {
   if (*(volatile const int*)fail >= 0) return;
   const int b = ts.b;
   const int64_t bb = (int64_t)b * b;
@@ -422,6 +495,10 @@ __global__ void k_panel_finish_dp(TileStore ts, int k, const int2* list, const d
     unsigned dummy = 0;
     p16[base + e] = hp_format == SPHEMU_HP_BF16 ? __bfloat16_as_ushort(to_bf16_sat(x, dummy))
                                                 : __half_as_ushort(to_half_sat(x, dummy));
+    if (h_hi) {
+      const int r = (int)(e / b);
+      f16_split(x, rowexp[min(i * ts.lb + r, ts.n - 1)], h_hi[base + e], h_lo[base + e]);
+    }
   }
 }
 
@@ -487,7 +564,8 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
         ts, k, d_dp, linv, p64, fail, sat);
     SPH_LAUNCH_CHECK();
     k_panel_finish_dp<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(n_dp)), 256, 0, s>>>(
-        ts, k, d_dp, p64, pf.p_hi.get(), pf.p_lo.get(), pf.p16.get(), pf.hp_format, fail);
+        ts, k, d_dp, p64, pf.p_hi.get(), pf.p_lo.get(), pf.p16.get(), pf.hp_format, fail,
+        pf.f16x3 ? pf.h_hi.get() : nullptr, pf.h_lo.get(), pf.rowexp);
     SPH_LAUNCH_CHECK();
   }
   if (n_lo) {
@@ -506,6 +584,10 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
     a.p_hi = pf.p_hi.get();
     a.p_lo = pf.p_lo.get();
     a.p16 = pf.p16.get();
+    a.h_hi = pf.f16x3 ? pf.h_hi.get() : nullptr;
+    a.h_lo = pf.h_lo.get();
+    a.rowexp = pf.rowexp;
+    a.lb = ts.lb;
     a.hp_format = pf.hp_format;
     a.fail = fail;
     a.sat = sat;
@@ -525,11 +607,16 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
   a.hp_format = hp_format;
   a.fail = fail;
   a.sat = sat;
+  a.rowexp = pf.rowexp;
+  a.lb = ts.lb;
   if (cls == SPHEMU_PREC_SP) {
     a.sub_n = ts.b / 128;
     a.sub_per = (ts.b / TC_BM) * a.sub_n;
     a.items = cnt * a.sub_per;
-    launch_tc<128, OP_TF32X3, MODE_UPDATE>(pf.m_phi_a, pf.m_plo_a, pf.m_phi_b, pf.m_plo_b, a, s, max_ctas);
+    if (pf.f16x3)
+      launch_tc<128, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_b, pf.m_hlo_b, a, s, max_ctas);
+    else
+      launch_tc<128, OP_TF32X3, MODE_UPDATE>(pf.m_phi_a, pf.m_plo_a, pf.m_phi_b, pf.m_plo_b, a, s, max_ctas);
   } else {
     a.sub_n = ts.b / pf.bn;
     a.sub_per = (ts.b / TC_BM) * a.sub_n;

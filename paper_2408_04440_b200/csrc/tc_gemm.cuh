@@ -30,8 +30,14 @@ struct PanelFormats {
   // TMA descriptors: A-role (128-row box) and B-role (BN-row box).
   CUtensorMap m_phi_a, m_plo_a, m_phi_b, m_plo_b, m_p16_a, m_p16_b;
   CUtensorMap m_inhi_a, m_inlo_a, m_lhi_b, m_llo_b;
+  // FP16x3 path for the SP class: x * 2^e_row = hi + lo, both fp16.
+  bool f16x3 = false;
+  const int* rowexp = nullptr;
+  DevBuf<uint16_t> h_hi, h_lo;
+  CUtensorMap m_hhi_a, m_hlo_a, m_hhi_b, m_hlo_b;
   int bn = 256;
-  void alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int hp_format_);
+  void alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int hp_format_, bool f16x3_,
+             const int* rowexp_);
 };
 
 // Panel TRSM for all i > k: DP-class tiles through FP64 DMMA, SP/HP-class

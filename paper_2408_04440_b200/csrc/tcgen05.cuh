@@ -152,4 +152,19 @@ __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
   lo = x - hi;
 }
 
+// x * 2^e = hi + lo with hi = fp16(x 2^e), lo = fp16(x 2^e - hi) (both RNE,
+// saturating). The row exponent keeps |x 2^e| <= 2^14 (Cholesky bound
+// |L_rj| <= sqrt(A_rr)), so hi + lo carries ~22 bits like a tf32 split while
+// running on the kind::f16 pipe (2x the kind::tf32 rate).
+__device__ __forceinline__ void f16_split(double x, int e, uint16_t& hi, uint16_t& lo) {
+  const float xs = ldexpf(__double2float_rn(x), e);
+  __half h;
+  asm("cvt.rn.satfinite.f16.f32 %0, %1;" : "=h"(*reinterpret_cast<unsigned short*>(&h)) : "f"(xs));
+  const float r = xs - __half2float(h);
+  __half l;
+  asm("cvt.rn.satfinite.f16.f32 %0, %1;" : "=h"(*reinterpret_cast<unsigned short*>(&l)) : "f"(r));
+  hi = __half_as_ushort(h);
+  lo = __half_as_ushort(l);
+}
+
 }  // namespace sphemu_gpu

@@ -188,3 +188,16 @@ def test_repeat_factorizations_are_deterministic(sph):
         h.wait()
         outs.append(h.factor_dense())
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("n,b", [(2500, 512), (4096, 512), (3000, 256)])
+@pytest.mark.parametrize("sp_compute", ["fp16x3", "tf32x3"])
+def test_sp_class_compute_modes(sph, O, n, b, sp_compute):
+    """Both tensor-core forms of the SP class (row-scaled fp16 hi+lo and
+    3xTF32) stay within max(2 x oracle residual, dpsp threshold)."""
+    a = O.make_spd(n, 6)
+    f, _ = sph.tiled_cholesky(a, "dpsp", tile_size=b, sp_compute=sp_compute)
+    ref, _ = O.tiled_cholesky(a, "dpsp", tile_size=b, workers=8)
+    r_gpu, r_ref = O.relative_residual(a, f), O.relative_residual(a, ref)
+    assert r_gpu <= max(2 * r_ref, THRESH["dpsp"]), (r_gpu, r_ref)
+    assert np.abs(f - ref).max() < 1e-5
