@@ -105,6 +105,15 @@ int sphemu_gpu_tiled_cholesky_dense(const double* a, int where_a, int n,
 typedef struct sphemu_chol_s* sphemu_chol_t;
 int sphemu_gpu_chol_create(int n, const sphemu_chol_config* cfg, sphemu_chol_t* out);
 int sphemu_gpu_chol_destroy(sphemu_chol_t h);
+/* 2D block-cyclic distribution over a P x Q grid of GPUs (one process per
+ * GPU, the caller sets the device first): tile (i, j) is stored on rank
+ * (i mod P) * Q + (j mod Q); panel tiles travel over NCCL at their storage
+ * precision. All ranks call every handle function collectively; the dense
+ * factor of store_dense is gathered on rank 0. uid128 comes from
+ * sphemu_gpu_nccl_unique_id on rank 0 (the caller distributes it). */
+int sphemu_gpu_nccl_unique_id(void* out128);
+int sphemu_gpu_chol_create_dist(int n, const sphemu_chol_config* cfg, int P, int Q, int rank,
+                                const void* uid128, sphemu_chol_t* out);
 /* TiledMatrix::from_dense (mpchol.cpp:124-138) + the input quantization of
  * mpchol.cpp:360-363; lda = row stride in elements. */
 int sphemu_gpu_chol_load_dense(sphemu_chol_t h, const double* a, int where, int64_t lda);

@@ -14,6 +14,7 @@ from ._sphemu import (  # noqa: F401
     forward_sht,
     inverse_sht,
     make_spd_matrix,
+    nccl_unique_id,
     max_band_limit,
     resolution_summary,
     tiled_cholesky,
@@ -21,6 +22,6 @@ from ._sphemu import (  # noqa: F401
 
 __all__ = [
     "Cholesky", "NotPositiveDefiniteError", "ShtPlan", "__version__", "assign_precisions",
-    "forward_sht", "inverse_sht", "make_spd_matrix", "max_band_limit", "resolution_summary",
+    "forward_sht", "inverse_sht", "make_spd_matrix", "nccl_unique_id", "max_band_limit", "resolution_summary",
     "tiled_cholesky",
 ]

@@ -108,6 +108,9 @@ def lib():
         L.sphemu_gpu_sht_stream.restype = vp
         L.sphemu_gpu_sht_plan_seconds.argtypes = [vp]
         L.sphemu_gpu_sht_plan_seconds.restype = C.c_double
+        L.sphemu_gpu_nccl_unique_id.argtypes = [vp]
+        L.sphemu_gpu_chol_create_dist.argtypes = [C.c_int, C.POINTER(CholConfig), C.c_int, C.c_int, C.c_int, vp,
+                                                  C.POINTER(vp)]
         L.sphemu_gpu_chol_set_profiling.argtypes = [vp, C.c_int]
         L.sphemu_gpu_chol_phase_times.argtypes = [vp, vp, vp, C.c_int]
         L.sphemu_gpu_chol_update_flops.argtypes = [vp, dp, dp, dp]
@@ -180,16 +183,35 @@ def make_spd_matrix(n, seed=1):
     return lower + np.tril(lower, -1).T
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (create on rank 0, share with the others)."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().sphemu_gpu_nccl_unique_id(C.byref(buf)))
+    return bytes(buf)
+
+
 class Cholesky:
-    """Device-resident factorization (TiledMatrix + tiled_cholesky)."""
+    """Device-resident factorization (TiledMatrix + tiled_cholesky).
+
+    dist=(P, Q, rank, uid) distributes the tiles 2D block-cyclically over a
+    P x Q grid of GPUs (one process per GPU, device already selected); every
+    method is then collective, and factor_dense() returns the gathered factor
+    on rank 0 (None elsewhere)."""
 
     def __init__(self, n, variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_fraction=0.05,
-                 hp_format="fp16", compute="tensor", lookahead=1, sp_compute="fp16x3"):
+                 hp_format="fp16", compute="tensor", lookahead=1, sp_compute="fp16x3", dist=None):
         self.n = n
         self.cfg = make_config(variant, tile_size, workers, band_width_dp, sp_fraction, hp_format,
                                compute, lookahead, sp_compute)
         h = C.c_void_p()
-        _check(lib().sphemu_gpu_chol_create(n, C.byref(self.cfg), C.byref(h)))
+        self.rank = 0
+        if dist is None:
+            _check(lib().sphemu_gpu_chol_create(n, C.byref(self.cfg), C.byref(h)))
+        else:
+            P, Q, rank, uid = dist
+            self.rank = rank
+            ub = (C.c_uint8 * 128).from_buffer_copy(uid)
+            _check(lib().sphemu_gpu_chol_create_dist(n, C.byref(self.cfg), P, Q, rank, C.byref(ub), C.byref(h)))
         self.h = h
 
     def __del__(self):
@@ -220,12 +242,12 @@ class Cholesky:
     def factor_dense(self):
         out = np.empty((self.n, self.n))
         _check(lib().sphemu_gpu_chol_store_dense(self.h, _ptr(out), HOST, self.n))
-        return out
+        return out if self.rank == 0 else None
 
     factor_dense_unfactored = factor_dense  # the stored tiles, before or after factor()
 
     def store(self, dev_ptr, ld=None):
-        _check(lib().sphemu_gpu_chol_store_dense(self.h, C.c_void_p(dev_ptr), DEVICE, ld or self.n))
+        _check(lib().sphemu_gpu_chol_store_dense(self.h, C.c_void_p(dev_ptr or 0), DEVICE, ld or self.n))
 
     def residual(self, a):
         a = np.ascontiguousarray(a, dtype=np.float64)

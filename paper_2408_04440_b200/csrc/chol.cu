@@ -18,11 +18,21 @@
 #include <tuple>
 #include <vector>
 
+#include <nccl.h>
+
 #include "chol_kernels.cuh"
 #include "potrf_coop.cuh"
 #include "tc_gemm.cuh"
+#include "tcgen05.cuh"
 
 namespace sphemu_gpu {
+
+#define SPH_NCCL(call)                                                                              \
+  do {                                                                                              \
+    ncclResult_t r__ = (call);                                                                      \
+    if (r__ != ncclSuccess)                                                                         \
+      throw ::sphemu_gpu::Error(SPHEMU_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r__)); \
+  } while (0)
 
 namespace {
 thread_local std::string g_last_error;
@@ -86,6 +96,10 @@ __global__ void k_rowexp(TileStore ts, int* rowexp) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= ts.n) return;
   const int t = r / ts.lb, o = r % ts.lb;
+  if (!ts.owned(t, t)) {  // another rank owns this diagonal tile (max-reduced later)
+    rowexp[r] = -0x40000000;
+    return;
+  }
   const double a = load_elem(ts.tile(t, t), ts.tprec(t, t), (int64_t)o * ts.b + o);
   int e = 0;
   if (a > 0.0 && a < INFINITY) {
@@ -94,6 +108,40 @@ __global__ void k_rowexp(TileStore ts, int* rowexp) {
     e = 14 - E;
   }
   rowexp[r] = e;
+}
+
+// 2D block-cyclic exchange: a panel tile received at its storage precision
+// (xbuf slot i-k-1) -> FP64 mirror P64 and the tensor-core mirrors, exactly as
+// the owner's panel epilogue writes them. blockIdx.y indexes the import list.
+__global__ void k_panel_import(TileStore ts, int k, const int2* __restrict__ list, const uint8_t* __restrict__ xbuf,
+                               double* p64, float* p_hi, float* p_lo, uint16_t* p16, uint16_t* h_hi, uint16_t* h_lo,
+                               const int* rowexp, int hp_format, const int* fail) {
+  if (*(volatile const int*)fail >= 0) return;
+  const int b = ts.b;
+  const int64_t bb = (int64_t)b * b;
+  const int i = list[blockIdx.y].x;
+  const int p = ts.tprec(i, k);
+  const int64_t base = (int64_t)(i - k - 1) * bb;
+  const void* src = xbuf + base * 8;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += (int64_t)gridDim.x * blockDim.x) {
+    const double x = load_elem(src, p, e);
+    p64[base + e] = x;
+    if (p_hi) {
+      float hi, lo;
+      tf32_split(__double2float_rn(x), hi, lo);
+      p_hi[base + e] = hi;
+      p_lo[base + e] = lo;
+    }
+    if (p16) {
+      unsigned dummy = 0;
+      p16[base + e] = hp_format == SPHEMU_HP_BF16 ? __bfloat16_as_ushort(to_bf16_sat(x, dummy))
+                                                  : __half_as_ushort(to_half_sat(x, dummy));
+    }
+    if (h_hi) {
+      const int r = (int)(e / b);
+      f16_split(x, rowexp[min(i * ts.lb + r, ts.n - 1)], h_hi[base + e], h_lo[base + e]);
+    }
+  }
 }
 
 // ---- residual probe kernels -------------------------------------------------
@@ -129,6 +177,7 @@ __global__ void k_spd_matvec(int n, const double* __restrict__ d, const double* 
 __global__ void k_tile_matvec(TileStore ts, const double* __restrict__ x, double* y, int trans) {
   int i, j;
   pair_from_index(blockIdx.x, i, j);
+  if (!ts.owned(i, j)) return;
   const void* tp = ts.tile(i, j);
   const int p = ts.tprec(i, j);
   const int ri = ts.rows(i), rj = ts.rows(j);
@@ -165,6 +214,16 @@ __global__ void k_diff_norms(int n, const double* a, const double* b, double* su
 struct Chol {
   int n = 0, b = 0, nt = 0;  // b = storage pitch (padded), lb = logical tile size
   int lb = 0;
+  // 2D block-cyclic distribution over a P x Q process grid (one GPU per
+  // rank): tile (i, j) lives on rank (i mod P) * Q + (j mod Q).
+  int P = 1, Q = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  bool dist() const { return P * Q > 1; }
+  int owner(int i, int j) const { return (i % P) * Q + (j % Q); }
+  bool mine(int i, int j) const { return owner(i, j) == rank; }
+  DevBuf<uint8_t> xbuf;                        // received panel tiles (storage precision)
+  DevBuf<int2> ilists;                         // per step: panel tiles owned elsewhere
+  std::vector<int64_t> ilist_off, ilist_cnt;
   sphemu_chol_config cfg{};
   std::vector<uint8_t> pmap, sprec;
   std::vector<int64_t> off;
@@ -243,7 +302,8 @@ struct Chol {
     return TileStore{arena.get(), d_off.get(), d_prec.get(), n, b, nt, lb};
   }
 
-  Chol(int n_, const sphemu_chol_config& c) : n(n_), cfg(c) {
+  Chol(int n_, const sphemu_chol_config& c, int P_ = 1, int Q_ = 1, int rank_ = 0, ncclComm_t comm_ = nullptr)
+      : n(n_), P(P_), Q(Q_), rank(rank_), comm(comm_), cfg(c) {
     validate_config(cfg);
     if (n < 1) throw std::invalid_argument("matrix is empty");
     lb = cfg.tile_size;
@@ -260,12 +320,23 @@ struct Chol {
     for (size_t t = 0; t < pmap.size(); ++t) {
       int sp = pmap[t] == SPHEMU_PREC_DP ? kDP : (pmap[t] == SPHEMU_PREC_SP ? kSP : (cfg.hp_format == SPHEMU_HP_BF16 ? kBF : kHP));
       sprec[t] = static_cast<uint8_t>(sp);
+      int ti = 0, tj = 0;
+      {
+        int64_t x = 0;
+        while ((x + 1) * (x + 2) / 2 <= static_cast<int64_t>(t)) ++x;
+        ti = static_cast<int>(x);
+        tj = static_cast<int>(t - x * (x + 1) / 2);
+      }
+      if (!mine(ti, tj)) {
+        off[t] = -1;  // stored on another rank
+        continue;
+      }
       off[t] = o;
       o += static_cast<int64_t>(b) * b * prec_bytes(sp);
       o = (o + 255) & ~int64_t{255};
     }
     off.back() = o;
-    arena.alloc(static_cast<size_t>(o));
+    arena.alloc(static_cast<size_t>(std::max<int64_t>(o, 256)));
     d_off.alloc(pmap.size());
     d_prec.alloc(pmap.size());
     SPH_CUDA(cudaMemcpy(d_off.get(), off.data(), pmap.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
@@ -289,7 +360,7 @@ struct Chol {
           const int j_lo = part == 0 ? k + 1 : k + 2, j_hi = part == 0 ? std::min(k + 2, nt) : nt;
           for (int j = j_lo; j < j_hi; ++j)
             for (int i = j; i < nt; ++i)
-              if (pmap[tix(i, j)] == cls) all.push_back(make_int2(i, j));
+              if (pmap[tix(i, j)] == cls && mine(i, j)) all.push_back(make_int2(i, j));
           list_cnt[slot] = static_cast<int64_t>(all.size()) - list_off[slot];
         }
     if (!all.empty()) {
@@ -303,15 +374,31 @@ struct Chol {
     for (int k = 0; k < nt; ++k) {
       plist_off[k] = static_cast<int64_t>(pl.size());
       for (int i = k + 1; i < nt; ++i)
-        if (pmap[tix(i, k)] == SPHEMU_PREC_DP) pl.push_back(make_int2(i, k));
+        if (pmap[tix(i, k)] == SPHEMU_PREC_DP && mine(i, k)) pl.push_back(make_int2(i, k));
       plist_dp[k] = static_cast<int64_t>(pl.size()) - plist_off[k];
       for (int i = k + 1; i < nt; ++i)
-        if (pmap[tix(i, k)] != SPHEMU_PREC_DP) pl.push_back(make_int2(i, k));
+        if (pmap[tix(i, k)] != SPHEMU_PREC_DP && mine(i, k)) pl.push_back(make_int2(i, k));
       plist_lo[k] = static_cast<int64_t>(pl.size()) - plist_off[k] - plist_dp[k];
     }
     if (!pl.empty()) {
       plists.alloc(pl.size());
       SPH_CUDA(cudaMemcpy(plists.get(), pl.data(), pl.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    }
+    if (dist()) {
+      ilist_off.assign(nt, 0);
+      ilist_cnt.assign(nt, 0);
+      std::vector<int2> il;
+      for (int k = 0; k < nt; ++k) {
+        ilist_off[k] = static_cast<int64_t>(il.size());
+        for (int i = k + 1; i < nt; ++i)
+          if (!mine(i, k)) il.push_back(make_int2(i, k));
+        ilist_cnt[k] = static_cast<int64_t>(il.size()) - ilist_off[k];
+      }
+      if (!il.empty()) {
+        ilists.alloc(il.size());
+        SPH_CUDA(cudaMemcpy(ilists.get(), il.data(), il.size() * sizeof(int2), cudaMemcpyHostToDevice));
+      }
+      if (nt > 1) xbuf.alloc(static_cast<size_t>(nt - 1) * b * b * 8);
     }
     rowexp.alloc(n);
     SPH_CUDA(cudaMemset(rowexp.get(), 0, n * sizeof(int)));
@@ -341,6 +428,7 @@ struct Chol {
     for (auto e : ev_bulk) cudaEventDestroy(e);
     if (ev_start_p) cudaEventDestroy(ev_start_p);
     if (pstream) cudaStreamDestroy(pstream);
+    if (comm) ncclCommDestroy(comm);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -372,6 +460,7 @@ struct Chol {
     SPH_LAUNCH_CHECK();
     k_rowexp<<<ceil_div(n, 256), 256, 0, stream>>>(store(), rowexp.get());
     SPH_LAUNCH_CHECK();
+    if (dist()) SPH_NCCL(ncclAllReduce(rowexp.get(), rowexp.get(), n, ncclInt32, ncclMax, comm, stream));
     prof_end(pl);
     SPH_CUDA(cudaStreamSynchronize(stream));
   }
@@ -450,7 +539,9 @@ struct Chol {
     t_start = std::chrono::steady_clock::now();
     SPH_CUDA(cudaEventRecord(ev0, stream));
     const int reserve = 32;  // SMs left to the chain while the bulk runs
-    if (!cfg.lookahead || nt == 1) {
+    if (dist()) {
+      factor_dist();
+    } else if (!cfg.lookahead || nt == 1) {
       for (int k = 0; k < nt; ++k) {
         op_potrf(k, stream);
         if (k + 1 >= nt) break;
@@ -479,6 +570,49 @@ struct Chol {
     SPH_CUDA(cudaEventRecord(ev1, stream));
     launches = launch_count() - launches_at_start;
     factored = true;
+  }
+
+  // 2D block-cyclic step sequence (PAPER.md:570 pattern): the owner of
+  // (k,k) factors it and broadcasts L_kk^{-1} (and the failure flag); the
+  // process column k mod Q computes its panel tiles; every panel tile is
+  // broadcast at its storage precision (the minimal bytes, rounded at the
+  // sender) and receivers rebuild the FP64 / tensor-core operand mirrors;
+  // every rank updates the trailing tiles it owns.
+  void factor_dist() {
+    for (int k = 0; k < nt; ++k) {
+      const int ok = owner(k, k);
+      if (rank == ok) op_potrf(k, stream);
+      SPH_NCCL(ncclBroadcast(fail.get(), fail.get(), 1, ncclInt32, ok, comm, stream));
+      if (k + 1 >= nt) break;
+      const int set = k & 1;
+      SPH_NCCL(ncclBroadcast(linv_[set].get(), linv_[set].get(), static_cast<size_t>(b) * b, ncclFloat64, ok, comm,
+                             stream));
+      op_panel(k, stream);  // owned panel tiles only
+      SPH_NCCL(ncclGroupStart());
+      for (int i = k + 1; i < nt; ++i) {
+        const int root = owner(i, k);
+        const size_t bytes = static_cast<size_t>(b) * b * prec_bytes(sprec[tix(i, k)]);
+        uint8_t* recv = xbuf.get() + static_cast<size_t>(i - k - 1) * b * b * 8;
+        const void* send = rank == root ? static_cast<const void*>(arena.get() + off[tix(i, k)]) : recv;
+        SPH_NCCL(ncclBroadcast(send, recv, bytes, ncclUint8, root, comm, stream));
+      }
+      SPH_NCCL(ncclGroupEnd());
+      note_launch();
+      if (ilist_cnt[k]) {
+        PanelFormats& pf = panel_[set];
+        const bool tensor = cfg.compute == SPHEMU_COMPUTE_TENSOR;
+        k_panel_import<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(ilist_cnt[k])), 256, 0,
+                         stream>>>(store(), k, ilists.get() + ilist_off[k], xbuf.get(), p64_[set].get(),
+                                   tensor ? pf.p_hi.get() : nullptr, tensor ? pf.p_lo.get() : nullptr,
+                                   tensor ? pf.p16.get() : nullptr, (tensor && pf.f16x3) ? pf.h_hi.get() : nullptr,
+                                   (tensor && pf.f16x3) ? pf.h_lo.get() : nullptr, rowexp.get(), cfg.hp_format,
+                                   fail.get());
+        SPH_LAUNCH_CHECK();
+      }
+      op_update(k, 0, stream, 0);
+      op_update(k, 1, stream, 0);
+    }
+    SPH_NCCL(ncclAllReduce(sat.get(), sat.get(), 1, ncclUint32, ncclSum, comm, stream));
   }
 
   // Diagonal tile factor + inverse on a cooperative grid (potrf_coop.cuh).
@@ -555,8 +689,54 @@ struct Chol {
     }
     const int threads = 256;
     dim3 grid(std::max(1, std::min(ceil_div(n, threads), 64)), static_cast<unsigned>(n));
-    k_store_dense<<<grid, threads, 0, stream>>>(store(), dptr, ld);
-    SPH_LAUNCH_CHECK();
+    if (dist()) {
+      // Gather every tile to rank 0 (collective: all ranks call store_dense).
+      DevBuf<char> full;
+      DevBuf<int64_t> goff;
+      std::vector<int64_t> g(pmap.size());
+      int64_t o = 0;
+      for (size_t t = 0; t < pmap.size(); ++t) {
+        g[t] = o;
+        o += static_cast<int64_t>(b) * b * prec_bytes(sprec[t]);
+        o = (o + 255) & ~int64_t{255};
+      }
+      if (rank == 0) {
+        full.alloc(static_cast<size_t>(o));
+        goff.alloc(pmap.size());
+        SPH_CUDA(cudaMemcpy(goff.get(), g.data(), g.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+      }
+      size_t t = 0;
+      while (t < pmap.size()) {  // groups of up to 512 point-to-point transfers
+        SPH_NCCL(ncclGroupStart());
+        for (size_t e = 0; e < 512 && t < pmap.size(); ++t, ++e) {
+          int x = 0;
+          while ((x + 1) * (x + 2) / 2 <= static_cast<int64_t>(t)) ++x;
+          const int ti = x, tj = static_cast<int>(t - static_cast<int64_t>(x) * (x + 1) / 2);
+          const int o_r = owner(ti, tj);
+          const size_t bytes = static_cast<size_t>(b) * b * prec_bytes(sprec[t]);
+          if (o_r == 0) {
+            if (rank == 0)
+              SPH_CUDA(cudaMemcpyAsync(full.get() + g[t], arena.get() + off[t], bytes, cudaMemcpyDeviceToDevice,
+                                       stream));
+          } else if (rank == o_r) {
+            SPH_NCCL(ncclSend(arena.get() + off[t], bytes, ncclUint8, 0, comm, stream));
+          } else if (rank == 0) {
+            SPH_NCCL(ncclRecv(full.get() + g[t], bytes, ncclUint8, o_r, comm, stream));
+          }
+        }
+        SPH_NCCL(ncclGroupEnd());
+      }
+      if (rank == 0) {
+        TileStore gs{full.get(), goff.get(), d_prec.get(), n, b, nt, lb};
+        k_store_dense<<<grid, threads, 0, stream>>>(gs, dptr, ld);
+        SPH_LAUNCH_CHECK();
+      }
+      SPH_CUDA(cudaStreamSynchronize(stream));
+      if (rank != 0) return;
+    } else {
+      k_store_dense<<<grid, threads, 0, stream>>>(store(), dptr, ld);
+      SPH_LAUNCH_CHECK();
+    }
     if (where == SPHEMU_HOST)
       SPH_CUDA(cudaMemcpy2DAsync(out, sizeof(double) * ldo, dptr, sizeof(double) * n,
                                  sizeof(double) * n, n, cudaMemcpyDeviceToHost, stream));
@@ -604,8 +784,10 @@ struct Chol {
       SPH_CUDA(cudaMemsetAsync(y2.get(), 0, n * sizeof(double), stream));
       k_tile_matvec<<<static_cast<unsigned>(pmap.size()), 256, 0, stream>>>(store(), x.get(), z.get(), 1);
       SPH_LAUNCH_CHECK();
+      if (dist()) SPH_NCCL(ncclAllReduce(z.get(), z.get(), n, ncclFloat64, ncclSum, comm, stream));
       k_tile_matvec<<<static_cast<unsigned>(pmap.size()), 256, 0, stream>>>(store(), z.get(), y2.get(), 0);
       SPH_LAUNCH_CHECK();
+      if (dist()) SPH_NCCL(ncclAllReduce(y2.get(), y2.get(), n, ncclFloat64, ncclSum, comm, stream));
       SPH_CUDA(cudaMemsetAsync(sums.get(), 0, 2 * sizeof(double), stream));
       k_diff_norms<<<ceil_div(n, 256), 256, 0, stream>>>(n, y1.get(), y2.get(), sums.get());
       SPH_LAUNCH_CHECK();
@@ -657,6 +839,7 @@ void Chol::generate_spd(uint64_t seed) {
   SPH_LAUNCH_CHECK();
   k_rowexp<<<ceil_div(n, 256), 256, 0, stream>>>(store(), rowexp.get());
   SPH_LAUNCH_CHECK();
+  if (dist()) SPH_NCCL(ncclAllReduce(rowexp.get(), rowexp.get(), n, ncclInt32, ncclMax, comm, stream));
   SPH_CUDA(cudaStreamSynchronize(stream));
 }
 
@@ -705,6 +888,36 @@ int sphemu_gpu_chol_create(int n, const sphemu_chol_config* cfg, sphemu_chol_t* 
     try {
       h->c = new Chol(n, *cfg);
     } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int sphemu_gpu_nccl_unique_id(void* out128) {
+  return guard([&] {
+    ncclUniqueId id;
+    SPH_NCCL(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int sphemu_gpu_chol_create_dist(int n, const sphemu_chol_config* cfg, int P, int Q, int rank, const void* uid128,
+                                sphemu_chol_t* out) {
+  return guard([&] {
+    *out = nullptr;
+    if (P < 1 || Q < 1 || rank < 0 || rank >= P * Q) throw std::invalid_argument("bad process grid");
+    ncclUniqueId id;
+    std::memcpy(&id, uid128, sizeof(id));
+    ncclComm_t comm = nullptr;
+    SPH_NCCL(ncclCommInitRank(&comm, P * Q, id, rank));
+    auto* h = new sphemu_chol_s{nullptr};
+    try {
+      h->c = new Chol(n, *cfg, P, Q, rank, comm);
+    } catch (...) {
+      ncclCommDestroy(comm);
       delete h;
       throw;
     }

@@ -23,6 +23,7 @@ struct TileStore {
   __device__ __forceinline__ void* tile(int i, int j) const { return base + off[idx(i, j)]; }
   __device__ __forceinline__ int tprec(int i, int j) const { return prec[idx(i, j)]; }
   __device__ __forceinline__ int rows(int i) const { return min(lb, n - i * lb); }
+  __device__ __forceinline__ bool owned(int i, int j) const { return off[idx(i, j)] >= 0; }
 };
 
 __device__ __forceinline__ void pair_from_index(int64_t p, int& a, int& c) {
@@ -46,6 +47,7 @@ __device__ __forceinline__ void flush_sat(unsigned local, unsigned* sat) {
 static __global__ void k_gen_spd(TileStore ts, const double* __restrict__ d, const double* __restrict__ pw,
                           unsigned* sat) {
   const int64_t t = blockIdx.x;
+  if (ts.off[t] < 0) return;  // tile owned by another rank
   int i, j;
   pair_from_index(t, i, j);
   void* tp = ts.tile(i, j);
@@ -70,6 +72,7 @@ static __global__ void k_gen_spd(TileStore ts, const double* __restrict__ d, con
 // TiledMatrix::from_dense (mpchol.cpp:124-138) + input quantization.
 static __global__ void k_load_dense(TileStore ts, const double* __restrict__ a, int64_t lda, unsigned* sat) {
   const int64_t t = blockIdx.x;
+  if (ts.off[t] < 0) return;  // tile owned by another rank
   int i, j;
   pair_from_index(t, i, j);
   void* tp = ts.tile(i, j);
