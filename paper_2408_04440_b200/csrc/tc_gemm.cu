@@ -341,31 +341,36 @@ __global__ void __launch_bounds__(256, 1)
               cp[t] = cv;
             }
           } else {
+            // HP class: packed pairs, cvt.rn.satfinite clamps to +-max finite
+            // exactly like half.hpp's saturation; values whose RNE result
+            // would overflow are counted (|x| >= 65520 for fp16, >= bf16's
+            // rounding threshold for bf16).
             uint16_t* cp = static_cast<uint16_t*>(tp) + e0;
+            const float thr = p == kHP ? 65520.0f : 3.3961514e38f;
 #pragma unroll
             for (int t = 0; t < 32; t += 8) {
               uint4 raw = cpre[(MODE == MODE_UPDATE) ? ((c0 + t) / 8) % kCWords : 0];
-              uint16_t* h = reinterpret_cast<uint16_t*>(&raw);
+              uint32_t* w2 = reinterpret_cast<uint32_t*>(&raw);
 #pragma unroll
-              for (int u = 0; u < 8; ++u) {
+              for (int u = 0; u < 4; ++u) {
+                float lo, hi;
                 if (p == kHP) {
-                  const float nv = __fsub_rn(__half2float(__ushort_as_half(h[u])), __uint_as_float(v[t + u]));
-                  __half hv = __float2half_rn(nv);
-                  if (__hisinf(hv)) {
-                    ++sat_local;
-                    hv = __ushort_as_half(nv < 0.f ? (unsigned short)0xfbffu : (unsigned short)0x7bffu);
-                  }
-                  h[u] = __half_as_ushort(hv);
+                  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w2[u]));
+                  lo = f.x;
+                  hi = f.y;
                 } else {
-                  const float nv =
-                      __fsub_rn(__bfloat162float(__ushort_as_bfloat16(h[u])), __uint_as_float(v[t + u]));
-                  __nv_bfloat16 hv = __float2bfloat16_rn(nv);
-                  if (__hisinf(hv)) {
-                    ++sat_local;
-                    hv = __ushort_as_bfloat16(nv < 0.f ? (unsigned short)0xff7fu : (unsigned short)0x7f7fu);
-                  }
-                  h[u] = __bfloat16_as_ushort(hv);
+                  lo = __uint_as_float(w2[u] << 16);
+                  hi = __uint_as_float(w2[u] & 0xffff0000u);
                 }
+                lo = __fsub_rn(lo, __uint_as_float(v[t + 2 * u]));
+                hi = __fsub_rn(hi, __uint_as_float(v[t + 2 * u + 1]));
+                sat_local += (fabsf(lo) >= thr) + (fabsf(hi) >= thr);
+                uint32_t packed;
+                if (p == kHP)
+                  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(packed) : "f"(hi), "f"(lo));
+                else
+                  asm("cvt.rn.satfinite.bf16x2.f32 %0, %1, %2;" : "=r"(packed) : "f"(hi), "f"(lo));
+                w2[u] = packed;
               }
               *reinterpret_cast<uint4*>(cp + t) = raw;
             }

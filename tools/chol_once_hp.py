@@ -1,0 +1,14 @@
+"""One warm factorization with an HP-dominated map (for ncu on the HP update)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2408_04440_b200 as sph  # noqa: E402
+
+n, b, v, hp = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3], sys.argv[4]
+h = sph.Cholesky(n, v, tile_size=b, hp_format=hp, lookahead=0)
+for _ in range(int(sys.argv[5]) if len(sys.argv) > 5 else 2):
+    h.generate_spd(1)
+    h.factor()
+    st = h.wait()
+print(f"n={n} b={b} {v} {hp} {st.device_ms:.2f} ms {n**3/3/st.device_ms/1e9:.1f} TFLOP/s")

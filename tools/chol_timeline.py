@@ -6,7 +6,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2408_04440_b200 as sph  # noqa: E402
 
 n, b, v = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
-h = sph.Cholesky(n, v, tile_size=b)
+hp = sys.argv[4] if len(sys.argv) > 4 else "fp16"
+h = sph.Cholesky(n, v, tile_size=b, hp_format=hp)
 h.set_profiling(True)
 for _ in range(2):
     h.generate_spd(1)
