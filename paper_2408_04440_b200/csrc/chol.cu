@@ -578,39 +578,84 @@ struct Chol {
   // broadcast at its storage precision (the minimal bytes, rounded at the
   // sender) and receivers rebuild the FP64 / tensor-core operand mirrors;
   // every rank updates the trailing tiles it owns.
-  void factor_dist() {
-    for (int k = 0; k < nt; ++k) {
-      const int ok = owner(k, k);
-      if (rank == ok) op_potrf(k, stream);
-      SPH_NCCL(ncclBroadcast(fail.get(), fail.get(), 1, ncclInt32, ok, comm, stream));
-      if (k + 1 >= nt) break;
+  // POTRF(k) on the owner of (k,k), then the failure flag and L_kk^{-1}
+  // broadcast from it.
+  void op_potrf_dist(int k, cudaStream_t s) {
+    const int ok = owner(k, k);
+    if (rank == ok) op_potrf(k, s);
+    SPH_NCCL(ncclBroadcast(fail.get(), fail.get(), 1, ncclInt32, ok, comm, s));
+    if (k + 1 < nt) {
       const int set = k & 1;
-      SPH_NCCL(ncclBroadcast(linv_[set].get(), linv_[set].get(), static_cast<size_t>(b) * b, ncclFloat64, ok, comm,
-                             stream));
-      op_panel(k, stream);  // owned panel tiles only
-      SPH_NCCL(ncclGroupStart());
-      for (int i = k + 1; i < nt; ++i) {
-        const int root = owner(i, k);
-        const size_t bytes = static_cast<size_t>(b) * b * prec_bytes(sprec[tix(i, k)]);
-        uint8_t* recv = xbuf.get() + static_cast<size_t>(i - k - 1) * b * b * 8;
-        const void* send = rank == root ? static_cast<const void*>(arena.get() + off[tix(i, k)]) : recv;
-        SPH_NCCL(ncclBroadcast(send, recv, bytes, ncclUint8, root, comm, stream));
+      SPH_NCCL(ncclBroadcast(linv_[set].get(), linv_[set].get(), static_cast<size_t>(b) * b, ncclFloat64, ok, comm, s));
+    }
+    note_launch(2);
+  }
+
+  // Panel TRSM on the owned panel tiles, then every panel tile broadcast at
+  // its storage precision and imported into the operand mirrors elsewhere.
+  void op_panel_dist(int k, cudaStream_t s) {
+    const int set = k & 1;
+    op_panel(k, s);
+    const int px = prof_begin(kPanel, s);
+    SPH_NCCL(ncclGroupStart());
+    for (int i = k + 1; i < nt; ++i) {
+      const int root = owner(i, k);
+      const size_t bytes = static_cast<size_t>(b) * b * prec_bytes(sprec[tix(i, k)]);
+      uint8_t* recv = xbuf.get() + static_cast<size_t>(i - k - 1) * b * b * 8;
+      const void* send = rank == root ? static_cast<const void*>(arena.get() + off[tix(i, k)]) : recv;
+      SPH_NCCL(ncclBroadcast(send, recv, bytes, ncclUint8, root, comm, s));
+    }
+    SPH_NCCL(ncclGroupEnd());
+    note_launch();
+    if (ilist_cnt[k]) {
+      PanelFormats& pf = panel_[set];
+      const bool tensor = cfg.compute == SPHEMU_COMPUTE_TENSOR;
+      k_panel_import<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(ilist_cnt[k])), 256, 0, s>>>(
+          store(), k, ilists.get() + ilist_off[k], xbuf.get(), p64_[set].get(), tensor ? pf.p_hi.get() : nullptr,
+          tensor ? pf.p_lo.get() : nullptr, tensor ? pf.p16.get() : nullptr,
+          (tensor && pf.f16x3) ? pf.h_hi.get() : nullptr, (tensor && pf.f16x3) ? pf.h_lo.get() : nullptr,
+          rowexp.get(), cfg.hp_format, fail.get());
+      SPH_LAUNCH_CHECK();
+    }
+    prof_end(px, s);
+  }
+
+  // 2D block-cyclic step sequence (PAPER.md:570 pattern): the owner of
+  // (k,k) factors it and broadcasts L_kk^{-1} (and the failure flag); the
+  // process column k mod Q computes its panel tiles; every panel tile is
+  // broadcast at its storage precision (the minimal bytes, rounded at the
+  // sender) and receivers rebuild the FP64 / tensor-core operand mirrors;
+  // every rank updates the trailing tiles it owns. With lookahead the whole
+  // chain (column k+1 update, POTRF, broadcasts, panel, exchange, import)
+  // runs on the high-priority stream, all collectives in step order, while
+  // the bulk update of step k runs on the main stream.
+  void factor_dist() {
+    if (!cfg.lookahead || nt == 1) {
+      for (int k = 0; k < nt; ++k) {
+        op_potrf_dist(k, stream);
+        if (k + 1 >= nt) break;
+        op_panel_dist(k, stream);
+        op_update(k, 0, stream, 0);
+        op_update(k, 1, stream, 0);
       }
-      SPH_NCCL(ncclGroupEnd());
-      note_launch();
-      if (ilist_cnt[k]) {
-        PanelFormats& pf = panel_[set];
-        const bool tensor = cfg.compute == SPHEMU_COMPUTE_TENSOR;
-        k_panel_import<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(ilist_cnt[k])), 256, 0,
-                         stream>>>(store(), k, ilists.get() + ilist_off[k], xbuf.get(), p64_[set].get(),
-                                   tensor ? pf.p_hi.get() : nullptr, tensor ? pf.p_lo.get() : nullptr,
-                                   tensor ? pf.p16.get() : nullptr, (tensor && pf.f16x3) ? pf.h_hi.get() : nullptr,
-                                   (tensor && pf.f16x3) ? pf.h_lo.get() : nullptr, rowexp.get(), cfg.hp_format,
-                                   fail.get());
-        SPH_LAUNCH_CHECK();
+    } else {
+      const int reserve = 32;
+      SPH_CUDA(cudaEventRecord(ev_start_p, stream));
+      SPH_CUDA(cudaStreamWaitEvent(pstream, ev_start_p, 0));
+      op_potrf_dist(0, pstream);
+      op_panel_dist(0, pstream);
+      SPH_CUDA(cudaEventRecord(ev_panel[0], pstream));
+      for (int k = 0; k + 1 < nt; ++k) {
+        if (k > 0) SPH_CUDA(cudaStreamWaitEvent(pstream, ev_bulk[k - 1], 0));
+        op_update(k, 0, pstream, 0);
+        op_potrf_dist(k + 1, pstream);
+        if (k + 2 < nt) op_panel_dist(k + 1, pstream);
+        SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
+        SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k], 0));
+        op_update(k, 1, stream, std::max(1, num_sms() - reserve));
+        SPH_CUDA(cudaEventRecord(ev_bulk[k], stream));
       }
-      op_update(k, 0, stream, 0);
-      op_update(k, 1, stream, 0);
+      SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[nt - 1], 0));
     }
     SPH_NCCL(ncclAllReduce(sat.get(), sat.get(), 1, ncclUint32, ncclSum, comm, stream));
   }

@@ -32,7 +32,7 @@ for n, b, v in ((3000, 256, "dpsphp"), (8192, 512, "dpsp")):
     for P, Q in grids:
         obj = [sph.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        h = sph.Cholesky(n, v, tile_size=b, lookahead=0, dist=(P, Q, rank, obj[0]))
+        h = sph.Cholesky(n, v, tile_size=b, lookahead=int(os.environ.get("LOOKAHEAD", "1")), dist=(P, Q, rank, obj[0]))
         h.generate_spd(3)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
