@@ -1,24 +1,31 @@
-"""Benchmark of the sphemu B200 hot path (BASELINE.json configs[1], "C2").
+"""Benchmark of the sphemu B200 hot path (BASELINE.json configs[1] and [2]).
 
-Workload C2 on one B200: the mixed-precision tiled Cholesky of
-make_spd_test_matrix(32 400, seed 1) (L = 180, N = L^2) with the dpsp
-precision map (band 1) and 256/512-wide tiles, plus forward+inverse SHT of
-1 000 snapshots on the 181 x 360 grid at L = 180.
+N = 1 (headline, configs[1] "C2"): the mixed-precision tiled Cholesky of
+make_spd_test_matrix(32 400, seed 1) (L = 180, N = L^2), dpsp precision map
+(band 1), 512-wide tiles; step = the dense FP64 input resident in HBM is
+tiled and quantized to the precision map (mpchol.cpp:124-138,360-363), then
+factored (mpchol.cpp:351-410). The N = 1 line also carries the 1-GPU point of
+C3 ("c3_1gpu") so the C3 scaling curve has its base.
 
-  step     = one factorization: the dense FP64 input (resident in HBM) is tiled
-             and quantized to the precision map (mpchol.cpp:124-138,360-363),
-             then factored (mpchol.cpp:351-410);
+N > 1 (configs[2] "C3"): make_spd_test_matrix(129 600, seed 1), dpsphp with
+BF16 HP storage, 2D block-cyclic over P x Q = 2x1 / 2x2 / 4x2 GPUs with NCCL
+panel broadcasts; step = the generator writes each rank's owned tiles at
+storage precision, then the distributed factorization. Strong scaling.
+
   value    = N^3/3 / device time per step, TFLOP/s (whole job, max over ranks);
-  e2e      = the same through the reference-facing C-ABI call
-             sphemu_gpu_tiled_cholesky_dense with pinned host buffers, H2D of
-             the input and D2H of the factor inside the timed region;
-  roofline = the dominant kernel (tcgen05 3xTF32 trailing update of the
-             SP-class tiles) against the measured 3xTF32 rate, plus the
-             precision-weighted roofline of the whole factorization;
-  inputs   = 8.4 GB > 126 MB L2, so no L2 flush is needed between steps.
+  e2e      = through the public API with host buffers, H2D of the input and
+             D2H of the factor inside the timed region (N = 1: the one-shot
+             C-ABI call sphemu_gpu_tiled_cholesky_dense with pinned buffers;
+             N > 1: the distributed handle on the C2 matrix, see e2e_dist);
+  roofline = the dominant trailing-update kernel against the measured peak of
+             its pipe, plus the precision-weighted roofline of the whole
+             factorization;
+  sht      = forward + inverse SHT of 1 000 snapshots on 181 x 360 at L = 180
+             per GPU (snapshots sharded, no collective);
+  inputs   = >= 8.4 GB of tiles >> 126 MB L2, so no L2 flush between steps.
 
 `--impl reference` times the reference algorithm's CPU restatement (oracle/,
-the reference itself cannot be built here) on the host cores.
+DESIGN.md §3) on the host cores on a bounded sample of the same workload.
 """
 import argparse
 import json
@@ -32,7 +39,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_C2, L_C2, B_C2, VARIANT = 32400, 180, 512, "dpsp"
+
 SHT_GRID, SHT_T = (181, 360, 180), 1000
 PEAKS_FILE = os.path.join(ROOT, "profiles", "peaks_r01.json")
 
@@ -121,7 +128,24 @@ def max_over_ranks(x, world):
 # ----------------------------------------------------------------------------
 # CPU baseline / reference arm: the oracle restatement on the host cores
 # ----------------------------------------------------------------------------
-def cpu_cholesky_sample(n=8192, reps=1):
+WORKLOADS = {
+    # BASELINE.json configs[1]: the 1-GPU headline (dense FP64 input resident in HBM).
+    "C2": {"n": 32400, "variant": "dpsp", "tile": 512, "hp": "fp16", "input": "dense",
+           "desc": "C2: tiled Cholesky make_spd_test_matrix(32400, 1) (L=180) dpsp b=512"},
+    # BASELINE.json configs[2]: 2D block-cyclic over 2/4/8 GPUs (inputs generated in place per step).
+    "C3": {"n": 129600, "variant": "dpsphp", "tile": 512, "hp": "bf16", "input": "generate",
+           "desc": "C3: tiled Cholesky make_spd_test_matrix(129600, 1) (L=360) dpsphp/BF16 b=512"},
+}
+GRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
+THRESH = {"dp": 1e-12, "dpsp": 5e-6, "dpsphp": 1e-2, "dphp": 5e-2}  # acceptance_main.cpp:226
+
+
+def pick_workload(args, world):
+    return WORKLOADS[args.workload or ("C2" if world == 1 else "C3")]
+
+
+def cpu_cholesky_sample(n=8192, reps=1, wl=None):
+    wl = wl or WORKLOADS["C2"]
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     O.build()
@@ -134,9 +158,10 @@ def cpu_cholesky_sample(n=8192, reps=1):
     best = 1e30
     for _ in range(reps):
         t0 = time.perf_counter()
-        O.tiled_cholesky(a, VARIANT, B_C2, workers=cores)
+        O.tiled_cholesky(a, wl["variant"], wl["tile"], workers=cores, hp_format=wl["hp"])
         best = min(best, time.perf_counter() - t0)
-    return n ** 3 / 3 / best / 1e12, cores, f"make_spd_test_matrix({n}, 1), {VARIANT}, b={B_C2}; {kind_note}", best
+    return (n ** 3 / 3 / best / 1e12, cores,
+            f"make_spd_test_matrix({n}, 1), {wl['variant']}/{wl['hp']}, b={wl['tile']}; {kind_note}", best)
 
 
 def cpu_sht_sample(t=32):
@@ -157,21 +182,24 @@ def cpu_sht_sample(t=32):
 def run_reference(args, world, rank):
     if rank != 0:
         return
+    wl = pick_workload(args, world)
     for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_cholesky_sample(n=4096)
+        cpu_cholesky_sample(n=4096, wl=wl)
     times = []
     val = sample = cores = None
     for _ in range(args.steps):
-        val, cores, sample, t = cpu_cholesky_sample(n=args.ref_n)
+        val, cores, sample, t = cpu_cholesky_sample(n=args.ref_n, wl=wl)
         times.append(t)
     v = args.ref_n ** 3 / 3 / (sum(times) / len(times)) / 1e12
     line = {
         "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64 compute, f32 storage (dpsp)",
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": f"f64 compute, {wl['variant']} storage",
         "data": "synthetic: make_spd_test_matrix (reference generator, bitwise)",
-        "config": {"workload": f"C2 Cholesky bounded sample N={args.ref_n} (full C2 N={N_C2}: "
-                               f"~{(N_C2/args.ref_n)**3:.0f}x the work)", "variant": VARIANT, "tile_size": B_C2},
+        "config": {"workload": f"{wl['desc']}; CPU bounded sample N={args.ref_n} "
+                               f"(~{(wl['n']/args.ref_n)**3:.0f}x less work than the full N={wl['n']})",
+                   "variant": wl["variant"], "tile_size": wl["tile"], "hp_format": wl["hp"]},
         "impl": "reference",
         "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -185,59 +213,81 @@ METRIC = "mixed-precision Cholesky TFLOP/s at 1/2/4/8 B200 (% of roofline); SHT 
 # ----------------------------------------------------------------------------
 # Our arm
 # ----------------------------------------------------------------------------
-def run_ours(args, world, rank, local):
-    import ctypes as C
+def share_uid(sph, world, rank):
+    if world == 1:
+        return None
+    import torch.distributed as dist
+    obj = [sph.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
 
-    import numpy as np
+
+def make_handle(sph, wl, args, world, rank):
+    P, Q = GRIDS.get(world, (world, 1))
+    uid = share_uid(sph, world, rank)
+    return sph.Cholesky(wl["n"], wl["variant"], tile_size=wl["tile"], hp_format=wl["hp"],
+                        lookahead=args.lookahead, sp_compute=args.sp_compute,
+                        dist=(P, Q, rank, uid) if world > 1 else None), (P, Q)
+
+
+def dense_input(sph, wl):
+    """The symmetric dense FP64 make_spd_test_matrix in HBM (built by a local
+    1-GPU handle: generator tiles -> dense lower -> mirrored)."""
     import torch
-
-    torch.cuda.set_device(local)
-    import paper_2408_04440_b200 as sph
-    lib = sph._sphemu.lib()
-    lib.sphemu_gpu_set_device(local)
-    n, b = args.n, args.tile
-    # Dense FP64 input resident in HBM (the tiled_cholesky_dense input form).
-    a_dev = torch.empty((n, n), dtype=torch.float64, device="cuda")
-    h = sph.Cholesky(n, VARIANT, tile_size=b, lookahead=args.lookahead, sp_compute=args.sp_compute)
-    h.generate_spd(1)
-    h.store(a_dev.data_ptr())          # lower triangle
-    a_dev += torch.tril(a_dev, -1).T   # symmetric dense A, bitwise the reference's values
+    n = wl["n"]
+    g = sph.Cholesky(n, "dp", tile_size=wl["tile"])
+    g.generate_spd(1)
+    a = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    g.store(a.data_ptr())
+    del g
+    a += torch.tril(a, -1).T
     torch.cuda.synchronize()
-    fl = h.flops()
-    h.set_profiling(True)
+    return a
+
+
+def time_factor(sph, h, wl, args, world, a_dev=None, steps=None, warmup=None, clocks_index=None):
+    """W untimed + K timed steps (input -> tiles at storage precision, factor),
+    barrier + synchronize on both sides; max over ranks."""
+    import torch
+    steps = args.steps if steps is None else steps
+    warmup = args.warmup if warmup is None else warmup
+    lib = sph._sphemu.lib()
 
     def step():
-        h.load(a_dev.data_ptr(), where=sph._sphemu.DEVICE, lda=n)
+        if a_dev is not None:
+            h.load(a_dev.data_ptr(), where=sph._sphemu.DEVICE, lda=wl["n"])
+        else:
+            h.generate_spd(1)
         h.factor()
         return h.wait()
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
     h.reset_phase_times()
     launches0 = lib.sphemu_gpu_launch_count()
     barrier(world)
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        start.record()
-        for _ in range(args.steps):
-            st = step()
-        end.record()
-        torch.cuda.synchronize()
+    clocks = ClockSampler(clocks_index) if clocks_index is not None else None
+    if clocks:
+        clocks.__enter__()
+    start.record()
+    for _ in range(steps):
+        st = step()
+    end.record()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.__exit__()
     barrier(world)
     launches = lib.sphemu_gpu_launch_count() - launches0
-    ms = max_over_ranks(start.elapsed_time(end) / args.steps, world)
-    flops = n ** 3 / 3
-    value = world * flops / (ms * 1e-3) / 1e12
-    phases = h.phase_times()
-    probe = h.residual_probe(1, 2)
+    ms = max_over_ranks(start.elapsed_time(end) / steps, world)
+    return ms, st, launches, clocks
 
-    # Roofline: dominant kernel and whole factorization (measured peaks).
+
+def roofline(h, wl, args, phases, steps, ms):
     peaks = load_peaks()
     own = peaks.get("own", {})
     p_dp = own.get("fp64_dgemm_tflops", 35.5)
-    # SP class runs on the pipe of the chosen split: fp16 hi+lo (3 kind::f16
-    # MMAs) -> cuBLAS FP16 / 3; 3xTF32 -> cuBLAS TF32 / 3.
     if args.sp_compute == "fp16x3":
         p_sp = own.get("fp16_tflops", 1546.6) / 3
         sp_src = "cuBLAS FP16 GEMM measured on this pool / 3 (3 kind::f16 MMAs per product; profiles/peaks_r01.json)"
@@ -246,44 +296,125 @@ def run_ours(args, world, rank, local):
         p_sp = own.get("tf32x3_effective_tflops", 244.7)
         sp_src = "cuBLAS TF32 GEMM measured on this pool / 3 (profiles/peaks_r01.json)"
         sp_kernel = "k_tc_gemm<128, TF32x3, UPDATE> (SP-class trailing update)"
-    p_hp = peaks.get("bf16_tflops", 1692.6)
-    sp_update_flops = h.class_update_flops()["sp"]
-    t_sp = phases["update_sp"]["ms"] / args.steps
-    dom = {"kernel": sp_kernel,
-           "bound": "tensor", "achieved": sp_update_flops / (t_sp * 1e-3) / 1e12 if t_sp > 0 else None,
-           "peak": p_sp, "unit": "TFLOP/s",
-           "peak_source": sp_src,
-           "traffic": None}
-    dom["frac"] = dom["achieved"] / p_sp if dom["achieved"] else None
+    if wl["hp"] == "bf16":
+        p_hp, hp_src = peaks.get("bf16_tflops", 1692.6), "MEASURED_PEAKS.json bf16_tflops (burst)"
+        hp_kernel = "k_tc_gemm<128, BF16, UPDATE> (HP-class trailing update, BF16 storage)"
+    else:
+        p_hp, hp_src = own.get("fp16_tflops", 1546.6), "cuBLAS FP16 GEMM measured on this pool (profiles/peaks_r01.json)"
+        hp_kernel = "k_tc_gemm<128, F16, UPDATE> (HP-class trailing update, FP16 storage)"
+    cuf = h.class_update_flops()
+    cls = {"dp": ("update_dp", p_dp, "FP64 DGEMM measured on this pool (profiles/peaks_r01.json)",
+                  "k_update_fp64_v2 (DP-class trailing update, DMMA)"),
+           "sp": ("update_sp", p_sp, sp_src, sp_kernel),
+           "hp": ("update_hp", p_hp, hp_src, hp_kernel)}
+    dom_c = max(cls, key=lambda c: phases[cls[c][0]]["ms"])
+    ph, peak, src, kern = cls[dom_c]
+    t = phases[ph]["ms"] / steps
+    ach = cuf[dom_c] / (t * 1e-3) / 1e12 if t > 0 else None
+    dom = {"kernel": kern, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+           "frac": ach / peak if ach else None, "peak_source": src, "traffic": None,
+           "per_launch_basis": f"{cuf[dom_c]/1e12:.3f} TFLOP of {dom_c.upper()}-class update per step on this rank "
+                               f"/ summed launch time {t:.2f} ms (CUDA events on the launching stream)"}
+    fl = h.flops()
     t_roof = fl["dp"] / (p_dp * 1e12) + fl["sp"] / (p_sp * 1e12) + fl["hp"] / (p_hp * 1e12)
-    dom["precision_weighted"] = {"t_roof_ms": 1e3 * t_roof, "frac": t_roof / (ms * 1e-3),
-                                 "flops_split": fl, "peaks_tflops": {"dp": p_dp, "sp": p_sp, "hp": p_hp}}
+    world = max(1, args.world)
+    dom["precision_weighted"] = {"t_roof_ms": 1e3 * t_roof / world, "frac": t_roof / world / (ms * 1e-3),
+                                 "flops_split": fl, "peaks_tflops": {"dp": p_dp, "sp": p_sp, "hp": p_hp},
+                                 "note": "T_roof = sum_p F_p / Peak_p over all tiles, divided by the GPU count"}
+    return dom
 
-    # End to end through the reference-facing call with pinned host buffers.
-    e2e = None
-    if rank == 0 or True:
-        a_host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+
+def e2e_single(sph, wl, args, a_dev):
+    """The reference-facing one-shot call with pinned host buffers: H2D of the
+    input and D2H of the factor inside the timed region."""
+    import ctypes as C
+    import torch
+    lib = sph._sphemu.lib()
+    n = wl["n"]
+    a_host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    a_host.copy_(a_dev)
+    f_host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    cfg = sph._sphemu.make_config(wl["variant"], wl["tile"], hp_format=wl["hp"], lookahead=args.lookahead,
+                                  sp_compute=args.sp_compute)
+    stats = sph._sphemu.CholStats()
+    failed = C.c_int(-1)
+
+    def call():
+        rc = lib.sphemu_gpu_tiled_cholesky_dense(C.c_void_p(a_host.data_ptr()), 0, n, C.byref(cfg),
+                                                 C.c_void_p(f_host.data_ptr()), 0, C.byref(stats), C.byref(failed))
+        assert rc == 0, rc
+
+    call()  # warm-up: first-call module load + the handle cache
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        call()
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    lib.sphemu_gpu_release_cache()
+    del a_host, f_host
+    return {"value": n ** 3 / 3 / t_e2e / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": 8 * n * n,
+            "d2h_bytes_per_step": 8 * n * n, "ms_per_step": 1e3 * t_e2e, "steps": e2e_steps,
+            "api": "sphemu_gpu_tiled_cholesky_dense (host pointers, pinned)",
+            "bytes_note": "counted as the dense n x n in and out; the library moves the lower triangle (H2D by "
+                          "tile rows, D2H by tile columns as they finish) and host threads write the zeros"}
+
+
+def e2e_dist(sph, args, world, rank):
+    """N GPUs through the distributed handle with host buffers: the dense C2
+    input lives once in shared host memory (/dev/shm, registered with every
+    rank's CUDA context), each rank copies the rows it owns; the factor is
+    gathered over NCCL and written to rank 0's pinned host buffer."""
+    import ctypes as C
+    import torch
+    wl = WORKLOADS["C2"]
+    n = wl["n"]
+    path = f"/dev/shm/sphemu_bench_{os.environ.get('MASTER_PORT', '0')}"
+    if rank == 0:
+        a_dev = dense_input(sph, wl)
+        a_host = torch.from_file(path, shared=True, size=n * n, dtype=torch.float64).view(n, n)
         a_host.copy_(a_dev)
-        f_host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-        cfg = sph._sphemu.make_config(VARIANT, b, lookahead=args.lookahead, sp_compute=args.sp_compute)
-        stats = sph._sphemu.CholStats()
-        failed = C.c_int(-1)
-        e2e_steps = max(1, min(args.steps, args.e2e_steps))
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            rc = lib.sphemu_gpu_tiled_cholesky_dense(C.c_void_p(a_host.data_ptr()), 0, n, C.byref(cfg),
-                                                     C.c_void_p(f_host.data_ptr()), 0, C.byref(stats),
-                                                     C.byref(failed))
-            assert rc == 0
-        t_e2e = (time.perf_counter() - t0) / e2e_steps
-        t_e2e = max_over_ranks(t_e2e, world)
-        e2e = {"value": world * flops / t_e2e / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": 8 * n * n,
-               "d2h_bytes_per_step": 8 * n * n, "ms_per_step": 1e3 * t_e2e, "steps": e2e_steps,
-               "api": "sphemu_gpu_tiled_cholesky_dense (host pointers, pinned)"}
-        del a_host, f_host
+        del a_dev
+        torch.cuda.empty_cache()
+    barrier(world)
+    if rank != 0:
+        a_host = torch.from_file(path, shared=True, size=n * n, dtype=torch.float64).view(n, n)
+    cudart = torch.cuda.cudart()
+    registered = int(cudart.cudaHostRegister(a_host.data_ptr(), 8 * n * n, 0)) == 0
+    f_host = torch.empty((n, n) if rank == 0 else (1, 1), dtype=torch.float64, pin_memory=True)
+    h, grid = make_handle(sph, wl, args, world, rank)
+    lib = sph._sphemu.lib()
 
-    # SHT throughput (device-resident), forward + inverse, T = 1000 at L = 180.
+    def call():
+        h.load(a_host.numpy())
+        h.factor()
+        h.wait()
+        rc = lib.sphemu_gpu_chol_store_dense(h.h, C.c_void_p(f_host.data_ptr()), 0, n)
+        assert rc == 0, rc
+
+    call()
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        call()
+    t_e2e = max_over_ranks((time.perf_counter() - t0) / e2e_steps, world)
+    del h
+    if registered:
+        cudart.cudaHostUnregister(a_host.data_ptr())
+    barrier(world)
+    if rank == 0:
+        os.unlink(path)
+    return {"value": n ** 3 / 3 / t_e2e / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": 8 * n * n,
+            "d2h_bytes_per_step": 8 * n * n, "ms_per_step": 1e3 * t_e2e, "steps": e2e_steps,
+            "workload": f"{wl['desc']} over {grid[0]}x{grid[1]} GPUs (C3's 134 GB dense host input and output "
+                        f"exceed this box's 196 GB host RAM)",
+            "api": "Cholesky(dist=...).load(host) + factor + sphemu_gpu_chol_store_dense(host); input in "
+                   "shared host memory" + (" (registered)" if registered else " (pageable)")}
+
+
+def sht_throughput(sph, world):
+    import torch
     nt, nphi, L = SHT_GRID
     plan = sph.ShtPlan(nt, nphi, L)
     coef = torch.randn(SHT_T, L * L, dtype=torch.float64, device="cuda")
@@ -295,6 +426,7 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = 5
+    barrier(world)
     s0.record()
     for _ in range(reps):
         plan.inverse_device(coef.data_ptr(), SHT_T, fld.data_ptr())
@@ -304,39 +436,94 @@ def run_ours(args, world, rank, local):
     sht_ms = max_over_ranks(s0.elapsed_time(s1) / reps, world)
     sht_rt = (back - coef).abs().max().item()
     sht_flops = 2 * (2 * nt * L * (L + 1)) * SHT_T
-    sht = {"snapshots_per_s": world * SHT_T / (sht_ms * 1e-3), "unit": "snapshots/s (forward+inverse pair)",
-           "grid": f"{nt}x{nphi}", "band_limit": L, "snapshots": SHT_T, "ms_per_batch": sht_ms,
-           "legendre_fp64_tflops": sht_flops / (sht_ms * 1e-3) / 1e12, "round_trip_max_abs": sht_rt}
+    return {"snapshots_per_s": world * SHT_T / (sht_ms * 1e-3), "unit": "snapshots/s (forward+inverse pair)",
+            "grid": f"{nt}x{nphi}", "band_limit": L, "snapshots_per_gpu": SHT_T, "ms_per_batch": sht_ms,
+            "sharding": "snapshots sharded across GPUs, no collective" if world > 1 else "single GPU",
+            "legendre_fp64_tflops_per_gpu": sht_flops / (sht_ms * 1e-3) / 1e12, "round_trip_max_abs": sht_rt}
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    torch.cuda.set_device(local)
+    import paper_2408_04440_b200 as sph
+    lib = sph._sphemu.lib()
+    lib.sphemu_gpu_set_device(local)
+    args.world = world
+    wl = pick_workload(args, world)
+    n = wl["n"]
+    a_dev = dense_input(sph, wl) if wl["input"] == "dense" else None
+    h, grid = make_handle(sph, wl, args, world, rank)
+    h.set_profiling(True)
+    ms, st, launches, clocks = time_factor(sph, h, wl, args, world, a_dev=a_dev, clocks_index=local)
+    flops = n ** 3 / 3
+    value = flops / (ms * 1e-3) / 1e12
+    phases = h.phase_times()
+    probe = h.residual_probe(1, 2)
+    dom = roofline(h, wl, args, phases, args.steps, ms)
+    sat = int(st.half_saturations)
+    del h
+    torch.cuda.empty_cache()
+
+    if world == 1:
+        e2e = e2e_single(sph, wl, args, a_dev) if a_dev is not None else None
+    else:
+        e2e = e2e_dist(sph, args, world, rank) if not args.no_e2e else None
+    del a_dev
+    torch.cuda.empty_cache()
+
+    # C3 on one GPU (the 1-GPU point of the C3 scaling curve; the headline N=1 line is C2).
+    c3_1 = None
+    if world == 1 and not args.no_c3:
+        wl3 = WORKLOADS["C3"]
+        h3, _ = make_handle(sph, wl3, args, 1, 0)
+        ms3, _, _, _ = time_factor(sph, h3, wl3, args, 1, steps=2, warmup=1)
+        c3_1 = {"ms_per_step": ms3, "tflops": wl3["n"] ** 3 / 3 / (ms3 * 1e-3) / 1e12, "steps": 2, "warmup": 1,
+                "step": "generate make_spd_test_matrix tiles in place + factor", "workload": wl3["desc"]}
+        del h3
+        torch.cuda.empty_cache()
+
+    sht = sht_throughput(sph, world)
 
     if rank != 0:
         return
-    cpu_val, cores, sample, _ = cpu_cholesky_sample(n=args.ref_n) if not args.no_cpu else (None, 0, "skipped", 0)
+    cpu_val, cores, sample, _ = (cpu_cholesky_sample(n=args.ref_n, wl=wl) if not args.no_cpu
+                                 else (None, 0, "skipped", 0))
     cpu_sht = cpu_sht_sample() if not args.no_cpu else (None, 0)
     clk = clocks.summary()
+    step_desc = ("dense FP64 input resident in HBM -> tiles at storage precision (from_dense + quantize), factor"
+                 if wl["input"] == "dense" else
+                 "make_spd_test_matrix generated into the owned tiles at storage precision, factor")
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 storage (dpsp): FP64 DMMA + 3xTF32 tcgen05",
-        "data": "synthetic: make_spd_test_matrix(32400, 1) bitwise the reference generator; "
-                "SHT on random coefficients",
-        "config": {"workload": f"C2: tiled Cholesky N={n} (L=180) {VARIANT} b={b} + SHT 1000 snapshots "
-                               f"181x360 L=180", "N": n, "tile_size": b, "variant": VARIANT,
-                   "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "inputs 8.4 GB > 126 MB L2, no flush needed"},
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+        "dtype": (f"f64 compute semantics; storage {wl['variant']} ({wl['hp']} HP): FP64 DMMA, "
+                  f"{args.sp_compute} tcgen05 for SP, {wl['hp']} tcgen05 for HP"),
+        "data": f"synthetic: make_spd_test_matrix({n}, 1) bitwise the reference generator; SHT on random coefficients",
+        "config": {"workload": f"{wl['desc']} + SHT 1000 snapshots 181x360 L=180 per GPU", "N": n,
+                   "tile_size": wl["tile"], "variant": wl["variant"], "hp_format": wl["hp"],
+                   "sp_compute": args.sp_compute, "lookahead": args.lookahead,
+                   "parallelism": f"2D block-cyclic {grid[0]}x{grid[1]} (NCCL panel broadcasts)" if world > 1
+                   else "single GPU",
+                   "step": step_desc,
+                   "l2": f"tiles {8 * n * n / 2 / 1e9 / world:.1f}+ GB per GPU >> 126 MB L2, no flush needed"},
         "roofline": dom,
         "cpu_baseline": {"value": cpu_val, "unit": "TFLOP/s", "cores": cores, "kind": "port",
-                         "sample": sample,
-                         "sht_snapshots_per_s": cpu_sht[0]},
+                         "sample": sample, "sht_snapshots_per_s": cpu_sht[0]},
         "e2e": e2e,
         "sht": sht,
         "clocks": clk,
         "gpu_launches": int(launches),
-        "phases_ms_per_step": {k: v["ms"] / args.steps for k, v in phases.items()},
-        "parity": {"residual_probe": probe, "threshold": 5e-6, "ok": bool(probe < 5e-6),
-                   "what": "||(A - LL^T)x|| / ||Ax|| on 2 seeded vectors, A regenerated on device; dpsp threshold "
-                           "(acceptance_main.cpp:226)"},
-        "half_saturations": int(st.half_saturations),
+        "phases_ms_per_step_rank0": {k: v["ms"] / args.steps for k, v in phases.items()},
+        "parity": {"residual_probe": probe, "threshold": THRESH[wl["variant"]],
+                   "ok": bool(probe < THRESH[wl["variant"]]),
+                   "what": "||(A - LL^T)x|| / ||Ax|| on 2 seeded vectors, A regenerated on device; thresholds of "
+                           "acceptance_main.cpp:226"},
+        "half_saturations": sat,
     }
+    if c3_1:
+        line["c3_1gpu"] = c3_1
     print(json.dumps(line), flush=True)
 
 
@@ -346,11 +533,13 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_C2)
-    ap.add_argument("--tile", type=int, default=B_C2)
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: C2 on 1 GPU, C3 (2D block-cyclic) on more")
     ap.add_argument("--ref-n", type=int, default=8192)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c3", action="store_true", help="skip the 1-GPU C3 point on N=1")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--lookahead", type=int, default=1)
     ap.add_argument("--sp-compute", default="fp16x3", choices=["fp16x3", "tf32x3"])
     args = ap.parse_args()

@@ -100,6 +100,10 @@ int sphemu_gpu_tiled_cholesky_dense(const double* a, int where_a, int n,
                                     const sphemu_chol_config* cfg, double* factor,
                                     int where_factor, sphemu_chol_stats* stats, int* failed_tile);
 
+/* The one-shot call keeps its device buffers cached for the next call with
+ * the same n, configuration and device; this frees them. */
+int sphemu_gpu_release_cache(void);
+
 /* Device-resident factorization handle (TiledMatrix + tiled_cholesky,
  * mpchol.hpp:47-71,135): tiles live in HBM at their storage precision. */
 typedef struct sphemu_chol_s* sphemu_chol_t;
@@ -145,7 +149,8 @@ int sphemu_gpu_chol_phase_times(sphemu_chol_t h, double* ms, int64_t* counts, in
  * ms from the factorization's start. Writes min(count, cap) entries. */
 int sphemu_gpu_chol_timeline(sphemu_chol_t h, int* phase, int* stream, double* t0, double* t1, int cap,
                              int* count);
-/* Trailing-update flops by output class (2 b_i b_j b_k per GEMM, b_i^2 b_k per SYRK). */
+/* Trailing-update flops by output class (2 b_i b_j b_k per GEMM, b_i^2 b_k per SYRK),
+ * over the tiles this rank stores. */
 int sphemu_gpu_chol_update_flops(sphemu_chol_t h, double* f_dp, double* f_sp, double* f_hp);
 /* Device stream the handle enqueues on (cudaStream_t as void*). */
 void* sphemu_gpu_chol_stream(sphemu_chol_t h);

@@ -13,8 +13,10 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -295,6 +297,96 @@ struct Chol {
   std::chrono::steady_clock::time_point t_start;
   bool factored = false;
 
+  // Host I/O pipeline. Host input is streamed by tile rows (row block i
+  // needs only columns [0, (i+1) lb): the lower triangle, half the bytes)
+  // through a ring of device slabs on a copy stream, and each slab is
+  // quantized into its tiles on the main stream as soon as it lands. The
+  // factor is streamed out by tile columns on a D2H stream as soon as each
+  // column is final (after POTRF(k) + panel(k)), overlapping the rest of the
+  // factorization; host threads write the zeros above the diagonal
+  // meanwhile.
+  static constexpr int kSlabs = 3;
+  cudaStream_t cstream = nullptr, dstream = nullptr;
+  DevBuf<double> islab, oslab;
+  cudaEvent_t ev_in_full[kSlabs] = {}, ev_in_free[kSlabs] = {}, ev_col = nullptr;
+  double* hout = nullptr;
+  int64_t hldo = 0;
+  std::vector<std::thread> zeroers;
+
+  void ensure_io() {
+    if (cstream) return;
+    SPH_CUDA(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
+    SPH_CUDA(cudaStreamCreateWithFlags(&dstream, cudaStreamNonBlocking));
+    for (int s = 0; s < kSlabs; ++s) {
+      SPH_CUDA(cudaEventCreateWithFlags(&ev_in_full[s], cudaEventDisableTiming));
+      SPH_CUDA(cudaEventCreateWithFlags(&ev_in_free[s], cudaEventDisableTiming));
+    }
+    SPH_CUDA(cudaEventCreateWithFlags(&ev_col, cudaEventDisableTiming));
+  }
+
+  void load_host(const double* a, int64_t lda) {
+    ensure_io();
+    const size_t slab = static_cast<size_t>(lb) * n;
+    if (islab.n < kSlabs * slab) islab.alloc(kSlabs * slab);
+    const int prow = rank / Q, pcol = rank % Q;
+    const unsigned gy = static_cast<unsigned>(std::max(1, b * b / (256 * 64)));
+    int used = 0;
+    for (int i = 0; i < nt; ++i) {
+      if (dist() && (i % P != prow || i < pcol)) continue;  // no owned tile in this row
+      const int s = used % kSlabs;
+      if (used >= kSlabs) SPH_CUDA(cudaStreamWaitEvent(cstream, ev_in_free[s], 0));
+      double* dst = islab.get() + s * slab;
+      const int w = std::min(n, (i + 1) * lb);
+      SPH_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * n, a + static_cast<int64_t>(i) * lb * lda, sizeof(double) * lda,
+                                 sizeof(double) * w, rows(i), cudaMemcpyHostToDevice, cstream));
+      SPH_CUDA(cudaEventRecord(ev_in_full[s], cstream));
+      SPH_CUDA(cudaStreamWaitEvent(stream, ev_in_full[s], 0));
+      k_load_dense<<<dim3(static_cast<unsigned>(i + 1), gy), 256, 0, stream>>>(store(), dst, n, sat.get(),
+                                                                               static_cast<int64_t>(tix(i, 0)), i * lb);
+      SPH_LAUNCH_CHECK();
+      SPH_CUDA(cudaEventRecord(ev_in_free[s], stream));
+      ++used;
+    }
+  }
+
+  void begin_host_out(double* out, int64_t ldo) {
+    ensure_io();
+    if (oslab.n < static_cast<size_t>(n) * lb) oslab.alloc(static_cast<size_t>(n) * lb);
+    hout = out;
+    hldo = ldo;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int T = static_cast<int>(std::min(8u, std::max(1u, hw / 2)));
+    const int nn = n, l = lb;
+    for (int t = 0; t < T; ++t)
+      zeroers.emplace_back([=] {
+        for (int64_t R = t; R < nn; R += T) {
+          const int64_t c0 = (R / l + 1) * l;
+          if (c0 < nn) std::memset(out + R * ldo + c0, 0, sizeof(double) * (nn - c0));
+        }
+      });
+  }
+
+  // Column k of the factor is final on stream s: convert and copy it out.
+  void col_out(int k, cudaStream_t s) {
+    if (!hout) return;
+    SPH_CUDA(cudaEventRecord(ev_col, s));
+    SPH_CUDA(cudaStreamWaitEvent(dstream, ev_col, 0));
+    const int h = n - k * lb;
+    k_store_col<<<h, 128, 0, dstream>>>(store(), k, oslab.get());
+    SPH_LAUNCH_CHECK();
+    SPH_CUDA(cudaMemcpy2DAsync(hout + static_cast<int64_t>(k) * lb * hldo + static_cast<int64_t>(k) * lb,
+                               sizeof(double) * hldo, oslab.get(), sizeof(double) * lb, sizeof(double) * rows(k), h,
+                               cudaMemcpyDeviceToHost, dstream));
+  }
+
+  void end_host_out() {
+    for (auto& t : zeroers) t.join();
+    zeroers.clear();
+    if (!hout) return;
+    hout = nullptr;
+    SPH_CUDA(cudaStreamSynchronize(dstream));
+  }
+
   int rows(int i) const { return std::min(lb, n - i * lb); }
   size_t tix(int i, int j) const { return static_cast<size_t>(i) * (i + 1) / 2 + j; }
 
@@ -421,6 +513,16 @@ struct Chol {
   }
 
   ~Chol() {
+    for (auto& t : zeroers) t.join();
+    if (dstream) cudaStreamSynchronize(dstream);
+    if (cstream) cudaStreamSynchronize(cstream);
+    for (int s = 0; s < kSlabs; ++s) {
+      if (ev_in_full[s]) cudaEventDestroy(ev_in_full[s]);
+      if (ev_in_free[s]) cudaEventDestroy(ev_in_free[s]);
+    }
+    if (ev_col) cudaEventDestroy(ev_col);
+    if (cstream) cudaStreamDestroy(cstream);
+    if (dstream) cudaStreamDestroy(dstream);
     if (stream) cudaStreamSynchronize(stream);
     if (pstream) cudaStreamSynchronize(pstream);
     for (auto e : ev_pool) cudaEventDestroy(e);
@@ -446,18 +548,13 @@ struct Chol {
   void load_dense(const double* a, int where, int64_t lda) {
     factored = false;
     reset_flags();
-    DevBuf<double> staging;
-    const double* dptr = a;
-    if (where == SPHEMU_HOST) {
-      staging.alloc(static_cast<size_t>(n) * n);
-      SPH_CUDA(cudaMemcpy2DAsync(staging.get(), sizeof(double) * n, a, sizeof(double) * lda,
-                                 sizeof(double) * n, n, cudaMemcpyHostToDevice, stream));
-      dptr = staging.get();
-      lda = n;
-    }
     const int pl = prof_begin(kLoad);
-    k_load_dense<<<tile_grid(), 256, 0, stream>>>(store(), dptr, lda, sat.get());
-    SPH_LAUNCH_CHECK();
+    if (where == SPHEMU_HOST) {
+      load_host(a, lda);
+    } else {
+      k_load_dense<<<tile_grid(), 256, 0, stream>>>(store(), a, lda, sat.get());
+      SPH_LAUNCH_CHECK();
+    }
     k_rowexp<<<ceil_div(n, 256), 256, 0, stream>>>(store(), rowexp.get());
     SPH_LAUNCH_CHECK();
     if (dist()) SPH_NCCL(ncclAllReduce(rowexp.get(), rowexp.get(), n, ncclInt32, ncclMax, comm, stream));
@@ -544,8 +641,12 @@ struct Chol {
     } else if (!cfg.lookahead || nt == 1) {
       for (int k = 0; k < nt; ++k) {
         op_potrf(k, stream);
-        if (k + 1 >= nt) break;
+        if (k + 1 >= nt) {
+          col_out(k, stream);
+          break;
+        }
         op_panel(k, stream);
+        col_out(k, stream);
         op_update(k, 0, stream, 0);
         op_update(k, 1, stream, 0);
       }
@@ -555,12 +656,14 @@ struct Chol {
       op_potrf(0, pstream);
       op_panel(0, pstream);
       SPH_CUDA(cudaEventRecord(ev_panel[0], pstream));
+      col_out(0, pstream);
       for (int k = 0; k + 1 < nt; ++k) {
         if (k > 0) SPH_CUDA(cudaStreamWaitEvent(pstream, ev_bulk[k - 1], 0));
         op_update(k, 0, pstream, 0);
         op_potrf(k + 1, pstream);
         if (k + 2 < nt) op_panel(k + 1, pstream);
         SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
+        col_out(k + 1, pstream);
         SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k], 0));
         op_update(k, 1, stream, std::max(1, num_sms() - reserve));
         SPH_CUDA(cudaEventRecord(ev_bulk[k], stream));
@@ -727,7 +830,7 @@ struct Chol {
     DevBuf<double> staging;
     double* dptr = out;
     int64_t ld = ldo;
-    if (where == SPHEMU_HOST) {
+    if (where == SPHEMU_HOST && dist() && rank == 0) {
       staging.alloc(static_cast<size_t>(n) * n);
       dptr = staging.get();
       ld = n;
@@ -778,6 +881,11 @@ struct Chol {
       }
       SPH_CUDA(cudaStreamSynchronize(stream));
       if (rank != 0) return;
+    } else if (where == SPHEMU_HOST) {
+      begin_host_out(out, ldo);
+      for (int k = 0; k < nt; ++k) col_out(k, stream);
+      end_host_out();
+      return;
     } else {
       k_store_dense<<<grid, threads, 0, stream>>>(store(), dptr, ld);
       SPH_LAUNCH_CHECK();
@@ -850,7 +958,7 @@ struct Chol {
     for (int k = 0; k < nt; ++k)
       for (int j = k + 1; j < nt; ++j)
         for (int i = j; i < nt; ++i)
-          f[pmap[tix(i, j)]] += (i == j ? 1.0 : 2.0) * rows(i) * rows(j) * rows(k);
+          if (mine(i, j)) f[pmap[tix(i, j)]] += (i == j ? 1.0 : 2.0) * rows(i) * rows(j) * rows(k);
   }
 
   void flops(double* f) const {
@@ -895,6 +1003,31 @@ using namespace sphemu_gpu;
 struct sphemu_chol_s {
   Chol* c;
 };
+
+// One-shot calls reuse a cached handle (arena, lists, streams, slabs) while
+// n, the configuration and the device are unchanged, so repeated
+// tiled_cholesky_dense calls pay neither cudaMalloc nor cudaFree;
+// sphemu_gpu_release_cache() frees it.
+static std::mutex g_dense_mu;
+static std::unique_ptr<Chol> g_dense;
+static int g_dense_dev = -1;
+
+static bool same_config(const sphemu_chol_config& x, const sphemu_chol_config& y) {
+  return x.variant == y.variant && x.tile_size == y.tile_size && x.band_width_dp == y.band_width_dp &&
+         x.sp_fraction == y.sp_fraction && x.workers == y.workers && x.hp_format == y.hp_format &&
+         x.compute == y.compute && x.lookahead == y.lookahead && x.sp_compute == y.sp_compute;
+}
+
+static Chol& dense_handle(int n, const sphemu_chol_config& cfg) {
+  int dev = 0;
+  SPH_CUDA(cudaGetDevice(&dev));
+  if (!g_dense || g_dense->n != n || g_dense_dev != dev || !same_config(g_dense->cfg, cfg)) {
+    g_dense.reset();
+    g_dense.reset(new Chol(n, cfg));
+    g_dense_dev = dev;
+  }
+  return *g_dense;
+}
 
 extern "C" {
 
@@ -1069,13 +1202,33 @@ int sphemu_gpu_chol_update_flops(sphemu_chol_t h, double* f_dp, double* f_sp, do
 
 void* sphemu_gpu_chol_stream(sphemu_chol_t h) { return h ? h->c->stream : nullptr; }
 
+int sphemu_gpu_release_cache(void) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(g_dense_mu);
+    g_dense.reset();
+    g_dense_dev = -1;
+  });
+}
+
 int sphemu_gpu_tiled_cholesky_dense(const double* a, int where_a, int n, const sphemu_chol_config* cfg,
                                     double* factor, int where_factor, sphemu_chol_stats* stats,
                                     int* failed_tile) {
   int rc = SPHEMU_OK;
   int g = guard([&] {
-    Chol c(n, *cfg);
+    std::lock_guard<std::mutex> lk(g_dense_mu);
+    Chol& c = dense_handle(n, *cfg);
     c.load_dense(a, where_a, n);
+    const bool stream_out = where_factor == SPHEMU_HOST;
+    if (stream_out) c.begin_host_out(factor, n);
+    struct Finish {  // joins the host zero-fill threads on every exit path
+      Chol& c;
+      ~Finish() {
+        try {
+          c.end_host_out();
+        } catch (...) {
+        }
+      }
+    } finish{c};
     c.factor();
     const int f = c.wait(stats);
     if (failed_tile) *failed_tile = f;
@@ -1084,7 +1237,8 @@ int sphemu_gpu_tiled_cholesky_dense(const double* a, int where_a, int n, const s
       rc = SPHEMU_ERR_NOT_SPD;
       return;
     }
-    c.store_dense(factor, where_factor, n);
+    if (stream_out) c.end_host_out();
+    else c.store_dense(factor, where_factor, n);
   });
   return g != SPHEMU_OK ? g : rc;
 }

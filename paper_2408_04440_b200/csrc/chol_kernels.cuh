@@ -70,8 +70,11 @@ static __global__ void k_gen_spd(TileStore ts, const double* __restrict__ d, con
 }
 
 // TiledMatrix::from_dense (mpchol.cpp:124-138) + input quantization.
-static __global__ void k_load_dense(TileStore ts, const double* __restrict__ a, int64_t lda, unsigned* sat) {
-  const int64_t t = blockIdx.x;
+// t0 / row0: launch over a run of packed tiles starting at t0, reading a
+// slab whose first row is global row row0 (the streamed host input).
+static __global__ void k_load_dense(TileStore ts, const double* __restrict__ a, int64_t lda, unsigned* sat,
+                                    int64_t t0 = 0, int row0 = 0) {
+  const int64_t t = t0 + blockIdx.x;
   if (ts.off[t] < 0) return;  // tile owned by another rank
   int i, j;
   pair_from_index(t, i, j);
@@ -83,7 +86,7 @@ static __global__ void k_load_dense(TileStore ts, const double* __restrict__ a, 
        e += (int64_t)gridDim.y * blockDim.x) {
     const int r = (int)(e / b), c = (int)(e % b);
     const int R = i * ts.lb + r, Cc = j * ts.lb + c;
-    const double v = (r < ts.lb && c < ts.lb && R < ts.n && Cc < ts.n) ? a[(int64_t)R * lda + Cc] : 0.0;
+    const double v = (r < ts.lb && c < ts.lb && R < ts.n && Cc < ts.n) ? a[(int64_t)(R - row0) * lda + Cc] : 0.0;
     store_elem(tp, p, e, v, local);
   }
   flush_sat(local, sat);
@@ -101,6 +104,19 @@ static __global__ void k_store_dense(TileStore ts, double* __restrict__ out, int
     }
     out[(int64_t)R * ldo + Cc] = v;
   }
+}
+
+// Tile column k of the factor as a dense (n - k lb) x lb slab (pitch lb):
+// exact zeros above the diagonal, one CTA per output row.
+static __global__ void k_store_col(TileStore ts, int k, double* __restrict__ slab) {
+  const int R = k * ts.lb + blockIdx.x;
+  const int w = min(ts.lb, ts.n - k * ts.lb);
+  const int i = R / ts.lb;
+  const void* tp = ts.tile(i, k);
+  const int p = ts.tprec(i, k);
+  const int64_t rb = (int64_t)(R % ts.lb) * ts.b;
+  for (int c = threadIdx.x; c < w; c += blockDim.x)
+    slab[(int64_t)blockIdx.x * ts.lb + c] = (k * ts.lb + c <= R) ? load_elem(tp, p, rb + c) : 0.0;
 }
 
 // ---------------------------------------------------------------------------
