@@ -19,7 +19,7 @@ import numpy as np
 __version__ = "0.1.0"  # proj/include/sphemu/version.hpp:4
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsphemu_gpu.so")
+LIB_PATH = os.environ.get("SPHEMU_LIB") or os.path.join(_HERE, "lib", "libsphemu_gpu.so")
 
 SPHEMU_OK, SPHEMU_ERR_INVALID_ARG, SPHEMU_ERR_NOT_SPD = 0, 1, 2
 HOST, DEVICE = 0, 1

@@ -115,8 +115,8 @@ __global__ void k_rowexp(TileStore ts, int* rowexp) {
 // 2D block-cyclic exchange: a panel tile received at its storage precision
 // (xbuf slot i-k-1) -> FP64 mirror P64 and the tensor-core mirrors, exactly as
 // the owner's panel epilogue writes them. blockIdx.y indexes the import list.
-__global__ void k_panel_import(TileStore ts, int k, const int2* __restrict__ list, const uint8_t* __restrict__ xbuf,
-                               double* p64, float* p_hi, float* p_lo, uint16_t* p16, uint16_t* h_hi, uint16_t* h_lo,
+__global__ void k_panel_import(TileStore ts, int k, const int2* __restrict__ list, const int64_t* __restrict__ xoff,
+                               const uint8_t* __restrict__ xbuf, double* p64, float* p_hi, float* p_lo, uint16_t* p16, uint16_t* h_hi, uint16_t* h_lo,
                                const int* rowexp, int hp_format, const int* fail) {
   if (*(volatile const int*)fail >= 0) return;
   const int b = ts.b;
@@ -124,7 +124,7 @@ __global__ void k_panel_import(TileStore ts, int k, const int2* __restrict__ lis
   const int i = list[blockIdx.y].x;
   const int p = ts.tprec(i, k);
   const int64_t base = (int64_t)(i - k - 1) * bb;
-  const void* src = xbuf + base * 8;
+  const void* src = xbuf + xoff[blockIdx.y];
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += (int64_t)gridDim.x * blockDim.x) {
     const double x = load_elem(src, p, e);
     p64[base + e] = x;
@@ -144,6 +144,20 @@ __global__ void k_panel_import(TileStore ts, int k, const int2* __restrict__ lis
       f16_split(x, rowexp[min(i * ts.lb + r, ts.n - 1)], h_hi[base + e], h_lo[base + e]);
     }
   }
+}
+
+// Sender side of the panel exchange: the owned panel tiles of step k, at
+// storage precision, packed root-contiguously into the exchange buffer so
+// each root sends one broadcast per step.
+__global__ void k_panel_pack(TileStore ts, int k, const int2* __restrict__ list, const int64_t* __restrict__ xoff,
+                             uint8_t* __restrict__ xbuf, const int* fail) {
+  if (*(volatile const int*)fail >= 0) return;
+  const int i = list[blockIdx.y].x;
+  const int64_t words = (int64_t)ts.b * ts.b * prec_bytes(ts.tprec(i, k)) / 16;
+  const uint4* src = static_cast<const uint4*>(ts.tile(i, k));
+  uint4* dst = reinterpret_cast<uint4*>(xbuf + xoff[blockIdx.y]);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < words; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = src[e];
 }
 
 // ---- residual probe kernels -------------------------------------------------
@@ -223,9 +237,19 @@ struct Chol {
   bool dist() const { return P * Q > 1; }
   int owner(int i, int j) const { return (i % P) * Q + (j % Q); }
   bool mine(int i, int j) const { return owner(i, j) == rank; }
-  DevBuf<uint8_t> xbuf;                        // received panel tiles (storage precision)
-  DevBuf<int2> ilists;                         // per step: panel tiles owned elsewhere
-  std::vector<int64_t> ilist_off, ilist_cnt;
+  // Panel exchange buffer: per step the panel tiles at storage precision,
+  // grouped by owning rank (root) so each root broadcasts one contiguous
+  // block; xsend / ilists list this rank's packed / imported tiles with their
+  // byte offsets, xroots the (root, offset, bytes) blocks.
+  DevBuf<uint8_t> xbuf;
+  DevBuf<int2> ilists, xsend;
+  DevBuf<int64_t> ioffs, xsoffs;
+  std::vector<int64_t> ilist_off, ilist_cnt, xsend_off, xsend_cnt;
+  struct XRoot {
+    int root;
+    int64_t off, bytes;
+  };
+  std::vector<std::vector<XRoot>> xroots;
   sphemu_chol_config cfg{};
   std::vector<uint8_t> pmap, sprec;
   std::vector<int64_t> off;
@@ -428,7 +452,7 @@ struct Chol {
       o = (o + 255) & ~int64_t{255};
     }
     off.back() = o;
-    arena.alloc(static_cast<size_t>(std::max<int64_t>(o, 256)));
+    arena.alloc(static_cast<size_t>(std::max<int64_t>(o, static_cast<int64_t>(128) * b)));
     d_off.alloc(pmap.size());
     d_prec.alloc(pmap.size());
     SPH_CUDA(cudaMemcpy(d_off.get(), off.data(), pmap.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
@@ -479,24 +503,59 @@ struct Chol {
     if (dist()) {
       ilist_off.assign(nt, 0);
       ilist_cnt.assign(nt, 0);
-      std::vector<int2> il;
-      for (int k = 0; k < nt; ++k) {
+      xsend_off.assign(nt, 0);
+      xsend_cnt.assign(nt, 0);
+      xroots.assign(nt, {});
+      std::vector<int2> il, xs;
+      std::vector<int64_t> io, xo;
+      int64_t xmax = 0;
+      for (int k = 0; k + 1 < nt; ++k) {
+        std::vector<int64_t> pos(nt, 0);
+        int64_t o = 0;
+        for (int pr = 0; pr < P; ++pr) {
+          const int root = pr * Q + k % Q;
+          const int64_t start = o;
+          for (int i = k + 1; i < nt; ++i)
+            if (owner(i, k) == root) {
+              pos[i] = o;
+              o += static_cast<int64_t>(b) * b * prec_bytes(sprec[tix(i, k)]);
+            }
+          if (o > start) xroots[k].push_back({root, start, o - start});
+        }
+        xmax = std::max(xmax, o);
         ilist_off[k] = static_cast<int64_t>(il.size());
-        for (int i = k + 1; i < nt; ++i)
-          if (!mine(i, k)) il.push_back(make_int2(i, k));
+        xsend_off[k] = static_cast<int64_t>(xs.size());
+        for (int i = k + 1; i < nt; ++i) {
+          if (!mine(i, k)) {
+            il.push_back(make_int2(i, k));
+            io.push_back(pos[i]);
+          } else {
+            xs.push_back(make_int2(i, k));
+            xo.push_back(pos[i]);
+          }
+        }
         ilist_cnt[k] = static_cast<int64_t>(il.size()) - ilist_off[k];
+        xsend_cnt[k] = static_cast<int64_t>(xs.size()) - xsend_off[k];
       }
-      if (!il.empty()) {
-        ilists.alloc(il.size());
-        SPH_CUDA(cudaMemcpy(ilists.get(), il.data(), il.size() * sizeof(int2), cudaMemcpyHostToDevice));
-      }
-      if (nt > 1) xbuf.alloc(static_cast<size_t>(nt - 1) * b * b * 8);
+      auto upload = [](auto& dev, const auto& host) {
+        if (host.empty()) return;
+        dev.alloc(host.size());
+        SPH_CUDA(cudaMemcpy(dev.get(), host.data(), host.size() * sizeof(host[0]), cudaMemcpyHostToDevice));
+      };
+      upload(ilists, il);
+      upload(ioffs, io);
+      upload(xsend, xs);
+      upload(xsoffs, xo);
+      if (xmax > 0) xbuf.alloc(static_cast<size_t>(xmax));
+
     }
     rowexp.alloc(n);
     SPH_CUDA(cudaMemset(rowexp.get(), 0, n * sizeof(int)));
     if (cfg.compute == SPHEMU_COMPUTE_TENSOR && nt > 1)
-      for (int p = 0; p < 2; ++p)
+      for (int p = 0; p < 2; ++p) {
         panel_[p].alloc(nt, b, pmap, cfg.hp_format, cfg.sp_compute == SPHEMU_SP_F16X3, rowexp.get());
+        panel_[p].set_arena(arena.get(), std::max<int64_t>(o, static_cast<int64_t>(128) * b), b);
+      }
     int prio_lo = 0, prio_hi = 0;
     SPH_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     SPH_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, prio_lo));
@@ -700,21 +759,23 @@ struct Chol {
     const int set = k & 1;
     op_panel(k, s);
     const int px = prof_begin(kPanel, s);
-    SPH_NCCL(ncclGroupStart());
-    for (int i = k + 1; i < nt; ++i) {
-      const int root = owner(i, k);
-      const size_t bytes = static_cast<size_t>(b) * b * prec_bytes(sprec[tix(i, k)]);
-      uint8_t* recv = xbuf.get() + static_cast<size_t>(i - k - 1) * b * b * 8;
-      const void* send = rank == root ? static_cast<const void*>(arena.get() + off[tix(i, k)]) : recv;
-      SPH_NCCL(ncclBroadcast(send, recv, bytes, ncclUint8, root, comm, s));
+    const unsigned gx = static_cast<unsigned>(std::max(1, b * b / (256 * 16)));
+    if (xsend_cnt[k]) {
+      k_panel_pack<<<dim3(gx, static_cast<unsigned>(xsend_cnt[k])), 256, 0, s>>>(
+          store(), k, xsend.get() + xsend_off[k], xsoffs.get() + xsend_off[k], xbuf.get(), fail.get());
+      SPH_LAUNCH_CHECK();
     }
+    SPH_NCCL(ncclGroupStart());
+    for (const XRoot& x : xroots[k])
+      SPH_NCCL(ncclBroadcast(xbuf.get() + x.off, xbuf.get() + x.off, static_cast<size_t>(x.bytes), ncclUint8, x.root,
+                             comm, s));
     SPH_NCCL(ncclGroupEnd());
     note_launch();
     if (ilist_cnt[k]) {
       PanelFormats& pf = panel_[set];
       const bool tensor = cfg.compute == SPHEMU_COMPUTE_TENSOR;
-      k_panel_import<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(ilist_cnt[k])), 256, 0, s>>>(
-          store(), k, ilists.get() + ilist_off[k], xbuf.get(), p64_[set].get(), tensor ? pf.p_hi.get() : nullptr,
+      k_panel_import<<<dim3(gx, static_cast<unsigned>(ilist_cnt[k])), 256, 0, s>>>(
+          store(), k, ilists.get() + ilist_off[k], ioffs.get() + ilist_off[k], xbuf.get(), p64_[set].get(), tensor ? pf.p_hi.get() : nullptr,
           tensor ? pf.p_lo.get() : nullptr, tensor ? pf.p16.get() : nullptr,
           (tensor && pf.f16x3) ? pf.h_hi.get() : nullptr, (tensor && pf.f16x3) ? pf.h_lo.get() : nullptr,
           rowexp.get(), cfg.hp_format, fail.get());

@@ -2,11 +2,13 @@
 // classes of the Cholesky (see tc_gemm.cuh), plus the panel producers that
 // write the sender-side operand mirrors.
 //
-// CTA = 256 threads: warp 0 issues TMA, warp 1 issues tcgen05.mma (one
-// elected lane), warp 2 owns the TMEM allocation, warps 4-7 run the epilogue
-// (TMEM lane quarter = warp % 4). Two TMEM accumulators let the epilogue of
+// CTA = 384 threads: warp 0 issues TMA, warp 1 issues tcgen05.mma (one
+// elected lane), warp 2 owns the TMEM allocation, warps 4-11 run the epilogue
+// (TMEM lane quarter = warp % 4, two warps per quarter splitting the columns
+// so every SM sub-partition has two epilogue warps to hide latency). Two TMEM accumulators let the epilogue of
 // sub-tile t overlap the MMAs of sub-tile t+1. Each work item is a 128 x BN
 // sub-tile of one b x b output tile with K = b.
+#include <cstdlib>
 #include <random>
 #include <vector>
 
@@ -36,13 +38,13 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// Row-major [rows x cols] array, box = 128 bytes of K x box_rows rows, SW128.
-CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int elem_bytes, int box_rows) {
+CUtensorMap make_map_strided(const void* base, int64_t rows, int64_t cols, int64_t row_bytes, int elem_bytes,
+                             int box_rows) {
   CUtensorMap m;
   const CUtensorMapDataType dt = elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                                  : CU_TENSOR_MAP_DATA_TYPE_UINT16;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * elem_bytes};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_bytes)};
   cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / elem_bytes), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
@@ -51,7 +53,20 @@ CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int elem_byte
   if (r != CUDA_SUCCESS) throw Error(SPHEMU_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
   return m;
 }
+// Row-major [rows x cols] array, box = 128 bytes of K x box_rows rows, SW128.
+CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int elem_bytes, int box_rows) {
+  return make_map_strided(base, rows, cols, cols * elem_bytes, elem_bytes, box_rows);
+}
+
 }  // namespace
+
+// The C-operand view of the tile arena for the update epilogue: the arena
+// as [bytes / (esz b)] rows of b elements (every tile offset is a multiple
+// of esz b bytes), one map per C class width, 32-row TMA boxes.
+void PanelFormats::set_arena(const void* base, int64_t bytes, int b_) {
+  m_c16 = make_map_strided(base, bytes / (2 * b_), b_, 2 * static_cast<int64_t>(b_), 2, 32);
+  m_c32 = make_map_strided(base, bytes / (4 * b_), b_, 4 * static_cast<int64_t>(b_), 4, 32);
+}
 
 void PanelFormats::alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int hp_format_, bool f16x3_,
                          const int* rowexp_) {
@@ -87,8 +102,8 @@ void PanelFormats::alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int 
     h_lo.alloc(elems);
     m_hhi_a = make_map(h_hi.get(), rows, b, 2, TC_BM);
     m_hlo_a = make_map(h_lo.get(), rows, b, 2, TC_BM);
-    m_hhi_b = make_map(h_hi.get(), rows, b, 2, 128);
-    m_hlo_b = make_map(h_lo.get(), rows, b, 2, 128);
+    m_hhi_b = make_map(h_hi.get(), rows, b, 2, bn);
+    m_hlo_b = make_map(h_lo.get(), rows, b, 2, bn);
   }
 }
 
@@ -117,6 +132,8 @@ struct TcArgs {
   int hp_format;
   const int* fail;
   unsigned* sat;
+  int dbg;           // diagnostics only (SPHEMU_TC_DBG): 1 = skip the C epilogue, 2 = also skip the MMAs
+  int opt;           // tuning switches (SPHEMU_TC_OPT): 1 = no C prefetch to L2, 2 = prefetch two items ahead
 };
 
 template <int OPK>
@@ -129,35 +146,58 @@ struct OpTraits {
   static constexpr int kFmt = (OPK == OP_F16 || OPK == OP_F16X3) ? 0 : (OPK == OP_BF16 ? 1 : 2);
 };
 
-template <int BN, int OPK>
+// CG = 2: a CTA pair (cluster of 2) runs cta_group::2 MMAs of M = 256: each
+// CTA stages its own 128 rows of A and half of the BN rows of B per stage
+// and holds its 128 accumulator rows in its own TMEM.
+template <int BN, int OPK, int MODE, int CG = 1>
 struct TcLayout {
   using T = OpTraits<OPK>;
+  static constexpr bool kUpd = (MODE == MODE_UPDATE);
   static constexpr int kA = TC_BM * 128;          // bytes of one A buffer
-  static constexpr int kB = BN * 128;             // bytes of one B buffer
+  static constexpr int kB = (BN / CG) * 128;      // bytes of one B buffer (this CTA's rows)
   static constexpr int kStage = (T::kSplit ? 2 : 1) * (kA + kB);
-  static constexpr int kStages = (T::kSplit ? 3 : 4);
-  static constexpr int kSmem = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
+  // Update mode stages the C tile through shared memory: per epilogue warp
+  // a ring of kRing TMA boxes (32 rows x 128 bytes each).
+#ifndef SPH_TC_RING
+#define SPH_TC_RING 1
+#endif
+#ifndef SPH_TC_RING2
+#define SPH_TC_RING2 3
+#endif
+  static constexpr int kRing = kUpd ? ((CG == 2 && !T::kSplit) ? SPH_TC_RING2 : SPH_TC_RING) : 0;
+  static constexpr int kStages = (232448 - 1536 - TC_EPI_WARPS * kRing * 32 * 128) / kStage > 6
+                                     ? 6
+                                     : (232448 - 1536 - TC_EPI_WARPS * kRing * 32 * 128) / kStage;
+  static constexpr int kCBox = 32 * 128;
+  static constexpr int kCBytes = TC_EPI_WARPS * kRing * kCBox;
+  static constexpr int kSmem = kStages * kStage + kCBytes + 1024 /*align*/ + 512 /*barriers*/;
   static constexpr int kTmemCols = 2 * BN;        // double-buffered accumulator
+  static_assert(kSmem <= 232448, "shared memory budget");
 };
 
-template <int BN, int OPK, int MODE>
-__global__ void __launch_bounds__(256, 1)
+template <int BN, int OPK, int MODE, int CG>
+__global__ void __launch_bounds__(TC_THREADS, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
               const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo,
-              const TcArgs args) {
+              const __grid_constant__ CUtensorMap mC, const TcArgs args) {
   using T = OpTraits<OPK>;
-  using Lay = TcLayout<BN, OPK>;
+  using Lay = TcLayout<BN, OPK, MODE, CG>;
+  static_assert(CG == 1 || MODE == MODE_UPDATE, "CTA pairs run the trailing update only");
   constexpr int S = Lay::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Lay::kStage);
+  uint8_t* cbuf = smem + S * Lay::kStage;  // 1024-aligned (stages are multiples of 1024 bytes)
+  uint64_t* full = reinterpret_cast<uint64_t*>(cbuf + Lay::kCBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* cfull = tempty + 2;  // [epilogue warp][kRing]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cfull + TC_EPI_WARPS * Lay::kRing);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (*(volatile const int*)args.fail >= 0) return;  // an earlier POTRF failed
+  if (*(volatile const int*)args.fail >= 0) return;  // an earlier POTRF failed (both CTAs of a pair see it)
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // 0 = pair leader (issues the MMAs)
+  const int64_t cid = blockIdx.x / CG, ncl = gridDim.x / CG;  // work is strided over clusters
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -166,21 +206,27 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], CG * TC_EPI_WARPS);  // one arrive per epilogue warp of each CTA
     }
+    for (int s = 0; s < TC_EPI_WARPS * Lay::kRing; ++s) mbar_init(&cfull[s], 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mA_hi);
     tma_prefetch(&mB_hi);
+    if (MODE == MODE_UPDATE) tma_prefetch(&mC);
     if (T::kSplit) {
       tma_prefetch(&mA_lo);
       tma_prefetch(&mB_lo);
     }
   }
-  if (warp == 2) tmem_alloc(tmem_holder, Lay::kTmemCols);
+  if (warp == 2) {
+    if constexpr (CG == 2) tmem_alloc_cg2(tmem_holder, Lay::kTmemCols);
+    else tmem_alloc(tmem_holder, Lay::kTmemCols);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
@@ -192,7 +238,7 @@ __global__ void __launch_bounds__(256, 1)
     const int sub = static_cast<int>(w % args.sub_per);
     i = ij.x;
     j = ij.y;
-    m0 = (sub / args.sub_n) * TC_BM;
+    m0 = (sub / args.sub_n) * (TC_BM * CG) + static_cast<int>(rank) * TC_BM;
     n0 = (sub % args.sub_n) * BN;
   };
 
@@ -201,21 +247,52 @@ __global__ void __launch_bounds__(256, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+      // Update mode: pull the C sub-tile of the next work item into L2 while
+      // this one's MMAs run, so the epilogue's C loads hit L2 instead of
+      // waiting on HBM latency.
+      auto prefetch_c = [&](int64_t wi) {
+        if (MODE != MODE_UPDATE || args.dbg == 1 || args.dbg == 2 || args.dbg == 5 || (args.opt & 1) || wi >= items)
+          return;
+        constexpr int kEszP = T::kSplit ? 4 : 2;
+        int ti, tj, tm, tn;
+        decode(wi, ti, tj, tm, tn);
+        const int row = static_cast<int>(args.ts.off[args.ts.idx(ti, tj)] / (static_cast<int64_t>(kEszP) * args.b));
+#pragma unroll 1
+        for (int rq = 0; rq < TC_BM; rq += 32)
+#pragma unroll 1
+          for (int cx = 0; cx < BN; cx += 128 / kEszP) tma_prefetch_l2_2d(&mC, tn + cx, row + tm + rq);
+      };
+      prefetch_c(cid);
+      if (args.opt & 2) prefetch_c(cid + ncl);
+      for (int64_t w = cid; w < items; w += ncl) {
         int i, j, m0, n0;
         decode(w, i, j, m0, n0);
+        prefetch_c(w + ((args.opt & 2) ? 2 : 1) * ncl);
         const int a_row = (i - args.k - 1) * args.b + m0;
-        const int b_row = (MODE == MODE_UPDATE) ? (j - args.k - 1) * args.b + n0 : n0;
+        const int b_row = (MODE == MODE_UPDATE) ? (j - args.k - 1) * args.b + n0 + static_cast<int>(rank) * (BN / CG)
+                                                : n0;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * Lay::kStage;
-          mbar_arrive_expect_tx(&full[stage], Lay::kStage);
           const int kx = kb * T::kBK;
-          tma_load_2d(&mA_hi, &full[stage], st, kx, a_row);
-          tma_load_2d(&mB_hi, &full[stage], st + Lay::kA, kx, b_row);
-          if (T::kSplit) {
-            tma_load_2d(&mA_lo, &full[stage], st + Lay::kA + Lay::kB, kx, a_row);
-            tma_load_2d(&mB_lo, &full[stage], st + 2 * Lay::kA + Lay::kB, kx, b_row);
+          if constexpr (CG == 2) {
+            // both CTAs' bytes complete on the leader's full barrier
+            const uint32_t fb = mapa_shared(&full[stage], 0);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], CG * Lay::kStage);
+            tma_load_2d_cg2(&mA_hi, fb, st, kx, a_row);
+            tma_load_2d_cg2(&mB_hi, fb, st + Lay::kA, kx, b_row);
+            if (T::kSplit) {
+              tma_load_2d_cg2(&mA_lo, fb, st + Lay::kA + Lay::kB, kx, a_row);
+              tma_load_2d_cg2(&mB_lo, fb, st + 2 * Lay::kA + Lay::kB, kx, b_row);
+            }
+          } else {
+            mbar_arrive_expect_tx(&full[stage], Lay::kStage);
+            tma_load_2d(&mA_hi, &full[stage], st, kx, a_row);
+            tma_load_2d(&mB_hi, &full[stage], st + Lay::kA, kx, b_row);
+            if (T::kSplit) {
+              tma_load_2d(&mA_lo, &full[stage], st + Lay::kA + Lay::kB, kx, a_row);
+              tma_load_2d(&mB_lo, &full[stage], st + 2 * Lay::kA + Lay::kB, kx, b_row);
+            }
           }
           if (++stage == S) {
             stage = 0;
@@ -224,21 +301,24 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ===== MMA issuer (single thread) =====
-    constexpr uint32_t idesc = umma_idesc(T::kFmt, TC_BM, BN);
+  } else if (warp == 1 && rank == 0) {
+    // ===== MMA issuer (single thread; the pair leader for CG = 2) =====
+    constexpr uint32_t idesc = umma_idesc(T::kFmt, TC_BM * CG, BN);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+    for (int64_t w = cid; w < items; w += ncl) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + acc * BN;
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        if (lane == 0) {
+        if (lane == 0 && args.dbg == 2) {
+          if constexpr (CG == 2) umma_commit_cg2(&empty[stage]);
+          else umma_commit(&empty[stage]);
+        } else if (lane == 0) {
           uint8_t* st = smem + stage * Lay::kStage;
           const uint64_t a_hi = umma_desc_sw128(st);
           const uint64_t b_hi = umma_desc_sw128(st + Lay::kA);
@@ -252,17 +332,26 @@ __global__ void __launch_bounds__(256, 1)
               umma_tf32(d, a_lo + koff, b_hi + koff, idesc, accum);
               umma_tf32(d, a_hi + koff, b_lo + koff, idesc, 1u);
               umma_tf32(d, a_hi + koff, b_hi + koff, idesc, 1u);
+            } else if constexpr (T::kSplit && CG == 2) {
+              const uint64_t a_lo = umma_desc_sw128(st + Lay::kA + Lay::kB);
+              const uint64_t b_lo = umma_desc_sw128(st + 2 * Lay::kA + Lay::kB);
+              umma_f16_cg2(d, a_lo + koff, b_hi + koff, idesc, accum);
+              umma_f16_cg2(d, a_hi + koff, b_lo + koff, idesc, 1u);
+              umma_f16_cg2(d, a_hi + koff, b_hi + koff, idesc, 1u);
             } else if constexpr (T::kSplit) {
               const uint64_t a_lo = umma_desc_sw128(st + Lay::kA + Lay::kB);
               const uint64_t b_lo = umma_desc_sw128(st + 2 * Lay::kA + Lay::kB);
               umma_f16(d, a_lo + koff, b_hi + koff, idesc, accum);
               umma_f16(d, a_hi + koff, b_lo + koff, idesc, 1u);
               umma_f16(d, a_hi + koff, b_hi + koff, idesc, 1u);
+            } else if constexpr (CG == 2) {
+              umma_f16_cg2(d, a_hi + koff, b_hi + koff, idesc, accum);
             } else {
               umma_f16(d, a_hi + koff, b_hi + koff, idesc, accum);
             }
           }
-          umma_commit(&empty[stage]);
+          if constexpr (CG == 2) umma_commit_cg2(&empty[stage]);
+          else umma_commit(&empty[stage]);
         }
         __syncwarp();
         if (++stage == S) {
@@ -270,7 +359,10 @@ __global__ void __launch_bounds__(256, 1)
           phase ^= 1;
         }
       }
-      if (lane == 0) umma_commit(&tfull[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) umma_commit_cg2(&tfull[acc]);
+        else umma_commit(&tfull[acc]);
+      }
       __syncwarp();
       if (++acc == 2) {
         acc = 0;
@@ -279,103 +371,161 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ===== epilogue: TMEM -> registers -> tile storage (+ panel mirrors) =====
-    const int q = warp - 4;  // TMEM lane quarter
+    const int q = warp & 3;         // TMEM lane quarter (hardware: warp % 4)
+    const int grp = (warp - 4) >> 2;  // two warps per quarter split the columns
     const int row_in = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
     unsigned sat_local = 0;
     const int b = args.b;
-    for (int64_t w = blockIdx.x; w < items; w += gridDim.x) {
+    // Update-mode C staging (see below): box geometry and the load ring.
+    constexpr int kEsz = T::kSplit ? 4 : 2;        // storage bytes of the C class (SP fp32, HP 16-bit)
+    constexpr int kBoxCols = 128 / kEsz;           // columns per 128-byte box row
+    constexpr int kNBox = BN / kBoxCols / 2;       // boxes per warp per work item (box grp + 2 bx)
+    constexpr int R = Lay::kRing > 0 ? Lay::kRing : 1;
+    uint8_t* cring = cbuf + (warp - 4) * R * Lay::kCBox;
+    uint64_t* cf = cfull + (warp - 4) * R;
+    int64_t gbox = 0, gissue = 0;  // next box to process / to load (sequence over this CTA's items)
+    auto c_row = [&](int ti, int tj) {  // first row of tile (ti, tj) in the arena viewed as [rows x b]
+      return static_cast<int>(args.ts.off[args.ts.idx(ti, tj)] / (static_cast<int64_t>(kEsz) * b));
+    };
+    auto issue_c = [&]() {  // lane 0: TMA-load the next C box into its ring slot
+      const int64_t wi = cid + (gissue / kNBox) * ncl;
+      if (wi >= items) return;
+      const int bx = grp + 2 * static_cast<int>(gissue % kNBox);
+      int ti, tj, tm, tn;
+      decode(wi, ti, tj, tm, tn);
+      const int slot = static_cast<int>(gissue % R);
+      mbar_arrive_expect_tx(&cf[slot], Lay::kCBox);
+      tma_load_2d(&mC, &cf[slot], cring + slot * Lay::kCBox, tn + bx * kBoxCols, c_row(ti, tj) + tm + q * 32);
+      ++gissue;
+    };
+    if (MODE == MODE_UPDATE && lane == 0 && (args.dbg == 0 || args.dbg >= 3) && args.dbg != 5)
+      for (int s = 0; s < R; ++s) issue_c();
+    for (int64_t w = cid; w < items; w += ncl) {
       int i, j, m0, n0;
       decode(w, i, j, m0, n0);
-      const int r = m0 + row_in;
       void* tp = args.ts.tile(i, j);
       const int p = args.ts.tprec(i, j);
-      const int64_t prow = (int64_t)(i - args.k - 1) * b + r;
-      // Update mode: fetch this thread's C row segment (BN values) before the
-      // accumulator is ready, so the HBM latency hides under the MMAs.
-      // uint4 words per row segment: fp32 C for the split (SP) kinds, fp16 C otherwise
-      constexpr int kCWords = (MODE == MODE_UPDATE) ? (T::kSplit ? BN / 4 : BN / 8) : 1;
-      uint4 cpre[kCWords];
       if constexpr (MODE == MODE_UPDATE) {
-        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const char*>(tp) +
-                                                          ((int64_t)r * b + n0) * prec_bytes(p));
-        const int words = T::kSplit ? BN / 4 : BN / 8;
+        // C = round_p(C - acc). The C sub-tile streams through shared
+        // memory by TMA: each epilogue warp owns a ring of kRing boxes of
+        // 32 rows x 128 bytes (its TMEM lane quarter); loads run kRing - 1
+        // boxes ahead (across work items), results go back in place and
+        // leave by TMA store. Thread t handles row t of the box, reading
+        // the 128B-swizzled row conflict-free. Element arithmetic: one
+        // correctly rounded fp32 subtraction (== the FP64 subtract + round
+        // of mpchol.cpp:311-312 up to the rare double-rounding tie), then
+        // the storage rounding.
+        // HP tiles of an F16 launch are fp16, of a BF16 launch bf16 (one class per launch).
+        constexpr bool kBf = (OPK == OP_BF16);
+        constexpr float kThr = kBf ? 3.3961514e38f : 65520.0f;
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+#pragma unroll 1
+        for (int bl = 0; bl < ((args.dbg == 1 || args.dbg == 2) ? 0 : kNBox); ++bl, ++gbox) {
+          const int bx = grp + 2 * bl;
+          const int slot = static_cast<int>(gbox % R);
+          if (args.dbg != 5) mbar_wait(&cf[slot], static_cast<uint32_t>((gbox / R) & 1));
+          const uint32_t row_s = smem_addr(cring + slot * Lay::kCBox) + lane * 128;
 #pragma unroll
-        for (int u = 0; u < kCWords; ++u)
-          if (u < words) cpre[u] = src[u];
-      }
+          for (int h = 0; h < (args.dbg == 3 ? 0 : kBoxCols / 32); ++h) {
+            uint32_t v[32];
+            tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + bx * kBoxCols + h * 32, v);
+            if constexpr (OPK == OP_F16X3) {
+              // operands were scaled by 2^e_row: undo exactly (powers of two)
+              const int er = args.rowexp[min(i * args.lb + m0 + row_in, args.ts.n - 1)];
+              const int cbase = j * args.lb + n0 + bx * kBoxCols + h * 32;
+              const float rs = __int_as_float((127 - er) << 23);
+#pragma unroll
+              for (int t = 0; t < 32; ++t) {
+                const int ec = __ldg(args.rowexp + min(cbase + t, args.ts.n - 1));
+                v[t] = __float_as_uint(__uint_as_float(v[t]) * (rs * __int_as_float((127 - ec) << 23)));
+              }
+            }
+            if constexpr (kEsz == 4) {
+#pragma unroll
+              for (int cc = 0; cc < 8; ++cc) {
+                const uint32_t ptr = row_s + ((cc ^ (lane & 7)) << 4);
+                uint4 cv = lds128(ptr);
+                cv.x = __float_as_uint(__fsub_rn(__uint_as_float(cv.x), __uint_as_float(v[4 * cc + 0])));
+                cv.y = __float_as_uint(__fsub_rn(__uint_as_float(cv.y), __uint_as_float(v[4 * cc + 1])));
+                cv.z = __float_as_uint(__fsub_rn(__uint_as_float(cv.z), __uint_as_float(v[4 * cc + 2])));
+                cv.w = __float_as_uint(__fsub_rn(__uint_as_float(cv.w), __uint_as_float(v[4 * cc + 3])));
+                sts128(ptr, cv);
+              }
+            } else {
+              // HP class: packed pairs, cvt.rn.satfinite clamps to +-max
+              // finite exactly like half.hpp's saturation; values whose RNE
+              // result would overflow are counted (|x| >= 65520 for fp16,
+              // >= bf16's rounding threshold for bf16).
+#pragma unroll
+              for (int cc = 0; cc < 4; ++cc) {
+                const uint32_t ptr = row_s + (((h * 4 + cc) ^ (lane & 7)) << 4);
+                uint4 raw = lds128(ptr);
+                uint32_t* w2 = reinterpret_cast<uint32_t*>(&raw);
+                float x[8];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  if constexpr (!kBf) {
+                    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w2[u]));
+                    x[2 * u] = f.x;
+                    x[2 * u + 1] = f.y;
+                  } else {
+                    x[2 * u] = __uint_as_float(w2[u] << 16);
+                    x[2 * u + 1] = __uint_as_float(w2[u] & 0xffff0000u);
+                  }
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) x[e] = __fsub_rn(x[e], __uint_as_float(v[8 * cc + e]));
+                // saturation count: one max-tree per 8 values, exact count only when one overflows
+                const float m01 = fmaxf(fabsf(x[0]), fabsf(x[1])), m23 = fmaxf(fabsf(x[2]), fabsf(x[3]));
+                const float m45 = fmaxf(fabsf(x[4]), fabsf(x[5])), m67 = fmaxf(fabsf(x[6]), fabsf(x[7]));
+                if (fmaxf(fmaxf(m01, m23), fmaxf(m45, m67)) >= kThr) {
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) sat_local += fabsf(x[e]) >= kThr;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  uint32_t packed;
+                  if constexpr (!kBf)
+                    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(packed) : "f"(x[2 * u + 1]), "f"(x[2 * u]));
+                  else
+                    asm("cvt.rn.satfinite.bf16x2.f32 %0, %1, %2;" : "=r"(packed) : "f"(x[2 * u + 1]), "f"(x[2 * u]));
+                  w2[u] = packed;
+                }
+                sts128(ptr, raw);
+              }
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            int bi, bj, bm, bn;
+            decode(w, bi, bj, bm, bn);
+            if (args.dbg != 3 && args.dbg != 4)
+              tma_store_2d(&mC, cring + slot * Lay::kCBox, bn + bx * kBoxCols, c_row(bi, bj) + bm + q * 32);
+            bulk_commit();
+            if (R == 1) {
+              bulk_wait_read0();  // the single slot is free again
+              issue_c();
+            } else if (gbox >= 1) {
+              bulk_wait_read1();  // box gbox-1 has left its slot: refill it
+              issue_c();
+            }
+          }
+          __syncwarp();
+        }
+      } else {
+      const int r = m0 + row_in;
+      const int64_t prow = (int64_t)(i - args.k - 1) * b + r;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-#pragma unroll(MODE == MODE_UPDATE ? BN / 32 : 1)
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = 32 * grp; c0 < BN; c0 += 64) {
         uint32_t v[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c0, v);
         const int64_t e0 = (int64_t)r * b + n0 + c0;
-        if constexpr (MODE == MODE_UPDATE) {
-          // C = round_p(C - acc): one correctly rounded fp32 subtraction per
-          // element (== the FP64 subtract + round of mpchol.cpp:311-312 up to
-          // the rare double-rounding tie), then the storage rounding.
-          if constexpr (OPK == OP_F16X3) {
-            // operands were scaled by 2^e_row: undo exactly (powers of two)
-            const int er = args.rowexp[min(i * args.lb + r, args.ts.n - 1)];
-            const int cbase = j * args.lb + n0 + c0;
-            const float rs = __int_as_float((127 - er) << 23);
-#pragma unroll
-            for (int t = 0; t < 32; ++t) {
-              const int ec = __ldg(args.rowexp + min(cbase + t, args.ts.n - 1));
-              v[t] = __float_as_uint(__uint_as_float(v[t]) * (rs * __int_as_float((127 - ec) << 23)));
-            }
-          }
-          if (p == kSP) {
-            float4* cp = reinterpret_cast<float4*>(static_cast<float*>(tp) + e0);
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-              const uint4 pre = cpre[(MODE == MODE_UPDATE) ? (c0 / 4 + t) % kCWords : 0];
-              float4 cv = make_float4(__uint_as_float(pre.x), __uint_as_float(pre.y), __uint_as_float(pre.z),
-                                      __uint_as_float(pre.w));
-              cv.x = __fsub_rn(cv.x, __uint_as_float(v[4 * t + 0]));
-              cv.y = __fsub_rn(cv.y, __uint_as_float(v[4 * t + 1]));
-              cv.z = __fsub_rn(cv.z, __uint_as_float(v[4 * t + 2]));
-              cv.w = __fsub_rn(cv.w, __uint_as_float(v[4 * t + 3]));
-              cp[t] = cv;
-            }
-          } else {
-            // HP class: packed pairs, cvt.rn.satfinite clamps to +-max finite
-            // exactly like half.hpp's saturation; values whose RNE result
-            // would overflow are counted (|x| >= 65520 for fp16, >= bf16's
-            // rounding threshold for bf16).
-            uint16_t* cp = static_cast<uint16_t*>(tp) + e0;
-            const float thr = p == kHP ? 65520.0f : 3.3961514e38f;
-#pragma unroll
-            for (int t = 0; t < 32; t += 8) {
-              uint4 raw = cpre[(MODE == MODE_UPDATE) ? ((c0 + t) / 8) % kCWords : 0];
-              uint32_t* w2 = reinterpret_cast<uint32_t*>(&raw);
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                float lo, hi;
-                if (p == kHP) {
-                  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w2[u]));
-                  lo = f.x;
-                  hi = f.y;
-                } else {
-                  lo = __uint_as_float(w2[u] << 16);
-                  hi = __uint_as_float(w2[u] & 0xffff0000u);
-                }
-                lo = __fsub_rn(lo, __uint_as_float(v[t + 2 * u]));
-                hi = __fsub_rn(hi, __uint_as_float(v[t + 2 * u + 1]));
-                sat_local += (fabsf(lo) >= thr) + (fabsf(hi) >= thr);
-                uint32_t packed;
-                if (p == kHP)
-                  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(packed) : "f"(hi), "f"(lo));
-                else
-                  asm("cvt.rn.satfinite.bf16x2.f32 %0, %1, %2;" : "=r"(packed) : "f"(hi), "f"(lo));
-                w2[u] = packed;
-              }
-              *reinterpret_cast<uint4*>(cp + t) = raw;
-            }
-          }
-        } else {
+        {
           // Panel: X = B * Linv^T rounded through p(i, k); write the tile, the
           // FP64 mirror and the tensor mirrors, 8 columns (>= 32 B) per store.
 #pragma unroll
@@ -435,18 +585,29 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
       }
+      }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) {  // this warp is done with the accumulator (the leader's barrier for a pair)
+        if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (MODE == MODE_UPDATE && lane == 0) bulk_wait_all();
     sat_local = warp_sum_u32(sat_local);
     if (lane == 0 && sat_local) atomicAdd(args.sat, sat_local);
   }
   __syncthreads();
-  if (warp == 2) tmem_dealloc(tmem_base, Lay::kTmemCols);
+  if constexpr (CG == 2) {
+    cluster_sync_all();  // both CTAs are done with the pair's TMEM
+    if (warp == 2) tmem_dealloc_cg2(tmem_base, Lay::kTmemCols);
+  } else {
+    if (warp == 2) tmem_dealloc(tmem_base, Lay::kTmemCols);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -534,19 +695,35 @@ __global__ void __launch_bounds__(DG_THREADS) k_panel_trsm_fp64_list(TileStore t
 // ---------------------------------------------------------------------------
 namespace {
 
-template <int BN, int OPK, int MODE>
+template <int BN, int OPK, int MODE, int CG = 1>
 void launch_tc(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi,
-               const CUtensorMap& b_lo, TcArgs args, cudaStream_t s, int max_ctas = 0) {
-  using Lay = TcLayout<BN, OPK>;
-  auto kern = k_tc_gemm<BN, OPK, MODE>;
+               const CUtensorMap& b_lo, const CUtensorMap& c_map, TcArgs args, cudaStream_t s, int max_ctas = 0) {
+  using Lay = TcLayout<BN, OPK, MODE, CG>;
+  auto kern = k_tc_gemm<BN, OPK, MODE, CG>;
   static bool attr = false;
   if (!attr) {
     SPH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::kSmem));
     attr = true;
   }
-  const int cap = max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms();
-  const int grid = static_cast<int>(std::min<int64_t>(args.items, cap));
-  kern<<<grid, 256, Lay::kSmem, s>>>(a_hi, a_lo, b_hi, b_lo, args);
+  const int cap = (max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms()) / CG;
+  const int grid = CG * static_cast<int>(std::min<int64_t>(args.items, std::max(1, cap)));
+  if constexpr (CG == 1) {
+    kern<<<grid, TC_THREADS, Lay::kSmem, s>>>(a_hi, a_lo, b_hi, b_lo, c_map, args);
+  } else {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(TC_THREADS);
+    lc.dynamicSmemBytes = Lay::kSmem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CG;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    SPH_CUDA(cudaLaunchKernelEx(&lc, kern, a_hi, a_lo, b_hi, b_lo, c_map, args));
+  }
   SPH_LAUNCH_CHECK();
 }
 
@@ -596,7 +773,7 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
     a.hp_format = pf.hp_format;
     a.fail = fail;
     a.sat = sat;
-    launch_tc<128, OP_TF32X3, MODE_PANEL>(pf.m_inhi_a, pf.m_inlo_a, pf.m_lhi_b, pf.m_llo_b, a, s);
+    launch_tc<128, OP_TF32X3, MODE_PANEL>(pf.m_inhi_a, pf.m_inlo_a, pf.m_lhi_b, pf.m_llo_b, pf.m_lhi_b, a, s);
   }
 }
 
@@ -614,28 +791,60 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
   a.sat = sat;
   a.rowexp = pf.rowexp;
   a.lb = ts.lb;
+  static const int dbg = [] {
+    const char* e = std::getenv("SPHEMU_TC_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.dbg = dbg;
+  static const int opt = [] {
+    const char* e = std::getenv("SPHEMU_TC_OPT");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.opt = opt;
+  // CTA pairs (cta_group::2, M = 256) for the 256-wide kinds with
+  // SPHEMU_TC_CG=2. Bitwise identical results; measured slower than single
+  // CTAs at b = 512 (the update is bound by the C-tile epilogue, which pairs
+  // do not shrink, and the pair's C ring costs mainloop stages), so off by
+  // default.
+  static const int cg_env = [] {
+    const char* e = std::getenv("SPHEMU_TC_CG");
+    return e ? std::atoi(e) : 1;
+  }();
+  const bool pair = cg_env == 2 && pf.bn == 256;
   if (cls == SPHEMU_PREC_SP) {
-    a.sub_n = ts.b / 128;
-    a.sub_per = (ts.b / TC_BM) * a.sub_n;
+    a.sub_n = ts.b / (pf.f16x3 ? pf.bn : 128);
+    a.sub_per = (ts.b / (TC_BM * (pair && pf.f16x3 ? 2 : 1))) * a.sub_n;
     a.items = cnt * a.sub_per;
-    if (pf.f16x3)
-      launch_tc<128, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_b, pf.m_hlo_b, a, s, max_ctas);
+    if (pf.f16x3 && pair)
+      launch_tc<256, OP_F16X3, MODE_UPDATE, 2>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_a, pf.m_hlo_a, pf.m_c32, a, s,
+                                               max_ctas);
+    else if (pf.f16x3 && pf.bn == 256)
+      launch_tc<256, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_b, pf.m_hlo_b, pf.m_c32, a, s, max_ctas);
+    else if (pf.f16x3)
+      launch_tc<128, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_b, pf.m_hlo_b, pf.m_c32, a, s, max_ctas);
     else
-      launch_tc<128, OP_TF32X3, MODE_UPDATE>(pf.m_phi_a, pf.m_plo_a, pf.m_phi_b, pf.m_plo_b, a, s, max_ctas);
+      launch_tc<128, OP_TF32X3, MODE_UPDATE>(pf.m_phi_a, pf.m_plo_a, pf.m_phi_b, pf.m_plo_b, pf.m_c32, a, s, max_ctas);
   } else {
     a.sub_n = ts.b / pf.bn;
-    a.sub_per = (ts.b / TC_BM) * a.sub_n;
+    a.sub_per = (ts.b / (TC_BM * (pair ? 2 : 1))) * a.sub_n;
     a.items = cnt * a.sub_per;
-    if (pf.bn == 256) {
+    if (pair) {
       if (hp_format == SPHEMU_HP_BF16)
-        launch_tc<256, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s, max_ctas);
+        launch_tc<256, OP_BF16, MODE_UPDATE, 2>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s,
+                                                max_ctas);
       else
-        launch_tc<256, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s, max_ctas);
+        launch_tc<256, OP_F16, MODE_UPDATE, 2>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s,
+                                               max_ctas);
+    } else if (pf.bn == 256) {
+      if (hp_format == SPHEMU_HP_BF16)
+        launch_tc<256, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas);
+      else
+        launch_tc<256, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas);
     } else {
       if (hp_format == SPHEMU_HP_BF16)
-        launch_tc<128, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s, max_ctas);
+        launch_tc<128, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas);
       else
-        launch_tc<128, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, a, s, max_ctas);
+        launch_tc<128, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas);
     }
   }
 }

@@ -19,6 +19,8 @@
 namespace sphemu_gpu {
 
 constexpr int TC_BM = 128;
+constexpr int TC_EPI_WARPS = 8;                  // epilogue warps 4 .. 11
+constexpr int TC_THREADS = 32 * (4 + TC_EPI_WARPS);
 
 // Tensor-core operand mirrors of the current panel (rows (i-k-1)*b + r).
 struct PanelFormats {
@@ -35,6 +37,8 @@ struct PanelFormats {
   const int* rowexp = nullptr;
   DevBuf<uint16_t> h_hi, h_lo;
   CUtensorMap m_hhi_a, m_hlo_a, m_hhi_b, m_hlo_b;
+  CUtensorMap m_c16{}, m_c32{};  // C operand: the tile arena as 16-bit / fp32 rows (set_arena)
+  void set_arena(const void* base, int64_t bytes, int b_);
   int bn = 256;
   void alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int hp_format_, bool f16x3_,
              const int* rowexp_);
