@@ -262,6 +262,7 @@ struct Chol {
   DevBuf<int> fail;
   DevBuf<unsigned> sat;
   DevBuf<int2> lists;
+  DevBuf<int> lrows;  // per update-list entry: the C tile's arena row (see constructor)
   // Update lists per (step k, part, class): part 0 = next column (k+1, the
   // critical chain), part 1 = the rest (columns >= k+2, the bulk).
   std::vector<int64_t> list_off, list_cnt;  // [(k * 2 + part) * 3 + class]
@@ -482,6 +483,15 @@ struct Chol {
     if (!all.empty()) {
       lists.alloc(all.size());
       SPH_CUDA(cudaMemcpy(lists.get(), all.data(), all.size() * sizeof(int2), cudaMemcpyHostToDevice));
+      // Per entry: the tile's first row in the arena viewed as rows of b
+      // elements at the tile's storage width (the update kernels' C operand).
+      std::vector<int> rowsv(all.size());
+      for (size_t e = 0; e < all.size(); ++e) {
+        const size_t t = tix(all[e].x, all[e].y);
+        rowsv[e] = static_cast<int>(off[t] / (static_cast<int64_t>(prec_bytes(sprec[t])) * b));
+      }
+      lrows.alloc(rowsv.size());
+      SPH_CUDA(cudaMemcpy(lrows.get(), rowsv.data(), rowsv.size() * sizeof(int), cudaMemcpyHostToDevice));
     }
     plist_off.assign(nt, 0);
     plist_dp.assign(nt, 0);
@@ -658,8 +668,8 @@ struct Chol {
       const int2* lst = lists.get() + list_off[slot];
       const int pu = prof_begin(kUpdDp + cls, s);
       if (cls != SPHEMU_PREC_DP && cfg.compute == SPHEMU_COMPUTE_TENSOR) {
-        tc_update(store(), k, cls, cfg.hp_format, lst, cnt, p64_[set].get(), panel_[set], fail.get(), sat.get(), s,
-                  max_ctas);
+        tc_update(store(), k, cls, cfg.hp_format, lst, lrows.get() + list_off[slot], cnt, p64_[set].get(),
+                  panel_[set], fail.get(), sat.get(), s, max_ctas);
       } else {
         if (b % D2_BM == 0) {
           static bool attr = false;

@@ -90,6 +90,37 @@ __device__ __forceinline__ void pc_mm(FA fa, FB fb, FO fo) {
   __syncthreads();
 }
 
+// The same product on the FP64 tensor pipe: m8n8k4 DMMA tiles, the four
+// warps splitting the (N/8)^2 output tiles.
+template <int N, class FA, class FB, class FO>
+__device__ __forceinline__ void pc_mm_t(FA fa, FB fb, FO fo) {
+  constexpr int TPW = (N / 8) * (N / 8) / 4;
+  static_assert(TPW >= 1, "N >= 16");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lr = lane >> 2, lk = lane & 3;
+  double acc[TPW][2];
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) acc[u][0] = acc[u][1] = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; k += 4) {
+#pragma unroll
+    for (int u = 0; u < TPW; ++u) {
+      const int tile = warp * TPW + u;
+      const int tr = (tile / (N / 8)) * 8, tc = (tile % (N / 8)) * 8;
+      dmma_8x8x4(acc[u][0], acc[u][1], fa(tr + lr, k + lk), fb(k + lk, tc + lr));
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < TPW; ++u) {
+    const int tile = warp * TPW + u;
+    const int tr = (tile / (N / 8)) * 8, tc = (tile % (N / 8)) * 8;
+    fo(tr + lr, tc + 2 * lk, acc[u][0]);
+    fo(tr + lr, tc + 2 * lk + 1, acc[u][1]);
+  }
+  __syncthreads();
+}
+
 // Cholesky + inverse of the H x H block at (o, o) of s.T into s.T / s.Di by
 // 2 x 2 recursion: L11, inv11 | L21 = A21 inv11^T | A22 -= L21 L21^T |
 // L22, inv22 | inv21 = -inv22 (L21 inv11).
@@ -102,26 +133,26 @@ __device__ void pc_chol_inv(PcSmallSmem& s, int o, int w) {
     constexpr int N = H / 2;
     pc_chol_inv<N>(s, o, min(w, N));
     if (s.bad) return;
-    pc_mm<N>([&](int r, int t) { return s.T[o + N + r][o + t]; },
-             [&](int t, int c) { return s.Di[o + c][o + t]; },
-             [&](int r, int c, double v) { s.T[o + N + r][o + c] = v; });
-    pc_mm<N>([&](int r, int t) { return s.T[o + N + r][o + t]; },
-             [&](int t, int c) { return s.T[o + N + c][o + t]; },
-             [&](int r, int c, double v) {
-               if (c <= r) s.T[o + N + r][o + N + c] -= v;
-             });
+    pc_mm_t<N>([&](int r, int t) { return s.T[o + N + r][o + t]; },
+               [&](int t, int c) { return s.Di[o + c][o + t]; },
+               [&](int r, int c, double v) { s.T[o + N + r][o + c] = v; });
+    pc_mm_t<N>([&](int r, int t) { return s.T[o + N + r][o + t]; },
+               [&](int t, int c) { return s.T[o + N + c][o + t]; },
+               [&](int r, int c, double v) {
+                 if (c <= r) s.T[o + N + r][o + N + c] -= v;
+               });
     pc_chol_inv<N>(s, o + N, max(0, w - N));
     if (s.bad) return;
     // M = L21 inv11 (after the recursion above: s.M is shared scratch).
-    pc_mm<N>([&](int r, int t) { return s.T[o + N + r][o + t]; },
-             [&](int t, int c) { return s.Di[o + t][o + c]; },
-             [&](int r, int c, double v) { s.M[r][c] = v; });
-    pc_mm<N>([&](int r, int t) { return s.Di[o + N + r][o + N + t]; },
-             [&](int t, int c) { return s.M[t][c]; },
-             [&](int r, int c, double v) {
-               s.Di[o + N + r][o + c] = -v;
-               s.Di[o + r][o + N + c] = 0.0;
-             });
+    pc_mm_t<N>([&](int r, int t) { return s.T[o + N + r][o + t]; },
+               [&](int t, int c) { return s.Di[o + t][o + c]; },
+               [&](int r, int c, double v) { s.M[r][c] = v; });
+    pc_mm_t<N>([&](int r, int t) { return s.Di[o + N + r][o + N + t]; },
+               [&](int t, int c) { return s.M[t][c]; },
+               [&](int r, int c, double v) {
+                 s.Di[o + N + r][o + c] = -v;
+                 s.Di[o + r][o + N + c] = 0.0;
+               });
   }
 }
 
@@ -129,19 +160,28 @@ __device__ void pc_chol_inv(PcSmallSmem& s, int o, int w) {
 // Returns false on a bad pivot (not > 0, or NaN) among the first w columns.
 __device__ bool pc_small(double* A, int b, int j0, int w, double* dinv_out, PcSmallSmem& s) {
   const int tid = threadIdx.x;
-  for (int e = tid; e < 64 * 64; e += blockDim.x) {
-    const int r = e >> 6, c = e & 63;
-    s.T[r][c] = (r < w && c <= r) ? A[(int64_t)(j0 + r) * b + j0 + c] : (r == c ? 1.0 : 0.0);
+#pragma unroll 4
+  for (int e = tid; e < 64 * 32; e += blockDim.x) {  // double2 granules, all loads in flight together
+    const int r = e >> 5, c = (e & 31) * 2;
+    double2 v = make_double2(0.0, 0.0);
+    if (r < w) v = __ldcg(reinterpret_cast<const double2*>(A + (int64_t)(j0 + r) * b + j0 + c));
+    s.T[r][c] = (r < w && c <= r) ? v.x : (r == c ? 1.0 : 0.0);
+    s.T[r][c + 1] = (r < w && c + 1 <= r) ? v.y : (r == c + 1 ? 1.0 : 0.0);
   }
   if (tid == 0) s.bad = 0;
   __syncthreads();
   pc_chol_inv<64>(s, 0, w);
   __syncthreads();
   if (s.bad) return false;
-  for (int e = tid; e < 64 * 64; e += blockDim.x) {
-    const int rr = e >> 6, c = e & 63;
-    if (rr < w && c <= rr) A[(int64_t)(j0 + rr) * b + j0 + c] = s.T[rr][c];
-    dinv_out[e] = s.Di[rr][c];
+#pragma unroll 4
+  for (int e = tid; e < 64 * 32; e += blockDim.x) {
+    const int rr = e >> 5, c = (e & 31) * 2;
+    if (rr < w) {
+      double* dst = A + (int64_t)(j0 + rr) * b + j0 + c;
+      if (c + 1 <= rr) *reinterpret_cast<double2*>(dst) = make_double2(s.T[rr][c], s.T[rr][c + 1]);
+      else if (c <= rr) dst[0] = s.T[rr][c];
+    }
+    *reinterpret_cast<double2*>(dinv_out + rr * 64 + c) = make_double2(s.Di[rr][c], s.Di[rr][c + 1]);
   }
   return true;
 }

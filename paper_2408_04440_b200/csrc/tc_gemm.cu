@@ -116,6 +116,7 @@ enum : int { MODE_UPDATE = 0, MODE_PANEL = 1 };
 struct TcArgs {
   TileStore ts;
   const int2* list;  // output tiles (i, j); panel mode: (i, k)
+  const int* crow;   // update mode: per list entry, the tile's first row in the C tensor map
   int64_t items;     // list entries * sub-tiles per entry
   int k;
   int b;
@@ -250,24 +251,37 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // Update mode: pull the C sub-tile of the next work item into L2 while
       // this one's MMAs run, so the epilogue's C loads hit L2 instead of
       // waiting on HBM latency.
-      auto prefetch_c = [&](int64_t wi) {
+      // The next item's list entry and C row are loaded while this item's
+      // first stages are in flight (a dependent global load here would stall
+      // the TMA issue at every item boundary).
+      auto prefetch_c = [&](int64_t wi, int2 ij, int crow) {
         if (MODE != MODE_UPDATE || args.dbg == 1 || args.dbg == 2 || args.dbg == 5 || (args.opt & 1) || wi >= items)
           return;
         constexpr int kEszP = T::kSplit ? 4 : 2;
-        int ti, tj, tm, tn;
-        decode(wi, ti, tj, tm, tn);
-        const int row = static_cast<int>(args.ts.off[args.ts.idx(ti, tj)] / (static_cast<int64_t>(kEszP) * args.b));
+        (void)ij;
+        const int sub = static_cast<int>(wi % args.sub_per);
+        const int tm = (sub / args.sub_n) * (TC_BM * CG) + static_cast<int>(rank) * TC_BM;
+        const int tn = (sub % args.sub_n) * BN;
 #pragma unroll 1
         for (int rq = 0; rq < TC_BM; rq += 32)
 #pragma unroll 1
-          for (int cx = 0; cx < BN; cx += 128 / kEszP) tma_prefetch_l2_2d(&mC, tn + cx, row + tm + rq);
+          for (int cx = 0; cx < BN; cx += 128 / kEszP) tma_prefetch_l2_2d(&mC, tn + cx, crow + tm + rq);
       };
-      prefetch_c(cid);
-      if (args.opt & 2) prefetch_c(cid + ncl);
+      int2 ij_cur = cid < items ? args.list[cid / args.sub_per] : make_int2(0, 0);
+      int crow_cur = (MODE == MODE_UPDATE && cid < items) ? args.crow[cid / args.sub_per] : 0;
+      prefetch_c(cid, ij_cur, crow_cur);
       for (int64_t w = cid; w < items; w += ncl) {
-        int i, j, m0, n0;
-        decode(w, i, j, m0, n0);
-        prefetch_c(w + ((args.opt & 2) ? 2 : 1) * ncl);
+        const int sub = static_cast<int>(w % args.sub_per);
+        const int i = ij_cur.x, j = ij_cur.y;
+        const int m0 = (sub / args.sub_n) * (TC_BM * CG) + static_cast<int>(rank) * TC_BM;
+        const int n0 = (sub % args.sub_n) * BN;
+        int2 ij_nxt = ij_cur;
+        int crow_nxt = crow_cur;
+        const bool more = w + ncl < items;
+        if (more) {
+          ij_nxt = args.list[(w + ncl) / args.sub_per];
+          if (MODE == MODE_UPDATE) crow_nxt = args.crow[(w + ncl) / args.sub_per];
+        }
         const int a_row = (i - args.k - 1) * args.b + m0;
         const int b_row = (MODE == MODE_UPDATE) ? (j - args.k - 1) * args.b + n0 + static_cast<int>(rank) * (BN / CG)
                                                 : n0;
@@ -294,11 +308,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               tma_load_2d(&mB_lo, &full[stage], st + 2 * Lay::kA + Lay::kB, kx, b_row);
             }
           }
+          if (kb == 1 && more) prefetch_c(w + ncl, ij_nxt, crow_nxt);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
           }
         }
+        ij_cur = ij_nxt;
+        crow_cur = crow_nxt;
       }
     }
   } else if (warp == 1 && rank == 0) {
@@ -386,9 +403,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint8_t* cring = cbuf + (warp - 4) * R * Lay::kCBox;
     uint64_t* cf = cfull + (warp - 4) * R;
     int64_t gbox = 0, gissue = 0;  // next box to process / to load (sequence over this CTA's items)
-    auto c_row = [&](int ti, int tj) {  // first row of tile (ti, tj) in the arena viewed as [rows x b]
-      return static_cast<int>(args.ts.off[args.ts.idx(ti, tj)] / (static_cast<int64_t>(kEsz) * b));
-    };
+    auto c_row = [&](int64_t wi) { return args.crow[wi / args.sub_per]; };  // tile's first arena row
     auto issue_c = [&]() {  // lane 0: TMA-load the next C box into its ring slot
       const int64_t wi = cid + (gissue / kNBox) * ncl;
       if (wi >= items) return;
@@ -397,7 +412,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       decode(wi, ti, tj, tm, tn);
       const int slot = static_cast<int>(gissue % R);
       mbar_arrive_expect_tx(&cf[slot], Lay::kCBox);
-      tma_load_2d(&mC, &cf[slot], cring + slot * Lay::kCBox, tn + bx * kBoxCols, c_row(ti, tj) + tm + q * 32);
+      tma_load_2d(&mC, &cf[slot], cring + slot * Lay::kCBox, tn + bx * kBoxCols, c_row(wi) + tm + q * 32);
       ++gissue;
     };
     if (MODE == MODE_UPDATE && lane == 0 && (args.dbg == 0 || args.dbg >= 3) && args.dbg != 5)
@@ -504,7 +519,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             int bi, bj, bm, bn;
             decode(w, bi, bj, bm, bn);
             if (args.dbg != 3 && args.dbg != 4)
-              tma_store_2d(&mC, cring + slot * Lay::kCBox, bn + bx * kBoxCols, c_row(bi, bj) + bm + q * 32);
+              tma_store_2d(&mC, cring + slot * Lay::kCBox, bn + bx * kBoxCols, c_row(w) + bm + q * 32);
             bulk_commit();
             if (R == 1) {
               bulk_wait_read0();  // the single slot is free again
@@ -777,13 +792,14 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
   }
 }
 
-void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* list, int64_t cnt,
+void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* list, const int* rows, int64_t cnt,
                const double* p64, PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s,
                int max_ctas) {
   (void)p64;
   TcArgs a{};
   a.ts = ts;
   a.list = list;
+  a.crow = rows;
   a.k = k;
   a.b = ts.b;
   a.hp_format = hp_format;
