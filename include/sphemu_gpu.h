@@ -155,6 +155,18 @@ int sphemu_gpu_chol_update_flops(sphemu_chol_t h, double* f_dp, double* f_sp, do
 /* Device stream the handle enqueues on (cudaStream_t as void*). */
 void* sphemu_gpu_chol_stream(sphemu_chol_t h);
 
+/* estimate_innovation_covariance (stochastic.cpp:109-172; stochastic.hpp:52-57):
+ * resid is the n_rows x d innovation matrix (row-major; n_rows must equal
+ * r_len*(t_len-order)). Writes u_hat (d x d, optional: NULL skips) and the
+ * dense lower factor v (d x d) of u_hat + nugget*I, with the nugget escalated
+ * as the reference does; every retry refactors on the device. Returns
+ * SPHEMU_ERR_INVALID_ARG for bad shapes and SPHEMU_ERR_RUNTIME for a
+ * non-positive mean diagonal or when the nugget passes 1e-2 * mean(diag). */
+int sphemu_gpu_estimate_innovation_covariance(const double* resid, int where_resid, int64_t n_rows, int d,
+                                              int r_len, int t_len, int order, const sphemu_chol_config* cfg,
+                                              double* u_hat, int where_u, double* v, int where_v,
+                                              double* nugget_out, sphemu_chol_stats* stats);
+
 /* ======================================================================
  * Spherical harmonic transform (replaces sht.hpp:105-129, wigner.hpp:48-63)
  * ====================================================================== */

@@ -118,6 +118,9 @@ def lib():
         L.sphemu_gpu_chol_residual_probe_spd.argtypes = [vp, C.c_uint64, C.c_int, dp]
         L.sphemu_gpu_emulate.argtypes = [vp, vp, C.c_int, vp, C.c_int, vp, vp, vp, C.c_int, C.c_uint64,
                                          C.c_int, C.c_int, vp]
+        L.sphemu_gpu_estimate_innovation_covariance.argtypes = [
+            vp, C.c_int, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(CholConfig), vp, C.c_int, vp, C.c_int,
+            dp, C.POINTER(CholStats)]
         _lib = L
     return _lib
 
@@ -316,6 +319,28 @@ def emulate(plan, v, phi, means, sigma, v2, t_out, seed=1, r_len=1, rng="referen
     _check(lib().sphemu_gpu_emulate(plan.h, _ptr(v), d, _ptr(phi_a), phi.shape[0], _ptr(means), _ptr(sigma),
                                     _ptr(v2), t_out, seed, r_len, mode, _ptr(out)))
     return out
+
+
+def estimate_innovation_covariance(residuals, r_len, t_len, order, variant="dp", tile_size=128, workers=1,
+                                   band_width_dp=1, sp_fraction=0.05, hp_format="fp16", compute="tensor",
+                                   lookahead=1, sp_compute="fp16x3"):
+    """estimate_innovation_covariance (stochastic.cpp:109-172) on the device:
+    returns (u_hat, v, nugget, stats_json) like InnovationModel
+    (stochastic.hpp:36-42); residuals is the (r_len*(t_len-order)) x d matrix."""
+    xi = np.ascontiguousarray(residuals, dtype=np.float64)
+    if xi.ndim != 2:
+        raise ValueError("residuals must be a 2-D array")
+    d = xi.shape[1]
+    cfg = make_config(variant, tile_size, workers, band_width_dp, sp_fraction, hp_format, compute, lookahead,
+                      sp_compute)
+    u = np.empty((d, d))
+    v = np.empty((d, d))
+    nug = C.c_double()
+    st = CholStats()
+    _check(lib().sphemu_gpu_estimate_innovation_covariance(_ptr(xi), HOST, xi.shape[0], d, r_len, t_len, order,
+                                                           C.byref(cfg), _ptr(u), HOST, _ptr(v), HOST,
+                                                           C.byref(nug), C.byref(st)))
+    return u, v, nug.value, st.to_json()
 
 
 def assign_precisions(n_tiles, variant="dp", band_width_dp=1, sp_fraction=0.05):

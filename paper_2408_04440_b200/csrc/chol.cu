@@ -23,6 +23,7 @@
 #include <nccl.h>
 
 #include "chol_kernels.cuh"
+#include "cov_kernels.cuh"
 #include "potrf_coop.cuh"
 #include "tc_gemm.cuh"
 #include "tcgen05.cuh"
@@ -349,7 +350,7 @@ struct Chol {
     SPH_CUDA(cudaEventCreateWithFlags(&ev_col, cudaEventDisableTiming));
   }
 
-  void load_host(const double* a, int64_t lda) {
+  void load_host(const double* a, int64_t lda, double diag_shift = 0.0) {
     ensure_io();
     const size_t slab = static_cast<size_t>(lb) * n;
     if (islab.n < kSlabs * slab) islab.alloc(kSlabs * slab);
@@ -366,8 +367,8 @@ struct Chol {
                                  sizeof(double) * w, rows(i), cudaMemcpyHostToDevice, cstream));
       SPH_CUDA(cudaEventRecord(ev_in_full[s], cstream));
       SPH_CUDA(cudaStreamWaitEvent(stream, ev_in_full[s], 0));
-      k_load_dense<<<dim3(static_cast<unsigned>(i + 1), gy), 256, 0, stream>>>(store(), dst, n, sat.get(),
-                                                                               static_cast<int64_t>(tix(i, 0)), i * lb);
+      k_load_dense<<<dim3(static_cast<unsigned>(i + 1), gy), 256, 0, stream>>>(
+          store(), dst, n, sat.get(), static_cast<int64_t>(tix(i, 0)), i * lb, diag_shift);
       SPH_LAUNCH_CHECK();
       SPH_CUDA(cudaEventRecord(ev_in_free[s], stream));
       ++used;
@@ -614,14 +615,14 @@ struct Chol {
     return dim3(static_cast<unsigned>(pmap.size()), static_cast<unsigned>(std::max(1, b * b / (256 * 64))));
   }
 
-  void load_dense(const double* a, int where, int64_t lda) {
+  void load_dense(const double* a, int where, int64_t lda, double diag_shift = 0.0) {
     factored = false;
     reset_flags();
     const int pl = prof_begin(kLoad);
     if (where == SPHEMU_HOST) {
-      load_host(a, lda);
+      load_host(a, lda, diag_shift);
     } else {
-      k_load_dense<<<tile_grid(), 256, 0, stream>>>(store(), a, lda, sat.get());
+      k_load_dense<<<tile_grid(), 256, 0, stream>>>(store(), a, lda, sat.get(), 0, 0, diag_shift);
       SPH_LAUNCH_CHECK();
     }
     k_rowexp<<<ceil_div(n, 256), 256, 0, stream>>>(store(), rowexp.get());
@@ -1278,6 +1279,74 @@ int sphemu_gpu_release_cache(void) {
     std::lock_guard<std::mutex> lk(g_dense_mu);
     g_dense.reset();
     g_dense_dev = -1;
+  });
+}
+
+// estimate_innovation_covariance (stochastic.cpp:109-172) with the sample
+// covariance and every nugget retry on the device: U = Xi^T Xi / n by DMMA
+// (cov_kernels.cuh), then tiled factorizations of U + nugget I read straight
+// from U in HBM, the nugget escalated tenfold from 0 (or 1e-8 mean diag when
+// n < d) until the factor succeeds, giving up past 1e-2 mean diag.
+int sphemu_gpu_estimate_innovation_covariance(const double* resid, int where_resid, int64_t n_rows, int d,
+                                              int r_len, int t_len, int order, const sphemu_chol_config* cfg,
+                                              double* u_hat, int where_u, double* v, int where_v,
+                                              double* nugget_out, sphemu_chol_stats* stats) {
+  return guard([&] {
+    if (n_rows < 2 || d < 1) throw std::invalid_argument("residual sample is too small");
+    if (n_rows != static_cast<int64_t>(r_len) * (t_len - order))
+      throw std::invalid_argument("residual row count does not match r_len*(t_len-order)");
+    validate_config(*cfg);
+    DevBuf<double> xi_dev, xt, u_dev;
+    const double* xi = resid;
+    if (where_resid == SPHEMU_HOST) {
+      xi_dev.alloc(static_cast<size_t>(n_rows) * d);
+      SPH_CUDA(cudaMemcpy(xi_dev.get(), resid, sizeof(double) * n_rows * d, cudaMemcpyHostToDevice));
+      xi = xi_dev.get();
+    }
+    const int64_t ldt = (n_rows + 1) & ~int64_t{1};  // even stride: 16-byte rows for the DMMA loader
+    xt.alloc(static_cast<size_t>(d) * ldt);
+    k_transpose_pad<<<dim3(static_cast<unsigned>((ldt + 31) / 32), static_cast<unsigned>((d + 31) / 32)), dim3(32, 8)>>>(
+        xi, n_rows, d, xt.get(), ldt);
+    SPH_LAUNCH_CHECK();
+    double* U = (where_u == SPHEMU_DEVICE && u_hat) ? u_hat : nullptr;
+    if (!U) {
+      u_dev.alloc(static_cast<size_t>(d) * d);
+      U = u_dev.get();
+    }
+    static bool attr = false;
+    if (!attr) {
+      SPH_CUDA(cudaFuncSetAttribute(k_cov_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(D2Smem)));
+      attr = true;
+    }
+    k_cov_syrk<<<dim3(static_cast<unsigned>((d + D2_BN - 1) / D2_BN), static_cast<unsigned>((d + D2_BM - 1) / D2_BM)),
+                 D2_THREADS, sizeof(D2Smem)>>>(xt.get(), ldt, n_rows, d, 1.0 / static_cast<double>(n_rows), U);
+    SPH_LAUNCH_CHECK();
+    std::vector<double> diag(d);
+    SPH_CUDA(cudaMemcpy2D(diag.data(), sizeof(double), U, sizeof(double) * (d + 1), sizeof(double), d,
+                          cudaMemcpyDeviceToHost));
+    double sum = 0.0;
+    for (double x : diag) sum += x;
+    const double mean_diag = sum / d;
+    if (!(mean_diag > 0.0)) throw std::runtime_error("innovation covariance has a non-positive mean diagonal");
+    xt.release();
+    xi_dev.release();
+    double nugget = (n_rows < d) ? 1e-8 * mean_diag : 0.0;
+    const double cap = 1e-2 * mean_diag;
+    Chol c(d, *cfg);
+    while (true) {
+      c.load_dense(U, SPHEMU_DEVICE, d, nugget);
+      c.factor();
+      if (c.wait(stats) < 0) break;
+      const double next = (nugget == 0.0) ? 1e-8 * mean_diag : 10.0 * nugget;
+      if (next > cap)
+        throw std::runtime_error(
+            "innovation covariance is not positive definite even with the largest allowed diagonal inflation");
+      nugget = next;
+    }
+    if (nugget_out) *nugget_out = nugget;
+    if (v) c.store_dense(v, where_v, d);
+    if (u_hat && where_u == SPHEMU_HOST)
+      SPH_CUDA(cudaMemcpy(u_hat, U, sizeof(double) * d * d, cudaMemcpyDeviceToHost));
   });
 }
 

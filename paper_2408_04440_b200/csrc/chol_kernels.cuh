@@ -72,8 +72,10 @@ static __global__ void k_gen_spd(TileStore ts, const double* __restrict__ d, con
 // TiledMatrix::from_dense (mpchol.cpp:124-138) + input quantization.
 // t0 / row0: launch over a run of packed tiles starting at t0, reading a
 // slab whose first row is global row row0 (the streamed host input).
+// diag_shift: added to the diagonal before quantization (the nugget of
+// stochastic.cpp:147-151, dense = u + nugget * I).
 static __global__ void k_load_dense(TileStore ts, const double* __restrict__ a, int64_t lda, unsigned* sat,
-                                    int64_t t0 = 0, int row0 = 0) {
+                                    int64_t t0 = 0, int row0 = 0, double diag_shift = 0.0) {
   const int64_t t = t0 + blockIdx.x;
   if (ts.off[t] < 0) return;  // tile owned by another rank
   int i, j;
@@ -86,7 +88,8 @@ static __global__ void k_load_dense(TileStore ts, const double* __restrict__ a, 
        e += (int64_t)gridDim.y * blockDim.x) {
     const int r = (int)(e / b), c = (int)(e % b);
     const int R = i * ts.lb + r, Cc = j * ts.lb + c;
-    const double v = (r < ts.lb && c < ts.lb && R < ts.n && Cc < ts.n) ? a[(int64_t)(R - row0) * lda + Cc] : 0.0;
+    double v = (r < ts.lb && c < ts.lb && R < ts.n && Cc < ts.n) ? a[(int64_t)(R - row0) * lda + Cc] : 0.0;
+    if (R == Cc && R < ts.n) v += diag_shift;
     store_elem(tp, p, e, v, local);
   }
   flush_sat(local, sat);
