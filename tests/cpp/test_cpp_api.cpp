@@ -1,0 +1,207 @@
+// C++ drop-in API checks (include/sphemu/*.hpp over the C-ABI), mirroring the
+// reference's own test cases: proj/tests/test_mpchol.cpp, test_sht.cpp,
+// test_grid.cpp, test_wigner.cpp, test_stochastic.cpp (file:line in each case).
+// Prints "ALL PASSED" and exits 0 when every check holds. Needs a GPU.
+#include <cmath>
+#include <cstdio>
+#include <numbers>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "sphemu/sphemu.hpp"
+
+static int g_fail = 0;
+#define CHECK(cond)                                                       \
+  do {                                                                    \
+    if (!(cond)) {                                                        \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+      ++g_fail;                                                           \
+    }                                                                     \
+  } while (0)
+
+template <class E, class F>
+static bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+// Unblocked host Cholesky (the untiled oracle of tests/support/reference.cpp).
+static std::vector<double> host_cholesky(std::vector<double> a, int n) {
+  for (int j = 0; j < n; ++j) {
+    double s = a[j * n + j];
+    for (int k = 0; k < j; ++k) s -= a[j * n + k] * a[j * n + k];
+    a[j * n + j] = std::sqrt(s);
+    for (int i = j + 1; i < n; ++i) {
+      double t = a[i * n + j];
+      for (int k = 0; k < j; ++k) t -= a[i * n + k] * a[j * n + k];
+      a[i * n + j] = t / a[j * n + j];
+    }
+    for (int c = j + 1; c < n; ++c) a[j * n + c] = 0.0;
+  }
+  return a;
+}
+
+int main() {
+  using namespace sphemu;
+  CHECK(std::string(kVersion) == "0.1.0");
+
+  // grid.cpp:18-49 (test_grid.cpp)
+  GridSpec g = GridSpec::from_band_limit(45);
+  CHECK(g.n_theta == 46 && g.n_phi == 90 && g.max_band_limit() == 45 && g.admissible(45) && !g.admissible(46));
+  CHECK(std::fabs(g.theta(45) - std::numbers::pi) < 1e-15);
+  CHECK(resolution_summary(180).grid_points == 179 * 360);
+  CHECK(throws<std::invalid_argument>([] { GridSpec{1, 4}.validate(); }));
+
+  // quantize KATs (test_mpchol.cpp:177-202)
+  {
+    std::vector<double> t{1.0 / 3.0};
+    ConversionCounters cc;
+    quantize_tile(t, Precision::kSingle, &cc);
+    CHECK(t[0] == static_cast<double>(1.0f / 3.0f) && cc.demotions_sp == 1);
+    std::vector<double> h{1.0 / 3.0, 65505.0, -70000.0};
+    ConversionCounters ch;
+    quantize_tile(h, Precision::kHalf, &ch);
+    CHECK(h[0] == 0.333251953125 && h[1] == 65504.0 && h[2] == -65504.0);
+    CHECK(ch.half_saturations == 1 && ch.demotions_hp == 3);
+  }
+
+  // DAG (test_mpchol.cpp:47-71)
+  for (auto [nt, want] : {std::pair{4, 20}, std::pair{8, 120}}) {
+    TaskGraph dag = build_task_graph(nt);
+    int sources = 0;
+    for (auto d : dag.indegree) sources += d == 0;
+    CHECK(static_cast<int>(dag.size()) == want && sources == 1);
+  }
+
+  // precision map (test_mpchol.cpp:73-108)
+  {
+    MpCholConfig c;
+    c.variant = PrecisionVariant::kDpSpHp;
+    PrecisionMap m = assign_precisions(10, c);
+    CHECK(m.count(Precision::kDouble) == 10 && m.count(Precision::kSingle) == 3);
+    CHECK(m.at(1, 0) == Precision::kSingle && m.at(2, 1) == Precision::kSingle && m.at(3, 2) == Precision::kSingle);
+    c.band_width_dp = 2;
+    CHECK(assign_precisions(10, c).count(Precision::kDouble) == 19);
+  }
+
+  // 2x2 known answer at b = 1 and 2 (test_mpchol.cpp:36-45)
+  for (int b : {1, 2}) {
+    MpCholConfig c;
+    c.tile_size = b;
+    c.compute = SPHEMU_COMPUTE_FP64;
+    auto r = tiled_cholesky_dense(std::vector<double>{4, 2, 2, 3}, 2, c);
+    CHECK(r.factor[0] == 2.0 && r.factor[1] == 0.0 && r.factor[2] == 1.0 && r.factor[3] == std::sqrt(2.0));
+  }
+
+  // DP factor vs the untiled oracle, n in {96, 100}, b = 32, seed 3 (test_mpchol.cpp:110-121)
+  for (int n : {96, 100}) {
+    std::vector<double> a = make_spd_test_matrix(n, 3);
+    CHECK(a[1] == a[n]);  // exactly symmetric
+    MpCholConfig c;
+    c.tile_size = 32;
+    auto r = tiled_cholesky_dense(a, n, c);
+    auto want = host_cholesky(a, n);
+    double md = 0.0;
+    for (std::size_t e = 0; e < want.size(); ++e) md = std::fmax(md, std::fabs(r.factor[e] - want[e]));
+    CHECK(md < 1e-13);
+    CHECK(r.stats.n_tiles == (n + 31) / 32 && r.stats.tasks_potrf == r.stats.n_tiles);
+    // in-place TiledMatrix path gives the same factor
+    TiledMatrix t = TiledMatrix::from_dense(a, n, 32);
+    tiled_cholesky(t, c);
+    CHECK(t.to_dense_lower() == r.factor);
+  }
+
+  // indefinite input -> NotPositiveDefiniteError on tile 1 (test_mpchol.cpp:142-154)
+  {
+    std::vector<double> a(16, 0.0);
+    a[0] = a[5] = a[15] = 1.0;
+    a[10] = -1.0;
+    MpCholConfig c;
+    c.tile_size = 2;
+    int tile = -2;
+    try {
+      tiled_cholesky_dense(a, 4, c);
+    } catch (const NotPositiveDefiniteError& e) {
+      tile = e.tile_index();
+    }
+    CHECK(tile == 1);
+  }
+
+  // stats JSON schema (mpchol.cpp:437-457)
+  {
+    MpCholConfig c;
+    c.variant = PrecisionVariant::kDpSp;
+    c.tile_size = 32;
+    auto r = tiled_cholesky_dense(make_spd_test_matrix(64, 1), 64, c);
+    const std::string js = r.stats.to_json();
+    CHECK(js.find("\"variant\": \"dpsp\"") != std::string::npos && js.find("\"total\": 4,") != std::string::npos);
+  }
+
+  // SHT: constant field (test_sht.cpp:72-83) and round trip (test_sht.cpp:85-102)
+  {
+    ShtPlan p = build_plan(GridSpec::from_band_limit(16), 16);
+    EquiangularField f(p.spec);
+    for (auto& v : f.values) v = 2.5;
+    HarmonicVector z = forward_sht(p, f);
+    CHECK(std::fabs(z.values[0] - 2.5 * std::sqrt(4.0 * std::numbers::pi)) < 1e-13);
+    std::mt19937_64 rng(7);
+    std::normal_distribution<double> nd;
+    HarmonicVector c(16);
+    for (int l = 0; l < 16; ++l) {
+      c.set_coeff(l, 0, {nd(rng), 0.0});
+      for (int m = 1; m <= l; ++m) c.set_coeff(l, m, {nd(rng), nd(rng)});
+    }
+    HarmonicVector back = forward_sht(p, inverse_sht(p, c));
+    double md = 0.0;
+    for (std::size_t e = 0; e < c.values.size(); ++e) md = std::fmax(md, std::fabs(back.values[e] - c.values[e]));
+    CHECK(md < 1e-10);
+    CHECK(std::fabs(c.parseval_energy() - back.parseval_energy()) < 1e-8 * c.parseval_energy());
+    // batch == single
+    FieldSeries s(p.spec, 3, 2);
+    for (std::size_t e = 0; e < s.values.size(); ++e) s.values[e] = std::sin(0.001 * e);
+    CoeffSeries cs = forward_sht_batch(p, s, 4);
+    std::vector<double> one(HarmonicVector::packed_size(16));
+    forward_sht(p, s.slice(1, 2), one);
+    double bd = 0.0;
+    for (std::size_t e = 0; e < one.size(); ++e) bd = std::fmax(bd, std::fabs(one[e] - cs.slice(1, 2)[e]));
+    CHECK(bd < 1e-14);
+  }
+  CHECK(throws<std::invalid_argument>([] { build_plan(GridSpec{9, 16}, 9); }));           // test_sht.cpp:196-199
+  CHECK(throws<std::invalid_argument>([] { build_wigner_tables(720); }));                 // 2 GiB cap (F5)
+  CHECK(!throws<std::invalid_argument>([] { build_wigner_tables(720, std::size_t{4} << 30); }));
+
+  // covariance + nugget (test_stochastic.cpp:159-210)
+  {
+    const int d = 36, r_len = 2, t_len = 40, order = 2;
+    const std::int64_t rows = r_len * (t_len - order);
+    std::vector<double> xi(static_cast<std::size_t>(rows) * d);
+    std::mt19937_64 rng(99);
+    std::normal_distribution<double> nd;
+    for (auto& x : xi) x = nd(rng);
+    MpCholConfig c;
+    c.tile_size = 16;
+    InnovationModel m = estimate_innovation_covariance(xi, rows, d, r_len, t_len, order, c);
+    double mu = 0.0, mv = 0.0, mx = 0.0;
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < d; ++j) {
+        double u = 0.0, vv = 0.0;
+        for (std::int64_t r = 0; r < rows; ++r) u += xi[r * d + i] * xi[r * d + j];
+        u /= static_cast<double>(rows);
+        for (int k = 0; k < d; ++k) vv += m.v[i * d + k] * m.v[j * d + k];
+        mu = std::fmax(mu, std::fabs(u - m.u_hat[i * d + j]));
+        mv = std::fmax(mv, std::fabs(vv - m.u_hat[i * d + j] - (i == j ? m.nugget : 0.0)));
+        mx = std::fmax(mx, std::fabs(u));
+      }
+    CHECK(mu < 1e-12 * mx && mv < 1e-12 * mx && m.nugget == 0.0);
+  }
+
+  if (g_fail == 0) std::printf("ALL PASSED\n");
+  return g_fail ? 1 : 0;
+}
