@@ -104,6 +104,12 @@ int sphemu_gpu_tiled_cholesky_dense(const double* a, int where_a, int n,
  * the same n, configuration and device; this frees them. */
 int sphemu_gpu_release_cache(void);
 
+/* Host-only view of the 2D block-cyclic layout a rank would use (no GPU
+ * needed): tiles it stores, its arena bytes, and xchg_bytes[k*P*Q + r] = the
+ * panel bytes rank r broadcasts at step k (nt*P*Q entries, may be NULL). */
+int sphemu_gpu_dist_layout(int n, const sphemu_chol_config* cfg, int P, int Q, int rank, int64_t* tiles_owned,
+                           int64_t* arena_bytes, int64_t* xchg_bytes);
+
 /* Device-resident factorization handle (TiledMatrix + tiled_cholesky,
  * mpchol.hpp:47-71,135): tiles live in HBM at their storage precision. */
 typedef struct sphemu_chol_s* sphemu_chol_t;

@@ -228,6 +228,61 @@ __global__ void k_diff_norms(int n, const double* a, const double* b, double* su
   }
 }
 
+// Host-only 2D block-cyclic layout (no CUDA calls): this rank's tile offsets
+// in its arena and the per-step panel exchange plan (panel tiles of step k
+// grouped by owning rank so each owner broadcasts one contiguous block). Chol
+// builds its device state from it; sphemu_gpu_dist_layout exposes it to
+// host-side tests.
+struct BlockCyclic {
+  struct XRoot {
+    int root;
+    int64_t off, bytes;
+  };
+  int nt = 0, b = 0, P = 1, Q = 1, rank = 0;
+  std::vector<int64_t> off;                 // per packed tile; -1 = stored elsewhere; back() = arena bytes
+  std::vector<std::vector<XRoot>> xroots;   // per step k
+  std::vector<std::vector<int64_t>> xpos;   // per step k: byte position of panel tile i at [i - k - 1]
+  int64_t xmax = 0;
+  int owner(int i, int j) const { return (i % P) * Q + (j % Q); }
+  bool mine(int i, int j) const { return owner(i, j) == rank; }
+
+  BlockCyclic(int nt_, int b_, const std::vector<uint8_t>& sprec, int P_, int Q_, int rank_)
+      : nt(nt_), b(b_), P(P_), Q(Q_), rank(rank_) {
+    off.assign(sprec.size() + 1, 0);
+    int64_t o = 0;
+    size_t t = 0;
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j <= i; ++j, ++t) {
+        if (!mine(i, j)) {
+          off[t] = -1;
+          continue;
+        }
+        off[t] = o;
+        o += static_cast<int64_t>(b) * b * prec_bytes(sprec[t]);
+        o = (o + 255) & ~int64_t{255};
+      }
+    off.back() = o;
+    if (P * Q == 1) return;
+    xroots.assign(nt, {});
+    xpos.assign(nt, {});
+    for (int k = 0; k + 1 < nt; ++k) {
+      xpos[k].assign(nt - k - 1, 0);
+      int64_t x = 0;
+      for (int pr = 0; pr < P; ++pr) {
+        const int root = pr * Q + k % Q;
+        const int64_t start = x;
+        for (int i = k + 1; i < nt; ++i)
+          if (owner(i, k) == root) {
+            xpos[k][i - k - 1] = x;
+            x += static_cast<int64_t>(b) * b * prec_bytes(sprec[static_cast<size_t>(i) * (i + 1) / 2 + k]);
+          }
+        if (x > start) xroots[k].push_back({root, start, x - start});
+      }
+      xmax = std::max(xmax, x);
+    }
+  }
+};
+
 struct Chol {
   int n = 0, b = 0, nt = 0;  // b = storage pitch (padded), lb = logical tile size
   int lb = 0;
@@ -246,10 +301,7 @@ struct Chol {
   DevBuf<int2> ilists, xsend;
   DevBuf<int64_t> ioffs, xsoffs;
   std::vector<int64_t> ilist_off, ilist_cnt, xsend_off, xsend_cnt;
-  struct XRoot {
-    int root;
-    int64_t off, bytes;
-  };
+  using XRoot = BlockCyclic::XRoot;
   std::vector<std::vector<XRoot>> xroots;
   sphemu_chol_config cfg{};
   std::vector<uint8_t> pmap, sprec;
@@ -433,27 +485,14 @@ struct Chol {
     nt = (n + lb - 1) / lb;
     pmap = assign_precisions(nt, cfg);
     sprec.resize(pmap.size());
-    off.resize(pmap.size() + 1);
-    int64_t o = 0;
-    for (size_t t = 0; t < pmap.size(); ++t) {
-      int sp = pmap[t] == SPHEMU_PREC_DP ? kDP : (pmap[t] == SPHEMU_PREC_SP ? kSP : (cfg.hp_format == SPHEMU_HP_BF16 ? kBF : kHP));
-      sprec[t] = static_cast<uint8_t>(sp);
-      int ti = 0, tj = 0;
-      {
-        int64_t x = 0;
-        while ((x + 1) * (x + 2) / 2 <= static_cast<int64_t>(t)) ++x;
-        ti = static_cast<int>(x);
-        tj = static_cast<int>(t - x * (x + 1) / 2);
-      }
-      if (!mine(ti, tj)) {
-        off[t] = -1;  // stored on another rank
-        continue;
-      }
-      off[t] = o;
-      o += static_cast<int64_t>(b) * b * prec_bytes(sp);
-      o = (o + 255) & ~int64_t{255};
-    }
-    off.back() = o;
+    for (size_t t = 0; t < pmap.size(); ++t)
+      sprec[t] = static_cast<uint8_t>(pmap[t] == SPHEMU_PREC_DP
+                                          ? kDP
+                                          : (pmap[t] == SPHEMU_PREC_SP ? kSP
+                                                                       : (cfg.hp_format == SPHEMU_HP_BF16 ? kBF : kHP)));
+    BlockCyclic layout(nt, b, sprec, P, Q, rank);
+    off = layout.off;
+    const int64_t o = off.back();
     arena.alloc(static_cast<size_t>(std::max<int64_t>(o, static_cast<int64_t>(128) * b)));
     d_off.alloc(pmap.size());
     d_prec.alloc(pmap.size());
@@ -519,21 +558,11 @@ struct Chol {
       xroots.assign(nt, {});
       std::vector<int2> il, xs;
       std::vector<int64_t> io, xo;
-      int64_t xmax = 0;
+      xroots = layout.xroots;
+      const int64_t xmax = layout.xmax;
       for (int k = 0; k + 1 < nt; ++k) {
         std::vector<int64_t> pos(nt, 0);
-        int64_t o = 0;
-        for (int pr = 0; pr < P; ++pr) {
-          const int root = pr * Q + k % Q;
-          const int64_t start = o;
-          for (int i = k + 1; i < nt; ++i)
-            if (owner(i, k) == root) {
-              pos[i] = o;
-              o += static_cast<int64_t>(b) * b * prec_bytes(sprec[tix(i, k)]);
-            }
-          if (o > start) xroots[k].push_back({root, start, o - start});
-        }
-        xmax = std::max(xmax, o);
+        for (int i = k + 1; i < nt; ++i) pos[i] = layout.xpos[k][i - k - 1];
         ilist_off[k] = static_cast<int64_t>(il.size());
         xsend_off[k] = static_cast<int64_t>(xs.size());
         for (int i = k + 1; i < nt; ++i) {
@@ -1279,6 +1308,32 @@ int sphemu_gpu_release_cache(void) {
     std::lock_guard<std::mutex> lk(g_dense_mu);
     g_dense.reset();
     g_dense_dev = -1;
+  });
+}
+
+int sphemu_gpu_dist_layout(int n, const sphemu_chol_config* cfg, int P, int Q, int rank, int64_t* tiles_owned,
+                           int64_t* arena_bytes, int64_t* xchg_bytes) {
+  return guard([&] {
+    validate_config(*cfg);
+    if (n < 1 || P < 1 || Q < 1 || rank < 0 || rank >= P * Q) throw std::invalid_argument("bad process grid");
+    const int lb = cfg->tile_size;
+    const int granule = cfg->compute == SPHEMU_COMPUTE_TENSOR ? 128 : 64;
+    const int b = (lb + granule - 1) / granule * granule;
+    const int nt = (n + lb - 1) / lb;
+    std::vector<uint8_t> pm = assign_precisions(nt, *cfg), sp(pm.size());
+    for (size_t t = 0; t < pm.size(); ++t)
+      sp[t] = static_cast<uint8_t>(pm[t] == SPHEMU_PREC_DP ? kDP
+                                   : (pm[t] == SPHEMU_PREC_SP ? kSP : (cfg->hp_format == SPHEMU_HP_BF16 ? kBF : kHP)));
+    BlockCyclic L(nt, b, sp, P, Q, rank);
+    int64_t owned = 0;
+    for (size_t t = 0; t + 1 < L.off.size(); ++t) owned += L.off[t] >= 0;
+    if (tiles_owned) *tiles_owned = owned;
+    if (arena_bytes) *arena_bytes = L.off.back();
+    if (xchg_bytes) {
+      std::fill(xchg_bytes, xchg_bytes + static_cast<size_t>(nt) * P * Q, int64_t{0});
+      for (int k = 0; k < static_cast<int>(L.xroots.size()); ++k)
+        for (const auto& x : L.xroots[k]) xchg_bytes[static_cast<size_t>(k) * P * Q + x.root] = x.bytes;
+    }
   });
 }
 
