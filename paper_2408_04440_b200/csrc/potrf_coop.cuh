@@ -13,6 +13,7 @@
 #include <cooperative_groups.h>
 
 #include "chol_kernels.cuh"
+#include "dgemm2.cuh"
 
 namespace sphemu_gpu {
 
@@ -29,7 +30,7 @@ struct PcSmallSmem {
 // right-looking Cholesky with one rsqrt per column, then the inverse by
 // right-looking forward substitution (lane j owns column j). Small unrolled
 // code (the 32-wide version thrashed the instruction cache).
-__device__ void pc_base16(PcSmallSmem& s, int o, int w, int lane) {
+__device__ __noinline__ void pc_base16(PcSmallSmem& s, int o, int w, int lane) {
   constexpr unsigned FULL = 0xffffffffu;
   const int row = lane & 15;
   double a[16], rl[16];
@@ -124,8 +125,10 @@ __device__ __forceinline__ void pc_mm_t(FA fa, FB fb, FO fo) {
 // Cholesky + inverse of the H x H block at (o, o) of s.T into s.T / s.Di by
 // 2 x 2 recursion: L11, inv11 | L21 = A21 inv11^T | A22 -= L21 L21^T |
 // L22, inv22 | inv21 = -inv22 (L21 inv11).
+// Not inlined: the two calls per level share one copy of the code (the
+// cooperative kernel is large enough for instruction fetch to matter).
 template <int H>
-__device__ void pc_chol_inv(PcSmallSmem& s, int o, int w) {
+__device__ __noinline__ void pc_chol_inv(PcSmallSmem& s, int o, int w) {
   if constexpr (H == 16) {
     if ((threadIdx.x >> 5) == 0) pc_base16(s, o, w, threadIdx.x & 31);
     __syncthreads();
@@ -156,36 +159,6 @@ __device__ void pc_chol_inv(PcSmallSmem& s, int o, int w) {
   }
 }
 
-// Factor + invert the 64 x 64 diagonal block at (j0, j0) (w valid rows).
-// Returns false on a bad pivot (not > 0, or NaN) among the first w columns.
-__device__ bool pc_small(double* A, int b, int j0, int w, double* dinv_out, PcSmallSmem& s) {
-  const int tid = threadIdx.x;
-#pragma unroll 4
-  for (int e = tid; e < 64 * 32; e += blockDim.x) {  // double2 granules, all loads in flight together
-    const int r = e >> 5, c = (e & 31) * 2;
-    double2 v = make_double2(0.0, 0.0);
-    if (r < w) v = __ldcg(reinterpret_cast<const double2*>(A + (int64_t)(j0 + r) * b + j0 + c));
-    s.T[r][c] = (r < w && c <= r) ? v.x : (r == c ? 1.0 : 0.0);
-    s.T[r][c + 1] = (r < w && c + 1 <= r) ? v.y : (r == c + 1 ? 1.0 : 0.0);
-  }
-  if (tid == 0) s.bad = 0;
-  __syncthreads();
-  pc_chol_inv<64>(s, 0, w);
-  __syncthreads();
-  if (s.bad) return false;
-#pragma unroll 4
-  for (int e = tid; e < 64 * 32; e += blockDim.x) {
-    const int rr = e >> 5, c = (e & 31) * 2;
-    if (rr < w) {
-      double* dst = A + (int64_t)(j0 + rr) * b + j0 + c;
-      if (c + 1 <= rr) *reinterpret_cast<double2*>(dst) = make_double2(s.T[rr][c], s.T[rr][c + 1]);
-      else if (c <= rr) dst[0] = s.T[rr][c];
-    }
-    *reinterpret_cast<double2*>(dinv_out + rr * 64 + c) = make_double2(s.Di[rr][c], s.Di[rr][c + 1]);
-  }
-  return true;
-}
-
 #ifdef SPHEMU_POTRF_TRACE
 __device__ unsigned long long* g_potrf_trace;
 #define PTRACE(slot)                                                                         \
@@ -202,6 +175,106 @@ __device__ unsigned long long* g_potrf_trace;
   } while (0)
 #endif
 
+// Factor + invert the 64 x 64 diagonal block at (j0, j0) (w valid rows).
+// Returns false on a bad pivot (not > 0, or NaN) among the first w columns.
+// 64 x 64 x K (K <= 64) FP64 product with both operands staged whole in
+// shared memory by cp.async (every load in flight at once: one memory round
+// trip instead of one per K-chunk), then 16 DMMA k-steps. Same accumulator
+// layout as dgemm_64x64 (dg_for_each). Row stride 68 doubles keeps the
+// m8n8k4 fragment loads conflict-free per half-warp.
+constexpr int PG_LD = 68;
+struct PgSmem {
+  double a[64 * PG_LD];
+  double b[64 * PG_LD];
+};
+
+template <class Acc>
+__device__ __forceinline__ void pg_stage(const Acc& X, int K, double* s) {
+  // KContig: element (r, k) at base[r*ld + k] -> s[r][k]; else (c, k) at base[k*ld + c] -> s[k][c]
+  for (int e = threadIdx.x; e < 64 * 32; e += blockDim.x) {
+    const int row = e >> 5, col = (e & 31) * 2;  // row: r (KContig) or k; col: k (KContig) or c
+    const int r_lim = Acc::kKContig ? X.rows : K, c_lim = Acc::kKContig ? K : X.rows;
+    int bytes = 0;
+    const double* src = X.base;
+    if (row < r_lim && col < c_lim) {
+      bytes = (c_lim - col >= 2) ? 16 : 8;
+      src = X.base + (int64_t)row * X.ld + col;
+    }
+    cp_async16(s + row * PG_LD + col, src, bytes);
+  }
+}
+
+template <class AccA, class AccB>
+__device__ __forceinline__ void pgemm_64(const AccA& A, const AccB& B, int K, PgSmem& sm, double (&acc)[4][4][2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  pg_stage(A, K, sm.a);
+  pg_stage(B, K, sm.b);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  const int kq = lane & 3, rq = lane >> 2;
+  for (int kk = 0; kk < K; kk += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = sm.a[(wm * 32 + mi * 8 + rq) * PG_LD + kk + kq];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const int cn = wn * 32 + ni * 8 + rq;
+      b[ni] = AccB::kKContig ? sm.b[cn * PG_LD + kk + kq] : sm.b[(kk + kq) * PG_LD + cn];
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+  }
+  __syncthreads();  // smem reusable by the caller
+}
+
+// Factor + invert the 64 x 64 block already staged in s.T (lower part, zero
+// upper part, unit diagonal on padding rows) and write back the factor and
+// the inverse. Returns false on a bad pivot (not > 0, or NaN) among the
+// first w columns.
+__device__ bool pc_small_finish(double* A, int b, int j0, int w, double* dinv_out, PcSmallSmem& s) {
+  const int tid = threadIdx.x;
+  if (tid == 0) s.bad = 0;
+  __syncthreads();
+  if (j0 == 64) PTRACE(40);
+  pc_chol_inv<64>(s, 0, w);
+  __syncthreads();
+  if (j0 == 64) PTRACE(41);
+  if (s.bad) return false;
+#pragma unroll 4
+  for (int e = tid; e < 64 * 32; e += blockDim.x) {
+    const int rr = e >> 5, c = (e & 31) * 2;
+    if (rr < w) {
+      double* dst = A + (int64_t)(j0 + rr) * b + j0 + c;
+      if (c + 1 <= rr) *reinterpret_cast<double2*>(dst) = make_double2(s.T[rr][c], s.T[rr][c + 1]);
+      else if (c <= rr) dst[0] = s.T[rr][c];
+    }
+    *reinterpret_cast<double2*>(dinv_out + rr * 64 + c) = make_double2(s.Di[rr][c], s.Di[rr][c + 1]);
+  }
+  return true;
+}
+
+// Factor + invert the 64 x 64 diagonal block at (j0, j0) (w valid rows).
+__device__ bool pc_small(double* A, int b, int j0, int w, double* dinv_out, PcSmallSmem& s) {
+  const int tid = threadIdx.x;
+#pragma unroll 4
+  for (int e = tid; e < 64 * 32; e += blockDim.x) {  // double2 granules, all loads in flight together
+    const int r = e >> 5, c = (e & 31) * 2;
+    double2 v = make_double2(0.0, 0.0);
+    if (r < w) v = __ldcg(reinterpret_cast<const double2*>(A + (int64_t)(j0 + r) * b + j0 + c));
+    s.T[r][c] = (r < w && c <= r) ? v.x : (r == c ? 1.0 : 0.0);
+    s.T[r][c + 1] = (r < w && c + 1 <= r) ? v.y : (r == c + 1 ? 1.0 : 0.0);
+  }
+  return pc_small_finish(A, b, j0, w, dinv_out, s);
+}
+
 __device__ __forceinline__ double* blk(double* A, int b, int r, int c) {
   return A + (int64_t)r * PC_BLK * b + (int64_t)c * PC_BLK;
 }
@@ -217,8 +290,8 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) uint8_t pc_smem[];
-  DgSmem& sm = *reinterpret_cast<DgSmem*>(pc_smem);
-  PcSmallSmem& ss = *reinterpret_cast<PcSmallSmem*>(pc_smem);
+  PgSmem& sm = *reinterpret_cast<PgSmem*>(pc_smem);
+  PcSmallSmem& ss = *reinterpret_cast<PcSmallSmem*>(pc_smem + sizeof(PgSmem));  // disjoint: staged during the SYRK
   if (*(volatile int*)fail >= 0) return;  // uniform across the grid
   const int nblk = (bk + PC_BLK - 1) / PC_BLK;
   const int G = gridDim.x, cta = blockIdx.x;
@@ -246,7 +319,7 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
         const int r = s + 1 + item;
         RowMajorK a{blk(A, b, r, s), b, rows_of(r), w};
         RowMajorK d{dinv, PC_BLK, PC_BLK, w};
-        dgemm_64x64(a, d, w, sm, acc);
+        pgemm_64(a, d, w, sm, acc);
         double* out = blk(A, b, r, s);
         const int rr = rows_of(r);
         dg_for_each(acc, [&](int i, int j, double v) {
@@ -256,7 +329,7 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
         const int c = item - n_trsm;
         RowMajorK d{dinv, PC_BLK, w, w};
         KMajor rsc{blk(Linv, b, s, c), b, rows_of(c), w};
-        dgemm_64x64(d, rsc, w, sm, acc);
+        pgemm_64(d, rsc, w, sm, acc);
         double* out = blk(Linv, b, s, c);
         const int cc = rows_of(c);
         dg_for_each(acc, [&](int i, int j, double v) {
@@ -272,15 +345,23 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
     // ---- phase B ----
     if (cta == 0) {
       if (s + 1 < nblk) {
-        const int r = s + 1, rr = rows_of(r);
+        // Lookahead block: A_rr -= X_rs X_rs^T straight into shared memory
+        // (A_rr staged by cp.async while the SYRK runs), then factor+invert.
+        const int r = s + 1, rr = rows_of(r), j0 = r * PC_BLK;
+        for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+          const int ri = e >> 6, ci = e & 63;
+          const bool in = ri < rr && ci <= ri;
+          cp_async8(&ss.T[ri][ci], in ? A + (int64_t)(j0 + ri) * b + j0 + ci : A, in ? 8 : 0);
+        }
+        cp_async_commit();
         RowMajorK x1{blk(A, b, r, s), b, rr, w};
-        dgemm_64x64(x1, x1, w, sm, acc);
-        double* out = blk(A, b, r, r);
+        pgemm_64(x1, x1, w, sm, acc);  // waits for every cp.async group, incl. the staging
         dg_for_each(acc, [&](int i, int j, double v) {
-          if (i < rr && j <= i) out[(int64_t)i * b + j] -= v;
+          if (i < rr && j <= i) ss.T[i][j] -= v;
         });
+        if (threadIdx.x >= rr && threadIdx.x < 64) ss.T[threadIdx.x][threadIdx.x] = 1.0;
         __syncthreads();
-        if (!pc_small(A, b, r * PC_BLK, rr, dinv_all + (int64_t)r * PC_BLK * PC_BLK, ss) && threadIdx.x == 0)
+        if (!pc_small_finish(A, b, j0, rr, dinv_all + (int64_t)r * PC_BLK * PC_BLK, ss) && threadIdx.x == 0)
           atomicCAS(fail, -1, k);
       }
     }
@@ -297,7 +378,7 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
           const int r = s + 1 + ri, c = s + 1 + ci;
           RowMajorK x1{blk(A, b, r, s), b, rows_of(r), w};
           RowMajorK x2{blk(A, b, c, s), b, rows_of(c), w};
-          dgemm_64x64(x1, x2, w, sm, acc);
+          pgemm_64(x1, x2, w, sm, acc);
           double* out = blk(A, b, r, c);
           const int rr = rows_of(r), cc = rows_of(c);
           dg_for_each(acc, [&](int i, int j, double v) {
@@ -308,7 +389,7 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
           const int r = s + 1 + q / (s + 1), c = q % (s + 1);
           RowMajorK l{blk(A, b, r, s), b, rows_of(r), w};
           KMajor x{blk(Linv, b, s, c), b, rows_of(c), w};
-          dgemm_64x64(l, x, w, sm, acc);
+          pgemm_64(l, x, w, sm, acc);
           double* out = blk(Linv, b, r, c);
           const int rr = rows_of(r), cc = rows_of(c);
           dg_for_each(acc, [&](int i, int j, double v) {
@@ -330,8 +411,6 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
   }
 }
 
-inline size_t potrf_coop_smem() {
-  return sizeof(PcSmallSmem) > sizeof(DgSmem) ? sizeof(PcSmallSmem) : sizeof(DgSmem);
-}
+inline size_t potrf_coop_smem() { return sizeof(PgSmem) + sizeof(PcSmallSmem); }
 
 }  // namespace sphemu_gpu

@@ -46,7 +46,7 @@ int main() {
       unsigned long long t0 = ~0ull;
       for (int c = 0; c < 32; ++c)
         if (t[c * 64] && t[c * 64] < t0) t0 = t[c * 64];
-      for (int slot = 0; slot < 36; ++slot) {
+      for (int slot = 0; slot < 48; ++slot) {
         unsigned long long mn = ~0ull, mx = 0, c0 = t[slot];
         for (int c = 0; c < 32; ++c) {
           unsigned long long v = t[c * 64 + slot];
