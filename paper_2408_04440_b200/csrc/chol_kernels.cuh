@@ -98,7 +98,7 @@ static __global__ void k_load_dense(TileStore ts, const double* __restrict__ a, 
 // TiledMatrix::to_dense_lower (mpchol.cpp:140-154): lower part from the
 // tiles, exact zeros above the diagonal. One thread per output element.
 static __global__ void k_store_dense(TileStore ts, double* __restrict__ out, int64_t ldo) {
-  const int R = blockIdx.y;
+  for (int R = blockIdx.y; R < ts.n; R += gridDim.y)  // gridDim.y <= 65535
   for (int Cc = blockIdx.x * blockDim.x + threadIdx.x; Cc < ts.n; Cc += gridDim.x * blockDim.x) {
     double v = 0.0;
     if (Cc <= R) {

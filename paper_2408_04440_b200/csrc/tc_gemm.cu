@@ -754,7 +754,7 @@ struct StepLists {
 
 void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, const int2* d_lo,
                    int64_t n_lo, const double* linv, double* p64, PanelFormats& pf, const int* fail,
-                   unsigned* sat, cudaStream_t s) {
+                   unsigned* sat, cudaStream_t s, int max_ctas) {
   const int b = ts.b;
   if (n_dp) {
     k_panel_trsm_fp64_list<<<dim3(static_cast<unsigned>(n_dp * (b / DG_BM)), b / DG_BN), DG_THREADS, 0, s>>>(
@@ -788,7 +788,7 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
     a.hp_format = pf.hp_format;
     a.fail = fail;
     a.sat = sat;
-    launch_tc<128, OP_TF32X3, MODE_PANEL>(pf.m_inhi_a, pf.m_inlo_a, pf.m_lhi_b, pf.m_llo_b, pf.m_lhi_b, a, s);
+    launch_tc<128, OP_TF32X3, MODE_PANEL>(pf.m_inhi_a, pf.m_inlo_a, pf.m_lhi_b, pf.m_llo_b, pf.m_lhi_b, a, s, max_ctas);
   }
 }
 
