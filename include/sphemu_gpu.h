@@ -147,7 +147,8 @@ int sphemu_gpu_chol_residual_probe_spd(sphemu_chol_t h, uint64_t seed, int n_vec
 int sphemu_gpu_chol_flops(sphemu_chol_t h, double* f_dp, double* f_sp, double* f_hp);
 /* Phase profiling (CUDA events around every phase; off by default). Phases:
  * 0 POTRF+TRTRI, 1 panel TRSM, 2/3/4 trailing update of the DP/SP/HP
- * classes, 5 tile load. ms/counts have 6 entries. */
+ * classes, 5 tile load. ms/counts have 6 entries. on = 1 records every
+ * phase; on = 0x100 | mask records only the phases whose bit is set. */
 int sphemu_gpu_chol_set_profiling(sphemu_chol_t h, int on);
 int sphemu_gpu_chol_phase_times(sphemu_chol_t h, double* ms, int64_t* counts, int reset);
 /* Timeline of the last profiled factorization: one span per phase launch

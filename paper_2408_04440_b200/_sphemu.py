@@ -269,8 +269,12 @@ class Cholesky:
 
     PHASES = ("potrf", "panel", "update_dp", "update_sp", "update_hp", "load")
 
-    def set_profiling(self, on=True):
-        _check(lib().sphemu_gpu_chol_set_profiling(self.h, 1 if on else 0))
+    def set_profiling(self, on=True, phases=None):
+        """Record phase times; phases (names of PHASES) limits which."""
+        v = 1 if on else 0
+        if on and phases is not None:
+            v = 0x100 | sum(1 << self.PHASES.index(p) for p in phases)
+        _check(lib().sphemu_gpu_chol_set_profiling(self.h, v))
 
     def phase_times(self, reset=False):
         ms = np.zeros(6)

@@ -333,6 +333,7 @@ struct Chol {
   // launch, folded into per-phase totals at wait().
   enum Phase { kPotrf = 0, kPanel = 1, kUpdDp = 2, kUpdSp = 3, kUpdHp = 4, kLoad = 5, kNumPhases = 6 };
   bool profiling = false;
+  unsigned prof_mask = 0x3f;  // phases recorded while profiling
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, int>> ev_marks;  // (phase, start event index)
   struct Span {
@@ -344,7 +345,7 @@ struct Chol {
   int64_t phase_n[kNumPhases] = {0};
   int prof_begin(int phase, cudaStream_t s = nullptr) {
     if (!s) s = stream;
-    if (!profiling) return -1;
+    if (!profiling || !(prof_mask & (1u << phase))) return -1;
     const size_t idx = ev_marks.size() * 2;
     while (ev_pool.size() < idx + 2) {
       cudaEvent_t e;
@@ -446,12 +447,12 @@ struct Chol {
   }
 
   // Column k of the factor is final on stream s: convert and copy it out.
-  void col_out(int k, cudaStream_t s) {
+  void col_out(int k, cudaStream_t s, const TileStore* from = nullptr) {
     if (!hout) return;
     SPH_CUDA(cudaEventRecord(ev_col, s));
     SPH_CUDA(cudaStreamWaitEvent(dstream, ev_col, 0));
     const int h = n - k * lb;
-    k_store_col<<<h, 128, 0, dstream>>>(store(), k, oslab.get());
+    k_store_col<<<h, 128, 0, dstream>>>(from ? *from : store(), k, oslab.get());
     SPH_LAUNCH_CHECK();
     SPH_CUDA(cudaMemcpy2DAsync(hout + static_cast<int64_t>(k) * lb * hldo + static_cast<int64_t>(k) * lb,
                                sizeof(double) * hldo, oslab.get(), sizeof(double) * lb, sizeof(double) * rows(k), h,
@@ -932,14 +933,8 @@ struct Chol {
   }
 
   void store_dense(double* out, int where, int64_t ldo) {
-    DevBuf<double> staging;
     double* dptr = out;
     int64_t ld = ldo;
-    if (where == SPHEMU_HOST && dist() && rank == 0) {
-      staging.alloc(static_cast<size_t>(n) * n);
-      dptr = staging.get();
-      ld = n;
-    }
     const int threads = 256;
     dim3 grid(std::max(1, std::min(ceil_div(n, threads), 64)), static_cast<unsigned>(std::min(n, 65535)));
     if (dist()) {
@@ -981,6 +976,12 @@ struct Chol {
       }
       if (rank == 0) {
         TileStore gs{full.get(), goff.get(), d_prec.get(), n, b, nt, lb};
+        if (where == SPHEMU_HOST) {  // stream the gathered tiles out by columns (lower triangle only)
+          begin_host_out(out, ldo);
+          for (int k = 0; k < nt; ++k) col_out(k, stream, &gs);
+          end_host_out();
+          return;
+        }
         k_store_dense<<<grid, threads, 0, stream>>>(gs, dptr, ld);
         SPH_LAUNCH_CHECK();
       }
@@ -995,9 +996,6 @@ struct Chol {
       k_store_dense<<<grid, threads, 0, stream>>>(store(), dptr, ld);
       SPH_LAUNCH_CHECK();
     }
-    if (where == SPHEMU_HOST)
-      SPH_CUDA(cudaMemcpy2DAsync(out, sizeof(double) * ldo, dptr, sizeof(double) * n,
-                                 sizeof(double) * n, n, cudaMemcpyDeviceToHost, stream));
     SPH_CUDA(cudaStreamSynchronize(stream));
   }
 
@@ -1264,7 +1262,10 @@ int sphemu_gpu_chol_residual_probe_spd(sphemu_chol_t h, uint64_t seed, int n_vec
 }
 
 int sphemu_gpu_chol_set_profiling(sphemu_chol_t h, int on) {
-  return guard([&] { h->c->profiling = on != 0; });
+  return guard([&] {
+    h->c->profiling = on != 0;
+    h->c->prof_mask = (on & 0x100) ? static_cast<unsigned>(on & 0x3f) : 0x3fu;
+  });
 }
 
 int sphemu_gpu_chol_phase_times(sphemu_chol_t h, double* ms, int64_t* counts, int reset) {
