@@ -12,6 +12,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -317,6 +318,17 @@ struct Chol {
   DevBuf<unsigned> sat;
   DevBuf<int2> lists;
   DevBuf<int> lrows;  // per update-list entry: the C tile's arena row (see constructor)
+  // Dynamic work claiming for the persistent tcgen05 kernels: one counter per
+  // stream (kernels on one stream run in order; the memset precedes each
+  // launch). SPHEMU_TC_DYN=0 falls back to static striding.
+  DevBuf<int> sched_ctr;
+  int* ctr(cudaStream_t s) {
+    static const bool on = [] {
+      const char* e = std::getenv("SPHEMU_TC_DYN");
+      return !(e && e[0] == '0');
+    }();
+    return on ? sched_ctr.get() + (s == pstream ? 1 : 0) : nullptr;
+  }
   // Update lists per (step k, part, class): part 0 = next column (k+1, the
   // critical chain), part 1 = the rest (columns >= k+2, the bulk).
   std::vector<int64_t> list_off, list_cnt;  // [(k * 2 + part) * 3 + class]
@@ -507,6 +519,7 @@ struct Chol {
       for (int p = 0; p < 2; ++p) p64_[p].alloc(static_cast<size_t>(nt - 1) * b * b);
     fail.alloc(1);
     sat.alloc(1);
+    sched_ctr.alloc(2);
     // Per-step output-tile lists by precision class.
     list_off.assign(static_cast<size_t>(nt) * 6 + 1, 0);
     list_cnt.assign(static_cast<size_t>(nt) * 6, 0);
@@ -681,7 +694,7 @@ struct Chol {
     if (cfg.compute == SPHEMU_COMPUTE_TENSOR) {
       const int2* base = plists.get() + plist_off[k];
       tc_panel_trsm(store(), k, base, plist_dp[k], base + plist_dp[k], plist_lo[k], linv_[set].get(),
-                    p64_[set].get(), panel_[set], fail.get(), sat.get(), s, max_ctas);
+                    p64_[set].get(), panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s));
     } else {
       const int below = nt - k - 1;
       k_panel_trsm_fp64<<<dim3(below * (b / DG_BM), b / DG_BN), DG_THREADS, 0, s>>>(
@@ -704,7 +717,7 @@ struct Chol {
       const int pu = prof_begin(kUpdDp + cls, s);
       if (cls != SPHEMU_PREC_DP && cfg.compute == SPHEMU_COMPUTE_TENSOR) {
         tc_update(store(), k, cls, cfg.hp_format, lst, lrows.get() + list_off[slot], cnt, p64_[set].get(),
-                  panel_[set], fail.get(), sat.get(), s, max_ctas);
+                  panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s));
       } else {
         if (b % D2_BM == 0) {
           static bool attr = false;

@@ -135,6 +135,7 @@ struct TcArgs {
   unsigned* sat;
   int dbg;           // diagnostics only (SPHEMU_TC_DBG): 1 = skip the C epilogue, 2 = also skip the MMAs
   int opt;           // tuning switches (SPHEMU_TC_OPT): 1 = no C prefetch to L2, 2 = prefetch two items ahead
+  int* counter;      // non-null: items are claimed dynamically (atomicAdd), zeroed before the launch
 };
 
 template <int OPK>
@@ -171,7 +172,7 @@ struct TcLayout {
                                      : (232448 - 1536 - TC_EPI_WARPS * kRing * 32 * 128) / kStage;
   static constexpr int kCBox = 32 * 128;
   static constexpr int kCBytes = TC_EPI_WARPS * kRing * kCBox;
-  static constexpr int kSmem = kStages * kStage + kCBytes + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int kSmem = kStages * kStage + kCBytes + 1024 /*align*/ + 1024 /*barriers + schedule*/;
   static constexpr int kTmemCols = 2 * BN;        // double-buffered accumulator
   static_assert(kSmem <= 232448, "shared memory budget");
 };
@@ -193,7 +194,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint64_t* cfull = tempty + 2;  // [epilogue warp][kRing]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(cfull + TC_EPI_WARPS * Lay::kRing);
+  uint64_t* sfull = cfull + TC_EPI_WARPS * Lay::kRing;  // dynamic schedule ring: producer -> consumers
+  uint64_t* sempty = sfull + 4;                          // consumers (MMA warp + epilogue warps) -> producer
+  int* sched = reinterpret_cast<int*>(sempty + 4);       // [4] claimed items (-1 = none left)
+  int* wcache = sched + 4;                               // [TC_EPI_WARPS][4] epilogue copies
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(wcache + TC_EPI_WARPS * 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (*(volatile const int*)args.fail >= 0) return;  // an earlier POTRF failed (both CTAs of a pair see it)
@@ -210,6 +215,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&tempty[a], CG * TC_EPI_WARPS);  // one arrive per epilogue warp of each CTA
     }
     for (int s = 0; s < TC_EPI_WARPS * Lay::kRing; ++s) mbar_init(&cfull[s], 1);
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], 1 + TC_EPI_WARPS);
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -233,6 +242,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int kblocks = args.b / T::kBK;
   const int64_t items = args.items;
+  // Work items: statically strided over clusters, or (CG = 1 with a counter)
+  // claimed one by one by the producer and handed to the MMA and epilogue
+  // warps through a 4-slot ring, so CTAs that start late (SMs still held by a
+  // concurrent kernel) simply find less work left.
+  const bool dyn = CG == 1 && args.counter != nullptr;
+  auto static_item = [&](int64_t n) -> int64_t {
+    const int64_t w = cid + n * ncl;
+    return w < items ? w : -1;
+  };
+  auto ring_take = [&](int64_t n) -> int64_t {  // consumer side; caller decides who arrives
+    const int slot = static_cast<int>(n & 3);
+    mbar_wait(&sfull[slot], static_cast<uint32_t>((n >> 2) & 1));
+    return static_cast<int64_t>(*(volatile int*)&sched[slot]);
+  };
 
   auto decode = [&](int64_t w, int& i, int& j, int& m0, int& n0) {
     const int2 ij = args.list[w / args.sub_per];
@@ -267,20 +290,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll 1
           for (int cx = 0; cx < BN; cx += 128 / kEszP) tma_prefetch_l2_2d(&mC, tn + cx, crow + tm + rq);
       };
-      int2 ij_cur = cid < items ? args.list[cid / args.sub_per] : make_int2(0, 0);
-      int crow_cur = (MODE == MODE_UPDATE && cid < items) ? args.crow[cid / args.sub_per] : 0;
-      prefetch_c(cid, ij_cur, crow_cur);
-      for (int64_t w = cid; w < items; w += ncl) {
+      auto fetch = [&]() -> int64_t {
+        const int64_t v = atomicAdd(args.counter, 1);
+        return v < items ? v : -1;
+      };
+      auto publish = [&](int64_t n, int64_t v) {
+        const int slot = static_cast<int>(n & 3);
+        mbar_wait(&sempty[slot], static_cast<uint32_t>(((n >> 2) & 1) ^ 1));
+        sched[slot] = static_cast<int>(v);
+        mbar_arrive(&sfull[slot]);  // release: the slot write is visible to the consumers
+      };
+      int64_t w = dyn ? fetch() : static_item(0);
+      if (dyn) publish(0, w);
+      int2 ij_cur = w >= 0 ? args.list[w / args.sub_per] : make_int2(0, 0);
+      int crow_cur = (MODE == MODE_UPDATE && w >= 0) ? args.crow[w / args.sub_per] : 0;
+      prefetch_c(w >= 0 ? w : items, ij_cur, crow_cur);
+      for (int64_t n = 0; w >= 0; ++n) {
+        const int64_t w_next = dyn ? fetch() : static_item(n + 1);
+        if (dyn) publish(n + 1, w_next);
         const int sub = static_cast<int>(w % args.sub_per);
         const int i = ij_cur.x, j = ij_cur.y;
         const int m0 = (sub / args.sub_n) * (TC_BM * CG) + static_cast<int>(rank) * TC_BM;
         const int n0 = (sub % args.sub_n) * BN;
         int2 ij_nxt = ij_cur;
         int crow_nxt = crow_cur;
-        const bool more = w + ncl < items;
+        const bool more = w_next >= 0;
         if (more) {
-          ij_nxt = args.list[(w + ncl) / args.sub_per];
-          if (MODE == MODE_UPDATE) crow_nxt = args.crow[(w + ncl) / args.sub_per];
+          ij_nxt = args.list[w_next / args.sub_per];
+          if (MODE == MODE_UPDATE) crow_nxt = args.crow[w_next / args.sub_per];
         }
         const int a_row = (i - args.k - 1) * args.b + m0;
         const int b_row = (MODE == MODE_UPDATE) ? (j - args.k - 1) * args.b + n0 + static_cast<int>(rank) * (BN / CG)
@@ -308,7 +345,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               tma_load_2d(&mB_lo, &full[stage], st + 2 * Lay::kA + Lay::kB, kx, b_row);
             }
           }
-          if (kb == 1 && more) prefetch_c(w + ncl, ij_nxt, crow_nxt);
+          if (kb == 1 && more) prefetch_c(w_next, ij_nxt, crow_nxt);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -316,6 +353,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         ij_cur = ij_nxt;
         crow_cur = crow_nxt;
+        w = w_next;
       }
     }
   } else if (warp == 1 && rank == 0) {
@@ -325,7 +363,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t w = cid; w < items; w += ncl) {
+    for (int64_t n = 0;; ++n) {
+      int64_t w;
+      if (dyn) {
+        w = ring_take(n);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[n & 3]);
+      } else {
+        w = static_item(n);
+      }
+      if (w < 0) break;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + acc * BN;
@@ -404,9 +451,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint64_t* cf = cfull + (warp - 4) * R;
     int64_t gbox = 0, gissue = 0;  // next box to process / to load (sequence over this CTA's items)
     auto c_row = [&](int64_t wi) { return args.crow[wi / args.sub_per]; };  // tile's first arena row
+    int* wc = wcache + (warp - 4) * 4;
+    int64_t rn = 0;  // items read from the schedule ring so far (lane 0)
+    auto item_lane0 = [&](int64_t idx) -> int64_t {  // lane 0 only
+      if (dyn) {
+        for (; rn <= idx; ++rn) {
+          wc[rn & 3] = static_cast<int>(ring_take(rn));
+          mbar_arrive(&sempty[rn & 3]);
+        }
+        return wc[idx & 3];
+      }
+      return static_item(idx);
+    };
     auto issue_c = [&]() {  // lane 0: TMA-load the next C box into its ring slot
-      const int64_t wi = cid + (gissue / kNBox) * ncl;
-      if (wi >= items) return;
+      const int64_t wi = item_lane0(gissue / kNBox);
+      if (wi < 0) return;
       const int bx = grp + 2 * static_cast<int>(gissue % kNBox);
       int ti, tj, tm, tn;
       decode(wi, ti, tj, tm, tn);
@@ -417,7 +476,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     };
     if (MODE == MODE_UPDATE && lane == 0 && (args.dbg == 0 || args.dbg >= 3) && args.dbg != 5)
       for (int s = 0; s < R; ++s) issue_c();
-    for (int64_t w = cid; w < items; w += ncl) {
+    for (int64_t n = 0;; ++n) {
+      if (lane == 0) item_lane0(n);
+      __syncwarp();
+      const int64_t w = dyn ? static_cast<int64_t>(*(volatile int*)&wc[n & 3]) : static_item(n);
+      __syncwarp();  // every lane has read the cache before lane 0 may overwrite it
+      if (w < 0) break;
       int i, j, m0, n0;
       decode(w, i, j, m0, n0);
       void* tp = args.ts.tile(i, j);
@@ -720,6 +784,7 @@ void launch_tc(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorM
     SPH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::kSmem));
     attr = true;
   }
+  if (args.counter) SPH_CUDA(cudaMemsetAsync(args.counter, 0, sizeof(int), s));
   const int cap = (max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms()) / CG;
   const int grid = CG * static_cast<int>(std::min<int64_t>(args.items, std::max(1, cap)));
   if constexpr (CG == 1) {
@@ -754,7 +819,7 @@ struct StepLists {
 
 void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, const int2* d_lo,
                    int64_t n_lo, const double* linv, double* p64, PanelFormats& pf, const int* fail,
-                   unsigned* sat, cudaStream_t s, int max_ctas) {
+                   unsigned* sat, cudaStream_t s, int max_ctas, int* counter) {
   const int b = ts.b;
   if (n_dp) {
     k_panel_trsm_fp64_list<<<dim3(static_cast<unsigned>(n_dp * (b / DG_BM)), b / DG_BN), DG_THREADS, 0, s>>>(
@@ -788,13 +853,14 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
     a.hp_format = pf.hp_format;
     a.fail = fail;
     a.sat = sat;
+    a.counter = counter;
     launch_tc<128, OP_TF32X3, MODE_PANEL>(pf.m_inhi_a, pf.m_inlo_a, pf.m_lhi_b, pf.m_llo_b, pf.m_lhi_b, a, s, max_ctas);
   }
 }
 
 void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* list, const int* rows, int64_t cnt,
                const double* p64, PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s,
-               int max_ctas) {
+               int max_ctas, int* counter) {
   (void)p64;
   TcArgs a{};
   a.ts = ts;
@@ -812,6 +878,7 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
     return e ? std::atoi(e) : 0;
   }();
   a.dbg = dbg;
+  a.counter = counter;
   static const int opt = [] {
     const char* e = std::getenv("SPHEMU_TC_OPT");
     return e ? std::atoi(e) : 0;

@@ -49,12 +49,12 @@ struct PanelFormats {
 // mirrors, and the tile storage.
 void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, const int2* d_lo,
                    int64_t n_lo, const double* linv, double* p64, PanelFormats& pf, const int* fail,
-                   unsigned* sat, cudaStream_t s, int max_ctas = 0);
+                   unsigned* sat, cudaStream_t s, int max_ctas = 0, int* counter = nullptr);
 
 // Trailing update of the SP (cls 1) or HP (cls 2) output tiles of step k.
 void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* list, const int* rows, int64_t cnt,
                const double* p64, PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s,
-               int max_ctas = 0);
+               int max_ctas = 0, int* counter = nullptr);
 
 // Host-side inputs of make_spd_test_matrix: d_i = exp(0.6 u_i - 0.3) with the
 // reference's GaussianRng uniform stream, pw[k] = std::pow(0.9, k).
