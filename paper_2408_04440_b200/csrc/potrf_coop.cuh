@@ -23,15 +23,16 @@ struct PcSmallSmem {
   double T[64][65];
   double Di[64][65];
   double M[32][33];
+  double col[17];  // base-case column broadcast
   int bad;
 };
 
-// 16 x 16 base case in registers (warp 0; lanes 0..15 own the rows):
-// right-looking Cholesky with one rsqrt per column, then the inverse by
-// right-looking forward substitution (lane j owns column j). Small unrolled
-// code (the 32-wide version thrashed the instruction cache).
+// 16 x 16 base case (warp 0; lanes 0..15 own the rows): right-looking
+// Cholesky with one rsqrt per column, the factored column broadcast through
+// shared memory (s.col), then the inverse by forward substitution (lane j owns
+// column j, reading L from s.T). Small unrolled code: the cooperative kernel
+// is sensitive to instruction-cache pressure.
 __device__ __noinline__ void pc_base16(PcSmallSmem& s, int o, int w, int lane) {
-  constexpr unsigned FULL = 0xffffffffu;
   const int row = lane & 15;
   double a[16], rl[16];
 #pragma unroll
@@ -39,13 +40,18 @@ __device__ __noinline__ void pc_base16(PcSmallSmem& s, int o, int w, int lane) {
   bool ok = true;
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
-    const double piv = __shfl_sync(FULL, a[c], c);
+    if (lane == c) s.col[16] = a[c];
+    __syncwarp();
+    const double piv = s.col[16];
     if (c < w && !(piv > 0.0)) ok = false;
     rl[c] = rsqrt(piv);
     const double lrc = (row == c) ? piv * rl[c] : a[c] * rl[c];
     a[c] = lrc;
+    if (lane < 16) s.col[row] = lrc;
+    __syncwarp();
 #pragma unroll
-    for (int j = c + 1; j < 16; ++j) a[j] -= lrc * __shfl_sync(FULL, lrc, j);
+    for (int j = c + 1; j < 16; ++j) a[j] -= lrc * s.col[j];
+    __syncwarp();
   }
   if (!ok) {
     if (lane == 0) s.bad = 1;
@@ -54,6 +60,7 @@ __device__ __noinline__ void pc_base16(PcSmallSmem& s, int o, int w, int lane) {
   if (lane < 16)
 #pragma unroll
     for (int t = 0; t < 16; ++t) s.T[o + lane][o + t] = t <= lane ? a[t] : 0.0;
+  __syncwarp();
   double x[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) x[i] = (i == row) ? 1.0 : 0.0;
@@ -61,7 +68,7 @@ __device__ __noinline__ void pc_base16(PcSmallSmem& s, int o, int w, int lane) {
   for (int r = 0; r < 16; ++r) {
     x[r] *= rl[r];
 #pragma unroll
-    for (int i = r + 1; i < 16; ++i) x[i] -= __shfl_sync(FULL, a[r], i) * x[r];
+    for (int i = r + 1; i < 16; ++i) x[i] -= s.T[o + i][o + r] * x[r];
   }
   if (lane < 16)
 #pragma unroll
@@ -186,6 +193,7 @@ constexpr int PG_LD = 68;
 struct PgSmem {
   double a[64 * PG_LD];
   double b[64 * PG_LD];
+  double c[64 * PG_LD];  // read-modify-write target of pgemm_64_rmw
 };
 
 template <class Acc>
@@ -233,6 +241,31 @@ __device__ __forceinline__ void pgemm_64(const AccA& A, const AccB& B, int K, Pg
       for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
   }
   __syncthreads();  // smem reusable by the caller
+}
+
+// out -= A B^T on the elements keep(i, j) selects: the 64 x 64 output block is
+// staged by cp.async together with the operands, updated in shared memory and
+// written back with coalesced 16-byte stores (the whole block: elements the
+// mask skips are written back unchanged; every block has one owner per phase).
+template <class AccA, class AccB, class Keep>
+__device__ __forceinline__ void pgemm_64_rmw(const AccA& A, const AccB& B, int K, double* out, int64_t ld,
+                                             PgSmem& sm, Keep keep) {
+  for (int e = threadIdx.x; e < 64 * 32; e += blockDim.x) {
+    const int row = e >> 5, col = (e & 31) * 2;
+    cp_async16(sm.c + row * PG_LD + col, out + (int64_t)row * ld + col, 16);
+  }
+  double acc[4][4][2];
+  pgemm_64(A, B, K, sm, acc);  // its cp.async wait covers the staging above
+  dg_for_each(acc, [&](int i, int j, double v) {
+    if (keep(i, j)) sm.c[i * PG_LD + j] -= v;
+  });
+  __syncthreads();
+  for (int e = threadIdx.x; e < 64 * 32; e += blockDim.x) {
+    const int row = e >> 5, col = (e & 31) * 2;
+    *reinterpret_cast<double2*>(out + (int64_t)row * ld + col) =
+        *reinterpret_cast<const double2*>(sm.c + row * PG_LD + col);
+  }
+  __syncthreads();
 }
 
 // Factor + invert the 64 x 64 block already staged in s.T (lower part, zero
@@ -378,23 +411,16 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
           const int r = s + 1 + ri, c = s + 1 + ci;
           RowMajorK x1{blk(A, b, r, s), b, rows_of(r), w};
           RowMajorK x2{blk(A, b, c, s), b, rows_of(c), w};
-          pgemm_64(x1, x2, w, sm, acc);
-          double* out = blk(A, b, r, c);
           const int rr = rows_of(r), cc = rows_of(c);
-          dg_for_each(acc, [&](int i, int j, double v) {
-            if (i < rr && j < cc && (r != c || j <= i)) out[(int64_t)i * b + j] -= v;
-          });
+          pgemm_64_rmw(x1, x2, w, blk(A, b, r, c), b, sm,
+                       [&](int i, int j) { return i < rr && j < cc && (r != c || j <= i); });
         } else {
           const int q = item - (pairs - 1);
           const int r = s + 1 + q / (s + 1), c = q % (s + 1);
           RowMajorK l{blk(A, b, r, s), b, rows_of(r), w};
           KMajor x{blk(Linv, b, s, c), b, rows_of(c), w};
-          pgemm_64(l, x, w, sm, acc);
-          double* out = blk(Linv, b, r, c);
           const int rr = rows_of(r), cc = rows_of(c);
-          dg_for_each(acc, [&](int i, int j, double v) {
-            if (i < rr && j < cc) out[(int64_t)i * b + j] -= v;
-          });
+          pgemm_64_rmw(l, x, w, blk(Linv, b, r, c), b, sm, [&](int i, int j) { return i < rr && j < cc; });
         }
         __syncthreads();
       }
