@@ -459,6 +459,40 @@ def sht_throughput(sph, world):
             "legendre_fp64_tflops_per_gpu": sht_flops / (sht_ms * 1e-3) / 1e12, "round_trip_max_abs": sht_rt}
 
 
+def sht_c4(sph, snapshots=1000):
+    """BASELINE configs[3] (C4): 721 x 1440 grid (720 x 1440 cannot resolve L = 720), L = 720,
+    forward and inverse timed separately on a device-resident batch."""
+    import torch
+    nt, nphi, L = 721, 1440, 720
+    t0 = time.perf_counter()
+    plan = sph.ShtPlan(nt, nphi, L, wigner_cap_bytes=8 << 30)  # the reference's 2 GiB cap rejects L = 720 (F5)
+    plan_s = time.perf_counter() - t0
+    coef = torch.randn(snapshots, L * L, dtype=torch.float64, device="cuda")
+    fld = torch.empty(snapshots, nt, nphi, dtype=torch.float64, device="cuda")
+    back = torch.empty_like(coef)
+    plan.inverse_device(coef.data_ptr(), snapshots, fld.data_ptr())
+    plan.forward_device(fld.data_ptr(), snapshots, back.data_ptr())
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    plan.inverse_device(coef.data_ptr(), snapshots, fld.data_ptr())
+    ev[1].record()
+    plan.forward_device(fld.data_ptr(), snapshots, back.data_ptr())
+    ev[2].record()
+    torch.cuda.synchronize()
+    inv_ms, fwd_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+    flops = 2 * nt * L * (L + 1) * snapshots
+    rt = ((back - coef).abs().max() / coef.abs().max()).item()
+    del coef, fld, back, plan
+    torch.cuda.empty_cache()
+    return {"grid": f"{nt}x{nphi}", "band_limit": L, "snapshots": snapshots,
+            "forward_snapshots_per_s": snapshots / (fwd_ms * 1e-3),
+            "inverse_snapshots_per_s": snapshots / (inv_ms * 1e-3),
+            "legendre_fp64_tflops_forward": flops / (fwd_ms * 1e-3) / 1e12,
+            "plan_build_s": plan_s, "round_trip_rel": rt,
+            "note": "the driver's 8 760-snapshot hourly year runs in chunks of this batch"}
+
+
 def run_ours(args, world, rank, local):
     import torch
 
@@ -501,6 +535,7 @@ def run_ours(args, world, rank, local):
         torch.cuda.empty_cache()
 
     sht = sht_throughput(sph, world)
+    c4 = sht_c4(sph) if (world == 1 and not args.no_c4) else None
 
     if rank != 0:
         return
@@ -543,6 +578,8 @@ def run_ours(args, world, rank, local):
     }
     if c3_1:
         line["c3_1gpu"] = c3_1
+    if c4:
+        line["sht_c4"] = c4
     print(json.dumps(line), flush=True)
 
 
@@ -559,6 +596,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c3", action="store_true", help="skip the 1-GPU C3 point on N=1")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the L=720 SHT point on N=1")
     ap.add_argument("--lookahead", type=int, default=1)
     ap.add_argument("--sp-compute", default="fp16x3", choices=["fp16x3", "tf32x3"])
     args = ap.parse_args()
