@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -214,8 +215,9 @@ __global__ void __launch_bounds__(DG_THREADS) k_sht_build_psi(const double* d, c
   const double sgn = ((m >> 1) & 1) ? -1.0 : 1.0;
   const double scale = sgn * 2.0 * 3.14159265358979323846;
   double* out = psi + psi_off[m];
+  const int ntp = (n_theta + 1) & ~1;  // even row stride (16-byte rows for the Legendre GEMM loader)
   dg_for_each(acc, [&](int r, int c, double v) {
-    if (r0 + r < rows && c0 + c < n_theta) out[(int64_t)(r0 + r) * n_theta + c0 + c] = scale * v;
+    if (r0 + r < rows && c0 + c < n_theta) out[(int64_t)(r0 + r) * ntp + c0 + c] = scale * v;
   });
 }
 
@@ -236,8 +238,9 @@ __global__ void __launch_bounds__(DG_THREADS) k_sht_build_y(const double* d, con
   dgemm_64x64(A, Bs, L, sm, acc);
   const double sgn = ((m >> 1) & 1) ? -1.0 : 1.0;
   double* out = y + y_off[m];
+  const int colsp = (cols + 1) & ~1;
   dg_for_each(acc, [&](int r, int c, double v) {
-    if (r0 + r < n_theta && c0 + c < cols) out[(int64_t)(r0 + r) * cols + c0 + c] = sgn * v;
+    if (r0 + r < n_theta && c0 + c < cols) out[(int64_t)(r0 + r) * colsp + c0 + c] = sgn * v;
   });
 }
 
@@ -256,8 +259,40 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
+// Generic radix p (O(p^2), p <= 64): kept out of line so the common
+// radix-2/3/4/5 path does not carry its register and local-memory footprint.
+template <int SIGN>
+__device__ __noinline__ void fft_generic_bfly(double2* base, int span, int p, int j, int tstep, const FftPlan& P) {
+  const int n = P.n;
+  double2 in[64];
+  const int pp = p <= 64 ? p : 64;
+  for (int r = 0; r < pp; ++r) in[r] = base[r * span];
+  for (int q = 0; q < pp; ++q) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int r = 0; r < pp; ++r) {
+      double2 w = P.tw[((int64_t)((r * q) % p) * (n / p)) % n];
+      if (SIGN > 0) w.y = -w.y;
+      const double2 v = cmul(in[r], w);
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    double2 w = P.tw[((int64_t)j * q * tstep) % n];
+    if (SIGN > 0) w.y = -w.y;
+    base[q * span] = cmul(acc, w);
+  }
+}
+
+// Exact t / d for t < 2^24 through a float reciprocal plus one correction step.
+__device__ __forceinline__ int fdiv(int t, int d, float inv) {
+  int q = static_cast<int>(static_cast<float>(t) * inv);
+  if (q * d > t) --q;
+  else if ((q + 1) * d <= t) ++q;
+  return q;
+}
+
 // One DIF pass over R rings held in x (R * n complex), sign -1 (analysis) or
-// +1 (synthesis, conjugated twiddles).
+// +1 (synthesis, conjugated twiddles). Twiddle indices of radix 2..5 stay
+// below n, so no modulo; butterfly coordinates use reciprocal divisions.
 template <int SIGN>
 __device__ void fft_dif_rings(double2* x, int R, const FftPlan& P) {
   const int n = P.n;
@@ -265,19 +300,20 @@ __device__ void fft_dif_rings(double2* x, int R, const FftPlan& P) {
   for (int s = 0; s < P.stages; ++s) {
     const int p = P.radix[s];
     const int span = len / p;
-    const int groups = n / len;
-    const int bfly = R * groups * span;
+    const int nb = n / p;  // butterflies per ring
+    const int bfly = R * nb;
+    const int tstep = n / len;
+    const float inv_nb = 1.0f / nb, inv_span = 1.0f / span;
     for (int t = threadIdx.x; t < bfly; t += blockDim.x) {
-      const int ring = t / (groups * span);
-      const int rem = t % (groups * span);
-      const int g = rem / span, j = rem % span;
+      const int ring = fdiv(t, nb, inv_nb);
+      const int rem = t - ring * nb;
+      const int g = fdiv(rem, span, inv_span), j = rem - g * span;
       double2* base = x + (int64_t)ring * n + g * len + j;
-      const int tstep = n / len;
       if (p == 2) {
         const double2 a = base[0], b = base[span];
         double2 y1 = make_double2(a.x - b.x, a.y - b.y);
         base[0] = make_double2(a.x + b.x, a.y + b.y);
-        double2 w = P.tw[(j * tstep) % n];
+        double2 w = P.tw[j * tstep];
         if (SIGN > 0) w.y = -w.y;
         base[span] = cmul(y1, w);
       } else if (p == 4) {
@@ -290,7 +326,7 @@ __device__ void fft_dif_rings(double2* x, int R, const FftPlan& P) {
         double2 y2 = make_double2(s02.x - s13.x, s02.y - s13.y);
         double2 y1 = make_double2(d02.x + rd13.x, d02.y + rd13.y);
         double2 y3 = make_double2(d02.x - rd13.x, d02.y - rd13.y);
-        double2 w1 = P.tw[(j * tstep) % n], w2 = P.tw[(2 * j * tstep) % n], w3 = P.tw[(3 * j * tstep) % n];
+        double2 w1 = P.tw[j * tstep], w2 = P.tw[2 * j * tstep], w3 = P.tw[3 * j * tstep];
         if (SIGN > 0) { w1.y = -w1.y; w2.y = -w2.y; w3.y = -w3.y; }
         base[0] = y0;
         base[span] = cmul(y1, w1);
@@ -303,7 +339,7 @@ __device__ void fft_dif_rings(double2* x, int R, const FftPlan& P) {
         const double h = 0.86602540378443864676 * (SIGN < 0 ? 1.0 : -1.0);
         const double2 m = make_double2(a0.x - 0.5 * t.x, a0.y - 0.5 * t.y);
         const double2 rd = make_double2(h * d.y, -h * d.x);  // -i s (sqrt3/2) d
-        double2 w1 = P.tw[(j * tstep) % n], w2 = P.tw[(2 * j * tstep) % n];
+        double2 w1 = P.tw[j * tstep], w2 = P.tw[2 * j * tstep];
         if (SIGN > 0) { w1.y = -w1.y; w2.y = -w2.y; }
         base[0] = make_double2(a0.x + t.x, a0.y + t.y);
         base[span] = cmul(make_double2(m.x + rd.x, m.y + rd.y), w1);
@@ -320,8 +356,7 @@ __device__ void fft_dif_rings(double2* x, int R, const FftPlan& P) {
         const double2 e1 = make_double2(s1 * d1.x + s2 * d2.x, s1 * d1.y + s2 * d2.y);
         const double2 e2 = make_double2(s2 * d1.x - s1 * d2.x, s2 * d1.y - s1 * d2.y);
         // -i e = (e.y, -e.x)
-        double2 w1 = P.tw[(j * tstep) % n], w2 = P.tw[(2 * j * tstep) % n], w3 = P.tw[(3 * j * tstep) % n],
-                w4 = P.tw[(4 * j * tstep) % n];
+        double2 w1 = P.tw[j * tstep], w2 = P.tw[2 * j * tstep], w3 = P.tw[3 * j * tstep], w4 = P.tw[4 * j * tstep];
         if (SIGN > 0) { w1.y = -w1.y; w2.y = -w2.y; w3.y = -w3.y; w4.y = -w4.y; }
         base[0] = make_double2(a0.x + b1.x + b2.x, a0.y + b1.y + b2.y);
         base[span] = cmul(make_double2(r1.x + e1.y, r1.y - e1.x), w1);
@@ -329,23 +364,7 @@ __device__ void fft_dif_rings(double2* x, int R, const FftPlan& P) {
         base[2 * span] = cmul(make_double2(r2.x + e2.y, r2.y - e2.x), w2);
         base[3 * span] = cmul(make_double2(r2.x - e2.y, r2.y + e2.x), w3);
       } else {
-        // generic radix p (O(p^2)); p <= 64 buffered in registers/local memory
-        double2 in[64];
-        const int pp = p <= 64 ? p : 64;
-        for (int r = 0; r < pp; ++r) in[r] = base[r * span];
-        for (int q = 0; q < pp; ++q) {
-          double2 acc = make_double2(0.0, 0.0);
-          for (int r = 0; r < pp; ++r) {
-            double2 w = P.tw[((int64_t)((r * q) % p) * (n / p)) % n];
-            if (SIGN > 0) w.y = -w.y;
-            const double2 v = cmul(in[r], w);
-            acc.x += v.x;
-            acc.y += v.y;
-          }
-          double2 w = P.tw[((int64_t)j * q * tstep) % n];
-          if (SIGN > 0) w.y = -w.y;
-          base[q * span] = cmul(acc, w);
-        }
+        fft_generic_bfly<SIGN>(base, span, p, j, tstep, P);
       }
     }
     __syncthreads();
@@ -364,55 +383,63 @@ __device__ __forceinline__ int fft_pos(int k, const FftPlan& P) {
   return pos;
 }
 
+// Ring stages work on one latitude ring of R consecutive snapshots per CTA, so
+// the staging G[m][i][s] (s = 2 t + {re, im} contiguous) is written and read
+// in runs of 2R doubles per (m, i).
+//
 // Forward ring stage (sht.cpp:211-222): fields (T, n_theta, n_phi) ->
-// G[m][s][i], s = 2 t + {re, im}, scaled by 1/n_phi. grid (ceil(n_theta/R), T).
+// G[m][i][s] scaled by 1/n_phi. grid (n_theta, ceil(T / R)).
 __global__ void k_ring_fft_fwd(const double* __restrict__ fields, int n_theta, int L, int R, FftPlan P,
                                int T, double* __restrict__ G) {
   extern __shared__ double2 xs[];
   const int n = P.n;
-  const int i0 = blockIdx.x * R, t = blockIdx.y;
-  const int rings = min(R, n_theta - i0);
-  const double* src = fields + ((int64_t)t * n_theta + i0) * n;
-  for (int e = threadIdx.x; e < rings * n; e += blockDim.x) xs[e] = make_double2(src[e], 0.0);
+  const int i = blockIdx.x, t0 = blockIdx.y * R;
+  const int nr = min(R, T - t0);
+  for (int e = threadIdx.x; e < nr * n; e += blockDim.x) {
+    const int r = e / n, j = e - r * n;
+    xs[e] = make_double2(fields[((int64_t)(t0 + r) * n_theta + i) * n + j], 0.0);
+  }
   __syncthreads();
-  fft_dif_rings<-1>(xs, rings, P);
+  fft_dif_rings<-1>(xs, nr, P);
   const double inv = 1.0 / n;
-  const int64_t sstride = (int64_t)2 * T * n_theta;  // per m
-  for (int e = threadIdx.x; e < L * 2 * rings; e += blockDim.x) {
-    const int r = e % rings, c = (e / rings) & 1, m = e / (2 * rings);
-    const double2 v = xs[r * n + fft_pos(m, P)];
-    G[(int64_t)m * sstride + (int64_t)(2 * t + c) * n_theta + i0 + r] = (c ? v.y : v.x) * inv;
+  const int ntp = (n_theta + 1) & ~1;
+  const int64_t mstride = (int64_t)ntp * 2 * T;
+  double* g = G + (int64_t)i * 2 * T + 2 * t0;
+  for (int e = threadIdx.x; e < L * 2 * nr; e += blockDim.x) {
+    const int m = e / (2 * nr), q = e - m * 2 * nr;  // q = 2 r + c
+    const double2 v = xs[(q >> 1) * n + fft_pos(m, P)];
+    g[m * mstride + q] = ((q & 1) ? v.y : v.x) * inv;
   }
 }
 
 // Inverse ring stage (sht.cpp:345-356): Hermitian fill, unnormalized
-// synthesis, real part. G[m][s][i] -> fields (T, n_theta, n_phi).
+// synthesis, real part. G[m][i][s] -> fields (T, n_theta, n_phi).
 __global__ void k_ring_fft_inv(const double* __restrict__ G, int n_theta, int L, int R, FftPlan P, int T,
                                double* __restrict__ fields) {
   extern __shared__ double2 xs[];
   const int n = P.n;
-  const int i0 = blockIdx.x * R, t = blockIdx.y;
-  const int rings = min(R, n_theta - i0);
-  const int64_t sstride = (int64_t)2 * T * n_theta;
-  for (int e = threadIdx.x; e < rings * n; e += blockDim.x) xs[e] = make_double2(0.0, 0.0);
+  const int i = blockIdx.x, t0 = blockIdx.y * R;
+  const int nr = min(R, T - t0);
+  const int ntp = (n_theta + 1) & ~1;
+  const int64_t mstride = (int64_t)ntp * 2 * T;
+  const double* g = G + (int64_t)i * 2 * T + 2 * t0;
+  for (int e = threadIdx.x; e < nr * n; e += blockDim.x) xs[e] = make_double2(0.0, 0.0);
   __syncthreads();
-  for (int e = threadIdx.x; e < rings * L; e += blockDim.x) {
-    const int r = e % rings, m = e / rings;
-    const double re = G[(int64_t)m * sstride + (int64_t)(2 * t) * n_theta + i0 + r];
-    const double im = G[(int64_t)m * sstride + (int64_t)(2 * t + 1) * n_theta + i0 + r];
+  for (int e = threadIdx.x; e < L * nr; e += blockDim.x) {
+    const int m = e / nr, r = e - m * nr;
+    const double2 z = *reinterpret_cast<const double2*>(g + m * mstride + 2 * r);
     if (m == 0) {
-      xs[r * n] = make_double2(re, im);
+      xs[r * n] = z;
     } else {
-      xs[r * n + m] = make_double2(re, im);
-      xs[r * n + n - m] = make_double2(re, -im);
+      xs[r * n + m] = z;
+      xs[r * n + n - m] = make_double2(z.x, -z.y);
     }
   }
   __syncthreads();
-  fft_dif_rings<+1>(xs, rings, P);
-  double* dst = fields + ((int64_t)t * n_theta + i0) * n;
-  for (int e = threadIdx.x; e < rings * n; e += blockDim.x) {
-    const int r = e / n, j = e % n;
-    dst[e] = xs[r * n + fft_pos(j, P)].x;
+  fft_dif_rings<+1>(xs, nr, P);
+  for (int e = threadIdx.x; e < nr * n; e += blockDim.x) {
+    const int r = e / n, j = e - r * n;
+    fields[((int64_t)(t0 + r) * n_theta + i) * n + j] = xs[r * n + fft_pos(j, P)].x;
   }
 }
 
@@ -431,10 +458,11 @@ __global__ void __launch_bounds__(D2_THREADS) k_legendre_fwd(const double* __res
   const int r0 = blockIdx.y * D2_BM, c0 = blockIdx.x * D2_BN;
   if (r0 >= rows) return;
   const int ncols = 2 * T;
-  D2Op A{psi + psi_off[m] + (int64_t)r0 * n_theta, n_theta, min(D2_BM, rows - r0), n_theta};
-  D2Op B{G + (int64_t)m * ncols * n_theta + (int64_t)c0 * n_theta, n_theta, min(D2_BN, ncols - c0), n_theta};
+  const int ntp = (n_theta + 1) & ~1;  // Psi rows padded with a zero column to an even stride: 16-byte cp.async
+  D2Op A{psi + psi_off[m] + (int64_t)r0 * ntp, ntp, min(D2_BM, rows - r0), ntp};
+  D2Op B{G + (int64_t)m * ntp * ncols + c0, ncols, ntp, min(D2_BN, ncols - c0)};  // G_m[i][s], K = i
   double acc[4][4][2];
-  dgemm2_128x64<D2B::kNT, false>(A, B, n_theta, sm, acc);
+  dgemm2_128x64<D2B::kNN, true>(A, B, ntp, sm, acc);
   const int64_t nc = (int64_t)L * L;
   d2_for_each(acc, [&](int r, int c, double v0, double v1) {
     const int l = m + r0 + r, s = c0 + c;  // s even: (re, im) of snapshot s/2
@@ -458,8 +486,9 @@ __global__ void k_gather_z(const double* __restrict__ coeffs, int L, int T, cons
   const int s = blockIdx.x;
   const int t = s >> 1, part = s & 1;
   const int cols = L - m;
+  const int colsp = (cols + 1) & ~1;
   const int64_t nc = (int64_t)L * L;
-  double* dst = Z + z_off[m] * 2 * T + (int64_t)s * cols;
+  double* dst = Z + z_off[m] * 2 * T + (int64_t)s * colsp;
   for (int r = threadIdx.x; r < cols; r += blockDim.x) {
     const int l = m + r;
     double v;
@@ -473,22 +502,23 @@ __global__ void k_gather_z(const double* __restrict__ coeffs, int L, int T, cons
 __global__ void __launch_bounds__(D2_THREADS) k_legendre_inv(const double* __restrict__ y, const int64_t* y_off,
                                                               const double* __restrict__ Z, const int64_t* z_off,
                                                               int L, int n_theta, int T, double* G) {
+  // G_m[i][s] (n_theta x 2T) = Y_m (n_theta x L-m) * Z_m^T, Z_m[s][l - m].
   extern __shared__ __align__(16) uint8_t d2_smem[];
   D2Smem& sm = *reinterpret_cast<D2Smem*>(d2_smem);
   const int m = blockIdx.z;
   const int cols = L - m;
   const int ncols = 2 * T;
   const int r0 = blockIdx.y * D2_BM, c0 = blockIdx.x * D2_BN;
-  if (r0 >= ncols) return;
-  D2Op A{Z + z_off[m] * ncols + (int64_t)r0 * cols, cols, min(D2_BM, ncols - r0), cols};
-  D2Op B{y + y_off[m] + (int64_t)c0 * cols, cols, min(D2_BN, n_theta - c0), cols};
+  if (r0 >= n_theta) return;
+  const int colsp = (cols + 1) & ~1, ntp = (n_theta + 1) & ~1;
+  D2Op A{y + y_off[m] + (int64_t)r0 * colsp, colsp, min(D2_BM, n_theta - r0), colsp};
+  D2Op B{Z + z_off[m] * ncols + (int64_t)c0 * colsp, colsp, min(D2_BN, ncols - c0), colsp};
   double acc[4][4][2];
-  dgemm2_128x64<D2B::kNT, false>(A, B, cols, sm, acc);
-  double* out = G + (int64_t)m * ncols * n_theta;
+  dgemm2_128x64<D2B::kNT, true>(A, B, colsp, sm, acc);
+  double* out = G + (int64_t)m * ntp * ncols;
   d2_for_each(acc, [&](int r, int c, double v0, double v1) {
-    if (r0 + r >= ncols) return;
-    if (c0 + c < n_theta) out[(int64_t)(r0 + r) * n_theta + c0 + c] = v0;
-    if (c0 + c + 1 < n_theta) out[(int64_t)(r0 + r) * n_theta + c0 + c + 1] = v1;
+    if (r0 + r >= n_theta || c0 + c >= ncols) return;  // ncols even, c even: the pair is in range
+    *reinterpret_cast<double2*>(out + (int64_t)(r0 + r) * ncols + c0 + c) = make_double2(v0, v1);
   });
 }
 
@@ -523,18 +553,26 @@ struct Sht {
     psi_off.resize(L + 1);
     y_off.resize(L + 1);
     z_off.resize(L + 1);
-    int64_t po = 0, zo = 0;
+    // Per-m operators with even row strides (zero padding), so every
+    // operand row of the Legendre GEMMs starts 16-byte aligned.
+    const int64_t ntp = (n_theta + 1) & ~1;
+    int64_t po = 0, yo = 0, zo = 0;
     for (int m = 0; m < L; ++m) {
       psi_off[m] = po;
-      y_off[m] = po;
+      y_off[m] = yo;
       z_off[m] = zo;
-      po += (int64_t)(L - m) * n_theta;
-      zo += L - m;
+      const int64_t colsp = (L - m + 1) & ~1;
+      po += (int64_t)(L - m) * ntp;
+      yo += (int64_t)n_theta * colsp;
+      zo += colsp;
     }
-    psi_off[L] = y_off[L] = po;
+    psi_off[L] = po;
+    y_off[L] = yo;
     z_off[L] = zo;
     psi.alloc(po);
-    y.alloc(po);
+    y.alloc(yo);
+    SPH_CUDA(cudaMemsetAsync(psi.get(), 0, sizeof(double) * po, stream));
+    SPH_CUDA(cudaMemsetAsync(y.get(), 0, sizeof(double) * yo, stream));
     d_psi_off.alloc(L + 1);
     d_y_off.alloc(L + 1);
     d_z_off.alloc(L + 1);
@@ -597,7 +635,13 @@ struct Sht {
     tw_phi.alloc(n_phi);
     SPH_CUDA(cudaMemcpy(tw_phi.get(), twp.data(), n_phi * sizeof(double2), cudaMemcpyHostToDevice));
     fplan.tw = tw_phi.get();
-    rings_per_cta = std::max(1, std::min(n_theta, 65536 / (16 * n_phi)));
+    // snapshots per FFT CTA: runs of >= 64 bytes per (m, ring) in G, within ~200 KB of smem
+    {
+      const char* e = std::getenv("SPHEMU_FFT_R");
+      const int cap = e ? std::max(1, std::atoi(e)) : 16;
+      // ~48 KB of rings per CTA (measured best for n_phi = 360 and 1440)
+      rings_per_cta = std::max(1, std::min(cap, (48 * 1024) / (16 * n_phi)));
+    }
     fft_smem = (size_t)rings_per_cta * n_phi * sizeof(double2);
     if (fft_smem > 48 * 1024) {
       SPH_CUDA(cudaFuncSetAttribute(k_ring_fft_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
@@ -620,10 +664,16 @@ struct Sht {
   }
 
   void ensure(int64_t tchunk) {
-    const size_t g = (size_t)L * 2 * tchunk * n_theta;
-    if (G.n < g) G.alloc(g);
+    const size_t g = (size_t)L * 2 * tchunk * ((n_theta + 1) & ~1);
+    if (G.n < g) {  // zero: the padding column is never written
+      G.alloc(g);
+      SPH_CUDA(cudaMemsetAsync(G.get(), 0, sizeof(double) * g, stream));
+    }
     const size_t z = (size_t)z_off[L] * 2 * tchunk;
-    if (Z.n < z) Z.alloc(z);
+    if (Z.n < z) {
+      Z.alloc(z);
+      SPH_CUDA(cudaMemsetAsync(Z.get(), 0, sizeof(double) * z, stream));
+    }
   }
 
   // Device-resident batched transforms.
@@ -632,7 +682,7 @@ struct Sht {
     for (int64_t t0 = 0; t0 < n; t0 += chunk) {
       const int T = (int)std::min<int64_t>(chunk, n - t0);
       ensure(T);
-      k_ring_fft_fwd<<<dim3(ceil_div(n_theta, rings_per_cta), T), 256, fft_smem, stream>>>(
+      k_ring_fft_fwd<<<dim3(n_theta, ceil_div(T, rings_per_cta)), 256, fft_smem, stream>>>(
           fields + t0 * pts, n_theta, L, rings_per_cta, fplan, T, G.get());
       SPH_LAUNCH_CHECK();
       k_legendre_fwd<<<dim3(ceil_div(2 * T, D2_BN), ceil_div(L, D2_BM), L), D2_THREADS, sizeof(D2Smem), stream>>>(
@@ -648,10 +698,10 @@ struct Sht {
       ensure(T);
       k_gather_z<<<dim3(2 * T, L), 128, 0, stream>>>(coeffs + t0 * nc, L, T, d_z_off.get(), Z.get());
       SPH_LAUNCH_CHECK();
-      k_legendre_inv<<<dim3(ceil_div(n_theta, D2_BN), ceil_div(2 * T, D2_BM), L), D2_THREADS, sizeof(D2Smem), stream>>>(
+      k_legendre_inv<<<dim3(ceil_div(2 * T, D2_BN), ceil_div(n_theta, D2_BM), L), D2_THREADS, sizeof(D2Smem), stream>>>(
           y.get(), d_y_off.get(), Z.get(), d_z_off.get(), L, n_theta, T, G.get());
       SPH_LAUNCH_CHECK();
-      k_ring_fft_inv<<<dim3(ceil_div(n_theta, rings_per_cta), T), 256, fft_smem, stream>>>(
+      k_ring_fft_inv<<<dim3(n_theta, ceil_div(T, rings_per_cta)), 256, fft_smem, stream>>>(
           G.get(), n_theta, L, rings_per_cta, fplan, T, fields + t0 * pts);
       SPH_LAUNCH_CHECK();
     }
