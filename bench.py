@@ -493,6 +493,37 @@ def sht_c4(sph, snapshots=1000):
             "note": "the driver's 8 760-snapshot hourly year runs in chunks of this batch"}
 
 
+def emulation_point(sph, L=90, replicates=100, t_out=24, order=3):
+    """Emulation generator throughput (stochastic.cpp:217-277): R replicates x T steps on the (L+1) x 2L grid,
+    V = the device factor of make_spd_test_matrix(L^2) (dp), AR(3), device Philox normals; the one-shot C-ABI
+    call with host buffers (V in, fields out) is the timed unit."""
+    import numpy as np
+    d = L * L
+    h = sph.Cholesky(d, "dp", tile_size=256)
+    h.generate_spd(1)
+    h.factor()
+    h.wait()
+    v = h.factor_dense()
+    del h
+    nt, nphi = L + 1, 2 * L
+    plan = sph.ShtPlan(nt, nphi, L)
+    phi = np.stack([np.full(d, x) for x in (0.6, 0.25, 0.15)[:order]])
+    pts = nt * nphi
+    means = np.zeros((t_out, pts))
+    sigma = np.ones(pts)
+    v2 = np.full(pts, 0.04)
+    sph._sphemu.emulate(plan, v, phi, means, sigma, v2, t_out, 7, 2, "philox")  # warm-up
+    t0 = time.perf_counter()
+    out = sph._sphemu.emulate(plan, v, phi, means, sigma, v2, t_out, 7, replicates, "philox")
+    dt = time.perf_counter() - t0
+    burn = 10 * order
+    return {"band_limit": L, "d": d, "grid": f"{nt}x{nphi}", "replicates": replicates, "steps": t_out,
+            "snapshots_per_s": replicates * t_out / dt, "seconds": dt,
+            "trmm_fp64_tflops": d * d * replicates * (burn + t_out) / dt / 1e12,
+            "finite": bool(np.isfinite(out).all()),
+            "api": "sphemu_gpu_emulate (host V and fields, H2D/D2H inside)"}
+
+
 def run_ours(args, world, rank, local):
     import torch
 
@@ -536,6 +567,7 @@ def run_ours(args, world, rank, local):
 
     sht = sht_throughput(sph, world)
     c4 = sht_c4(sph) if (world == 1 and not args.no_c4) else None
+    emul = emulation_point(sph) if (world == 1 and not args.no_c4) else None
 
     if rank != 0:
         return
@@ -580,6 +612,8 @@ def run_ours(args, world, rank, local):
         line["c3_1gpu"] = c3_1
     if c4:
         line["sht_c4"] = c4
+    if emul:
+        line["emulation"] = emul
     print(json.dumps(line), flush=True)
 
 
