@@ -893,7 +893,11 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
     const char* e = std::getenv("SPHEMU_TC_CG");
     return e ? std::atoi(e) : 1;
   }();
-  const bool pair = cg_env == 2 && pf.bn == 256;
+  static const int cg_sp = [] {
+    const char* e = std::getenv("SPHEMU_TC_CG_SP");
+    return e ? std::atoi(e) : 1;
+  }();
+  const bool pair = (cls == SPHEMU_PREC_SP ? cg_sp : cg_env) == 2 && pf.bn == 256;
   if (cls == SPHEMU_PREC_SP) {
     a.sub_n = ts.b / (pf.f16x3 ? pf.bn : 128);
     a.sub_per = (ts.b / (TC_BM * (pair && pf.f16x3 ? 2 : 1))) * a.sub_n;
