@@ -328,8 +328,16 @@ def roofline(h, wl, args, phases, steps, ms):
     ph, peak, src, kern = cls[dom_c]
     t = phases[ph]["ms"] / steps
     ach = cuf[dom_c] / (t * 1e-3) / 1e12 if t > 0 else None
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tf) and dom_c in ("sp", "hp"):
+        t = json.load(open(tf))[dom_c]
+        traffic = {"dram_bytes_per_launch": t["dram_read_bytes"] + t["dram_write_bytes"],
+                   "algorithmic_bytes_per_launch": t["c_bytes"] + t["panel_operand_bytes"],
+                   "launch": f"{t['workload']}: {t['sub_tiles']} sub-tiles of 128x256, K=512",
+                   "source": "profiles/r01_traffic.json (ncu --set full, one launch)"}
     dom = {"kernel": kern, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-           "frac": ach / peak if ach else None, "peak_source": src, "traffic": None,
+           "frac": ach / peak if ach else None, "peak_source": src, "traffic": traffic,
            "per_launch_basis": f"{cuf[dom_c]/1e12:.3f} TFLOP of {dom_c.upper()}-class update per step on this rank "
                                f"/ summed launch time {t:.2f} ms (CUDA events on the launching stream)"}
     fl = h.flops()
