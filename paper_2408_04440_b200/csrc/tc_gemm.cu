@@ -39,23 +39,25 @@ EncodeFn encode_fn() {
 }
 
 CUtensorMap make_map_strided(const void* base, int64_t rows, int64_t cols, int64_t row_bytes, int elem_bytes,
-                             int box_rows) {
+                             int box_rows, int swizzle_bytes = 128) {
   CUtensorMap m;
   const CUtensorMapDataType dt = elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                                  : CU_TENSOR_MAP_DATA_TYPE_UINT16;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_bytes)};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / elem_bytes), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(swizzle_bytes / elem_bytes), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(SPHEMU_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
   return m;
 }
 // Row-major [rows x cols] array, box = 128 bytes of K x box_rows rows, SW128.
-CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int elem_bytes, int box_rows) {
-  return make_map_strided(base, rows, cols, cols * elem_bytes, elem_bytes, box_rows);
+CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int elem_bytes, int box_rows,
+                     int swizzle_bytes = 128) {
+  return make_map_strided(base, rows, cols, cols * elem_bytes, elem_bytes, box_rows, swizzle_bytes);
 }
 
 }  // namespace
@@ -100,10 +102,10 @@ void PanelFormats::alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int 
   if (f16x3) {
     h_hi.alloc(elems);
     h_lo.alloc(elems);
-    m_hhi_a = make_map(h_hi.get(), rows, b, 2, TC_BM);
-    m_hlo_a = make_map(h_lo.get(), rows, b, 2, TC_BM);
-    m_hhi_b = make_map(h_hi.get(), rows, b, 2, bn);
-    m_hlo_b = make_map(h_lo.get(), rows, b, 2, bn);
+    m_hhi_a = make_map(h_hi.get(), rows, b, 2, TC_BM, 128);
+    m_hlo_a = make_map(h_lo.get(), rows, b, 2, TC_BM, 128);
+    m_hhi_b = make_map(h_hi.get(), rows, b, 2, bn, 128);
+    m_hlo_b = make_map(h_lo.get(), rows, b, 2, bn, 128);
   }
 }
 
@@ -143,7 +145,10 @@ struct OpTraits {
   static constexpr bool kSplit = (OPK == OP_TF32X3 || OPK == OP_F16X3);
   static constexpr bool kTf32 = (OPK == OP_TF32X3);
   static constexpr int kElem = kTf32 ? 4 : 2;
-  static constexpr int kBK = 128 / kElem;       // K elements per stage (one 128B swizzle row)
+  // smem row of K per stage (swizzle width). 64-byte rows (SWIZZLE_64B, twice
+  // the stages) were measured slower for FP16x3 than 128-byte rows.
+  static constexpr int kRowBytes = 128;
+  static constexpr int kBK = kRowBytes / kElem;  // K elements per stage
   static constexpr int kUK = kTf32 ? 8 : 16;    // K per tcgen05.mma
   static constexpr int kFmt = (OPK == OP_F16 || OPK == OP_F16X3) ? 0 : (OPK == OP_BF16 ? 1 : 2);
 };
@@ -155,8 +160,8 @@ template <int BN, int OPK, int MODE, int CG = 1>
 struct TcLayout {
   using T = OpTraits<OPK>;
   static constexpr bool kUpd = (MODE == MODE_UPDATE);
-  static constexpr int kA = TC_BM * 128;          // bytes of one A buffer
-  static constexpr int kB = (BN / CG) * 128;      // bytes of one B buffer (this CTA's rows)
+  static constexpr int kA = TC_BM * T::kRowBytes;          // bytes of one A buffer
+  static constexpr int kB = (BN / CG) * T::kRowBytes;      // bytes of one B buffer (this CTA's rows)
   static constexpr int kStage = (T::kSplit ? 2 : 1) * (kA + kB);
   // Update mode stages the C tile through shared memory: per epilogue warp
   // a ring of kRing TMA boxes (32 rows x 128 bytes each).
@@ -167,9 +172,9 @@ struct TcLayout {
 #define SPH_TC_RING2 3
 #endif
   static constexpr int kRing = kUpd ? ((CG == 2 && !T::kSplit) ? SPH_TC_RING2 : SPH_TC_RING) : 0;
-  static constexpr int kStages = (232448 - 1536 - TC_EPI_WARPS * kRing * 32 * 128) / kStage > 6
+  static constexpr int kStages = (232448 - 2048 - TC_EPI_WARPS * kRing * 32 * 128) / kStage > 6
                                      ? 6
-                                     : (232448 - 1536 - TC_EPI_WARPS * kRing * 32 * 128) / kStage;
+                                     : (232448 - 2048 - TC_EPI_WARPS * kRing * 32 * 128) / kStage;
   static constexpr int kCBox = 32 * 128;
   static constexpr int kCBytes = TC_EPI_WARPS * kRing * kCBox;
   static constexpr int kSmem = kStages * kStage + kCBytes + 1024 /*align*/ + 1024 /*barriers + schedule*/;
@@ -384,27 +389,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           else umma_commit(&empty[stage]);
         } else if (lane == 0) {
           uint8_t* st = smem + stage * Lay::kStage;
-          const uint64_t a_hi = umma_desc_sw128(st);
-          const uint64_t b_hi = umma_desc_sw128(st + Lay::kA);
+          const uint64_t a_hi = umma_desc_k<T::kRowBytes>(st);
+          const uint64_t b_hi = umma_desc_k<T::kRowBytes>(st + Lay::kA);
 #pragma unroll
           for (int kk = 0; kk < T::kBK / T::kUK; ++kk) {
             const uint64_t koff = (kk * T::kUK * T::kElem) >> 4;
             const uint32_t accum = (kb | kk) ? 1u : 0u;
             if constexpr (T::kTf32) {
-              const uint64_t a_lo = umma_desc_sw128(st + Lay::kA + Lay::kB);
-              const uint64_t b_lo = umma_desc_sw128(st + 2 * Lay::kA + Lay::kB);
+              const uint64_t a_lo = umma_desc_k<T::kRowBytes>(st + Lay::kA + Lay::kB);
+              const uint64_t b_lo = umma_desc_k<T::kRowBytes>(st + 2 * Lay::kA + Lay::kB);
               umma_tf32(d, a_lo + koff, b_hi + koff, idesc, accum);
               umma_tf32(d, a_hi + koff, b_lo + koff, idesc, 1u);
               umma_tf32(d, a_hi + koff, b_hi + koff, idesc, 1u);
             } else if constexpr (T::kSplit && CG == 2) {
-              const uint64_t a_lo = umma_desc_sw128(st + Lay::kA + Lay::kB);
-              const uint64_t b_lo = umma_desc_sw128(st + 2 * Lay::kA + Lay::kB);
+              const uint64_t a_lo = umma_desc_k<T::kRowBytes>(st + Lay::kA + Lay::kB);
+              const uint64_t b_lo = umma_desc_k<T::kRowBytes>(st + 2 * Lay::kA + Lay::kB);
               umma_f16_cg2(d, a_lo + koff, b_hi + koff, idesc, accum);
               umma_f16_cg2(d, a_hi + koff, b_lo + koff, idesc, 1u);
               umma_f16_cg2(d, a_hi + koff, b_hi + koff, idesc, 1u);
             } else if constexpr (T::kSplit) {
-              const uint64_t a_lo = umma_desc_sw128(st + Lay::kA + Lay::kB);
-              const uint64_t b_lo = umma_desc_sw128(st + 2 * Lay::kA + Lay::kB);
+              const uint64_t a_lo = umma_desc_k<T::kRowBytes>(st + Lay::kA + Lay::kB);
+              const uint64_t b_lo = umma_desc_k<T::kRowBytes>(st + 2 * Lay::kA + Lay::kB);
               umma_f16(d, a_lo + koff, b_hi + koff, idesc, accum);
               umma_f16(d, a_hi + koff, b_lo + koff, idesc, 1u);
               umma_f16(d, a_hi + koff, b_hi + koff, idesc, 1u);

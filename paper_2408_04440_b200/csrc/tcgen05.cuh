@@ -170,6 +170,22 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(const void* p) {
   return d;
 }
 
+// Same for SWIZZLE_64B: rows of 64 bytes, 8-row groups 512 bytes apart.
+__device__ __forceinline__ uint64_t umma_desc_sw64(const void* p) {
+  const uint64_t addr = smem_addr(p);
+  uint64_t d = (addr >> 4) & 0x3FFFull;
+  d |= 1ull << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= 1ull << 46;
+  d |= 4ull << 61;  // SWIZZLE_64B
+  return d;
+}
+template <int ROW_BYTES>
+__device__ __forceinline__ uint64_t umma_desc_k(const void* p) {
+  if constexpr (ROW_BYTES == 64) return umma_desc_sw64(p);
+  else return umma_desc_sw128(p);
+}
+
 // Instruction descriptor: FP32 accumulate, K-major A and B, M x N.
 // fmt: 0 = f16, 1 = bf16, 2 = tf32.
 __host__ __device__ constexpr uint32_t umma_idesc(int fmt, int M, int N) {
