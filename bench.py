@@ -331,10 +331,10 @@ def roofline(h, wl, args, phases, steps, ms):
     traffic = None
     tf = os.path.join(ROOT, "profiles", "r01_traffic.json")
     if os.path.exists(tf) and dom_c in ("sp", "hp"):
-        t = json.load(open(tf))[dom_c]
-        traffic = {"dram_bytes_per_launch": t["dram_read_bytes"] + t["dram_write_bytes"],
-                   "algorithmic_bytes_per_launch": t["c_bytes"] + t["panel_operand_bytes"],
-                   "launch": f"{t['workload']}: {t['sub_tiles']} sub-tiles of 128x256, K=512",
+        tj = json.load(open(tf))[dom_c]
+        traffic = {"dram_bytes_per_launch": tj["dram_read_bytes"] + tj["dram_write_bytes"],
+                   "algorithmic_bytes_per_launch": tj["c_bytes"] + tj["panel_operand_bytes"],
+                   "launch": f"{tj['workload']}: {tj['sub_tiles']} sub-tiles of 128x256, K=512",
                    "source": "profiles/r01_traffic.json (ncu --set full, one launch)"}
     dom = {"kernel": kern, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
            "frac": ach / peak if ach else None, "peak_source": src, "traffic": traffic,

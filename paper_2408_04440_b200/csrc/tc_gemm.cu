@@ -171,7 +171,13 @@ struct TcLayout {
 #ifndef SPH_TC_RING2
 #define SPH_TC_RING2 3
 #endif
-  static constexpr int kRing = kUpd ? ((CG == 2 && !T::kSplit) ? SPH_TC_RING2 : SPH_TC_RING) : 0;
+#ifndef SPH_TC_RING_SPLIT128
+#define SPH_TC_RING_SPLIT128 1
+#endif
+  static constexpr int kRing =
+      kUpd ? ((CG == 2 && !T::kSplit) ? SPH_TC_RING2
+                                      : ((T::kSplit && BN == 128) ? SPH_TC_RING_SPLIT128 : SPH_TC_RING))
+           : 0;
   static constexpr int kStages = (232448 - 2048 - TC_EPI_WARPS * kRing * 32 * 128) / kStage > 6
                                      ? 6
                                      : (232448 - 2048 - TC_EPI_WARPS * kRing * 32 * 128) / kStage;
@@ -902,18 +908,23 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
     const char* e = std::getenv("SPHEMU_TC_CG_SP");
     return e ? std::atoi(e) : 1;
   }();
+  static const int sp_bn = [] {
+    const char* e = std::getenv("SPHEMU_SP_BN");
+    return e ? std::atoi(e) : 256;
+  }();
   const bool pair = (cls == SPHEMU_PREC_SP ? cg_sp : cg_env) == 2 && pf.bn == 256;
   if (cls == SPHEMU_PREC_SP) {
-    a.sub_n = ts.b / (pf.f16x3 ? pf.bn : 128);
+    const int bn_sp = (pf.f16x3 && pf.bn == 256 && sp_bn == 256 && !pair) ? 256 : (pair ? 256 : 128);
+    a.sub_n = ts.b / (pf.f16x3 ? bn_sp : 128);
     a.sub_per = (ts.b / (TC_BM * (pair && pf.f16x3 ? 2 : 1))) * a.sub_n;
     a.items = cnt * a.sub_per;
     if (pf.f16x3 && pair)
       launch_tc<256, OP_F16X3, MODE_UPDATE, 2>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_a, pf.m_hlo_a, pf.m_c32, a, s,
                                                max_ctas);
-    else if (pf.f16x3 && pf.bn == 256)
+    else if (pf.f16x3 && bn_sp == 256)
       launch_tc<256, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_b, pf.m_hlo_b, pf.m_c32, a, s, max_ctas);
-    else if (pf.f16x3)
-      launch_tc<128, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_b, pf.m_hlo_b, pf.m_c32, a, s, max_ctas);
+    else if (pf.f16x3)  // 128-wide N: B boxes of 128 rows (the A-side maps)
+      launch_tc<128, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_a, pf.m_hlo_a, pf.m_c32, a, s, max_ctas);
     else
       launch_tc<128, OP_TF32X3, MODE_UPDATE>(pf.m_phi_a, pf.m_plo_a, pf.m_phi_b, pf.m_plo_b, pf.m_c32, a, s, max_ctas);
   } else {
