@@ -229,6 +229,14 @@ __global__ void k_diff_norms(int n, const double* a, const double* b, double* su
   }
 }
 
+// 2D block-cyclic owner of tile (i, j) on a P x Q grid: process column
+// j mod Q (so panel column k lives in one process column, as the exchange
+// plan assumes) and process row (i + j div Q) mod P. The shift by the
+// column-block index spreads the diagonal tiles — the FP64 band, whose SYRK
+// updates cost ~50x a BF16 tile's — over every rank instead of only the
+// P = Q diagonal ranks of the plain (i mod P, j mod Q) map.
+inline int block_cyclic_owner(int i, int j, int P, int Q) { return ((i + j / Q) % P) * Q + (j % Q); }
+
 // Host-only 2D block-cyclic layout (no CUDA calls): this rank's tile offsets
 // in its arena and the per-step panel exchange plan (panel tiles of step k
 // grouped by owning rank so each owner broadcasts one contiguous block). Chol
@@ -244,7 +252,7 @@ struct BlockCyclic {
   std::vector<std::vector<XRoot>> xroots;   // per step k
   std::vector<std::vector<int64_t>> xpos;   // per step k: byte position of panel tile i at [i - k - 1]
   int64_t xmax = 0;
-  int owner(int i, int j) const { return (i % P) * Q + (j % Q); }
+  int owner(int i, int j) const { return block_cyclic_owner(i, j, P, Q); }
   bool mine(int i, int j) const { return owner(i, j) == rank; }
 
   BlockCyclic(int nt_, int b_, const std::vector<uint8_t>& sprec, int P_, int Q_, int rank_)
@@ -293,7 +301,7 @@ struct Chol {
   int P = 1, Q = 1, rank = 0;
   ncclComm_t comm = nullptr;
   bool dist() const { return P * Q > 1; }
-  int owner(int i, int j) const { return (i % P) * Q + (j % Q); }
+  int owner(int i, int j) const { return block_cyclic_owner(i, j, P, Q); }
   bool mine(int i, int j) const { return owner(i, j) == rank; }
   // Panel exchange buffer: per step the panel tiles at storage precision,
   // grouped by owning rank (root) so each root broadcasts one contiguous
@@ -420,11 +428,13 @@ struct Chol {
     ensure_io();
     const size_t slab = static_cast<size_t>(lb) * n;
     if (islab.n < kSlabs * slab) islab.alloc(kSlabs * slab);
-    const int prow = rank / Q, pcol = rank % Q;
+    std::vector<char> row_has(nt, 0);  // rows holding at least one tile of this rank
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j <= i && !row_has[i]; ++j) row_has[i] = mine(i, j);
     const unsigned gy = static_cast<unsigned>(std::max(1, b * b / (256 * 64)));
     int used = 0;
     for (int i = 0; i < nt; ++i) {
-      if (dist() && (i % P != prow || i < pcol)) continue;  // no owned tile in this row
+      if (dist() && !row_has[i]) continue;
       const int s = used % kSlabs;
       if (used >= kSlabs) SPH_CUDA(cudaStreamWaitEvent(cstream, ev_in_free[s], 0));
       double* dst = islab.get() + s * slab;
