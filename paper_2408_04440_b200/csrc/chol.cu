@@ -871,7 +871,13 @@ struct Chol {
         op_update(k, 1, stream, 0);
       }
     } else {
-      const int reserve = kChainCtas;
+      // SMs left free for the chain while the bulk runs: the distributed chain
+      // also carries the panel exchange and import, and each rank's bulk
+      // shrinks with the grid (SPHEMU_DIST_RESERVE overrides).
+      static const int reserve = [] {
+        const char* e = std::getenv("SPHEMU_DIST_RESERVE");
+        return e ? std::atoi(e) : 48;  // 4-GPU C3: 32 -> 501, 48 -> 488, 64 -> 515 ms
+      }();
       SPH_CUDA(cudaEventRecord(ev_start_p, stream));
       SPH_CUDA(cudaStreamWaitEvent(pstream, ev_start_p, 0));
       op_potrf_dist(0, pstream);
