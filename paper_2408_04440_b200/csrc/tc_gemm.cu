@@ -100,6 +100,15 @@ void PanelFormats::alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int 
   m_lhi_b = make_map(l_hi.get(), b, b, 4, bn_tf32);
   m_llo_b = make_map(l_lo.get(), b, b, 4, bn_tf32);
   if (f16x3) {
+    in16_hi.alloc(elems);
+    in16_lo.alloc(elems);
+    l16_hi.alloc(static_cast<size_t>(b) * b);
+    l16_lo.alloc(static_cast<size_t>(b) * b);
+    lexp.alloc(b);
+    m_in16hi_a = make_map(in16_hi.get(), rows, b, 2, TC_BM);
+    m_in16lo_a = make_map(in16_lo.get(), rows, b, 2, TC_BM);
+    m_l16hi_b = make_map(l16_hi.get(), b, b, 2, 128);
+    m_l16lo_b = make_map(l16_lo.get(), b, b, 2, 128);
     h_hi.alloc(elems);
     h_lo.alloc(elems);
     m_hhi_a = make_map(h_hi.get(), rows, b, 2, TC_BM, 128);
@@ -138,6 +147,7 @@ struct TcArgs {
   int dbg;           // diagnostics only (SPHEMU_TC_DBG): 1 = skip the C epilogue, 2 = also skip the MMAs
   int opt;           // tuning switches (SPHEMU_TC_OPT): 1 = no C prefetch to L2, 2 = prefetch two items ahead
   int* counter;      // non-null: items are claimed dynamically (atomicAdd), zeroed before the launch
+  const int* lexp;   // FP16x3 panel: per output column (Linv row) power-of-two exponent
 };
 
 template <int OPK>
@@ -615,6 +625,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         uint32_t v[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c0, v);
         const int64_t e0 = (int64_t)r * b + n0 + c0;
+        if constexpr (OPK == OP_F16X3) {
+          // X = acc * 2^(-rowexp(row) - g(col)): exact power-of-two unscale of the scaled operands
+          const int er = args.rowexp[min(i * args.lb + r, args.ts.n - 1)];
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int g = __ldg(args.lexp + n0 + c0 + t);
+            v[t] = __float_as_uint(__uint_as_float(v[t]) * __int_as_float((127 - er - g) << 23));
+          }
+        }
         {
           // Panel: X = B * Linv^T rounded through p(i, k); write the tile, the
           // FP64 mirror and the tensor mirrors, 8 columns (>= 32 B) per store.
@@ -731,6 +750,71 @@ __global__ void k_panel_prep(TileStore ts, int k, const int2* list, const double
   }
 }
 
+// FP16x3 panel TRSM inputs. With 2^(14 - rowexp[x]) ~ sqrt(A_xx) (k_rowexp):
+//   B_s[r][c]   = B[r][c] 2^(rowexp[R] + rowexp[C] - 14)      |B_s| <~ 2^14
+//   L_s[j][c]   = Linv[j][c] 2^(14 - rowexp[C] + g_j)        g_j: row max -> <= 2^14
+// so (B_s L_s^T)[r][j] = X[r][j] 2^(rowexp[R] + g_j), undone exactly in the
+// panel epilogue; hi + lo fp16 carry ~22 bits like a tf32 split.
+__global__ void k_linv_prep16(const double* __restrict__ linv, int b, int k, int lb, int n, const int* rowexp,
+                              uint16_t* l_hi, uint16_t* l_lo, int* lexp, const int* fail) {
+  if (*(volatile const int*)fail >= 0) return;
+  __shared__ float red[32];
+  const int j = blockIdx.x;
+  float m = 0.f;
+  for (int c = threadIdx.x; c < b; c += blockDim.x) {
+    const int C = min(k * lb + c, n - 1);
+    m = fmaxf(m, fabsf(ldexpf(__double2float_rn(linv[(int64_t)j * b + c]), 14 - rowexp[C])));
+  }
+  m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+  m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+  m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+  m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (int)(blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    if (threadIdx.x == 0) red[0] = m;
+  }
+  __syncthreads();
+  m = red[0];
+  int e = 0;
+  if (m > 0.f) frexpf(m, &e);  // m = f 2^e, f in [0.5, 1)
+  const int g = m > 0.f ? 14 - e : 0;
+  if (threadIdx.x == 0) lexp[j] = g;
+  for (int c = threadIdx.x; c < b; c += blockDim.x) {
+    const int C = min(k * lb + c, n - 1);
+    uint16_t hi, lo;
+    f16_split(linv[(int64_t)j * b + c], 14 - rowexp[C] + g, hi, lo);
+    l_hi[(int64_t)j * b + c] = hi;
+    l_lo[(int64_t)j * b + c] = lo;
+  }
+}
+
+__global__ void k_panel_prep16(TileStore ts, int k, const int2* list, const int* rowexp, uint16_t* in_hi,
+                               uint16_t* in_lo, const int* fail) {
+  if (*(volatile const int*)fail >= 0) return;
+  const int b = ts.b;
+  const int64_t bb = (int64_t)b * b;
+  const int i = list[blockIdx.y].x;
+  const void* tp = ts.tile(i, k);
+  const int p = ts.tprec(i, k);
+  const int64_t base = (int64_t)(i - k - 1) * bb;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / b), c = (int)(e % b);
+    const int R = min(i * ts.lb + r, ts.n - 1), Cc = min(k * ts.lb + c, ts.n - 1);
+    uint16_t hi, lo;
+    f16_split(load_elem(tp, p, e), rowexp[R] + rowexp[Cc] - 14, hi, lo);
+    in_hi[base + e] = hi;
+    in_lo[base + e] = lo;
+  }
+}
+
 // DP-class panel tiles: P64 (already rounded) -> tile storage + mirrors.
 __global__ void k_panel_finish_dp(TileStore ts, int k, const int2* list, const double* __restrict__ p64,
                                   float* p_hi, float* p_lo, uint16_t* p16, int hp_format, const int* fail,
@@ -841,10 +925,26 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
         pf.f16x3 ? pf.h_hi.get() : nullptr, pf.h_lo.get(), pf.rowexp);
     SPH_LAUNCH_CHECK();
   }
-  if (n_lo) {
+  static const bool panel16 = [] {
+    // FP16x3 panel TRSM: same speed as 3xTF32 here (the panel is latency-
+    // bound) with a slightly larger backward error, so opt-in only.
+    const char* e = std::getenv("SPHEMU_PANEL_F16X3");
+    return e && e[0] == '1';
+  }();
+  const bool p16 = panel16 && pf.f16x3;
+  if (n_lo && p16) {
+    k_linv_prep16<<<b, 128, 0, s>>>(linv, b, k, ts.lb, ts.n, pf.rowexp, pf.l16_hi.get(), pf.l16_lo.get(),
+                                     pf.lexp.get(), fail);
+    SPH_LAUNCH_CHECK();
+    k_panel_prep16<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(n_lo)), 256, 0, s>>>(
+        ts, k, d_lo, pf.rowexp, pf.in16_hi.get(), pf.in16_lo.get(), fail);
+    SPH_LAUNCH_CHECK();
+  } else if (n_lo) {
     k_panel_prep<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(n_lo + 1)), 256, 0, s>>>(
         ts, k, d_lo, linv, pf.in_hi.get(), pf.in_lo.get(), pf.l_hi.get(), pf.l_lo.get(), fail);
     SPH_LAUNCH_CHECK();
+  }
+  if (n_lo) {
     TcArgs a{};
     a.ts = ts;
     a.list = d_lo;
@@ -865,7 +965,13 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
     a.fail = fail;
     a.sat = sat;
     a.counter = counter;
-    launch_tc<128, OP_TF32X3, MODE_PANEL>(pf.m_inhi_a, pf.m_inlo_a, pf.m_lhi_b, pf.m_llo_b, pf.m_lhi_b, a, s, max_ctas);
+    a.lexp = pf.lexp.get();
+    if (p16)
+      launch_tc<128, OP_F16X3, MODE_PANEL>(pf.m_in16hi_a, pf.m_in16lo_a, pf.m_l16hi_b, pf.m_l16lo_b, pf.m_l16hi_b, a, s,
+                                           max_ctas);
+    else
+      launch_tc<128, OP_TF32X3, MODE_PANEL>(pf.m_inhi_a, pf.m_inlo_a, pf.m_lhi_b, pf.m_llo_b, pf.m_lhi_b, a, s,
+                                            max_ctas);
   }
 }
 

@@ -32,6 +32,11 @@ struct PanelFormats {
   // TMA descriptors: A-role (128-row box) and B-role (BN-row box).
   CUtensorMap m_phi_a, m_plo_a, m_phi_b, m_plo_b, m_p16_a, m_p16_b;
   CUtensorMap m_inhi_a, m_inlo_a, m_lhi_b, m_llo_b;
+  // FP16x3 panel TRSM operands: fp16 hi/lo of the scaled B_i and Linv, and
+  // the per-Linv-row exponents g_j (see k_panel_prep16).
+  DevBuf<uint16_t> in16_hi, in16_lo, l16_hi, l16_lo;
+  DevBuf<int> lexp;
+  CUtensorMap m_in16hi_a, m_in16lo_a, m_l16hi_b, m_l16lo_b;
   // FP16x3 path for the SP class: x * 2^e_row = hi + lo, both fp16.
   bool f16x3 = false;
   const int* rowexp = nullptr;
