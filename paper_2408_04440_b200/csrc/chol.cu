@@ -339,13 +339,17 @@ struct Chol {
   }
   // Update lists per (step k, part, class): part 0 = next column (k+1, the
   // critical chain), part 1 = the rest (columns >= k+2, the bulk).
-  std::vector<int64_t> list_off, list_cnt;  // [(k * 2 + part) * 3 + class]
+  // Parts: 0 = the next diagonal tile (k+1, k+1) (feeds POTRF(k+1), the
+  // critical chain), 1 = columns >= k+2 (the bulk), 2 = column k+1 below the
+  // diagonal (feeds panel(k+1), runs ahead of the bulk on the main stream).
+  static constexpr int kParts = 3;
+  std::vector<int64_t> list_off, list_cnt;  // [(k * kParts + part) * 3 + class]
   DevBuf<int2> plists;                      // panel tiles per step: DP class, then SP/HP
   std::vector<int64_t> plist_off, plist_dp, plist_lo;
   PanelFormats panel_[2];                   // tensor-core operand mirrors per parity
   cudaStream_t stream = nullptr;            // main stream: bulk trailing updates
   cudaStream_t pstream = nullptr;           // high-priority stream: POTRF + panel chain
-  std::vector<cudaEvent_t> ev_panel, ev_bulk;
+  std::vector<cudaEvent_t> ev_panel, ev_bulk, ev_colrest;
   cudaEvent_t ev_start_p = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches_at_start = 0, launches = 0;
@@ -531,18 +535,21 @@ struct Chol {
     sat.alloc(1);
     sched_ctr.alloc(2);
     // Per-step output-tile lists by precision class.
-    list_off.assign(static_cast<size_t>(nt) * 6 + 1, 0);
-    list_cnt.assign(static_cast<size_t>(nt) * 6, 0);
+    list_off.assign(static_cast<size_t>(nt) * kParts * 3 + 1, 0);
+    list_cnt.assign(static_cast<size_t>(nt) * kParts * 3, 0);
     std::vector<int2> all;
     for (int k = 0; k < nt; ++k)
-      for (int part = 0; part < 2; ++part)
+      for (int part = 0; part < kParts; ++part)
         for (int cls = 0; cls < 3; ++cls) {
-          const size_t slot = (static_cast<size_t>(k) * 2 + part) * 3 + cls;
+          const size_t slot = (static_cast<size_t>(k) * kParts + part) * 3 + cls;
           list_off[slot] = static_cast<int64_t>(all.size());
-          const int j_lo = part == 0 ? k + 1 : k + 2, j_hi = part == 0 ? std::min(k + 2, nt) : nt;
+          const int j_lo = part == 1 ? k + 2 : k + 1, j_hi = part == 1 ? nt : std::min(k + 2, nt);
           for (int j = j_lo; j < j_hi; ++j)
-            for (int i = j; i < nt; ++i)
+            for (int i = j; i < nt; ++i) {
+              if (part == 0 && i != j) continue;
+              if (part == 2 && i == j) continue;
               if (pmap[tix(i, j)] == cls && mine(i, j)) all.push_back(make_int2(i, j));
+            }
           list_cnt[slot] = static_cast<int64_t>(all.size()) - list_off[slot];
         }
     if (!all.empty()) {
@@ -627,6 +634,8 @@ struct Chol {
     SPH_CUDA(cudaStreamCreateWithPriority(&pstream, cudaStreamNonBlocking, prio_hi));
     ev_panel.resize(nt);
     ev_bulk.resize(nt);
+    ev_colrest.resize(nt);
+    for (int k = 0; k < nt; ++k) SPH_CUDA(cudaEventCreateWithFlags(&ev_colrest[k], cudaEventDisableTiming));
     for (int k = 0; k < nt; ++k) {
       SPH_CUDA(cudaEventCreateWithFlags(&ev_panel[k], cudaEventDisableTiming));
       SPH_CUDA(cudaEventCreateWithFlags(&ev_bulk[k], cudaEventDisableTiming));
@@ -652,6 +661,7 @@ struct Chol {
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (auto e : ev_panel) cudaEventDestroy(e);
     for (auto e : ev_bulk) cudaEventDestroy(e);
+    for (auto e : ev_colrest) cudaEventDestroy(e);
     if (ev_start_p) cudaEventDestroy(ev_start_p);
     if (pstream) cudaStreamDestroy(pstream);
     if (comm) ncclCommDestroy(comm);
@@ -720,7 +730,7 @@ struct Chol {
   void op_update(int k, int part, cudaStream_t s, int max_ctas) {
     const int set = k & 1;
     for (int cls = 0; cls < 3; ++cls) {
-      const size_t slot = (static_cast<size_t>(k) * 2 + part) * 3 + cls;
+      const size_t slot = (static_cast<size_t>(k) * kParts + part) * 3 + cls;
       const int64_t cnt = list_cnt[slot];
       if (!cnt) continue;
       const int2* lst = lists.get() + list_off[slot];
@@ -775,6 +785,7 @@ struct Chol {
         op_panel(k, stream);
         col_out(k, stream);
         op_update(k, 0, stream, 0);
+        op_update(k, 2, stream, 0);
         op_update(k, 1, stream, 0);
       }
     } else {
@@ -785,13 +796,21 @@ struct Chol {
       SPH_CUDA(cudaEventRecord(ev_panel[0], pstream));
       col_out(0, pstream);
       for (int k = 0; k + 1 < nt; ++k) {
+        // chain: SYRK of the next diagonal tile -> POTRF -> (column below ready) -> panel
         if (k > 0) SPH_CUDA(cudaStreamWaitEvent(pstream, ev_bulk[k - 1], 0));
         op_update(k, 0, pstream, 0);
         op_potrf(k + 1, pstream);
-        if (k + 2 < nt) op_panel(k + 1, pstream);
+        // main stream: column k+1 below the diagonal first (the chain's panel
+        // waits for it), then the bulk of step k on the SMs the chain leaves
+        SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k], 0));
+        op_update(k, 2, stream, 0);
+        SPH_CUDA(cudaEventRecord(ev_colrest[k], stream));
+        if (k + 2 < nt) {
+          SPH_CUDA(cudaStreamWaitEvent(pstream, ev_colrest[k], 0));
+          op_panel(k + 1, pstream);
+        }
         SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
         col_out(k + 1, pstream);
-        SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k], 0));
         op_update(k, 1, stream, std::max(1, num_sms() - reserve));
         SPH_CUDA(cudaEventRecord(ev_bulk[k], stream));
       }
@@ -868,6 +887,7 @@ struct Chol {
         if (k + 1 >= nt) break;
         op_panel_dist(k, stream);
         op_update(k, 0, stream, 0);
+        op_update(k, 2, stream, 0);
         op_update(k, 1, stream, 0);
       }
     } else {
@@ -887,9 +907,14 @@ struct Chol {
         if (k > 0) SPH_CUDA(cudaStreamWaitEvent(pstream, ev_bulk[k - 1], 0));
         op_update(k, 0, pstream, 0);
         op_potrf_dist(k + 1, pstream);
-        if (k + 2 < nt) op_panel_dist(k + 1, pstream);
-        SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
         SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k], 0));
+        op_update(k, 2, stream, 0);  // no collectives on the main stream
+        SPH_CUDA(cudaEventRecord(ev_colrest[k], stream));
+        if (k + 2 < nt) {
+          SPH_CUDA(cudaStreamWaitEvent(pstream, ev_colrest[k], 0));
+          op_panel_dist(k + 1, pstream);
+        }
+        SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
         op_update(k, 1, stream, std::max(1, num_sms() - reserve));
         SPH_CUDA(cudaEventRecord(ev_bulk[k], stream));
       }
