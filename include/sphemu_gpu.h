@@ -117,8 +117,8 @@ int sphemu_gpu_chol_create(int n, const sphemu_chol_config* cfg, sphemu_chol_t* 
 int sphemu_gpu_chol_destroy(sphemu_chol_t h);
 /* 2D block-cyclic distribution over a P x Q grid of GPUs (one process per
  * GPU, the caller sets the device first): tile (i, j) is stored on rank
- * ((i + j div Q) mod P) * Q + (j mod Q) (a block-cyclic map whose row shift spreads
- * the diagonal tiles over all ranks); panel tiles travel over NCCL at their storage
+ * ((i + s (j div Q)) mod P) * Q + (j mod Q), s the smallest shift with
+ * gcd(Q + s, P) = 1 (block-cyclic with the diagonal tiles spread over all ranks); panel tiles travel over NCCL at their storage
  * precision. All ranks call every handle function collectively; the dense
  * factor of store_dense is gathered on rank 0. uid128 comes from
  * sphemu_gpu_nccl_unique_id on rank 0 (the caller distributes it). */

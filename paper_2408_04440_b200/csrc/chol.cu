@@ -16,6 +16,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <numeric>
 #include <string>
 #include <thread>
 #include <tuple>
@@ -231,11 +232,19 @@ __global__ void k_diff_norms(int n, const double* a, const double* b, double* su
 
 // 2D block-cyclic owner of tile (i, j) on a P x Q grid: process column
 // j mod Q (so panel column k lives in one process column, as the exchange
-// plan assumes) and process row (i + j div Q) mod P. The shift by the
-// column-block index spreads the diagonal tiles — the FP64 band, whose SYRK
-// updates cost ~50x a BF16 tile's — over every rank instead of only the
-// P = Q diagonal ranks of the plain (i mod P, j mod Q) map.
-inline int block_cyclic_owner(int i, int j, int P, int Q) { return ((i + j / Q) % P) * Q + (j % Q); }
+// plan assumes) and process row (i + s * (j div Q)) mod P. The shift s is the
+// smallest with gcd(Q + s, P) = 1, which makes the diagonal tiles — the FP64
+// band, whose SYRK updates cost ~50x a BF16 tile's — visit every rank
+// (i = Q a + c lands on row ((Q + s) a + c) mod P) instead of only the
+// diagonal ranks of the plain (i mod P, j mod Q) map when gcd(P, Q) > 1.
+inline int block_cyclic_shift(int P, int Q) {
+  int s = 0;
+  while (std::gcd(Q + s, P) != 1) ++s;
+  return s;
+}
+inline int block_cyclic_owner(int i, int j, int P, int Q) {
+  return ((i + block_cyclic_shift(P, Q) * (j / Q)) % P) * Q + (j % Q);
+}
 
 // Host-only 2D block-cyclic layout (no CUDA calls): this rank's tile offsets
 // in its arena and the per-step panel exchange plan (panel tiles of step k
@@ -894,10 +903,9 @@ struct Chol {
       // SMs left free for the chain while the bulk runs: the distributed chain
       // also carries the panel exchange and import, and each rank's bulk
       // shrinks with the grid (SPHEMU_DIST_RESERVE overrides).
-      static const int reserve = [] {
-        const char* e = std::getenv("SPHEMU_DIST_RESERVE");
-        return e ? std::atoi(e) : 48;  // 4-GPU C3: 32 -> 501, 48 -> 488, 64 -> 515 ms
-      }();
+      // measured C3: 2x1 grid 32 -> 749 ms, 48 -> 816; 2x2 grid 32 -> 501, 48 -> 488, 64 -> 515
+      const char* env_reserve = std::getenv("SPHEMU_DIST_RESERVE");
+      const int reserve = env_reserve ? std::atoi(env_reserve) : (P * Q >= 4 ? 48 : kChainCtas);
       SPH_CUDA(cudaEventRecord(ev_start_p, stream));
       SPH_CUDA(cudaStreamWaitEvent(pstream, ev_start_p, 0));
       op_potrf_dist(0, pstream);
