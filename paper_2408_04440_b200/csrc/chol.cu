@@ -452,8 +452,19 @@ struct Chol {
       if (used >= kSlabs) SPH_CUDA(cudaStreamWaitEvent(cstream, ev_in_free[s], 0));
       double* dst = islab.get() + s * slab;
       const int w = std::min(n, (i + 1) * lb);
-      SPH_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * n, a + static_cast<int64_t>(i) * lb * lda, sizeof(double) * lda,
-                                 sizeof(double) * w, rows(i), cudaMemcpyHostToDevice, cstream));
+      if (!dist()) {
+        SPH_CUDA(cudaMemcpy2DAsync(dst, sizeof(double) * n, a + static_cast<int64_t>(i) * lb * lda,
+                                   sizeof(double) * lda, sizeof(double) * w, rows(i), cudaMemcpyHostToDevice, cstream));
+      } else {  // only this rank's tiles of the row cross the host link
+        for (int j = 0; j <= i; ++j) {
+          if (!mine(i, j)) continue;
+          const int cw = std::min(lb, n - j * lb);
+          SPH_CUDA(cudaMemcpy2DAsync(dst + static_cast<int64_t>(j) * lb, sizeof(double) * n,
+                                     a + static_cast<int64_t>(i) * lb * lda + static_cast<int64_t>(j) * lb,
+                                     sizeof(double) * lda, sizeof(double) * cw, rows(i), cudaMemcpyHostToDevice,
+                                     cstream));
+        }
+      }
       SPH_CUDA(cudaEventRecord(ev_in_full[s], cstream));
       SPH_CUDA(cudaStreamWaitEvent(stream, ev_in_full[s], 0));
       k_load_dense<<<dim3(static_cast<unsigned>(i + 1), gy), 256, 0, stream>>>(
