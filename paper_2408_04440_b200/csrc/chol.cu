@@ -477,11 +477,16 @@ struct Chol {
 
   void begin_host_out(double* out, int64_t ldo) {
     ensure_io();
-    if (oslab.n < static_cast<size_t>(n) * lb) oslab.alloc(static_cast<size_t>(n) * lb);
+    if (oslab.n < static_cast<size_t>(n) * lb * col_group()) oslab.alloc(static_cast<size_t>(n) * lb * col_group());
+    col_pending = -1;
     hout = out;
     hldo = ldo;
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const int T = static_cast<int>(std::min(8u, std::max(1u, hw / 2)));
+    static const int t_env = [] {
+      const char* e = std::getenv("SPHEMU_ZERO_THREADS");
+      return e ? std::atoi(e) : -1;
+    }();
+    const int T = t_env >= 0 ? t_env : static_cast<int>(std::min(8u, std::max(1u, hw / 2)));
     const int nn = n, l = lb;
     for (int t = 0; t < T; ++t)
       zeroers.emplace_back([=] {
@@ -493,15 +498,33 @@ struct Chol {
   }
 
   // Column k of the factor is final on stream s: convert and copy it out.
+  // Column k of the factor is final on stream s. Columns leave in groups of
+  // kColGroup (one conversion kernel + one 2-D copy with rows of
+  // kColGroup * lb doubles: wide rows keep the D2H engine efficient).
+  int col_group() const {
+    static const int g = [] {
+      const char* e = std::getenv("SPHEMU_COL_GROUP");
+      return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    return g;
+  }
+  int col_pending = -1;  // first column of the open group
   void col_out(int k, cudaStream_t s, const TileStore* from = nullptr) {
     if (!hout) return;
+    const int G = col_group();
+    if (col_pending < 0) col_pending = k;
+    if (k - col_pending + 1 < G && k + 1 < nt) return;
+    const int k0 = col_pending;
+    col_pending = -1;
     SPH_CUDA(cudaEventRecord(ev_col, s));
     SPH_CUDA(cudaStreamWaitEvent(dstream, ev_col, 0));
-    const int h = n - k * lb;
-    k_store_col<<<h, 128, 0, dstream>>>(from ? *from : store(), k, oslab.get());
+    const int h = n - k0 * lb;
+    const int W = G * lb;
+    k_store_cols<<<h, 256, 0, dstream>>>(from ? *from : store(), k0, k + 1, W, oslab.get());
     SPH_LAUNCH_CHECK();
-    SPH_CUDA(cudaMemcpy2DAsync(hout + static_cast<int64_t>(k) * lb * hldo + static_cast<int64_t>(k) * lb,
-                               sizeof(double) * hldo, oslab.get(), sizeof(double) * lb, sizeof(double) * rows(k), h,
+    const int width = std::min(n, (k + 1) * lb) - k0 * lb;
+    SPH_CUDA(cudaMemcpy2DAsync(hout + static_cast<int64_t>(k0) * lb * hldo + static_cast<int64_t>(k0) * lb,
+                               sizeof(double) * hldo, oslab.get(), sizeof(double) * W, sizeof(double) * width, h,
                                cudaMemcpyDeviceToHost, dstream));
   }
 

@@ -122,6 +122,25 @@ static __global__ void k_store_col(TileStore ts, int k, double* __restrict__ sla
     slab[(int64_t)blockIdx.x * ts.lb + c] = (k * ts.lb + c <= R) ? load_elem(tp, p, rb + c) : 0.0;
 }
 
+// Tile columns [k0, k1) of the factor as a dense (n - k0 lb) x (k1 - k0) lb
+// slab (pitch W): exact zeros above the diagonal, one CTA per output row.
+static __global__ void k_store_cols(TileStore ts, int k0, int k1, int W, double* __restrict__ slab) {
+  const int R = k0 * ts.lb + blockIdx.x;
+  const int w = min(W, ts.n - k0 * ts.lb);
+  const int i = R / ts.lb;
+  const int64_t rb = (int64_t)(R % ts.lb) * ts.b;
+  for (int c = threadIdx.x; c < w; c += blockDim.x) {
+    const int C = k0 * ts.lb + c;
+    double v = 0.0;
+    if (C <= R) {
+      const int j = C / ts.lb;
+      v = load_elem(ts.tile(i, j), ts.tprec(i, j), rb + C % ts.lb);
+    }
+    slab[(int64_t)blockIdx.x * W + c] = v;
+  }
+  (void)k1;
+}
+
 // ---------------------------------------------------------------------------
 // Diagonal tile: blocked right-looking POTRF (inner block 32) followed by the
 // explicit inverse of the factor (used to turn the panel TRSM into a GEMM).
