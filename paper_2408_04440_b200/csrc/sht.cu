@@ -443,6 +443,70 @@ __global__ void k_ring_fft_inv(const double* __restrict__ G, int n_theta, int L,
   }
 }
 
+// Real-input rings (n_phi even): a ring of n reals is one complex FFT of
+// N = n / 2 points on z_j = x_2j + i x_2j+1, then
+//   X_m = E_m + w^m O_m,  E_m = (Z_m + conj Z_{N-m}) / 2,  O_m = (Z_m - conj Z_{N-m}) / 2i
+// (w = exp(-2 pi i / n)); synthesis builds Z'_k = (X_k + conj X_{N-k}) +
+// i w^-k (X_k - conj X_{N-k}) and one inverse FFT of N points yields
+// x_2j + i x_2j+1. Half the butterflies and half the shared memory of the
+// complex path.
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+
+__global__ void k_ring_rfft_fwd(const double* __restrict__ fields, int n_theta, int L, int R, FftPlan H,
+                                const double2* __restrict__ twn, int T, double* __restrict__ G) {
+  extern __shared__ double2 xs[];
+  const int N = H.n;
+  const int i = blockIdx.x, t0 = blockIdx.y * R;
+  const int nr = min(R, T - t0);
+  for (int e = threadIdx.x; e < nr * N; e += blockDim.x) {
+    const int r = e / N, j = e - r * N;
+    xs[e] = reinterpret_cast<const double2*>(fields + ((int64_t)(t0 + r) * n_theta + i) * 2 * N)[j];
+  }
+  __syncthreads();
+  fft_dif_rings<-1>(xs, nr, H);
+  const double inv = 0.5 / (2 * N);  // the 1/2 of E and O folded into the 1/n_phi scaling
+  const int ntp = (n_theta + 1) & ~1;
+  const int64_t mstride = (int64_t)ntp * 2 * T;
+  double* g = G + (int64_t)i * 2 * T + 2 * t0;
+  for (int e = threadIdx.x; e < L * nr; e += blockDim.x) {
+    const int m = e / nr, r = e - m * nr;
+    const double2 zk = xs[r * N + fft_pos(m, H)];
+    const double2 zc = cconj(xs[r * N + fft_pos(m == 0 ? 0 : N - m, H)]);
+    const double2 e2 = make_double2(zk.x + zc.x, zk.y + zc.y);                 // 2 E
+    const double2 d = make_double2(zk.x - zc.x, zk.y - zc.y);
+    const double2 o2 = make_double2(d.y, -d.x);                                // 2 O = -i d
+    const double2 wo = cmul(twn[m], o2);
+    *reinterpret_cast<double2*>(g + m * mstride + 2 * r) = make_double2((e2.x + wo.x) * inv, (e2.y + wo.y) * inv);
+  }
+}
+
+__global__ void k_ring_rfft_inv(const double* __restrict__ G, int n_theta, int L, int R, FftPlan H,
+                                const double2* __restrict__ twn, int T, double* __restrict__ fields) {
+  extern __shared__ double2 xs[];
+  const int N = H.n;
+  const int i = blockIdx.x, t0 = blockIdx.y * R;
+  const int nr = min(R, T - t0);
+  const int ntp = (n_theta + 1) & ~1;
+  const int64_t mstride = (int64_t)ntp * 2 * T;
+  const double* g = G + (int64_t)i * 2 * T + 2 * t0;
+  for (int e = threadIdx.x; e < nr * N; e += blockDim.x) {
+    const int r = e / N, k = e - r * N;
+    const double2 xk = k < L ? *reinterpret_cast<const double2*>(g + k * mstride + 2 * r) : make_double2(0.0, 0.0);
+    const int km = N - k;  // k = 0 -> X_N = 0 (L <= N)
+    const double2 xm = km < L ? cconj(*reinterpret_cast<const double2*>(g + km * mstride + 2 * r)) : make_double2(0.0, 0.0);
+    const double2 a = make_double2(xk.x + xm.x, xk.y + xm.y);
+    const double2 bv = make_double2(xk.x - xm.x, xk.y - xm.y);
+    const double2 wb = cmul(cconj(twn[k]), bv);
+    xs[r * N + k] = make_double2(a.x - wb.y, a.y + wb.x);  // a + i (w^-k b)
+  }
+  __syncthreads();
+  fft_dif_rings<+1>(xs, nr, H);
+  for (int e = threadIdx.x; e < nr * N; e += blockDim.x) {
+    const int r = e / N, j = e - r * N;
+    reinterpret_cast<double2*>(fields + ((int64_t)(t0 + r) * n_theta + i) * 2 * N)[j] = xs[r * N + fft_pos(j, H)];
+  }
+}
+
 // ===========================================================================
 // Device: Legendre stages (grouped FP64 GEMMs over m)
 // ===========================================================================
@@ -531,8 +595,9 @@ struct Sht {
   DevBuf<double> psi, y;
   DevBuf<int64_t> d_psi_off, d_y_off, d_z_off;
   std::vector<int64_t> psi_off, y_off, z_off;
-  DevBuf<double2> tw_phi;
-  FftPlan fplan{};
+  DevBuf<double2> tw_phi, tw_half;
+  FftPlan fplan{}, hplan{};
+  bool real_rings = false;
   int rings_per_cta = 1;
   size_t fft_smem = 0;
   int chunk = 64;
@@ -635,17 +700,41 @@ struct Sht {
     tw_phi.alloc(n_phi);
     SPH_CUDA(cudaMemcpy(tw_phi.get(), twp.data(), n_phi * sizeof(double2), cudaMemcpyHostToDevice));
     fplan.tw = tw_phi.get();
+    // Half-length plan for real rings (n_phi even and L <= n_phi / 2).
+    real_rings = (n_phi % 2 == 0) && L <= n_phi / 2 && !(std::getenv("SPHEMU_SHT_COMPLEX_RINGS"));
+    if (real_rings) {
+      const int N = n_phi / 2;
+      hplan.n = N;
+      hplan.stages = 0;
+      int r2 = N;
+      auto hpush = [&](int p) { hplan.radix[hplan.stages++] = p; };
+      while (r2 % 4 == 0) { hpush(4); r2 /= 4; }
+      while (r2 % 2 == 0) { hpush(2); r2 /= 2; }
+      for (int p = 3; r2 > 1; p += 2)
+        while (r2 % p == 0) { hpush(p); r2 /= p; }
+      std::vector<double2> twh(N);
+      for (int t = 0; t < N; ++t) {
+        const double a = 2.0 * M_PI * t / N;
+        twh[t] = make_double2(std::cos(a), -std::sin(a));
+      }
+      tw_half.alloc(N);
+      SPH_CUDA(cudaMemcpy(tw_half.get(), twh.data(), N * sizeof(double2), cudaMemcpyHostToDevice));
+      hplan.tw = tw_half.get();
+    }
     // snapshots per FFT CTA: runs of >= 64 bytes per (m, ring) in G, within ~200 KB of smem
     {
       const char* e = std::getenv("SPHEMU_FFT_R");
       const int cap = e ? std::max(1, std::atoi(e)) : 16;
       // ~48 KB of rings per CTA (measured best for n_phi = 360 and 1440)
-      rings_per_cta = std::max(1, std::min(cap, (48 * 1024) / (16 * n_phi)));
+      const int pts_ring = real_rings ? n_phi / 2 : n_phi;
+      rings_per_cta = std::max(1, std::min(cap, (48 * 1024) / (16 * pts_ring)));
     }
-    fft_smem = (size_t)rings_per_cta * n_phi * sizeof(double2);
+    fft_smem = (size_t)rings_per_cta * (real_rings ? n_phi / 2 : n_phi) * sizeof(double2);
     if (fft_smem > 48 * 1024) {
       SPH_CUDA(cudaFuncSetAttribute(k_ring_fft_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
       SPH_CUDA(cudaFuncSetAttribute(k_ring_fft_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
+      SPH_CUDA(cudaFuncSetAttribute(k_ring_rfft_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
+      SPH_CUDA(cudaFuncSetAttribute(k_ring_rfft_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fft_smem));
     }
     SPH_CUDA(cudaFuncSetAttribute(k_legendre_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(D2Smem)));
     SPH_CUDA(cudaFuncSetAttribute(k_legendre_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(D2Smem)));
@@ -682,8 +771,12 @@ struct Sht {
     for (int64_t t0 = 0; t0 < n; t0 += chunk) {
       const int T = (int)std::min<int64_t>(chunk, n - t0);
       ensure(T);
-      k_ring_fft_fwd<<<dim3(n_theta, ceil_div(T, rings_per_cta)), 256, fft_smem, stream>>>(
-          fields + t0 * pts, n_theta, L, rings_per_cta, fplan, T, G.get());
+      if (real_rings)
+        k_ring_rfft_fwd<<<dim3(n_theta, ceil_div(T, rings_per_cta)), 256, fft_smem, stream>>>(
+            fields + t0 * pts, n_theta, L, rings_per_cta, hplan, tw_phi.get(), T, G.get());
+      else
+        k_ring_fft_fwd<<<dim3(n_theta, ceil_div(T, rings_per_cta)), 256, fft_smem, stream>>>(
+            fields + t0 * pts, n_theta, L, rings_per_cta, fplan, T, G.get());
       SPH_LAUNCH_CHECK();
       k_legendre_fwd<<<dim3(ceil_div(2 * T, D2_BN), ceil_div(L, D2_BM), L), D2_THREADS, sizeof(D2Smem), stream>>>(
           psi.get(), d_psi_off.get(), G.get(), L, n_theta, T, coeffs + t0 * nc);
@@ -701,8 +794,12 @@ struct Sht {
       k_legendre_inv<<<dim3(ceil_div(2 * T, D2_BN), ceil_div(n_theta, D2_BM), L), D2_THREADS, sizeof(D2Smem), stream>>>(
           y.get(), d_y_off.get(), Z.get(), d_z_off.get(), L, n_theta, T, G.get());
       SPH_LAUNCH_CHECK();
-      k_ring_fft_inv<<<dim3(n_theta, ceil_div(T, rings_per_cta)), 256, fft_smem, stream>>>(
-          G.get(), n_theta, L, rings_per_cta, fplan, T, fields + t0 * pts);
+      if (real_rings)
+        k_ring_rfft_inv<<<dim3(n_theta, ceil_div(T, rings_per_cta)), 256, fft_smem, stream>>>(
+            G.get(), n_theta, L, rings_per_cta, hplan, tw_phi.get(), T, fields + t0 * pts);
+      else
+        k_ring_fft_inv<<<dim3(n_theta, ceil_div(T, rings_per_cta)), 256, fft_smem, stream>>>(
+            G.get(), n_theta, L, rings_per_cta, fplan, T, fields + t0 * pts);
       SPH_LAUNCH_CHECK();
     }
   }
