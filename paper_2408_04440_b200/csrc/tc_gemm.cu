@@ -194,7 +194,8 @@ struct TcLayout {
   static constexpr int kCBox = 32 * 128;
   static constexpr int kCBytes = TC_EPI_WARPS * kRing * kCBox;
   static constexpr int kSmem = kStages * kStage + kCBytes + 1024 /*align*/ + 1024 /*barriers + schedule*/;
-  static constexpr int kTmemCols = 2 * BN;        // double-buffered accumulator
+  static constexpr int kAcc = (512 / BN) > 4 ? 4 : (512 / BN);  // TMEM accumulators in flight (512 columns)
+  static constexpr int kTmemCols = kAcc * BN;
   static_assert(kSmem <= 232448, "shared memory budget");
 };
 
@@ -213,8 +214,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(cbuf + Lay::kCBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* cfull = tempty + 2;  // [epilogue warp][kRing]
+  uint64_t* tempty = tfull + Lay::kAcc;
+  uint64_t* cfull = tempty + Lay::kAcc;  // [epilogue warp][kRing]
   uint64_t* sfull = cfull + TC_EPI_WARPS * Lay::kRing;  // dynamic schedule ring: producer -> consumers
   uint64_t* sempty = sfull + 4;                          // consumers (MMA warp + epilogue warps) -> producer
   int* sched = reinterpret_cast<int*>(sempty + 4);       // [4] claimed items (-1 = none left)
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < Lay::kAcc; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], CG * TC_EPI_WARPS);  // one arrive per epilogue warp of each CTA
     }
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         else umma_commit(&tfull[acc]);
       }
       __syncwarp();
-      if (++acc == 2) {
+      if (++acc == Lay::kAcc) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -701,7 +702,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
         else mbar_arrive(&tempty[acc]);
       }
-      if (++acc == 2) {
+      if (++acc == Lay::kAcc) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -1034,7 +1035,12 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
     else
       launch_tc<128, OP_TF32X3, MODE_UPDATE>(pf.m_phi_a, pf.m_plo_a, pf.m_phi_b, pf.m_plo_b, pf.m_c32, a, s, max_ctas);
   } else {
-    a.sub_n = ts.b / pf.bn;
+    static const int hp_bn = [] {
+      const char* e = std::getenv("SPHEMU_HP_BN");
+      return e ? std::atoi(e) : 256;
+    }();
+    const int bn_hp = (pf.bn == 256 && hp_bn == 256) || pair ? 256 : 128;
+    a.sub_n = ts.b / bn_hp;
     a.sub_per = (ts.b / (TC_BM * (pair ? 2 : 1))) * a.sub_n;
     a.items = cnt * a.sub_per;
     if (pair) {
@@ -1044,16 +1050,16 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
       else
         launch_tc<256, OP_F16, MODE_UPDATE, 2>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s,
                                                max_ctas);
-    } else if (pf.bn == 256) {
+    } else if (bn_hp == 256) {
       if (hp_format == SPHEMU_HP_BF16)
         launch_tc<256, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas);
       else
         launch_tc<256, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas);
-    } else {
+    } else {  // 128-wide N: B boxes of 128 rows (the A-side map)
       if (hp_format == SPHEMU_HP_BF16)
-        launch_tc<128, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas);
+        launch_tc<128, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas);
       else
-        launch_tc<128, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas);
+        launch_tc<128, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas);
     }
   }
 }
