@@ -770,6 +770,16 @@ struct Chol {
     prof_end(pp, s);
   }
 
+  // The chain's single diagonal-tile SYRK is latency-bound: 64 x 64 CTAs
+  // (36 active on a 512 tile) finish sooner than the 128 x 64 bulk kernel's 20.
+  static bool chain_small_syrk() {
+    static const bool on = [] {
+      const char* e = std::getenv("SPHEMU_CHAIN_SYRK64");
+      return !(e && e[0] == '0');
+    }();
+    return on;
+  }
+
   void op_update(int k, int part, cudaStream_t s, int max_ctas) {
     const int set = k & 1;
     for (int cls = 0; cls < 3; ++cls) {
@@ -782,7 +792,7 @@ struct Chol {
         tc_update(store(), k, cls, cfg.hp_format, lst, lrows.get() + list_off[slot], cnt, p64_[set].get(),
                   panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s));
       } else {
-        if (b % D2_BM == 0) {
+        if (b % D2_BM == 0 && !(part == 0 && chain_small_syrk())) {
           static bool attr = false;
           if (!attr) {
             SPH_CUDA(cudaFuncSetAttribute(k_update_fp64_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
