@@ -501,7 +501,7 @@ def sht_c4(sph, snapshots=1000):
             "note": "the driver's 8 760-snapshot hourly year runs in chunks of this batch"}
 
 
-def emulation_point(sph, L=90, replicates=100, t_out=24, order=3):
+def emulation_point(sph, L=90, replicates=100, t_out=24, order=3, world=1, rank=0):
     """Emulation generator throughput (stochastic.cpp:217-277): R replicates x T steps on the (L+1) x 2L grid,
     V = the device factor of make_spd_test_matrix(L^2) (dp), AR(3), device Philox normals; the one-shot C-ABI
     call with host buffers (V in, fields out) is the timed unit."""
@@ -521,11 +521,18 @@ def emulation_point(sph, L=90, replicates=100, t_out=24, order=3):
     sigma = np.ones(pts)
     v2 = np.full(pts, 0.04)
     sph._sphemu.emulate(plan, v, phi, means, sigma, v2, t_out, 7, 2, "philox")  # warm-up
+    # replicates sharded over the ranks (draws depend only on the replicate: no communication)
+    per = (replicates + world - 1) // world
+    r0 = min(replicates, rank * per)
+    cnt = max(0, min(per, replicates - r0))
+    barrier(world)
     t0 = time.perf_counter()
-    out = sph._sphemu.emulate(plan, v, phi, means, sigma, v2, t_out, 7, replicates, "philox")
-    dt = time.perf_counter() - t0
+    out = sph._sphemu.emulate(plan, v, phi, means, sigma, v2, t_out, 7, cnt, "philox", r_begin=r0) if cnt else \
+        np.zeros(1)
+    dt = max_over_ranks(time.perf_counter() - t0, world)
     burn = 10 * order
     return {"band_limit": L, "d": d, "grid": f"{nt}x{nphi}", "replicates": replicates, "steps": t_out,
+            "sharding": f"replicate ranges over {world} GPU(s)",
             "snapshots_per_s": replicates * t_out / dt, "seconds": dt,
             "trmm_fp64_tflops": d * d * replicates * (burn + t_out) / dt / 1e12,
             "finite": bool(np.isfinite(out).all()),
@@ -575,7 +582,7 @@ def run_ours(args, world, rank, local):
 
     sht = sht_throughput(sph, world)
     c4 = sht_c4(sph) if (world == 1 and not args.no_c4) else None
-    emul = emulation_point(sph) if (world == 1 and not args.no_c4) else None
+    emul = emulation_point(sph, world=world, rank=rank) if not args.no_c4 else None
 
     if rank != 0:
         return

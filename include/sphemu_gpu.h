@@ -211,6 +211,15 @@ int sphemu_gpu_emulate(sphemu_sht_t p, const double* v, int d, const double* phi
                        const double* means, const double* sigma, const double* v2, int t_out,
                        uint64_t seed, int r_len, int rng_mode, double* out);
 
+/* Replicates [r_begin, r_begin + r_count) of the same emulation (out holds
+ * r_count replicates): the draws of replicate r do not depend on the split,
+ * so replicate ranges can run on different GPUs with no communication
+ * (reference mode skips the earlier replicates' draws on the
+ * host, Philox mode indexes the counter by replicate). */
+int sphemu_gpu_emulate_range(sphemu_sht_t p, const double* v, int d, const double* phi, int order,
+                             const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed,
+                             int r_begin, int r_count, int rng_mode, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -118,6 +118,8 @@ def lib():
         L.sphemu_gpu_chol_residual_probe_spd.argtypes = [vp, C.c_uint64, C.c_int, dp]
         L.sphemu_gpu_emulate.argtypes = [vp, vp, C.c_int, vp, C.c_int, vp, vp, vp, C.c_int, C.c_uint64,
                                          C.c_int, C.c_int, vp]
+        L.sphemu_gpu_emulate_range.argtypes = [vp, vp, C.c_int, vp, C.c_int, vp, vp, vp, C.c_int, C.c_uint64,
+                                               C.c_int, C.c_int, C.c_int, vp]
         L.sphemu_gpu_estimate_innovation_covariance.argtypes = [
             vp, C.c_int, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(CholConfig), vp, C.c_int, vp, C.c_int,
             dp, C.POINTER(CholStats)]
@@ -307,7 +309,7 @@ class Cholesky:
         return out.value
 
 
-def emulate(plan, v, phi, means, sigma, v2, t_out, seed=1, r_len=1, rng="reference"):
+def emulate(plan, v, phi, means, sigma, v2, t_out, seed=1, r_len=1, rng="reference", r_begin=0):
     """emulate (stochastic.cpp:217-277) with the trend evaluated by the caller
     (means: t_out x points, sigma/v2: points). rng="reference" reproduces the
     reference's serial mt19937_64 stream; "philox" draws on the device."""
@@ -320,8 +322,12 @@ def emulate(plan, v, phi, means, sigma, v2, t_out, seed=1, r_len=1, rng="referen
     v2 = np.ascontiguousarray(v2, dtype=np.float64)
     out = np.empty((r_len, t_out, plan.n_theta, plan.n_phi))
     mode = {"reference": 0, "philox": 1}[rng]
-    _check(lib().sphemu_gpu_emulate(plan.h, _ptr(v), d, _ptr(phi_a), phi.shape[0], _ptr(means), _ptr(sigma),
-                                    _ptr(v2), t_out, seed, r_len, mode, _ptr(out)))
+    if r_begin:
+        _check(lib().sphemu_gpu_emulate_range(plan.h, _ptr(v), d, _ptr(phi_a), phi.shape[0], _ptr(means),
+                                              _ptr(sigma), _ptr(v2), t_out, seed, r_begin, r_len, mode, _ptr(out)))
+    else:
+        _check(lib().sphemu_gpu_emulate(plan.h, _ptr(v), d, _ptr(phi_a), phi.shape[0], _ptr(means), _ptr(sigma),
+                                        _ptr(v2), t_out, seed, r_len, mode, _ptr(out)))
     return out
 
 

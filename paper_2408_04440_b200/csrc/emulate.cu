@@ -100,17 +100,25 @@ __device__ __forceinline__ void philox(uint32_t (&c)[4], uint32_t k0, uint32_t k
   }
 }
 
-__global__ void k_philox_normals(uint64_t seed, uint64_t stream, int64_t n, double* out) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t c[4] = {(uint32_t)e, (uint32_t)(e >> 32), (uint32_t)stream, (uint32_t)(stream >> 32)};
+// Normals for replicates [r0, r0 + nrep), per_rep values each: replicate r's
+// values depend only on (seed, stream, r), so any split of the replicates
+// over calls or GPUs draws identical numbers.
+__global__ void k_philox_normals(uint64_t seed, uint64_t stream, int64_t per_rep, int r0, int nrep, double* out) {
+  const int64_t half = (per_rep + 1) / 2;
+  const int64_t n = half * nrep;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rr = q / half, e = q - rr * half;
+    const uint64_t st = stream + ((uint64_t)(r0 + rr) << 8);
+    uint32_t c[4] = {(uint32_t)e, (uint32_t)(e >> 32), (uint32_t)st, (uint32_t)(st >> 32)};
     philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
     const double u1 = ((double)((((uint64_t)c[0] << 32) | c[1]) >> 11) + 1.0) * 0x1.0p-53;
     const double u2 = ((double)((((uint64_t)c[2] << 32) | c[3]) >> 11) + 1.0) * 0x1.0p-53;
     const double rad = sqrt(-2.0 * log(u1));
     double s, co;
     sincospi(2.0 * u2, &s, &co);
-    out[2 * e] = rad * co;
-    if (2 * e + 1 < n) out[2 * e + 1] = rad * s;
+    double* o = out + rr * per_rep;
+    o[2 * e] = rad * co;
+    if (2 * e + 1 < per_rep) o[2 * e + 1] = rad * s;
   }
 }
 
@@ -138,7 +146,8 @@ struct RefGaussian {
 
 void emulate(void* plan, int n_theta, int n_phi, int L, const double* v, int d, const double* phi, int order,
              const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed, int r_len,
-             int rng_mode, double* out) {
+             int rng_mode, double* out, int r_begin) {
+  if (r_begin < 0) throw std::invalid_argument("first replicate must be >= 0");
   if (t_out < 1 || r_len < 1) throw std::invalid_argument("need t_out, r_len >= 1");
   if (d != L * L) throw std::invalid_argument("transform plan does not match the model");
   if (order < 0 || order > 16) throw std::invalid_argument("lag order must lie in [0, 16]");
@@ -165,6 +174,8 @@ void emulate(void* plan, int n_theta, int n_phi, int L, const double* v, int d, 
     hH.resize((size_t)S * d);
     hE.resize(ytot);
     RefGaussian g(seed);
+    for (int r = 0; r < r_begin; ++r)  // one serial stream: skip the replicates drawn elsewhere
+      for (int64_t e = 0; e < steps * d + (int64_t)t_out * points; ++e) g.normal();
     for (int r = 0; r < r_len; ++r) {
       double* h = hH.data() + (size_t)r * steps * d;
       for (int64_t e = 0; e < steps * d; ++e) h[e] = g.normal();
@@ -174,9 +185,9 @@ void emulate(void* plan, int n_theta, int n_phi, int L, const double* v, int d, 
     SPH_CUDA(cudaMemcpyAsync(dH.get(), hH.data(), hH.size() * sizeof(double), cudaMemcpyHostToDevice, s));
     SPH_CUDA(cudaMemcpyAsync(dEps.get(), hE.data(), hE.size() * sizeof(double), cudaMemcpyHostToDevice, s));
   } else {
-    k_philox_normals<<<4 * num_sms(), 256, 0, s>>>(seed, 1, S * d, dH.get());
+    k_philox_normals<<<4 * num_sms(), 256, 0, s>>>(seed, 1, steps * d, r_begin, r_len, dH.get());
     SPH_LAUNCH_CHECK();
-    k_philox_normals<<<4 * num_sms(), 256, 0, s>>>(seed, 2, ytot, dEps.get());
+    k_philox_normals<<<4 * num_sms(), 256, 0, s>>>(seed, 2, (int64_t)t_out * points, r_begin, r_len, dEps.get());
     SPH_LAUNCH_CHECK();
   }
   SPH_CUDA(cudaFuncSetAttribute(k_emul_xi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(D2Smem)));

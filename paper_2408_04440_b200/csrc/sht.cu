@@ -869,7 +869,7 @@ struct sphemu_sht_s {
 namespace sphemu_gpu {
 void emulate(void* plan, int n_theta, int n_phi, int L, const double* v, int d, const double* phi, int order,
              const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed, int r_len,
-             int rng_mode, double* out);
+             int rng_mode, double* out, int r_begin);
 
 // Bridge for emulate.cu: the plan's stream, and a device-resident inverse.
 void sht_inverse_device(void* plan, const double* coeffs, int64_t n, double* fields, cudaStream_t* s_out) {
@@ -921,7 +921,16 @@ int sphemu_gpu_emulate(sphemu_sht_t p, const double* v, int d, const double* phi
                        double* out) {
   return guard([&] {
     emulate(p, p->p->n_theta, p->p->n_phi, p->p->L, v, d, phi, order, means, sigma, v2, t_out, seed, r_len,
-            rng_mode, out);
+            rng_mode, out, 0);
+  });
+}
+
+int sphemu_gpu_emulate_range(sphemu_sht_t p, const double* v, int d, const double* phi, int order,
+                             const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed,
+                             int r_begin, int r_count, int rng_mode, double* out) {
+  return guard([&] {
+    emulate(p, p->p->n_theta, p->p->n_phi, p->p->L, v, d, phi, order, means, sigma, v2, t_out, seed, r_count,
+            rng_mode, out, r_begin);
   });
 }
 

@@ -50,3 +50,19 @@ def test_philox_stream_statistics(sph, O):
     va, vb = a.reshape(-1, nt * nphi).var(0), b.reshape(-1, nt * nphi).var(0)
     assert np.abs(va / vb - 1).max() < 0.1
     assert np.abs(a.mean(axis=(0, 1))).max() < 5 * np.sqrt(va.max() / (t_out * r_len) * 10)
+
+
+@pytest.mark.parametrize("rng_mode", [0, 1])
+def test_replicate_ranges_compose(sph, O, rng_mode):
+    """replicate ranges run independently (one GPU each, no
+    communication) and reproduce the single call bitwise."""
+    L, order = 6, 2
+    v, phi, sigma, v2, nt, nphi = model(O, L, order)
+    t_out, r_len = 12, 5
+    means = np.zeros((t_out, nt * nphi))
+    plan = sph.ShtPlan(nt, nphi, L)
+    mode = ["reference", "philox"][rng_mode]
+    full = sph._sphemu.emulate(plan, v, phi, means, sigma, v2, t_out, 21, r_len, mode)
+    parts = [sph._sphemu.emulate(plan, v, phi, means, sigma, v2, t_out, 21, cnt, mode, r_begin=beg)
+             for beg, cnt in ((0, 2), (2, 1), (3, 2))]
+    assert np.array_equal(np.concatenate(parts), full)
