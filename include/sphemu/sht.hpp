@@ -151,6 +151,14 @@ inline EquiangularField inverse_sht(const ShtPlan& plan, const HarmonicVector& c
   return out;
 }
 
+// synth_bandlimited (sht.hpp:143, sht.cpp:435-466): direct synthesis on any grid, including under-resolved ones.
+inline EquiangularField synth_bandlimited(const HarmonicVector& coeffs, GridSpec target) {
+  EquiangularField out(target);
+  detail::check(sphemu_gpu_synth_bandlimited(coeffs.values.data(), SPHEMU_HOST, 1, coeffs.band_limit, target.n_theta,
+                                             target.n_phi, out.values.data(), SPHEMU_HOST));
+  return out;
+}
+
 // Batches (sht.cpp:374-404); threads is accepted for API parity (the device batches every slice).
 inline CoeffSeries forward_sht_batch(const ShtPlan& plan, const FieldSeries& series, int threads = 1) {
   (void)threads;

@@ -193,6 +193,12 @@ int sphemu_gpu_sht_forward(sphemu_sht_t p, const double* fields, int where_in, i
 /* inverse_sht_batch (sht.cpp:390-404). */
 int sphemu_gpu_sht_inverse(sphemu_sht_t p, const double* coeffs, int where_in, int64_t n,
                            double* fields, int where_out);
+/* synth_bandlimited (sht.cpp:435-466, declared sht.hpp:143): direct
+ * Legendre synthesis of n packed L^2 coefficient vectors onto any
+ * n_theta x n_phi equiangular grid, including grids that cannot resolve L
+ * (the Python inverse_sht fallback, bindings/module.cpp:92-94). */
+int sphemu_gpu_synth_bandlimited(const double* coeffs, int where_in, int64_t n, int band_limit,
+                                 int n_theta, int n_phi, double* fields, int where_out);
 void* sphemu_gpu_sht_stream(sphemu_sht_t p);
 /* Seconds spent building the plan (Wigner recurrence + operator build). */
 double sphemu_gpu_sht_plan_seconds(sphemu_sht_t p);

@@ -11,17 +11,20 @@ from ._sphemu import (  # noqa: F401
     ShtPlan,
     __version__,
     assign_precisions,
+    emulate,
+    estimate_innovation_covariance,
     forward_sht,
     inverse_sht,
     make_spd_matrix,
     nccl_unique_id,
     max_band_limit,
     resolution_summary,
+    synth_bandlimited,
     tiled_cholesky,
 )
 
 __all__ = [
-    "Cholesky", "NotPositiveDefiniteError", "ShtPlan", "__version__", "assign_precisions",
-    "forward_sht", "inverse_sht", "make_spd_matrix", "nccl_unique_id", "max_band_limit", "resolution_summary",
-    "tiled_cholesky",
+    "Cholesky", "NotPositiveDefiniteError", "ShtPlan", "__version__", "assign_precisions", "emulate",
+    "estimate_innovation_covariance", "forward_sht", "inverse_sht", "make_spd_matrix", "nccl_unique_id", "max_band_limit", "resolution_summary",
+    "synth_bandlimited", "tiled_cholesky",
 ]

@@ -105,6 +105,8 @@ def lib():
         L.sphemu_gpu_sht_forward.argtypes = [vp, vp, C.c_int, i64, vp, C.c_int]
         L.sphemu_gpu_sht_inverse.argtypes = [vp, vp, C.c_int, i64, vp, C.c_int]
         L.sphemu_gpu_sht_stream.argtypes = [vp]
+        L.sphemu_gpu_synth_bandlimited.argtypes = [vp, C.c_int, i64, C.c_int, C.c_int, C.c_int, vp,
+                                                   C.c_int]
         L.sphemu_gpu_sht_stream.restype = vp
         L.sphemu_gpu_sht_plan_seconds.argtypes = [vp]
         L.sphemu_gpu_sht_plan_seconds.restype = C.c_double
@@ -442,10 +444,27 @@ def inverse_sht(coeffs, n_theta=0, n_phi=0):
     if n_theta <= 0:
         n_theta, n_phi = big_l + 1, 2 * big_l  # GridSpec::from_band_limit
     if big_l > max_band_limit(n_theta, n_phi):
-        raise ValueError(f"grid {n_theta}x{n_phi} does not resolve band limit {big_l} "
-                         "(direct Legendre synthesis onto under-resolved grids is not on the "
-                         "B200 path yet)")
+        return synth_bandlimited(c, n_theta, n_phi)  # module.cpp:92-94
     return ShtPlan(n_theta, n_phi, big_l).inverse(c)[0]
+
+
+def synth_bandlimited(coeffs, n_theta, n_phi):
+    """synth_bandlimited (sht.cpp:435-466): direct synthesis on any grid.
+
+    coeffs is (L^2,) or (n, L^2); the result is (n_theta, n_phi) or
+    (n, n_theta, n_phi).
+    """
+    c = np.ascontiguousarray(coeffs, dtype=np.float64)
+    single = c.ndim == 1
+    c2 = c.reshape(1, -1) if single else c
+    if c2.ndim != 2:
+        raise ValueError("expected (L^2,) or (n, L^2) coefficients")
+    big_l = _band_limit_of_coeffs(c2.shape[1])
+    max_band_limit(n_theta, n_phi)  # grid validation (grid.cpp:27-29)
+    out = np.empty((c2.shape[0], n_theta, n_phi), dtype=np.float64)
+    _check(lib().sphemu_gpu_synth_bandlimited(_ptr(c2), HOST, c2.shape[0], big_l, n_theta, n_phi,
+                                              _ptr(out), HOST))
+    return out[0] if single else out
 
 
 def resolution_summary(band_limit):

@@ -935,3 +935,105 @@ int sphemu_gpu_emulate_range(sphemu_sht_t p, const double* v, int d, const doubl
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// Direct synthesis onto grids that cannot resolve L (sht.cpp:406-466,
+// synth_bandlimited; the Python inverse_sht fallback of module.cpp:92-94).
+// ===========================================================================
+namespace sphemu_gpu {
+
+// Fully normalized P~_lm(cos theta_i) (normalized_legendre_all, sht.cpp:406-427):
+// P[i][l(l+1)/2 + m]. One CTA per ring: thread 0 runs the sectoral chain,
+// then each thread walks the l-recurrence of its m columns.
+__global__ void k_legendre_table(int L, int n_theta, double* P) {
+  const int i = blockIdx.x;
+  const double th = 3.14159265358979323846 * i / (n_theta - 1);
+  const double ct = cos(th), st = sin(th);
+  double* p = P + (int64_t)i * L * (L + 1) / 2;
+  auto at = [&](int l, int m) -> double& { return p[(int64_t)l * (l + 1) / 2 + m]; };
+  if (threadIdx.x == 0) {
+    at(0, 0) = 1.0 / sqrt(4.0 * 3.14159265358979323846);
+    for (int m = 1; m < L; ++m) at(m, m) = -sqrt((2.0 * m + 1.0) / (2.0 * m)) * st * at(m - 1, m - 1);
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < L; m += blockDim.x) {
+    if (m + 1 < L) at(m + 1, m) = sqrt(2.0 * m + 3.0) * ct * at(m, m);
+    for (int l = m + 2; l < L; ++l) {
+      const double a = sqrt((4.0 * l * l - 1.0) / ((double)l * l - (double)m * m));
+      const double b = sqrt(((double)(l - 1) * (l - 1) - (double)m * m) / (4.0 * (double)(l - 1) * (l - 1) - 1.0));
+      at(l, m) = a * (ct * at(l - 1, m) - b * at(l - 2, m));
+    }
+  }
+}
+
+// One CTA per (ring i, snapshot t): s_m = sum_l P_lm z_lm, then
+// f(theta_i, phi_j) = Re s_0 + 2 sum_{m>=1} Re(s_m e^{i m phi_j}).
+__global__ void k_synth_direct(const double* __restrict__ coeffs, const double* __restrict__ P, int L, int n_theta,
+                               int n_phi, double* __restrict__ fields) {
+  extern __shared__ double2 sm_s[];
+  const int i = blockIdx.x, t = blockIdx.y;
+  const double* z = coeffs + (int64_t)t * L * L;
+  const double* p = P + (int64_t)i * L * (L + 1) / 2;
+  for (int m = threadIdx.x; m < L; m += blockDim.x) {
+    double re = 0.0, im = 0.0;
+    for (int l = m; l < L; ++l) {
+      const double pl = p[(int64_t)l * (l + 1) / 2 + m];
+      if (m == 0) {
+        re += pl * z[(int64_t)l * l];
+      } else {
+        re += pl * z[(int64_t)l * l + 2 * m - 1];
+        im += pl * z[(int64_t)l * l + 2 * m];
+      }
+    }
+    sm_s[m] = make_double2(re, im);
+  }
+  __syncthreads();
+  double* out = fields + ((int64_t)t * n_theta + i) * n_phi;
+  for (int j = threadIdx.x; j < n_phi; j += blockDim.x) {
+    double v = sm_s[0].x;
+    for (int m = 1; m < L; ++m) {
+      double s, c;
+      sincospi(2.0 * (double)((int64_t)m * j % n_phi) / n_phi, &s, &c);  // phi_j = 2 pi j / n_phi
+      v += 2.0 * (sm_s[m].x * c - sm_s[m].y * s);
+    }
+    out[j] = v;
+  }
+}
+
+}  // namespace sphemu_gpu
+
+extern "C" int sphemu_gpu_synth_bandlimited(const double* coeffs, int where_in, int64_t n, int band_limit,
+                                            int n_theta, int n_phi, double* fields, int where_out) {
+  using namespace sphemu_gpu;
+  return guard([&] {
+    if (band_limit < 1) throw std::invalid_argument("band limit must be positive");
+    if (n_theta < 2) throw std::invalid_argument("grid needs at least two latitude rings");
+    if (n_phi < 1) throw std::invalid_argument("grid needs at least one longitude point");
+    if (n <= 0) return;
+    const int L = band_limit;
+    const int64_t nc = (int64_t)L * L, pts = (int64_t)n_theta * n_phi;
+    DevBuf<double> dP((size_t)n_theta * L * (L + 1) / 2), dc, df;
+    const double* cin = coeffs;
+    double* fout = fields;
+    if (where_in == SPHEMU_HOST) {
+      dc.alloc((size_t)n * nc);
+      SPH_CUDA(cudaMemcpy(dc.get(), coeffs, sizeof(double) * n * nc, cudaMemcpyHostToDevice));
+      cin = dc.get();
+    }
+    if (where_out == SPHEMU_HOST) {
+      df.alloc((size_t)n * pts);
+      fout = df.get();
+    }
+    k_legendre_table<<<n_theta, 128>>>(L, n_theta, dP.get());
+    SPH_LAUNCH_CHECK();
+    for (int64_t t0 = 0; t0 < n; t0 += 65535) {
+      const int64_t T = std::min<int64_t>(65535, n - t0);
+      k_synth_direct<<<dim3(n_theta, (unsigned)T), 128, L * sizeof(double2)>>>(cin + t0 * nc, dP.get(), L, n_theta,
+                                                                              n_phi, fout + t0 * pts);
+      SPH_LAUNCH_CHECK();
+    }
+    if (where_out == SPHEMU_HOST)
+      SPH_CUDA(cudaMemcpy(fields, fout, sizeof(double) * n * pts, cudaMemcpyDeviceToHost));
+    SPH_CUDA(cudaDeviceSynchronize());
+  });
+}

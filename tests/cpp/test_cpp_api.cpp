@@ -172,6 +172,13 @@ int main() {
     double bd = 0.0;
     for (std::size_t e = 0; e < one.size(); ++e) bd = std::fmax(bd, std::fabs(one[e] - cs.slice(1, 2)[e]));
     CHECK(bd < 1e-14);
+    // direct synthesis agrees with the plan on a resolved grid (test_sht.cpp:145-152)
+    EquiangularField via_plan = inverse_sht(p, c), direct = synth_bandlimited(c, p.spec);
+    double sd = 0.0;
+    for (std::size_t e = 0; e < direct.values.size(); ++e)
+      sd = std::fmax(sd, std::fabs(via_plan.values[e] - direct.values[e]));
+    CHECK(sd < 1e-9);
+    CHECK(synth_bandlimited(c, GridSpec{9, 16}).values.size() == 9 * 16);  // under-resolved target
   }
   CHECK(throws<std::invalid_argument>([] { build_plan(GridSpec{9, 16}, 9); }));           // test_sht.cpp:196-199
   CHECK(throws<std::invalid_argument>([] { build_wigner_tables(720); }));                 // 2 GiB cap (F5)

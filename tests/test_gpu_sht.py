@@ -98,3 +98,34 @@ def test_c4_round_trip_property(sph):
     g.forward_device(f.data_ptr(), T, back.data_ptr())
     torch.cuda.synchronize()
     assert (back - c).abs().max().item() < 1e-9 * c.abs().max().item()
+
+
+@pytest.mark.parametrize("grid", [(7, 12, 6), (9, 16, 16), (21, 40, 45), (121, 256, 20)])
+def test_synth_bandlimited_matches_reference_golden(sph, grid):  # sht.cpp:435-466
+    nt, nphi, L = grid
+    G = np.load(GOLDEN)
+    key = f"synth_{nt}x{nphi}_L{L}"
+    assert rel(sph.synth_bandlimited(G[key + "_coeffs"], nt, nphi), G[key + "_field"]) < 1e-12
+
+
+def test_direct_synthesis_matches_transform(sph, O):  # test_sht.cpp:145-152
+    c = O.draw_random_coefficients(6, 13)
+    assert np.abs(sph.ShtPlan(7, 12, 6).inverse(c)[0] - sph.synth_bandlimited(c, 7, 12)).max() < 1e-9
+    c = O.draw_random_coefficients(64, 5)
+    assert rel(sph.synth_bandlimited(c, 65, 128), sph.inverse_sht(c)) < 1e-11
+
+
+def test_inverse_sht_under_resolved_falls_back(sph, O):  # bindings/module.cpp:92-94
+    L = 24
+    c = O.draw_random_coefficients(L, 3)
+    want = np.empty((10, 18))
+    O.lib().so_synth_bandlimited(c, L, 10, 18, want)
+    assert rel(sph.inverse_sht(c, 10, 18), want) < 1e-12
+    batch = np.stack([O.draw_random_coefficients(L, s) for s in range(5)])
+    got = sph.synth_bandlimited(batch, 10, 18)
+    assert got.shape == (5, 10, 18)
+    for s in range(5):
+        O.lib().so_synth_bandlimited(np.ascontiguousarray(batch[s]), L, 10, 18, want)
+        assert rel(got[s], want) < 1e-12
+    with pytest.raises(ValueError):
+        sph.synth_bandlimited(c, 1, 18)

@@ -198,6 +198,16 @@ def test_direct_synthesis_matches(O):  # test_sht.cpp:145-152
     assert np.abs(P.inverse(c)[0] - d).max() < 1e-9
 
 
+@pytest.mark.parametrize("grid", [(7, 12, 6), (9, 16, 16), (21, 40, 45), (121, 256, 20)])
+def test_synth_bandlimited_matches_reference_golden(O, grid):  # sht.cpp:435-466 via oracle/_ref
+    nt, nphi, L = grid
+    G = np.load(GOLDEN)
+    key = f"synth_{nt}x{nphi}_L{L}"
+    d = np.empty((nt, nphi))
+    O.lib().so_synth_bandlimited(G[key + "_coeffs"], L, nt, nphi, d)
+    assert np.array_equal(d, G[key + "_field"])
+
+
 def test_batch_thread_invariance(O):  # test_sht.cpp:163-181
     P = O.Plan(11, 20, 10)
     f = P.inverse(np.stack([O.draw_random_coefficients(10, 100 + s) for s in range(14)]))

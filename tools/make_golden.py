@@ -46,5 +46,12 @@ for (nt, nphi, L) in ((9, 16, 8), (33, 64, 16), (17, 20, 9), (46, 90, 45)):
     out[f"sht_{nt}x{nphi}_L{L}_fields"] = f
     out[f"sht_{nt}x{nphi}_L{L}_x"] = x
     out[f"sht_{nt}x{nphi}_L{L}_fx"] = g
+# synth_bandlimited (sht.cpp:435-466) on resolved and under-resolved grids
+for (nt, nphi, L) in ((7, 12, 6), (9, 16, 16), (21, 40, 45), (121, 256, 20)):
+    c = O.draw_random_coefficients(L, 7 * L + 1)
+    f = np.empty((nt, nphi))
+    R.ref_synth_bandlimited(c, L, nt, nphi, f)
+    out[f"synth_{nt}x{nphi}_L{L}_coeffs"] = c
+    out[f"synth_{nt}x{nphi}_L{L}_field"] = f
 np.savez_compressed(os.path.join(ROOT, "tests", "golden", "ref_vectors.npz"), **out)
 print("wrote", len(out), "arrays")
