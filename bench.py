@@ -55,48 +55,79 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """nvidia-smi clocks + throttle reasons during the timed region.
+
+    nvidia-smi needs a few hundred ms to start, longer than a short timed
+    region, so the sampler is started before the warm-up, waits for its first
+    row, and the summary keeps only the rows stamped inside [mark_start,
+    mark_end] (the nearest row on each side when the region is shorter than
+    the sampling period)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    PERIOD_MS = 50
 
     def __init__(self, index):
         self.index, self.rows, self.proc = index, [], None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", str(self.PERIOD_MS)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.time() + 10.0
+            while not self.rows and time.time() < deadline and self.proc.poll() is None:
+                time.sleep(0.02)
         except OSError:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+        time.sleep(2.5 * self.PERIOD_MS / 1000.0)  # let the row after the region arrive
 
     def __exit__(self, *a):
         if self.proc:
             self.proc.terminate()
             self.proc.wait()
 
+    def window(self):
+        rows = list(self.rows)
+        if self.t0 is None or self.t1 is None:
+            return rows, "whole run"
+        inside = [r for t, r in rows if self.t0 <= t <= self.t1]
+        if inside:
+            return inside, "timed region"
+        before = [r for t, r in rows if t < self.t0][-1:]
+        after = [r for t, r in rows if t > self.t1][:1]
+        return before + after, "nearest rows around a timed region shorter than the sampling period"
+
     def summary(self):
-        if not self.rows:
+        rows, where = self.window()
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         reasons = set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        for r in rows:
             for nm, v in zip(names, r[4:8]):
                 if v.strip().lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "reasons": sorted(reasons), "samples": len(rows), "window": where,
+                "period_ms": self.PERIOD_MS}
 
 
 def dist_setup(args):
@@ -269,6 +300,9 @@ def time_factor(sph, h, wl, args, world, a_dev=None, steps=None, warmup=None, cl
     # CUDA events (the roofline's achieved rate); the full phase breakdown
     # comes from one extra profiled step afterwards.
     h.set_profiling(True, phases=["update_" + dominant_class(wl)])
+    clocks = ClockSampler(clocks_index) if clocks_index is not None else None
+    if clocks:
+        clocks.__enter__()
     for _ in range(warmup):
         step()
     h.reset_phase_times()
@@ -276,15 +310,15 @@ def time_factor(sph, h, wl, args, world, a_dev=None, steps=None, warmup=None, cl
     barrier(world)
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks = ClockSampler(clocks_index) if clocks_index is not None else None
     if clocks:
-        clocks.__enter__()
+        clocks.mark_start()
     start.record()
     for _ in range(steps):
         st = step()
     end.record()
     torch.cuda.synchronize()
     if clocks:
+        clocks.mark_end()
         clocks.__exit__()
     barrier(world)
     launches = lib.sphemu_gpu_launch_count() - launches0

@@ -48,3 +48,16 @@ def test_help_parses():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--help"], capture_output=True, text=True,
                        timeout=120)
     assert r.returncode == 0 and "--gpus" in r.stdout
+
+
+def test_clock_window():
+    c = bench.ClockSampler(0)
+    row = ["1965", "1965", "900", "0x0", "Not Active", "Not Active", "Not Active", "Active"]
+    slow = ["1200", "1965", "900", "0x0", "Active", "Not Active", "Not Active", "Not Active"]
+    c.rows = [(1.0, slow), (2.0, row), (2.1, row), (3.0, slow)]
+    c.t0, c.t1 = 1.5, 2.5
+    s = c.summary()
+    assert s["sm_mhz"] == 1965.0 and s["samples"] == 2 and s["reasons"] == ["sw_power_cap"]
+    c.t0, c.t1 = 2.3, 2.4  # shorter than the period: nearest row on each side
+    s = c.summary()
+    assert s["samples"] == 2 and "hw_slowdown" in s["reasons"]
