@@ -184,23 +184,46 @@ struct TcLayout {
 #ifndef SPH_TC_RING_SPLIT128
 #define SPH_TC_RING_SPLIT128 1
 #endif
+  // Epilogue warps: 8 (two per TMEM lane quarter), or 16 for the CTA-pair
+  // 16-bit update (four per quarter, one 64-column box each): that epilogue
+  // is latency-bound, and more warps per sub-partition hide the C box round
+  // trip better than a deeper per-warp ring, which would cost operand stages
+  // (measured at N = 98 304 dpsphp/bf16: HP update 798 TFLOP/s vs 758 with 8
+  // warps and a 3-box ring; single CTAs with 16 warps drop to 3 stages, 633).
+#ifndef SPH_TC_EPI16
+#define SPH_TC_EPI16 1
+#endif
+#ifndef SPH_TC_RING16
+#define SPH_TC_RING16 1
+#endif
+#ifndef SPH_TC_REGC
+#define SPH_TC_REGC 1  // register-staged C boxes (see the epilogue); 0 = TMA load/store ring
+#endif
+  static constexpr bool kWide = kUpd && !T::kSplit && BN == 256 && CG == 2 && SPH_TC_EPI16;
+  static constexpr int kEpi = kWide ? 16 : TC_EPI_WARPS;
+  static constexpr int kThreads = 32 * (4 + kEpi);
   static constexpr int kRing =
-      kUpd ? ((CG == 2 && !T::kSplit) ? SPH_TC_RING2
-                                      : ((T::kSplit && BN == 128) ? SPH_TC_RING_SPLIT128 : SPH_TC_RING))
+      kUpd ? ((kWide || SPH_TC_REGC) ? (SPH_TC_REGC ? 1 : SPH_TC_RING16)
+                    : ((CG == 2 && !T::kSplit) ? SPH_TC_RING2
+                                               : ((T::kSplit && BN == 128) ? SPH_TC_RING_SPLIT128 : SPH_TC_RING)))
            : 0;
-  static constexpr int kStages = (232448 - 2048 - TC_EPI_WARPS * kRing * 32 * 128) / kStage > 6
+  static constexpr int kStages = (232448 - 2048 - kEpi * kRing * 32 * 128) / kStage > 6
                                      ? 6
-                                     : (232448 - 2048 - TC_EPI_WARPS * kRing * 32 * 128) / kStage;
+                                     : (232448 - 2048 - kEpi * kRing * 32 * 128) / kStage;
   static constexpr int kCBox = 32 * 128;
-  static constexpr int kCBytes = TC_EPI_WARPS * kRing * kCBox;
+  static constexpr int kCBytes = kEpi * kRing * kCBox;
   static constexpr int kSmem = kStages * kStage + kCBytes + 1024 /*align*/ + 1024 /*barriers + schedule*/;
   static constexpr int kAcc = (512 / BN) > 4 ? 4 : (512 / BN);  // TMEM accumulators in flight (512 columns)
   static constexpr int kTmemCols = kAcc * BN;
   static_assert(kSmem <= 232448, "shared memory budget");
 };
 
+#ifndef SPH_TC_CLAIM_AHEAD
+#define SPH_TC_CLAIM_AHEAD 0
+#endif
+
 template <int BN, int OPK, int MODE, int CG>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
               const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo,
               const __grid_constant__ CUtensorMap mC, const TcArgs args) {
@@ -216,11 +239,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + Lay::kAcc;
   uint64_t* cfull = tempty + Lay::kAcc;  // [epilogue warp][kRing]
-  uint64_t* sfull = cfull + TC_EPI_WARPS * Lay::kRing;  // dynamic schedule ring: producer -> consumers
+  uint64_t* sfull = cfull + Lay::kEpi * Lay::kRing;  // dynamic schedule ring: producer -> consumers
   uint64_t* sempty = sfull + 4;                          // consumers (MMA warp + epilogue warps) -> producer
   int* sched = reinterpret_cast<int*>(sempty + 4);       // [4] claimed items (-1 = none left)
-  int* wcache = sched + 4;                               // [TC_EPI_WARPS][4] epilogue copies
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(wcache + TC_EPI_WARPS * 4);
+  int* wcache = sched + 4;                               // [kEpi][4] epilogue copies
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(wcache + Lay::kEpi * 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (*(volatile const int*)args.fail >= 0) return;  // an earlier POTRF failed (both CTAs of a pair see it)
@@ -234,12 +257,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int a = 0; a < Lay::kAcc; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], CG * TC_EPI_WARPS);  // one arrive per epilogue warp of each CTA
+      mbar_init(&tempty[a], CG * Lay::kEpi);  // one arrive per epilogue warp of each CTA
     }
-    for (int s = 0; s < TC_EPI_WARPS * Lay::kRing; ++s) mbar_init(&cfull[s], 1);
+    for (int s = 0; s < Lay::kEpi * Lay::kRing; ++s) mbar_init(&cfull[s], 1);
     for (int s = 0; s < 4; ++s) {
       mbar_init(&sfull[s], 1);
-      mbar_init(&sempty[s], 1 + TC_EPI_WARPS);
+      mbar_init(&sempty[s], 1 + Lay::kEpi);
     }
     fence_barrier_init();
   }
@@ -324,12 +347,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       };
       int64_t w = dyn ? fetch() : static_item(0);
       if (dyn) publish(0, w);
+#if SPH_TC_CLAIM_AHEAD
+      // Claims run one item further ahead: the atomic for item n + 2 is issued
+      // at the top of item n and its result consumed only after item n's
+      // loads, so its round trip never sits between two items' TMA issues.
+      int64_t w_ahead = dyn ? (w >= 0 ? fetch() : -1) : -1;
+      if (dyn) publish(1, w_ahead);
+#endif
       int2 ij_cur = w >= 0 ? args.list[w / args.sub_per] : make_int2(0, 0);
       int crow_cur = (MODE == MODE_UPDATE && w >= 0) ? args.crow[w / args.sub_per] : 0;
       prefetch_c(w >= 0 ? w : items, ij_cur, crow_cur);
       for (int64_t n = 0; w >= 0; ++n) {
+#if SPH_TC_CLAIM_AHEAD
+        const int64_t w_next = dyn ? w_ahead : static_item(n + 1);
+        const int64_t claim = (dyn && w_next >= 0) ? atomicAdd(args.counter, 1) : -1;
+#else
         const int64_t w_next = dyn ? fetch() : static_item(n + 1);
         if (dyn) publish(n + 1, w_next);
+#endif
         const int sub = static_cast<int>(w % args.sub_per);
         const int i = ij_cur.x, j = ij_cur.y;
         const int m0 = (sub / args.sub_n) * (TC_BM * CG) + static_cast<int>(rank) * TC_BM;
@@ -373,6 +408,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             phase ^= 1;
           }
         }
+#if SPH_TC_CLAIM_AHEAD
+        if (dyn && w_next >= 0) {
+          w_ahead = claim < items ? claim : -1;
+          publish(n + 2, w_ahead);
+        }
+#endif
         ij_cur = ij_nxt;
         crow_cur = crow_nxt;
         w = w_next;
@@ -458,7 +499,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp >= 4) {
     // ===== epilogue: TMEM -> registers -> tile storage (+ panel mirrors) =====
     const int q = warp & 3;         // TMEM lane quarter (hardware: warp % 4)
-    const int grp = (warp - 4) >> 2;  // two warps per quarter split the columns
+    constexpr int NG = Lay::kEpi / 4;  // warps per quarter, splitting the columns
+    const int grp = (warp - 4) >> 2;
     const int row_in = q * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -467,7 +509,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // Update-mode C staging (see below): box geometry and the load ring.
     constexpr int kEsz = T::kSplit ? 4 : 2;        // storage bytes of the C class (SP fp32, HP 16-bit)
     constexpr int kBoxCols = 128 / kEsz;           // columns per 128-byte box row
-    constexpr int kNBox = BN / kBoxCols / 2;       // boxes per warp per work item (box grp + 2 bx)
+    constexpr int kNBox = BN / kBoxCols / NG;      // boxes per warp per work item (box grp + NG bx)
+    static_assert(MODE != MODE_UPDATE || kNBox * NG * kBoxCols == BN, "boxes split evenly over the warps");
     constexpr int R = Lay::kRing > 0 ? Lay::kRing : 1;
     uint8_t* cring = cbuf + (warp - 4) * R * Lay::kCBox;
     uint64_t* cf = cfull + (warp - 4) * R;
@@ -488,7 +531,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     auto issue_c = [&]() {  // lane 0: TMA-load the next C box into its ring slot
       const int64_t wi = item_lane0(gissue / kNBox);
       if (wi < 0) return;
-      const int bx = grp + 2 * static_cast<int>(gissue % kNBox);
+      const int bx = grp + NG * static_cast<int>(gissue % kNBox);
       int ti, tj, tm, tn;
       decode(wi, ti, tj, tm, tn);
       const int slot = static_cast<int>(gissue % R);
@@ -496,8 +539,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tma_load_2d(&mC, &cf[slot], cring + slot * Lay::kCBox, tn + bx * kBoxCols, c_row(wi) + tm + q * 32);
       ++gissue;
     };
+#if SPH_TC_REGC
+    // Register-staged C (default): each box is read from L2 by coalesced
+    // 16-byte loads (4 rows x 128 B per instruction) one box ahead, so the
+    // loads of the next box fly while this one is computed and across the
+    // accumulator wait; the warp's 4 KB smem slot only transposes the box
+    // between the coalesced order and the TMEM row-per-lane order, and the
+    // result leaves by coalesced stores that nobody waits for.
+    uint4 cpre[8];
+    char* cpre_ptr = nullptr;  // this lane's first 16 B of the prefetched box (nullptr = none)
+    const int64_t c_pitch = static_cast<int64_t>(args.ts.b) * (T::kSplit ? 4 : 2);
+    auto load_box = [&](int64_t seq) {
+      int64_t wi = -1;
+      if (lane == 0) wi = item_lane0(seq / kNBox);
+      wi = __shfl_sync(0xffffffffu, static_cast<int>(wi), 0);
+      if (wi < 0) {
+        cpre_ptr = nullptr;
+        return;
+      }
+      const int bx = grp + NG * static_cast<int>(seq % kNBox);
+      int ti, tj, tm, tn;
+      decode(wi, ti, tj, tm, tn);
+      const int64_t row0 = static_cast<int64_t>(c_row(wi)) + tm + q * 32 + (lane >> 3);
+      cpre_ptr = args.ts.base + row0 * c_pitch + static_cast<int64_t>(tn + bx * kBoxCols) * (T::kSplit ? 4 : 2) +
+                 (lane & 7) * 16;
+#pragma unroll
+      for (int s8 = 0; s8 < 8; ++s8)
+        cpre[s8] = args.dbg == 5 ? make_uint4(0, 0, 0, 0)
+                                 : __ldcg(reinterpret_cast<const uint4*>(cpre_ptr + s8 * 4 * c_pitch));
+    };
+    if (MODE == MODE_UPDATE) load_box(0);
+#else
     if (MODE == MODE_UPDATE && lane == 0 && (args.dbg == 0 || args.dbg >= 3) && args.dbg != 5)
       for (int s = 0; s < R; ++s) issue_c();
+#endif
     for (int64_t n = 0;; ++n) {
       if (lane == 0) item_lane0(n);
       __syncwarp();
@@ -525,14 +600,40 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_fence_after();
 #pragma unroll 1
         for (int bl = 0; bl < ((args.dbg == 1 || args.dbg == 2) ? 0 : kNBox); ++bl, ++gbox) {
-          const int bx = grp + 2 * bl;
+          const int bx = grp + NG * bl;
+#if SPH_TC_REGC
+          (void)bx;
+          const int slot = 0;
+          char* const cur_ptr = cpre_ptr;
+          // the first 32 accumulator columns come from TMEM while the box is transposed
+          uint32_t v_first[32];
+          tmem_ld32_nowait(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + bx * kBoxCols, v_first);
+          {
+            const uint32_t sb = smem_addr(cring);
+#pragma unroll
+            for (int s8 = 0; s8 < 8; ++s8) {
+              const int r = 4 * s8 + (lane >> 3);
+              sts128(sb + r * 128 + (((lane & 7) ^ (r & 7)) << 4), cpre[s8]);
+            }
+          }
+          __syncwarp();
+          load_box(gbox + 1);
+#else
           const int slot = static_cast<int>(gbox % R);
           if (args.dbg != 5) mbar_wait(&cf[slot], static_cast<uint32_t>((gbox / R) & 1));
+#endif
           const uint32_t row_s = smem_addr(cring + slot * Lay::kCBox) + lane * 128;
 #pragma unroll
           for (int h = 0; h < (args.dbg == 3 ? 0 : kBoxCols / 32); ++h) {
             uint32_t v[32];
-            tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + bx * kBoxCols + h * 32, v);
+#if SPH_TC_REGC
+            if (h == 0) {
+              tmem_wait_ld();
+#pragma unroll
+              for (int t = 0; t < 32; ++t) v[t] = v_first[t];
+            } else
+#endif
+              tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + bx * kBoxCols + h * 32, v);
             if constexpr (OPK == OP_F16X3) {
               // operands were scaled by 2^e_row: undo exactly (powers of two)
               const int er = args.rowexp[min(i * args.lb + m0 + row_in, args.ts.n - 1)];
@@ -599,6 +700,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               }
             }
           }
+#if SPH_TC_REGC
+          __syncwarp();
+          {
+            const uint32_t sb = smem_addr(cring);
+#pragma unroll
+            for (int s8 = 0; s8 < 8; ++s8) {
+              const int r = 4 * s8 + (lane >> 3);
+              const uint4 v = lds128(sb + r * 128 + (((lane & 7) ^ (r & 7)) << 4));
+              if (args.dbg != 4) __stcg(reinterpret_cast<uint4*>(cur_ptr + s8 * 4 * c_pitch), v);
+            }
+          }
+          __syncwarp();  // the slot is free for the next box
+          continue;
+#endif
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -622,7 +737,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int64_t prow = (int64_t)(i - args.k - 1) * b + r;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      for (int c0 = 32 * grp; c0 < BN; c0 += 64) {
+      for (int c0 = 32 * grp; c0 < BN; c0 += 32 * NG) {
         uint32_t v[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c0, v);
         const int64_t e0 = (int64_t)r * b + n0 + c0;
@@ -884,11 +999,11 @@ void launch_tc(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorM
   const int cap = (max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms()) / CG;
   const int grid = CG * static_cast<int>(std::min<int64_t>(args.items, std::max(1, cap)));
   if constexpr (CG == 1) {
-    kern<<<grid, TC_THREADS, Lay::kSmem, s>>>(a_hi, a_lo, b_hi, b_lo, c_map, args);
+    kern<<<grid, Lay::kThreads, Lay::kSmem, s>>>(a_hi, a_lo, b_hi, b_lo, c_map, args);
   } else {
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(grid);
-    lc.blockDim = dim3(TC_THREADS);
+    lc.blockDim = dim3(Lay::kThreads);
     lc.dynamicSmemBytes = Lay::kSmem;
     lc.stream = s;
     cudaLaunchAttribute at[1];
@@ -1002,14 +1117,14 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
     return e ? std::atoi(e) : 0;
   }();
   a.opt = opt;
-  // CTA pairs (cta_group::2, M = 256) for the 256-wide kinds with
-  // SPHEMU_TC_CG=2. Bitwise identical results; measured slower than single
-  // CTAs at b = 512 (the update is bound by the C-tile epilogue, which pairs
-  // do not shrink, and the pair's C ring costs mainloop stages), so off by
-  // default.
+  // CTA pairs (cta_group::2, M = 256) for the 256-wide kinds: bitwise
+  // identical results. Default for the HP class, where the pair's smaller
+  // operand stages leave room for 16 epilogue warps (update 820 vs 767
+  // TFLOP/s single-CTA at N = 98 304 dpsphp/bf16); the SP class (fp16x3,
+  // 96 KB stages) stays on single CTAs (SPHEMU_TC_CG_SP=2: 247 vs 285).
   static const int cg_env = [] {
     const char* e = std::getenv("SPHEMU_TC_CG");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 2;
   }();
   static const int cg_sp = [] {
     const char* e = std::getenv("SPHEMU_TC_CG_SP");
