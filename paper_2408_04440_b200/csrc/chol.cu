@@ -915,8 +915,8 @@ struct Chol {
       PanelFormats& pf = panel_[set];
       const bool tensor = cfg.compute == SPHEMU_COMPUTE_TENSOR;
       k_panel_import<<<dim3(gx, static_cast<unsigned>(ilist_cnt[k])), 256, 0, s>>>(
-          store(), k, ilists.get() + ilist_off[k], ioffs.get() + ilist_off[k], xbuf.get(), p64_[set].get(), tensor ? pf.p_hi.get() : nullptr,
-          tensor ? pf.p_lo.get() : nullptr, tensor ? pf.p16.get() : nullptr,
+          store(), k, ilists.get() + ilist_off[k], ioffs.get() + ilist_off[k], xbuf.get(), p64_[set].get(), tensor ? pf.tf32_hi() : nullptr,
+          tensor ? pf.tf32_lo() : nullptr, tensor ? pf.half16() : nullptr,
           (tensor && pf.f16x3) ? pf.h_hi.get() : nullptr, (tensor && pf.f16x3) ? pf.h_lo.get() : nullptr,
           rowexp.get(), cfg.hp_format, fail.get());
       SPH_LAUNCH_CHECK();

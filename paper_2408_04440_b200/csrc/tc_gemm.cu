@@ -72,8 +72,10 @@ void PanelFormats::set_arena(const void* base, int64_t bytes, int b_) {
 
 void PanelFormats::alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int hp_format_, bool f16x3_,
                          const int* rowexp_) {
-  (void)pmap;
   f16x3 = f16x3_;
+  need_tf32 = !f16x3_;
+  need_p16 = false;
+  for (uint8_t p : pmap) need_p16 |= (p == SPHEMU_PREC_HP);  // pmap holds SPHEMU_PREC_* per tile
   rowexp = rowexp_;
   nt = nt_;
   b = b_;
@@ -789,16 +791,18 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
             double2* pd = reinterpret_cast<double2*>(args.p64 + pe);
 #pragma unroll
             for (int u = 0; u < 4; ++u) pd[u] = make_double2(qv[2 * u], qv[2 * u + 1]);
-            float hi[8], lo[8];
+            if (args.p_hi) {
+              float hi[8], lo[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) tf32_split((float)qv[u], hi[u], lo[u]);
-            float4* ph = reinterpret_cast<float4*>(args.p_hi + pe);
-            float4* pl = reinterpret_cast<float4*>(args.p_lo + pe);
-            ph[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
-            ph[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
-            pl[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
-            pl[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
-            *reinterpret_cast<uint4*>(args.p16 + pe) = *reinterpret_cast<const uint4*>(h16);
+              for (int u = 0; u < 8; ++u) tf32_split((float)qv[u], hi[u], lo[u]);
+              float4* ph = reinterpret_cast<float4*>(args.p_hi + pe);
+              float4* pl = reinterpret_cast<float4*>(args.p_lo + pe);
+              ph[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+              ph[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
+              pl[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+              pl[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
+            }
+            if (args.p16) *reinterpret_cast<uint4*>(args.p16 + pe) = *reinterpret_cast<const uint4*>(h16);
             if (args.h_hi) {
               const int er = args.rowexp[min(i * args.lb + r, args.ts.n - 1)];
               uint16_t hh[8], hl[8];
@@ -944,13 +948,17 @@ __global__ void k_panel_finish_dp(TileStore ts, int k, const int2* list, const d
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += (int64_t)gridDim.x * blockDim.x) {
     const double x = p64[base + e];
     tp[e] = x;
-    float hi, lo;
-    tf32_split(__double2float_rn(x), hi, lo);
-    p_hi[base + e] = hi;
-    p_lo[base + e] = lo;
-    unsigned dummy = 0;
-    p16[base + e] = hp_format == SPHEMU_HP_BF16 ? __bfloat16_as_ushort(to_bf16_sat(x, dummy))
-                                                : __half_as_ushort(to_half_sat(x, dummy));
+    if (p_hi) {
+      float hi, lo;
+      tf32_split(__double2float_rn(x), hi, lo);
+      p_hi[base + e] = hi;
+      p_lo[base + e] = lo;
+    }
+    if (p16) {
+      unsigned dummy = 0;
+      p16[base + e] = hp_format == SPHEMU_HP_BF16 ? __bfloat16_as_ushort(to_bf16_sat(x, dummy))
+                                                  : __half_as_ushort(to_half_sat(x, dummy));
+    }
     if (h_hi) {
       const int r = (int)(e / b);
       f16_split(x, rowexp[min(i * ts.lb + r, ts.n - 1)], h_hi[base + e], h_lo[base + e]);
@@ -1037,7 +1045,7 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
         ts, k, d_dp, linv, p64, fail, sat);
     SPH_LAUNCH_CHECK();
     k_panel_finish_dp<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(n_dp)), 256, 0, s>>>(
-        ts, k, d_dp, p64, pf.p_hi.get(), pf.p_lo.get(), pf.p16.get(), pf.hp_format, fail,
+        ts, k, d_dp, p64, pf.tf32_hi(), pf.tf32_lo(), pf.half16(), pf.hp_format, fail,
         pf.f16x3 ? pf.h_hi.get() : nullptr, pf.h_lo.get(), pf.rowexp);
     SPH_LAUNCH_CHECK();
   }
@@ -1070,9 +1078,9 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
     a.sub_per = (b / TC_BM) * a.sub_n;
     a.items = n_lo * a.sub_per;
     a.p64 = p64;
-    a.p_hi = pf.p_hi.get();
-    a.p_lo = pf.p_lo.get();
-    a.p16 = pf.p16.get();
+    a.p_hi = pf.tf32_hi();
+    a.p_lo = pf.tf32_lo();
+    a.p16 = pf.half16();
     a.h_hi = pf.f16x3 ? pf.h_hi.get() : nullptr;
     a.h_lo = pf.h_lo.get();
     a.rowexp = pf.rowexp;

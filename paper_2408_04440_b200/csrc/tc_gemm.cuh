@@ -39,6 +39,12 @@ struct PanelFormats {
   CUtensorMap m_in16hi_a, m_in16lo_a, m_l16hi_b, m_l16lo_b;
   // FP16x3 path for the SP class: x * 2^e_row = hi + lo, both fp16.
   bool f16x3 = false;
+  // Which mirrors have a consumer: the tf32 split only feeds the 3xTF32 SP
+  // update, the 16-bit copy only the HP update; the panel skips the others.
+  bool need_tf32 = true, need_p16 = true;
+  float* tf32_hi() { return need_tf32 ? p_hi.get() : nullptr; }
+  float* tf32_lo() { return need_tf32 ? p_lo.get() : nullptr; }
+  uint16_t* half16() { return need_p16 ? p16.get() : nullptr; }
   const int* rowexp = nullptr;
   DevBuf<uint16_t> h_hi, h_lo;
   CUtensorMap m_hhi_a, m_hlo_a, m_hhi_b, m_hlo_b;
