@@ -346,10 +346,10 @@ def roofline(h, wl, args, phases, steps, ms):
         sp_kernel = "k_tc_gemm<128, TF32x3, UPDATE> (SP-class trailing update)"
     if wl["hp"] == "bf16":
         p_hp, hp_src = peaks.get("bf16_tflops", 1692.6), "MEASURED_PEAKS.json bf16_tflops (burst)"
-        hp_kernel = "k_tc_gemm<128, BF16, UPDATE> (HP-class trailing update, BF16 storage)"
+        hp_kernel = "k_tc_gemm<128, BF16, UPDATE, 2> (HP-class trailing update, CTA pairs, BF16 storage)"
     else:
         p_hp, hp_src = own.get("fp16_tflops", 1546.6), "cuBLAS FP16 GEMM measured on this pool (profiles/peaks_r01.json)"
-        hp_kernel = "k_tc_gemm<128, F16, UPDATE> (HP-class trailing update, FP16 storage)"
+        hp_kernel = "k_tc_gemm<128, F16, UPDATE, 2> (HP-class trailing update, CTA pairs, FP16 storage)"
     cuf = h.class_update_flops()
     bn = 256 if wl["tile"] % 256 == 0 else 128
     sp_kernel = sp_kernel.replace("<128,", f"<{bn},")
@@ -370,8 +370,16 @@ def roofline(h, wl, args, phases, steps, ms):
                    "algorithmic_bytes_per_launch": tj["c_bytes"] + tj["panel_operand_bytes"],
                    "launch": f"{tj['workload']}: {tj['sub_tiles']} sub-tiles of 128x256, K=512",
                    "source": "profiles/r01_traffic.json (ncu --set full, one launch)"}
+    # The bulk update runs on SMs - reserve CTAs (the reserve serves the
+    # POTRF/panel chain stream concurrently); frac is against the whole GPU.
+    import torch
+    n_sm = (torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            if torch.cuda.is_available() else 148)
+    reserve = 32 if max(1, args.world) < 4 else 48
     dom = {"kernel": kern, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
            "frac": ach / peak if ach else None, "peak_source": src, "traffic": traffic,
+           "sms": {"bulk_ctas": n_sm - reserve, "device_sms": n_sm,
+                   "frac_of_bulk_sms_peak": ach / (peak * (n_sm - reserve) / n_sm) if ach else None},
            "per_launch_basis": f"{cuf[dom_c]/1e12:.3f} TFLOP of {dom_c.upper()}-class update per step on this rank "
                                f"/ summed launch time {t:.2f} ms (CUDA events on the launching stream)"}
     fl = h.flops()
