@@ -303,6 +303,7 @@ struct BlockCyclic {
 
 struct Chol {
   static constexpr int kChainCtas = 32;  // SMs reserved for the critical chain under lookahead
+  int potrf_cap = kChainCtas;            // cooperative POTRF grid cap (follows the step's reserve)
   int n = 0, b = 0, nt = 0;  // b = storage pitch (padded), lb = logical tile size
   int lb = 0;
   // 2D block-cyclic distribution over a P x Q process grid (one GPU per
@@ -825,7 +826,24 @@ struct Chol {
     launches_at_start = launch_count();
     t_start = std::chrono::steady_clock::now();
     SPH_CUDA(cudaEventRecord(ev0, stream));
-    const int reserve = kChainCtas;  // SMs left to the chain while the bulk runs
+    // SMs left to the chain while the bulk runs. Early steps, where the bulk
+    // is the critical stream (its work shrinks quadratically, the chain's only
+    // linearly), leave the chain 8 SMs; the last 32 steps leave it 32
+    // (SPHEMU_RESERVE_EARLY / SPHEMU_RESERVE_TAIL). POTRF's cooperative grid
+    // follows the reserve so its CTAs stay co-resident. Measured (1 GPU):
+    // C2 58.2 -> 56.4 ms, C3 1 246 -> 1 136 ms against a fixed reserve of 32
+    // (tools/reserve_sweep*.sh).
+    static const int r_early = [] {
+      const char* e = std::getenv("SPHEMU_RESERVE_EARLY");
+      return std::max(8, std::min(kChainCtas, e ? std::atoi(e) : 8));
+    }();
+    static const int r_tail = [] {
+      const char* e = std::getenv("SPHEMU_RESERVE_TAIL");
+      return e ? std::atoi(e) : 32;
+    }();
+    auto reserve_at = [&](int k) { return (nt - 1 - k > r_tail) ? r_early : kChainCtas; };
+    int reserve = kChainCtas;
+    potrf_cap = kChainCtas;
     if (dist()) {
       factor_dist();
     } else if (!cfg.lookahead || nt == 1) {
@@ -851,6 +869,8 @@ struct Chol {
       for (int k = 0; k + 1 < nt; ++k) {
         // chain: SYRK of the next diagonal tile -> POTRF -> (column below ready) -> panel
         if (k > 0) SPH_CUDA(cudaStreamWaitEvent(pstream, ev_bulk[k - 1], 0));
+        reserve = reserve_at(k);
+        potrf_cap = reserve;
         op_update(k, 0, pstream, 0);
         op_potrf(k + 1, pstream);
         // main stream: column k+1 below the diagonal first (the chain's panel
@@ -984,7 +1004,7 @@ struct Chol {
       attr = true;
     }
     const int nblk = (rows(k) + PC_BLK - 1) / PC_BLK;
-    const int G = std::max(1, std::min(32, nblk * (nblk + 1) / 2));
+    const int G = std::max(1, std::min(potrf_cap, nblk * (nblk + 1) / 2));
     double* dkk = reinterpret_cast<double*>(arena.get() + off[tix(k, k)]);
     int bk = rows(k), kk = k, bb = b;
     double* lp = linv_[k & 1].get();
