@@ -969,7 +969,13 @@ struct Chol {
       // shrinks with the grid (SPHEMU_DIST_RESERVE overrides).
       // measured C3: 2x1 grid 32 -> 749 ms, 48 -> 816; 2x2 grid 32 -> 501, 48 -> 488, 64 -> 515
       const char* env_reserve = std::getenv("SPHEMU_DIST_RESERVE");
-      const int reserve = env_reserve ? std::atoi(env_reserve) : (P * Q >= 4 ? 48 : kChainCtas);
+      const int reserve_late = env_reserve ? std::atoi(env_reserve) : (P * Q >= 4 ? 48 : kChainCtas);
+      // early steps may leave the chain fewer SMs, as on one GPU
+      const char* env_early = std::getenv("SPHEMU_DIST_RESERVE_EARLY");
+      const char* env_tail = std::getenv("SPHEMU_DIST_RESERVE_TAIL");
+      const int reserve_early = env_early ? std::max(8, std::atoi(env_early)) : reserve_late;
+      const int tail = env_tail ? std::atoi(env_tail) : 32;
+      int reserve = reserve_late;
       SPH_CUDA(cudaEventRecord(ev_start_p, stream));
       SPH_CUDA(cudaStreamWaitEvent(pstream, ev_start_p, 0));
       op_potrf_dist(0, pstream);
@@ -977,6 +983,8 @@ struct Chol {
       SPH_CUDA(cudaEventRecord(ev_panel[0], pstream));
       for (int k = 0; k + 1 < nt; ++k) {
         if (k > 0) SPH_CUDA(cudaStreamWaitEvent(pstream, ev_bulk[k - 1], 0));
+        reserve = (nt - 1 - k > tail) ? reserve_early : reserve_late;
+        potrf_cap = std::min(kChainCtas, reserve);
         op_update(k, 0, pstream, 0);
         op_potrf_dist(k + 1, pstream);
         SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k], 0));
