@@ -1551,7 +1551,8 @@ int sphemu_gpu_tiled_cholesky_dense(const double* a, int where_a, int n, const s
   int g = guard([&] {
     std::lock_guard<std::mutex> lk(g_dense_mu);
     Chol& c = dense_handle(n, *cfg);
-    c.load_dense(a, where_a, n);
+    // The host zero-fill of the output's upper triangle starts first, so it
+    // overlaps the input's H2D instead of competing with the factor's D2H.
     const bool stream_out = where_factor == SPHEMU_HOST;
     if (stream_out) c.begin_host_out(factor, n);
     struct Finish {  // joins the host zero-fill threads on every exit path
@@ -1563,6 +1564,7 @@ int sphemu_gpu_tiled_cholesky_dense(const double* a, int where_a, int n, const s
         }
       }
     } finish{c};
+    c.load_dense(a, where_a, n);
     c.factor();
     const int f = c.wait(stats);
     if (failed_tile) *failed_tile = f;
