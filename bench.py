@@ -339,7 +339,7 @@ def roofline(h, wl, args, phases, steps, ms):
     if args.sp_compute == "fp16x3":
         p_sp = own.get("fp16_tflops", 1546.6) / 3
         sp_src = "cuBLAS FP16 GEMM measured on this pool / 3 (3 kind::f16 MMAs per product; profiles/peaks_r01.json)"
-        sp_kernel = "k_tc_gemm<128, F16x3, UPDATE> (SP-class trailing update, row-scaled fp16 hi+lo)"
+        sp_kernel = "k_tc_gemm<128, F16x3, UPDATE, 1> (SP-class trailing update, row-scaled fp16 hi+lo)"
     else:
         p_sp = own.get("tf32x3_effective_tflops", 244.7)
         sp_src = "cuBLAS TF32 GEMM measured on this pool / 3 (profiles/peaks_r01.json)"
@@ -375,11 +375,13 @@ def roofline(h, wl, args, phases, steps, ms):
     import torch
     n_sm = (torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
             if torch.cuda.is_available() else 148)
-    reserve = 32 if max(1, args.world) < 4 else 48
+    # one GPU: 8 SMs reserved for the chain except in the last 32 steps (32); multi-GPU: 32 (2 GPUs) or 48
+    world = max(1, args.world)
+    bulk = [n_sm - 8, n_sm - 32] if world == 1 else [n_sm - (32 if world < 4 else 48)]
     dom = {"kernel": kern, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
            "frac": ach / peak if ach else None, "peak_source": src, "traffic": traffic,
-           "sms": {"bulk_ctas": n_sm - reserve, "device_sms": n_sm,
-                   "frac_of_bulk_sms_peak": ach / (peak * (n_sm - reserve) / n_sm) if ach else None},
+           "sms": {"bulk_ctas": bulk, "device_sms": n_sm,
+                   "note": "the bulk update runs on these CTAs while the POTRF/panel chain holds the rest"},
            "per_launch_basis": f"{cuf[dom_c]/1e12:.3f} TFLOP of {dom_c.upper()}-class update per step on this rank "
                                f"/ summed launch time {t:.2f} ms (CUDA events on the launching stream)"}
     fl = h.flops()
