@@ -1,8 +1,10 @@
 // sphemu/wigner.hpp — drop-in for proj/include/sphemu/wigner.hpp:13-49. The
 // device plan (sphemu_gpu_sht_create) runs the Wigner recurrence itself, so
-// this object only carries the band limit and the memory cap the plan is
-// built under; the cap check and its message are the reference's
-// (wigner.cpp:50-64).
+// this object carries the band limit and the memory cap the plan is built
+// under (cap check and message as wigner.cpp:50-64); d_half_pi
+// (wigner.cpp:136-150) reads the device-built tables through
+// sphemu_gpu_wigner_d_half_pi, one table build per call (a lookup for tests
+// and diagnostics, not a hot path).
 #pragma once
 
 #include <cstddef>
@@ -11,11 +13,25 @@
 #include <stdexcept>
 #include <string>
 
+#include "detail_status.hpp"
+
 namespace sphemu {
 
 class WignerTables {
  public:
   int band_limit() const { return band_limit_; }
+  double d_half_pi(int l, int m2, int m) const {
+    if (l < 0 || l >= band_limit_) throw std::out_of_range("degree outside the table");
+    double v = 0.0;
+    detail::check(sphemu_gpu_wigner_d_half_pi(band_limit_, cap_, 1, &l, &m2, &m, &v, nullptr));
+    return v;
+  }
+  int renorm_warnings() const {
+    int r = 0, l = 0;
+    double v = 0.0;
+    detail::check(sphemu_gpu_wigner_d_half_pi(band_limit_, cap_, 1, &l, &l, &l, &v, &r));
+    return r;
+  }
   std::size_t memory_cap_bytes() const { return cap_; }
   // d chains + q rows + offsets, as wigner.cpp:54-60 sizes them.
   static std::size_t estimated_bytes(int band_limit) {

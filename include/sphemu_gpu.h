@@ -202,6 +202,17 @@ int sphemu_gpu_synth_bandlimited(const double* coeffs, int where_in, int64_t n, 
 void* sphemu_gpu_sht_stream(sphemu_sht_t p);
 /* Seconds spent building the plan (Wigner recurrence + operator build). */
 double sphemu_gpu_sht_plan_seconds(sphemu_sht_t p);
+/* WignerTables::d_half_pi (wigner.cpp:136-150) over the tables of
+ * build_wigner_tables(band_limit) (wigner.cpp:49-134), built on the device:
+ * out[i] = d^{l[i]}_{m2[i], m[i]}(pi/2), with the reference's sign rules for
+ * negative orders and 0 for |m2| or |m| > l. All arrays host, n entries.
+ * SPHEMU_ERR_INVALID_ARG for a degree outside [0, band_limit) or a cap
+ * violation (wigner_cap_bytes = 0: the 2 GiB default of wigner.hpp:48-49).
+ * renorm_warnings (may be NULL) receives the guard count
+ * (WignerTables::renorm_warnings). The Python wigner_d_half_pi(l, m2, m) of
+ * bindings/module.cpp:201-207 calls this with band_limit = l + 1. */
+int sphemu_gpu_wigner_d_half_pi(int band_limit, size_t wigner_cap_bytes, int64_t n, const int* l, const int* m2,
+                                const int* m, double* out, int* renorm_warnings);
 
 /* ======================================================================
  * Emulation generator (replaces stochastic.hpp:84-86 emulate)

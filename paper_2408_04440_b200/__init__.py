@@ -21,10 +21,11 @@ from ._sphemu import (  # noqa: F401
     resolution_summary,
     synth_bandlimited,
     tiled_cholesky,
+    wigner_d_half_pi,
 )
 
 __all__ = [
     "Cholesky", "NotPositiveDefiniteError", "ShtPlan", "__version__", "assign_precisions", "emulate",
     "estimate_innovation_covariance", "forward_sht", "inverse_sht", "make_spd_matrix", "nccl_unique_id", "max_band_limit", "resolution_summary",
-    "synth_bandlimited", "tiled_cholesky",
+    "synth_bandlimited", "tiled_cholesky", "wigner_d_half_pi",
 ]

@@ -111,6 +111,8 @@ def lib():
         L.sphemu_gpu_sht_plan_seconds.argtypes = [vp]
         L.sphemu_gpu_sht_plan_seconds.restype = C.c_double
         L.sphemu_gpu_nccl_unique_id.argtypes = [vp]
+        L.sphemu_gpu_wigner_d_half_pi.argtypes = [C.c_int, C.c_size_t, i64, vp, vp, vp, vp,
+                                                  C.POINTER(C.c_int)]
         L.sphemu_gpu_chol_create_dist.argtypes = [C.c_int, C.POINTER(CholConfig), C.c_int, C.c_int, C.c_int, vp,
                                                   C.POINTER(vp)]
         L.sphemu_gpu_chol_set_profiling.argtypes = [vp, C.c_int]
@@ -465,6 +467,22 @@ def synth_bandlimited(coeffs, n_theta, n_phi):
     _check(lib().sphemu_gpu_synth_bandlimited(_ptr(c2), HOST, c2.shape[0], big_l, n_theta, n_phi,
                                               _ptr(out), HOST))
     return out[0] if single else out
+
+
+def wigner_d_half_pi(l, m2, m):
+    """wigner_d_half_pi(l, m2, m) (bindings/module.cpp:201-207): d^l_{m2,m}(pi/2)
+    from the tables of build_wigner_tables(l + 1) (wigner.cpp:49-150), built on
+    the device. Scalars give a float; equal-shape integer arrays give an array
+    (one table build, band limit max(l) + 1)."""
+    ls, m2s, ms = (np.ascontiguousarray(np.asarray(x), dtype=np.int32) for x in (l, m2, m))
+    if not (ls.shape == m2s.shape == ms.shape):
+        raise ValueError("l, m2 and m must have the same shape")
+    if ls.size == 0:
+        return np.empty(ls.shape, dtype=np.float64)
+    out = np.empty(ls.shape, dtype=np.float64)
+    _check(lib().sphemu_gpu_wigner_d_half_pi(int(ls.max()) + 1, 0, ls.size, _ptr(ls), _ptr(m2s), _ptr(ms),
+                                             _ptr(out), None))
+    return float(out) if out.ndim == 0 else out
 
 
 def resolution_summary(band_limit):

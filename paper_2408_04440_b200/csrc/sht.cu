@@ -32,20 +32,17 @@
 namespace sphemu_gpu {
 
 // ===========================================================================
-// Host: Wigner d(pi/2) tables (wigner.cpp:18-134). Product code: the plan
-// build needs them; they are restated here, not linked from the oracle.
+// Wigner d(pi/2) tables (wigner.cpp:49-134), built on the device.
+// Layout as the reference: chain (a, b) = (m2, m) >= 0 holds l = max(a,b)..L-1
+// contiguously, starting at off[a * L + b]. One thread per chain runs the
+// degree recurrence; one thread per (l, b) runs the renormalization guard
+// (every guard column touches its own entries, so the columns are
+// independent). The recurrence and the guard use explicitly rounded
+// operations in the reference's evaluation order (no FMA contraction), so
+// they match the host arithmetic of wigner.cpp; the chain seed
+// 2^-l0 sqrt(prod (l0+lo+k)/k) (wigner.cpp:18-28, long double there) is a
+// double-double product with power-of-two rescaling.
 // ===========================================================================
-struct WignerHost {
-  int L = 0;
-  int renorm = 0;
-  std::vector<double> d;
-  std::vector<int64_t> off;  // (a, b) -> start of the chain l = max(a,b)..L-1
-  double get(int l, int m2, int m) const {  // m2, m >= 0, l >= max
-    return d[off[(int64_t)m2 * L + m] + l - std::max(m2, m)];
-  }
-};
-
-static int parity_sign(int e) { return (e & 1) ? -1 : 1; }
 
 static size_t wigner_bytes(int L) {
   size_t d_entries = 0;
@@ -55,66 +52,143 @@ static size_t wigner_bytes(int L) {
   return (d_entries + q_entries) * sizeof(double) + (static_cast<size_t>(L) * L + 1) * sizeof(size_t);
 }
 
-static WignerHost build_wigner(int L, size_t cap) {
+__device__ __forceinline__ void dd_mul(double& h, double& lo, double bh, double bl) {
+  const double p = h * bh;
+  double e = fma(h, bh, -p);
+  e += h * bl + lo * bh;
+  const double s = p + e;
+  lo = e - (s - p);
+  h = s;
+}
+
+__device__ double wigner_seed(int a, int b) {
+  const int l0 = max(a, b), lo = min(a, b);
+  double h = 1.0, hl = 0.0;
+  int e2 = 0;  // product = (h + hl) * 2^e2, e2 even
+  for (int k = 1; k <= l0 - lo; ++k) {
+    const double num = (double)(l0 + lo + k), den = (double)k;
+    const double q = num / den;
+    const double r = fma(-q, den, num) / den;
+    dd_mul(h, hl, q, r);
+    if (h > 0x1p600) { h *= 0x1p-600; hl *= 0x1p-600; e2 += 600; }
+  }
+  const double s = sqrt(h);
+  const double t = (fma(-s, s, h) + hl) / (2.0 * s);
+  const double v = ldexp(s + t, e2 / 2 - l0);
+  return ((l0 - b) & 1) ? -v : v;
+}
+
+__global__ void k_wigner_chains(int L, const int64_t* __restrict__ off, double* __restrict__ d) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)L * L) return;
+  const int a = (int)(t / L), b = (int)(t % L);
+  const int l0 = max(a, b);
+  double* chain = d + off[t];
+  const double seed = wigner_seed(a, b);
+  chain[0] = seed;
+  if (l0 + 1 >= L) return;
+  const double da = (double)a, db = (double)b;
+  double prev = 0.0, cur = seed;
+  double c0 = __dmul_rn(__dmul_rn(__dmul_rn(sqrt((double)(l0 + a)), sqrt((double)(l0 - a))), sqrt((double)(l0 + b))),
+                        sqrt((double)(l0 - b)));
+  for (int l = l0; l + 1 < L; ++l) {
+    double next;
+    const double c1 = __dmul_rn(__dmul_rn(__dmul_rn(sqrt((double)(l + 1 + a)), sqrt((double)(l + 1 - a))),
+                                          sqrt((double)(l + 1 + b))),
+                                sqrt((double)(l + 1 - b)));
+    if (l == 0) {
+      next = 0.0;
+    } else {
+      const double dl = (double)l;
+      const double t1 = __dmul_rn(__dmul_rn(__dmul_rn(-(2.0 * dl + 1.0), da), db), cur);
+      const double t2 = __dmul_rn(__dmul_rn(dl + 1.0, c0), prev);
+      next = __ddiv_rn(__dsub_rn(t1, t2), __dmul_rn(dl, c1));
+    }
+    chain[l + 1 - l0] = next;
+    prev = cur;
+    cur = next;
+    c0 = c1;
+  }
+}
+
+__global__ void k_wigner_renorm(int L, const int64_t* __restrict__ off, double* __restrict__ d, int* renorm) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)L * (L + 1) / 2) return;
+  int l = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((int64_t)l * (l + 1) / 2 > t) --l;
+  while ((int64_t)(l + 1) * (l + 2) / 2 <= t) ++l;
+  const int b = (int)(t - (int64_t)l * (l + 1) / 2);
+  bool bad = false;
+  double s = 0.0;
+  for (int a = 0; a <= l; ++a) {
+    const double v = d[off[(int64_t)a * L + b] + l - max(a, b)];
+    if (fabs(v) > 1.0 + 1e-9) bad = true;
+    s = __dadd_rn(s, __dmul_rn(__dmul_rn(a == 0 ? 1.0 : 2.0, v), v));
+  }
+  if (!bad) return;
+  atomicAdd(renorm, 1);
+  const double scale = __ddiv_rn(1.0, sqrt(s));
+  for (int a = 0; a <= l; ++a) {
+    double* e = d + off[(int64_t)a * L + b] + l - max(a, b);
+    *e = __dmul_rn(*e, scale);
+  }
+}
+
+struct WignerDev {
+  int L = 0;
+  int renorm = 0;
+  DevBuf<double> d;
+  DevBuf<int64_t> off;
+};
+
+static void check_wigner_cap(int L, size_t cap) {
   if (L < 1) throw std::invalid_argument("band limit must be positive");
   const size_t bytes = wigner_bytes(L);
   if (bytes > cap)
     throw std::invalid_argument("Wigner tables for band limit " + std::to_string(L) + " need " +
                                 std::to_string(bytes) + " bytes, over the cap of " +
                                 std::to_string(cap));
-  WignerHost t;
-  t.L = L;
-  t.off.assign(static_cast<size_t>(L) * L + 1, 0);
+}
+
+static void build_wigner_device(WignerDev& w, int L, size_t cap, cudaStream_t stream) {
+  check_wigner_cap(L, cap);
+  w.L = L;
+  std::vector<int64_t> off(static_cast<size_t>(L) * L + 1, 0);
   int64_t o = 0;
   for (int a = 0; a < L; ++a)
     for (int b = 0; b < L; ++b) {
-      t.off[(size_t)a * L + b] = o;
+      off[(size_t)a * L + b] = o;
       o += L - std::max(a, b);
     }
-  t.off.back() = o;
-  t.d.assign(static_cast<size_t>(o), 0.0);
-  for (int a = 0; a < L; ++a)
-    for (int b = 0; b < L; ++b) {
-      const int l0 = std::max(a, b), lo = std::min(a, b);
-      long double prod = 1.0L;
-      for (int k = 1; k <= l0 - lo; ++k) prod *= static_cast<long double>(l0 + lo + k) / k;
-      const long double v = std::ldexp(1.0L, -l0) * std::sqrt(prod);
-      double* chain = t.d.data() + t.off[(size_t)a * L + b];
-      chain[0] = static_cast<double>(parity_sign(l0 - b) * v);
-      if (l0 + 1 >= L) continue;
-      double prev = 0.0, cur = chain[0];
-      for (int l = l0; l + 1 < L; ++l) {
-        double next;
-        if (l == 0) {
-          next = 0.0;
-        } else {
-          const double c1 = std::sqrt(static_cast<double>(l + 1 + a)) * std::sqrt(static_cast<double>(l + 1 - a)) *
-                            std::sqrt(static_cast<double>(l + 1 + b)) * std::sqrt(static_cast<double>(l + 1 - b));
-          const double c0 = std::sqrt(static_cast<double>(l + a)) * std::sqrt(static_cast<double>(l - a)) *
-                            std::sqrt(static_cast<double>(l + b)) * std::sqrt(static_cast<double>(l - b));
-          next = (-(2.0 * l + 1.0) * a * b * cur - (l + 1.0) * c0 * prev) / (l * c1);
-        }
-        chain[l + 1 - l0] = next;
-        prev = cur;
-        cur = next;
-      }
-    }
-  // Renormalization guard (wigner.cpp:111-130).
-  for (int l = 0; l < L; ++l)
-    for (int b = 0; b <= l; ++b) {
-      bool bad = false;
-      double s = 0.0;
-      for (int a = 0; a <= l; ++a) {
-        const double v = t.get(l, a, b);
-        if (std::abs(v) > 1.0 + 1e-9) bad = true;
-        s += (a == 0 ? 1.0 : 2.0) * v * v;
-      }
-      if (!bad) continue;
-      ++t.renorm;
-      const double scale = 1.0 / std::sqrt(s);
-      for (int a = 0; a <= l; ++a) t.d[t.off[(size_t)a * L + b] + l - std::max(a, b)] *= scale;
-    }
-  return t;
+  off.back() = o;
+  w.d.alloc((size_t)o);
+  w.off.alloc(off.size());
+  SPH_CUDA(cudaMemcpyAsync(w.off.get(), off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
+  DevBuf<int> cnt(1);
+  SPH_CUDA(cudaMemsetAsync(cnt.get(), 0, sizeof(int), stream));
+  const int64_t chains = (int64_t)L * L, cols = (int64_t)L * (L + 1) / 2;
+  k_wigner_chains<<<(unsigned)ceil_div(chains, (int64_t)128), 128, 0, stream>>>(L, w.off.get(), w.d.get());
+  SPH_LAUNCH_CHECK();
+  k_wigner_renorm<<<(unsigned)ceil_div(cols, (int64_t)128), 128, 0, stream>>>(L, w.off.get(), w.d.get(), cnt.get());
+  SPH_LAUNCH_CHECK();
+  SPH_CUDA(cudaMemcpyAsync(&w.renorm, cnt.get(), sizeof(int), cudaMemcpyDeviceToHost, stream));
+  SPH_CUDA(cudaStreamSynchronize(stream));
+}
+
+// Gather d^l_{m2,m}(pi/2) with the sign rules of WignerTables::d_half_pi
+// (wigner.cpp:136-150): zero for |m2| or |m| > l.
+__global__ void k_wigner_gather(int L, const int64_t* __restrict__ off, const double* __restrict__ d, int64_t n,
+                                const int* __restrict__ ls, const int* __restrict__ m2s, const int* __restrict__ ms,
+                                double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int l = ls[i];
+  int m2 = m2s[i], m = ms[i];
+  if (abs(m2) > l || abs(m) > l) { out[i] = 0.0; return; }
+  int sign = 1;
+  if (m2 < 0) { sign *= ((l + m) & 1) ? -1 : 1; m2 = -m2; }
+  if (m < 0) { sign *= ((l + m2) & 1) ? -1 : 1; m = -m; }
+  out[i] = sign * d[off[(int64_t)m2 * L + m] + l - max(m2, m)];
 }
 
 // ===========================================================================
@@ -612,8 +686,10 @@ struct Sht {
     if (L < 1 || L > maxL)
       throw std::invalid_argument("grid " + std::to_string(n_theta) + "x" + std::to_string(n_phi) +
                                   " does not resolve band limit " + std::to_string(L));
-    WignerHost w = build_wigner(L, cap ? cap : (size_t{2} << 30));
+    check_wigner_cap(L, cap ? cap : (size_t{2} << 30));  // before any CUDA call
     SPH_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    WignerDev wigner;  // freed once the operators below are built
+    build_wigner_device(wigner, L, cap ? cap : (size_t{2} << 30), stream);
     // Offsets of the per-m operators.
     psi_off.resize(L + 1);
     y_off.resize(L + 1);
@@ -644,11 +720,8 @@ struct Sht {
     SPH_CUDA(cudaMemcpy(d_psi_off.get(), psi_off.data(), (L + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
     SPH_CUDA(cudaMemcpy(d_y_off.get(), y_off.data(), (L + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
     SPH_CUDA(cudaMemcpy(d_z_off.get(), z_off.data(), (L + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
-    // Wigner chains to the device.
-    DevBuf<double> dd(w.d.size());
-    DevBuf<int64_t> doff(w.off.size());
-    SPH_CUDA(cudaMemcpy(dd.get(), w.d.data(), w.d.size() * sizeof(double), cudaMemcpyHostToDevice));
-    SPH_CUDA(cudaMemcpy(doff.get(), w.off.data(), w.off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    const double* dd_p = wigner.d.get();
+    const int64_t* doff_p = wigner.off.get();
     // Twiddles of the extended line and the T_+/- tables (host, exact angles).
     const int n_ext = 2 * n_theta - 2;
     std::vector<double2> tw_ext(n_ext);
@@ -672,10 +745,10 @@ struct Sht {
     k_sht_vtables<<<dim3(ceil_div(n_theta, 128), L), 128, 0, stream>>>(L, n_theta, dtw.get(), vre.get(), vim.get());
     SPH_LAUNCH_CHECK();
     k_sht_build_psi<<<dim3(ceil_div(n_theta, DG_BN), ceil_div(L, DG_BM), L), DG_THREADS, 0, stream>>>(
-        dd.get(), doff.get(), L, n_theta, vre.get(), vim.get(), d_psi_off.get(), psi.get());
+        dd_p, doff_p, L, n_theta, vre.get(), vim.get(), d_psi_off.get(), psi.get());
     SPH_LAUNCH_CHECK();
     k_sht_build_y<<<dim3(ceil_div(n_theta, DG_BM), ceil_div(L, DG_BN), L), DG_THREADS, 0, stream>>>(
-        dd.get(), doff.get(), L, n_theta, dtc.get(), dts.get(), d_y_off.get(), y.get());
+        dd_p, doff_p, L, n_theta, dtc.get(), dts.get(), d_y_off.get(), y.get());
     SPH_LAUNCH_CHECK();
     // Ring FFT plan.
     fplan.n = n_phi;
@@ -915,6 +988,39 @@ int sphemu_gpu_sht_inverse(sphemu_sht_t p, const double* coeffs, int where_in, i
 
 void* sphemu_gpu_sht_stream(sphemu_sht_t p) { return p ? p->p->stream : nullptr; }
 double sphemu_gpu_sht_plan_seconds(sphemu_sht_t p) { return p ? p->p->plan_seconds : 0.0; }
+
+int sphemu_gpu_wigner_d_half_pi(int band_limit, size_t wigner_cap_bytes, int64_t n, const int* l, const int* m2,
+                                const int* m, double* out, int* renorm_warnings) {
+  return guard([&] {
+    using namespace sphemu_gpu;
+    if (n < 0) throw std::invalid_argument("negative entry count");
+    for (int64_t i = 0; i < n; ++i)
+      if (l[i] < 0 || l[i] >= band_limit) throw std::invalid_argument("degree outside the table");
+    const size_t cap = wigner_cap_bytes ? wigner_cap_bytes : (size_t{2} << 30);
+    check_wigner_cap(band_limit, cap);
+    cudaStream_t s = nullptr;
+    SPH_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+    } sg{s};
+    WignerDev w;
+    build_wigner_device(w, band_limit, cap, s);
+    if (renorm_warnings) *renorm_warnings = w.renorm;
+    if (n == 0) return;
+    DevBuf<int> idx((size_t)n * 3);
+    DevBuf<double> dout((size_t)n);
+    SPH_CUDA(cudaMemcpyAsync(idx.get(), l, n * sizeof(int), cudaMemcpyHostToDevice, s));
+    SPH_CUDA(cudaMemcpyAsync(idx.get() + n, m2, n * sizeof(int), cudaMemcpyHostToDevice, s));
+    SPH_CUDA(cudaMemcpyAsync(idx.get() + 2 * n, m, n * sizeof(int), cudaMemcpyHostToDevice, s));
+    k_wigner_gather<<<(unsigned)ceil_div(n, (int64_t)256), 256, 0, s>>>(band_limit, w.off.get(), w.d.get(), n,
+                                                                         idx.get(), idx.get() + n, idx.get() + 2 * n,
+                                                                         dout.get());
+    SPH_LAUNCH_CHECK();
+    SPH_CUDA(cudaMemcpyAsync(out, dout.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPH_CUDA(cudaStreamSynchronize(s));
+  });
+}
 
 int sphemu_gpu_emulate(sphemu_sht_t p, const double* v, int d, const double* phi, int order, const double* means,
                        const double* sigma, const double* v2, int t_out, uint64_t seed, int r_len, int rng_mode,

@@ -183,6 +183,15 @@ int main() {
   CHECK(throws<std::invalid_argument>([] { build_plan(GridSpec{9, 16}, 9); }));           // test_sht.cpp:196-199
   CHECK(throws<std::invalid_argument>([] { build_wigner_tables(720); }));                 // 2 GiB cap (F5)
   CHECK(!throws<std::invalid_argument>([] { build_wigner_tables(720, std::size_t{4} << 30); }));
+  {  // test_wigner.cpp:23-31 closed forms, read from the device-built tables
+    auto w = build_wigner_tables(8);
+    CHECK(std::fabs(w->d_half_pi(1, 0, 0)) < 1e-15);
+    CHECK(std::fabs(w->d_half_pi(1, 1, 1) - 0.5) < 1e-15);
+    CHECK(std::fabs(w->d_half_pi(1, 1, 0) + std::sqrt(0.5)) < 1e-15);
+    CHECK(std::fabs(w->d_half_pi(2, 0, 0) + 0.5) < 1e-15);
+    CHECK(w->d_half_pi(3, 4, 0) == 0.0);
+    CHECK(throws<std::out_of_range>([&] { w->d_half_pi(8, 0, 0); }));
+  }
 
   // covariance + nugget (test_stochastic.cpp:159-210)
   {

@@ -50,7 +50,7 @@ def test_config_validation_like_reference(sph):  # test_mpchol.cpp:263-280
 
 def test_python_names_mirror_reference(sph):  # proj/python/sphemu/__init__.py
     for name in ("forward_sht", "inverse_sht", "tiled_cholesky", "make_spd_matrix", "max_band_limit",
-                 "resolution_summary", "__version__"):
+                 "resolution_summary", "wigner_d_half_pi", "__version__"):
         assert hasattr(sph, name)
     assert sph.max_band_limit(721, 1440) == 720
     assert sph.max_band_limit(720, 1440) == 719

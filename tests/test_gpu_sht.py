@@ -1,6 +1,7 @@
 """GPU parity of the SHT against the reference's own sht.cpp outputs (golden
 vectors from oracle/_ref) and the oracle. Restates proj/tests/test_sht.cpp and
 acceptance criteria 1-2. Tolerance: 1e-10 relative in FP64 (north star)."""
+import ctypes as C
 import math
 import os
 
@@ -129,3 +130,53 @@ def test_inverse_sht_under_resolved_falls_back(sph, O):  # bindings/module.cpp:9
         assert rel(got[s], want) < 1e-12
     with pytest.raises(ValueError):
         sph.synth_bandlimited(c, 1, 18)
+
+
+# ---- Wigner d(pi/2) tables built on the device (wigner.cpp:49-150) --------
+def _all_d_indices(L):
+    idx = np.array([(l, m2, m) for l in range(L) for m2 in range(-l, l + 1) for m in range(-l, l + 1)],
+                   dtype=np.int32)
+    return idx[:, 0].copy(), idx[:, 1].copy(), idx[:, 2].copy()
+
+
+@pytest.mark.parametrize("L", [13, 33])
+def test_device_wigner_matches_reference_golden(sph, L):
+    """Same ordering as the reference-generated golden vectors
+    (tests/golden/make_golden.py, via oracle/_ref): agreement to the last bit
+    or two (the chain seed is a double-double product here, long double in
+    wigner.cpp:18-28; the recurrence itself is evaluated in the reference's
+    order with no FMA contraction)."""
+    G = np.load(GOLDEN)
+    want = G[f"wigner_d_L{L}"]
+    l, m2, m = _all_d_indices(L)
+    got = sph.wigner_d_half_pi(l, m2, m)
+    assert np.abs(got - want).max() <= 4e-16 * max(1.0, np.abs(want).max())
+    assert (got == want).mean() > 0.9
+
+
+def test_device_wigner_python_api(sph, O):  # test_smoke.py:33, test_wigner.cpp:23-31
+    assert sph.wigner_d_half_pi(1, 0, 0) == pytest.approx(0.0, abs=1e-15)
+    for (l, m2, m) in [(1, 1, 1), (2, 1, 0), (3, -2, 1), (4, 3, -3), (5, 5, 0), (7, 2, 9)]:
+        assert sph.wigner_d_half_pi(l, m2, m) == pytest.approx(O.lib().so_wigner_brute(l, m2, m), abs=1e-14)
+    with pytest.raises(ValueError):
+        sph.wigner_d_half_pi(-1, 0, 0)
+
+
+@pytest.mark.parametrize("L", [181, 361])
+def test_device_wigner_matches_oracle_large(sph, O, L):
+    """C2 / C3 band limits: the device tables against the oracle restatement of
+    wigner.cpp on a seeded sample of entries, plus the guard count."""
+    w = O.Wigner(L, cap=8 << 30)
+    rng = np.random.default_rng(L)
+    n = 20000
+    l = rng.integers(0, L, n).astype(np.int32)
+    m2 = (rng.integers(-L, L, n) % (l + 1) * rng.choice([-1, 1], n)).astype(np.int32)
+    m = (rng.integers(-L, L, n) % (l + 1) * rng.choice([-1, 1], n)).astype(np.int32)
+    want = np.array([w.d(int(a), int(b), int(c)) for a, b, c in zip(l, m2, m)])
+    renorm = C.c_int(-1)
+    got = np.empty(n)
+    rc = sph._sphemu.lib().sphemu_gpu_wigner_d_half_pi(L, 8 << 30, n, l.ctypes.data, m2.ctypes.data,
+                                                        m.ctypes.data, got.ctypes.data, C.byref(renorm))
+    assert rc == 0
+    assert np.abs(got - want).max() < 1e-13
+    assert renorm.value == w.renorm_warnings
