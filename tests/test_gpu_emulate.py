@@ -66,3 +66,57 @@ def test_replicate_ranges_compose(sph, O, rng_mode):
     parts = [sph._sphemu.emulate(plan, v, phi, means, sigma, v2, t_out, 21, cnt, mode, r_begin=beg)
              for beg, cnt in ((0, 2), (2, 1), (3, 2))]
     assert np.array_equal(np.concatenate(parts), full)
+
+
+def _ar_psi_weights(phi):  # tests/support/reference.cpp:123-133
+    psi = [1.0]
+    for s in range(1, 100000):
+        v = sum(phi[j - 1] * psi[s - j] for j in range(1, min(len(phi), s) + 1))
+        if s > len(phi) and abs(v) < 1e-12:
+            break
+        psi.append(v)
+    return np.array(psi)
+
+
+def test_acceptance8_emulation_consistency(sph):
+    """acceptance_main.cpp:383-531 (criterion 8): L = 8 on the 9 x 16 grid,
+    dense innovation covariance U_ij = d_i d_j 0.7^|i-j|, AR(3) by degree
+    (make_generating_model(0.25, 0.75, 0.8), :249-300), v^2 = 0.04, 200
+    replicates x 48 steps, seed 88. Screens as the reference: per-location
+    3-SE mean and variance screens (<= 2 of 144 locations each, variance
+    against the model-implied value) and the hp/dp std ratio (< 0.10) with
+    the factor of the same covariance stored in half precision (dphp). The
+    factors are the device's; the draws follow the reference stream."""
+    L, d, t_len, reps = 8, 64, 48, 200
+    nt, nphi = L + 1, 2 * L
+    points = nt * nphi
+    deg = np.sqrt(np.arange(d)).astype(int)
+    di = 0.3 * (1.0 + 0.2 * np.sin(0.37 * np.arange(d)))
+    u = di[:, None] * di[None, :] * 0.7 ** np.abs(np.arange(d)[:, None] - np.arange(d)[None, :])
+    g = 0.25 + (0.75 - 0.25) * np.arange(L) / (L - 1)
+    phi_deg = np.stack([0.60 * g, 0.25 * g, 0.15 * g])
+    phi = phi_deg[:, deg]
+    sigma = 0.5 + 1.5 * ((7 * np.arange(points)) % 144) / 143.0
+    v2 = np.full(points, 0.04)
+    tt = np.arange(1, t_len + 1)[:, None]
+    means = 0.8 + 0.5 * np.cos(2 * np.pi * tt / 12) - 0.3 * np.sin(2 * np.pi * tt / 12) + np.zeros((1, points))
+    plan = sph.ShtPlan(nt, nphi, L)
+    f_dp, _ = sph.tiled_cholesky(u, variant="dp", tile_size=16)
+    f_hp, _ = sph.tiled_cholesky(u, variant="dphp", tile_size=16)
+    y = sph._sphemu.emulate(plan, f_dp, phi, means, sigma, v2, t_len, 88, reps, "reference").reshape(reps, t_len, -1)
+    y_hp = sph._sphemu.emulate(plan, f_hp, phi, means, sigma, v2, t_len, 88, reps, "reference").reshape(reps, t_len, -1)
+    # model-implied per-location variance (:416-456)
+    psi = [_ar_psi_weights(phi_deg[:, l]) for l in range(L)]
+    s_ll = np.array([[np.dot(psi[a][:min(len(psi[a]), len(psi[b]))], psi[b][:min(len(psi[a]), len(psi[b]))])
+                      for b in range(L)] for a in range(L)])
+    cols = plan.inverse(np.eye(d)).reshape(d, points)
+    w = u * s_ll[deg][:, deg]
+    implied = sigma ** 2 * (np.einsum("il,ij,jl->l", cols, w, cols) + 0.04)
+    dev = y - means[None]
+    a_rep, b_rep = dev.mean(1), (dev ** 2).mean(1)
+    z_mean = a_rep.mean(0) / np.sqrt(a_rep.var(0, ddof=1) / reps)
+    z_std = (b_rep.mean(0) - implied) / np.sqrt(b_rep.var(0, ddof=1) / reps)
+    ratio = np.sqrt(((y_hp - means[None]) ** 2).sum((0, 1)) / (dev ** 2).sum((0, 1)))
+    assert (np.abs(z_mean) > 3).sum() <= 2, np.abs(z_mean).max()
+    assert (np.abs(z_std) > 3).sum() <= 2, np.abs(z_std).max()
+    assert np.abs(ratio - 1).max() < 0.10

@@ -180,3 +180,39 @@ def test_device_wigner_matches_oracle_large(sph, O, L):
     assert rc == 0
     assert np.abs(got - want).max() < 1e-13
     assert renorm.value == w.renorm_warnings
+
+
+def test_device_wigner_acceptance(sph, O):
+    """acceptance_main.cpp:132-159 on the device tables: recursion vs the
+    factorial sum (l <= 12, < 1e-12) and orthonormality of d^l(pi/2) up to
+    l = 64 (< 1e-10), also at the C4 band limit on sampled degrees."""
+    l, m2, m = _all_d_indices(13)
+    brute = np.array([O.lib().so_wigner_brute(int(a), int(b), int(c)) for a, b, c in zip(l, m2, m)])
+    assert np.abs(sph.wigner_d_half_pi(l, m2, m) - brute).max() < 1e-12
+    for L, degrees in ((65, range(65)), (720, (100, 359, 600, 719))):
+        worst = 0.0
+        for deg in degrees:
+            k = np.arange(-deg, deg + 1, dtype=np.int32)
+            M2, M = np.meshgrid(k, k, indexing="ij")
+            ls = np.full(M.size, deg, dtype=np.int32)
+            vals = np.empty(M.size)
+            rc = sph._sphemu.lib().sphemu_gpu_wigner_d_half_pi(
+                L, 8 << 30, M.size, ls.ctypes.data, np.ascontiguousarray(M2.ravel()).ctypes.data,
+                np.ascontiguousarray(M.ravel()).ctypes.data, vals.ctypes.data, None)
+            assert rc == 0
+            D = vals.reshape(M2.shape)
+            worst = max(worst, np.abs(D.T @ D - np.eye(2 * deg + 1)).max())
+        assert worst < 1e-10, (L, worst)
+
+
+def test_parseval_on_device(sph, O):  # test_sht.cpp:135-143, acceptance_main.cpp:86-109
+    for L in (8, 16, 32, 64):  # oversampled (2L+1) x 4L grids
+        p = sph.ShtPlan(2 * L + 1, 4 * L, L)
+        for rep in range(3):
+            c = O.draw_random_coefficients(L, 100 * L + rep)
+            f = p.inverse(c)[0]
+            back = p.forward(f)[0]
+            assert np.abs(back - c).max() < 1e-9 * max(1.0, np.abs(c).max())
+            e_c = O.lib().so_parseval_energy(np.ascontiguousarray(c), L)
+            e_f = O.lib().so_field_energy_quadrature(np.ascontiguousarray(f), 2 * L + 1, 4 * L)
+            assert abs(e_c - e_f) / e_c < 1e-8
