@@ -425,8 +425,9 @@ def e2e_single(sph, wl, args, a_dev):
     return {"value": n ** 3 / 3 / t_e2e / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": 8 * n * n,
             "d2h_bytes_per_step": 8 * n * n, "ms_per_step": 1e3 * t_e2e, "steps": e2e_steps,
             "api": "sphemu_gpu_tiled_cholesky_dense (host pointers, pinned)",
-            "bytes_note": "counted as the dense n x n in and out; the library moves the lower triangle (H2D by "
-                          "tile rows, D2H by tile columns as they finish) and host threads write the zeros"}
+            "bytes_note": "counted as the dense n x n in and out; the library moves the lower triangle at storage "
+                          "width (fp64 DP tiles, fp32 the rest: H2D by tile rows, D2H by tile-column groups as they "
+                          "finish), host threads narrow / widen it and stream the zeros"}
 
 
 def e2e_dist(sph, args, world, rank):

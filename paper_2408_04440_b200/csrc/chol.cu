@@ -10,6 +10,9 @@
 //          -> trailing update grouped by output precision class.
 #include <algorithm>
 #include <atomic>
+#include <emmintrin.h>
+#include <condition_variable>
+#include <functional>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -301,6 +304,111 @@ struct BlockCyclic {
   }
 };
 
+// fp64 <-> fp32 row conversion with streaming (non-temporal) stores: the
+// destination is written once and read by the DMA engine or the caller, so
+// skipping the read-for-ownership cuts the host memory traffic per element
+// from 16 (20) to 12 bytes.
+static void narrow_row(float* dst, const double* src, int cw) {
+  int c = 0;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)
+    for (; c + 4 <= cw; c += 4) {
+      const __m128 lo = _mm_cvtpd_ps(_mm_loadu_pd(src + c));
+      const __m128 hi = _mm_cvtpd_ps(_mm_loadu_pd(src + c + 2));
+      _mm_stream_ps(dst + c, _mm_movelh_ps(lo, hi));
+    }
+  for (; c < cw; ++c) dst[c] = static_cast<float>(src[c]);
+}
+
+static void zero_row(double* dst, int64_t cnt) {
+  int64_t c = 0;
+  for (; c < cnt && (reinterpret_cast<uintptr_t>(dst + c) & 15); ++c) dst[c] = 0.0;
+  const __m128d z = _mm_setzero_pd();
+  for (; c + 2 <= cnt; c += 2) _mm_stream_pd(dst + c, z);
+  for (; c < cnt; ++c) dst[c] = 0.0;
+}
+
+static void widen_row(double* dst, const float* src, int cw) {
+  int c = 0;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)
+    for (; c + 4 <= cw; c += 4) {
+      const __m128 v = _mm_loadu_ps(src + c);
+      _mm_stream_pd(dst + c, _mm_cvtps_pd(v));
+      _mm_stream_pd(dst + c + 2, _mm_cvtps_pd(_mm_movehl_ps(v, v)));
+    }
+  for (; c < cw; ++c) dst[c] = static_cast<double>(src[c]);
+}
+
+// Blocking parallel-for over a fixed set of host threads (the caller runs
+// share 0). Used by the packed host I/O to convert tile rows between fp64 and
+// their storage width on the host side of the link.
+class HostPool {
+ public:
+  explicit HostPool(int n) : n_(std::max(1, n)) {
+    for (int t = 1; t < n_; ++t) th_.emplace_back([this, t] { loop(t); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return n_; }
+  void run(const std::function<void(int, int)>& f) {
+    std::unique_lock<std::mutex> lk(mu_);
+    job_ = &f;
+    pending_ = n_ - 1;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    f(0, n_);
+    lk.lock();
+    done_.wait(lk, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop(int t) {
+    uint64_t seen = 0;
+    while (true) {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      const auto* f = job_;
+      lk.unlock();
+      (*f)(t, n_);
+      lk.lock();
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  int n_;
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int, int)>* job_ = nullptr;
+  uint64_t gen_ = 0;
+  int pending_ = 0;
+  bool stop_ = false;
+};
+
+struct PinnedBuf {
+  char* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t bytes) {
+    if (n >= bytes) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    SPH_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), bytes, cudaHostAllocDefault));
+    n = bytes;
+  }
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
 struct Chol {
   static constexpr int kChainCtas = 32;  // SMs reserved for the critical chain under lookahead
   int potrf_cap = kChainCtas;            // cooperative POTRF grid cap (follows the step's reserve)
@@ -427,6 +535,177 @@ struct Chol {
   int64_t hldo = 0;
   std::vector<std::thread> zeroers;
 
+  // Packed host I/O (single GPU, host buffers; SPHEMU_PACKED_IO=0 disables):
+  // tile rows cross the link at storage width (k_load_packed), the factor
+  // comes back the same way by column groups (k_store_cols_packed) and host
+  // threads widen it into the caller's fp64 buffer while the factorization
+  // continues. Halves the PCIe bytes of an SP-dominated matrix.
+  std::unique_ptr<HostPool> iopool;
+  PinnedBuf pin_in, pin_out;
+  DevBuf<int64_t> d_grp_off, d_grp_rb;
+  std::vector<int64_t> grp_off, grp_rb, grp_base;
+  std::vector<cudaEvent_t> ev_grp;
+  std::thread expander;
+  std::mutex out_mu;
+  std::condition_variable out_cv;
+  int groups_issued = 0, groups_total = 0;
+  bool out_abort = false, packed_out = false;
+  std::exception_ptr out_err;
+
+  bool packed_io() const {
+    static const bool on = [] {
+      const char* e = std::getenv("SPHEMU_PACKED_IO");
+      return !(e && std::atoi(e) == 0);
+    }();
+    return on && !dist();
+  }
+  HostPool& pool() {
+    if (!iopool) {
+      const char* e = std::getenv("SPHEMU_IO_THREADS");
+      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+      const int T = e ? std::max(1, std::atoi(e)) : static_cast<int>(std::min(24u, std::max(1u, hw - 1)));
+      iopool = std::make_unique<HostPool>(T);
+    }
+    return *iopool;
+  }
+  int64_t seg_bytes(int i, int j) const { return packed_seg_bytes(std::min(lb, n - j * lb), sprec[tix(i, j)]); }
+
+  void load_host_packed(const double* a, int64_t lda, double diag_shift) {
+    std::vector<int64_t> rbytes(nt), boff(nt + 1, 0);
+    for (int i = 0; i < nt; ++i) {
+      int64_t w = 0;
+      for (int j = 0; j <= i; ++j) w += seg_bytes(i, j);
+      rbytes[i] = w;
+      boff[i + 1] = boff[i] + w * rows(i);
+    }
+    pin_in.ensure(static_cast<size_t>(boff[nt]));
+    const size_t slab_bytes = sizeof(double) * static_cast<size_t>(lb) * n;  // >= any packed row block
+    if (islab.n < kSlabs * static_cast<size_t>(lb) * n) islab.alloc(kSlabs * static_cast<size_t>(lb) * n);
+    char* dslab = reinterpret_cast<char*>(islab.get());
+    const unsigned gy = static_cast<unsigned>(std::max(1, b * b / (256 * 64)));
+    HostPool& P = pool();
+    for (int i = 0; i < nt; ++i) {
+      char* hb = pin_in.p + boff[i];
+      const int nr = rows(i);
+      const int64_t rbi = rbytes[i];
+      P.run([&](int t, int T) {
+        const int r0 = static_cast<int>(static_cast<int64_t>(nr) * t / T);
+        const int r1 = static_cast<int>(static_cast<int64_t>(nr) * (t + 1) / T);
+        for (int r = r0; r < r1; ++r) {
+          const double* src = a + static_cast<int64_t>(i * lb + r) * lda;
+          char* dst = hb + static_cast<int64_t>(r) * rbi;
+          for (int j = 0; j <= i; ++j) {
+            const int cw = std::min(lb, n - j * lb);
+            const double* sj = src + static_cast<int64_t>(j) * lb;
+            if (sprec[tix(i, j)] == kDP) {
+              std::memcpy(dst, sj, sizeof(double) * cw);
+            } else {
+              narrow_row(reinterpret_cast<float*>(dst), sj, cw);
+            }
+            dst += seg_bytes(i, j);
+          }
+        }
+        _mm_sfence();
+      });
+      const int s = i % kSlabs;
+      if (i >= kSlabs) SPH_CUDA(cudaStreamWaitEvent(cstream, ev_in_free[s], 0));
+      char* dst = dslab + s * slab_bytes;
+      SPH_CUDA(cudaMemcpyAsync(dst, hb, static_cast<size_t>(rbi) * nr, cudaMemcpyHostToDevice, cstream));
+      SPH_CUDA(cudaEventRecord(ev_in_full[s], cstream));
+      SPH_CUDA(cudaStreamWaitEvent(stream, ev_in_full[s], 0));
+      k_load_packed<<<dim3(static_cast<unsigned>(i + 1), gy), 256, 0, stream>>>(store(), dst, rbi, sat.get(), i,
+                                                                                 diag_shift);
+      SPH_LAUNCH_CHECK();
+      SPH_CUDA(cudaEventRecord(ev_in_free[s], stream));
+    }
+  }
+
+  void begin_packed_out() {
+    const int G = col_group();
+    groups_total = (nt + G - 1) / G;
+    grp_off.assign(static_cast<size_t>(groups_total) * nt, 0);
+    grp_rb.assign(static_cast<size_t>(groups_total) * nt, 0);
+    grp_base.assign(groups_total + 1, 0);
+    for (int g = 0; g < groups_total; ++g) {
+      const int k0 = g * G, k1 = std::min(nt, k0 + G);
+      int64_t o = 0;
+      for (int i = k0; i < nt; ++i) {
+        int64_t w = 0;
+        for (int j = k0; j < k1 && j <= i; ++j) w += seg_bytes(i, j);
+        grp_off[static_cast<size_t>(g) * nt + i] = o;
+        grp_rb[static_cast<size_t>(g) * nt + i] = w;
+        o += w * rows(i);
+      }
+      grp_base[g + 1] = grp_base[g] + o;
+    }
+    pin_out.ensure(static_cast<size_t>(grp_base[groups_total]));
+    d_grp_off.alloc(grp_off.size());
+    d_grp_rb.alloc(grp_rb.size());
+    SPH_CUDA(cudaMemcpy(d_grp_off.get(), grp_off.data(), grp_off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    SPH_CUDA(cudaMemcpy(d_grp_rb.get(), grp_rb.data(), grp_rb.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    while (static_cast<int>(ev_grp.size()) < groups_total) {
+      cudaEvent_t e;
+      SPH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev_grp.push_back(e);
+    }
+    groups_issued = 0;
+    out_abort = false;
+    out_err = nullptr;
+    packed_out = true;
+    expander = std::thread([this, G] {
+      try {
+        for (int g = 0; g < groups_total; ++g) {
+          {
+            std::unique_lock<std::mutex> lk(out_mu);
+            out_cv.wait(lk, [&] { return out_abort || groups_issued > g; });
+            if (groups_issued <= g) return;
+          }
+          SPH_CUDA(cudaEventSynchronize(ev_grp[g]));
+          widen_group(g, G);
+        }
+      } catch (...) {
+        out_err = std::current_exception();
+      }
+    });
+  }
+
+  void widen_group(int g, int G) {
+    const int k0 = g * G, k1 = std::min(nt, k0 + G);
+    const int R0 = k0 * lb, nr = n - R0;
+    const char* base = pin_out.p + grp_base[g];
+    pool().run([&](int t, int T) {
+      const int a0 = R0 + static_cast<int>(static_cast<int64_t>(nr) * t / T);
+      const int a1 = R0 + static_cast<int>(static_cast<int64_t>(nr) * (t + 1) / T);
+      for (int R = a0; R < a1; ++R) {
+        const int i = R / lb;
+        const size_t gi = static_cast<size_t>(g) * nt + i;
+        const char* src = base + grp_off[gi] + static_cast<int64_t>(R - i * lb) * grp_rb[gi];
+        double* dst = hout + static_cast<int64_t>(R) * hldo + static_cast<int64_t>(k0) * lb;
+        for (int j = k0; j < k1 && j <= i; ++j) {
+          const int cw = std::min(lb, n - j * lb);
+          if (sprec[tix(i, j)] == kDP) {
+            std::memcpy(dst, src, sizeof(double) * cw);
+          } else {
+            widen_row(dst, reinterpret_cast<const float*>(src), cw);
+          }
+          dst += cw;
+          src += seg_bytes(i, j);
+        }
+      }
+      _mm_sfence();
+    });
+  }
+
+  void stop_expander() {
+    if (!expander.joinable()) return;
+    {
+      std::lock_guard<std::mutex> lk(out_mu);
+      out_abort = true;
+    }
+    out_cv.notify_all();
+    expander.join();
+  }
+
   void ensure_io() {
     if (cstream) return;
     SPH_CUDA(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
@@ -440,6 +719,10 @@ struct Chol {
 
   void load_host(const double* a, int64_t lda, double diag_shift = 0.0) {
     ensure_io();
+    if (packed_io()) {
+      load_host_packed(a, lda, diag_shift);
+      return;
+    }
     const size_t slab = static_cast<size_t>(lb) * n;
     if (islab.n < kSlabs * slab) islab.alloc(kSlabs * slab);
     std::vector<char> row_has(nt, 0);  // rows holding at least one tile of this rank
@@ -482,6 +765,8 @@ struct Chol {
     col_pending = -1;
     hout = out;
     hldo = ldo;
+    packed_out = false;
+    if (packed_io()) begin_packed_out();
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     static const int t_env = [] {
       const char* e = std::getenv("SPHEMU_ZERO_THREADS");
@@ -493,8 +778,9 @@ struct Chol {
       zeroers.emplace_back([=] {
         for (int64_t R = t; R < nn; R += T) {
           const int64_t c0 = (R / l + 1) * l;
-          if (c0 < nn) std::memset(out + R * ldo + c0, 0, sizeof(double) * (nn - c0));
+          if (c0 < nn) zero_row(out + R * ldo + c0, nn - c0);
         }
+        _mm_sfence();
       });
   }
 
@@ -520,6 +806,24 @@ struct Chol {
     SPH_CUDA(cudaEventRecord(ev_col, s));
     SPH_CUDA(cudaStreamWaitEvent(dstream, ev_col, 0));
     const int h = n - k0 * lb;
+    if (packed_out) {
+      if (k0 % G) throw std::runtime_error("packed output expects column groups aligned to the group size");
+      const int g = k0 / G;
+      k_store_cols_packed<<<h, 256, 0, dstream>>>(from ? *from : store(), k0, k + 1,
+                                                  d_grp_off.get() + static_cast<size_t>(g) * nt,
+                                                  d_grp_rb.get() + static_cast<size_t>(g) * nt,
+                                                  reinterpret_cast<char*>(oslab.get()));
+      SPH_LAUNCH_CHECK();
+      SPH_CUDA(cudaMemcpyAsync(pin_out.p + grp_base[g], oslab.get(), static_cast<size_t>(grp_base[g + 1] - grp_base[g]),
+                               cudaMemcpyDeviceToHost, dstream));
+      SPH_CUDA(cudaEventRecord(ev_grp[g], dstream));
+      {
+        std::lock_guard<std::mutex> lk(out_mu);
+        groups_issued = g + 1;
+      }
+      out_cv.notify_all();
+      return;
+    }
     const int W = G * lb;
     k_store_cols<<<h, 256, 0, dstream>>>(from ? *from : store(), k0, k + 1, W, oslab.get());
     SPH_LAUNCH_CHECK();
@@ -530,11 +834,18 @@ struct Chol {
   }
 
   void end_host_out() {
+    stop_expander();  // every group was issued by now, or the factorization failed
     for (auto& t : zeroers) t.join();
     zeroers.clear();
+    packed_out = false;
     if (!hout) return;
     hout = nullptr;
     SPH_CUDA(cudaStreamSynchronize(dstream));
+    if (out_err) {
+      std::exception_ptr e = out_err;
+      out_err = nullptr;
+      std::rethrow_exception(e);
+    }
   }
 
   int rows(int i) const { return std::min(lb, n - i * lb); }
@@ -690,7 +1001,9 @@ struct Chol {
   }
 
   ~Chol() {
+    stop_expander();
     for (auto& t : zeroers) t.join();
+    for (auto e : ev_grp) cudaEventDestroy(e);
     if (dstream) cudaStreamSynchronize(dstream);
     if (cstream) cudaStreamSynchronize(cstream);
     for (int s = 0; s < kSlabs; ++s) {

@@ -95,6 +95,64 @@ static __global__ void k_load_dense(TileStore ts, const double* __restrict__ a, 
   flush_sat(local, sat);
 }
 
+// Packed host I/O (single GPU, host buffers): a tile row crosses the host
+// link at its storage width — DP tiles as fp64, every other class as fp32
+// (the reference's quantize goes double -> float first, so the float is the
+// exact value the device stores or rounds further to binary16 / bf16). Each
+// tile's segment of a row is padded to 16 bytes.
+__host__ __device__ __forceinline__ int64_t packed_seg_bytes(int cw, int prec) {
+  return ((int64_t)cw * (prec == kDP ? 8 : 4) + 15) & ~(int64_t)15;
+}
+
+// Row block i (tiles j = 0..i) from a packed slab with rowbytes per row.
+static __global__ void k_load_packed(TileStore ts, const char* __restrict__ blk, int64_t rowbytes, unsigned* sat,
+                                     int i, double diag_shift) {
+  const int j = blockIdx.x;
+  int64_t seg = 0;
+  for (int jj = 0; jj < j; ++jj) seg += packed_seg_bytes(min(ts.lb, ts.n - jj * ts.lb), ts.tprec(i, jj));
+  void* tp = ts.tile(i, j);
+  const int p = ts.tprec(i, j);
+  const int b = ts.b;
+  const int rows = min(ts.lb, ts.n - i * ts.lb), cw = min(ts.lb, ts.n - j * ts.lb);
+  unsigned local = 0;
+  for (int64_t e = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; e < (int64_t)b * b;
+       e += (int64_t)gridDim.y * blockDim.x) {
+    const int r = (int)(e / b), c = (int)(e % b);
+    double v = 0.0;
+    if (r < rows && c < cw) {
+      const char* row = blk + (int64_t)r * rowbytes + seg;
+      v = p == kDP ? reinterpret_cast<const double*>(row)[c] : (double)reinterpret_cast<const float*>(row)[c];
+      if (i == j && r == c) v += diag_shift;
+    }
+    store_elem(tp, p, e, v, local);
+  }
+  flush_sat(local, sat);
+}
+
+// Tile columns [k0, k1) of the factor, packed: one CTA per output row R >=
+// k0 lb; row-block byte offsets rb_off[i] (from k0's block) and row widths
+// rb_bytes[i] come from the host. Zeros above the diagonal inside the
+// diagonal tile, like k_store_cols.
+static __global__ void k_store_cols_packed(TileStore ts, int k0, int k1, const int64_t* __restrict__ rb_off,
+                                           const int64_t* __restrict__ rb_bytes, char* __restrict__ slab) {
+  const int R = k0 * ts.lb + blockIdx.x;
+  const int i = R / ts.lb;
+  char* row = slab + rb_off[i] + (int64_t)(R - i * ts.lb) * rb_bytes[i];
+  const int64_t rb = (int64_t)(R % ts.lb) * ts.b;
+  for (int j = k0; j < k1 && j <= i; ++j) {
+    const int p = ts.tprec(i, j);
+    const int cw = min(ts.lb, ts.n - j * ts.lb);
+    const void* tp = ts.tile(i, j);
+    for (int c = threadIdx.x; c < cw; c += blockDim.x) {
+      const int C = j * ts.lb + c;
+      const double v = C <= R ? load_elem(tp, p, rb + c) : 0.0;
+      if (p == kDP) reinterpret_cast<double*>(row)[c] = v;
+      else reinterpret_cast<float*>(row)[c] = (float)v;  // exact: the stored value is a float or narrower
+    }
+    row += packed_seg_bytes(cw, p);
+  }
+}
+
 // TiledMatrix::to_dense_lower (mpchol.cpp:140-154): lower part from the
 // tiles, exact zeros above the diagonal. One thread per output element.
 static __global__ void k_store_dense(TileStore ts, double* __restrict__ out, int64_t ldo) {
