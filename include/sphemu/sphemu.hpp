@@ -5,5 +5,6 @@
 #include "sphemu/mpchol.hpp"
 #include "sphemu/sht.hpp"
 #include "sphemu/stochastic.hpp"
+#include "sphemu/trend.hpp"
 #include "sphemu/version.hpp"
 #include "sphemu/wigner.hpp"

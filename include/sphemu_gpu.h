@@ -237,6 +237,32 @@ int sphemu_gpu_emulate_range(sphemu_sht_t p, const double* v, int d, const doubl
                              const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed,
                              int r_begin, int r_count, int rng_mode, double* out);
 
+/* ======================================================================
+ * Trend mean structure (replaces trend.hpp:79-82 mean_table and
+ * trend.hpp:71-76 detrend / retrend; trend.cpp:252-324)
+ * ====================================================================== */
+/* records: points x (5 + 2*harmonics) host doubles, TrendModel::values
+ * (beta0, beta1, beta2, rho, a_1..a_K, b_1..b_K, sigma; trend.hpp:37-59).
+ * Forcing: ForcingTrajectory{x, history} (trend.hpp:24-35) as two host
+ * arrays; n_x = n_history = 0 is the empty trajectory (no forcing terms).
+ * SPHEMU_ERR_INVALID_ARG for t_start < 1 ("time steps are 1-based") and for a
+ * missing lag history (require_lag_history, trend.cpp:21-25). Results are
+ * bitwise those of the reference (no FMA contraction, same libm cos/sin). */
+int sphemu_gpu_mean_table(const double* records, int64_t points, int harmonics, int period,
+                          const double* forcing_x, int64_t n_x, const double* forcing_history, int64_t n_history,
+                          int t_len, int64_t t_start, double* table, int where_out);
+/* detrend (trend.cpp:289-305): out = (series - m_t) / sigma over an
+ * (r_len, t_len, points) series. */
+int sphemu_gpu_detrend(const double* series, int where_in, int r_len, int t_len, const double* records,
+                       int64_t points, int harmonics, int period, const double* forcing_x, int64_t n_x,
+                       const double* forcing_history, int64_t n_history, int64_t t_start, double* out,
+                       int where_out);
+/* retrend (trend.cpp:307-324): out = m_t + sigma * standardized. */
+int sphemu_gpu_retrend(const double* standardized, int where_in, int r_len, int t_len, const double* records,
+                       int64_t points, int harmonics, int period, const double* forcing_x, int64_t n_x,
+                       const double* forcing_history, int64_t n_history, int64_t t_start, double* out,
+                       int where_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -137,6 +137,13 @@ def lib():
             C.POINTER(C.c_double), C.POINTER(CholStats)]
         L.so_emulate.argtypes = [C.c_void_p, _dp, C.c_int, _dp, C.c_int, _dp, _dp, _dp, C.c_int,
                                  C.c_uint64, C.c_int, C.c_int, _dp]
+        L.so_eval_mean_trend.restype = C.c_double
+        L.so_eval_mean_trend.argtypes = [_dp, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                         C.c_void_p, C.c_int64, C.POINTER(C.c_int)]
+        L.so_mean_table.argtypes = [_dp, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_int64, C.c_void_p,
+                                    C.c_int64, C.c_int, C.c_int64, _dp]
+        L.so_trend_apply.argtypes = [C.c_int, _dp, C.c_int, C.c_int, _dp, C.c_int64, C.c_int, C.c_int,
+                                     C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64, _dp]
         _lib = L
     return _lib
 
@@ -337,3 +344,48 @@ def find_openblas():
     except Exception:
         pass
     return None
+
+
+def _forcing(forcing):
+    x, h = forcing if forcing is not None else (None, None)
+    x = np.ascontiguousarray(np.zeros(0) if x is None else x, dtype=np.float64)
+    h = np.ascontiguousarray(np.zeros(0) if h is None else h, dtype=np.float64)
+    return (x, h), [x.ctypes.data if x.size else None, x.size, h.ctypes.data if h.size else None, h.size]
+
+
+def eval_mean_trend(records, harmonics, period, loc, t, forcing=None):
+    """eval_mean_trend (trend.cpp:65-83); raises ValueError on missing lag history."""
+    keep, fa = _forcing(forcing)
+    err = C.c_int()
+    v = lib().so_eval_mean_trend(np.ascontiguousarray(records, dtype=np.float64), harmonics, period, loc, t,
+                                 *fa, C.byref(err))
+    if err.value:
+        raise ValueError("lagged forcing term needs history")
+    return v
+
+
+def mean_table(records, harmonics, period, t_len, t_start=1, forcing=None):
+    """mean_table (trend.cpp:252-287): (t_len, points)."""
+    rec = np.ascontiguousarray(records, dtype=np.float64)
+    points = rec.size // (5 + 2 * harmonics)
+    keep, fa = _forcing(forcing)
+    out = np.empty((t_len, points))
+    rc = lib().so_mean_table(rec, points, harmonics, period, *fa, t_len, t_start, out)
+    if rc:
+        raise ValueError("time steps are 1-based" if rc == -1 else "lagged forcing term needs history")
+    return out
+
+
+def trend_apply(mode, series, records, harmonics, period, forcing=None, t_start=1):
+    """mode "detrend" (trend.cpp:289-305) or "retrend" (trend.cpp:307-324) over (r, t, points)."""
+    rec = np.ascontiguousarray(records, dtype=np.float64)
+    points = rec.size // (5 + 2 * harmonics)
+    x = np.ascontiguousarray(series, dtype=np.float64).reshape(-1, series.shape[-2] if series.ndim == 3 else
+                                                               series.shape[0], points)
+    keep, fa = _forcing(forcing)
+    out = np.empty(x.shape)
+    rc = lib().so_trend_apply({"detrend": 0, "retrend": 1}[mode], x, x.shape[0], x.shape[1], rec, points,
+                              harmonics, period, *fa, t_start, out)
+    if rc:
+        raise ValueError("time steps are 1-based" if rc == -1 else "lagged forcing term needs history")
+    return out.reshape(series.shape)

@@ -170,6 +170,21 @@ int so_emulate(const so_plan* p, const double* v, int d, const double* phi, int 
                const double* means, const double* sigma, const double* v2, int t_out,
                uint64_t seed, int r_len, int threads, double* out);
 
+/* ---------------- trend.cpp:18-57,59-83,252-324 (mean structure) ----------------
+ * records: points x (5 + 2K) TrendModel::values; forcing {x[n_x], history[n_h]}
+ * (n_x = n_h = 0: empty trajectory). Return 0, or -1 for t_start < 1,
+ * -2 for a missing lag history (require_lag_history, trend.cpp:21-25). */
+double so_eval_mean_trend(const double* records, int harmonics, int period, int64_t loc, int64_t t,
+                          const double* fx, int64_t n_x, const double* fh, int64_t n_h, int* err);
+int so_mean_table(const double* records, int64_t points, int harmonics, int period,
+                  const double* fx, int64_t n_x, const double* fh, int64_t n_h,
+                  int t_len, int64_t t_start, double* table);
+/* mode 0: detrend (y - m) / sigma (trend.cpp:289-305); 1: retrend m + sigma z
+ * (trend.cpp:307-324). in/out are (r_len, t_len, points). */
+int so_trend_apply(int mode, const double* in, int r_len, int t_len, const double* records, int64_t points,
+                   int harmonics, int period, const double* fx, int64_t n_x, const double* fh, int64_t n_h,
+                   int64_t t_start, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,25 +7,29 @@ sm_100a kernels in lib/libsphemu_gpu.so (see include/sphemu_gpu.h).
 """
 from ._sphemu import (  # noqa: F401
     Cholesky,
+    ForcingTrajectory,
     NotPositiveDefiniteError,
     ShtPlan,
     __version__,
     assign_precisions,
+    detrend,
     emulate,
     estimate_innovation_covariance,
     forward_sht,
     inverse_sht,
     make_spd_matrix,
+    mean_table,
     nccl_unique_id,
     max_band_limit,
     resolution_summary,
+    retrend,
     synth_bandlimited,
     tiled_cholesky,
     wigner_d_half_pi,
 )
 
 __all__ = [
-    "Cholesky", "NotPositiveDefiniteError", "ShtPlan", "__version__", "assign_precisions", "emulate",
+    "Cholesky", "ForcingTrajectory", "NotPositiveDefiniteError", "ShtPlan", "__version__", "assign_precisions", "emulate",
     "estimate_innovation_covariance", "forward_sht", "inverse_sht", "make_spd_matrix", "nccl_unique_id", "max_band_limit", "resolution_summary",
-    "synth_bandlimited", "tiled_cholesky", "wigner_d_half_pi",
+    "synth_bandlimited", "tiled_cholesky", "wigner_d_half_pi", "mean_table", "detrend", "retrend",
 ]

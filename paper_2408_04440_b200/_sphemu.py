@@ -127,6 +127,11 @@ def lib():
         L.sphemu_gpu_estimate_innovation_covariance.argtypes = [
             vp, C.c_int, i64, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(CholConfig), vp, C.c_int, vp, C.c_int,
             dp, C.POINTER(CholStats)]
+        trend = [vp, C.c_int, C.c_int, C.c_int, vp, i64, C.c_int, C.c_int, vp, i64, vp, i64, i64, vp, C.c_int]
+        L.sphemu_gpu_mean_table.argtypes = [vp, i64, C.c_int, C.c_int, vp, i64, vp, i64, C.c_int, i64, vp,
+                                            C.c_int]
+        L.sphemu_gpu_detrend.argtypes = trend
+        L.sphemu_gpu_retrend.argtypes = trend
         _lib = L
     return _lib
 
@@ -492,3 +497,66 @@ def resolution_summary(band_limit):
     return {"band_limit": band_limit, "degrees_per_cell": 180.0 / band_limit,
             "km_per_cell": 180.0 * 111.2 / band_limit,
             "grid_points": (band_limit - 1) * (2 * band_limit)}
+
+
+class ForcingTrajectory:
+    """ForcingTrajectory (trend.hpp:24-35): x[k] is year k+1, history[k] is
+    year -k (newest first). Empty (both None) = no forcing terms."""
+
+    def __init__(self, x=None, history=None):
+        self.x = np.ascontiguousarray(np.zeros(0) if x is None else x, dtype=np.float64).ravel()
+        self.history = np.ascontiguousarray(np.zeros(0) if history is None else history, dtype=np.float64).ravel()
+
+    def empty(self) -> bool:
+        return self.x.size == 0 and self.history.size == 0
+
+
+def _forcing_args(forcing):
+    f = forcing if isinstance(forcing, ForcingTrajectory) else ForcingTrajectory(
+        *(forcing if forcing is not None else (None, None)))
+    return f, [_ptr(f.x) if f.x.size else None, f.x.size, _ptr(f.history) if f.history.size else None,
+               f.history.size]
+
+
+def _records(records, harmonics):
+    rec = np.ascontiguousarray(records, dtype=np.float64)
+    stride = 5 + 2 * harmonics
+    if rec.size % stride:
+        raise ValueError(f"records must hold (5 + 2*harmonics) = {stride} values per location")
+    return rec, rec.size // stride
+
+
+def mean_table(records, harmonics, period, t_len, t_start=1, forcing=None):
+    """mean_table (trend.cpp:252-287) on the device: (t_len, points) means of
+    the TrendModel records (points x (5 + 2*harmonics)) for steps
+    t_start..t_start+t_len-1. forcing: ForcingTrajectory or (x, history)."""
+    rec, points = _records(records, harmonics)
+    f, fa = _forcing_args(forcing)
+    out = np.empty((t_len, points))
+    _check(lib().sphemu_gpu_mean_table(_ptr(rec), points, harmonics, period, *fa, t_len, t_start, _ptr(out), HOST))
+    return out
+
+
+def _trend_apply(fn, series, records, harmonics, period, forcing, t_start):
+    rec, points = _records(records, harmonics)
+    f, fa = _forcing_args(forcing)
+    x = np.ascontiguousarray(series, dtype=np.float64)
+    if x.ndim == 2:
+        x = x[None]
+    r_len, t_len = x.shape[0], x.shape[1]
+    if x.size != r_len * t_len * points:
+        raise ValueError("series grid differs from model")
+    out = np.empty(x.shape)
+    _check(fn(_ptr(x), HOST, r_len, t_len, _ptr(rec), points, harmonics, period, *fa, t_start, _ptr(out), HOST))
+    return out.reshape(np.shape(series))
+
+
+def detrend(series, records, harmonics, period, forcing=None, t_start=1):
+    """detrend (trend.cpp:289-305): (y - m_t) / sigma over a (r, t, ...)
+    series whose trailing axes hold the model's points."""
+    return _trend_apply(lib().sphemu_gpu_detrend, series, records, harmonics, period, forcing, t_start)
+
+
+def retrend(standardized, records, harmonics, period, forcing=None, t_start=1):
+    """retrend (trend.cpp:307-324): m_t + sigma * z."""
+    return _trend_apply(lib().sphemu_gpu_retrend, standardized, records, harmonics, period, forcing, t_start)

@@ -1,0 +1,267 @@
+// trend.cu — the deterministic mean structure either side of the emulator's
+// hot path: mean_table / detrend / retrend of
+// proj/src/trend.cpp:252-324 on the device.
+//
+// Work split. The per-step scalars (current-year forcing x_t, the lagged
+// forcing average of the shared rho, and the K seasonal cos/sin pairs) are
+// O(t_len) host work done here in the library (same libm, same operation
+// order as trend.cpp:258-277). The O(t_len * points) evaluation runs in one
+// HBM-bound kernel: a CTA owns 128 consecutive locations and a run of time
+// rows; the CTA's location records are staged once in shared memory with
+// coalesced loads and held in registers (compile-time harmonic count) for
+// every row, the rows' per-step scalars sit in shared memory (broadcast reads),
+// four rows' loads are in flight per thread, each row's output is written (and
+// for detrend/retrend its input read) fully coalesced. Algorithmic bytes per
+// element: 8 (table) or 16 (detrend / retrend). All arithmetic is explicit
+// round-to-nearest without FMA contraction, in the reference's expression
+// order, so the results are bitwise those of the reference's x86-64 Release
+// build (no FMA), which the oracle restates.
+#include <cmath>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "sphemu_gpu.h"
+
+namespace sphemu_gpu {
+namespace {
+
+constexpr double kTwoPi = 2.0 * 3.14159265358979323846;  // trend.cpp:14
+constexpr double kLagWeightCutoff = 1e-12;                // trend.cpp:15
+constexpr int kTrendThreads = 128;
+constexpr int kTrendRows = 64;
+
+enum TrendMode { kTable = 0, kDetrend = 1, kRetrend = 2 };
+
+// ForcingTrajectory (trend.hpp:24-35; trend.cpp:35-57).
+struct Forcing {
+  const double* x;
+  int64_t nx;
+  const double* hist;
+  int64_t nh;
+  bool empty() const { return nx == 0 && nh == 0; }
+  bool has_year(int64_t year) const { return year >= 1 ? year <= nx : -year < nh; }
+  double at_year(int64_t year) const {
+    if (!has_year(year)) return 0.0;
+    return year >= 1 ? x[year - 1] : hist[-year];
+  }
+  double lagged_mean(int64_t year, double rho) const {
+    double acc = 0.0, w = 1.0;
+    for (int64_t s = 1;; ++s) {
+      if (!has_year(year - s)) break;
+      acc += w * at_year(year - s);
+      w *= rho;
+      if (w < kLagWeightCutoff) break;
+    }
+    return (1.0 - rho) * acc;
+  }
+};
+
+int64_t year_of(int64_t t, int period) { return (t + period - 1) / period; }  // trend.cpp:18
+
+// One row of per-step scalars: {x_t, lagged, cos(base), sin(base), ..., cos(K base), sin(K base)}
+// (trend.cpp:259-275). Throws like require_lag_history (trend.cpp:21-25).
+std::vector<double> row_params(const double* records, int64_t points, int harmonics, int period,
+                               const Forcing& f, int t_len, int64_t t_start) {
+  const int64_t stride = 5 + 2 * (int64_t)harmonics;
+  const int rp = 2 + 2 * harmonics;
+  std::vector<double> out((size_t)t_len * rp, 0.0);
+  const bool with_forcing = !f.empty();
+  bool any_lag = false;
+  if (with_forcing)
+    for (int64_t loc = 0; loc < points && !any_lag; ++loc) any_lag = records[loc * stride + 2] != 0.0;
+  for (int row = 0; row < t_len; ++row) {
+    const int64_t t = t_start + row;
+    double* o = out.data() + (size_t)row * rp;
+    const double base = kTwoPi * static_cast<double>(t % period) / period;
+    for (int k = 1; k <= harmonics; ++k) {
+      o[2 + 2 * (k - 1)] = std::cos(base * k);
+      o[2 + 2 * (k - 1) + 1] = std::sin(base * k);
+    }
+    if (with_forcing) {
+      const int64_t year = year_of(t, period);
+      if (any_lag && !f.has_year(year - 1))
+        throw std::invalid_argument("lagged forcing term needs history before year " + std::to_string(year));
+      o[0] = f.at_year(year);
+      o[1] = f.lagged_mean(year, records[3]);  // rho is shared: record(0)[3]
+    }
+  }
+  return out;
+}
+
+// m_t at one location (trend.cpp:270-279 order). K >= 0: compile-time
+// harmonics, rec is a register array; K < 0: runtime count, rec in smem.
+template <int K>
+__device__ __forceinline__ double eval_mean(const double* rec, const double* p, int harmonics, int with_forcing) {
+  const int hk = K >= 0 ? K : harmonics;
+  double m = rec[0];
+  if (with_forcing) m = __dadd_rn(m, __dadd_rn(__dmul_rn(rec[1], p[0]), __dmul_rn(rec[2], p[1])));
+#pragma unroll
+  for (int k = 0; k < (K >= 0 ? K : hk); ++k)
+    m = __dadd_rn(m, __dadd_rn(__dmul_rn(rec[4 + k], p[2 + 2 * k]), __dmul_rn(rec[4 + hk + k], p[3 + 2 * k])));
+  return m;
+}
+
+// grid: x = location blocks of kTrendThreads, y = blocks of kTrendRows (r, t) rows.
+// Shared memory: the CTA's records (kTrendThreads x stride) then its rows'
+// per-step scalars (kTrendRows x rp).
+template <int MODE, int K>
+__global__ void __launch_bounds__(kTrendThreads) k_trend(const double* __restrict__ records, int64_t points,
+                                                         int harmonics, const double* __restrict__ rowp,
+                                                         int with_forcing, int t_len, int64_t row_base,
+                                                         int64_t n_rows, const double* __restrict__ in,
+                                                         double* __restrict__ out) {
+  extern __shared__ double s_mem[];
+  const int hk = K >= 0 ? K : harmonics;
+  const int stride = 5 + 2 * hk;
+  const int rp = 2 + 2 * hk;
+  double* s_rec = s_mem;
+  double* s_row = s_mem + kTrendThreads * stride;
+  const int64_t loc0 = (int64_t)blockIdx.x * kTrendThreads;
+  const int nloc = (int)(points - loc0 < kTrendThreads ? points - loc0 : kTrendThreads);
+  const int64_t r_begin = row_base + (int64_t)blockIdx.y * kTrendRows;
+  const int nr = (int)(r_begin + kTrendRows < n_rows ? kTrendRows : n_rows - r_begin);
+  // Coalesced stage of this CTA's records (contiguous nloc * stride doubles) and row scalars.
+  const double* src = records + loc0 * stride;
+  for (int i = threadIdx.x; i < nloc * stride; i += kTrendThreads) s_rec[i] = src[i];
+  for (int i = threadIdx.x; i < nr * rp; i += kTrendThreads)
+    s_row[i] = rowp[((r_begin + i / rp) % t_len) * rp + i % rp];
+  __syncthreads();
+  if ((int)threadIdx.x >= nloc) return;
+  const int64_t loc = loc0 + threadIdx.x;
+  constexpr int kRegs = K >= 0 ? 5 + 2 * K : 1;
+  double reg[kRegs];
+  const double* rec = s_rec + threadIdx.x * stride;
+  if constexpr (K >= 0) {
+#pragma unroll
+    for (int i = 0; i < kRegs; ++i) reg[i] = rec[i];
+    rec = reg;
+  }
+  const double sigma = rec[stride - 1];
+  const double* pin = in + r_begin * points + loc;
+  double* pout = out + r_begin * points + loc;
+  constexpr int U = 4;  // rows in flight per thread
+  for (int j = 0; j < nr; j += U) {
+    double x[U];
+    if (MODE != kTable) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = j + u < nr ? __ldcs(pin + (int64_t)(j + u) * points) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (j + u >= nr) break;
+      const double m = eval_mean<K>(rec, s_row + (j + u) * rp, hk, with_forcing);
+      double v;
+      if (MODE == kTable) v = m;
+      else if (MODE == kDetrend) v = __ddiv_rn(__dsub_rn(x[u], m), sigma);  // trend.cpp:302
+      else v = __dadd_rn(m, __dmul_rn(sigma, x[u]));                        // trend.cpp:320
+      __stcs(pout + (int64_t)(j + u) * points, v);
+    }
+  }
+}
+
+template <int MODE>
+void launch_trend(dim3 grid, size_t smem, const double* rec, int64_t points, int harmonics, const double* rowp,
+                  int wf, int t_len, int64_t row_base, int64_t n_rows, const double* in, double* out) {
+#define SPH_TREND_CASE(KK)                                                                                  \
+  case KK:                                                                                                   \
+    SPH_CUDA(cudaFuncSetAttribute(k_trend<MODE, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_trend<MODE, KK><<<grid, kTrendThreads, smem>>>(rec, points, harmonics, rowp, wf, t_len, row_base, n_rows, \
+                                                     in, out);                                               \
+    break;
+  switch (harmonics) {
+    SPH_TREND_CASE(0)
+    SPH_TREND_CASE(1)
+    SPH_TREND_CASE(2)
+    SPH_TREND_CASE(3)
+    SPH_TREND_CASE(4)
+    SPH_TREND_CASE(5)
+    SPH_TREND_CASE(6)
+    SPH_TREND_CASE(8)
+    default:
+      SPH_CUDA(cudaFuncSetAttribute(k_trend<MODE, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_trend<MODE, -1><<<grid, kTrendThreads, smem>>>(rec, points, harmonics, rowp, wf, t_len, row_base, n_rows,
+                                                       in, out);
+  }
+#undef SPH_TREND_CASE
+  SPH_LAUNCH_CHECK();
+}
+
+template <int MODE>
+void run_trend(const double* records, int64_t points, int harmonics, int period, const double* fx, int64_t nx,
+               const double* fh, int64_t nh, int r_len, int t_len, int64_t t_start, const double* in, int where_in,
+               double* out, int where_out) {
+  if (t_start < 1) throw std::invalid_argument("time steps are 1-based");
+  if (period < 1) throw std::invalid_argument("period must be positive");
+  if (harmonics < 0) throw std::invalid_argument("harmonics must be non-negative");
+  if (points < 0 || t_len < 0 || r_len < 0) throw std::invalid_argument("negative extent");
+  if ((nx > 0 && !fx) || (nh > 0 && !fh) || nx < 0 || nh < 0)
+    throw std::invalid_argument("forcing arrays missing");
+  const Forcing f{fx, nx, fh, nh};
+  if (points == 0 || t_len == 0 || r_len == 0) return;
+  const int64_t stride = 5 + 2 * (int64_t)harmonics;
+  const size_t smem = ((size_t)kTrendThreads * stride + (size_t)kTrendRows * (2 + 2 * harmonics)) * sizeof(double);
+  if (smem > 200 * 1024) throw std::invalid_argument("harmonics too large for the device trend kernel");
+  std::vector<double> rp = row_params(records, points, harmonics, period, f, t_len, t_start);
+  const int64_t n_rows = (int64_t)r_len * t_len;
+  const size_t n_el = (size_t)n_rows * points;
+  DevBuf<double> d_rec((size_t)points * stride), d_rp(rp.size()), d_in, d_out;
+  SPH_CUDA(cudaMemcpy(d_rec.get(), records, sizeof(double) * points * stride, cudaMemcpyHostToDevice));
+  SPH_CUDA(cudaMemcpy(d_rp.get(), rp.data(), sizeof(double) * rp.size(), cudaMemcpyHostToDevice));
+  const double* din = in;
+  if (MODE != kTable && where_in == SPHEMU_HOST) {
+    d_in.alloc(n_el);
+    SPH_CUDA(cudaMemcpy(d_in.get(), in, sizeof(double) * n_el, cudaMemcpyHostToDevice));
+    din = d_in.get();
+  }
+  double* dout = out;
+  if (where_out == SPHEMU_HOST) {
+    d_out.alloc(n_el);
+    dout = d_out.get();
+  }
+  const int64_t gy = (n_rows + kTrendRows - 1) / kTrendRows;
+  for (int64_t y0 = 0; y0 < gy; y0 += 65535) {
+    const dim3 grid((unsigned)ceil_div(points, kTrendThreads), (unsigned)std::min<int64_t>(65535, gy - y0));
+    launch_trend<MODE>(grid, smem, d_rec.get(), points, harmonics, d_rp.get(), !f.empty(), t_len, y0 * kTrendRows,
+                       n_rows, din, dout);
+  }
+  if (where_out == SPHEMU_HOST)
+    SPH_CUDA(cudaMemcpy(out, dout, sizeof(double) * n_el, cudaMemcpyDeviceToHost));
+  SPH_CUDA(cudaDeviceSynchronize());
+}
+
+}  // namespace
+}  // namespace sphemu_gpu
+
+extern "C" int sphemu_gpu_mean_table(const double* records, int64_t points, int harmonics, int period,
+                                     const double* forcing_x, int64_t n_x, const double* forcing_history,
+                                     int64_t n_history, int t_len, int64_t t_start, double* table, int where_out) {
+  using namespace sphemu_gpu;
+  return guard([&] {
+    run_trend<kTable>(records, points, harmonics, period, forcing_x, n_x, forcing_history, n_history, 1, t_len,
+                      t_start, nullptr, SPHEMU_HOST, table, where_out);
+  });
+}
+
+extern "C" int sphemu_gpu_detrend(const double* series, int where_in, int r_len, int t_len, const double* records,
+                                  int64_t points, int harmonics, int period, const double* forcing_x, int64_t n_x,
+                                  const double* forcing_history, int64_t n_history, int64_t t_start, double* out,
+                                  int where_out) {
+  using namespace sphemu_gpu;
+  return guard([&] {
+    run_trend<kDetrend>(records, points, harmonics, period, forcing_x, n_x, forcing_history, n_history, r_len,
+                        t_len, t_start, series, where_in, out, where_out);
+  });
+}
+
+extern "C" int sphemu_gpu_retrend(const double* standardized, int where_in, int r_len, int t_len,
+                                  const double* records, int64_t points, int harmonics, int period,
+                                  const double* forcing_x, int64_t n_x, const double* forcing_history,
+                                  int64_t n_history, int64_t t_start, double* out, int where_out) {
+  using namespace sphemu_gpu;
+  return guard([&] {
+    run_trend<kRetrend>(records, points, harmonics, period, forcing_x, n_x, forcing_history, n_history, r_len,
+                        t_len, t_start, standardized, where_in, out, where_out);
+  });
+}

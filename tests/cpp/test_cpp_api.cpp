@@ -218,6 +218,30 @@ int main() {
     CHECK(mu < 1e-12 * mx && mv < 1e-12 * mx && m.nugget == 0.0);
   }
 
+  // trend mean structure (test_trend.cpp:165-206)
+  {
+    TrendModel m;
+    m.spec = GridSpec{3, 4};
+    m.config.harmonics = 1;
+    m.config.period = 12;
+    m.config.validate();
+    const std::size_t pts = m.spec.points();
+    for (std::size_t loc = 0; loc < pts; ++loc) {
+      const double rec[7] = {1.0 + 0.1 * loc, 0.0, 0.0, 0.6, 0.5, -0.25, 0.5 + 0.05 * loc};
+      m.values.insert(m.values.end(), rec, rec + 7);
+    }
+    auto table = mean_table(m, {}, 24, 12);  // t = 12: base 0 -> beta0 + a_1
+    CHECK(table.size() == 24 * pts && table[0] == m.values[0] + 0.5);
+    FieldSeries y(m.spec, 24, 2);
+    for (std::size_t i = 0; i < y.values.size(); ++i) y.values[i] = std::sin(0.1 * i);
+    FieldSeries back = retrend(detrend(y, m, {}), m, {});
+    double worst = 0.0;
+    for (std::size_t i = 0; i < y.values.size(); ++i) worst = std::fmax(worst, std::fabs(back.values[i] - y.values[i]));
+    CHECK(worst < 1e-12);
+    CHECK(throws<std::invalid_argument>([&] { mean_table(m, {}, 4, 0); }));
+    CHECK(throws<std::invalid_argument>([] { TrendConfig{2, 13}.validate(); }));
+  }
+
   if (g_fail == 0) std::printf("ALL PASSED\n");
   return g_fail ? 1 : 0;
 }
