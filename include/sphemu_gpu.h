@@ -228,6 +228,16 @@ int sphemu_gpu_emulate(sphemu_sht_t p, const double* v, int d, const double* phi
                        const double* means, const double* sigma, const double* v2, int t_out,
                        uint64_t seed, int r_len, int rng_mode, double* out);
 
+/* emulate(model, plan, forcing, t_out, seed, r_len, threads, t_start)
+ * (stochastic.hpp:84-86) with the model's trend given as TrendModel records
+ * (points x (5 + 2*harmonics), trend.hpp:37-59) and the forcing as two
+ * arrays: the mean table (stochastic.cpp:229) and sigma are evaluated on the
+ * device (trend.cu) instead of crossing PCIe. */
+int sphemu_gpu_emulate_trend(sphemu_sht_t p, const double* v, int d, const double* phi, int order,
+                             const double* records, int harmonics, int period, const double* forcing_x, int64_t n_x,
+                             const double* forcing_history, int64_t n_history, int64_t t_start, const double* v2,
+                             int t_out, uint64_t seed, int r_len, int rng_mode, double* out);
+
 /* Replicates [r_begin, r_begin + r_count) of the same emulation (out holds
  * r_count replicates): the draws of replicate r do not depend on the split,
  * so replicate ranges can run on different GPUs with no communication

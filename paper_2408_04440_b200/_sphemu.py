@@ -130,6 +130,8 @@ def lib():
         trend = [vp, C.c_int, C.c_int, C.c_int, vp, i64, C.c_int, C.c_int, vp, i64, vp, i64, i64, vp, C.c_int]
         L.sphemu_gpu_mean_table.argtypes = [vp, i64, C.c_int, C.c_int, vp, i64, vp, i64, C.c_int, i64, vp,
                                             C.c_int]
+        L.sphemu_gpu_emulate_trend.argtypes = [vp, vp, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int, vp, i64, vp,
+                                               i64, i64, vp, C.c_int, C.c_uint64, C.c_int, C.c_int, vp]
         L.sphemu_gpu_detrend.argtypes = trend
         L.sphemu_gpu_retrend.argtypes = trend
         _lib = L
@@ -560,3 +562,25 @@ def detrend(series, records, harmonics, period, forcing=None, t_start=1):
 def retrend(standardized, records, harmonics, period, forcing=None, t_start=1):
     """retrend (trend.cpp:307-324): m_t + sigma * z."""
     return _trend_apply(lib().sphemu_gpu_retrend, standardized, records, harmonics, period, forcing, t_start)
+
+
+def emulate_model(plan, v, phi, records, harmonics, period, v2, t_out, seed=1, r_len=1, t_start=1, forcing=None,
+                  rng="reference"):
+    """emulate(model, plan, forcing, t_out, seed, r_len, threads, t_start)
+    (stochastic.cpp:217-277) with the model's trend as TrendModel records
+    (points x (5 + 2*harmonics)): the mean table and sigma are evaluated on
+    the device (trend.cu) instead of by the caller."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    d = v.shape[0]
+    phi = np.zeros((0, d)) if phi is None else np.ascontiguousarray(phi, dtype=np.float64).reshape(-1, d)
+    phi_a = phi if phi.shape[0] else np.zeros((1, d))
+    rec, points = _records(records, harmonics)
+    if points != plan.n_theta * plan.n_phi:
+        raise ValueError("trend model grid differs from the transform plan")
+    f, fa = _forcing_args(forcing)
+    v2 = np.ascontiguousarray(v2, dtype=np.float64)
+    out = np.empty((r_len, t_out, plan.n_theta, plan.n_phi))
+    _check(lib().sphemu_gpu_emulate_trend(plan.h, _ptr(v), d, _ptr(phi_a), phi.shape[0], _ptr(rec), harmonics,
+                                          period, *fa, t_start, _ptr(v2), t_out, seed, r_len,
+                                          {"reference": 0, "philox": 1}[rng], _ptr(out)))
+    return out

@@ -176,4 +176,20 @@ inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) 
 
 int num_sms();
 
+// TrendModel records + ForcingTrajectory for emulate's trend-model overload
+// (trend.cu mean_table_device; trend.hpp:24-59).
+struct TrendArgs {
+  const double* records;
+  int harmonics;
+  int period;
+  const double* fx;
+  int64_t nx;
+  const double* fh;
+  int64_t nh;
+  int64_t t_start;
+};
+void mean_table_device(const double* records, int64_t points, int harmonics, int period, const double* fx,
+                       int64_t nx, const double* fh, int64_t nh, int t_len, int64_t t_start, double* d_table,
+                       double* d_sigma, cudaStream_t stream, DevBuf<double>& d_rec, DevBuf<double>& d_rp);
+
 }  // namespace sphemu_gpu

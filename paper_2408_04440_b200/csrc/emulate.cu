@@ -146,7 +146,7 @@ struct RefGaussian {
 
 void emulate(void* plan, int n_theta, int n_phi, int L, const double* v, int d, const double* phi, int order,
              const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed, int r_len,
-             int rng_mode, double* out, int r_begin) {
+             int rng_mode, double* out, int r_begin, const TrendArgs* trend) {
   if (r_begin < 0) throw std::invalid_argument("first replicate must be >= 0");
   if (t_out < 1 || r_len < 1) throw std::invalid_argument("need t_out, r_len >= 1");
   if (d != L * L) throw std::invalid_argument("transform plan does not match the model");
@@ -162,8 +162,15 @@ void emulate(void* plan, int n_theta, int n_phi, int L, const double* v, int d, 
   DevBuf<double> dEps(ytot), dSynth(ytot), dMeans((size_t)t_out * points), dSigma(points), dV2(points),
       dPhi(order > 0 ? (size_t)order * d : 1);
   SPH_CUDA(cudaMemcpyAsync(dV.get(), v, (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice, s));
-  SPH_CUDA(cudaMemcpyAsync(dMeans.get(), means, (size_t)t_out * points * sizeof(double), cudaMemcpyHostToDevice, s));
-  SPH_CUDA(cudaMemcpyAsync(dSigma.get(), sigma, points * sizeof(double), cudaMemcpyHostToDevice, s));
+  DevBuf<double> dTrendRec, dTrendRows;
+  if (trend) {  // stochastic.cpp:229: mean_table(model.trend, forcing, t_out, t_start), on the device
+    mean_table_device(trend->records, points, trend->harmonics, trend->period, trend->fx, trend->nx, trend->fh,
+                      trend->nh, t_out, trend->t_start, dMeans.get(), dSigma.get(), s, dTrendRec, dTrendRows);
+  } else {
+    SPH_CUDA(cudaMemcpyAsync(dMeans.get(), means, (size_t)t_out * points * sizeof(double), cudaMemcpyHostToDevice,
+                             s));
+    SPH_CUDA(cudaMemcpyAsync(dSigma.get(), sigma, points * sizeof(double), cudaMemcpyHostToDevice, s));
+  }
   SPH_CUDA(cudaMemcpyAsync(dV2.get(), v2, points * sizeof(double), cudaMemcpyHostToDevice, s));
   if (order > 0)
     SPH_CUDA(cudaMemcpyAsync(dPhi.get(), phi, (size_t)order * d * sizeof(double), cudaMemcpyHostToDevice, s));

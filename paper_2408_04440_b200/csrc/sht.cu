@@ -942,7 +942,7 @@ struct sphemu_sht_s {
 namespace sphemu_gpu {
 void emulate(void* plan, int n_theta, int n_phi, int L, const double* v, int d, const double* phi, int order,
              const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed, int r_len,
-             int rng_mode, double* out, int r_begin);
+             int rng_mode, double* out, int r_begin, const TrendArgs* trend = nullptr);
 
 // Bridge for emulate.cu: the plan's stream, and a device-resident inverse.
 void sht_inverse_device(void* plan, const double* coeffs, int64_t n, double* fields, cudaStream_t* s_out) {
@@ -1028,6 +1028,17 @@ int sphemu_gpu_emulate(sphemu_sht_t p, const double* v, int d, const double* phi
   return guard([&] {
     emulate(p, p->p->n_theta, p->p->n_phi, p->p->L, v, d, phi, order, means, sigma, v2, t_out, seed, r_len,
             rng_mode, out, 0);
+  });
+}
+
+int sphemu_gpu_emulate_trend(sphemu_sht_t p, const double* v, int d, const double* phi, int order,
+                             const double* records, int harmonics, int period, const double* forcing_x, int64_t n_x,
+                             const double* forcing_history, int64_t n_history, int64_t t_start, const double* v2,
+                             int t_out, uint64_t seed, int r_len, int rng_mode, double* out) {
+  return guard([&] {
+    const TrendArgs ta{records, harmonics, period, forcing_x, n_x, forcing_history, n_history, t_start};
+    emulate(p, p->p->n_theta, p->p->n_phi, p->p->L, v, d, phi, order, nullptr, nullptr, v2, t_out, seed, r_len,
+            rng_mode, out, 0, &ta);
   });
 }
 

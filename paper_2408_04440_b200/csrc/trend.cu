@@ -163,11 +163,13 @@ __global__ void __launch_bounds__(kTrendThreads) k_trend(const double* __restric
 
 template <int MODE>
 void launch_trend(dim3 grid, size_t smem, const double* rec, int64_t points, int harmonics, const double* rowp,
-                  int wf, int t_len, int64_t row_base, int64_t n_rows, const double* in, double* out) {
+                  int wf, int t_len, int64_t row_base, int64_t n_rows, const double* in, double* out,
+                  cudaStream_t stream = nullptr) {
 #define SPH_TREND_CASE(KK)                                                                                  \
   case KK:                                                                                                   \
     SPH_CUDA(cudaFuncSetAttribute(k_trend<MODE, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_trend<MODE, KK><<<grid, kTrendThreads, smem>>>(rec, points, harmonics, rowp, wf, t_len, row_base, n_rows, \
+    k_trend<MODE, KK><<<grid, kTrendThreads, smem, stream>>>(rec, points, harmonics, rowp, wf, t_len, row_base, \
+                                                             n_rows,                                         \
                                                      in, out);                                               \
     break;
   switch (harmonics) {
@@ -181,8 +183,8 @@ void launch_trend(dim3 grid, size_t smem, const double* rec, int64_t points, int
     SPH_TREND_CASE(8)
     default:
       SPH_CUDA(cudaFuncSetAttribute(k_trend<MODE, -1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_trend<MODE, -1><<<grid, kTrendThreads, smem>>>(rec, points, harmonics, rowp, wf, t_len, row_base, n_rows,
-                                                       in, out);
+      k_trend<MODE, -1><<<grid, kTrendThreads, smem, stream>>>(rec, points, harmonics, rowp, wf, t_len, row_base,
+                                                               n_rows, in, out);
   }
 #undef SPH_TREND_CASE
   SPH_LAUNCH_CHECK();
@@ -232,6 +234,44 @@ void run_trend(const double* records, int64_t points, int harmonics, int period,
 }
 
 }  // namespace
+
+__global__ void k_trend_sigma(const double* __restrict__ records, int64_t points, int stride,
+                              double* __restrict__ sigma) {
+  for (int64_t loc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; loc < points; loc += (int64_t)gridDim.x * blockDim.x)
+    sigma[loc] = records[loc * stride + stride - 1];
+}
+
+// mean_table + the sigma column into device buffers on `stream` (emulate's
+// trend-model overload, stochastic.cpp:262-273 with trend.cpp:252-287). The
+// device records/row buffers live until the stream reaches them: the caller
+// synchronizes the stream before returning.
+void mean_table_device(const double* records, int64_t points, int harmonics, int period, const double* fx,
+                       int64_t nx, const double* fh, int64_t nh, int t_len, int64_t t_start, double* d_table,
+                       double* d_sigma, cudaStream_t stream, DevBuf<double>& d_rec, DevBuf<double>& d_rp) {
+  if (t_start < 1) throw std::invalid_argument("time steps are 1-based");
+  if (period < 1) throw std::invalid_argument("period must be positive");
+  if (harmonics < 0) throw std::invalid_argument("harmonics must be non-negative");
+  if ((nx > 0 && !fx) || (nh > 0 && !fh) || nx < 0 || nh < 0) throw std::invalid_argument("forcing arrays missing");
+  const Forcing f{fx, nx, fh, nh};
+  const int64_t stride = 5 + 2 * (int64_t)harmonics;
+  const size_t smem = ((size_t)kTrendThreads * stride + (size_t)kTrendRows * (2 + 2 * harmonics)) * sizeof(double);
+  if (smem > 200 * 1024) throw std::invalid_argument("harmonics too large for the device trend kernel");
+  std::vector<double> rp = row_params(records, points, harmonics, period, f, t_len, t_start);
+  d_rec.alloc((size_t)points * stride);
+  d_rp.alloc(rp.size());
+  SPH_CUDA(cudaMemcpyAsync(d_rec.get(), records, sizeof(double) * points * stride, cudaMemcpyHostToDevice, stream));
+  SPH_CUDA(cudaMemcpyAsync(d_rp.get(), rp.data(), sizeof(double) * rp.size(), cudaMemcpyHostToDevice, stream));
+  const int64_t gy = (t_len + kTrendRows - 1) / kTrendRows;
+  for (int64_t y0 = 0; y0 < gy; y0 += 65535) {
+    const dim3 grid((unsigned)ceil_div(points, kTrendThreads), (unsigned)std::min<int64_t>(65535, gy - y0));
+    launch_trend<kTable>(grid, smem, d_rec.get(), points, harmonics, d_rp.get(), !f.empty(), t_len, y0 * kTrendRows,
+                         t_len, nullptr, d_table, stream);
+  }
+  k_trend_sigma<<<2 * num_sms(), 256, 0, stream>>>(d_rec.get(), points, (int)stride, d_sigma);
+  SPH_LAUNCH_CHECK();
+  // rp is a pageable host vector: the async copy above is staged before it returns.
+}
+
 }  // namespace sphemu_gpu
 
 extern "C" int sphemu_gpu_mean_table(const double* records, int64_t points, int harmonics, int period,

@@ -120,3 +120,24 @@ def test_acceptance8_emulation_consistency(sph):
     assert (np.abs(z_mean) > 3).sum() <= 2, np.abs(z_mean).max()
     assert (np.abs(z_std) > 3).sum() <= 2, np.abs(z_std).max()
     assert np.abs(ratio - 1).max() < 0.10
+
+
+@pytest.mark.parametrize("forcing", [None, (np.linspace(0.2, 1.0, 4), np.array([0.1, 0.05]))])
+def test_trend_model_overload(sph, O, forcing):
+    """emulate with the TrendModel records (stochastic.cpp:229 mean_table on
+    the device) equals emulate with the oracle's mean table and sigma column,
+    bitwise (same draws, same device arithmetic)."""
+    L, order, K, period, t_out, r_len, t_start = 6, 2, 2, 12, 24, 2, 5
+    v, phi, _, v2, nt, nphi = model(O, L, order)
+    rng = np.random.default_rng(4)
+    rec = rng.standard_normal((nt * nphi, 5 + 2 * K))
+    rec[:, 2] = 0.3
+    rec[:, 3] = 0.6
+    rec[:, -1] = 0.5 + rng.random(nt * nphi)
+    means = O.mean_table(rec, K, period, t_out, t_start, forcing=forcing)
+    plan = sph.ShtPlan(nt, nphi, L)
+    want = sph._sphemu.emulate(plan, v, phi, means, rec[:, -1].copy(), v2, t_out, 13, r_len)
+    got = sph.emulate_model(plan, v, phi, rec, K, period, v2, t_out, 13, r_len, t_start=t_start, forcing=forcing)
+    assert np.array_equal(got, want)
+    with pytest.raises(ValueError):
+        sph.emulate_model(plan, v, phi, rec, K, period, v2, t_out, 13, r_len, t_start=0)
