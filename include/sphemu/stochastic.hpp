@@ -14,6 +14,7 @@
 #include "sphemu/grid.hpp"
 #include "sphemu/mpchol.hpp"
 #include "sphemu/sht.hpp"
+#include "sphemu/trend.hpp"
 #include "sphemu_gpu.h"
 
 namespace sphemu {
@@ -71,6 +72,29 @@ inline FieldSeries emulate(const ShtPlan& plan, std::span<const double> v, int d
   if (phi_pad.empty()) phi_pad.assign(static_cast<std::size_t>(d), 0.0);
   detail::check(sphemu_gpu_emulate(plan.device->h, v.data(), d, phi_pad.data(), order, means.data(), sigma.data(),
                                    v2.data(), t_out, seed, r_len, static_cast<int>(rng), out.values.data()));
+  return out;
+}
+
+// emulate(model, plan, forcing, t_out, seed, r_len, threads, t_start)
+// (stochastic.hpp:84-86) with the model's trend and forcing: the mean table
+// (stochastic.cpp:229) and sigma are evaluated on the device.
+inline FieldSeries emulate(const ShtPlan& plan, std::span<const double> v, int d, std::span<const double> phi,
+                           int order, const TrendModel& trend, const ForcingTrajectory& forcing,
+                           std::span<const double> v2, int t_out, std::uint64_t seed, int r_len = 1,
+                           std::int64_t t_start = 1, EmulationRng rng = EmulationRng::kReference) {
+  const std::size_t pts = plan.spec.points();
+  if (!(trend.spec == plan.spec) || d != plan.band_limit * plan.band_limit ||
+      v.size() != static_cast<std::size_t>(d) * d || phi.size() != static_cast<std::size_t>(order) * d ||
+      trend.values.size() != pts * trend.record_stride() || v2.size() != pts)
+    throw std::invalid_argument("transform plan does not match the model");
+  FieldSeries out(plan.spec, t_out, r_len);
+  std::vector<double> phi_pad(phi.begin(), phi.end());
+  if (phi_pad.empty()) phi_pad.assign(static_cast<std::size_t>(d), 0.0);
+  detail::check(sphemu_gpu_emulate_trend(plan.device->h, v.data(), d, phi_pad.data(), order, trend.values.data(),
+                                         trend.config.harmonics, trend.config.period, forcing.x.data(),
+                                         static_cast<std::int64_t>(forcing.x.size()), forcing.history.data(),
+                                         static_cast<std::int64_t>(forcing.history.size()), t_start, v2.data(), t_out,
+                                         seed, r_len, static_cast<int>(rng), out.values.data()));
   return out;
 }
 
