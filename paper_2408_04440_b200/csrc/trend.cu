@@ -30,7 +30,7 @@ namespace {
 constexpr double kTwoPi = 2.0 * 3.14159265358979323846;  // trend.cpp:14
 constexpr double kLagWeightCutoff = 1e-12;                // trend.cpp:15
 constexpr int kTrendThreads = 128;
-constexpr int kTrendRows = 64;
+constexpr int kTrendRows = 128;
 
 enum TrendMode { kTable = 0, kDetrend = 1, kRetrend = 2 };
 
