@@ -98,4 +98,42 @@ inline FieldSeries emulate(const ShtPlan& plan, std::span<const double> v, int d
   return out;
 }
 
+// VarModel / VarFit (stochastic.hpp:18-37) with the residuals as a dense
+// row-major (rows x d) vector instead of an Eigen matrix.
+struct VarModel {
+  int band_limit = 0;
+  int order = 0;
+  std::vector<double> phi;  // order rows of band_limit^2 coefficients
+  std::int64_t zeroed_count = 0;
+  std::int64_t unstable_count = 0;
+  double phi_at(int p, std::size_t idx) const {
+    return phi[static_cast<std::size_t>(p - 1) * band_limit * band_limit + idx];
+  }
+};
+
+struct VarFit {
+  VarModel model;
+  std::int64_t residual_rows = 0;
+  std::vector<double> residuals;
+  std::vector<double> phi_se;
+  double residual_mean_norm = 0.0;
+};
+
+// fit_var (stochastic.cpp:30-107) on the device.
+inline VarFit fit_var(const CoeffSeries& coeffs, int order) {
+  const std::int64_t d = static_cast<std::int64_t>(coeffs.slice_stride());
+  VarFit fit;
+  fit.model.band_limit = coeffs.band_limit;
+  fit.model.order = order;
+  const int rows_per_rep = order > 0 ? coeffs.t_len - order : coeffs.t_len;
+  fit.residual_rows = static_cast<std::int64_t>(coeffs.r_len) * (rows_per_rep > 0 ? rows_per_rep : 0);
+  fit.residuals.resize(static_cast<std::size_t>(fit.residual_rows * d));
+  fit.model.phi.assign(static_cast<std::size_t>(order > 0 ? order : 0) * d, 0.0);
+  fit.phi_se.assign(fit.model.phi.size(), 0.0);
+  detail::check(sphemu_gpu_fit_var(coeffs.values.data(), SPHEMU_HOST, coeffs.r_len, coeffs.t_len, d, order,
+                                   fit.model.phi.data(), fit.phi_se.data(), fit.residuals.data(), SPHEMU_HOST,
+                                   &fit.model.zeroed_count, &fit.model.unstable_count, &fit.residual_mean_norm));
+  return fit;
+}
+
 }  // namespace sphemu

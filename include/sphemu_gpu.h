@@ -247,6 +247,19 @@ int sphemu_gpu_emulate_range(sphemu_sht_t p, const double* v, int d, const doubl
                              const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed,
                              int r_begin, int r_count, int rng_mode, double* out);
 
+/* fit_var (stochastic.cpp:30-107, declared stochastic.hpp:41): per packed
+ * coefficient AR(order) least squares over an (r_len, t_len, d) coefficient
+ * series. phi / phi_se: order x d host (row p-1 = lag p; may be NULL);
+ * residuals: (r_len * (t_len - order)) x d (r_len * t_len rows for order 0),
+ * host or device — a device buffer feeds
+ * sphemu_gpu_estimate_innovation_covariance directly. Counts and the residual
+ * column-mean norm as VarModel::zeroed_count / unstable_count and
+ * VarFit::residual_mean_norm. SPHEMU_ERR_INVALID_ARG for order < 0 or > 16
+ * and t_len <= order (the reference's messages). */
+int sphemu_gpu_fit_var(const double* coeffs, int where_in, int r_len, int t_len, int64_t d, int order, double* phi,
+                       double* phi_se, double* residuals, int where_resid, int64_t* zeroed_count,
+                       int64_t* unstable_count, double* residual_mean_norm);
+
 /* ======================================================================
  * Trend mean structure (replaces trend.hpp:79-82 mean_table and
  * trend.hpp:71-76 detrend / retrend; trend.cpp:252-324)

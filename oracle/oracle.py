@@ -389,3 +389,70 @@ def trend_apply(mode, series, records, harmonics, period, forcing=None, t_start=
     if rc:
         raise ValueError("time steps are 1-based" if rc == -1 else "lagged forcing term needs history")
     return out.reshape(series.shape)
+
+
+def _fullpiv_rank(a, threshold=1e-13):
+    """Rank of Eigen's FullPivLU with setThreshold(threshold) (stochastic.cpp:72-74):
+    full pivoting, column-major first maximum, count |u_kk| > threshold * max pivot."""
+    a = np.array(a, dtype=np.float64)
+    n = a.shape[0]
+    maxpiv = 0.0
+    for k in range(n):
+        sub = np.abs(a[k:, k:])
+        flat = int(np.argmax(sub.T.ravel()))  # column-major scan
+        bj, bi = divmod(flat, n - k)
+        big = sub[bi, bj]
+        maxpiv = max(maxpiv, big)
+        if big == 0.0:
+            break
+        a[[k, k + bi]] = a[[k + bi, k]]
+        a[:, [k, k + bj]] = a[:, [k + bj, k]]
+        a[k + 1:, k] /= a[k, k]
+        a[k + 1:, k + 1:] -= np.outer(a[k + 1:, k], a[k, k + 1:])
+    return int(np.sum(np.abs(np.diag(a)) > threshold * maxpiv))
+
+
+def fit_var(coeffs, order):
+    """fit_var (stochastic.cpp:30-107) restated in numpy: per coefficient the
+    normal equations accumulated in (r, t) order, the rank rule of FullPivLU,
+    phi by a dense solve, residuals, OLS standard errors, and the unstable count
+    from the companion matrix eigenvalues (stochastic.cpp:19-27)."""
+    c = np.asarray(coeffs, dtype=np.float64)
+    r_len, t_len, d = c.shape
+    if order == 0:
+        mean = c.reshape(-1, d).sum(axis=0) / (r_len * t_len)
+        res = (c - mean).reshape(-1, d)
+        return dict(phi=np.zeros((0, d)), phi_se=np.zeros((0, d)), residuals=res, zeroed_count=0,
+                    unstable_count=0, residual_mean_norm=float(np.linalg.norm(res.mean(axis=0))))
+    rows = t_len - order
+    X = np.stack([c[:, order - 1 - p:t_len - 1 - p, :] for p in range(order)], axis=-1)  # (r, rows, d, P)
+    Y = c[:, order:, :]
+    phi = np.zeros((order, d))
+    se = np.zeros((order, d))
+    res = np.empty((r_len * rows, d))
+    zeroed = unstable = 0
+    n_rows = r_len * rows
+    for i in range(d):
+        x = X[:, :, i, :].reshape(-1, order)
+        y = Y[:, :, i].reshape(-1)
+        a = np.zeros((order, order))
+        b = np.zeros(order)
+        for row in range(x.shape[0]):  # sequential accumulation like Eigen's a += x x^T
+            a += np.outer(x[row], x[row])
+            b += x[row] * y[row]
+        degenerate = _fullpiv_rank(a) < order
+        ph = np.zeros(order) if degenerate else np.linalg.solve(a, b)
+        zeroed += degenerate
+        phi[:, i] = ph
+        e = y - x @ ph
+        res[:, i] = e
+        if not degenerate and n_rows > order:
+            s2 = float(e @ e) / (n_rows - order)
+            se[:, i] = np.sqrt(np.maximum(0.0, s2 * np.diag(np.linalg.inv(a))))
+        comp = np.zeros((order, order))
+        comp[0, :] = ph
+        comp[1:, :-1] += np.eye(order - 1)
+        rad = abs(ph[0]) if order == 1 else float(np.max(np.abs(np.linalg.eigvals(comp))))
+        unstable += rad >= 1.0 - 1e-8
+    return dict(phi=phi, phi_se=se, residuals=res, zeroed_count=int(zeroed), unstable_count=int(unstable),
+                residual_mean_norm=float(np.linalg.norm(res.mean(axis=0))))

@@ -132,6 +132,8 @@ def lib():
                                             C.c_int]
         L.sphemu_gpu_emulate_trend.argtypes = [vp, vp, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int, vp, i64, vp,
                                                i64, i64, vp, C.c_int, C.c_uint64, C.c_int, C.c_int, vp]
+        L.sphemu_gpu_fit_var.argtypes = [vp, C.c_int, C.c_int, C.c_int, i64, C.c_int, vp, vp, vp, C.c_int,
+                                         C.POINTER(i64), C.POINTER(i64), dp]
         L.sphemu_gpu_detrend.argtypes = trend
         L.sphemu_gpu_retrend.argtypes = trend
         _lib = L
@@ -584,3 +586,31 @@ def emulate_model(plan, v, phi, records, harmonics, period, v2, t_out, seed=1, r
                                           period, *fa, t_start, _ptr(v2), t_out, seed, r_len,
                                           {"reference": 0, "philox": 1}[rng], _ptr(out)))
     return out
+
+
+class VarFit:
+    """VarFit (stochastic.hpp:29-37): phi / phi_se are order x d (row p-1 is
+    lag p), residuals (r_len * (t_len - order)) x d, replicate-major."""
+
+    def __init__(self, phi, phi_se, residuals, zeroed_count, unstable_count, residual_mean_norm):
+        self.phi, self.phi_se, self.residuals = phi, phi_se, residuals
+        self.zeroed_count, self.unstable_count = zeroed_count, unstable_count
+        self.residual_mean_norm = residual_mean_norm
+
+
+def fit_var(coeffs, order):
+    """fit_var (stochastic.cpp:30-107) on the device: coeffs is the
+    (r_len, t_len, d) packed coefficient series (CoeffSeries, sht.hpp:45-69)."""
+    c = np.ascontiguousarray(coeffs, dtype=np.float64)
+    if c.ndim == 2:
+        c = c[None]
+    r_len, t_len, d = c.shape
+    rows = r_len * (t_len - order) if order > 0 else r_len * t_len
+    phi = np.zeros((max(order, 0), d))
+    se = np.zeros((max(order, 0), d))
+    res = np.empty((max(rows, 0), d))
+    zc, uc, nrm = C.c_int64(), C.c_int64(), C.c_double()
+    _check(lib().sphemu_gpu_fit_var(_ptr(c), HOST, r_len, t_len, d, order, _ptr(phi) if order > 0 else None,
+                                    _ptr(se) if order > 0 else None, _ptr(res), HOST, C.byref(zc), C.byref(uc),
+                                    C.byref(nrm)))
+    return VarFit(phi, se, res, zc.value, uc.value, nrm.value)

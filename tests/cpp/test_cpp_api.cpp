@@ -218,6 +218,17 @@ int main() {
     CHECK(mu < 1e-12 * mx && mv < 1e-12 * mx && m.nugget == 0.0);
   }
 
+  // fit_var: silent and explosive series (test_stochastic.cpp:144-157)
+  {
+    CoeffSeries coeffs(2, 400, 1);
+    for (int t = 0; t < 400; ++t) coeffs.slice(0, t)[0] = static_cast<double>(t + 1);
+    VarFit fit = fit_var(coeffs, 1);
+    CHECK(fit.model.zeroed_count == 3 && fit.model.unstable_count == 1);
+    CHECK(fit.model.phi_at(1, 0) > 1.0 && fit.model.phi_at(1, 1) == 0.0);
+    CHECK(fit.residual_rows == 399);
+    CHECK(throws<std::invalid_argument>([&] { fit_var(coeffs, 400); }));
+  }
+
   // trend mean structure (test_trend.cpp:165-206)
   {
     TrendModel m;
