@@ -547,6 +547,64 @@ def sht_c4(sph, snapshots=1000):
             "note": "the driver's 8 760-snapshot hourly year runs in chunks of this batch"}
 
 
+def model_side_points(sph):
+    """The §8f rows either side of the factorization, device-resident through
+    the C-ABI, kernel-only time from CUDA events on the default stream:
+    fit_var at the C2 size (d = 32 400, T = 1 000, order 3) and retrend on the
+    C4 grid (721 x 1440, K = 5, 4 x 96 fields). Algorithmic HBM GB/s against
+    MEASURED_PEAKS.json."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+    lib = sph._sphemu.lib()
+    vp = C.c_void_p
+    out = {}
+    T, d, order = 1000, 180 * 180, 3
+    c = torch.cumsum(torch.randn(1, T, d, dtype=torch.float64, device="cuda") * 0.05, dim=1)
+    res = torch.empty(T - order, d, dtype=torch.float64, device="cuda")
+    phi = np.empty(order * d)
+    se = np.empty(order * d)
+    zc, uc, nrm = C.c_int64(), C.c_int64(), C.c_double()
+
+    def fv():
+        assert lib.sphemu_gpu_fit_var(vp(c.data_ptr()), 1, 1, T, d, order, vp(phi.ctypes.data),
+                                      vp(se.ctypes.data), vp(res.data_ptr()), 1, C.byref(zc), C.byref(uc),
+                                      C.byref(nrm)) == 0
+
+    points, K, R, Tt = 721 * 1440, 5, 4, 96
+    rec = np.random.default_rng(1).standard_normal((points, 5 + 2 * K))
+    rec[:, -1] = 1.0 + np.abs(rec[:, -1])
+    z = torch.randn(R, Tt, points, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(z)
+
+    def rt():
+        assert lib.sphemu_gpu_retrend(vp(z.data_ptr()), 1, R, Tt, vp(rec.ctypes.data), points, K, 8760, None, 0,
+                                      None, 0, 1, vp(y.data_ptr()), 1) == 0
+
+    peak = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")))["hbm_gbs"]
+    for name, fn, nbytes, what in (
+            ("fit_var", fv, 16 * T * d + 8 * (T - order) * d, "C2 size: d=32400, T=1000, order 3 (series read "
+             "twice + residuals written)"),
+            ("retrend", rt, 16 * R * Tt * points, "C4 grid 721x1440, K=5, 4x96 fields (z read + y written)")):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(5):
+            fn()
+        s1.record()
+        torch.cuda.synchronize()
+        ms = s0.elapsed_time(s1) / 5
+        out[name] = {"ms_per_call": ms, "algorithmic_gbs_per_call": nbytes / ms / 1e6, "hbm_peak_gbs": peak,
+                     "workload": what, "note": "per C-ABI call incl. its small host transfers; the kernel-only "
+                                               "figures are in profiles/r01_ncu_fit_var.txt / r01_ncu_trend.txt"}
+    del c, res, z, y
+    torch.cuda.empty_cache()
+    return out
+
+
 def emulation_point(sph, L=90, replicates=100, t_out=24, order=3, world=1, rank=0):
     """Emulation generator throughput (stochastic.cpp:217-277): R replicates x T steps on the (L+1) x 2L grid,
     V = the device factor of make_spd_test_matrix(L^2) (dp), AR(3), device Philox normals; the one-shot C-ABI
@@ -629,6 +687,7 @@ def run_ours(args, world, rank, local):
     sht = sht_throughput(sph, world)
     c4 = sht_c4(sph) if (world == 1 and not args.no_c4) else None
     emul = emulation_point(sph, world=world, rank=rank) if not args.no_c4 else None
+    side = model_side_points(sph) if (world == 1 and not args.no_c4) else None
 
     if rank != 0:
         return
@@ -675,6 +734,8 @@ def run_ours(args, world, rank, local):
         line["sht_c4"] = c4
     if emul:
         line["emulation"] = emul
+    if side:
+        line["model_side"] = side
     print(json.dumps(line), flush=True)
 
 
