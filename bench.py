@@ -235,7 +235,7 @@ def run_reference(args, world, rank):
         "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 METRIC = "mixed-precision Cholesky TFLOP/s at 1/2/4/8 B200 (% of roofline); SHT snapshots/s"
@@ -736,10 +736,26 @@ def run_ours(args, world, rank, local):
         line["emulation"] = emul
     if side:
         line["model_side"] = side
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line, on the process's original stdout. Everything else
+    that native code writes to fd 1 (NCCL's version banner, library chatter)
+    is routed to stderr by main() so stdout carries exactly this line."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)

@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(kVarThreads) k_fit_var_fixed(const double* __r
     for (int t0 = P; t0 < t_len; t0 += kVarUnroll) {
       double yv[kVarUnroll];
 #pragma unroll
-      for (int u = 0; u < kVarUnroll; ++u) yv[u] = t0 + u < t_len ? ser(coeffs, d, t_len, r, t0 + u, idx) : 0.0;
+      for (int u = 0; u < kVarUnroll; ++u)  // clamped, unpredicated: independent loads in flight
+        yv[u] = ser(coeffs, d, t_len, r, min(t0 + u, t_len - 1), idx);
 #pragma unroll
       for (int u = 0; u < kVarUnroll; ++u) {
         if (t0 + u < t_len) {
@@ -226,7 +227,8 @@ __global__ void __launch_bounds__(kVarThreads) k_fit_var_fixed(const double* __r
     for (int t0 = P; t0 < t_len; t0 += kVarUnroll) {
       double yv[kVarUnroll];
 #pragma unroll
-      for (int u = 0; u < kVarUnroll; ++u) yv[u] = t0 + u < t_len ? ser(coeffs, d, t_len, r, t0 + u, idx) : 0.0;
+      for (int u = 0; u < kVarUnroll; ++u)  // clamped, unpredicated: independent loads in flight
+        yv[u] = ser(coeffs, d, t_len, r, min(t0 + u, t_len - 1), idx);
 #pragma unroll
       for (int u = 0; u < kVarUnroll; ++u) {
         if (t0 + u < t_len) {
