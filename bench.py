@@ -753,9 +753,6 @@ def emit(line):
 
 def main():
     global _JSON_OUT
-    sys.stdout.flush()
-    _JSON_OUT = os.fdopen(os.dup(1), "w")
-    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -772,6 +769,9 @@ def main():
     ap.add_argument("--lookahead", type=int, default=1)
     ap.add_argument("--sp-compute", default="fp16x3", choices=["fp16x3", "tf32x3"])
     args = ap.parse_args()
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, world, rank)
