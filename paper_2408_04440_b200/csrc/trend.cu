@@ -7,7 +7,7 @@
 // O(t_len) host work done here in the library (same libm, same operation
 // order as trend.cpp:258-277). The O(t_len * points) evaluation runs in one
 // HBM-bound kernel: a CTA owns 128 consecutive locations and a run of time
-// rows; the CTA's location records are staged once in shared memory with
+// rows; each thread keeps its location record in registers (loaded once,
 // coalesced loads and held in registers (compile-time harmonic count) for
 // every row, the rows' per-step scalars sit in shared memory (broadcast reads),
 // four rows' loads are in flight per thread, each row's output is written (and
@@ -116,15 +116,19 @@ __global__ void __launch_bounds__(kTrendThreads) k_trend(const double* __restric
   const int hk = K >= 0 ? K : harmonics;
   const int stride = 5 + 2 * hk;
   const int rp = 2 + 2 * hk;
+  // Compile-time K: each thread reads its own record straight into registers
+  // (the warp's 15 loads cover one contiguous span, served from L1), so shared
+  // memory only holds the rows' per-step scalars and occupancy stays high.
+  // Runtime K: the records are staged in shared memory first.
   double* s_rec = s_mem;
-  double* s_row = s_mem + kTrendThreads * stride;
+  double* s_row = K >= 0 ? s_mem : s_mem + kTrendThreads * stride;
   const int64_t loc0 = (int64_t)blockIdx.x * kTrendThreads;
   const int nloc = (int)(points - loc0 < kTrendThreads ? points - loc0 : kTrendThreads);
   const int64_t r_begin = row_base + (int64_t)blockIdx.y * kTrendRows;
   const int nr = (int)(r_begin + kTrendRows < n_rows ? kTrendRows : n_rows - r_begin);
-  // Coalesced stage of this CTA's records (contiguous nloc * stride doubles) and row scalars.
   const double* src = records + loc0 * stride;
-  for (int i = threadIdx.x; i < nloc * stride; i += kTrendThreads) s_rec[i] = src[i];
+  if (K < 0)
+    for (int i = threadIdx.x; i < nloc * stride; i += kTrendThreads) s_rec[i] = src[i];
   for (int i = threadIdx.x; i < nr * rp; i += kTrendThreads)
     s_row[i] = rowp[((r_begin + i / rp) % t_len) * rp + i % rp];
   __syncthreads();
@@ -135,13 +139,13 @@ __global__ void __launch_bounds__(kTrendThreads) k_trend(const double* __restric
   const double* rec = s_rec + threadIdx.x * stride;
   if constexpr (K >= 0) {
 #pragma unroll
-    for (int i = 0; i < kRegs; ++i) reg[i] = rec[i];
+    for (int i = 0; i < kRegs; ++i) reg[i] = __ldg(src + threadIdx.x * stride + i);
     rec = reg;
   }
   const double sigma = rec[stride - 1];
   const double* pin = in + r_begin * points + loc;
   double* pout = out + r_begin * points + loc;
-  constexpr int U = 4;  // rows in flight per thread
+  constexpr int U = 8;  // rows in flight per thread
   for (int j = 0; j < nr; j += U) {
     double x[U];
     if (MODE != kTable) {
@@ -165,10 +169,10 @@ template <int MODE>
 void launch_trend(dim3 grid, size_t smem, const double* rec, int64_t points, int harmonics, const double* rowp,
                   int wf, int t_len, int64_t row_base, int64_t n_rows, const double* in, double* out,
                   cudaStream_t stream = nullptr) {
+  const size_t smem_rows = (size_t)kTrendRows * (2 + 2 * harmonics) * sizeof(double);
 #define SPH_TREND_CASE(KK)                                                                                  \
   case KK:                                                                                                   \
-    SPH_CUDA(cudaFuncSetAttribute(k_trend<MODE, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_trend<MODE, KK><<<grid, kTrendThreads, smem, stream>>>(rec, points, harmonics, rowp, wf, t_len, row_base, \
+    k_trend<MODE, KK><<<grid, kTrendThreads, smem_rows, stream>>>(rec, points, harmonics, rowp, wf, t_len, row_base, \
                                                              n_rows,                                         \
                                                      in, out);                                               \
     break;
