@@ -6,12 +6,12 @@
 // forcing average of the shared rho, and the K seasonal cos/sin pairs) are
 // O(t_len) host work done here in the library (same libm, same operation
 // order as trend.cpp:258-277). The O(t_len * points) evaluation runs in one
-// HBM-bound kernel: a CTA owns 128 consecutive locations and a run of time
-// rows; each thread keeps its location record in registers (loaded once,
-// coalesced loads and held in registers (compile-time harmonic count) for
-// every row, the rows' per-step scalars sit in shared memory (broadcast reads),
-// four rows' loads are in flight per thread, each row's output is written (and
-// for detrend/retrend its input read) fully coalesced. Algorithmic bytes per
+// HBM-bound kernel: a CTA owns 128 consecutive locations and 128 time rows;
+// each thread loads its location record once into registers (compile-time
+// harmonic count; runtime counts stage the records in shared memory), the
+// rows' per-step scalars sit in shared memory (broadcast reads), eight rows'
+// loads are in flight per thread, and each row's output is written (and for
+// detrend/retrend its input read) fully coalesced. Algorithmic bytes per
 // element: 8 (table) or 16 (detrend / retrend). All arithmetic is explicit
 // round-to-nearest without FMA contraction, in the reference's expression
 // order, so the results are bitwise those of the reference's x86-64 Release
