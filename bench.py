@@ -577,9 +577,10 @@ def model_side_points(sph):
     rec[:, -1] = 1.0 + np.abs(rec[:, -1])
     z = torch.randn(R, Tt, points, dtype=torch.float64, device="cuda")
     y = torch.empty_like(z)
+    rec_d = torch.from_numpy(rec).cuda()  # device-resident records: read in place by the kernel
 
     def rt():
-        assert lib.sphemu_gpu_retrend(vp(z.data_ptr()), 1, R, Tt, vp(rec.ctypes.data), points, K, 8760, None, 0,
+        assert lib.sphemu_gpu_retrend(vp(z.data_ptr()), 1, R, Tt, vp(rec_d.data_ptr()), points, K, 8760, None, 0,
                                       None, 0, 1, vp(y.data_ptr()), 1) == 0
 
     peak = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")))["hbm_gbs"]
@@ -600,7 +601,7 @@ def model_side_points(sph):
         out[name] = {"ms_per_call": ms, "algorithmic_gbs_per_call": nbytes / ms / 1e6, "hbm_peak_gbs": peak,
                      "workload": what, "note": "per C-ABI call incl. its small host transfers; the kernel-only "
                                                "figures are in profiles/r01_ncu_fit_var.txt / r01_ncu_trend.txt"}
-    del c, res, z, y
+    del c, res, z, y, rec_d
     torch.cuda.empty_cache()
     return out
 

@@ -264,7 +264,9 @@ int sphemu_gpu_fit_var(const double* coeffs, int where_in, int r_len, int t_len,
  * Trend mean structure (replaces trend.hpp:79-82 mean_table and
  * trend.hpp:71-76 detrend / retrend; trend.cpp:252-324)
  * ====================================================================== */
-/* records: points x (5 + 2*harmonics) host doubles, TrendModel::values
+/* records: points x (5 + 2*harmonics) doubles, host or device (detected;
+ * device records stay in HBM, only the lag column and rho are read back),
+ * TrendModel::values
  * (beta0, beta1, beta2, rho, a_1..a_K, b_1..b_K, sigma; trend.hpp:37-59).
  * Forcing: ForcingTrajectory{x, history} (trend.hpp:24-35) as two host
  * arrays; n_x = n_history = 0 is the empty trajectory (no forcing terms).

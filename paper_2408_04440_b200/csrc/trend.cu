@@ -62,15 +62,11 @@ int64_t year_of(int64_t t, int period) { return (t + period - 1) / period; }  //
 
 // One row of per-step scalars: {x_t, lagged, cos(base), sin(base), ..., cos(K base), sin(K base)}
 // (trend.cpp:259-275). Throws like require_lag_history (trend.cpp:21-25).
-std::vector<double> row_params(const double* records, int64_t points, int harmonics, int period,
-                               const Forcing& f, int t_len, int64_t t_start) {
-  const int64_t stride = 5 + 2 * (int64_t)harmonics;
+std::vector<double> row_params(bool any_lag, double rho, int harmonics, int period, const Forcing& f, int t_len,
+                               int64_t t_start) {
   const int rp = 2 + 2 * harmonics;
   std::vector<double> out((size_t)t_len * rp, 0.0);
   const bool with_forcing = !f.empty();
-  bool any_lag = false;
-  if (with_forcing)
-    for (int64_t loc = 0; loc < points && !any_lag; ++loc) any_lag = records[loc * stride + 2] != 0.0;
   for (int row = 0; row < t_len; ++row) {
     const int64_t t = t_start + row;
     double* o = out.data() + (size_t)row * rp;
@@ -84,7 +80,7 @@ std::vector<double> row_params(const double* records, int64_t points, int harmon
       if (any_lag && !f.has_year(year - 1))
         throw std::invalid_argument("lagged forcing term needs history before year " + std::to_string(year));
       o[0] = f.at_year(year);
-      o[1] = f.lagged_mean(year, records[3]);  // rho is shared: record(0)[3]
+      o[1] = f.lagged_mean(year, rho);  // rho is shared: record(0)[3]
     }
   }
   return out;
@@ -101,6 +97,37 @@ __device__ __forceinline__ double eval_mean(const double* rec, const double* p, 
   for (int k = 0; k < (K >= 0 ? K : hk); ++k)
     m = __dadd_rn(m, __dadd_rn(__dmul_rn(rec[4 + k], p[2 + 2 * k]), __dmul_rn(rec[4 + hk + k], p[3 + 2 * k])));
   return m;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return pa.type == cudaMemoryTypeDevice;  // not Managed: with HMM, pageable host memory reports as managed
+}
+
+// The two record columns the host needs for the per-step scalars: whether any
+// location has a lag coefficient (require_lag_history) and the shared rho.
+// Device records: only column 2 and record(0)[3] cross PCIe.
+void lag_info(const double* records, bool dev, int64_t points, int64_t stride, bool with_forcing, bool& any_lag,
+              double& rho) {
+  any_lag = false;
+  rho = 0.0;
+  if (!with_forcing || points == 0) return;
+  std::vector<double> col;
+  const double* c2 = records + 2;
+  if (dev) {
+    col.resize(points);
+    SPH_CUDA(cudaMemcpy2D(col.data(), sizeof(double), records + 2, stride * sizeof(double), sizeof(double), points,
+                          cudaMemcpyDeviceToHost));
+    SPH_CUDA(cudaMemcpy(&rho, records + 3, sizeof(double), cudaMemcpyDeviceToHost));
+    for (int64_t loc = 0; loc < points && !any_lag; ++loc) any_lag = col[loc] != 0.0;
+  } else {
+    rho = records[3];
+    for (int64_t loc = 0; loc < points && !any_lag; ++loc) any_lag = c2[loc * stride] != 0.0;
+  }
 }
 
 // grid: x = location blocks of kTrendThreads, y = blocks of kTrendRows (r, t) rows.
@@ -209,11 +236,20 @@ void run_trend(const double* records, int64_t points, int harmonics, int period,
   const int64_t stride = 5 + 2 * (int64_t)harmonics;
   const size_t smem = ((size_t)kTrendThreads * stride + (size_t)kTrendRows * (2 + 2 * harmonics)) * sizeof(double);
   if (smem > 200 * 1024) throw std::invalid_argument("harmonics too large for the device trend kernel");
-  std::vector<double> rp = row_params(records, points, harmonics, period, f, t_len, t_start);
+  const bool rec_dev = is_device_ptr(records);
+  bool any_lag;
+  double rho;
+  lag_info(records, rec_dev, points, stride, !f.empty(), any_lag, rho);
+  std::vector<double> rp = row_params(any_lag, rho, harmonics, period, f, t_len, t_start);
   const int64_t n_rows = (int64_t)r_len * t_len;
   const size_t n_el = (size_t)n_rows * points;
-  DevBuf<double> d_rec((size_t)points * stride), d_rp(rp.size()), d_in, d_out;
-  SPH_CUDA(cudaMemcpy(d_rec.get(), records, sizeof(double) * points * stride, cudaMemcpyHostToDevice));
+  DevBuf<double> d_rec, d_rp(rp.size()), d_in, d_out;
+  const double* drec = records;
+  if (!rec_dev) {
+    d_rec.alloc((size_t)points * stride);
+    SPH_CUDA(cudaMemcpy(d_rec.get(), records, sizeof(double) * points * stride, cudaMemcpyHostToDevice));
+    drec = d_rec.get();
+  }
   SPH_CUDA(cudaMemcpy(d_rp.get(), rp.data(), sizeof(double) * rp.size(), cudaMemcpyHostToDevice));
   const double* din = in;
   if (MODE != kTable && where_in == SPHEMU_HOST) {
@@ -229,7 +265,7 @@ void run_trend(const double* records, int64_t points, int harmonics, int period,
   const int64_t gy = (n_rows + kTrendRows - 1) / kTrendRows;
   for (int64_t y0 = 0; y0 < gy; y0 += 65535) {
     const dim3 grid((unsigned)ceil_div(points, kTrendThreads), (unsigned)std::min<int64_t>(65535, gy - y0));
-    launch_trend<MODE>(grid, smem, d_rec.get(), points, harmonics, d_rp.get(), !f.empty(), t_len, y0 * kTrendRows,
+    launch_trend<MODE>(grid, smem, drec, points, harmonics, d_rp.get(), !f.empty(), t_len, y0 * kTrendRows,
                        n_rows, din, dout);
   }
   if (where_out == SPHEMU_HOST)
@@ -260,7 +296,10 @@ void mean_table_device(const double* records, int64_t points, int harmonics, int
   const int64_t stride = 5 + 2 * (int64_t)harmonics;
   const size_t smem = ((size_t)kTrendThreads * stride + (size_t)kTrendRows * (2 + 2 * harmonics)) * sizeof(double);
   if (smem > 200 * 1024) throw std::invalid_argument("harmonics too large for the device trend kernel");
-  std::vector<double> rp = row_params(records, points, harmonics, period, f, t_len, t_start);
+  bool any_lag;
+  double rho;
+  lag_info(records, false, points, stride, !f.empty(), any_lag, rho);
+  std::vector<double> rp = row_params(any_lag, rho, harmonics, period, f, t_len, t_start);
   d_rec.alloc((size_t)points * stride);
   d_rp.alloc(rp.size());
   SPH_CUDA(cudaMemcpyAsync(d_rec.get(), records, sizeof(double) * points * stride, cudaMemcpyHostToDevice, stream));

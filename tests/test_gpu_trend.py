@@ -58,3 +58,24 @@ def test_errors(sph):
     with pytest.raises(ValueError):
         sph.detrend(np.zeros((1, 4, 5)), records(4, 1), 1, 12)
     assert sph.mean_table(records(4, 1), 1, 12, 0, 1).shape == (0, 4)
+
+
+def test_device_records_match_host(sph, O):
+    """records may be a device pointer (detected): only the lag column and rho
+    cross PCIe; results identical to the host-records call."""
+    import ctypes as C
+
+    import torch
+    rec = records(5000, 3, lag=0.2)
+    x, hist = np.linspace(0.1, 1.0, 4), np.array([0.05])
+    y = np.random.default_rng(2).standard_normal((2, 30, 5000))
+    want = sph.retrend(y, rec, 3, 12, forcing=(x, hist), t_start=2)
+    d_rec = torch.from_numpy(rec).cuda()
+    lib = sph._sphemu.lib()
+    out = np.empty_like(y)
+    vp = C.c_void_p
+    rc = lib.sphemu_gpu_retrend(vp(y.ctypes.data), 0, 2, 30, vp(d_rec.data_ptr()), 5000, 3, 12, vp(x.ctypes.data),
+                                4, vp(hist.ctypes.data), 1, 2, vp(out.ctypes.data), 0)
+    assert rc == 0, lib.sphemu_gpu_last_error()
+    assert np.array_equal(out, want)
+    assert np.array_equal(want, O.trend_apply("retrend", y, rec, 3, 12, (x, hist), 2))
