@@ -176,6 +176,21 @@ inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) 
 
 int num_sms();
 
+// Grow-only device scratch reused across calls on this host thread and device
+// (the per-call buffers of the trend / fit_var entry points, which synchronize
+// before returning). Never freed: no CUDA calls from static destructors.
+template <class T>
+T* scratch(int slot, size_t count) {
+  static thread_local DevBuf<T>* bufs[4][16] = {};
+  int dev = 0;
+  SPH_CUDA(cudaGetDevice(&dev));
+  if (slot < 0 || slot >= 4 || dev < 0 || dev >= 16) throw Error(SPHEMU_ERR_RUNTIME, "scratch slot out of range");
+  DevBuf<T>*& b = bufs[slot][dev];
+  if (!b) b = new DevBuf<T>();
+  if (b->n < count) b->alloc(count);
+  return b->get();
+}
+
 // TrendModel records + ForcingTrajectory for emulate's trend-model overload
 // (trend.cu mean_table_device; trend.hpp:24-59).
 struct TrendArgs {

@@ -243,14 +243,15 @@ void run_trend(const double* records, int64_t points, int harmonics, int period,
   std::vector<double> rp = row_params(any_lag, rho, harmonics, period, f, t_len, t_start);
   const int64_t n_rows = (int64_t)r_len * t_len;
   const size_t n_el = (size_t)n_rows * points;
-  DevBuf<double> d_rec, d_rp(rp.size()), d_in, d_out;
+  DevBuf<double> d_in, d_out;
+  double* const d_rp = scratch<double>(1, rp.size());
   const double* drec = records;
   if (!rec_dev) {
-    d_rec.alloc((size_t)points * stride);
-    SPH_CUDA(cudaMemcpy(d_rec.get(), records, sizeof(double) * points * stride, cudaMemcpyHostToDevice));
-    drec = d_rec.get();
+    double* const d_rec = scratch<double>(2, (size_t)points * stride);
+    SPH_CUDA(cudaMemcpy(d_rec, records, sizeof(double) * points * stride, cudaMemcpyHostToDevice));
+    drec = d_rec;
   }
-  SPH_CUDA(cudaMemcpy(d_rp.get(), rp.data(), sizeof(double) * rp.size(), cudaMemcpyHostToDevice));
+  SPH_CUDA(cudaMemcpy(d_rp, rp.data(), sizeof(double) * rp.size(), cudaMemcpyHostToDevice));
   const double* din = in;
   if (MODE != kTable && where_in == SPHEMU_HOST) {
     d_in.alloc(n_el);
@@ -265,7 +266,7 @@ void run_trend(const double* records, int64_t points, int harmonics, int period,
   const int64_t gy = (n_rows + kTrendRows - 1) / kTrendRows;
   for (int64_t y0 = 0; y0 < gy; y0 += 65535) {
     const dim3 grid((unsigned)ceil_div(points, kTrendThreads), (unsigned)std::min<int64_t>(65535, gy - y0));
-    launch_trend<MODE>(grid, smem, drec, points, harmonics, d_rp.get(), !f.empty(), t_len, y0 * kTrendRows,
+    launch_trend<MODE>(grid, smem, drec, points, harmonics, d_rp, !f.empty(), t_len, y0 * kTrendRows,
                        n_rows, din, dout);
   }
   if (where_out == SPHEMU_HOST)

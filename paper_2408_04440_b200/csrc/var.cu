@@ -311,8 +311,9 @@ extern "C" int sphemu_gpu_fit_var(const double* coeffs, int where_in, int r_len,
     const size_t n_in = (size_t)r_len * t_len * d, n_res = (size_t)n_rows * d;
     // One device block for the small outputs: phi | se | column means | flags.
     const int64_t op = order > 0 ? order : 0;
-    DevBuf<double> dIn, dRes, dSmall((size_t)(2 * op + 2) * d);
-    double* dPhi = dSmall.get();
+    DevBuf<double> dIn, dRes;
+    double* const dSmall = scratch<double>(0, (size_t)(2 * op + 2) * d);
+    double* dPhi = dSmall;
     double* dSe = dPhi + op * d;
     double* dMean = dSe + op * d;
     int* dFlags = reinterpret_cast<int*>(dMean + d);
@@ -339,7 +340,7 @@ extern "C" int sphemu_gpu_fit_var(const double* coeffs, int where_in, int r_len,
     if (where_resid == SPHEMU_HOST)
       SPH_CUDA(cudaMemcpy(residuals, res, sizeof(double) * n_res, cudaMemcpyDeviceToHost));
     std::vector<double> small((size_t)(2 * op + 2) * d);
-    SPH_CUDA(cudaMemcpy(small.data(), dSmall.get(), sizeof(double) * small.size(), cudaMemcpyDeviceToHost));
+    SPH_CUDA(cudaMemcpy(small.data(), dSmall, sizeof(double) * small.size(), cudaMemcpyDeviceToHost));
     if (op > 0) {
       if (phi) std::copy(small.begin(), small.begin() + op * d, phi);
       if (phi_se) std::copy(small.begin() + op * d, small.begin() + 2 * op * d, phi_se);
