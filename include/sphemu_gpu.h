@@ -61,6 +61,8 @@ int64_t sphemu_gpu_launch_count(void);
 
 #define SPHEMU_SP_F16X3 0  /* SP-class updates: fp16 hi+lo split of row-scaled operands, kind::f16 */
 #define SPHEMU_SP_TF32X3 1 /* SP-class updates: 3xTF32 on kind::tf32 */
+#define SPHEMU_SP_FP64 2   /* SP-class panel + updates in FP64 DMMA: the oracle's arithmetic (mpchol.cpp:283-316)
+                              on SP tiles, tensor cores for the HP class only */
 
 /* MpCholConfig (mpchol.hpp:18-28) plus appended GPU fields whose zero values
  * keep reference behaviour. */
@@ -246,6 +248,29 @@ int sphemu_gpu_emulate_trend(sphemu_sht_t p, const double* v, int d, const doubl
 int sphemu_gpu_emulate_range(sphemu_sht_t p, const double* v, int d, const double* phi, int order,
                              const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed,
                              int r_begin, int r_count, int rng_mode, double* out);
+
+/* emulate(model, plan, forcing, t_out, seed, r_len) (stochastic.hpp:84-86;
+ * stochastic.cpp:217-277) with V = the device-resident tiled factor of h
+ * (after sphemu_gpu_chol_factor + wait; no dense V anywhere): each step's
+ * xi = V eta is a TRMM over the stored tiles at their storage precision —
+ * FP64 DMMA for DP tiles, tcgen05 for SP (fp16 hi/lo of the tile x eta's
+ * hi/lo) and HP tiles (the stored fp16/bf16 tile x eta's hi/lo), fp32 TMEM
+ * partial sums over <= 2048 of K added into FP64. Replicates
+ * [r_begin, r_begin + r_count) run in chunks that fit HBM. phi (order x d),
+ * means (t_out x points), sigma, v2 (points) host; out (r_count, t_out,
+ * n_theta, n_phi) host or device (where_out). Distributed handles: every rank
+ * calls collectively; the replicates are split in world contiguous balanced
+ * blocks (rank q: [r_begin + floor(q r_count / W), r_begin + floor((q+1) r_count / W))),
+ * each rank computes the partial product over its own tiles for every rank's
+ * chunk columns and the blocks are reduced onto their owners over NCCL; out
+ * receives this rank's block (rng_mode must be SPHEMU_RNG_PHILOX). */
+int sphemu_gpu_emulate_chol(sphemu_chol_t h, sphemu_sht_t plan, const double* phi, int order, const double* means,
+                            const double* sigma, const double* v2, int t_out, uint64_t seed, int r_begin,
+                            int r_count, int rng_mode, double* out, int where_out);
+/* The innovation product alone: xi (S x n) = eta (S x n) L^T over the
+ * handle's tiles (row-major, host or device); distributed handles all-reduce
+ * the partial products so every rank receives the full xi. */
+int sphemu_gpu_chol_trmm(sphemu_chol_t h, const double* eta, int where_in, int64_t S, double* xi, int where_out);
 
 /* fit_var (stochastic.cpp:30-107, declared stochastic.hpp:41): per packed
  * coefficient AR(order) least squares over an (r_len, t_len, d) coefficient

@@ -134,6 +134,9 @@ def lib():
                                                i64, i64, vp, C.c_int, C.c_uint64, C.c_int, C.c_int, vp]
         L.sphemu_gpu_fit_var.argtypes = [vp, C.c_int, C.c_int, C.c_int, i64, C.c_int, vp, vp, vp, C.c_int,
                                          C.POINTER(i64), C.POINTER(i64), dp]
+        L.sphemu_gpu_chol_trmm.argtypes = [vp, vp, C.c_int, i64, vp, C.c_int]
+        L.sphemu_gpu_emulate_chol.argtypes = [vp, vp, vp, C.c_int, vp, vp, vp, C.c_int, C.c_uint64, C.c_int,
+                                              C.c_int, C.c_int, vp, C.c_int]
         L.sphemu_gpu_detrend.argtypes = trend
         L.sphemu_gpu_retrend.argtypes = trend
         _lib = L
@@ -155,6 +158,12 @@ def _ptr(a: np.ndarray) -> C.c_void_p:
     return C.c_void_p(a.ctypes.data)
 
 
+# SP-class arithmetic (tensor mode): "fp16x3" row-scaled fp16 hi+lo on kind::f16
+# (default), "tf32x3" on kind::tf32, "fp64" the oracle's FP64 arithmetic on
+# the SP tiles (DMMA; exact parity with mpchol.cpp at ~6x the SP-class time).
+SP_COMPUTE = {"fp16x3": 0, "tf32x3": 1, "fp64": 2}
+
+
 def make_config(variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_fraction=0.05,
                 hp_format="fp16", compute="tensor", lookahead=0, sp_compute="fp16x3") -> CholConfig:
     if variant not in VARIANTS:
@@ -163,11 +172,11 @@ def make_config(variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_frac
         raise ValueError(f"unknown half-precision format: {hp_format}")
     if compute not in ("tensor", "fp64"):
         raise ValueError(f"unknown compute mode: {compute}")
-    if sp_compute not in ("fp16x3", "tf32x3"):
+    if sp_compute not in SP_COMPUTE:
         raise ValueError(f"unknown single-precision compute: {sp_compute}")
     return CholConfig(VARIANTS[variant], tile_size, band_width_dp, sp_fraction, workers,
                       1 if hp_format == "bf16" else 0, 0 if compute == "tensor" else 1, lookahead,
-                      0 if sp_compute == "fp16x3" else 1)
+                      SP_COMPUTE[sp_compute])
 
 
 # ---------------------------------------------------------------------------
@@ -223,6 +232,7 @@ class Cholesky:
                                compute, lookahead, sp_compute)
         h = C.c_void_p()
         self.rank = 0
+        self.dist = dist
         if dist is None:
             _check(lib().sphemu_gpu_chol_create(n, C.byref(self.cfg), C.byref(h)))
         else:
@@ -321,6 +331,34 @@ class Cholesky:
         _check(lib().sphemu_gpu_chol_residual_probe_spd(self.h, seed, n_vec, C.byref(out)))
         return out.value
 
+    def trmm(self, eta):
+        """xi = eta L^T (row per snapshot) over the stored tiles: the emulation
+        generator's innovation product alone (sphemu_gpu_chol_trmm)."""
+        eta = np.ascontiguousarray(eta, dtype=np.float64)
+        out = np.empty((eta.shape[0], self.n))
+        _check(lib().sphemu_gpu_chol_trmm(self.h, _ptr(eta), HOST, eta.shape[0], _ptr(out), HOST))
+        return out
+
+    def emulate(self, plan, phi, means, sigma, v2, t_out, seed=1, r_len=1, rng="philox", r_begin=0):
+        """emulate (stochastic.cpp:217-277) with V = this handle's tiled factor
+        (sphemu_gpu_emulate_chol); distributed handles return this rank's
+        contiguous block of the replicates."""
+        d = self.n
+        phi = np.zeros((0, d)) if phi is None else np.ascontiguousarray(phi, dtype=np.float64).reshape(-1, d)
+        phi_a = phi if phi.shape[0] else np.zeros((1, d))
+        means = np.ascontiguousarray(means, dtype=np.float64)
+        sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+        v2 = np.ascontiguousarray(v2, dtype=np.float64)
+        world = 1 if self.dist is None else self.dist[0] * self.dist[1]
+        rank = self.rank
+        lo = r_begin + (r_len * rank) // world
+        hi = r_begin + (r_len * (rank + 1)) // world
+        out = np.empty((hi - lo, t_out, plan.n_theta, plan.n_phi))
+        mode = {"reference": 0, "philox": 1}[rng]
+        _check(lib().sphemu_gpu_emulate_chol(self.h, plan.h, _ptr(phi_a), phi.shape[0], _ptr(means), _ptr(sigma),
+                                             _ptr(v2), t_out, seed, r_begin, r_len, mode, _ptr(out), HOST))
+        return out
+
 
 def emulate(plan, v, phi, means, sigma, v2, t_out, seed=1, r_len=1, rng="reference", r_begin=0):
     """emulate (stochastic.cpp:217-277) with the trend evaluated by the caller
@@ -346,10 +384,14 @@ def emulate(plan, v, phi, means, sigma, v2, t_out, seed=1, r_len=1, rng="referen
 
 def estimate_innovation_covariance(residuals, r_len, t_len, order, variant="dp", tile_size=128, workers=1,
                                    band_width_dp=1, sp_fraction=0.05, hp_format="fp16", compute="tensor",
-                                   lookahead=1, sp_compute="fp16x3"):
+                                   lookahead=1, sp_compute="fp64"):
     """estimate_innovation_covariance (stochastic.cpp:109-172) on the device:
     returns (u_hat, v, nugget, stats_json) like InnovationModel
-    (stochastic.hpp:36-42); residuals is the (r_len*(t_len-order)) x d matrix."""
+    (stochastic.hpp:36-42); residuals is the (r_len*(t_len-order)) x d matrix.
+
+    The nugget is a discrete decision taken on the factorization's success,
+    so the SP class defaults to its FP64 arithmetic here (the oracle's): the
+    fp16x3 tensor form may need a larger nugget on rank-deficient input."""
     xi = np.ascontiguousarray(residuals, dtype=np.float64)
     if xi.ndim != 2:
         raise ValueError("residuals must be a 2-D array")

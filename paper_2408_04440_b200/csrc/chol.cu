@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -30,10 +31,13 @@
 #include "chol_kernels.cuh"
 #include "cov_kernels.cuh"
 #include "potrf_coop.cuh"
+#include "emulate.cuh"
 #include "tc_gemm.cuh"
 #include "tcgen05.cuh"
+#include "trmm.cuh"
 
 namespace sphemu_gpu {
+void sht_plan_dims(void* plan, int* n_theta, int* n_phi, int* L);  // sht.cu
 
 #define SPH_NCCL(call)                                                                              \
   do {                                                                                              \
@@ -49,7 +53,56 @@ std::atomic<int64_t> g_launches{0};
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 void note_launch(int64_t n) { g_launches += n; }
+bool sync_check() {
+  static const bool on = [] {
+    const char* e = std::getenv("SPHEMU_SYNC_CHECK");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 int64_t launch_count() { return g_launches.load(); }
+
+namespace {
+struct ScratchKey {
+  std::thread::id tid;
+  int dev, slot;
+  bool operator<(const ScratchKey& o) const {
+    return std::tie(tid, dev, slot) < std::tie(o.tid, o.dev, o.slot);
+  }
+};
+std::mutex g_scratch_mu;
+std::map<ScratchKey, DevBuf<char>>& scratch_map() {
+  static auto* m = new std::map<ScratchKey, DevBuf<char>>();  // never destroyed: no CUDA calls at exit
+  return *m;
+}
+}  // namespace
+
+void* scratch_bytes(int slot, size_t bytes) {
+  if (slot < 0 || slot >= 8) throw Error(SPHEMU_ERR_RUNTIME, "scratch slot out of range");
+  int dev = 0;
+  SPH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  DevBuf<char>& b = scratch_map()[ScratchKey{std::this_thread::get_id(), dev, slot}];
+  if (b.n < bytes) b.alloc(bytes);
+  return b.get();
+}
+
+void smem_optin(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static auto* done = new std::map<std::pair<const void*, int>, int>();
+  int dev = 0;
+  SPH_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = (*done)[{kernel, dev}];
+  if (have >= bytes) return;
+  SPH_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  have = bytes;
+}
+
+void scratch_release_all() {
+  std::lock_guard<std::mutex> lk(g_scratch_mu);
+  scratch_map().clear();
+}
 
 int num_sms() {
   static int sms = [] {
@@ -71,6 +124,10 @@ void validate_config(const sphemu_chol_config& c) {
   if (c.variant < 0 || c.variant > 3) throw std::invalid_argument("unknown precision variant");
   if (c.hp_format != SPHEMU_HP_FP16 && c.hp_format != SPHEMU_HP_BF16)
     throw std::invalid_argument("unknown half-precision format");
+  if (c.compute != SPHEMU_COMPUTE_TENSOR && c.compute != SPHEMU_COMPUTE_FP64)
+    throw std::invalid_argument("unknown compute mode");
+  if (c.sp_compute < SPHEMU_SP_F16X3 || c.sp_compute > SPHEMU_SP_FP64)
+    throw std::invalid_argument("unknown single-precision compute");
 }
 
 // assign_precisions (mpchol.cpp:67-93): band tiles double; off-band tiles
@@ -927,10 +984,10 @@ struct Chol {
     for (int k = 0; k < nt; ++k) {
       plist_off[k] = static_cast<int64_t>(pl.size());
       for (int i = k + 1; i < nt; ++i)
-        if (pmap[tix(i, k)] == SPHEMU_PREC_DP && mine(i, k)) pl.push_back(make_int2(i, k));
+        if (fp64_class(pmap[tix(i, k)]) && mine(i, k)) pl.push_back(make_int2(i, k));
       plist_dp[k] = static_cast<int64_t>(pl.size()) - plist_off[k];
       for (int i = k + 1; i < nt; ++i)
-        if (pmap[tix(i, k)] != SPHEMU_PREC_DP && mine(i, k)) pl.push_back(make_int2(i, k));
+        if (!fp64_class(pmap[tix(i, k)]) && mine(i, k)) pl.push_back(make_int2(i, k));
       plist_lo[k] = static_cast<int64_t>(pl.size()) - plist_off[k] - plist_dp[k];
     }
     if (!pl.empty()) {
@@ -1094,6 +1151,14 @@ struct Chol {
     return on;
   }
 
+  // Classes whose panel TRSM and trailing updates run in FP64 (DMMA): the DP
+  // class always; the SP class too under SPHEMU_SP_FP64 (exact-parity mode:
+  // the tensor cores' truncating fp32 accumulation is what separates the
+  // fp16x3 / 3xTF32 SP results from the FP64 oracle on ill-conditioned input).
+  bool fp64_class(int cls) const {
+    return cls == SPHEMU_PREC_DP || (cls == SPHEMU_PREC_SP && cfg.sp_compute == SPHEMU_SP_FP64);
+  }
+
   void op_update(int k, int part, cudaStream_t s, int max_ctas) {
     const int set = k & 1;
     for (int cls = 0; cls < 3; ++cls) {
@@ -1102,17 +1167,12 @@ struct Chol {
       if (!cnt) continue;
       const int2* lst = lists.get() + list_off[slot];
       const int pu = prof_begin(kUpdDp + cls, s);
-      if (cls != SPHEMU_PREC_DP && cfg.compute == SPHEMU_COMPUTE_TENSOR) {
+      if (!fp64_class(cls) && cfg.compute == SPHEMU_COMPUTE_TENSOR) {
         tc_update(store(), k, cls, cfg.hp_format, lst, lrows.get() + list_off[slot], cnt, p64_[set].get(),
                   panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s));
       } else {
         if (b % D2_BM == 0 && !(part == 0 && chain_small_syrk())) {
-          static bool attr = false;
-          if (!attr) {
-            SPH_CUDA(cudaFuncSetAttribute(k_update_fp64_v2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)sizeof(D2Smem)));
-            attr = true;
-          }
+          smem_optin(reinterpret_cast<const void*>(k_update_fp64_v2), (int)sizeof(D2Smem));
           const int per = (b / D2_BM) * (b / D2_BN);
           k_update_fp64_v2<<<static_cast<unsigned>(cnt * per), D2_THREADS, sizeof(D2Smem), s>>>(
               store(), k, lst, p64_[set].get(), fail.get(), sat.get());
@@ -1318,12 +1378,8 @@ struct Chol {
 
   // Diagonal tile factor + inverse on a cooperative grid (potrf_coop.cuh).
   void launch_potrf(int k, cudaStream_t s) {
-    static bool attr = false;
     const size_t smem = potrf_coop_smem();
-    if (!attr) {
-      SPH_CUDA(cudaFuncSetAttribute(k_potrf_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
+    smem_optin(reinterpret_cast<const void*>(k_potrf_coop), (int)smem);
     const int nblk = (rows(k) + PC_BLK - 1) / PC_BLK;
     const int G = std::max(1, std::min(potrf_cap, nblk * (nblk + 1) / 2));
     double* dkk = reinterpret_cast<double*>(arena.get() + off[tix(k, k)]);
@@ -1347,6 +1403,153 @@ struct Chol {
     prof_fold();
     if (st) fill_stats(st, s);
     return f;
+  }
+
+  // ---- emulation: Xi = H L^T over the stored tiles (trmm.cu) ----------------
+  // Host plan per class, built on first use: DP tiles by band offset, SP / HP
+  // tiles as CSR rows (j, first row of the tile in the class's A tensor map).
+  struct TrmmPlan {
+    bool built = false;
+    std::vector<std::vector<int2>> dp_by_offset;
+    std::vector<DevBuf<int2>> d_dp;
+    std::vector<int> row_ptr[2];  // [0] SP, [1] HP
+    std::vector<int2> ent[2];
+    DevBuf<int> d_row_ptr[2];
+    DevBuf<int2> d_ent[2];
+    std::vector<int2> sp_tiles;
+    DevBuf<int2> d_sp_tiles;
+    DevBuf<uint16_t> sp_hi, sp_lo;  // fp16 split of the SP tiles (row-scaled), refreshed per call
+    CUtensorMap m_arena16{}, m_sp_hi{}, m_sp_lo{};
+    DevBuf<double> hp;
+    DevBuf<uint16_t> h16[2][2];  // [fmt fp16 / bf16][hi / lo]
+    int64_t h_cols = 0;
+  } tp;
+
+  void trmm_build() {
+    if (tp.built) return;
+    int max_off = 0;
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j <= i; ++j)
+        if (pmap[tix(i, j)] == SPHEMU_PREC_DP && mine(i, j)) max_off = std::max(max_off, i - j);
+    tp.dp_by_offset.assign(max_off + 1, {});
+    for (int i = 0; i < nt; ++i)
+      for (int j = 0; j <= i; ++j)
+        if (pmap[tix(i, j)] == SPHEMU_PREC_DP && mine(i, j)) tp.dp_by_offset[i - j].push_back(make_int2(i, j));
+    tp.d_dp.resize(tp.dp_by_offset.size());
+    for (size_t q = 0; q < tp.dp_by_offset.size(); ++q) {
+      const auto& v = tp.dp_by_offset[q];
+      if (v.empty()) continue;
+      tp.d_dp[q].alloc(v.size());
+      SPH_CUDA(cudaMemcpy(tp.d_dp[q].get(), v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    }
+    for (int c = 0; c < 2; ++c) {
+      const int cls = c == 0 ? SPHEMU_PREC_SP : SPHEMU_PREC_HP;
+      tp.row_ptr[c].assign(nt + 1, 0);
+      tp.ent[c].clear();
+      for (int i = 0; i < nt; ++i) {
+        tp.row_ptr[c][i] = static_cast<int>(tp.ent[c].size());
+        for (int j = 0; j < i; ++j) {
+          if (pmap[tix(i, j)] != cls || !mine(i, j)) continue;
+          int arow;
+          if (c == 0) {
+            arow = static_cast<int>(tp.sp_tiles.size()) * b;
+            tp.sp_tiles.push_back(make_int2(i, j));
+          } else {
+            arow = static_cast<int>(off[tix(i, j)] / (2 * static_cast<int64_t>(b)));
+          }
+          tp.ent[c].push_back(make_int2(j, arow));
+        }
+      }
+      tp.row_ptr[c][nt] = static_cast<int>(tp.ent[c].size());
+      tp.d_row_ptr[c].alloc(nt + 1);
+      SPH_CUDA(cudaMemcpy(tp.d_row_ptr[c].get(), tp.row_ptr[c].data(), (nt + 1) * sizeof(int),
+                          cudaMemcpyHostToDevice));
+      if (!tp.ent[c].empty()) {
+        tp.d_ent[c].alloc(tp.ent[c].size());
+        SPH_CUDA(cudaMemcpy(tp.d_ent[c].get(), tp.ent[c].data(), tp.ent[c].size() * sizeof(int2),
+                            cudaMemcpyHostToDevice));
+      }
+    }
+    if (!tp.sp_tiles.empty()) {
+      tp.d_sp_tiles.alloc(tp.sp_tiles.size());
+      SPH_CUDA(cudaMemcpy(tp.d_sp_tiles.get(), tp.sp_tiles.data(), tp.sp_tiles.size() * sizeof(int2),
+                          cudaMemcpyHostToDevice));
+      const size_t el = tp.sp_tiles.size() * static_cast<size_t>(b) * b;
+      tp.sp_hi.alloc(el);
+      tp.sp_lo.alloc(el);
+      const int64_t rows = static_cast<int64_t>(tp.sp_tiles.size()) * b;
+      tp.m_sp_hi = make_map_strided(tp.sp_hi.get(), rows, b, 2 * static_cast<int64_t>(b), 2, 128);
+      tp.m_sp_lo = make_map_strided(tp.sp_lo.get(), rows, b, 2 * static_cast<int64_t>(b), 2, 128);
+    }
+    tp.m_arena16 = make_map_strided(arena.get(), static_cast<int64_t>(arena.n) / (2 * b), b,
+                                    2 * static_cast<int64_t>(b), 2, 128);
+    tp.built = true;
+  }
+
+  // Xi (S x n, row-major FP64) = H (S x n) L^T on stream s, over the tiles
+  // this rank stores (the caller reduces across ranks). The factorization
+  // must have been enqueued (and waited for) before.
+  void trmm(const double* eta, int64_t S, double* xi, cudaStream_t s) {
+    if (!factored) throw std::invalid_argument("the handle holds no factor: call factor() and wait() first");
+    trmm_build();
+    SPH_CUDA(cudaStreamWaitEvent(s, ev1, 0));
+    const int64_t ldh = static_cast<int64_t>(nt) * b;
+    const bool fp16_hp = cfg.hp_format != SPHEMU_HP_BF16;
+    const bool need_bf = !fp16_hp && !tp.ent[1].empty();
+    if (tp.h_cols < S) {
+      tp.hp.alloc(static_cast<size_t>(S) * ldh);
+      for (int f = 0; f < 2; ++f)
+        for (int h = 0; h < 2; ++h) tp.h16[f][h].release();
+      tp.h_cols = S;
+    }
+    for (int f = 0; f < (need_bf ? 2 : 1); ++f)
+      if (!tp.h16[f][0].get())
+        for (int h = 0; h < 2; ++h) tp.h16[f][h].alloc(static_cast<size_t>(tp.h_cols) * ldh);
+    // eta -> padded FP64 (the DP operand) + its fp16 (and bf16) hi/lo splits
+    trmm_prep_eta(eta, S, n, lb, b, nt, tp.hp.get(), tp.h16[0][0].get(), tp.h16[0][1].get(), 0, s);
+    if (need_bf) trmm_prep_eta(eta, S, n, lb, b, nt, tp.hp.get(), tp.h16[1][0].get(), tp.h16[1][1].get(), 1, s);
+    SPH_CUDA(cudaMemsetAsync(xi, 0, static_cast<size_t>(S) * n * sizeof(double), s));
+    // DP tiles, one band offset per launch (deterministic FP64 order)
+    for (size_t q = 0; q < tp.dp_by_offset.size(); ++q)
+      if (!tp.dp_by_offset[q].empty())
+        trmm_dp_launch(store(), tp.d_dp[q].get(), static_cast<int64_t>(tp.dp_by_offset[q].size()), tp.hp.get(), ldh,
+                       S, xi, s);
+    static const int flush_env = [] {
+      const char* e = std::getenv("SPHEMU_TRMM_FLUSH_K");
+      return e ? std::atoi(e) : 2048;
+    }();
+    const int flush = std::max(1, flush_env / b);
+    for (int c = 0; c < 2; ++c) {
+      if (tp.ent[c].empty()) continue;
+      if (c == 0)
+        trmm_prep_sp(store(), tp.d_sp_tiles.get(), static_cast<int64_t>(tp.sp_tiles.size()), rowexp.get(),
+                     tp.sp_hi.get(), tp.sp_lo.get(), s);
+      // items: (tile row, 128-row block, 256-snapshot block), longest rows first
+      std::vector<std::pair<int, int4>> its;
+      const int mblk = (lb + 127) / 128;
+      const int nblk = static_cast<int>((S + 255) / 256);
+      for (int i = 0; i < nt; ++i) {
+        const int cnt = tp.row_ptr[c][i + 1] - tp.row_ptr[c][i];
+        if (!cnt) continue;
+        for (int mb = 0; mb < mblk; ++mb) {
+          if (mb * 128 >= rows(i)) continue;
+          for (int nb = 0; nb < nblk; ++nb) its.push_back({cnt, make_int4(i, mb * 128, nb * 256, 0)});
+        }
+      }
+      std::stable_sort(its.begin(), its.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+      std::vector<int4> items(its.size());
+      for (size_t e = 0; e < its.size(); ++e) items[e] = its[e].second;
+      DevBuf<int4> d_items(items.size());
+      SPH_CUDA(cudaMemcpyAsync(d_items.get(), items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice, s));
+      const int f = (c == 1 && !fp16_hp) ? 1 : 0;
+      const CUtensorMap mh = make_map_strided(tp.h16[f][0].get(), S, ldh, 2 * ldh, 2, 256);
+      const CUtensorMap ml = make_map_strided(tp.h16[f][1].get(), S, ldh, 2 * ldh, 2, 256);
+      TrmmArgs a{tp.d_row_ptr[c].get(), tp.d_ent[c].get(), d_items.get(), static_cast<int64_t>(items.size()), b, lb,
+                 n, S, xi, c == 0 ? rowexp.get() : nullptr, flush};
+      const int opk = c == 0 ? TR_F16X3 : (fp16_hp ? TR_F16 : TR_BF16);
+      trmm_tc_launch(opk, c == 0 ? tp.m_sp_hi : tp.m_arena16, c == 0 ? tp.m_sp_lo : tp.m_arena16, mh, ml, a, s);
+      SPH_CUDA(cudaStreamSynchronize(s));  // d_items and the host vectors go out of scope
+    }
   }
 
   void fill_stats(sphemu_chol_stats* st, unsigned saturations) const {
@@ -1760,6 +1963,7 @@ int sphemu_gpu_release_cache(void) {
     std::lock_guard<std::mutex> lk(g_dense_mu);
     g_dense.reset();
     g_dense_dev = -1;
+    scratch_release_all();
   });
 }
 
@@ -1820,11 +2024,7 @@ int sphemu_gpu_estimate_innovation_covariance(const double* resid, int where_res
       u_dev.alloc(static_cast<size_t>(d) * d);
       U = u_dev.get();
     }
-    static bool attr = false;
-    if (!attr) {
-      SPH_CUDA(cudaFuncSetAttribute(k_cov_syrk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(D2Smem)));
-      attr = true;
-    }
+    smem_optin(reinterpret_cast<const void*>(k_cov_syrk), (int)sizeof(D2Smem));
     k_cov_syrk<<<dim3(static_cast<unsigned>((d + D2_BN - 1) / D2_BN), static_cast<unsigned>((d + D2_BM - 1) / D2_BM)),
                  D2_THREADS, sizeof(D2Smem)>>>(xt.get(), ldt, n_rows, d, 1.0 / static_cast<double>(n_rows), U);
     SPH_LAUNCH_CHECK();
@@ -1854,6 +2054,85 @@ int sphemu_gpu_estimate_innovation_covariance(const double* resid, int where_res
     if (v) c.store_dense(v, where_v, d);
     if (u_hat && where_u == SPHEMU_HOST)
       SPH_CUDA(cudaMemcpy(u_hat, U, sizeof(double) * d * d, cudaMemcpyDeviceToHost));
+  });
+}
+
+int sphemu_gpu_chol_trmm(sphemu_chol_t h, const double* eta, int where_in, int64_t S, double* xi, int where_out) {
+  return guard([&] {
+    if (!h) throw std::invalid_argument("null handle");
+    if (S < 1) throw std::invalid_argument("need at least one column");
+    Chol& c = *h->c;
+    const size_t el = static_cast<size_t>(S) * c.n;
+    DevBuf<double> de, dx;
+    const double* e = eta;
+    if (where_in == SPHEMU_HOST) {
+      de.alloc(el);
+      SPH_CUDA(cudaMemcpyAsync(de.get(), eta, el * sizeof(double), cudaMemcpyHostToDevice, c.stream));
+      e = de.get();
+    }
+    double* x = xi;
+    if (where_out == SPHEMU_HOST) {
+      dx.alloc(el);
+      x = dx.get();
+    }
+    c.trmm(e, S, x, c.stream);
+    if (c.dist()) SPH_NCCL(ncclAllReduce(x, x, el, ncclFloat64, ncclSum, c.comm, c.stream));
+    if (where_out == SPHEMU_HOST)
+      SPH_CUDA(cudaMemcpyAsync(xi, x, el * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    SPH_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int sphemu_gpu_emulate_chol(sphemu_chol_t h, sphemu_sht_t plan, const double* phi, int order, const double* means,
+                            const double* sigma, const double* v2, int t_out, uint64_t seed, int r_begin,
+                            int r_count, int rng_mode, double* out, int where_out) {
+  return guard([&] {
+    if (!h || !plan) throw std::invalid_argument("null handle");
+    Chol& c = *h->c;
+    EmulArgs a{};
+    a.plan = plan;
+    sht_plan_dims(plan, &a.n_theta, &a.n_phi, &a.L);
+    a.d = c.n;
+    a.phi = phi;
+    a.order = order;
+    a.means = means;
+    a.sigma = sigma;
+    a.v2 = v2;
+    a.t_out = t_out;
+    a.seed = seed;
+    a.r_begin = r_begin;
+    a.r_len = r_count;
+    a.rng_mode = rng_mode;
+    a.out = out;
+    a.where_out = where_out;
+    a.world = c.P * c.Q;
+    a.rank = c.rank;
+    static const int64_t budget = [] {
+      const char* e = std::getenv("SPHEMU_EMUL_CHUNK_MB");
+      return e ? (int64_t)std::atoll(e) << 20 : int64_t{0};
+    }();
+    a.chunk_bytes = budget;
+    DevBuf<double> part;
+    emulate_core(a, [&](const double* dH, int64_t S_all, const std::vector<int64_t>& col_off, double* dXi,
+                        cudaStream_t s) {
+      if (!c.dist()) {
+        c.trmm(dH, S_all, dXi, s);
+        return;
+      }
+      // partial product over this rank's tiles for every rank's columns, then
+      // each rank's column block summed onto it (reduce-scatter by replicates)
+      const size_t el = static_cast<size_t>(S_all) * c.n;
+      if (part.n < el) part.alloc(el);
+      c.trmm(dH, S_all, part.get(), s);
+      SPH_NCCL(ncclGroupStart());
+      for (int q = 0; q < c.P * c.Q; ++q) {
+        const size_t cnt = static_cast<size_t>(col_off[q + 1] - col_off[q]) * c.n;
+        if (!cnt) continue;
+        SPH_NCCL(ncclReduce(part.get() + col_off[q] * c.n, dXi, cnt, ncclFloat64, ncclSum, q, c.comm, s));
+      }
+      SPH_NCCL(ncclGroupEnd());
+      note_launch();
+    });
   });
 }
 

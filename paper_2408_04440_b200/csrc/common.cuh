@@ -35,13 +35,17 @@ int64_t launch_count();
                                                      cudaGetErrorString(err__));          \
   } while (0)
 
+// SPHEMU_SYNC_CHECK=1 (debugging): every launch is followed by a device
+// synchronize, so an asynchronous fault is reported at the kernel that raised it.
+bool sync_check();
 #define SPH_LAUNCH_CHECK()                                                                 \
   do {                                                                                     \
     ::sphemu_gpu::note_launch();                                                           \
     cudaError_t err__ = cudaGetLastError();                                                \
+    if (err__ == cudaSuccess && ::sphemu_gpu::sync_check()) err__ = cudaDeviceSynchronize(); \
     if (err__ != cudaSuccess)                                                              \
-      throw ::sphemu_gpu::Error(SPHEMU_ERR_CUDA,                                           \
-                                std::string("kernel launch: ") + cudaGetErrorString(err__)); \
+      throw ::sphemu_gpu::Error(SPHEMU_ERR_CUDA, std::string("kernel launch (") + __FILE__ + \
+                                ":" + std::to_string(__LINE__) + "): " + cudaGetErrorString(err__)); \
   } while (0)
 
 // Runs f and converts exceptions to C-ABI status codes.
@@ -176,19 +180,21 @@ inline int ceil_div(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) 
 
 int num_sms();
 
-// Grow-only device scratch reused across calls on this host thread and device
-// (the per-call buffers of the trend / fit_var entry points, which synchronize
-// before returning). Never freed: no CUDA calls from static destructors.
+// Grow-only device scratch reused across calls, one set of slots per (host
+// thread, device) (the per-call buffers of the trend / fit_var entry points,
+// which synchronize before returning). The buffers live in a process-wide,
+// mutex-guarded registry so sphemu_gpu_release_cache() frees them (also those
+// of threads that have exited); callers must not run entry points
+// concurrently with that release.
+void* scratch_bytes(int slot, size_t bytes);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// the opt-in is per device context, so a process driving several GPUs needs it
+// on each.
+void smem_optin(const void* kernel, int bytes);
+void scratch_release_all();
 template <class T>
 T* scratch(int slot, size_t count) {
-  static thread_local DevBuf<T>* bufs[4][16] = {};
-  int dev = 0;
-  SPH_CUDA(cudaGetDevice(&dev));
-  if (slot < 0 || slot >= 4 || dev < 0 || dev >= 16) throw Error(SPHEMU_ERR_RUNTIME, "scratch slot out of range");
-  DevBuf<T>*& b = bufs[slot][dev];
-  if (!b) b = new DevBuf<T>();
-  if (b->n < count) b->alloc(count);
-  return b->get();
+  return static_cast<T*>(scratch_bytes(slot, count * sizeof(T)));
 }
 
 // TrendModel records + ForcingTrajectory for emulate's trend-model overload

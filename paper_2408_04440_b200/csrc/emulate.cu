@@ -16,13 +16,16 @@
 // stochastic.cpp:230-259), generated on the host because that stream is
 // serial by definition; SPHEMU_RNG_PHILOX draws counter-based normals on the
 // device.
+#include <algorithm>
 #include <cmath>
+#include <memory>
 #include <random>
 #include <vector>
 
 #include "common.cuh"
 #include "dgemm.cuh"
 #include "dgemm2.cuh"
+#include "emulate.cuh"
 
 namespace sphemu_gpu {
 
@@ -144,72 +147,131 @@ struct RefGaussian {
   }
 };
 
+void emulate_core(const EmulArgs& a, const XiFn& xi_fn) {
+  if (a.r_begin < 0) throw std::invalid_argument("first replicate must be >= 0");
+  if (a.t_out < 1 || a.r_len < 1) throw std::invalid_argument("need t_out, r_len >= 1");
+  if (a.d != a.L * a.L) throw std::invalid_argument("transform plan does not match the model");
+  if (a.order < 0 || a.order > 16) throw std::invalid_argument("lag order must lie in [0, 16]");
+  const int W = std::max(1, a.world);
+  if (W > 1 && a.rng_mode == SPHEMU_RNG_REFERENCE)
+    throw std::invalid_argument("the reference's serial RNG stream cannot be split over ranks: use rng='philox'");
+  const int d = a.d;
+  const int burn = 10 * a.order;  // stochastic.cpp:17,227
+  const int64_t steps = burn + a.t_out;
+  const int64_t points = (int64_t)a.n_theta * a.n_phi;
+  cudaStream_t s = nullptr;
+  sht_inverse_device(a.plan, nullptr, 0, nullptr, &s);  // fetch the plan's stream
+  std::vector<int> lo(W), cnt(W);
+  int cnt_max = 0;
+  for (int q = 0; q < W; ++q) {
+    int l, h;
+    emul_share(a.r_begin, a.r_len, W, q, l, h);
+    lo[q] = l;
+    cnt[q] = h - l;
+    cnt_max = std::max(cnt_max, cnt[q]);
+  }
+  const int mine = cnt[a.rank];
+  // Replicates run in chunks whose buffers fit the budget: per snapshot
+  // column the normals of every rank (8 d W), the innovations and the
+  // tiled product's padded operands (~32 d), the kept draws, fields and eps.
+  const int64_t col_bytes = (int64_t)d * (8 * W + 32) + points * 8 * 2;
+  const int64_t budget = a.chunk_bytes > 0 ? a.chunk_bytes : (int64_t{8} << 30);
+  const int rc = (int)std::max<int64_t>(1, std::min<int64_t>(cnt_max, budget / std::max<int64_t>(1, col_bytes * steps)));
+  const int n_chunks = (cnt_max + rc - 1) / rc;
+  const int64_t ymax = (int64_t)rc * a.t_out * points;
+  DevBuf<double> dH((size_t)W * rc * steps * d), dXi((size_t)rc * steps * d), dDraws((size_t)rc * a.t_out * d);
+  DevBuf<double> dEps(ymax), dSynth(ymax), dMeans((size_t)a.t_out * points), dSigma(points), dV2(points),
+      dPhi(a.order > 0 ? (size_t)a.order * d : 1);
+  DevBuf<double> dTrendRec, dTrendRows;
+  if (a.trend) {  // stochastic.cpp:229: mean_table(model.trend, forcing, t_out, t_start), on the device
+    const TrendArgs& t = *a.trend;
+    mean_table_device(t.records, points, t.harmonics, t.period, t.fx, t.nx, t.fh, t.nh, a.t_out, t.t_start,
+                      dMeans.get(), dSigma.get(), s, dTrendRec, dTrendRows);
+  } else {
+    SPH_CUDA(cudaMemcpyAsync(dMeans.get(), a.means, (size_t)a.t_out * points * sizeof(double), cudaMemcpyHostToDevice,
+                             s));
+    SPH_CUDA(cudaMemcpyAsync(dSigma.get(), a.sigma, points * sizeof(double), cudaMemcpyHostToDevice, s));
+  }
+  SPH_CUDA(cudaMemcpyAsync(dV2.get(), a.v2, points * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (a.order > 0)
+    SPH_CUDA(cudaMemcpyAsync(dPhi.get(), a.phi, (size_t)a.order * d * sizeof(double), cudaMemcpyHostToDevice, s));
+  std::vector<double> hH, hE;
+  std::unique_ptr<RefGaussian> g;
+  if (a.rng_mode == SPHEMU_RNG_REFERENCE) {
+    g.reset(new RefGaussian(a.seed));
+    for (int r = 0; r < a.r_begin; ++r)  // one serial stream: skip the replicates drawn elsewhere
+      for (int64_t e = 0; e < steps * d + (int64_t)a.t_out * points; ++e) g->normal();
+    hH.resize((size_t)rc * steps * d);
+    hE.resize(ymax);
+  }
+  std::vector<int64_t> col_off(W + 1);
+  for (int c = 0; c < n_chunks; ++c) {
+    col_off[0] = 0;
+    for (int q = 0; q < W; ++q)
+      col_off[q + 1] = col_off[q] + (int64_t)std::max(0, std::min(rc, cnt[q] - c * rc)) * steps;
+    const int nr = (int)((col_off[a.rank + 1] - col_off[a.rank]) / steps);
+    const int64_t ytot = (int64_t)nr * a.t_out * points;
+    if (g) {
+      // Exact reference order: per replicate, (burn + t_out) x d innovations,
+      // then t_out x points small-scale normals.
+      SPH_CUDA(cudaStreamSynchronize(s));  // the staging vectors are reused per chunk
+      for (int r = 0; r < nr; ++r) {
+        double* h = hH.data() + (size_t)r * steps * d;
+        for (int64_t e = 0; e < steps * d; ++e) h[e] = g->normal();
+        double* ep = hE.data() + (size_t)r * a.t_out * points;
+        for (int64_t e = 0; e < (int64_t)a.t_out * points; ++e) ep[e] = g->normal();
+      }
+      SPH_CUDA(cudaMemcpyAsync(dH.get(), hH.data(), (size_t)nr * steps * d * sizeof(double), cudaMemcpyHostToDevice,
+                               s));
+      SPH_CUDA(cudaMemcpyAsync(dEps.get(), hE.data(), ytot * sizeof(double), cudaMemcpyHostToDevice, s));
+    } else {
+      for (int q = 0; q < W; ++q) {
+        const int nq = (int)((col_off[q + 1] - col_off[q]) / steps);
+        if (!nq) continue;
+        k_philox_normals<<<4 * num_sms(), 256, 0, s>>>(a.seed, 1, steps * d, lo[q] + c * rc, nq,
+                                                        dH.get() + col_off[q] * d);
+        SPH_LAUNCH_CHECK();
+      }
+      if (nr) {
+        k_philox_normals<<<4 * num_sms(), 256, 0, s>>>(a.seed, 2, (int64_t)a.t_out * points, lo[a.rank] + c * rc, nr,
+                                                        dEps.get());
+        SPH_LAUNCH_CHECK();
+      }
+    }
+    xi_fn(dH.get(), col_off[W], col_off, dXi.get(), s);
+    if (!nr) continue;
+    k_emul_ar<<<dim3(ceil_div(d, 128), nr), 128, 0, s>>>(dXi.get(), dPhi.get(), a.order, d, burn, a.t_out, nr,
+                                                          dDraws.get());
+    SPH_LAUNCH_CHECK();
+    sht_inverse_device(a.plan, dDraws.get(), (int64_t)nr * a.t_out, dSynth.get(), nullptr);
+    k_emul_retrend<<<8 * num_sms(), 256, 0, s>>>(dSynth.get(), dEps.get(), dMeans.get(), dSigma.get(), dV2.get(),
+                                                  points, a.t_out, ytot, dEps.get());
+    SPH_LAUNCH_CHECK();
+    double* dst = a.out + (int64_t)c * rc * a.t_out * points;
+    SPH_CUDA(cudaMemcpyAsync(dst, dEps.get(), ytot * sizeof(double),
+                             a.where_out == SPHEMU_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  }
+  (void)mine;
+  SPH_CUDA(cudaStreamSynchronize(s));
+}
+
+// The dense-V form (sphemu_gpu_emulate*): V uploaded once per call, Xi = H V^T by DMMA.
 void emulate(void* plan, int n_theta, int n_phi, int L, const double* v, int d, const double* phi, int order,
              const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed, int r_len,
              int rng_mode, double* out, int r_begin, const TrendArgs* trend) {
-  if (r_begin < 0) throw std::invalid_argument("first replicate must be >= 0");
-  if (t_out < 1 || r_len < 1) throw std::invalid_argument("need t_out, r_len >= 1");
-  if (d != L * L) throw std::invalid_argument("transform plan does not match the model");
-  if (order < 0 || order > 16) throw std::invalid_argument("lag order must lie in [0, 16]");
-  const int burn = 10 * order;  // stochastic.cpp:17,227
-  const int64_t steps = burn + t_out;
-  const int64_t S = (int64_t)r_len * steps;
-  const int64_t points = (int64_t)n_theta * n_phi;
-  const int64_t ytot = (int64_t)r_len * t_out * points;
+  EmulArgs a{plan, n_theta, n_phi, L, d, phi, order, means, sigma, v2, t_out, seed, r_begin, r_len, rng_mode,
+             out, SPHEMU_HOST, trend, 0};
   cudaStream_t s = nullptr;
-  sht_inverse_device(plan, nullptr, 0, nullptr, &s);  // fetch the plan's stream
-  DevBuf<double> dV((size_t)d * d), dH((size_t)S * d), dXi((size_t)S * d), dDraws((size_t)r_len * t_out * d);
-  DevBuf<double> dEps(ytot), dSynth(ytot), dMeans((size_t)t_out * points), dSigma(points), dV2(points),
-      dPhi(order > 0 ? (size_t)order * d : 1);
+  sht_inverse_device(plan, nullptr, 0, nullptr, &s);
+  if (d != L * L) throw std::invalid_argument("transform plan does not match the model");
+  DevBuf<double> dV((size_t)d * d);
   SPH_CUDA(cudaMemcpyAsync(dV.get(), v, (size_t)d * d * sizeof(double), cudaMemcpyHostToDevice, s));
-  DevBuf<double> dTrendRec, dTrendRows;
-  if (trend) {  // stochastic.cpp:229: mean_table(model.trend, forcing, t_out, t_start), on the device
-    mean_table_device(trend->records, points, trend->harmonics, trend->period, trend->fx, trend->nx, trend->fh,
-                      trend->nh, t_out, trend->t_start, dMeans.get(), dSigma.get(), s, dTrendRec, dTrendRows);
-  } else {
-    SPH_CUDA(cudaMemcpyAsync(dMeans.get(), means, (size_t)t_out * points * sizeof(double), cudaMemcpyHostToDevice,
-                             s));
-    SPH_CUDA(cudaMemcpyAsync(dSigma.get(), sigma, points * sizeof(double), cudaMemcpyHostToDevice, s));
-  }
-  SPH_CUDA(cudaMemcpyAsync(dV2.get(), v2, points * sizeof(double), cudaMemcpyHostToDevice, s));
-  if (order > 0)
-    SPH_CUDA(cudaMemcpyAsync(dPhi.get(), phi, (size_t)order * d * sizeof(double), cudaMemcpyHostToDevice, s));
-  std::vector<double> hH, hE;
-  if (rng_mode == SPHEMU_RNG_REFERENCE) {
-    // Exact reference order: per replicate, (burn + t_out) x d innovations,
-    // then t_out x points small-scale normals.
-    hH.resize((size_t)S * d);
-    hE.resize(ytot);
-    RefGaussian g(seed);
-    for (int r = 0; r < r_begin; ++r)  // one serial stream: skip the replicates drawn elsewhere
-      for (int64_t e = 0; e < steps * d + (int64_t)t_out * points; ++e) g.normal();
-    for (int r = 0; r < r_len; ++r) {
-      double* h = hH.data() + (size_t)r * steps * d;
-      for (int64_t e = 0; e < steps * d; ++e) h[e] = g.normal();
-      double* ep = hE.data() + (size_t)r * t_out * points;
-      for (int64_t e = 0; e < (int64_t)t_out * points; ++e) ep[e] = g.normal();
-    }
-    SPH_CUDA(cudaMemcpyAsync(dH.get(), hH.data(), hH.size() * sizeof(double), cudaMemcpyHostToDevice, s));
-    SPH_CUDA(cudaMemcpyAsync(dEps.get(), hE.data(), hE.size() * sizeof(double), cudaMemcpyHostToDevice, s));
-  } else {
-    k_philox_normals<<<4 * num_sms(), 256, 0, s>>>(seed, 1, steps * d, r_begin, r_len, dH.get());
+  smem_optin(reinterpret_cast<const void*>(k_emul_xi), (int)sizeof(D2Smem));
+  emulate_core(a, [&](const double* dH, int64_t S, const std::vector<int64_t>&, double* dXi, cudaStream_t st) {
+    k_emul_xi<<<dim3(ceil_div(d, D2_BN), (unsigned)ceil_div(S, D2_BM)), D2_THREADS, sizeof(D2Smem), st>>>(
+        dH, dV.get(), S, d, dXi);
     SPH_LAUNCH_CHECK();
-    k_philox_normals<<<4 * num_sms(), 256, 0, s>>>(seed, 2, (int64_t)t_out * points, r_begin, r_len, dEps.get());
-    SPH_LAUNCH_CHECK();
-  }
-  SPH_CUDA(cudaFuncSetAttribute(k_emul_xi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(D2Smem)));
-  k_emul_xi<<<dim3(ceil_div(d, D2_BN), (unsigned)ceil_div(S, D2_BM)), D2_THREADS, sizeof(D2Smem), s>>>(
-      dH.get(), dV.get(), S, d, dXi.get());
-  SPH_LAUNCH_CHECK();
-  k_emul_ar<<<dim3(ceil_div(d, 128), r_len), 128, 0, s>>>(dXi.get(), dPhi.get(), order, d, burn, t_out, r_len,
-                                                           dDraws.get());
-  SPH_LAUNCH_CHECK();
-  sht_inverse_device(plan, dDraws.get(), (int64_t)r_len * t_out, dSynth.get(), nullptr);
-  k_emul_retrend<<<8 * num_sms(), 256, 0, s>>>(dSynth.get(), dEps.get(), dMeans.get(), dSigma.get(), dV2.get(),
-                                                points, t_out, ytot, dEps.get());
-  SPH_LAUNCH_CHECK();
-  SPH_CUDA(cudaMemcpyAsync(out, dEps.get(), ytot * sizeof(double), cudaMemcpyDeviceToHost, s));
-  SPH_CUDA(cudaStreamSynchronize(s));
+  });
 }
 
 }  // namespace sphemu_gpu

@@ -944,6 +944,13 @@ void emulate(void* plan, int n_theta, int n_phi, int L, const double* v, int d, 
              const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed, int r_len,
              int rng_mode, double* out, int r_begin, const TrendArgs* trend = nullptr);
 
+void sht_plan_dims(void* plan, int* n_theta, int* n_phi, int* L) {
+  Sht* p = static_cast<sphemu_sht_s*>(plan)->p;
+  *n_theta = p->n_theta;
+  *n_phi = p->n_phi;
+  *L = p->L;
+}
+
 // Bridge for emulate.cu: the plan's stream, and a device-resident inverse.
 void sht_inverse_device(void* plan, const double* coeffs, int64_t n, double* fields, cudaStream_t* s_out) {
   Sht* p = static_cast<sphemu_sht_s*>(plan)->p;

@@ -38,8 +38,10 @@ EncodeFn encode_fn() {
   return fn;
 }
 
+}  // namespace
+
 CUtensorMap make_map_strided(const void* base, int64_t rows, int64_t cols, int64_t row_bytes, int elem_bytes,
-                             int box_rows, int swizzle_bytes = 128) {
+                             int box_rows, int swizzle_bytes) {
   CUtensorMap m;
   const CUtensorMapDataType dt = elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                                  : CU_TENSOR_MAP_DATA_TYPE_UINT16;
@@ -54,6 +56,7 @@ CUtensorMap make_map_strided(const void* base, int64_t rows, int64_t cols, int64
   if (r != CUDA_SUCCESS) throw Error(SPHEMU_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
   return m;
 }
+namespace {
 // Row-major [rows x cols] array, box = 128 bytes of K x box_rows rows, SW128.
 CUtensorMap make_map(const void* base, int64_t rows, int64_t cols, int elem_bytes, int box_rows,
                      int swizzle_bytes = 128) {
@@ -955,11 +958,13 @@ __global__ void k_panel_finish_dp(TileStore ts, int k, const int2* list, const d
   const int b = ts.b;
   const int64_t bb = (int64_t)b * b;
   const int i = list[blockIdx.y].x;
-  double* tp = static_cast<double*>(ts.tile(i, k));
+  void* tp = ts.tile(i, k);
+  const int p = ts.tprec(i, k);
   const int64_t base = (int64_t)(i - k - 1) * bb;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += (int64_t)gridDim.x * blockDim.x) {
-    const double x = p64[base + e];
-    tp[e] = x;
+    const double x = p64[base + e];  // already rounded through p(i, k): the store is exact
+    unsigned none = 0;
+    store_elem(tp, p, e, x, none);
     if (p_hi) {
       float hi, lo;
       tf32_split(__double2float_rn(x), hi, lo);
@@ -1010,11 +1015,7 @@ void launch_tc(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorM
                const CUtensorMap& b_lo, const CUtensorMap& c_map, TcArgs args, cudaStream_t s, int max_ctas = 0) {
   using Lay = TcLayout<BN, OPK, MODE, CG>;
   auto kern = k_tc_gemm<BN, OPK, MODE, CG>;
-  static bool attr = false;
-  if (!attr) {
-    SPH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Lay::kSmem));
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(kern), Lay::kSmem);
   if (args.counter) SPH_CUDA(cudaMemsetAsync(args.counter, 0, sizeof(int), s));
   const int cap = (max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms()) / CG;
   const int grid = CG * static_cast<int>(std::min<int64_t>(args.items, std::max(1, cap)));
@@ -1038,13 +1039,7 @@ void launch_tc(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorM
   SPH_LAUNCH_CHECK();
 }
 
-struct StepLists {
-  // per (k, class) panel-tile lists, cached per TileStore shape
-  int nt = -1;
-  const uint8_t* key = nullptr;
-  std::vector<std::vector<int2>> host;
-  std::vector<DevBuf<int2>> dev;
-};
+
 
 }  // namespace
 

@@ -18,6 +18,11 @@
 
 namespace sphemu_gpu {
 
+// 2-D TMA map of a row-major array: rows x cols elements (2- or 4-byte), row
+// pitch row_bytes, box = swizzle_bytes of K x box_rows rows (SWIZZLE_128B / 64B).
+CUtensorMap make_map_strided(const void* base, int64_t rows, int64_t cols, int64_t row_bytes, int elem_bytes,
+                             int box_rows, int swizzle_bytes = 128);
+
 constexpr int TC_BM = 128;
 constexpr int TC_EPI_WARPS = 8;                  // epilogue warps 4 .. 11
 constexpr int TC_THREADS = 32 * (4 + TC_EPI_WARPS);

@@ -105,7 +105,22 @@ bool is_device_ptr(const void* p) {
     (void)cudaGetLastError();
     return false;
   }
-  return pa.type == cudaMemoryTypeDevice;  // not Managed: with HMM, pageable host memory reports as managed
+  if (pa.type != cudaMemoryTypeDevice) return false;  // not Managed: with HMM, pageable host memory reports as managed
+  int dev = 0;
+  SPH_CUDA(cudaGetDevice(&dev));
+  if (pa.device != dev)
+    throw std::invalid_argument("trend records live on device " + std::to_string(pa.device) +
+                                ", not on the current device " + std::to_string(dev));
+  return true;
+}
+
+// any(record[loc][2] != 0) over device records: one flag word back to the host.
+__global__ void k_any_lag(const double* __restrict__ records, int64_t points, int64_t stride, int* flag) {
+  int hit = 0;
+  for (int64_t loc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; loc < points && !hit;
+       loc += (int64_t)gridDim.x * blockDim.x)
+    hit = records[loc * stride + 2] != 0.0;
+  if (__syncthreads_or(hit) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
 // The two record columns the host needs for the per-step scalars: whether any
@@ -116,14 +131,16 @@ void lag_info(const double* records, bool dev, int64_t points, int64_t stride, b
   any_lag = false;
   rho = 0.0;
   if (!with_forcing || points == 0) return;
-  std::vector<double> col;
   const double* c2 = records + 2;
   if (dev) {
-    col.resize(points);
-    SPH_CUDA(cudaMemcpy2D(col.data(), sizeof(double), records + 2, stride * sizeof(double), sizeof(double), points,
-                          cudaMemcpyDeviceToHost));
+    int* flag = scratch<int>(3, 4);
+    SPH_CUDA(cudaMemset(flag, 0, sizeof(int)));
+    k_any_lag<<<std::max(1, std::min(ceil_div(points, 256), 4 * num_sms())), 256>>>(records, points, stride, flag);
+    SPH_LAUNCH_CHECK();
+    int h = 0;
+    SPH_CUDA(cudaMemcpy(&h, flag, sizeof(int), cudaMemcpyDeviceToHost));
     SPH_CUDA(cudaMemcpy(&rho, records + 3, sizeof(double), cudaMemcpyDeviceToHost));
-    for (int64_t loc = 0; loc < points && !any_lag; ++loc) any_lag = col[loc] != 0.0;
+    any_lag = h != 0;
   } else {
     rho = records[3];
     for (int64_t loc = 0; loc < points && !any_lag; ++loc) any_lag = c2[loc * stride] != 0.0;
@@ -299,19 +316,25 @@ void mean_table_device(const double* records, int64_t points, int harmonics, int
   if (smem > 200 * 1024) throw std::invalid_argument("harmonics too large for the device trend kernel");
   bool any_lag;
   double rho;
-  lag_info(records, false, points, stride, !f.empty(), any_lag, rho);
+  // records may be host or device memory (detected as in the trend calls)
+  const bool dev = is_device_ptr(records);
+  lag_info(records, dev, points, stride, !f.empty(), any_lag, rho);
   std::vector<double> rp = row_params(any_lag, rho, harmonics, period, f, t_len, t_start);
-  d_rec.alloc((size_t)points * stride);
   d_rp.alloc(rp.size());
-  SPH_CUDA(cudaMemcpyAsync(d_rec.get(), records, sizeof(double) * points * stride, cudaMemcpyHostToDevice, stream));
+  const double* rec = records;
+  if (!dev) {
+    d_rec.alloc((size_t)points * stride);
+    SPH_CUDA(cudaMemcpyAsync(d_rec.get(), records, sizeof(double) * points * stride, cudaMemcpyHostToDevice, stream));
+    rec = d_rec.get();
+  }
   SPH_CUDA(cudaMemcpyAsync(d_rp.get(), rp.data(), sizeof(double) * rp.size(), cudaMemcpyHostToDevice, stream));
   const int64_t gy = (t_len + kTrendRows - 1) / kTrendRows;
   for (int64_t y0 = 0; y0 < gy; y0 += 65535) {
     const dim3 grid((unsigned)ceil_div(points, kTrendThreads), (unsigned)std::min<int64_t>(65535, gy - y0));
-    launch_trend<kTable>(grid, smem, d_rec.get(), points, harmonics, d_rp.get(), !f.empty(), t_len, y0 * kTrendRows,
+    launch_trend<kTable>(grid, smem, rec, points, harmonics, d_rp.get(), !f.empty(), t_len, y0 * kTrendRows,
                          t_len, nullptr, d_table, stream);
   }
-  k_trend_sigma<<<2 * num_sms(), 256, 0, stream>>>(d_rec.get(), points, (int)stride, d_sigma);
+  k_trend_sigma<<<2 * num_sms(), 256, 0, stream>>>(rec, points, (int)stride, d_sigma);
   SPH_LAUNCH_CHECK();
   // rp is a pageable host vector: the async copy above is staged before it returns.
 }

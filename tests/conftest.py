@@ -25,3 +25,11 @@ def sph():
     import paper_2408_04440_b200 as m
 
     return m
+
+
+@pytest.fixture(scope="session")
+def G():
+    """Golden vectors generated from the reference's own sources (tools/make_golden.py)."""
+    import numpy as np
+
+    return dict(np.load(os.path.join(ROOT, "tests", "golden", "ref_vectors.npz")))

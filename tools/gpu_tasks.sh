@@ -1,0 +1,35 @@
+#!/bin/bash
+# One entry point for the gpurun jobs this repo runs (replaces the per-experiment
+# scratch scripts): tools/gpu_tasks.sh <task> [args]. Outputs go to gpurun_out/.
+#   check            pytest -m gpu + smoke() (the round-end gate)
+#   bench [N]        bench.py at N GPUs (torchrun for N > 1) + the reference arm
+#   launches         ncu launch list (gpu__time_duration) of a short bench run
+#   ncu <regex> [n]  one --set full capture of the n-th launch of kernels matching regex
+#   epi <args>       tools/epi_probe.py (SPHEMU_TC_DBG / SPHEMU_TC_CG from the env)
+#   sweep <k=v,..>   tools/ab.py under each listed environment assignment
+set -u
+mkdir -p gpurun_out
+task=${1:-check}; shift || true
+case "$task" in
+  check)
+    timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "PYTEST_EXIT $?" >> gpurun_out/pytest_gpu.log
+    timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "SMOKE_EXIT $?" >> gpurun_out/smoke.log
+    tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log ;;
+  bench)
+    n=${1:-1}
+    if [ "$n" = 1 ]; then
+      timeout 1200 python bench.py --steps ${STEPS:-20} --warmup ${WARMUP:-5} > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err
+      timeout 1200 python bench.py --impl reference --steps ${STEPS:-20} --warmup ${WARMUP:-5} > gpurun_out/bench_ref_n1.json 2> gpurun_out/bench_ref_n1.err
+    else
+      timeout 1800 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $n --steps ${STEPS:-3} --warmup ${WARMUP:-3} > gpurun_out/bench_n$n.json 2> gpurun_out/bench_n$n.err
+    fi
+    echo "EXIT $?"; tail -c 3000 gpurun_out/bench_n$n.json ;;
+  launches)
+    timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c ${COUNT:-20000} --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/ncu_launches.log 2>&1; echo "EXIT $?" ;;
+  ncu)
+    timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:$1" -s ${2:-5} -c 1 -o gpurun_out/ncu_${NAME:-kernel} -f python ${SCRIPT:-bench.py} ${SCRIPT_ARGS:---steps 1 --warmup 3} > gpurun_out/ncu_${NAME:-kernel}.log 2>&1; echo "EXIT $?" ;;
+  epi)
+    python tools/epi_probe.py "$@" ;;
+  *)
+    echo "unknown task $task"; exit 2 ;;
+esac
