@@ -171,6 +171,20 @@ GRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
 THRESH = {"dp": 1e-12, "dpsp": 5e-6, "dpsphp": 1e-2, "dphp": 5e-2}  # acceptance_main.cpp:226
 
 
+def workload_config(wl, args, world):
+    """The config object both arms print (the driver compares them)."""
+    grid = GRIDS.get(world, (world, 1))
+    n = wl["n"]
+    step = ("dense FP64 input resident in memory -> tiles at storage precision (from_dense + quantize), factor"
+            if wl["input"] == "dense" else
+            "make_spd_test_matrix generated into the tiles at storage precision, factor")
+    return {"workload": wl["desc"], "N": n, "tile_size": wl["tile"], "variant": wl["variant"],
+            "hp_format": wl["hp"], "sp_compute": args.sp_compute, "lookahead": args.lookahead,
+            "parallelism": f"2D block-cyclic {grid[0]}x{grid[1]} (NCCL panel broadcasts)" if world > 1
+            else "single GPU", "step": step,
+            "l2": f"tiles {8 * n * n / 2 / 1e9 / world:.1f}+ GB per GPU >> 126 MB L2, no flush needed"}
+
+
 def pick_workload(args, world):
     return WORKLOADS[args.workload or ("C2" if world == 1 else "C3")]
 
@@ -211,28 +225,48 @@ def cpu_sht_sample(t=32):
 
 
 def run_reference(args, world, rank):
+    """The reference arm: the oracle's restatement of mpchol.cpp (DAG
+    scheduler, all host cores, OpenBLAS tile kernels for Eigen) on this
+    workload's config. The host rate keeps rising with N (more tile
+    parallelism), so the K timed steps factor the workload's own N whenever
+    K of them fit the time budget (C2: ~14 s each on the GPU box's host);
+    otherwise (C3/C5: 134 GB+ dense) the largest sample N that fits, with the
+    rate curve at 4096 / 8192 / 16384 beside it."""
     if rank != 0:
         return
     wl = pick_workload(args, world)
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_cholesky_sample(n=4096, wl=wl)
+    for _ in range(args.warmup):
+        cpu_cholesky_sample(n=2048, wl=wl)
+    curve = {}
+    for n in (4096, 8192, 16384):
+        curve[str(n)] = cpu_cholesky_sample(n=n, wl=wl)[0]
+    n_step = args.ref_n
+    if not n_step:
+        # estimated time of one full-size step from the 16384 rate (the rate still grows with N)
+        full_t = wl["n"] ** 3 / 3 / (curve["16384"] * 1e12)
+        n_step = wl["n"] if (wl["n"] <= 40000 and args.steps * full_t <= args.ref_budget_s) else 16384
     times = []
-    val = sample = cores = None
+    sample = cores = None
     for _ in range(args.steps):
-        val, cores, sample, t = cpu_cholesky_sample(n=args.ref_n, wl=wl)
+        _, cores, sample, t = cpu_cholesky_sample(n=n_step, wl=wl)
         times.append(t)
-    v = args.ref_n ** 3 / 3 / (sum(times) / len(times)) / 1e12
+    v = n_step ** 3 / 3 / (sum(times) / len(times)) / 1e12
+    curve[str(n_step)] = v
+    same = n_step == wl["n"]
     line = {
         "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
-        "dtype": f"f64 compute, {wl['variant']} storage",
+        "dtype": "f64 compute (Eigen stand-in: OpenBLAS), " + wl["variant"] + " storage",
         "data": "synthetic: make_spd_test_matrix (reference generator, bitwise)",
-        "config": {"workload": f"{wl['desc']}; CPU bounded sample N={args.ref_n} "
-                               f"(~{(wl['n']/args.ref_n)**3:.0f}x less work than the full N={wl['n']})",
-                   "variant": wl["variant"], "tile_size": wl["tile"], "hp_format": wl["hp"]},
+        "config": workload_config(wl, args, world),
         "impl": "reference",
-        "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": (f"{sample}; every timed step factors the full N={wl['n']}" if same else
+                                    f"{sample}; each timed step factors N={n_step} (the full N={wl['n']} dense "
+                                    f"matrix does not fit the host / the time budget)")},
+        "full_size": same,
+        "rate_curve_tflops": curve,
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -274,6 +308,12 @@ def dense_input(sph, wl):
     a += torch.tril(a, -1).T
     torch.cuda.synchronize()
     return a
+
+
+def sp_desc(spc):
+    return {"fp16x3": "fp16 hi/lo split tcgen05 (3 MMAs, fp32 accumulate)",
+            "tf32x3": "3xTF32 tcgen05 (fp32 accumulate)",
+            "fp64": "FP64 DMMA (the oracle's arithmetic)"}[spc]
 
 
 def dominant_class(wl):
@@ -330,6 +370,18 @@ def time_factor(sph, h, wl, args, world, a_dev=None, steps=None, warmup=None, cl
     h.all_phases = h.phase_times()
     h.set_profiling(False)
     return ms, st, launches, clocks
+
+
+def kms_probe(h, rho=0.999):
+    """Parity where the flops are: the reference generator's 0.9 decay leaves
+    every tile beyond distance 1 ~0 at b >= 256, so the handle is refactored on
+    the same family with rho = 0.999 (every tile O(1): 0.999^512 = 0.6) and
+    probed the same way (A regenerated on the device)."""
+    h.generate_spd(1, rho=rho)
+    h.factor()
+    h.wait()
+    return {"kms_rho": rho, "kms_residual_probe": h.residual_probe(1, 2, rho=rho),
+            "kms_note": "||(A - LL^T)x|| / ||Ax|| with a_ij = 0.25 d_i d_j rho^|i-j| (O(1) tiles everywhere)"}
 
 
 def roofline(h, wl, args, phases, steps, ms):
@@ -394,23 +446,27 @@ def roofline(h, wl, args, phases, steps, ms):
 
 
 def e2e_single(sph, wl, args, a_dev):
-    """The reference-facing one-shot call with pinned host buffers: H2D of the
-    input and D2H of the factor inside the timed region."""
+    """The reference-facing one-shot call (tiled_cholesky_dense's C-ABI) with
+    ordinary pageable host arrays, as the drop-in callers pass them (numpy /
+    std::vector): H2D of the input and D2H of the factor inside the timed
+    region."""
     import ctypes as C
+
+    import numpy as np
     import torch
     lib = sph._sphemu.lib()
     n = wl["n"]
-    a_host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
-    a_host.copy_(a_dev)
-    f_host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+    a_host = np.empty((n, n))
+    a_host[...] = a_dev.cpu().numpy()
+    f_host = np.empty((n, n))
     cfg = sph._sphemu.make_config(wl["variant"], wl["tile"], hp_format=wl["hp"], lookahead=args.lookahead,
                                   sp_compute=args.sp_compute)
     stats = sph._sphemu.CholStats()
     failed = C.c_int(-1)
 
     def call():
-        rc = lib.sphemu_gpu_tiled_cholesky_dense(C.c_void_p(a_host.data_ptr()), 0, n, C.byref(cfg),
-                                                 C.c_void_p(f_host.data_ptr()), 0, C.byref(stats), C.byref(failed))
+        rc = lib.sphemu_gpu_tiled_cholesky_dense(C.c_void_p(a_host.ctypes.data), 0, n, C.byref(cfg),
+                                                 C.c_void_p(f_host.ctypes.data), 0, C.byref(stats), C.byref(failed))
         assert rc == 0, rc
 
     for _ in range(max(3, args.warmup)):
@@ -423,12 +479,16 @@ def e2e_single(sph, wl, args, a_dev):
     t_e2e = (time.perf_counter() - t0) / e2e_steps
     lib.sphemu_gpu_release_cache()
     del a_host, f_host
-    return {"value": n ** 3 / 3 / t_e2e / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": 8 * n * n,
-            "d2h_bytes_per_step": 8 * n * n, "ms_per_step": 1e3 * t_e2e, "steps": e2e_steps,
-            "api": "sphemu_gpu_tiled_cholesky_dense (host pointers, pinned)",
-            "bytes_note": "counted as the dense n x n in and out; the library moves the lower triangle at storage "
-                          "width (fp64 DP tiles, fp32 the rest: H2D by tile rows, D2H by tile-column groups as they "
-                          "finish), host threads narrow / widen it and stream the zeros"}
+    # what crosses PCIe: the lower triangle at storage width each way (FactorizationStats bytes)
+    moved = int(stats.bytes_dp + stats.bytes_sp + stats.bytes_hp)
+    return {"value": n ** 3 / 3 / t_e2e / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": moved,
+            "d2h_bytes_per_step": moved, "ms_per_step": 1e3 * t_e2e, "steps": e2e_steps,
+            "api": "sphemu_gpu_tiled_cholesky_dense (pageable host numpy arrays in and out)",
+            "host_bytes_per_step": {"read": 8 * n * n, "written": 8 * n * n},
+            "bytes_note": "h2d/d2h = the lower triangle at storage width (fp64 DP tiles, fp32 SP, 16-bit HP: H2D "
+                          "by tile rows, D2H by tile-column groups as they finish); host threads narrow the dense "
+                          "fp64 input into pinned staging and widen the factor into the caller's buffer, and "
+                          "write the zeros above the diagonal"}
 
 
 def e2e_dist(sph, args, world, rank):
@@ -583,7 +643,7 @@ def model_side_points(sph):
         assert lib.sphemu_gpu_retrend(vp(z.data_ptr()), 1, R, Tt, vp(rec_d.data_ptr()), points, K, 8760, None, 0,
                                       None, 0, 1, vp(y.data_ptr()), 1) == 0
 
-    peak = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")))["hbm_gbs"]
+    peak = load_peaks().get("hbm_gbs", 6434.2)  # MEASURED_PEAKS.json is driver-written; BASELINE.md §3 value else
     for name, fn, nbytes, what in (
             ("fit_var", fv, 16 * T * d + 8 * (T - order) * d, "C2 size: d=32400, T=1000, order 3 (series read "
              "twice + residuals written)"),
@@ -606,18 +666,17 @@ def model_side_points(sph):
     return out
 
 
-def emulation_point(sph, L=90, replicates=100, t_out=24, order=3, world=1, rank=0):
-    """Emulation generator throughput (stochastic.cpp:217-277): R replicates x T steps on the (L+1) x 2L grid,
-    V = the device factor of make_spd_test_matrix(L^2) (dp), AR(3), device Philox normals; the one-shot C-ABI
-    call with host buffers (V in, fields out) is the timed unit."""
+def emulation_point(sph, h, L, world=1, rank=0, replicates=100, t_out=24, order=3):
+    """Emulation generator throughput (stochastic.cpp:217-277) from the
+    device-resident tiled factor of handle h (d = L^2; no dense V anywhere):
+    R replicates x T steps on the (L+1) x 2L grid, AR(3), device Philox
+    normals, xi = V eta by the TRMM over the stored tiles, fields written to
+    HBM. Distributed handles split the replicates (partial products over
+    each rank's tiles reduced onto the replicate owners). Device time per
+    call (CUDA events), max over ranks."""
     import numpy as np
+    import torch
     d = L * L
-    h = sph.Cholesky(d, "dp", tile_size=256)
-    h.generate_spd(1)
-    h.factor()
-    h.wait()
-    v = h.factor_dense()
-    del h
     nt, nphi = L + 1, 2 * L
     plan = sph.ShtPlan(nt, nphi, L)
     phi = np.stack([np.full(d, x) for x in (0.6, 0.25, 0.15)[:order]])
@@ -625,23 +684,30 @@ def emulation_point(sph, L=90, replicates=100, t_out=24, order=3, world=1, rank=
     means = np.zeros((t_out, pts))
     sigma = np.ones(pts)
     v2 = np.full(pts, 0.04)
-    sph._sphemu.emulate(plan, v, phi, means, sigma, v2, t_out, 7, 2, "philox")  # warm-up
-    # replicates sharded over the ranks (draws depend only on the replicate: no communication)
-    per = (replicates + world - 1) // world
-    r0 = min(replicates, rank * per)
-    cnt = max(0, min(per, replicates - r0))
+    mine = (replicates * (rank + 1)) // world - (replicates * rank) // world
+    out = torch.empty((max(1, mine), t_out, nt, nphi), dtype=torch.float64, device="cuda")
+    h.emulate(plan, phi, means, sigma, v2, t_out, seed=7, r_len=min(2 * world, replicates), out_ptr=out.data_ptr())
+    torch.cuda.synchronize()
     barrier(world)
-    t0 = time.perf_counter()
-    out = sph._sphemu.emulate(plan, v, phi, means, sigma, v2, t_out, 7, cnt, "philox", r_begin=r0) if cnt else \
-        np.zeros(1)
-    dt = max_over_ranks(time.perf_counter() - t0, world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    h.emulate(plan, phi, means, sigma, v2, t_out, seed=7, r_len=replicates, out_ptr=out.data_ptr())
+    e1.record()
+    torch.cuda.synchronize()
+    dt = max_over_ranks(e0.elapsed_time(e1) * 1e-3, world)
+    finite = bool(torch.isfinite(out).all().item())
     burn = 10 * order
+    cols = replicates * (burn + t_out)
+    del out, plan
+    torch.cuda.empty_cache()
     return {"band_limit": L, "d": d, "grid": f"{nt}x{nphi}", "replicates": replicates, "steps": t_out,
-            "sharding": f"replicate ranges over {world} GPU(s)",
+            "sharding": f"replicates split over {world} GPU(s), partial TRMMs reduced over NCCL" if world > 1
+            else "single GPU",
             "snapshots_per_s": replicates * t_out / dt, "seconds": dt,
-            "trmm_fp64_tflops": d * d * replicates * (burn + t_out) / dt / 1e12,
-            "finite": bool(np.isfinite(out).all()),
-            "api": "sphemu_gpu_emulate (host V and fields, H2D/D2H inside)"}
+            "trmm_tflops": d * d * cols / dt / 1e12,
+            "trmm_note": "d^2 flops per innovation column (triangular V), R (burn + T) columns; the whole "
+                         "call incl. RNG, AR(3), inverse SHT and retrend",
+            "finite": finite, "api": "sphemu_gpu_emulate_chol (tiled factor, fields to HBM)"}
 
 
 def run_ours(args, world, rank, local):
@@ -664,6 +730,9 @@ def run_ours(args, world, rank, local):
     probe = h.residual_probe(1, 2)
     dom = roofline(h, wl, args, h.timed_phases, args.steps, ms)
     sat = int(st.half_saturations)
+    probe_kms = kms_probe(h)
+    # emulation from this factor (C2: L = 180; N > 1: the C3 matrix, L = 360)
+    emul = emulation_point(sph, h, int(round(n ** 0.5)), world, rank) if not args.no_emul else None
     del h
     torch.cuda.empty_cache()
 
@@ -681,38 +750,33 @@ def run_ours(args, world, rank, local):
         h3, _ = make_handle(sph, wl3, args, 1, 0)
         ms3, _, _, _ = time_factor(sph, h3, wl3, args, 1, steps=2, warmup=1)
         c3_1 = {"ms_per_step": ms3, "tflops": wl3["n"] ** 3 / 3 / (ms3 * 1e-3) / 1e12, "steps": 2, "warmup": 1,
-                "step": "generate make_spd_test_matrix tiles in place + factor", "workload": wl3["desc"]}
+                "step": "generate make_spd_test_matrix tiles in place + factor", "workload": wl3["desc"],
+                "parity": {"residual_probe": h3.residual_probe(1, 2), "threshold": THRESH[wl3["variant"]],
+                           **kms_probe(h3)}}
+        if not args.no_emul:
+            c3_1["emulation"] = emulation_point(sph, h3, 360, 1, 0)
         del h3
         torch.cuda.empty_cache()
 
     sht = sht_throughput(sph, world)
     c4 = sht_c4(sph) if (world == 1 and not args.no_c4) else None
-    emul = emulation_point(sph, world=world, rank=rank) if not args.no_c4 else None
     side = model_side_points(sph) if (world == 1 and not args.no_c4) else None
 
     if rank != 0:
         return
-    cpu_val, cores, sample, _ = (cpu_cholesky_sample(n=args.ref_n, wl=wl) if not args.no_cpu
+    cpu_val, cores, sample, _ = (cpu_cholesky_sample(n=args.cpu_n, wl=wl) if not args.no_cpu
                                  else (None, 0, "skipped", 0))
     cpu_sht = cpu_sht_sample() if not args.no_cpu else (None, 0)
     clk = clocks.summary()
-    step_desc = ("dense FP64 input resident in HBM -> tiles at storage precision (from_dense + quantize), factor"
-                 if wl["input"] == "dense" else
-                 "make_spd_test_matrix generated into the owned tiles at storage precision, factor")
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
-        "dtype": (f"f64 compute semantics; storage {wl['variant']} ({wl['hp']} HP): FP64 DMMA, "
-                  f"{args.sp_compute} tcgen05 for SP, {wl['hp']} tcgen05 for HP"),
+        "dtype": (f"f64 in/out; tiles stored per the {wl['variant']} map (DP fp64, SP fp32, HP {wl['hp']}); "
+                  f"DP tiles FP64 DMMA; SP tiles {sp_desc(args.sp_compute)}; HP tiles {wl['hp']} tcgen05 "
+                  f"(fp32 accumulate); panel TRSM = X B Linv^T with the FP64 inverse of the diagonal tile"),
         "data": f"synthetic: make_spd_test_matrix({n}, 1) bitwise the reference generator; SHT on random coefficients",
-        "config": {"workload": f"{wl['desc']} + SHT 1000 snapshots 181x360 L=180 per GPU", "N": n,
-                   "tile_size": wl["tile"], "variant": wl["variant"], "hp_format": wl["hp"],
-                   "sp_compute": args.sp_compute, "lookahead": args.lookahead,
-                   "parallelism": f"2D block-cyclic {grid[0]}x{grid[1]} (NCCL panel broadcasts)" if world > 1
-                   else "single GPU",
-                   "step": step_desc,
-                   "l2": f"tiles {8 * n * n / 2 / 1e9 / world:.1f}+ GB per GPU >> 126 MB L2, no flush needed"},
+        "config": workload_config(wl, args, world),
         "roofline": dom,
         "cpu_baseline": {"value": cpu_val, "unit": "TFLOP/s", "cores": cores, "kind": "port",
                          "sample": sample, "sht_snapshots_per_s": cpu_sht[0]},
@@ -724,7 +788,8 @@ def run_ours(args, world, rank, local):
         "phases_note": "one extra fully profiled step after the timed region (busy time per phase, chain and bulk "
                        "streams overlap)",
         "parity": {"residual_probe": probe, "threshold": THRESH[wl["variant"]],
-                   "ok": bool(probe < THRESH[wl["variant"]]),
+                   "ok": bool(probe < THRESH[wl["variant"]] and probe_kms["kms_residual_probe"] < THRESH[wl["variant"]]),
+                   **probe_kms,
                    "what": "||(A - LL^T)x|| / ||Ax|| on 2 seeded vectors, A regenerated on device; thresholds of "
                            "acceptance_main.cpp:226"},
         "half_saturations": sat,
@@ -761,14 +826,17 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
                     help="default: C2 on 1 GPU, C3 (2D block-cyclic) on more")
-    ap.add_argument("--ref-n", type=int, default=8192)
+    ap.add_argument("--ref-n", type=int, default=0, help="reference arm step size (0: the workload's N if it fits)")
+    ap.add_argument("--ref-budget-s", type=float, default=330.0, help="reference arm: time budget of the K steps")
+    ap.add_argument("--cpu-n", type=int, default=16384, help="our arm's cpu_baseline sample N")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c3", action="store_true", help="skip the 1-GPU C3 point on N=1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the L=720 SHT point on N=1")
+    ap.add_argument("--no-emul", action="store_true", help="skip the emulation points")
     ap.add_argument("--lookahead", type=int, default=1)
-    ap.add_argument("--sp-compute", default="fp16x3", choices=["fp16x3", "tf32x3"])
+    ap.add_argument("--sp-compute", default="fp16x3", choices=["fp16x3", "tf32x3", "fp64"])
     args = ap.parse_args()
     sys.stdout.flush()
     _JSON_OUT = os.fdopen(os.dup(1), "w")

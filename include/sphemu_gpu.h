@@ -108,7 +108,9 @@ int sphemu_gpu_release_cache(void);
 
 /* Host-only view of the 2D block-cyclic layout a rank would use (no GPU
  * needed): tiles it stores, its arena bytes, and xchg_bytes[k*P*Q + r] = the
- * panel bytes rank r broadcasts at step k (nt*P*Q entries, may be NULL). */
+ * panel bytes rank r receives at step k (nt*P*Q entries, may be NULL): each
+ * panel tile (i, k) travels point to point from its owner to the owners of
+ * row i and column i only. */
 int sphemu_gpu_dist_layout(int n, const sphemu_chol_config* cfg, int P, int Q, int rank, int64_t* tiles_owned,
                            int64_t* arena_bytes, int64_t* xchg_bytes);
 
@@ -118,10 +120,10 @@ typedef struct sphemu_chol_s* sphemu_chol_t;
 int sphemu_gpu_chol_create(int n, const sphemu_chol_config* cfg, sphemu_chol_t* out);
 int sphemu_gpu_chol_destroy(sphemu_chol_t h);
 /* 2D block-cyclic distribution over a P x Q grid of GPUs (one process per
- * GPU, the caller sets the device first): tile (i, j) is stored on rank
- * ((i + s (j div Q)) mod P) * Q + (j mod Q), s the smallest shift with
- * gcd(Q + s, P) = 1 (block-cyclic with the diagonal tiles spread over all ranks); panel tiles travel over NCCL at their storage
- * precision. All ranks call every handle function collectively; the dense
+ * GPU, the caller sets the device first): off-diagonal tile (i, j) is
+ * stored on rank (i mod P) * Q + (j mod Q), diagonal tile (i, i) on rank
+ * i mod (P Q); panel tiles travel over NCCL point to point at their storage
+ * precision, each only to the ranks that update with it. All ranks call every handle function collectively; the dense
  * factor of store_dense is gathered on rank 0. uid128 comes from
  * sphemu_gpu_nccl_unique_id on rank 0 (the caller distributes it). */
 int sphemu_gpu_nccl_unique_id(void* out128);
@@ -146,6 +148,13 @@ int sphemu_gpu_chol_residual(sphemu_chol_t h, const double* a, int where, int64_
 /* Size-independent check for sizes the host cannot hold: ||(A - L L^T) x|| /
  * ||A x|| for n_vec seeded random vectors x, against make_spd_test_matrix(seed). */
 int sphemu_gpu_chol_residual_probe_spd(sphemu_chol_t h, uint64_t seed, int n_vec, double* out);
+/* The same generator family with the 0.9 decay replaced by rho in (0, 1):
+ * a_ii = 1.25 d_i^2, a_ij = 0.25 d_i d_j rho^|i-j| = D (I + K/4) D with K the
+ * Kac-Murdock-Szego matrix (SPD). rho = 0.9 is make_spd_test_matrix; rho ->
+ * 1 keeps every tile O(1) (0.999^512 = 0.6), the parity input where the
+ * flops are. The probe regenerates A the same way. */
+int sphemu_gpu_chol_generate_spd_decay(sphemu_chol_t h, uint64_t seed, double rho);
+int sphemu_gpu_chol_residual_probe_spd_decay(sphemu_chol_t h, uint64_t seed, double rho, int n_vec, double* out);
 /* Per-precision flop split of the factorization (BASELINE.md §4 units). */
 int sphemu_gpu_chol_flops(sphemu_chol_t h, double* f_dp, double* f_sp, double* f_hp);
 /* Phase profiling (CUDA events around every phase; off by default). Phases:

@@ -247,8 +247,13 @@ class Cholesky:
             lib().sphemu_gpu_chol_destroy(self.h)
             self.h = None
 
-    def generate_spd(self, seed=1):
-        _check(lib().sphemu_gpu_chol_generate_spd(self.h, seed))
+    def generate_spd(self, seed=1, rho=None):
+        """make_spd_test_matrix(n, seed) into the tiles; rho (0 < rho < 1)
+        replaces the reference's 0.9 decay (non-decaying tiles as rho -> 1)."""
+        if rho is None:
+            _check(lib().sphemu_gpu_chol_generate_spd(self.h, seed))
+        else:
+            _check(lib().sphemu_gpu_chol_generate_spd_decay(self.h, C.c_uint64(seed), C.c_double(rho)))
 
     def load(self, a, where=HOST, lda=None):
         if where == HOST:
@@ -326,9 +331,13 @@ class Cholesky:
         _check(lib().sphemu_gpu_chol_update_flops(self.h, *[C.byref(x) for x in f]))
         return {"dp": f[0].value, "sp": f[1].value, "hp": f[2].value}
 
-    def residual_probe(self, seed=1, n_vec=2):
+    def residual_probe(self, seed=1, n_vec=2, rho=None):
         out = C.c_double()
-        _check(lib().sphemu_gpu_chol_residual_probe_spd(self.h, seed, n_vec, C.byref(out)))
+        if rho is None:
+            _check(lib().sphemu_gpu_chol_residual_probe_spd(self.h, seed, n_vec, C.byref(out)))
+        else:
+            _check(lib().sphemu_gpu_chol_residual_probe_spd_decay(self.h, C.c_uint64(seed), C.c_double(rho), n_vec,
+                                                                   C.byref(out)))
         return out.value
 
     def trmm(self, eta):
@@ -339,7 +348,7 @@ class Cholesky:
         _check(lib().sphemu_gpu_chol_trmm(self.h, _ptr(eta), HOST, eta.shape[0], _ptr(out), HOST))
         return out
 
-    def emulate(self, plan, phi, means, sigma, v2, t_out, seed=1, r_len=1, rng="philox", r_begin=0):
+    def emulate(self, plan, phi, means, sigma, v2, t_out, seed=1, r_len=1, rng="philox", r_begin=0, out_ptr=None):
         """emulate (stochastic.cpp:217-277) with V = this handle's tiled factor
         (sphemu_gpu_emulate_chol); distributed handles return this rank's
         contiguous block of the replicates."""
@@ -353,8 +362,13 @@ class Cholesky:
         rank = self.rank
         lo = r_begin + (r_len * rank) // world
         hi = r_begin + (r_len * (rank + 1)) // world
-        out = np.empty((hi - lo, t_out, plan.n_theta, plan.n_phi))
         mode = {"reference": 0, "philox": 1}[rng]
+        if out_ptr is not None:  # device buffer of (hi - lo, t_out, n_theta, n_phi) doubles
+            _check(lib().sphemu_gpu_emulate_chol(self.h, plan.h, _ptr(phi_a), phi.shape[0], _ptr(means),
+                                                 _ptr(sigma), _ptr(v2), t_out, seed, r_begin, r_len, mode,
+                                                 C.c_void_p(out_ptr), DEVICE))
+            return hi - lo
+        out = np.empty((hi - lo, t_out, plan.n_theta, plan.n_phi))
         _check(lib().sphemu_gpu_emulate_chol(self.h, plan.h, _ptr(phi_a), phi.shape[0], _ptr(means), _ptr(sigma),
                                              _ptr(v2), t_out, seed, r_begin, r_len, mode, _ptr(out), HOST))
         return out

@@ -290,39 +290,48 @@ __global__ void k_diff_norms(int n, const double* a, const double* b, double* su
   }
 }
 
-// 2D block-cyclic owner of tile (i, j) on a P x Q grid: process column
-// j mod Q (so panel column k lives in one process column, as the exchange
-// plan assumes) and process row (i + s * (j div Q)) mod P. The shift s is the
-// smallest with gcd(Q + s, P) = 1, which makes the diagonal tiles — the FP64
-// band, whose SYRK updates cost ~50x a BF16 tile's — visit every rank
-// (i = Q a + c lands on row ((Q + s) a + c) mod P) instead of only the
-// diagonal ranks of the plain (i mod P, j mod Q) map when gcd(P, Q) > 1.
-inline int block_cyclic_shift(int P, int Q) {
-  int s = 0;
-  while (std::gcd(Q + s, P) != 1) ++s;
-  return s;
-}
+// Owner of tile (i, j) on a P x Q process grid: off-diagonal tiles are 2D
+// block-cyclic, (i mod P, j mod Q), so row i lives on process row i mod P and
+// column i on process column i mod Q; diagonal tiles — the FP64 band, whose
+// SYRK updates cost ~50x a BF16 tile's — go round-robin over all P Q ranks
+// (the plain map would give them only to the ranks with i mod P == i mod Q).
 inline int block_cyclic_owner(int i, int j, int P, int Q) {
-  return ((i + block_cyclic_shift(P, Q) * (j / Q)) % P) * Q + (j % Q);
+  return i == j ? i % (P * Q) : (i % P) * Q + (j % Q);
 }
 
 // Host-only 2D block-cyclic layout (no CUDA calls): this rank's tile offsets
-// in its arena and the per-step panel exchange plan (panel tiles of step k
-// grouped by owning rank so each owner broadcasts one contiguous block). Chol
-// builds its device state from it; sphemu_gpu_dist_layout exposes it to
+// in its arena and the per-step panel exchange plan. Panel tile (i, k) goes
+// from its owner to exactly the ranks whose updates read it — the owners of
+// row i's tiles (i, j), k < j <= i (process row i mod P + the owner of the
+// diagonal tile) and of column i's tiles (j, i), j > i (process column
+// i mod Q): P + Q ranks at most instead of all P Q.
+// Chol builds its device state from it; sphemu_gpu_dist_layout exposes it to
 // host-side tests.
 struct BlockCyclic {
-  struct XRoot {
-    int root;
-    int64_t off, bytes;
+  struct Xfer {
+    int i;      // panel tile row
+    int peer;   // destination (sends) or source (recvs)
+    int64_t pos, bytes;
   };
   int nt = 0, b = 0, P = 1, Q = 1, rank = 0;
   std::vector<int64_t> off;                 // per packed tile; -1 = stored elsewhere; back() = arena bytes
-  std::vector<std::vector<XRoot>> xroots;   // per step k
+  std::vector<std::vector<Xfer>> sends, recvs;  // this rank's, per step k
   std::vector<std::vector<int64_t>> xpos;   // per step k: byte position of panel tile i at [i - k - 1]
+  std::vector<std::vector<int64_t>> recv_bytes;  // per step k, per rank: bytes that rank receives
   int64_t xmax = 0;
   int owner(int i, int j) const { return block_cyclic_owner(i, j, P, Q); }
   bool mine(int i, int j) const { return owner(i, j) == rank; }
+  // ranks that read panel tile (i, k) in step k, its owner excluded
+  std::vector<int> needers(int i, int k) const {
+    std::vector<char> need(static_cast<size_t>(P) * Q, 0);
+    for (int j = k + 1; j <= i; ++j) need[owner(i, j)] = 1;
+    for (int j = i + 1; j < nt; ++j) need[owner(j, i)] = 1;
+    need[owner(i, k)] = 0;
+    std::vector<int> r;
+    for (int q = 0; q < P * Q; ++q)
+      if (need[q]) r.push_back(q);
+    return r;
+  }
 
   BlockCyclic(int nt_, int b_, const std::vector<uint8_t>& sprec, int P_, int Q_, int rank_)
       : nt(nt_), b(b_), P(P_), Q(Q_), rank(rank_) {
@@ -341,22 +350,29 @@ struct BlockCyclic {
       }
     off.back() = o;
     if (P * Q == 1) return;
-    xroots.assign(nt, {});
+    sends.assign(nt, {});
+    recvs.assign(nt, {});
     xpos.assign(nt, {});
+    recv_bytes.assign(nt, std::vector<int64_t>(static_cast<size_t>(P) * Q, 0));
     for (int k = 0; k + 1 < nt; ++k) {
       xpos[k].assign(nt - k - 1, 0);
       int64_t x = 0;
-      for (int pr = 0; pr < P; ++pr) {
-        const int root = pr * Q + k % Q;
-        const int64_t start = x;
+      for (int root = 0; root < P * Q; ++root)  // grouped by owner: each owner packs one contiguous block
         for (int i = k + 1; i < nt; ++i)
           if (owner(i, k) == root) {
             xpos[k][i - k - 1] = x;
             x += static_cast<int64_t>(b) * b * prec_bytes(sprec[static_cast<size_t>(i) * (i + 1) / 2 + k]);
           }
-        if (x > start) xroots[k].push_back({root, start, x - start});
-      }
       xmax = std::max(xmax, x);
+      for (int i = k + 1; i < nt; ++i) {
+        const int src = owner(i, k);
+        const int64_t bytes = static_cast<int64_t>(b) * b * prec_bytes(sprec[static_cast<size_t>(i) * (i + 1) / 2 + k]);
+        for (int r : needers(i, k)) {
+          recv_bytes[k][r] += bytes;
+          if (src == rank) sends[k].push_back({i, r, xpos[k][i - k - 1], bytes});
+          if (r == rank) recvs[k].push_back({i, src, xpos[k][i - k - 1], bytes});
+        }
+      }
     }
   }
 };
@@ -478,16 +494,16 @@ struct Chol {
   bool dist() const { return P * Q > 1; }
   int owner(int i, int j) const { return block_cyclic_owner(i, j, P, Q); }
   bool mine(int i, int j) const { return owner(i, j) == rank; }
-  // Panel exchange buffer: per step the panel tiles at storage precision,
-  // grouped by owning rank (root) so each root broadcasts one contiguous
-  // block; xsend / ilists list this rank's packed / imported tiles with their
-  // byte offsets, xroots the (root, offset, bytes) blocks.
+  // Panel exchange buffer: per step the panel tiles at storage precision at
+  // fixed positions (grouped by owner); xsend / ilists list this rank's packed
+  // / received tiles with their byte positions, xsends / xrecvs the
+  // point-to-point transfers of each step (BlockCyclic).
   DevBuf<uint8_t> xbuf;
   DevBuf<int2> ilists, xsend;
   DevBuf<int64_t> ioffs, xsoffs;
   std::vector<int64_t> ilist_off, ilist_cnt, xsend_off, xsend_cnt;
-  using XRoot = BlockCyclic::XRoot;
-  std::vector<std::vector<XRoot>> xroots;
+  using Xfer = BlockCyclic::Xfer;
+  std::vector<std::vector<Xfer>> xsends, xrecvs;
   sphemu_chol_config cfg{};
   std::vector<uint8_t> pmap, sprec;
   std::vector<int64_t> off;
@@ -999,25 +1015,23 @@ struct Chol {
       ilist_cnt.assign(nt, 0);
       xsend_off.assign(nt, 0);
       xsend_cnt.assign(nt, 0);
-      xroots.assign(nt, {});
       std::vector<int2> il, xs;
       std::vector<int64_t> io, xo;
-      xroots = layout.xroots;
+      xsends = layout.sends;
+      xrecvs = layout.recvs;
       const int64_t xmax = layout.xmax;
       for (int k = 0; k + 1 < nt; ++k) {
-        std::vector<int64_t> pos(nt, 0);
-        for (int i = k + 1; i < nt; ++i) pos[i] = layout.xpos[k][i - k - 1];
         ilist_off[k] = static_cast<int64_t>(il.size());
         xsend_off[k] = static_cast<int64_t>(xs.size());
-        for (int i = k + 1; i < nt; ++i) {
-          if (!mine(i, k)) {
-            il.push_back(make_int2(i, k));
-            io.push_back(pos[i]);
-          } else {
-            xs.push_back(make_int2(i, k));
-            xo.push_back(pos[i]);
-          }
+        for (const Xfer& x : layout.recvs[k]) {
+          il.push_back(make_int2(x.i, k));
+          io.push_back(x.pos);
         }
+        for (int i = k + 1; i < nt; ++i)
+          if (mine(i, k) && !layout.needers(i, k).empty()) {
+            xs.push_back(make_int2(i, k));
+            xo.push_back(layout.xpos[k][i - k - 1]);
+          }
         ilist_cnt[k] = static_cast<int64_t>(il.size()) - ilist_off[k];
         xsend_cnt[k] = static_cast<int64_t>(xs.size()) - xsend_off[k];
       }
@@ -1110,7 +1124,7 @@ struct Chol {
     SPH_CUDA(cudaStreamSynchronize(stream));
   }
 
-  void generate_spd(uint64_t seed);
+  void generate_spd(uint64_t seed, double rho = 0.9);
 
   // ---- the per-step operations, on a given stream and panel buffer set ----
   void op_potrf(int k, cudaStream_t s) {
@@ -1299,9 +1313,10 @@ struct Chol {
       SPH_LAUNCH_CHECK();
     }
     SPH_NCCL(ncclGroupStart());
-    for (const XRoot& x : xroots[k])
-      SPH_NCCL(ncclBroadcast(xbuf.get() + x.off, xbuf.get() + x.off, static_cast<size_t>(x.bytes), ncclUint8, x.root,
-                             comm, s));
+    for (const Xfer& x : xsends[k])
+      SPH_NCCL(ncclSend(xbuf.get() + x.pos, static_cast<size_t>(x.bytes), ncclUint8, x.peer, comm, s));
+    for (const Xfer& x : xrecvs[k])
+      SPH_NCCL(ncclRecv(xbuf.get() + x.pos, static_cast<size_t>(x.bytes), ncclUint8, x.peer, comm, s));
     SPH_NCCL(ncclGroupEnd());
     note_launch();
     if (ilist_cnt[k]) {
@@ -1516,8 +1531,11 @@ struct Chol {
                        S, xi, s);
     static const int flush_env = [] {
       const char* e = std::getenv("SPHEMU_TRMM_FLUSH_K");
-      return e ? std::atoi(e) : 2048;
+      return e ? std::atoi(e) : 512;
     }();
+    // fp32 TMEM partial sums over at most max(b, 512) of K: the tensor cores'
+    // truncating fp32 accumulation error grows with the length (measured
+    // max rel. error 1.1e-6 at 512, 4.5e-6 at 2048, 8.9e-6 at 8192).
     const int flush = std::max(1, flush_env / b);
     for (int c = 0; c < 2; ++c) {
       if (tp.ent[c].empty()) continue;
@@ -1674,9 +1692,9 @@ struct Chol {
   // ||(A - L L^T) x|| / ||A x|| over n_vec seeded vectors, A regenerated
   // from (d, pw) on the fly: a size-independent check at sizes the host
   // cannot hold.
-  double residual_probe(uint64_t seed, int n_vec) {
+  double residual_probe(uint64_t seed, int n_vec, double rho = 0.9) {
     std::vector<double> d(n), pw(n);
-    host_spd_factors(n, seed, d.data(), pw.data());
+    host_spd_factors(n, seed, d.data(), pw.data(), rho);
     DevBuf<double> dd(n), dpw(n), x(n), y1(n), z(n), y2(n), sums(2);
     SPH_CUDA(cudaMemcpyAsync(dd.get(), d.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream));
     SPH_CUDA(cudaMemcpyAsync(dpw.get(), pw.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream));
@@ -1732,10 +1750,10 @@ struct Chol {
 
 // make_spd_test_matrix inputs computed on the host exactly as the reference
 // does (GaussianRng uniform -> exp, std::pow(0.9, k)), matrix built on device.
-void Chol::generate_spd(uint64_t seed) {
+void Chol::generate_spd(uint64_t seed, double rho) {
   factored = false;
   std::vector<double> d(n), pw(n);
-  host_spd_factors(n, seed, d.data(), pw.data());
+  host_spd_factors(n, seed, d.data(), pw.data(), rho);
   spd_d.alloc(n);
   spd_pw.alloc(n);
   SPH_CUDA(cudaMemcpyAsync(spd_d.get(), d.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream));
@@ -1907,6 +1925,17 @@ int sphemu_gpu_chol_flops(sphemu_chol_t h, double* f_dp, double* f_sp, double* f
   });
 }
 
+int sphemu_gpu_chol_generate_spd_decay(sphemu_chol_t h, uint64_t seed, double rho) {
+  return guard([&] {
+    if (!(rho > 0.0 && rho < 1.0)) throw std::invalid_argument("decay must lie in (0, 1)");
+    h->c->generate_spd(seed, rho);
+  });
+}
+
+int sphemu_gpu_chol_residual_probe_spd_decay(sphemu_chol_t h, uint64_t seed, double rho, int n_vec, double* out) {
+  return guard([&] { *out = h->c->residual_probe(seed, n_vec, rho); });
+}
+
 int sphemu_gpu_chol_residual_probe_spd(sphemu_chol_t h, uint64_t seed, int n_vec, double* out) {
   return guard([&] { *out = h->c->residual_probe(seed, n_vec); });
 }
@@ -1987,8 +2016,8 @@ int sphemu_gpu_dist_layout(int n, const sphemu_chol_config* cfg, int P, int Q, i
     if (arena_bytes) *arena_bytes = L.off.back();
     if (xchg_bytes) {
       std::fill(xchg_bytes, xchg_bytes + static_cast<size_t>(nt) * P * Q, int64_t{0});
-      for (int k = 0; k < static_cast<int>(L.xroots.size()); ++k)
-        for (const auto& x : L.xroots[k]) xchg_bytes[static_cast<size_t>(k) * P * Q + x.root] = x.bytes;
+      for (int k = 0; k < static_cast<int>(L.recv_bytes.size()); ++k)
+        for (int r = 0; r < P * Q; ++r) xchg_bytes[static_cast<size_t>(k) * P * Q + r] = L.recv_bytes[k][r];
     }
   });
 }

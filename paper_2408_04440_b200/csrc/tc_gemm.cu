@@ -1196,13 +1196,13 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
 
 // rng.hpp:12-39 uniform stream (mt19937_64, 53-bit in (0,1]) and
 // mpchol.cpp:423-429's d_i = exp(0.6u - 0.3), pw[k] = pow(0.9, k).
-void host_spd_factors(int n, uint64_t seed, double* d, double* pw) {
+void host_spd_factors(int n, uint64_t seed, double* d, double* pw, double rho) {
   std::mt19937_64 eng(seed);
   for (int i = 0; i < n; ++i) {
     const double u = static_cast<double>((eng() >> 11) + 1) * 0x1.0p-53;
     d[i] = std::exp(0.6 * u - 0.3);
   }
-  for (int k = 0; k < n; ++k) pw[k] = std::pow(0.9, k);
+  for (int k = 0; k < n; ++k) pw[k] = std::pow(rho, k);
 }
 
 }  // namespace sphemu_gpu

@@ -73,7 +73,9 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
                int max_ctas = 0, int* counter = nullptr);
 
 // Host-side inputs of make_spd_test_matrix: d_i = exp(0.6 u_i - 0.3) with the
-// reference's GaussianRng uniform stream, pw[k] = std::pow(0.9, k).
-void host_spd_factors(int n, uint64_t seed, double* d, double* pw);
+// reference's GaussianRng uniform stream, pw[k] = std::pow(rho, k) (rho = 0.9:
+// the reference generator; rho -> 1: the same D (I + K/4) D family with
+// O(1) off-diagonal tiles, K the Kac-Murdock-Szego matrix).
+void host_spd_factors(int n, uint64_t seed, double* d, double* pw, double rho = 0.9);
 
 }  // namespace sphemu_gpu
