@@ -281,6 +281,39 @@ int sphemu_gpu_emulate_chol(sphemu_chol_t h, sphemu_sht_t plan, const double* ph
  * the partial products so every rank receives the full xi. */
 int sphemu_gpu_chol_trmm(sphemu_chol_t h, const double* eta, int where_in, int64_t S, double* xi, int where_out);
 
+/* sphemu_gpu_emulate_chol with the model's trend as TrendModel records
+ * (points x (5 + 2*harmonics)) and a forcing trajectory, evaluated on the
+ * device like sphemu_gpu_emulate_trend (stochastic.cpp:229,262-273). */
+int sphemu_gpu_emulate_chol_trend(sphemu_chol_t h, sphemu_sht_t plan, const double* phi, int order,
+                                  const double* records, int harmonics, int period, const double* forcing_x,
+                                  int64_t n_x, const double* forcing_history, int64_t n_history, int64_t t_start,
+                                  const double* v2, int t_out, uint64_t seed, int r_begin, int r_count,
+                                  int rng_mode, double* out, int where_out);
+/* estimate_innovation_covariance keeping the factor on the device: *out is
+ * a factored handle of u_hat + nugget*I (for sphemu_gpu_emulate_chol*,
+ * sphemu_gpu_chol_store_dense, ...; destroy with sphemu_gpu_chol_destroy). */
+int sphemu_gpu_innovation_factor(const double* resid, int where_resid, int64_t n_rows, int d, int r_len,
+                                 int t_len, int order, const sphemu_chol_config* cfg, double* u_hat, int where_u,
+                                 double* nugget_out, sphemu_chol_stats* stats, sphemu_chol_t* out);
+/* Loads a stored lower factor (e.g. a model bundle's UCOV v, read_ucov,
+ * stochastic.cpp:323-350) into the handle's tiles as its factor: the tiles
+ * are quantized to the precision map like load_dense, no factorization runs. */
+int sphemu_gpu_chol_load_factor(sphemu_chol_t h, const double* l, int where, int64_t ldl);
+
+/* fit_trend(series, {}, TrendConfig{harmonics, period}) (trend.cpp:129-250)
+ * without forcing — the Python Emulator.train path (module.cpp:145-157): the
+ * pooled replicate mean and within-ensemble scatter, least squares on
+ * [1, cos(k base), sin(k base)] (a host Householder QR of the t_len x p
+ * design gives R^-1 Q^T; the projection and residual variance run per
+ * location on the device). series (r_len, t_len, points) host or device;
+ * records points x (5 + 2*harmonics) (trend.hpp:37-59) host or device. */
+int sphemu_gpu_fit_trend(const double* series, int where_in, int r_len, int t_len, int64_t points, int harmonics,
+                         int period, double* records, int where_out);
+/* fit_noise_field (stochastic.cpp:176-196): v2[loc] = mean over the n_slices
+ * (r, t) slices of (detrended - reconstructed)^2. */
+int sphemu_gpu_noise_field(const double* detrended, const double* reconstructed, int where_in, int64_t n_slices,
+                           int64_t points, double* v2, int where_out);
+
 /* fit_var (stochastic.cpp:30-107, declared stochastic.hpp:41): per packed
  * coefficient AR(order) least squares over an (r_len, t_len, d) coefficient
  * series. phi / phi_se: order x d host (row p-1 = lag p; may be NULL);

@@ -1126,6 +1126,15 @@ struct Chol {
 
   void generate_spd(uint64_t seed, double rho = 0.9);
 
+  // The loaded tiles are a factor already (a stored model's V): usable by
+  // trmm / emulate without factoring.
+  void mark_factored() {
+    SPH_CUDA(cudaEventRecord(ev0, stream));
+    SPH_CUDA(cudaEventRecord(ev1, stream));
+    launches = 0;
+    factored = true;
+  }
+
   // ---- the per-step operations, on a given stream and panel buffer set ----
   void op_potrf(int k, cudaStream_t s) {
     const int pe = prof_begin(kPotrf, s);
@@ -2022,6 +2031,70 @@ int sphemu_gpu_dist_layout(int n, const sphemu_chol_config* cfg, int P, int Q, i
   });
 }
 
+}  // extern "C"
+
+namespace sphemu_gpu {
+// estimate_innovation_covariance on the device; returns the factored handle
+// of u_hat + nugget I (owned by the caller).
+std::unique_ptr<Chol> innovation_factor(const double* resid, int where_resid, int64_t n_rows, int d, int r_len,
+                                        int t_len, int order, const sphemu_chol_config* cfg, double* u_hat,
+                                        int where_u, double* nugget_out, sphemu_chol_stats* stats) {
+  if (n_rows < 2 || d < 1) throw std::invalid_argument("residual sample is too small");
+  if (n_rows != static_cast<int64_t>(r_len) * (t_len - order))
+    throw std::invalid_argument("residual row count does not match r_len*(t_len-order)");
+  validate_config(*cfg);
+  DevBuf<double> xi_dev, xt, u_dev;
+  const double* xi = resid;
+  if (where_resid == SPHEMU_HOST) {
+    xi_dev.alloc(static_cast<size_t>(n_rows) * d);
+    SPH_CUDA(cudaMemcpy(xi_dev.get(), resid, sizeof(double) * n_rows * d, cudaMemcpyHostToDevice));
+    xi = xi_dev.get();
+  }
+  const int64_t ldt = (n_rows + 1) & ~int64_t{1};  // even stride: 16-byte rows for the DMMA loader
+  xt.alloc(static_cast<size_t>(d) * ldt);
+  k_transpose_pad<<<dim3(static_cast<unsigned>((ldt + 31) / 32), static_cast<unsigned>((d + 31) / 32)), dim3(32, 8)>>>(
+      xi, n_rows, d, xt.get(), ldt);
+  SPH_LAUNCH_CHECK();
+  double* U = (where_u == SPHEMU_DEVICE && u_hat) ? u_hat : nullptr;
+  if (!U) {
+    u_dev.alloc(static_cast<size_t>(d) * d);
+    U = u_dev.get();
+  }
+  smem_optin(reinterpret_cast<const void*>(k_cov_syrk), (int)sizeof(D2Smem));
+  k_cov_syrk<<<dim3(static_cast<unsigned>((d + D2_BN - 1) / D2_BN), static_cast<unsigned>((d + D2_BM - 1) / D2_BM)),
+               D2_THREADS, sizeof(D2Smem)>>>(xt.get(), ldt, n_rows, d, 1.0 / static_cast<double>(n_rows), U);
+  SPH_LAUNCH_CHECK();
+  std::vector<double> diag(d);
+  SPH_CUDA(cudaMemcpy2D(diag.data(), sizeof(double), U, sizeof(double) * (d + 1), sizeof(double), d,
+                        cudaMemcpyDeviceToHost));
+  double sum = 0.0;
+  for (double x : diag) sum += x;
+  const double mean_diag = sum / d;
+  if (!(mean_diag > 0.0)) throw std::runtime_error("innovation covariance has a non-positive mean diagonal");
+  xt.release();
+  xi_dev.release();
+  double nugget = (n_rows < d) ? 1e-8 * mean_diag : 0.0;
+  const double cap = 1e-2 * mean_diag;
+  std::unique_ptr<Chol> c(new Chol(d, *cfg));
+  while (true) {
+    c->load_dense(U, SPHEMU_DEVICE, d, nugget);
+    c->factor();
+    if (c->wait(stats) < 0) break;
+    const double next = (nugget == 0.0) ? 1e-8 * mean_diag : 10.0 * nugget;
+    if (next > cap)
+      throw std::runtime_error(
+          "innovation covariance is not positive definite even with the largest allowed diagonal inflation");
+    nugget = next;
+  }
+  if (nugget_out) *nugget_out = nugget;
+  if (u_hat && where_u == SPHEMU_HOST)
+    SPH_CUDA(cudaMemcpy(u_hat, U, sizeof(double) * d * d, cudaMemcpyDeviceToHost));
+  return c;
+}
+}  // namespace sphemu_gpu
+
+extern "C" {
+
 // estimate_innovation_covariance (stochastic.cpp:109-172) with the sample
 // covariance and every nugget retry on the device: U = Xi^T Xi / n by DMMA
 // (cov_kernels.cuh), then tiled factorizations of U + nugget I read straight
@@ -2032,57 +2105,28 @@ int sphemu_gpu_estimate_innovation_covariance(const double* resid, int where_res
                                               double* u_hat, int where_u, double* v, int where_v,
                                               double* nugget_out, sphemu_chol_stats* stats) {
   return guard([&] {
-    if (n_rows < 2 || d < 1) throw std::invalid_argument("residual sample is too small");
-    if (n_rows != static_cast<int64_t>(r_len) * (t_len - order))
-      throw std::invalid_argument("residual row count does not match r_len*(t_len-order)");
-    validate_config(*cfg);
-    DevBuf<double> xi_dev, xt, u_dev;
-    const double* xi = resid;
-    if (where_resid == SPHEMU_HOST) {
-      xi_dev.alloc(static_cast<size_t>(n_rows) * d);
-      SPH_CUDA(cudaMemcpy(xi_dev.get(), resid, sizeof(double) * n_rows * d, cudaMemcpyHostToDevice));
-      xi = xi_dev.get();
-    }
-    const int64_t ldt = (n_rows + 1) & ~int64_t{1};  // even stride: 16-byte rows for the DMMA loader
-    xt.alloc(static_cast<size_t>(d) * ldt);
-    k_transpose_pad<<<dim3(static_cast<unsigned>((ldt + 31) / 32), static_cast<unsigned>((d + 31) / 32)), dim3(32, 8)>>>(
-        xi, n_rows, d, xt.get(), ldt);
-    SPH_LAUNCH_CHECK();
-    double* U = (where_u == SPHEMU_DEVICE && u_hat) ? u_hat : nullptr;
-    if (!U) {
-      u_dev.alloc(static_cast<size_t>(d) * d);
-      U = u_dev.get();
-    }
-    smem_optin(reinterpret_cast<const void*>(k_cov_syrk), (int)sizeof(D2Smem));
-    k_cov_syrk<<<dim3(static_cast<unsigned>((d + D2_BN - 1) / D2_BN), static_cast<unsigned>((d + D2_BM - 1) / D2_BM)),
-                 D2_THREADS, sizeof(D2Smem)>>>(xt.get(), ldt, n_rows, d, 1.0 / static_cast<double>(n_rows), U);
-    SPH_LAUNCH_CHECK();
-    std::vector<double> diag(d);
-    SPH_CUDA(cudaMemcpy2D(diag.data(), sizeof(double), U, sizeof(double) * (d + 1), sizeof(double), d,
-                          cudaMemcpyDeviceToHost));
-    double sum = 0.0;
-    for (double x : diag) sum += x;
-    const double mean_diag = sum / d;
-    if (!(mean_diag > 0.0)) throw std::runtime_error("innovation covariance has a non-positive mean diagonal");
-    xt.release();
-    xi_dev.release();
-    double nugget = (n_rows < d) ? 1e-8 * mean_diag : 0.0;
-    const double cap = 1e-2 * mean_diag;
-    Chol c(d, *cfg);
-    while (true) {
-      c.load_dense(U, SPHEMU_DEVICE, d, nugget);
-      c.factor();
-      if (c.wait(stats) < 0) break;
-      const double next = (nugget == 0.0) ? 1e-8 * mean_diag : 10.0 * nugget;
-      if (next > cap)
-        throw std::runtime_error(
-            "innovation covariance is not positive definite even with the largest allowed diagonal inflation");
-      nugget = next;
-    }
-    if (nugget_out) *nugget_out = nugget;
-    if (v) c.store_dense(v, where_v, d);
-    if (u_hat && where_u == SPHEMU_HOST)
-      SPH_CUDA(cudaMemcpy(u_hat, U, sizeof(double) * d * d, cudaMemcpyDeviceToHost));
+    auto c = innovation_factor(resid, where_resid, n_rows, d, r_len, t_len, order, cfg, u_hat, where_u, nugget_out,
+                               stats);
+    if (v) c->store_dense(v, where_v, d);
+  });
+}
+
+int sphemu_gpu_innovation_factor(const double* resid, int where_resid, int64_t n_rows, int d, int r_len,
+                                 int t_len, int order, const sphemu_chol_config* cfg, double* u_hat, int where_u,
+                                 double* nugget_out, sphemu_chol_stats* stats, sphemu_chol_t* out) {
+  return guard([&] {
+    *out = nullptr;
+    auto c = innovation_factor(resid, where_resid, n_rows, d, r_len, t_len, order, cfg, u_hat, where_u, nugget_out,
+                               stats);
+    *out = new sphemu_chol_s{c.release()};
+  });
+}
+
+int sphemu_gpu_chol_load_factor(sphemu_chol_t h, const double* l, int where, int64_t ldl) {
+  return guard([&] {
+    Chol& c = *h->c;
+    c.load_dense(l, where, ldl);
+    c.mark_factored();
   });
 }
 
@@ -2112,10 +2156,37 @@ int sphemu_gpu_chol_trmm(sphemu_chol_t h, const double* eta, int where_in, int64
   });
 }
 
+static void emulate_chol_impl(sphemu_chol_t h, sphemu_sht_t plan, const double* phi, int order,
+                              const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed,
+                              int r_begin, int r_count, int rng_mode, double* out, int where_out,
+                              const TrendArgs* trend);
+
 int sphemu_gpu_emulate_chol(sphemu_chol_t h, sphemu_sht_t plan, const double* phi, int order, const double* means,
                             const double* sigma, const double* v2, int t_out, uint64_t seed, int r_begin,
                             int r_count, int rng_mode, double* out, int where_out) {
   return guard([&] {
+    emulate_chol_impl(h, plan, phi, order, means, sigma, v2, t_out, seed, r_begin, r_count, rng_mode, out, where_out,
+                      nullptr);
+  });
+}
+
+int sphemu_gpu_emulate_chol_trend(sphemu_chol_t h, sphemu_sht_t plan, const double* phi, int order,
+                                  const double* records, int harmonics, int period, const double* forcing_x,
+                                  int64_t n_x, const double* forcing_history, int64_t n_history, int64_t t_start,
+                                  const double* v2, int t_out, uint64_t seed, int r_begin, int r_count,
+                                  int rng_mode, double* out, int where_out) {
+  return guard([&] {
+    const TrendArgs ta{records, harmonics, period, forcing_x, n_x, forcing_history, n_history, t_start};
+    emulate_chol_impl(h, plan, phi, order, nullptr, nullptr, v2, t_out, seed, r_begin, r_count, rng_mode, out,
+                      where_out, &ta);
+  });
+}
+
+static void emulate_chol_impl(sphemu_chol_t h, sphemu_sht_t plan, const double* phi, int order,
+                              const double* means, const double* sigma, const double* v2, int t_out, uint64_t seed,
+                              int r_begin, int r_count, int rng_mode, double* out, int where_out,
+                              const TrendArgs* trend) {
+  {
     if (!h || !plan) throw std::invalid_argument("null handle");
     Chol& c = *h->c;
     EmulArgs a{};
@@ -2134,6 +2205,7 @@ int sphemu_gpu_emulate_chol(sphemu_chol_t h, sphemu_sht_t plan, const double* ph
     a.rng_mode = rng_mode;
     a.out = out;
     a.where_out = where_out;
+    a.trend = trend;
     a.world = c.P * c.Q;
     a.rank = c.rank;
     static const int64_t budget = [] {
@@ -2162,7 +2234,7 @@ int sphemu_gpu_emulate_chol(sphemu_chol_t h, sphemu_sht_t plan, const double* ph
       SPH_NCCL(ncclGroupEnd());
       note_launch();
     });
-  });
+  }
 }
 
 int sphemu_gpu_tiled_cholesky_dense(const double* a, int where_a, int n, const sphemu_chol_config* cfg,

@@ -339,7 +339,219 @@ void mean_table_device(const double* records, int64_t points, int harmonics, int
   // rp is a pageable host vector: the async copy above is staged before it returns.
 }
 
+// ---- fit_trend (trend.cpp:129-250) without forcing ---------------------------
+// Pooled ensemble mean (trend.cpp:144-150, replicates summed in order then
+// divided) and the within-ensemble scatter (trend.cpp:151-159), one thread
+// per location, every (r, t) row read coalesced.
+__global__ void k_trend_pool(const double* __restrict__ s, int r_len, int t_len, int64_t points,
+                             double* __restrict__ ybar, double* __restrict__ within) {
+  const int64_t loc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (loc >= points) return;
+  for (int t = 0; t < t_len; ++t) {
+    double acc = 0.0;
+    for (int r = 0; r < r_len; ++r) acc = __dadd_rn(acc, s[((int64_t)r * t_len + t) * points + loc]);
+    ybar[(int64_t)t * points + loc] = acc / r_len;
+  }
+  double w = 0.0;
+  for (int r = 0; r < r_len; ++r)
+    for (int t = 0; t < t_len; ++t) {
+      const double d = s[((int64_t)r * t_len + t) * points + loc] - ybar[(int64_t)t * points + loc];
+      w = __dadd_rn(w, __dmul_rn(d, d));
+    }
+  within[loc] = w;
+}
+
+// beta = Pinv ybar (Pinv = R^-1 Q^T of the design, p x t_len, broadcast reads),
+// then the residual sum of squares and the record (trend.cpp:230-249).
+template <int PMAX>
+__global__ void k_trend_solve(const double* __restrict__ ybar, int t_len, int64_t points, int p,
+                              const double* __restrict__ pinv, const double* __restrict__ x, const double* within,
+                              int r_len, int harmonics, double* __restrict__ rec) {
+  const int64_t loc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (loc >= points) return;
+  double beta[PMAX];
+#pragma unroll
+  for (int c = 0; c < PMAX; ++c) beta[c] = 0.0;
+  for (int t = 0; t < t_len; ++t) {
+    const double y = ybar[(int64_t)t * points + loc];
+#pragma unroll
+    for (int c = 0; c < PMAX; ++c)
+      if (c < p) beta[c] = fma(__ldg(pinv + (int64_t)c * t_len + t), y, beta[c]);
+  }
+  double rss = 0.0;
+  for (int t = 0; t < t_len; ++t) {
+    double fit = 0.0;
+#pragma unroll
+    for (int c = 0; c < PMAX; ++c)
+      if (c < p) fit = fma(__ldg(x + (int64_t)t * p + c), beta[c], fit);
+    const double e = ybar[(int64_t)t * points + loc] - fit;
+    rss = fma(e, e, rss);
+  }
+  const int stride = 5 + 2 * harmonics;
+  double* o = rec + loc * stride;
+  o[0] = beta[0];
+  o[1] = o[2] = o[3] = 0.0;
+#pragma unroll
+  for (int k = 0; k < (PMAX - 1) / 2; ++k)
+    if (k < harmonics) {
+      o[4 + k] = beta[1 + 2 * k];
+      o[4 + harmonics + k] = beta[2 + 2 * k];
+    }
+  const double var = (r_len * rss + within[loc]) / (static_cast<double>(r_len) * t_len);
+  o[stride - 1] = sqrt(fmax(var, 1e-12));  // kSigmaFloor (trend.cpp:16)
+}
+
+// fit_noise_field (stochastic.cpp:176-196): mean over slices of (a - b)^2.
+__global__ void k_noise_field(const double* __restrict__ a, const double* __restrict__ b, int64_t n_slices,
+                              int64_t points, double* __restrict__ v2) {
+  const int64_t loc = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (loc >= points) return;
+  double acc = 0.0;
+  for (int64_t sl = 0; sl < n_slices; ++sl) {
+    const double e = a[sl * points + loc] - b[sl * points + loc];
+    acc = __dadd_rn(acc, __dmul_rn(e, e));
+  }
+  v2[loc] = acc * (1.0 / static_cast<double>(n_slices));
+}
+
+// Householder QR of the t_len x p design (column-major work copy), giving
+// Pinv = R^-1 Q^T (p x t_len) — the least-squares solve of
+// Eigen::HouseholderQR::solve (trend.cpp:231-232) as one matrix.
+std::vector<double> design_pinv(const std::vector<double>& x, int m, int p) {
+  std::vector<double> a(x);  // row-major m x p
+  std::vector<double> qt((size_t)m * m, 0.0);  // accumulate Q^T applied to I, only first p rows needed
+  std::vector<std::vector<double>> vs;
+  std::vector<double> taus;
+  for (int k = 0; k < p; ++k) {
+    double nrm = 0.0;
+    for (int i = k; i < m; ++i) nrm += a[(size_t)i * p + k] * a[(size_t)i * p + k];
+    nrm = std::sqrt(nrm);
+    const double alpha = a[(size_t)k * p + k] >= 0 ? -nrm : nrm;
+    std::vector<double> v(m, 0.0);
+    for (int i = k; i < m; ++i) v[i] = a[(size_t)i * p + k];
+    v[k] -= alpha;
+    double vn = 0.0;
+    for (int i = k; i < m; ++i) vn += v[i] * v[i];
+    const double tau = vn > 0.0 ? 2.0 / vn : 0.0;
+    for (int j = k; j < p; ++j) {
+      double d = 0.0;
+      for (int i = k; i < m; ++i) d += v[i] * a[(size_t)i * p + j];
+      d *= tau;
+      for (int i = k; i < m; ++i) a[(size_t)i * p + j] -= d * v[i];
+    }
+    vs.push_back(std::move(v));
+    taus.push_back(tau);
+  }
+  // rows 0..p-1 of Q^T: apply H_{p-1} ... H_0 to e_i^T from the left, i.e. Q^T = H_{p-1} .. H_0
+  std::vector<double> pinv((size_t)p * m, 0.0);
+  std::vector<double> col(m);
+  for (int t = 0; t < m; ++t) {  // column t of Q^T = Q^T e_t
+    std::fill(col.begin(), col.end(), 0.0);
+    col[t] = 1.0;
+    for (int k = 0; k < p; ++k) {
+      double d = 0.0;
+      for (int i = k; i < m; ++i) d += vs[k][i] * col[i];
+      d *= taus[k];
+      for (int i = k; i < m; ++i) col[i] -= d * vs[k][i];
+    }
+    // back-substitute R z = (Q^T e_t)[0:p]
+    for (int c = p - 1; c >= 0; --c) {
+      double acc = col[c];
+      for (int j = c + 1; j < p; ++j) acc -= a[(size_t)c * p + j] * pinv[(size_t)j * m + t];
+      pinv[(size_t)c * m + t] = acc / a[(size_t)c * p + c];
+    }
+  }
+  return pinv;
+}
+
+void fit_trend_device(const double* series, int where_in, int r_len, int t_len, int64_t points, int harmonics,
+                      int period, double* records, int where_out) {
+  if (period != 12 && period != 365 && period != 8760)
+    throw std::invalid_argument("period must be 12, 365 or 8760 steps per year");  // trend.cpp:28-34
+  if (harmonics < 0) throw std::invalid_argument("harmonics must be non-negative");
+  if (2 * harmonics >= period) throw std::invalid_argument("harmonics must stay below half the period");
+  if (r_len < 1 || t_len < 1 || points < 1) throw std::invalid_argument("series needs t_len, r_len >= 1");
+  if (t_len < 4 + 2 * harmonics)
+    throw std::invalid_argument("need at least 4 + 2*harmonics time steps to fit the trend");
+  if (harmonics > 7) throw std::invalid_argument("harmonics above 7 are not supported by the device trend fit");
+  const int p = 1 + 2 * harmonics;
+  // design rows t = 1..t_len: 1, cos(k base), sin(k base) (trend.cpp:96-111)
+  std::vector<double> x((size_t)t_len * p);
+  for (int row = 0; row < t_len; ++row) {
+    const int64_t t = row + 1;
+    double* o = x.data() + (size_t)row * p;
+    o[0] = 1.0;
+    const double base = kTwoPi * static_cast<double>(t % period) / period;
+    for (int k = 1; k <= harmonics; ++k) {
+      o[1 + 2 * (k - 1)] = std::cos(base * k);
+      o[2 + 2 * (k - 1)] = std::sin(base * k);
+    }
+  }
+  const std::vector<double> pinv = design_pinv(x, t_len, p);
+  const size_t n = (size_t)r_len * t_len * points;
+  DevBuf<double> d_in, ybar((size_t)t_len * points), within(points), d_x(x.size()), d_p(pinv.size()), d_rec;
+  const double* s = series;
+  if (where_in == SPHEMU_HOST) {
+    d_in.alloc(n);
+    SPH_CUDA(cudaMemcpy(d_in.get(), series, n * sizeof(double), cudaMemcpyHostToDevice));
+    s = d_in.get();
+  }
+  SPH_CUDA(cudaMemcpy(d_x.get(), x.data(), x.size() * sizeof(double), cudaMemcpyHostToDevice));
+  SPH_CUDA(cudaMemcpy(d_p.get(), pinv.data(), pinv.size() * sizeof(double), cudaMemcpyHostToDevice));
+  const int stride = 5 + 2 * harmonics;
+  double* rec = records;
+  if (where_out == SPHEMU_HOST) {
+    d_rec.alloc((size_t)points * stride);
+    rec = d_rec.get();
+  }
+  const unsigned grid = (unsigned)ceil_div(points, 128);
+  k_trend_pool<<<grid, 128>>>(s, r_len, t_len, points, ybar.get(), within.get());
+  SPH_LAUNCH_CHECK();
+  k_trend_solve<15><<<grid, 128>>>(ybar.get(), t_len, points, p, d_p.get(), d_x.get(), within.get(), r_len,
+                                   harmonics, rec);
+  SPH_LAUNCH_CHECK();
+  if (where_out == SPHEMU_HOST)
+    SPH_CUDA(cudaMemcpy(records, rec, (size_t)points * stride * sizeof(double), cudaMemcpyDeviceToHost));
+  SPH_CUDA(cudaDeviceSynchronize());
+}
+
 }  // namespace sphemu_gpu
+
+extern "C" int sphemu_gpu_fit_trend(const double* series, int where_in, int r_len, int t_len, int64_t points,
+                                    int harmonics, int period, double* records, int where_out) {
+  using namespace sphemu_gpu;
+  return guard([&] { fit_trend_device(series, where_in, r_len, t_len, points, harmonics, period, records, where_out); });
+}
+
+extern "C" int sphemu_gpu_noise_field(const double* detrended, const double* reconstructed, int where_in,
+                                      int64_t n_slices, int64_t points, double* v2, int where_out) {
+  using namespace sphemu_gpu;
+  return guard([&] {
+    if (n_slices < 1 || points < 1) throw std::invalid_argument("empty series");
+    const size_t n = (size_t)n_slices * points;
+    DevBuf<double> da, db, dv;
+    const double* a = detrended;
+    const double* b = reconstructed;
+    if (where_in == SPHEMU_HOST) {
+      da.alloc(n);
+      db.alloc(n);
+      SPH_CUDA(cudaMemcpy(da.get(), detrended, n * sizeof(double), cudaMemcpyHostToDevice));
+      SPH_CUDA(cudaMemcpy(db.get(), reconstructed, n * sizeof(double), cudaMemcpyHostToDevice));
+      a = da.get();
+      b = db.get();
+    }
+    double* v = v2;
+    if (where_out == SPHEMU_HOST) {
+      dv.alloc(points);
+      v = dv.get();
+    }
+    k_noise_field<<<(unsigned)ceil_div(points, 128), 128>>>(a, b, n_slices, points, v);
+    SPH_LAUNCH_CHECK();
+    if (where_out == SPHEMU_HOST) SPH_CUDA(cudaMemcpy(v2, v, points * sizeof(double), cudaMemcpyDeviceToHost));
+    SPH_CUDA(cudaDeviceSynchronize());
+  });
+}
+
 
 extern "C" int sphemu_gpu_mean_table(const double* records, int64_t points, int harmonics, int period,
                                      const double* forcing_x, int64_t n_x, const double* forcing_history,
