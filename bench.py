@@ -372,6 +372,43 @@ def time_factor(sph, h, wl, args, world, a_dev=None, steps=None, warmup=None, cl
     return ms, st, launches, clocks
 
 
+def c1_point(sph):
+    """BASELINE configs[0] (C1) end to end: the acceptance-pattern daily
+    series (180 x 360, L = 45, T = 100, seed 91) -> Emulator.train(K = 2,
+    period 365, P = 3, chol dp b = 256) -> emulate(100 steps, seed 42, 10
+    replicates, reference RNG), on the GPU through the Python drop-in, and
+    the oracle's restatement of the same pipeline on the host cores; wall
+    time of each and the parity of the trained model and the fields."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    O.build()
+    x = O.synth_training_series(180, 360, 45, 100, 1, 91, period=365)
+    kw = dict(harmonics=2, period=365, var_order=3, band_limit=45, tile_size=256)
+    sph.Emulator.train(x, **kw).emulate(4, seed=1, replicates=1)  # warm-up: module load, plan, kernels
+    t0 = time.perf_counter()
+    em = sph.Emulator.train(x, **kw)
+    t1 = time.perf_counter()
+    got = em.emulate(100, seed=42, replicates=10)
+    t2 = time.perf_counter()
+    cores = os.cpu_count() or 1
+    m = O.train(x, 2, 365, 3, 45, "dp", 256)
+    t3 = time.perf_counter()
+    want = O.emulate_model(m, 100, 42, 10, threads=cores)
+    t4 = time.perf_counter()
+    rel = lambda a, b: float(np.abs(a - b).max() / np.abs(b).max())
+    return {"workload": "C1: 180x360 L=45 T=100 daily synthetic series (acceptance_main.cpp:535-559, seed 91); "
+                        "train K=2 period 365 P=3 chol dp b=256; emulate 10 x 100 steps seed 42",
+            "gpu_s": {"train": t1 - t0, "emulate": t2 - t1, "total": t2 - t0},
+            "cpu_s": {"train": t3 - t2, "emulate": t4 - t3, "total": t4 - t2, "cores": cores,
+                      "kind": "port (oracle restatement of pipeline.cpp/stochastic.cpp/trend.cpp)"},
+            "speedup_total": (t4 - t2) / (t2 - t0),
+            "parity": {"nugget_gpu": em.nugget, "nugget_cpu": m["nugget"],
+                       "trend_rel": rel(em.records, m["records"]), "factor_rel": rel(em.factor(), m["v"]),
+                       "fields_rel": rel(got, want), "tolerance": 1e-9},
+            "api": "paper_2408_04440_b200.Emulator.train / .emulate (module.cpp:232-243 drop-in)"}
+
+
 def kms_probe(h, rho=0.999):
     """Parity where the flops are: the reference generator's 0.9 decay leaves
     every tile beyond distance 1 ~0 at b >= 256, so the handle is refactored on
@@ -761,6 +798,7 @@ def run_ours(args, world, rank, local):
     sht = sht_throughput(sph, world)
     c4 = sht_c4(sph) if (world == 1 and not args.no_c4) else None
     side = model_side_points(sph) if (world == 1 and not args.no_c4) else None
+    c1 = c1_point(sph) if (world == 1 and not args.no_c1) else None
 
     if rank != 0:
         return
@@ -802,6 +840,8 @@ def run_ours(args, world, rank, local):
         line["emulation"] = emul
     if side:
         line["model_side"] = side
+    if c1:
+        line["c1"] = c1
     emit(line)
 
 
@@ -835,6 +875,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the L=720 SHT point on N=1")
     ap.add_argument("--no-emul", action="store_true", help="skip the emulation points")
+    ap.add_argument("--no-c1", action="store_true", help="skip the C1 end-to-end pipeline point")
     ap.add_argument("--lookahead", type=int, default=1)
     ap.add_argument("--sp-compute", default="fp16x3", choices=["fp16x3", "tf32x3", "fp64"])
     args = ap.parse_args()

@@ -225,6 +225,14 @@ double sphemu_gpu_sht_plan_seconds(sphemu_sht_t p);
 int sphemu_gpu_wigner_d_half_pi(int band_limit, size_t wigner_cap_bytes, int64_t n, const int* l, const int* m2,
                                 const int* m, double* out, int* renorm_warnings);
 
+/* build_wigner_tables(band_limit, cap) (wigner.cpp:49-134) on the device,
+ * copied out: offsets[m2 * band_limit + m] (band_limit^2 + 1 entries) is the
+ * start of the d^l_{m2,m}(pi/2) chain for l = max(m2, m) .. band_limit - 1 in
+ * d (d_count = offsets[band_limit^2] entries = sum_k (2k+1)(band_limit-k)),
+ * the layout of WignerTables::d_ / d_offset_ (wigner.hpp:36-41). */
+int sphemu_gpu_wigner_tables(int band_limit, size_t wigner_cap_bytes, int64_t* offsets, double* d, int64_t d_count,
+                             int* renorm_warnings);
+
 /* ======================================================================
  * Emulation generator (replaces stochastic.hpp:84-86 emulate)
  * ====================================================================== */

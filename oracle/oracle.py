@@ -456,3 +456,109 @@ def fit_var(coeffs, order):
         unstable += rad >= 1.0 - 1e-8
     return dict(phi=phi, phi_se=se, residuals=res, zeroed_count=int(zeroed), unstable_count=int(unstable),
                 residual_mean_norm=float(np.linalg.norm(res.mean(axis=0))))
+
+
+# ----------------------------------------------------------------------------
+# train pipeline (pipeline.cpp:18-54) restated over the pieces above — the C1
+# end-to-end checker (test infrastructure only)
+# ----------------------------------------------------------------------------
+def fit_trend(series, harmonics, period):
+    """fit_trend(series, {}, TrendConfig) without forcing (trend.cpp:129-250):
+    pooled mean over replicates, least squares by Householder QR (numpy's
+    LAPACK QR for Eigen's HouseholderQR), sigma from the pooled residual plus
+    the within-ensemble scatter, floored at 1e-12."""
+    x = np.asarray(series, dtype=np.float64)
+    if x.ndim == 2:
+        x = x[None]
+    r_len, t_len = x.shape[0], x.shape[1]
+    points = x[0, 0].size
+    y = x.reshape(r_len, t_len, points)
+    ybar = np.zeros((t_len, points))
+    for r in range(r_len):
+        ybar += y[r]
+    ybar /= r_len
+    within = np.zeros(points)
+    for r in range(r_len):
+        d = y[r] - ybar
+        within += (d * d).sum(axis=0)
+    p = 1 + 2 * harmonics
+    t = np.arange(1, t_len + 1)
+    base = 2.0 * np.pi * (t % period) / period
+    X = np.empty((t_len, p))
+    X[:, 0] = 1.0
+    for k in range(1, harmonics + 1):
+        X[:, 2 * k - 1] = np.cos(base * k)
+        X[:, 2 * k] = np.sin(base * k)
+    q, rr = np.linalg.qr(X)
+    beta = np.linalg.solve(rr, q.T @ ybar)
+    resid = ybar - X @ beta
+    rec = np.zeros((points, 5 + 2 * harmonics))
+    rec[:, 0] = beta[0]
+    for k in range(harmonics):
+        rec[:, 4 + k] = beta[1 + 2 * k]
+        rec[:, 4 + harmonics + k] = beta[2 + 2 * k]
+    var = (r_len * (resid * resid).sum(axis=0) + within) / (r_len * t_len)
+    rec[:, -1] = np.sqrt(np.maximum(var, 1e-12))
+    return rec
+
+
+def estimate_innovation_covariance(xi, variant="dp", tile=128):
+    n, d = xi.shape
+    u, v = np.empty((d, d)), np.empty((d, d))
+    nug = C.c_double()
+    st = CholStats()
+    rc = lib().so_estimate_innovation_covariance(np.ascontiguousarray(xi), n, d, C.byref(config(variant, tile)), 1,
+                                                 u, v, C.byref(nug), C.byref(st))
+    if rc:
+        raise RuntimeError("innovation covariance is not positive definite")
+    return u, v, nug.value
+
+
+def train(series, harmonics, period, var_order, band_limit, variant="dp", tile=128):
+    """train(series, {}, TrainConfig) (pipeline.cpp:18-54): returns the model dict."""
+    x = np.asarray(series, dtype=np.float64)
+    if x.ndim == 3:
+        x = x[None]
+    r_len, t_len, nt, nphi = x.shape
+    rec = fit_trend(x, harmonics, period)
+    std = trend_apply("detrend", x.reshape(r_len, t_len, nt * nphi), rec, harmonics, period)
+    plan = Plan(nt, nphi, band_limit)
+    coeffs = plan.forward(std.reshape(-1, nt, nphi)).reshape(r_len, t_len, -1)
+    vf = fit_var(coeffs, var_order)
+    u, v, nug = estimate_innovation_covariance(vf["residuals"], variant, tile)
+    recon = plan.inverse(coeffs.reshape(r_len * t_len, -1)).reshape(r_len, t_len, nt * nphi)
+    e = std.reshape(r_len, t_len, -1) - recon
+    v2 = (e * e).sum(axis=(0, 1)) / (r_len * t_len)
+    return dict(records=rec, phi=vf["phi"], u_hat=u, v=v, nugget=nug, v2=v2, plan=plan, harmonics=harmonics,
+                period=period, grid=(nt, nphi), band_limit=band_limit)
+
+
+def emulate_model(model, t_out, seed, r_len=1, t_start=1, threads=1):
+    """emulate(model, plan, {}, t_out, seed, r_len, threads, t_start) (stochastic.cpp:217-277)."""
+    means = mean_table(model["records"], model["harmonics"], model["period"], t_out, t_start)
+    sigma = np.ascontiguousarray(model["records"][:, -1])
+    return emulate(model["plan"], model["v"], model["phi"] if model["phi"].shape[0] else None, means, sigma,
+                   model["v2"], t_out, seed, r_len, threads)
+
+
+def synth_training_series(n_theta, n_phi, band_limit, t_len, r_len, seed, period=12):
+    """AR(1)-in-coefficients series with a seasonal cycle
+    (acceptance_main.cpp:535-559): state = 0.55 state + 0.5/(1+l) N(0,1) per
+    slot, inverse SHT, + 1.7 + 1.1 cos(2 pi (t+1)/period) + 0.05 N(0,1); one
+    GaussianRng stream (slots, then points, per step)."""
+    d = band_limit * band_limit
+    points = n_theta * n_phi
+    plan = Plan(n_theta, n_phi, band_limit)
+    z = normals(seed, r_len * t_len * (d + points)).reshape(r_len, t_len, d + points)
+    deg = np.floor(np.sqrt(np.arange(d))).astype(int)
+    scale = 0.5 / (1.0 + deg)
+    out = np.empty((r_len, t_len, n_theta, n_phi))
+    for r in range(r_len):
+        state = np.zeros(d)
+        for t in range(t_len):
+            for i in range(d):  # sequential like the reference (no vectorized FMA differences)
+                state[i] = 0.55 * state[i] + scale[i] * z[r, t, i]
+            synth = plan.inverse(state[None])[0].reshape(points)
+            season = 1.1 * np.cos(2.0 * np.pi * (t + 1) / period)
+            out[r, t] = (1.7 + season + synth + 0.05 * z[r, t, d:]).reshape(n_theta, n_phi)
+    return out

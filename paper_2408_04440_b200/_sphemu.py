@@ -135,6 +135,15 @@ def lib():
         L.sphemu_gpu_fit_var.argtypes = [vp, C.c_int, C.c_int, C.c_int, i64, C.c_int, vp, vp, vp, C.c_int,
                                          C.POINTER(i64), C.POINTER(i64), dp]
         L.sphemu_gpu_chol_trmm.argtypes = [vp, vp, C.c_int, i64, vp, C.c_int]
+        L.sphemu_gpu_fit_trend.argtypes = [vp, C.c_int, C.c_int, C.c_int, i64, C.c_int, C.c_int, vp, C.c_int]
+        L.sphemu_gpu_noise_field.argtypes = [vp, vp, C.c_int, i64, i64, vp, C.c_int]
+        L.sphemu_gpu_innovation_factor.argtypes = [vp, C.c_int, i64, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                   C.POINTER(CholConfig), vp, C.c_int, dp, C.POINTER(CholStats),
+                                                   C.POINTER(vp)]
+        L.sphemu_gpu_chol_load_factor.argtypes = [vp, vp, C.c_int, i64]
+        L.sphemu_gpu_emulate_chol_trend.argtypes = [vp, vp, vp, C.c_int, vp, C.c_int, C.c_int, vp, i64, vp, i64,
+                                                    i64, vp, C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_int, vp,
+                                                    C.c_int]
         L.sphemu_gpu_emulate_chol.argtypes = [vp, vp, vp, C.c_int, vp, vp, vp, C.c_int, C.c_uint64, C.c_int,
                                               C.c_int, C.c_int, vp, C.c_int]
         L.sphemu_gpu_detrend.argtypes = trend

@@ -1029,6 +1029,32 @@ int sphemu_gpu_wigner_d_half_pi(int band_limit, size_t wigner_cap_bytes, int64_t
   });
 }
 
+int sphemu_gpu_wigner_tables(int band_limit, size_t wigner_cap_bytes, int64_t* offsets, double* d, int64_t d_count,
+                             int* renorm_warnings) {
+  return guard([&] {
+    using namespace sphemu_gpu;
+    const size_t cap = wigner_cap_bytes ? wigner_cap_bytes : (size_t{2} << 30);
+    check_wigner_cap(band_limit, cap);
+    cudaStream_t s = nullptr;
+    SPH_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+    } sg{s};
+    WignerDev w;
+    build_wigner_device(w, band_limit, cap, s);
+    const size_t n_off = static_cast<size_t>(band_limit) * band_limit + 1;
+    std::vector<int64_t> off(n_off);
+    SPH_CUDA(cudaMemcpyAsync(off.data(), w.off.get(), n_off * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    SPH_CUDA(cudaStreamSynchronize(s));
+    if (d_count != off.back()) throw std::invalid_argument("d buffer size does not match the table");
+    std::copy(off.begin(), off.end(), offsets);
+    SPH_CUDA(cudaMemcpyAsync(d, w.d.get(), static_cast<size_t>(d_count) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SPH_CUDA(cudaStreamSynchronize(s));
+    if (renorm_warnings) *renorm_warnings = w.renorm;
+  });
+}
+
 int sphemu_gpu_emulate(sphemu_sht_t p, const double* v, int d, const double* phi, int order, const double* means,
                        const double* sigma, const double* v2, int t_out, uint64_t seed, int r_len, int rng_mode,
                        double* out) {

@@ -10,6 +10,7 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs through the C-ABI on cuda:0)")
+    config.addinivalue_line("markers", "slow: full-size configuration (minutes)")
 
 
 @pytest.fixture(scope="session")

@@ -192,6 +192,85 @@ int main() {
     CHECK(w->d_half_pi(3, 4, 0) == 0.0);
     CHECK(throws<std::out_of_range>([&] { w->d_half_pi(8, 0, 0); }));
   }
+  // test_wigner.cpp:23-31 factorial sums
+  CHECK(std::fabs(wigner_brute_force(1, 1, -1) - 0.5) < 1e-14);
+  CHECK(std::fabs(wigner_brute_force(2, 2, 0) - std::sqrt(3.0 / 8.0)) < 1e-14);
+  {  // test_wigner.cpp:33-43 recursion vs factorial sum, l <= 12
+    auto t = build_wigner_tables(13);
+    double worst = 0.0;
+    for (int l = 0; l <= 12; ++l)
+      for (int m2 = -l; m2 <= l; ++m2)
+        for (int m = -l; m <= l; ++m)
+          worst = std::fmax(worst, std::fabs(t->d_half_pi(l, m2, m) - wigner_brute_force(l, m2, m)));
+    CHECK(worst < 1e-12);
+  }
+  {  // test_wigner.cpp:45-59 orthonormal rows, no renormalization
+    auto t = build_wigner_tables(32);
+    CHECK(t->renormalization_warnings() == 0);
+    double worst = 0.0;
+    for (int l = 0; l < 32; ++l)
+      for (int m = 0; m <= l; ++m)
+        for (int mp = m; mp <= l; ++mp) {
+          double dot = 0.0;
+          for (int m2 = -l; m2 <= l; ++m2) dot += t->d_half_pi(l, m2, m) * t->d_half_pi(l, m2, mp);
+          worst = std::fmax(worst, std::fabs(dot - (m == mp ? 1.0 : 0.0)));
+        }
+    CHECK(worst < 1e-10);
+  }
+  {  // test_wigner.cpp:61-73 synthesis products, sizes
+    auto t = build_wigner_tables(4);
+    CHECK(std::fabs(t->q(0, 0, 0) - 0.2820947917738781) < 1e-15);
+    CHECK(std::fabs(t->q(1, 0, 1) - std::sqrt(3.0 / (4.0 * std::numbers::pi)) * 0.5) < 1e-15);
+    CHECK(t->q(1, 1, 3) == 0.0);
+    CHECK(t->q_entry_count() == 4u * 4u * 5u / 2u);
+    CHECK(t->memory_bytes() == WignerTables::estimated_bytes(4));
+    CHECK(throws<std::out_of_range>([&] { t->q(4, 0, 0); }));
+  }
+  {  // test_wigner.cpp:75-104 WIGD cache round trip, load_or_build
+    auto built = build_wigner_tables(10);
+    const std::string path = "/tmp/sphemu_cpp_tables.wigd";
+    write_wigd(path, *built);
+    auto loaded = read_wigd(path);
+    CHECK(loaded->band_limit() == 10 && loaded->renormalization_warnings() == built->renormalization_warnings());
+    bool same = true;
+    for (int l = 0; l < 10; ++l)
+      for (int m2 = -l; m2 <= l; ++m2)
+        for (int m = 0; m <= l; ++m) same &= loaded->d_half_pi(l, m2, m) == built->d_half_pi(l, m2, m);
+    for (int l = 0; l < 10; ++l)
+      for (int m = 0; m <= l; ++m)
+        for (int m2 = 0; m2 <= l; ++m2) same &= loaded->q(l, m, m2) == built->q(l, m, m2);
+    CHECK(same);
+    std::remove("/tmp/sphemu_cpp_cache.wigd");
+    auto first = load_or_build_wigner(6, "/tmp/sphemu_cpp_cache.wigd");
+    auto second = load_or_build_wigner(6, "/tmp/sphemu_cpp_cache.wigd");
+    CHECK(second->band_limit() == 6 && second->d_half_pi(5, 3, 2) == first->d_half_pi(5, 3, 2));
+    auto third = load_or_build_wigner(7, "/tmp/sphemu_cpp_cache.wigd");  // mismatched band limit: rebuilt
+    CHECK(third->band_limit() == 7);
+  }
+  // test_sht.cpp:51-59 I(q) known answers
+  CHECK(i_integral(0).real() == 2.0 && i_integral(2).real() == 2.0 / (1.0 - 4.0));
+  CHECK(i_integral(1).imag() == std::numbers::pi / 2.0 && i_integral(-1).imag() == -std::numbers::pi / 2.0);
+  CHECK(i_integral(3) == std::complex<double>(0.0, 0.0));
+  {  // generators (sht.cpp:406-527): Legendre vs the plan, random fields, energy quadrature
+    CHECK(std::fabs(normalized_legendre(0, 0, 0.3) - 1.0 / std::sqrt(4.0 * std::numbers::pi)) < 1e-15);
+    CHECK(throws<std::out_of_range>([] { normalized_legendre(2, 3, 0.1); }));
+    HarmonicVector c1 = draw_random_coefficients(8, 5), c2 = draw_random_coefficients(8, 5);
+    CHECK(c1.values == c2.values && c1.values != draw_random_coefficients(8, 6).values);
+    ShtPlan p8 = build_plan(GridSpec{17, 32}, 8);
+    EquiangularField f = synth_random_field(p8, 5);
+    EquiangularField direct = synth_bandlimited(c1, p8.spec);
+    double md = 0.0;
+    for (std::size_t e = 0; e < f.values.size(); ++e) md = std::fmax(md, std::fabs(f.values[e] - direct.values[e]));
+    CHECK(md < 1e-10);
+    CHECK(synth_random_field(GridSpec{17, 32}, 8, 5).values == f.values);
+    // Parseval (test_sht.cpp:135-143): energy quadrature = sum |f_lm|^2 for a band-limited field
+    CHECK(std::fabs(field_energy_quadrature(f) - c1.parseval_energy()) < 1e-8 * c1.parseval_energy());
+    // quadrature oracle (test_sht.cpp:104-110): a single Y_{2,1} pattern is recovered
+    HarmonicVector q = quadrature_oracle_sht(
+        [](double th, double ph) { return std::sin(th) * std::cos(th) * std::cos(ph); }, 4, 4001);
+    CHECK(std::fabs(q.values[HarmonicVector::index_mean(2)]) < 1e-6);
+    CHECK(std::fabs(q.values[HarmonicVector::index_im(2, 1)]) < 1e-6 && std::fabs(q.values[HarmonicVector::index_re(2, 1)]) > 0.1);
+  }
 
   // covariance + nugget (test_stochastic.cpp:159-210)
   {
