@@ -32,6 +32,21 @@ class WignerTables {
   double d_half_pi(int l, int m2, int m) const {
     if (l < 0 || l >= band_limit_) throw std::out_of_range("degree outside the table");
     ensure();
+    return d_raw(l, m2, m);
+  }
+
+  // q(l, m, m2) = sqrt((2l+1)/(4 pi)) d^l_{m2,0} d^l_{m2,m} (wigner.cpp:152-170).
+  double q(int l, int m, int m2) const {
+    if (l < 0 || l >= band_limit_ || m < 0 || m > l || m2 < 0 || m2 >= band_limit_)
+      throw std::out_of_range("q index outside the table");
+    if (m2 > l) return 0.0;
+    ensure();
+    return q_[(static_cast<std::size_t>(l) * (l + 1) / 2 + m) * band_limit_ + m2];
+  }
+
+ private:
+  // d_half_pi on filled tables (no ensure: build_q runs inside the fill)
+  double d_raw(int l, int m2, int m) const {
     if (std::abs(m2) > l || std::abs(m) > l) return 0.0;
     int sign = 1;
     if (m2 < 0) {
@@ -46,14 +61,7 @@ class WignerTables {
     return sign * d_[o + l - std::max(m2, m)];
   }
 
-  // q(l, m, m2) = sqrt((2l+1)/(4 pi)) d^l_{m2,0} d^l_{m2,m} (wigner.cpp:152-170).
-  double q(int l, int m, int m2) const {
-    if (l < 0 || l >= band_limit_ || m < 0 || m > l || m2 < 0 || m2 >= band_limit_)
-      throw std::out_of_range("q index outside the table");
-    if (m2 > l) return 0.0;
-    ensure();
-    return q_[(static_cast<std::size_t>(l) * (l + 1) / 2 + m) * band_limit_ + m2];
-  }
+ public:
 
   std::size_t q_entry_count() const {
     ensure();
@@ -107,7 +115,7 @@ class WignerTables {
       const double norm = std::sqrt((2.0 * l + 1.0) / (4.0 * 3.14159265358979323846));
       for (int m = 0; m <= l; ++m) {
         const std::size_t row = (static_cast<std::size_t>(l) * (l + 1) / 2 + m) * big_l;
-        for (int m2 = 0; m2 <= l; ++m2) q_[row + m2] = norm * d_half_pi(l, m2, 0) * d_half_pi(l, m2, m);
+        for (int m2 = 0; m2 <= l; ++m2) q_[row + m2] = norm * d_raw(l, m2, 0) * d_raw(l, m2, m);
       }
     }
   }
