@@ -114,11 +114,25 @@ int sphemu_gpu_release_cache(void);
 int sphemu_gpu_dist_layout(int n, const sphemu_chol_config* cfg, int P, int Q, int rank, int64_t* tiles_owned,
                            int64_t* arena_bytes, int64_t* xchg_bytes);
 
+/* Tile-norm precision policy ("tile-centric" precision), an
+ * opt-in next to the band rule of assign_precisions: tile Frobenius norms of
+ * the dense row-major A (host or device) on the device, then, off the DP
+ * band, tile (i, j) takes the lowest precision the variant allows with
+ * u_p ||A_ij||_F <= tolerance ||A||_F / n_tiles (u: 2^-53, 2^-24, 2^-11 fp16 /
+ * 2^-8 bf16) — the tiles' storage rounding then sums to <= tolerance ||A||_F.
+ * map: n_tiles (n_tiles + 1) / 2 bytes, packed i(i+1)/2 + j, SPHEMU_PREC_*. */
+int sphemu_gpu_tile_norm_precisions(const double* a, int where, int64_t lda, int n, const sphemu_chol_config* cfg,
+                                    double tolerance, uint8_t* map);
+
 /* Device-resident factorization handle (TiledMatrix + tiled_cholesky,
  * mpchol.hpp:47-71,135): tiles live in HBM at their storage precision. */
 typedef struct sphemu_chol_s* sphemu_chol_t;
 int sphemu_gpu_chol_create(int n, const sphemu_chol_config* cfg, sphemu_chol_t* out);
 int sphemu_gpu_chol_destroy(sphemu_chol_t h);
+/* The same handle with an explicit precision map (e.g. from
+ * sphemu_gpu_tile_norm_precisions) in place of assign_precisions; diagonal
+ * tiles must be SPHEMU_PREC_DP. */
+int sphemu_gpu_chol_create_map(int n, const sphemu_chol_config* cfg, const uint8_t* map, sphemu_chol_t* out);
 /* 2D block-cyclic distribution over a P x Q grid of GPUs (one process per
  * GPU, the caller sets the device first): off-diagonal tile (i, j) is
  * stored on rank (i mod P) * Q + (j mod Q), diagonal tile (i, i) on rank

@@ -237,14 +237,21 @@ def quantize(x: np.ndarray, prec: int, hp_format="fp16"):
 
 
 def tiled_cholesky(a: np.ndarray, variant="dp", tile_size=128, workers=1, band_width_dp=1,
-                   sp_fraction=0.05, hp_format="fp16"):
+                   sp_fraction=0.05, hp_format="fp16", precision_map=None):
     a = np.ascontiguousarray(a, dtype=np.float64)
     n = a.shape[0]
     out = np.empty_like(a)
     st = CholStats()
     failed = C.c_int(-1)
     cfg = config(variant, tile_size, band_width_dp, sp_fraction, workers, hp_format)
-    rc = lib().so_tiled_cholesky_dense(a, n, C.byref(cfg), out, C.byref(st), C.byref(failed))
+    if precision_map is not None:
+        pm = np.ascontiguousarray(precision_map, dtype=np.uint8)
+        lib().so_tiled_cholesky_dense_map.argtypes = [C.c_void_p, C.c_int, C.POINTER(CholConfig), C.c_void_p,
+                                                      C.c_void_p, C.POINTER(CholStats), C.POINTER(C.c_int)]
+        rc = lib().so_tiled_cholesky_dense_map(a.ctypes.data, n, C.byref(cfg), pm.ctypes.data, out.ctypes.data,
+                                               C.byref(st), C.byref(failed))
+    else:
+        rc = lib().so_tiled_cholesky_dense(a, n, C.byref(cfg), out, C.byref(st), C.byref(failed))
     if rc == 1:
         raise NotPositiveDefinite(failed.value)
     if rc:
@@ -561,4 +568,29 @@ def synth_training_series(n_theta, n_phi, band_limit, t_len, r_len, seed, period
             synth = plan.inverse(state[None])[0].reshape(points)
             season = 1.1 * np.cos(2.0 * np.pi * (t + 1) / period)
             out[r, t] = (1.7 + season + synth + 0.05 * z[r, t, d:]).reshape(n_theta, n_phi)
+    return out
+
+
+def tile_norm_precisions(a, variant, tile_size, band_width_dp=1, tolerance=1e-8, hp_format="fp16"):
+    """The tile-norm ("tile-centric") precision rule restated:
+    off the DP band, tile (i, j) takes the lowest precision p the variant
+    allows with u_p ||A_ij||_F <= tolerance ||A||_F / nt (so the storage
+    rounding of all tiles sums to <= tolerance ||A||_F in Frobenius norm);
+    packed i(i+1)/2 + j, 0/1/2 = dp/sp/hp."""
+    a = np.asarray(a, dtype=np.float64)
+    n = a.shape[0]
+    nt = (n + tile_size - 1) // tile_size
+    total = np.linalg.norm(a)
+    allowed = {"dp": [0], "dpsp": [1, 0], "dpsphp": [2, 1, 0], "dphp": [2, 0]}[variant]
+    u = {0: 2.0 ** -53, 1: 2.0 ** -24, 2: 2.0 ** -11 if hp_format == "fp16" else 2.0 ** -8}
+    out = np.zeros(nt * (nt + 1) // 2, dtype=np.uint8)
+    for i in range(nt):
+        for j in range(i + 1):
+            if i - j < band_width_dp:
+                continue
+            t = np.linalg.norm(a[i * tile_size:(i + 1) * tile_size, j * tile_size:(j + 1) * tile_size])
+            for p in allowed:
+                if u[p] * t <= tolerance * total / nt:
+                    out[i * (i + 1) // 2 + j] = p
+                    break
     return out

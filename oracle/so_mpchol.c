@@ -428,9 +428,16 @@ static double now_s(void) {
   return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
 }
 
-/* mpchol.cpp:351-410 */
+/* mpchol.cpp:351-410; map (optional): an explicit precision map replacing
+ * assign_precisions (the tile-norm policy of the GPU path). */
+static int tiled_cholesky_impl(double* tiles, int n, const so_chol_config* c, const uint8_t* map,
+                               so_chol_stats* st, int* failed_tile);
 int so_tiled_cholesky(double* tiles, int n, const so_chol_config* c, so_chol_stats* st,
                       int* failed_tile) {
+  return tiled_cholesky_impl(tiles, n, c, NULL, st, failed_tile);
+}
+static int tiled_cholesky_impl(double* tiles, int n, const so_chol_config* c, const uint8_t* map,
+                               so_chol_stats* st, int* failed_tile) {
   if (so_config_validate(c) || n < 1) return -1;
   const double t0 = now_s();
   sched s;
@@ -443,7 +450,8 @@ int so_tiled_cholesky(double* tiles, int n, const so_chol_config* c, so_chol_sta
   s.off = tile_offsets(n, s.b);
   const int nt = s.nt;
   uint8_t* pmap = malloc((size_t)nt * (nt + 1) / 2);
-  so_assign_precisions(nt, c, pmap);
+  if (map) memcpy(pmap, map, (size_t)nt * (nt + 1) / 2);
+  else so_assign_precisions(nt, c, pmap);
   s.pmap = pmap;
   s.count = so_task_count(nt);
   s.kind = malloc((size_t)s.count);
@@ -532,6 +540,17 @@ int so_tiled_cholesky_dense(const double* a, int n, const so_chol_config* c, dou
   double* tiles = malloc(sizeof(double) * (size_t)so_tiled_size(n, c->tile_size));
   so_tiled_from_dense(a, n, c->tile_size, tiles);
   int rc = so_tiled_cholesky(tiles, n, c, st, failed_tile);
+  if (rc == 0) so_tiled_to_dense_lower(tiles, n, c->tile_size, factor);
+  free(tiles);
+  return rc;
+}
+
+int so_tiled_cholesky_dense_map(const double* a, int n, const so_chol_config* c, const uint8_t* map,
+                                double* factor, so_chol_stats* st, int* failed_tile) {
+  if (so_config_validate(c) || n < 1) return -1;
+  double* tiles = malloc(sizeof(double) * (size_t)so_tiled_size(n, c->tile_size));
+  so_tiled_from_dense(a, n, c->tile_size, tiles);
+  int rc = tiled_cholesky_impl(tiles, n, c, map, st, failed_tile);
   if (rc == 0) so_tiled_to_dense_lower(tiles, n, c->tile_size, factor);
   free(tiles);
   return rc;

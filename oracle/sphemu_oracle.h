@@ -97,6 +97,8 @@ void so_tiled_to_dense_lower(const double* tiles, int n, int b, double* a);
 int so_tiled_cholesky(double* tiles, int n, const so_chol_config* c, so_chol_stats* st,
                       int* failed_tile);
 /* mpchol.cpp:412-417 */
+int so_tiled_cholesky_dense_map(const double* a, int n, const so_chol_config* c, const uint8_t* map,
+                                double* factor, so_chol_stats* st, int* failed_tile);
 int so_tiled_cholesky_dense(const double* a, int n, const so_chol_config* c, double* factor,
                             so_chol_stats* st, int* failed_tile);
 /* mpchol.cpp:419-435 */

@@ -27,6 +27,7 @@ from ._sphemu import (  # noqa: F401
     retrend,
     synth_bandlimited,
     tiled_cholesky,
+    tile_norm_precisions,
     wigner_d_half_pi,
 )
 from .emulator import Emulator, read_sphf, write_sphf  # noqa: F401
@@ -35,5 +36,5 @@ __all__ = [
     "Cholesky", "ForcingTrajectory", "NotPositiveDefiniteError", "ShtPlan", "__version__", "assign_precisions", "emulate", "emulate_model",
     "estimate_innovation_covariance", "fit_var", "forward_sht", "inverse_sht", "make_spd_matrix", "nccl_unique_id", "max_band_limit", "resolution_summary",
     "synth_bandlimited", "tiled_cholesky", "wigner_d_half_pi", "mean_table", "detrend", "retrend",
-    "Emulator", "read_sphf", "write_sphf",
+    "Emulator", "read_sphf", "write_sphf", "tile_norm_precisions",
 ]

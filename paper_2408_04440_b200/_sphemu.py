@@ -135,6 +135,9 @@ def lib():
         L.sphemu_gpu_fit_var.argtypes = [vp, C.c_int, C.c_int, C.c_int, i64, C.c_int, vp, vp, vp, C.c_int,
                                          C.POINTER(i64), C.POINTER(i64), dp]
         L.sphemu_gpu_chol_trmm.argtypes = [vp, vp, C.c_int, i64, vp, C.c_int]
+        L.sphemu_gpu_chol_create_map.argtypes = [C.c_int, C.POINTER(CholConfig), vp, C.POINTER(vp)]
+        L.sphemu_gpu_tile_norm_precisions.argtypes = [vp, C.c_int, i64, C.c_int, C.POINTER(CholConfig), C.c_double,
+                                                      vp]
         L.sphemu_gpu_fit_trend.argtypes = [vp, C.c_int, C.c_int, C.c_int, i64, C.c_int, C.c_int, vp, C.c_int]
         L.sphemu_gpu_noise_field.argtypes = [vp, vp, C.c_int, i64, i64, vp, C.c_int]
         L.sphemu_gpu_innovation_factor.argtypes = [vp, C.c_int, i64, C.c_int, C.c_int, C.c_int, C.c_int,
@@ -191,13 +194,39 @@ def make_config(variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_frac
 # ---------------------------------------------------------------------------
 # module.cpp:209-214 tiled_cholesky / make_spd_matrix
 # ---------------------------------------------------------------------------
+def tile_norm_precisions(a, variant="dpsphp", tile_size=128, band_width_dp=1, tolerance=1e-8, hp_format="fp16"):
+    """Tile-norm precision map (sphemu_gpu_tile_norm_precisions): off the DP
+    band, each tile takes the lowest precision the variant allows with
+    u_p ||A_ij||_F <= tolerance ||A||_F / n_tiles."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    n = a.shape[0]
+    nt = (n + tile_size - 1) // tile_size
+    cfg = make_config(variant, tile_size, 1, band_width_dp, 0.05, hp_format)
+    out = np.empty(nt * (nt + 1) // 2, dtype=np.uint8)
+    _check(lib().sphemu_gpu_tile_norm_precisions(_ptr(a), HOST, n, n, C.byref(cfg), C.c_double(tolerance), _ptr(out)))
+    return out
+
+
 def tiled_cholesky(a, variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_fraction=0.05,
-                   hp_format="fp16", compute="tensor", lookahead=1, sp_compute="fp16x3"):
-    """Tiled Cholesky factorization; returns (lower_factor, stats_json)."""
+                   hp_format="fp16", compute="tensor", lookahead=1, sp_compute="fp16x3", precision_policy="band",
+                   norm_tolerance=1e-8):
+    """Tiled Cholesky factorization; returns (lower_factor, stats_json).
+    precision_policy="norm" replaces the band rule by the tile-norm map
+    (tile_norm_precisions) at norm_tolerance."""
     a = np.ascontiguousarray(a, dtype=np.float64)
     if a.ndim != 2 or a.shape[0] != a.shape[1]:
         raise ValueError("expected a square matrix")
     n = a.shape[0]
+    if precision_policy not in ("band", "norm"):
+        raise ValueError(f"unknown precision policy: {precision_policy}")
+    if precision_policy == "norm":
+        pm = tile_norm_precisions(a, variant, tile_size, band_width_dp, norm_tolerance, hp_format)
+        h = Cholesky(n, variant, tile_size, workers, band_width_dp, sp_fraction, hp_format, compute, lookahead,
+                     sp_compute, precision_map=pm)
+        h.load(a)
+        h.factor()
+        st = h.wait()
+        return h.factor_dense(), st.to_json()
     cfg = make_config(variant, tile_size, workers, band_width_dp, sp_fraction, hp_format, compute, lookahead,
                       sp_compute)
     out = np.empty_like(a)
@@ -235,14 +264,20 @@ class Cholesky:
     on rank 0 (None elsewhere)."""
 
     def __init__(self, n, variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_fraction=0.05,
-                 hp_format="fp16", compute="tensor", lookahead=1, sp_compute="fp16x3", dist=None):
+                 hp_format="fp16", compute="tensor", lookahead=1, sp_compute="fp16x3", dist=None,
+                 precision_map=None):
         self.n = n
         self.cfg = make_config(variant, tile_size, workers, band_width_dp, sp_fraction, hp_format,
                                compute, lookahead, sp_compute)
         h = C.c_void_p()
         self.rank = 0
         self.dist = dist
-        if dist is None:
+        if precision_map is not None:
+            if dist is not None:
+                raise ValueError("explicit precision maps are single-GPU")
+            pm = np.ascontiguousarray(precision_map, dtype=np.uint8)
+            _check(lib().sphemu_gpu_chol_create_map(n, C.byref(self.cfg), _ptr(pm), C.byref(h)))
+        elif dist is None:
             _check(lib().sphemu_gpu_chol_create(n, C.byref(self.cfg), C.byref(h)))
         else:
             P, Q, rank, uid = dist

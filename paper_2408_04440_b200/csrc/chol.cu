@@ -154,6 +154,60 @@ std::vector<uint8_t> assign_precisions(int nt, const sphemu_chol_config& c) {
   return map;
 }
 
+// Squared Frobenius norm of every b x b tile of a dense row-major A (both
+// triangles; the lower ones feed the tile-norm precision policy). One CTA per
+// tile, coalesced row reads, warp-shuffle + smem reduction.
+__global__ void k_tile_sqnorms(const double* __restrict__ a, int64_t lda, int n, int b, double* sq) {
+  const int ti = blockIdx.y, tj = blockIdx.x;
+  const int r0 = ti * b, c0 = tj * b;
+  const int rows = min(b, n - r0), cols = min(b, n - c0);
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+    const double v = a[(int64_t)(r0 + e / cols) * lda + c0 + e % cols];
+    acc = fma(v, v, acc);
+  }
+  __shared__ double red[32];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    acc = warp_sum(acc);
+    if (threadIdx.x == 0) sq[(int64_t)ti * gridDim.x + tj] = acc;
+  }
+}
+
+// The tile-norm ("tile-centric") precision rule, opt-in next to
+// the band rule of mpchol.cpp:67-93: off the DP band, tile (i, j) takes the
+// lowest precision the variant allows with u_p ||A_ij||_F <= tol ||A||_F / nt,
+// so the storage rounding of all tiles sums to <= tol ||A||_F (Frobenius).
+void tile_norm_map(const std::vector<double>& sq, int nt, const sphemu_chol_config& c, double tol, uint8_t* map) {
+  double total = 0.0;
+  for (double v : sq) total += v;
+  total = std::sqrt(total);
+  const double u_dp = 0x1.0p-53, u_sp = 0x1.0p-24, u_hp = c.hp_format == SPHEMU_HP_BF16 ? 0x1.0p-8 : 0x1.0p-11;
+  std::vector<std::pair<int, double>> allowed;
+  switch (c.variant) {
+    case SPHEMU_VARIANT_DP: allowed = {{SPHEMU_PREC_DP, u_dp}}; break;
+    case SPHEMU_VARIANT_DPSP: allowed = {{SPHEMU_PREC_SP, u_sp}, {SPHEMU_PREC_DP, u_dp}}; break;
+    case SPHEMU_VARIANT_DPSPHP: allowed = {{SPHEMU_PREC_HP, u_hp}, {SPHEMU_PREC_SP, u_sp}, {SPHEMU_PREC_DP, u_dp}}; break;
+    default: allowed = {{SPHEMU_PREC_HP, u_hp}, {SPHEMU_PREC_DP, u_dp}}; break;
+  }
+  for (int i = 0; i < nt; ++i)
+    for (int j = 0; j <= i; ++j) {
+      uint8_t p = SPHEMU_PREC_DP;
+      if (i - j >= c.band_width_dp) {
+        const double t = std::sqrt(sq[static_cast<size_t>(i) * nt + j]);
+        for (const auto& a : allowed)
+          if (a.second * t <= tol * total / nt) {
+            p = static_cast<uint8_t>(a.first);
+            break;
+          }
+      }
+      map[static_cast<size_t>(i) * (i + 1) / 2 + j] = p;
+    }
+}
+
 // Row scale exponents for the FP16x3 path: |L_rj| <= sqrt(A_rr), so with
 // sqrt(A_rr) = m 2^E (m in [0.5, 1)) every operand of row r times 2^(14-E)
 // stays below 2^14 in magnitude.
@@ -928,7 +982,8 @@ struct Chol {
     return TileStore{arena.get(), d_off.get(), d_prec.get(), n, b, nt, lb};
   }
 
-  Chol(int n_, const sphemu_chol_config& c, int P_ = 1, int Q_ = 1, int rank_ = 0, ncclComm_t comm_ = nullptr)
+  Chol(int n_, const sphemu_chol_config& c, int P_ = 1, int Q_ = 1, int rank_ = 0, ncclComm_t comm_ = nullptr,
+       const uint8_t* map = nullptr)
       : n(n_), P(P_), Q(Q_), rank(rank_), comm(comm_), cfg(c) {
     validate_config(cfg);
     if (n < 1) throw std::invalid_argument("matrix is empty");
@@ -940,6 +995,15 @@ struct Chol {
     b = (lb + granule - 1) / granule * granule;
     nt = (n + lb - 1) / lb;
     pmap = assign_precisions(nt, cfg);
+    if (map) {  // an explicit precision map (the tile-norm policy): the diagonal stays DP (POTRF is FP64)
+      for (int i = 0; i < nt; ++i)
+        for (int j = 0; j <= i; ++j) {
+          const uint8_t p = map[tix(i, j)];
+          if (p > SPHEMU_PREC_HP) throw std::invalid_argument("precision map entries must be 0, 1 or 2");
+          if (i == j && p != SPHEMU_PREC_DP) throw std::invalid_argument("diagonal tiles must be double precision");
+        }
+      pmap.assign(map, map + pmap.size());
+    }
     sprec.resize(pmap.size());
     for (size_t t = 0; t < pmap.size(); ++t)
       sprec[t] = static_cast<uint8_t>(pmap[t] == SPHEMU_PREC_DP
@@ -1836,6 +1900,43 @@ int sphemu_gpu_assign_precisions(int n_tiles, const sphemu_chol_config* cfg, uin
   return guard([&] {
     auto m = assign_precisions(n_tiles, *cfg);
     std::memcpy(out, m.data(), m.size());
+  });
+}
+
+int sphemu_gpu_chol_create_map(int n, const sphemu_chol_config* cfg, const uint8_t* map, sphemu_chol_t* out) {
+  return guard([&] {
+    *out = nullptr;
+    auto* h = new sphemu_chol_s{nullptr};
+    try {
+      h->c = new Chol(n, *cfg, 1, 1, 0, nullptr, map);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int sphemu_gpu_tile_norm_precisions(const double* a, int where, int64_t lda, int n, const sphemu_chol_config* cfg,
+                                    double tolerance, uint8_t* map) {
+  return guard([&] {
+    validate_config(*cfg);
+    if (n < 1) throw std::invalid_argument("matrix is empty");
+    if (!(tolerance > 0.0)) throw std::invalid_argument("norm tolerance must be positive");
+    const int b = cfg->tile_size, nt = (n + b - 1) / b;
+    const size_t nel = static_cast<size_t>(n) * lda;
+    DevBuf<double> da, sq(static_cast<size_t>(nt) * nt);
+    const double* A = a;
+    if (where == SPHEMU_HOST) {
+      da.alloc(nel);
+      SPH_CUDA(cudaMemcpy(da.get(), a, nel * sizeof(double), cudaMemcpyHostToDevice));
+      A = da.get();
+    }
+    k_tile_sqnorms<<<dim3(nt, nt), 256>>>(A, lda, n, b, sq.get());
+    SPH_LAUNCH_CHECK();
+    std::vector<double> h(static_cast<size_t>(nt) * nt);
+    SPH_CUDA(cudaMemcpy(h.data(), sq.get(), h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    tile_norm_map(h, nt, *cfg, tolerance, map);
   });
 }
 

@@ -276,3 +276,36 @@ def test_epilogue_saturation_matches_oracle(sph, O):
         import json
         assert json.loads(js)["conversions"]["half_saturations"] == ro["conversions"]["half_saturations"] > 0
         assert np.abs(f - ref).max() <= 1e-3 * np.abs(ref).max()
+
+
+# ---- tile-norm precision policy (opt-in next to mpchol.cpp:67-93) ----
+@pytest.mark.parametrize("name", ["xtx2048", "kms999"])
+@pytest.mark.parametrize("variant", ["dpsp", "dpsphp", "dphp"])
+def test_tile_norm_policy_matches_oracle(sph, O, name, variant):
+    """The device tile norms give the oracle's map; the factorization on that
+    map matches the oracle run on the same map within the class bounds, and
+    the backward error stays at the policy's tolerance scale."""
+    a, b = inputs(O, name)
+    for tol in (1e-6, 1e-9):
+        pm = sph.tile_norm_precisions(a, variant, b, tolerance=tol)
+        assert np.array_equal(pm, O.tile_norm_precisions(a, variant, b, tolerance=tol))
+        f, js = sph.tiled_cholesky(a, variant, tile_size=b, precision_policy="norm", norm_tolerance=tol,
+                                   sp_compute="fp64")
+        ref, st = O.tiled_cholesky(a, variant, tile_size=b, workers=WORKERS, precision_map=pm)
+        r, r_ref = O.relative_residual(a, f), O.relative_residual(a, ref)
+        assert r <= 1.15 * r_ref + 1e-15, (tol, r, r_ref)
+
+
+def test_tile_norm_policy_on_reference_generator(sph, O):
+    """On make_spd_test_matrix the norm rule demotes the vanishing far tiles to
+    HP and keeps the distance-1 tiles wide: far better accuracy than the band
+    rule's dpsphp at nearly the same memory."""
+    a = O.make_spd(2048, 1)
+    pm = sph.tile_norm_precisions(a, "dpsphp", 256, tolerance=1e-8)
+    nt = 8
+    dist1 = [pm[i * (i + 1) // 2 + i - 1] for i in range(1, nt)]
+    far = [pm[i * (i + 1) // 2 + j] for i in range(nt) for j in range(i - 1)]
+    assert all(p != 2 for p in dist1) and all(p == 2 for p in far)
+    f, _ = sph.tiled_cholesky(a, "dpsphp", tile_size=256, precision_policy="norm", norm_tolerance=1e-8)
+    g, _ = sph.tiled_cholesky(a, "dpsphp", tile_size=256)
+    assert O.relative_residual(a, f) < 1e-6 < O.relative_residual(a, g)
