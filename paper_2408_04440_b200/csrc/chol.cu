@@ -572,15 +572,27 @@ struct Chol {
   DevBuf<int2> lists;
   DevBuf<int> lrows;  // per update-list entry: the C tile's arena row (see constructor)
   // Dynamic work claiming for the persistent tcgen05 kernels: one counter per
-  // stream (kernels on one stream run in order; the memset precedes each
-  // launch). SPHEMU_TC_DYN=0 falls back to static striding.
+  // (stream, class) (kernels on one stream run in order; the memset precedes
+  // each launch, a resumed launch continues from its class's counter).
+  // SPHEMU_TC_DYN=0 falls back to static striding.
   DevBuf<int> sched_ctr;
-  int* ctr(cudaStream_t s) {
+  int* ctr(cudaStream_t s, int cls) {
     static const bool on = [] {
       const char* e = std::getenv("SPHEMU_TC_DYN");
       return !(e && e[0] == '0');
     }();
-    return on ? sched_ctr.get() + (s == pstream ? 1 : 0) : nullptr;
+    return on ? sched_ctr.get() + (s == pstream ? 4 : 0) + cls : nullptr;
+  }
+  // Bulk yield: the chain raises the flag when the next panel is ready; the
+  // bulk's persistent CTAs stop claiming items so the panel gets the SMs, and
+  // the bulk resumes after it (SPHEMU_YIELD=0 disables).
+  DevBuf<int> yield_flag;
+  static bool yield_on() {
+    static const bool on = [] {
+      const char* e = std::getenv("SPHEMU_YIELD");
+      return !(e && e[0] == '0');
+    }();
+    return on;
   }
   // Update lists per (step k, part, class): part 0 = next column (k+1, the
   // critical chain), part 1 = the rest (columns >= k+2, the bulk).
@@ -1025,7 +1037,9 @@ struct Chol {
       for (int p = 0; p < 2; ++p) p64_[p].alloc(static_cast<size_t>(nt - 1) * b * b);
     fail.alloc(1);
     sat.alloc(1);
-    sched_ctr.alloc(2);
+    sched_ctr.alloc(8);  // [stream][class 0..2, 3 = panel]
+    yield_flag.alloc(1);
+    SPH_CUDA(cudaMemset(yield_flag.get(), 0, sizeof(int)));
     // Per-step output-tile lists by precision class.
     list_off.assign(static_cast<size_t>(nt) * kParts * 3 + 1, 0);
     list_cnt.assign(static_cast<size_t>(nt) * kParts * 3, 0);
@@ -1215,7 +1229,7 @@ struct Chol {
     if (cfg.compute == SPHEMU_COMPUTE_TENSOR) {
       const int2* base = plists.get() + plist_off[k];
       tc_panel_trsm(store(), k, base, plist_dp[k], base + plist_dp[k], plist_lo[k], linv_[set].get(),
-                    p64_[set].get(), panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s));
+                    p64_[set].get(), panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s, 3));
     } else {
       const int below = nt - k - 1;
       k_panel_trsm_fp64<<<dim3(below * (b / DG_BM), b / DG_BN), DG_THREADS, 0, s>>>(
@@ -1246,17 +1260,19 @@ struct Chol {
     return cls == SPHEMU_PREC_DP || (cls == SPHEMU_PREC_SP && cfg.sp_compute == SPHEMU_SP_FP64);
   }
 
-  void op_update(int k, int part, cudaStream_t s, int max_ctas) {
+  void op_update(int k, int part, cudaStream_t s, int max_ctas, const int* yield = nullptr, bool resume = false) {
     const int set = k & 1;
     for (int cls = 0; cls < 3; ++cls) {
       const size_t slot = (static_cast<size_t>(k) * kParts + part) * 3 + cls;
       const int64_t cnt = list_cnt[slot];
       if (!cnt) continue;
       const int2* lst = lists.get() + list_off[slot];
+      const bool tensor = !fp64_class(cls) && cfg.compute == SPHEMU_COMPUTE_TENSOR;
+      if (resume && !tensor) continue;  // only the persistent tcgen05 launches yield
       const int pu = prof_begin(kUpdDp + cls, s);
-      if (!fp64_class(cls) && cfg.compute == SPHEMU_COMPUTE_TENSOR) {
+      if (tensor) {
         tc_update(store(), k, cls, cfg.hp_format, lst, lrows.get() + list_off[slot], cnt, p64_[set].get(),
-                  panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s));
+                  panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s, cls), yield, resume);
       } else {
         if (b % D2_BM == 0 && !(part == 0 && chain_small_syrk())) {
           smem_optin(reinterpret_cast<const void*>(k_update_fp64_v2), (int)sizeof(D2Smem));
@@ -1338,13 +1354,22 @@ struct Chol {
         SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k], 0));
         op_update(k, 2, stream, 0);
         SPH_CUDA(cudaEventRecord(ev_colrest[k], stream));
+        const bool yield = yield_on() && k + 2 < nt;
         if (k + 2 < nt) {
           SPH_CUDA(cudaStreamWaitEvent(pstream, ev_colrest[k], 0));
+          // the bulk of step k hands its SMs to panel(k+1) and resumes after it
+          if (yield) SPH_CUDA(cudaMemsetAsync(yield_flag.get(), 1, sizeof(int), pstream));
           op_panel(k + 1, pstream);
+          if (yield) SPH_CUDA(cudaMemsetAsync(yield_flag.get(), 0, sizeof(int), pstream));
         }
         SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
         col_out(k + 1, pstream);
-        op_update(k, 1, stream, std::max(1, num_sms() - reserve));
+        const int bulk_ctas = std::max(1, num_sms() - reserve);
+        op_update(k, 1, stream, bulk_ctas, yield ? yield_flag.get() : nullptr);
+        if (yield) {
+          SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k + 1], 0));
+          op_update(k, 1, stream, bulk_ctas, nullptr, true);
+        }
         SPH_CUDA(cudaEventRecord(ev_bulk[k], stream));
       }
       SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[nt - 1], 0));
@@ -1604,11 +1629,13 @@ struct Chol {
                        S, xi, s);
     static const int flush_env = [] {
       const char* e = std::getenv("SPHEMU_TRMM_FLUSH_K");
-      return e ? std::atoi(e) : 512;
+      return e ? std::atoi(e) : 8192;
     }();
-    // fp32 TMEM partial sums over at most max(b, 512) of K: the tensor cores'
-    // truncating fp32 accumulation error grows with the length (measured
-    // max rel. error 1.1e-6 at 512, 4.5e-6 at 2048, 8.9e-6 at 8192).
+    // fp32 TMEM partial sums over at most max(b, 8192) of K before the FP64
+    // add: the tensor cores' truncating fp32 accumulation error grows with
+    // the length (measured max rel. error 1.1e-6 at 512, 4.5e-6 at 2048,
+    // 8.9e-6 at 8192) while every flush is an FP64 read-modify-write of the
+    // 128 x 256 output block (at K = 512 those dominated the traffic).
     const int flush = std::max(1, flush_env / b);
     for (int c = 0; c < 2; ++c) {
       if (tp.ent[c].empty()) continue;
@@ -1627,7 +1654,10 @@ struct Chol {
           for (int nb = 0; nb < nblk; ++nb) its.push_back({cnt, make_int4(i, mb * 128, nb * 256, 0)});
         }
       }
-      std::stable_sort(its.begin(), its.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+      // snapshot-block-major (the eta block stays in L2), longest rows first within a block
+      std::stable_sort(its.begin(), its.end(), [](const auto& x, const auto& y) {
+        return x.second.z != y.second.z ? x.second.z < y.second.z : x.first > y.first;
+      });
       std::vector<int4> items(its.size());
       for (size_t e = 0; e < its.size(); ++e) items[e] = its[e].second;
       DevBuf<int4> d_items(items.size());

@@ -150,9 +150,11 @@ struct TcArgs {
   const int* fail;
   unsigned* sat;
   int dbg;           // diagnostics only (SPHEMU_TC_DBG): 1 = skip the C epilogue, 2 = also skip the MMAs
-  int opt;           // tuning switches (SPHEMU_TC_OPT): 1 = no C prefetch to L2, 2 = prefetch two items ahead
+  int opt;           // tuning switches (SPHEMU_TC_OPT): 1 = no C prefetch to L2, 2 = prefetch two items ahead,
+                     // 4 = operands evict_first (not evict_last), 8 = C through L2 normally (not streaming)
   int* counter;      // non-null: items are claimed dynamically (atomicAdd), zeroed before the launch
   const int* lexp;   // FP16x3 panel: per output column (Linv row) power-of-two exponent
+  const int* yield;  // non-null: stop claiming items once *yield != 0 (dynamic scheduling only)
 };
 
 template <int OPK>
@@ -321,6 +323,7 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t keep = (args.opt & 4) ? l2_evict_first() : l2_evict_last();  // SPHEMU_TC_OPT bit 2: A/B test
       // Update mode: pull the C sub-tile of the next work item into L2 while
       // this one's MMAs run, so the epilogue's C loads hit L2 instead of
       // waiting on HBM latency.
@@ -341,6 +344,8 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
           for (int cx = 0; cx < BN; cx += 128 / kEszP) tma_prefetch_l2_2d(&mC, tn + cx, crow + tm + rq);
       };
       auto fetch = [&]() -> int64_t {
+        // a yield request stops new claims; claimed items are always processed
+        if (args.yield && *(volatile const int*)args.yield) return -1;
         const int64_t v = atomicAdd(args.counter, 1);
         return v < items ? v : -1;
       };
@@ -388,23 +393,25 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * Lay::kStage;
           const int kx = kb * T::kBK;
+          // The panel operands are re-read by every work item of the step
+          // while the C tiles stream through once: keep them in L2.
           if constexpr (CG == 2) {
             // both CTAs' bytes complete on the leader's full barrier
             const uint32_t fb = mapa_shared(&full[stage], 0);
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], CG * Lay::kStage);
-            tma_load_2d_cg2(&mA_hi, fb, st, kx, a_row);
-            tma_load_2d_cg2(&mB_hi, fb, st + Lay::kA, kx, b_row);
+            tma_load_2d_cg2_hint(&mA_hi, fb, st, kx, a_row, keep);
+            tma_load_2d_cg2_hint(&mB_hi, fb, st + Lay::kA, kx, b_row, keep);
             if (T::kSplit) {
-              tma_load_2d_cg2(&mA_lo, fb, st + Lay::kA + Lay::kB, kx, a_row);
-              tma_load_2d_cg2(&mB_lo, fb, st + 2 * Lay::kA + Lay::kB, kx, b_row);
+              tma_load_2d_cg2_hint(&mA_lo, fb, st + Lay::kA + Lay::kB, kx, a_row, keep);
+              tma_load_2d_cg2_hint(&mB_lo, fb, st + 2 * Lay::kA + Lay::kB, kx, b_row, keep);
             }
           } else {
             mbar_arrive_expect_tx(&full[stage], Lay::kStage);
-            tma_load_2d(&mA_hi, &full[stage], st, kx, a_row);
-            tma_load_2d(&mB_hi, &full[stage], st + Lay::kA, kx, b_row);
+            tma_load_2d_hint(&mA_hi, &full[stage], st, kx, a_row, keep);
+            tma_load_2d_hint(&mB_hi, &full[stage], st + Lay::kA, kx, b_row, keep);
             if (T::kSplit) {
-              tma_load_2d(&mA_lo, &full[stage], st + Lay::kA + Lay::kB, kx, a_row);
-              tma_load_2d(&mB_lo, &full[stage], st + 2 * Lay::kA + Lay::kB, kx, b_row);
+              tma_load_2d_hint(&mA_lo, &full[stage], st + Lay::kA + Lay::kB, kx, a_row, keep);
+              tma_load_2d_hint(&mB_lo, &full[stage], st + 2 * Lay::kA + Lay::kB, kx, b_row, keep);
             }
           }
           if (kb == 1 && more) prefetch_c(w_next, ij_nxt, crow_nxt);
@@ -571,7 +578,8 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
 #pragma unroll
       for (int s8 = 0; s8 < 8; ++s8)
         cpre[s8] = args.dbg == 5 ? make_uint4(0, 0, 0, 0)
-                                 : __ldcg(reinterpret_cast<const uint4*>(cpre_ptr + s8 * 4 * c_pitch));
+                                 : ((args.opt & 8) ? __ldcg(reinterpret_cast<const uint4*>(cpre_ptr + s8 * 4 * c_pitch))
+                                                   : __ldcs(reinterpret_cast<const uint4*>(cpre_ptr + s8 * 4 * c_pitch)));
     };
     if (MODE == MODE_UPDATE) load_box(0);
 #else
@@ -725,7 +733,10 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
             for (int s8 = 0; s8 < 8; ++s8) {
               const int r = 4 * s8 + (lane >> 3);
               const uint4 v = lds128(sb + r * 128 + (((lane & 7) ^ (r & 7)) << 4));
-              if (args.dbg != 4) __stcg(reinterpret_cast<uint4*>(cur_ptr + s8 * 4 * c_pitch), v);
+              if (args.dbg != 4) {  // the C tile is not read again this step: stream it out
+                if (args.opt & 8) __stcg(reinterpret_cast<uint4*>(cur_ptr + s8 * 4 * c_pitch), v);
+                else __stcs(reinterpret_cast<uint4*>(cur_ptr + s8 * 4 * c_pitch), v);
+              }
             }
           }
           __syncwarp();  // the slot is free for the next box
@@ -1012,11 +1023,12 @@ namespace {
 
 template <int BN, int OPK, int MODE, int CG = 1>
 void launch_tc(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi,
-               const CUtensorMap& b_lo, const CUtensorMap& c_map, TcArgs args, cudaStream_t s, int max_ctas = 0) {
+               const CUtensorMap& b_lo, const CUtensorMap& c_map, TcArgs args, cudaStream_t s, int max_ctas = 0,
+               bool resume = false) {
   using Lay = TcLayout<BN, OPK, MODE, CG>;
   auto kern = k_tc_gemm<BN, OPK, MODE, CG>;
   smem_optin(reinterpret_cast<const void*>(kern), Lay::kSmem);
-  if (args.counter) SPH_CUDA(cudaMemsetAsync(args.counter, 0, sizeof(int), s));
+  if (args.counter && !resume) SPH_CUDA(cudaMemsetAsync(args.counter, 0, sizeof(int), s));
   const int cap = (max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms()) / CG;
   const int grid = CG * static_cast<int>(std::min<int64_t>(args.items, std::max(1, cap)));
   if constexpr (CG == 1) {
@@ -1108,7 +1120,7 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
 
 void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* list, const int* rows, int64_t cnt,
                const double* p64, PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s,
-               int max_ctas, int* counter) {
+               int max_ctas, int* counter, const int* yield, bool resume) {
   (void)p64;
   TcArgs a{};
   a.ts = ts;
@@ -1150,20 +1162,22 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
     return e ? std::atoi(e) : 256;
   }();
   const bool pair = (cls == SPHEMU_PREC_SP ? cg_sp : cg_env) == 2 && pf.bn == 256;
+  const bool dyn = !pair && counter != nullptr;
+  if (resume && !dyn) return;  // statically scheduled launches never yield
+  a.yield = dyn ? yield : nullptr;
   if (cls == SPHEMU_PREC_SP) {
     const int bn_sp = (pf.f16x3 && pf.bn == 256 && sp_bn == 256 && !pair) ? 256 : (pair ? 256 : 128);
     a.sub_n = ts.b / (pf.f16x3 ? bn_sp : 128);
     a.sub_per = (ts.b / (TC_BM * (pair && pf.f16x3 ? 2 : 1))) * a.sub_n;
     a.items = cnt * a.sub_per;
     if (pf.f16x3 && pair)
-      launch_tc<256, OP_F16X3, MODE_UPDATE, 2>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_a, pf.m_hlo_a, pf.m_c32, a, s,
-                                               max_ctas);
+      launch_tc<256, OP_F16X3, MODE_UPDATE, 2>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_a, pf.m_hlo_a, pf.m_c32, a, s, max_ctas, resume);
     else if (pf.f16x3 && bn_sp == 256)
-      launch_tc<256, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_b, pf.m_hlo_b, pf.m_c32, a, s, max_ctas);
+      launch_tc<256, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_b, pf.m_hlo_b, pf.m_c32, a, s, max_ctas, resume);
     else if (pf.f16x3)  // 128-wide N: B boxes of 128 rows (the A-side maps)
-      launch_tc<128, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_a, pf.m_hlo_a, pf.m_c32, a, s, max_ctas);
+      launch_tc<128, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_a, pf.m_hlo_a, pf.m_c32, a, s, max_ctas, resume);
     else
-      launch_tc<128, OP_TF32X3, MODE_UPDATE>(pf.m_phi_a, pf.m_plo_a, pf.m_phi_b, pf.m_plo_b, pf.m_c32, a, s, max_ctas);
+      launch_tc<128, OP_TF32X3, MODE_UPDATE>(pf.m_phi_a, pf.m_plo_a, pf.m_phi_b, pf.m_plo_b, pf.m_c32, a, s, max_ctas, resume);
   } else {
     static const int hp_bn = [] {
       const char* e = std::getenv("SPHEMU_HP_BN");
@@ -1175,21 +1189,19 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
     a.items = cnt * a.sub_per;
     if (pair) {
       if (hp_format == SPHEMU_HP_BF16)
-        launch_tc<256, OP_BF16, MODE_UPDATE, 2>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s,
-                                                max_ctas);
+        launch_tc<256, OP_BF16, MODE_UPDATE, 2>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas, resume);
       else
-        launch_tc<256, OP_F16, MODE_UPDATE, 2>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s,
-                                               max_ctas);
+        launch_tc<256, OP_F16, MODE_UPDATE, 2>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas, resume);
     } else if (bn_hp == 256) {
       if (hp_format == SPHEMU_HP_BF16)
-        launch_tc<256, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas);
+        launch_tc<256, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas, resume);
       else
-        launch_tc<256, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas);
+        launch_tc<256, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas, resume);
     } else {  // 128-wide N: B boxes of 128 rows (the A-side map)
       if (hp_format == SPHEMU_HP_BF16)
-        launch_tc<128, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas);
+        launch_tc<128, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas, resume);
       else
-        launch_tc<128, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas);
+        launch_tc<128, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas, resume);
     }
   }
 }

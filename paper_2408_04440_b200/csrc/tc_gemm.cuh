@@ -68,9 +68,13 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
                    unsigned* sat, cudaStream_t s, int max_ctas = 0, int* counter = nullptr);
 
 // Trailing update of the SP (cls 1) or HP (cls 2) output tiles of step k.
+// yield (non-null, dynamically scheduled launches only): the CTAs stop
+// claiming work items once *yield != 0 (the chain wants the SMs for the
+// panel); resume = true continues such a launch from its counter (no reset).
+// Statically scheduled launches (CTA pairs) never yield and skip the resume.
 void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* list, const int* rows, int64_t cnt,
                const double* p64, PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s,
-               int max_ctas = 0, int* counter = nullptr);
+               int max_ctas = 0, int* counter = nullptr, const int* yield = nullptr, bool resume = false);
 
 // Host-side inputs of make_spd_test_matrix: d_i = exp(0.6 u_i - 0.3) with the
 // reference's GaussianRng uniform stream, pw[k] = std::pow(rho, k) (rho = 0.9:

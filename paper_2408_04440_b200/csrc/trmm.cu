@@ -80,6 +80,10 @@ __global__ void __launch_bounds__(TrLayout<OPK>::kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // items run snapshot-block-major: the eta block (256 rows of the
+      // splits) is re-read by every tile row and stays in L2; each factor
+      // tile streams through once per snapshot block.
+      const uint64_t keep = l2_evict_last(), stream = l2_evict_first();
       for (int64_t n = 0;; ++n) {
         const int64_t w = item_at(n);
         if (w < 0) break;
@@ -93,10 +97,10 @@ __global__ void __launch_bounds__(TrLayout<OPK>::kThreads, 1)
             uint8_t* st = smem + stage * Lay::kStage;
             mbar_arrive_expect_tx(&full[stage], Lay::kStage);
             const int kx = kb * TR_BK;
-            tma_load_2d(&mA_hi, &full[stage], st, kx, arow);
-            if (OPK == TR_F16X3) tma_load_2d(&mA_lo, &full[stage], st + Lay::kA, kx, arow);
-            tma_load_2d(&mH_hi, &full[stage], st + Lay::kNA * Lay::kA, hcol + kx, it.z);
-            tma_load_2d(&mH_lo, &full[stage], st + Lay::kNA * Lay::kA + Lay::kB, hcol + kx, it.z);
+            tma_load_2d_hint(&mA_hi, &full[stage], st, kx, arow, stream);
+            if (OPK == TR_F16X3) tma_load_2d_hint(&mA_lo, &full[stage], st + Lay::kA, kx, arow, stream);
+            tma_load_2d_hint(&mH_hi, &full[stage], st + Lay::kNA * Lay::kA, hcol + kx, it.z, keep);
+            tma_load_2d_hint(&mH_lo, &full[stage], st + Lay::kNA * Lay::kA + Lay::kB, hcol + kx, it.z, keep);
             if (++stage == NS) {
               stage = 0;
               phase ^= 1;

@@ -6,8 +6,8 @@ the oracle of stochastic.cpp:217-277.
 
 Tolerances (relative to max|xi|): DP tiles FP64 DMMA 1e-13; SP tiles
 fp16 hi/lo x eta hi/lo and HP fp16 tiles x eta's fp16 hi/lo, with fp32
-TMEM partial sums over <= max(b, 512) of K added into FP64: 4e-6 (the
-tensor cores' fp32 accumulation truncates: measured 1.1e-6 at K = 512);
+TMEM partial sums over <= max(b, 8192) of K added into FP64: 2e-5 (the
+tensor cores' fp32 accumulation truncates: measured 8.9e-6 at K = 8192);
 HP bf16 tiles x eta's bf16 hi/lo (16 bits of eta) 1e-4."""
 import os
 import subprocess
@@ -18,7 +18,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-TOL = {("dp", "fp16"): 1e-13, ("dpsp", "fp16"): 4e-6, ("dpsphp", "fp16"): 4e-6, ("dphp", "fp16"): 4e-6,
+TOL = {("dp", "fp16"): 1e-13, ("dpsp", "fp16"): 2e-5, ("dpsphp", "fp16"): 2e-5, ("dphp", "fp16"): 2e-5,
        ("dpsphp", "bf16"): 1e-4, ("dphp", "bf16"): 1e-4}
 
 
@@ -61,7 +61,7 @@ def test_trmm_band_width_and_fp64_mode(sph):
         eta = np.random.default_rng(2).standard_normal((130, 1000))
         got = h.trmm(eta)
         want = eta @ L.T
-        assert np.abs(got - want).max() <= 4e-6 * np.abs(want).max()
+        assert np.abs(got - want).max() <= 2e-5 * np.abs(want).max()
 
 
 def test_trmm_needs_a_factor(sph):
