@@ -209,6 +209,28 @@ def cpu_cholesky_sample(n=8192, reps=1, wl=None):
             f"make_spd_test_matrix({n}, 1), {wl['variant']}/{wl['hp']}, b={wl['tile']}; {kind_note}", best)
 
 
+def cpu_sht_c4_sample(t=64):
+    """The oracle's SHT (ring FFT -> extended-theta FFT -> J = K I -> Wigner
+    contraction, sht.cpp:226-263) at C4 (721 x 1440, L = 720) on 64 snapshots,
+    all host cores: forward and inverse snapshots/s."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import oracle as O
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    P = O.Plan(721, 1440, 720)
+    plan_s = time.perf_counter() - t0
+    c = np.stack([O.draw_random_coefficients(720, 1000 + i) for i in range(t)])
+    t0 = time.perf_counter()
+    f = P.inverse(c, threads=cores)
+    t_inv = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    P.forward(f, threads=cores)
+    t_fwd = time.perf_counter() - t0
+    return {"snapshots": t, "cores": cores, "plan_build_s": plan_s, "inverse_snapshots_per_s": t / t_inv,
+            "forward_snapshots_per_s": t / t_fwd, "kind": "port (oracle restatement of sht.cpp, in-tree FFT)"}
+
+
 def cpu_sht_sample(t=32):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import numpy as np
@@ -610,7 +632,7 @@ def sht_throughput(sph, world):
             "legendre_fp64_tflops_per_gpu": sht_flops / (sht_ms * 1e-3) / 1e12, "round_trip_max_abs": sht_rt}
 
 
-def sht_c4(sph, snapshots=1000):
+def sht_c4(sph, snapshots=1000, year_snapshots=8760):
     """BASELINE configs[3] (C4): 721 x 1440 grid (720 x 1440 cannot resolve L = 720), L = 720,
     forward and inverse timed separately on a device-resident batch."""
     import torch
@@ -634,14 +656,51 @@ def sht_c4(sph, snapshots=1000):
     inv_ms, fwd_ms = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
     flops = 2 * nt * L * (L + 1) * snapshots
     rt = ((back - coef).abs().max() / coef.abs().max()).item()
-    del coef, fld, back, plan
+    year = None
+    if year_snapshots:
+        # The hourly year streamed through the public API with host buffers:
+        # 8 760 snapshots in calls of <= `snapshots` over one host buffer of
+        # `snapshots` fields / coefficients (host RAM cannot hold the 73 GB +
+        # 36 GB year twice); every call moves its inputs H2D and outputs D2H.
+        import numpy as np
+        h_c = np.empty((snapshots, L * L))
+        h_f = np.empty((snapshots, nt, nphi))
+        h_c[...] = coef.cpu().numpy()
+        h_f[...] = fld.cpu().numpy()
+        del coef, fld, back
+        torch.cuda.empty_cache()
+        plan.inverse(h_c[:8])
+        plan.forward(h_f[:8])  # warm the pinned ring
+        t0 = time.perf_counter()
+        done = 0
+        while done < year_snapshots:
+            k = min(snapshots, year_snapshots - done)
+            h_f[:k] = plan.inverse(h_c[:k])
+            done += k
+        t_inv = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        done = 0
+        while done < year_snapshots:
+            k = min(snapshots, year_snapshots - done)
+            h_c[:k] = plan.forward(h_f[:k])
+            done += k
+        t_fwd = time.perf_counter() - t0
+        year = {"snapshots": year_snapshots, "inverse_s": t_inv, "forward_s": t_fwd,
+                "inverse_snapshots_per_s": year_snapshots / t_inv, "forward_snapshots_per_s": year_snapshots / t_fwd,
+                "bytes_moved_per_direction": year_snapshots * 8 * (nt * nphi + L * L),
+                "api": "ShtPlan.inverse / .forward (sphemu_gpu_sht_inverse / _forward, host buffers)",
+                "note": f"calls of <= {snapshots} snapshots over one pageable host buffer; chunks stream through a "
+                        "ring of pinned + device slots (host copy, H2D, transform, D2H overlapped)"}
+    else:
+        del coef, fld, back
+    del plan
     torch.cuda.empty_cache()
     return {"grid": f"{nt}x{nphi}", "band_limit": L, "snapshots": snapshots,
             "forward_snapshots_per_s": snapshots / (fwd_ms * 1e-3),
             "inverse_snapshots_per_s": snapshots / (inv_ms * 1e-3),
             "legendre_fp64_tflops_forward": flops / (fwd_ms * 1e-3) / 1e12,
-            "plan_build_s": plan_s, "round_trip_rel": rt,
-            "note": "the driver's 8 760-snapshot hourly year runs in chunks of this batch"}
+            "plan_build_s": plan_s, "round_trip_rel": rt, "year": year,
+            "note": "device-resident batch of 1 000 snapshots; 'year' = the 8 760-snapshot hourly year with host I/O"}
 
 
 def model_side_points(sph):
@@ -805,6 +864,11 @@ def run_ours(args, world, rank, local):
     cpu_val, cores, sample, _ = (cpu_cholesky_sample(n=args.cpu_n, wl=wl) if not args.no_cpu
                                  else (None, 0, "skipped", 0))
     cpu_sht = cpu_sht_sample() if not args.no_cpu else (None, 0)
+    if c4 is not None and not args.no_cpu:
+        try:
+            c4["cpu_baseline"] = cpu_sht_c4_sample()
+        except Exception as e:  # noqa: BLE001 (host memory / time limits of the GPU box)
+            c4["cpu_baseline"] = {"error": repr(e)[:200]}
     clk = clocks.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,

@@ -32,6 +32,7 @@
 #include "cov_kernels.cuh"
 #include "potrf_coop.cuh"
 #include "emulate.cuh"
+#include "hostio.cuh"
 #include "tc_gemm.cuh"
 #include "tcgen05.cuh"
 #include "trmm.cuh"
@@ -465,76 +466,7 @@ static void widen_row(double* dst, const float* src, int cw) {
   for (; c < cw; ++c) dst[c] = static_cast<double>(src[c]);
 }
 
-// Blocking parallel-for over a fixed set of host threads (the caller runs
-// share 0). Used by the packed host I/O to convert tile rows between fp64 and
-// their storage width on the host side of the link.
-class HostPool {
- public:
-  explicit HostPool(int n) : n_(std::max(1, n)) {
-    for (int t = 1; t < n_; ++t) th_.emplace_back([this, t] { loop(t); });
-  }
-  ~HostPool() {
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      stop_ = true;
-    }
-    cv_.notify_all();
-    for (auto& t : th_) t.join();
-  }
-  int size() const { return n_; }
-  void run(const std::function<void(int, int)>& f) {
-    std::unique_lock<std::mutex> lk(mu_);
-    job_ = &f;
-    pending_ = n_ - 1;
-    ++gen_;
-    cv_.notify_all();
-    lk.unlock();
-    f(0, n_);
-    lk.lock();
-    done_.wait(lk, [this] { return pending_ == 0; });
-    job_ = nullptr;
-  }
 
- private:
-  void loop(int t) {
-    uint64_t seen = 0;
-    while (true) {
-      std::unique_lock<std::mutex> lk(mu_);
-      cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
-      if (stop_) return;
-      seen = gen_;
-      const auto* f = job_;
-      lk.unlock();
-      (*f)(t, n_);
-      lk.lock();
-      if (--pending_ == 0) done_.notify_one();
-    }
-  }
-  int n_;
-  std::vector<std::thread> th_;
-  std::mutex mu_;
-  std::condition_variable cv_, done_;
-  const std::function<void(int, int)>* job_ = nullptr;
-  uint64_t gen_ = 0;
-  int pending_ = 0;
-  bool stop_ = false;
-};
-
-struct PinnedBuf {
-  char* p = nullptr;
-  size_t n = 0;
-  void ensure(size_t bytes) {
-    if (n >= bytes) return;
-    if (p) cudaFreeHost(p);
-    p = nullptr;
-    n = 0;
-    SPH_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p), bytes, cudaHostAllocDefault));
-    n = bytes;
-  }
-  ~PinnedBuf() {
-    if (p) cudaFreeHost(p);
-  }
-};
 
 struct Chol {
   static constexpr int kChainCtas = 32;  // SMs reserved for the critical chain under lookahead
@@ -606,7 +538,7 @@ struct Chol {
   PanelFormats panel_[2];                   // tensor-core operand mirrors per parity
   cudaStream_t stream = nullptr;            // main stream: bulk trailing updates
   cudaStream_t pstream = nullptr;           // high-priority stream: POTRF + panel chain
-  std::vector<cudaEvent_t> ev_panel, ev_bulk, ev_colrest;
+  std::vector<cudaEvent_t> ev_panel, ev_bulk, ev_colrest, ev_bulkdp;
   cudaEvent_t ev_start_p = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches_at_start = 0, launches = 0;
@@ -1140,6 +1072,8 @@ struct Chol {
     ev_bulk.resize(nt);
     ev_colrest.resize(nt);
     for (int k = 0; k < nt; ++k) SPH_CUDA(cudaEventCreateWithFlags(&ev_colrest[k], cudaEventDisableTiming));
+    ev_bulkdp.resize(nt);
+    for (int k = 0; k < nt; ++k) SPH_CUDA(cudaEventCreateWithFlags(&ev_bulkdp[k], cudaEventDisableTiming));
     for (int k = 0; k < nt; ++k) {
       SPH_CUDA(cudaEventCreateWithFlags(&ev_panel[k], cudaEventDisableTiming));
       SPH_CUDA(cudaEventCreateWithFlags(&ev_bulk[k], cudaEventDisableTiming));
@@ -1168,6 +1102,7 @@ struct Chol {
     for (auto e : ev_panel) cudaEventDestroy(e);
     for (auto e : ev_bulk) cudaEventDestroy(e);
     for (auto e : ev_colrest) cudaEventDestroy(e);
+    for (auto e : ev_bulkdp) cudaEventDestroy(e);
     if (ev_start_p) cudaEventDestroy(ev_start_p);
     if (pstream) cudaStreamDestroy(pstream);
     if (comm) ncclCommDestroy(comm);
@@ -1260,9 +1195,14 @@ struct Chol {
     return cls == SPHEMU_PREC_DP || (cls == SPHEMU_PREC_SP && cfg.sp_compute == SPHEMU_SP_FP64);
   }
 
-  void op_update(int k, int part, cudaStream_t s, int max_ctas, const int* yield = nullptr, bool resume = false) {
+  // dp_done (optional): recorded on s once the DP-class launch of this part
+  // is enqueued (before the SP / HP launches), so the chain can wait for the
+  // DP diagonal tiles only.
+  void op_update(int k, int part, cudaStream_t s, int max_ctas, const int* yield = nullptr, bool resume = false,
+                 cudaEvent_t dp_done = nullptr) {
     const int set = k & 1;
     for (int cls = 0; cls < 3; ++cls) {
+      if (cls == 1 && dp_done) SPH_CUDA(cudaEventRecord(dp_done, s));
       const size_t slot = (static_cast<size_t>(k) * kParts + part) * 3 + cls;
       const int64_t cnt = list_cnt[slot];
       if (!cnt) continue;
@@ -1343,8 +1283,11 @@ struct Chol {
       SPH_CUDA(cudaEventRecord(ev_panel[0], pstream));
       col_out(0, pstream);
       for (int k = 0; k + 1 < nt; ++k) {
-        // chain: SYRK of the next diagonal tile -> POTRF -> (column below ready) -> panel
-        if (k > 0) SPH_CUDA(cudaStreamWaitEvent(pstream, ev_bulk[k - 1], 0));
+        // chain: SYRK of the next diagonal tile -> POTRF -> (column below ready) -> panel.
+        // Tile (k+1, k+1) last changed in the DP-class launch of bulk(k-1):
+        // the chain waits for that launch only, not for the SP / HP bulk
+        // (panel(k+1) still waits for column k+1, after all of bulk(k-1)).
+        if (k > 0) SPH_CUDA(cudaStreamWaitEvent(pstream, ev_bulkdp[k - 1], 0));
         reserve = reserve_at(k);
         potrf_cap = reserve;
         op_update(k, 0, pstream, 0);
@@ -1365,7 +1308,7 @@ struct Chol {
         SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
         col_out(k + 1, pstream);
         const int bulk_ctas = std::max(1, num_sms() - reserve);
-        op_update(k, 1, stream, bulk_ctas, yield ? yield_flag.get() : nullptr);
+        op_update(k, 1, stream, bulk_ctas, yield ? yield_flag.get() : nullptr, false, ev_bulkdp[k]);
         if (yield) {
           SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k + 1], 0));
           op_update(k, 1, stream, bulk_ctas, nullptr, true);

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "hostio.cuh"
 #include "dgemm.cuh"
 #include "dgemm2.cuh"
 
@@ -823,6 +824,98 @@ struct Sht {
       cudaStreamSynchronize(stream);
       cudaStreamDestroy(stream);
     }
+    for (auto st : {hcs, hds})
+      if (st) {
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+      }
+    for (int r = 0; r < kRing; ++r)
+      for (auto e : {ev_h2d[r], ev_comp[r], ev_d2h[r]})
+        if (e) cudaEventDestroy(e);
+  }
+
+  // ---- host-buffer batches (the 8 760-snapshot year of C4) ----------------
+  // Chunks of hchunk snapshots stream through a ring of kRing pinned + device
+  // slots: host threads copy the caller's (pageable) array into the pinned
+  // slot, H2D on hcs, the transform on `stream`, D2H on hds, and the host
+  // drains chunk c-1 while the GPU works on chunk c; pinned memory is kept
+  // (grow-only) for the next call.
+  static constexpr int kRing = 3;
+  cudaStream_t hcs = nullptr, hds = nullptr;
+  cudaEvent_t ev_h2d[kRing] = {}, ev_comp[kRing] = {}, ev_d2h[kRing] = {};
+  PinnedBuf pin_in, pin_out;
+  DevBuf<double> ring_in, ring_out;
+  std::unique_ptr<HostPool> hpool;
+
+  void run_host(bool fwd, const double* in, int win, int64_t n, double* out, int wout) {
+    const int64_t pts = (int64_t)n_theta * n_phi, nc = (int64_t)L * L;
+    const int64_t isz = fwd ? pts : nc, osz = fwd ? nc : pts;
+    const bool hin = win == SPHEMU_HOST, hout = wout == SPHEMU_HOST;
+    const int64_t T = std::max<int64_t>(1, std::min<int64_t>(chunk, (int64_t{512} << 20) / (8 * std::max(isz, osz))));
+    const int64_t nch = (n + T - 1) / T;
+    if (!hcs) {
+      SPH_CUDA(cudaStreamCreateWithFlags(&hcs, cudaStreamNonBlocking));
+      SPH_CUDA(cudaStreamCreateWithFlags(&hds, cudaStreamNonBlocking));
+      for (int r = 0; r < kRing; ++r) {
+        SPH_CUDA(cudaEventCreateWithFlags(&ev_h2d[r], cudaEventDisableTiming));
+        SPH_CUDA(cudaEventCreateWithFlags(&ev_comp[r], cudaEventDisableTiming));
+        SPH_CUDA(cudaEventCreateWithFlags(&ev_d2h[r], cudaEventDisableTiming));
+      }
+      const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+      hpool.reset(new HostPool(static_cast<int>(std::min(16u, hw))));
+    }
+    const size_t in_b = (size_t)T * isz * sizeof(double), out_b = (size_t)T * osz * sizeof(double);
+    if (hin) {
+      pin_in.ensure(kRing * in_b);
+      if (ring_in.n < (size_t)kRing * T * isz) ring_in.alloc((size_t)kRing * T * isz);
+    }
+    if (hout) {
+      pin_out.ensure(kRing * out_b);
+      if (ring_out.n < (size_t)kRing * T * osz) ring_out.alloc((size_t)kRing * T * osz);
+    }
+    auto host_copy = [&](char* dst, const char* src, size_t bytes) {
+      hpool->run([&](int t, int nt) {
+        const size_t per = (bytes / nt + 4095) & ~size_t{4095};
+        const size_t a = std::min(bytes, per * t), b = std::min(bytes, a + per);
+        if (b > a) std::memcpy(dst + a, src + a, b - a);
+      });
+    };
+    auto drain = [&](int64_t c) {
+      const int slot = static_cast<int>(c % kRing);
+      const int64_t Tc = std::min(T, n - c * T);
+      SPH_CUDA(cudaEventSynchronize(ev_d2h[slot]));
+      host_copy(reinterpret_cast<char*>(out + c * T * osz), pin_out.p + slot * out_b, (size_t)Tc * osz * 8);
+    };
+    for (int64_t c = 0; c < nch; ++c) {
+      const int slot = static_cast<int>(c % kRing);
+      const int64_t Tc = std::min(T, n - c * T);
+      const double* src = in + c * T * isz;
+      if (hin) {
+        SPH_CUDA(cudaEventSynchronize(ev_h2d[slot]));  // the slot's previous H2D has read the pinned copy
+        host_copy(pin_in.p + slot * in_b, reinterpret_cast<const char*>(src), (size_t)Tc * isz * 8);
+        double* d = ring_in.get() + (size_t)slot * T * isz;
+        SPH_CUDA(cudaStreamWaitEvent(hcs, ev_comp[slot], 0));  // the slot's previous transform has read it
+        SPH_CUDA(cudaMemcpyAsync(d, pin_in.p + slot * in_b, (size_t)Tc * isz * 8, cudaMemcpyHostToDevice, hcs));
+        SPH_CUDA(cudaEventRecord(ev_h2d[slot], hcs));
+        SPH_CUDA(cudaStreamWaitEvent(stream, ev_h2d[slot], 0));
+        src = d;
+      }
+      double* dst = hout ? ring_out.get() + (size_t)slot * T * osz : out + c * T * osz;
+      if (hout) SPH_CUDA(cudaStreamWaitEvent(stream, ev_d2h[slot], 0));  // the slot's previous D2H is done
+      if (fwd) forward_dev(src, Tc, dst);
+      else inverse_dev(src, Tc, dst);
+      SPH_CUDA(cudaEventRecord(ev_comp[slot], stream));
+      if (hout) {
+        SPH_CUDA(cudaStreamWaitEvent(hds, ev_comp[slot], 0));
+        SPH_CUDA(cudaMemcpyAsync(pin_out.p + slot * out_b, dst, (size_t)Tc * osz * 8, cudaMemcpyDeviceToHost, hds));
+        SPH_CUDA(cudaEventRecord(ev_d2h[slot], hds));
+      }
+      if (hout && c >= 1) drain(c - 1);
+    }
+    if (hout && nch >= 1) drain(nch - 1);
+    SPH_CUDA(cudaStreamSynchronize(stream));
+    SPH_CUDA(cudaStreamSynchronize(hcs));
+    SPH_CUDA(cudaStreamSynchronize(hds));
   }
 
   void ensure(int64_t tchunk) {
@@ -879,55 +972,22 @@ struct Sht {
 
   void forward(const double* in, int win, int64_t n, double* out, int wout) {
     if (n <= 0) return;
-    const int64_t pts = (int64_t)n_theta * n_phi, nc = (int64_t)L * L;
     if (win == SPHEMU_DEVICE && wout == SPHEMU_DEVICE) {
       forward_dev(in, n, out);
       SPH_CUDA(cudaStreamSynchronize(stream));
       return;
     }
-    // Host buffers: stream chunks through device staging.
-    const int64_t step = chunk;
-    DevBuf<double> fin(win == SPHEMU_HOST ? (size_t)std::min(n, step) * pts : 0);
-    DevBuf<double> cout(wout == SPHEMU_HOST ? (size_t)std::min(n, step) * nc : 0);
-    for (int64_t t0 = 0; t0 < n; t0 += step) {
-      const int64_t T = std::min(step, n - t0);
-      const double* src = in + t0 * pts;
-      if (win == SPHEMU_HOST) {
-        SPH_CUDA(cudaMemcpyAsync(fin.get(), src, T * pts * sizeof(double), cudaMemcpyHostToDevice, stream));
-        src = fin.get();
-      }
-      double* dst = wout == SPHEMU_HOST ? cout.get() : out + t0 * nc;
-      forward_dev(src, T, dst);
-      if (wout == SPHEMU_HOST)
-        SPH_CUDA(cudaMemcpyAsync(out + t0 * nc, dst, T * nc * sizeof(double), cudaMemcpyDeviceToHost, stream));
-      SPH_CUDA(cudaStreamSynchronize(stream));
-    }
+    run_host(true, in, win, n, out, wout);
   }
 
   void inverse(const double* in, int win, int64_t n, double* out, int wout) {
     if (n <= 0) return;
-    const int64_t pts = (int64_t)n_theta * n_phi, nc = (int64_t)L * L;
     if (win == SPHEMU_DEVICE && wout == SPHEMU_DEVICE) {
       inverse_dev(in, n, out);
       SPH_CUDA(cudaStreamSynchronize(stream));
       return;
     }
-    const int64_t step = chunk;
-    DevBuf<double> cin(win == SPHEMU_HOST ? (size_t)std::min(n, step) * nc : 0);
-    DevBuf<double> fout(wout == SPHEMU_HOST ? (size_t)std::min(n, step) * pts : 0);
-    for (int64_t t0 = 0; t0 < n; t0 += step) {
-      const int64_t T = std::min(step, n - t0);
-      const double* src = in + t0 * nc;
-      if (win == SPHEMU_HOST) {
-        SPH_CUDA(cudaMemcpyAsync(cin.get(), src, T * nc * sizeof(double), cudaMemcpyHostToDevice, stream));
-        src = cin.get();
-      }
-      double* dst = wout == SPHEMU_HOST ? fout.get() : out + t0 * pts;
-      inverse_dev(src, T, dst);
-      if (wout == SPHEMU_HOST)
-        SPH_CUDA(cudaMemcpyAsync(out + t0 * pts, dst, T * pts * sizeof(double), cudaMemcpyDeviceToHost, stream));
-      SPH_CUDA(cudaStreamSynchronize(stream));
-    }
+    run_host(false, in, win, n, out, wout);
   }
 };
 
