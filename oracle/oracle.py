@@ -68,7 +68,8 @@ def build(force: bool = False) -> None:
     if force or not os.path.exists(LIB_PATH) or _stale():
         subprocess.run(["make", "-s", "-C", HERE], check=True)
     if os.path.isdir(os.environ.get("SPHEMU_REFERENCE", "/root/reference/proj")) and (
-            force or not os.path.exists(REF_PATH)):
+            force or not os.path.exists(REF_PATH) or not os.path.exists(os.path.join(HERE, "_ref",
+                                                                                      "libsphemu_ref_mpchol.so"))):
         subprocess.run([os.path.join(HERE, "ref", "build_ref.sh")], check=True)
 
 
@@ -150,6 +151,36 @@ def lib():
 
 def ref_available() -> bool:
     return os.path.exists(REF_PATH)
+
+
+REF_MPCHOL_PATH = os.path.join(HERE, "_ref", "libsphemu_ref_mpchol.so")
+_ref_mpchol = None
+
+
+def ref_mpchol():
+    """The reference's own mpchol.cpp over the Eigen shim (oracle/_ref), or None."""
+    global _ref_mpchol
+    if _ref_mpchol is None and os.path.exists(REF_MPCHOL_PATH):
+        R = C.CDLL(REF_MPCHOL_PATH)
+        R.ref_tiled_cholesky_dense.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                               C.c_void_p, C.c_char_p, C.c_int, C.POINTER(C.c_int)]
+        R.ref_assign_precisions.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p]
+        R.ref_make_spd.argtypes = [C.c_int, C.c_uint64, C.c_void_p]
+        _ref_mpchol = R
+    return _ref_mpchol
+
+
+def ref_tiled_cholesky(a, variant="dp", tile_size=128, workers=1, band_width_dp=1, sp_fraction=0.05):
+    """mpchol.cpp's tiled_cholesky_dense itself: (rc, factor, stats_json_or_message, failed_tile)."""
+    R = ref_mpchol()
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    n = a.shape[0]
+    out = np.zeros_like(a)
+    buf = C.create_string_buffer(1 << 14)
+    failed = C.c_int(-1)
+    rc = R.ref_tiled_cholesky_dense(a.ctypes.data, n, VARIANTS[variant], tile_size, workers, band_width_dp,
+                                    sp_fraction, out.ctypes.data, buf, len(buf), C.byref(failed))
+    return rc, out, buf.value.decode(), failed.value
 
 
 def ref():
