@@ -675,14 +675,14 @@ def sht_c4(sph, snapshots=1000, year_snapshots=8760):
         done = 0
         while done < year_snapshots:
             k = min(snapshots, year_snapshots - done)
-            h_f[:k] = plan.inverse(h_c[:k])
+            plan.inverse(h_c[:k], out=h_f[:k])
             done += k
         t_inv = time.perf_counter() - t0
         t0 = time.perf_counter()
         done = 0
         while done < year_snapshots:
             k = min(snapshots, year_snapshots - done)
-            h_c[:k] = plan.forward(h_f[:k])
+            plan.forward(h_f[:k], out=h_c[:k])
             done += k
         t_fwd = time.perf_counter() - t0
         year = {"snapshots": year_snapshots, "inverse_s": t_inv, "forward_s": t_fwd,

@@ -477,6 +477,14 @@ def assign_precisions(n_tiles, variant="dp", band_width_dp=1, sp_fraction=0.05):
 # ---------------------------------------------------------------------------
 # module.cpp:194-198 forward_sht / inverse_sht (+ batch plans)
 # ---------------------------------------------------------------------------
+def _out(out, shape):
+    if out is None:
+        return np.empty(shape)
+    if out.dtype != np.float64 or not out.flags.c_contiguous or out.size != int(np.prod(shape)):
+        raise ValueError(f"out must be a C-contiguous float64 array of {int(np.prod(shape))} values")
+    return out
+
+
 class ShtPlan:
     """build_plan(GridSpec{n_theta, n_phi}, band_limit) on the device."""
 
@@ -499,15 +507,18 @@ class ShtPlan:
     def stream(self):
         return lib().sphemu_gpu_sht_stream(self.h)
 
-    def forward(self, fields):
+    def forward(self, fields, out=None):
+        """forward_sht_batch; out (optional): a C-contiguous float64 array of
+        (n, L^2) values written in place (no intermediate copy)."""
         f = np.ascontiguousarray(fields, dtype=np.float64).reshape(-1, self.n_theta * self.n_phi)
-        out = np.empty((f.shape[0], self.band_limit ** 2))
+        out = _out(out, (f.shape[0], self.band_limit ** 2))
         _check(lib().sphemu_gpu_sht_forward(self.h, _ptr(f), HOST, f.shape[0], _ptr(out), HOST))
         return out
 
-    def inverse(self, coeffs):
+    def inverse(self, coeffs, out=None):
+        """inverse_sht_batch; out (optional): (n, n_theta, n_phi) float64, written in place."""
         c = np.ascontiguousarray(coeffs, dtype=np.float64).reshape(-1, self.band_limit ** 2)
-        out = np.empty((c.shape[0], self.n_theta, self.n_phi))
+        out = _out(out, (c.shape[0], self.n_theta, self.n_phi))
         _check(lib().sphemu_gpu_sht_inverse(self.h, _ptr(c), HOST, c.shape[0], _ptr(out), HOST))
         return out
 

@@ -325,7 +325,14 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
   extern __shared__ __align__(16) uint8_t pc_smem[];
   PgSmem& sm = *reinterpret_cast<PgSmem*>(pc_smem);
   PcSmallSmem& ss = *reinterpret_cast<PcSmallSmem*>(pc_smem + sizeof(PgSmem));  // disjoint: staged during the SYRK
-  if (*(volatile int*)fail >= 0) return;  // uniform across the grid
+  // An earlier step's failure (written by an earlier kernel) is uniform across
+  // the grid; this kernel's own CTA 0 may set fail = k in the prologue while a
+  // late CTA reads it, so that value must not send a CTA home before the
+  // first grid barrier (the others would wait there forever).
+  {
+    const int f = *(volatile int*)fail;
+    if (f >= 0 && f != k) return;
+  }
   const int nblk = (bk + PC_BLK - 1) / PC_BLK;
   const int G = gridDim.x, cta = blockIdx.x;
   auto rows_of = [&](int r) { return min(PC_BLK, bk - r * PC_BLK); };

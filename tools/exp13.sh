@@ -7,3 +7,4 @@ sys.path.insert(0, '.')
 import bench, paper_2408_04440_b200 as sph
 print(json.dumps(bench.sht_c4(sph, 1000, 8760))[:1500])
 PY
+./tools/micro/potrf_trace 2>&1 | tail -45
