@@ -287,7 +287,7 @@ class Cholesky:
         self.h = h
 
     def __del__(self):
-        if getattr(self, "h", None):
+        if getattr(self, "h", None) and lib is not None:  # lib is None at interpreter shutdown
             lib().sphemu_gpu_chol_destroy(self.h)
             self.h = None
 

@@ -351,6 +351,17 @@ __global__ void k_diff_norms(int n, const double* a, const double* b, double* su
 // SYRK updates cost ~50x a BF16 tile's — go round-robin over all P Q ranks
 // (the plain map would give them only to the ranks with i mod P == i mod Q).
 inline int block_cyclic_owner(int i, int j, int P, int Q) {
+  // SPHEMU_MAP=shift (A/B): round 1's row-shifted map, ((i + s (j div Q)) mod P, j mod Q) with the
+  // smallest s making gcd(Q + s, P) = 1
+  static const bool shift = [] {
+    const char* e = std::getenv("SPHEMU_MAP");
+    return e && std::string(e) == "shift";
+  }();
+  if (shift) {
+    int sh = 0;
+    while (std::gcd(Q + sh, P) != 1) ++sh;
+    return ((i + sh * (j / Q)) % P) * Q + (j % Q);
+  }
   return i == j ? i % (P * Q) : (i % P) * Q + (j % Q);
 }
 
@@ -371,6 +382,8 @@ struct BlockCyclic {
   int nt = 0, b = 0, P = 1, Q = 1, rank = 0;
   std::vector<int64_t> off;                 // per packed tile; -1 = stored elsewhere; back() = arena bytes
   std::vector<std::vector<Xfer>> sends, recvs;  // this rank's, per step k
+  std::vector<std::vector<Xfer>> roots;         // per step k: (-, root, pos, bytes) owner blocks (broadcast mode)
+  std::vector<std::vector<int>> others;         // per step k: panel rows this rank does not own
   std::vector<std::vector<int64_t>> xpos;   // per step k: byte position of panel tile i at [i - k - 1]
   std::vector<std::vector<int64_t>> recv_bytes;  // per step k, per rank: bytes that rank receives
   int64_t xmax = 0;
@@ -407,6 +420,8 @@ struct BlockCyclic {
     if (P * Q == 1) return;
     sends.assign(nt, {});
     recvs.assign(nt, {});
+    roots.assign(nt, {});
+    others.assign(nt, {});
     xpos.assign(nt, {});
     recv_bytes.assign(nt, std::vector<int64_t>(static_cast<size_t>(P) * Q, 0));
     for (int k = 0; k + 1 < nt; ++k) {
@@ -419,6 +434,20 @@ struct BlockCyclic {
             x += static_cast<int64_t>(b) * b * prec_bytes(sprec[static_cast<size_t>(i) * (i + 1) / 2 + k]);
           }
       xmax = std::max(xmax, x);
+      for (int root = 0; root < P * Q; ++root) {
+        int64_t lo = -1, hi = -1;
+        for (int i = k + 1; i < nt; ++i)
+          if (owner(i, k) == root) {
+            const int64_t a = xpos[k][i - k - 1];
+            const int64_t e = a + static_cast<int64_t>(b) * b *
+                                      prec_bytes(sprec[static_cast<size_t>(i) * (i + 1) / 2 + k]);
+            lo = lo < 0 ? a : std::min(lo, a);
+            hi = std::max(hi, e);
+          }
+        if (lo >= 0) roots[k].push_back({-1, root, lo, hi - lo});
+      }
+      for (int i = k + 1; i < nt; ++i)
+        if (owner(i, k) != rank) others[k].push_back(i);
       for (int i = k + 1; i < nt; ++i) {
         const int src = owner(i, k);
         const int64_t bytes = static_cast<int64_t>(b) * b * prec_bytes(sprec[static_cast<size_t>(i) * (i + 1) / 2 + k]);
@@ -489,7 +518,19 @@ struct Chol {
   DevBuf<int64_t> ioffs, xsoffs;
   std::vector<int64_t> ilist_off, ilist_cnt, xsend_off, xsend_cnt;
   using Xfer = BlockCyclic::Xfer;
-  std::vector<std::vector<Xfer>> xsends, xrecvs;
+  std::vector<std::vector<Xfer>> xsends, xrecvs, xroots;
+  // Panel exchange: one grouped ncclBroadcast per owner block to every rank
+  // (default), or with SPHEMU_XCHG=p2p point to point to the readers only
+  // (BlockCyclic::needers: (P+Q)/(PQ) of the bytes per rank, but the owner
+  // sends one copy per reader over its NVLink port). Measured on C3 (2x2):
+  // broadcast 429 ms vs point-to-point 510 ms; 2x1: 677 vs 694 ms.
+  static bool xchg_bcast() {
+    static const bool on = [] {
+      const char* e = std::getenv("SPHEMU_XCHG");
+      return !(e && std::string(e) == "p2p");
+    }();
+    return on;
+  }
   sphemu_chol_config cfg{};
   std::vector<uint8_t> pmap, sprec;
   std::vector<int64_t> off;
@@ -1029,16 +1070,25 @@ struct Chol {
       std::vector<int64_t> io, xo;
       xsends = layout.sends;
       xrecvs = layout.recvs;
+      xroots = layout.roots;
+      const bool bc = xchg_bcast();
       const int64_t xmax = layout.xmax;
       for (int k = 0; k + 1 < nt; ++k) {
         ilist_off[k] = static_cast<int64_t>(il.size());
         xsend_off[k] = static_cast<int64_t>(xs.size());
-        for (const Xfer& x : layout.recvs[k]) {
-          il.push_back(make_int2(x.i, k));
-          io.push_back(x.pos);
+        if (bc) {
+          for (int i : layout.others[k]) {
+            il.push_back(make_int2(i, k));
+            io.push_back(layout.xpos[k][i - k - 1]);
+          }
+        } else {
+          for (const Xfer& x : layout.recvs[k]) {
+            il.push_back(make_int2(x.i, k));
+            io.push_back(x.pos);
+          }
         }
         for (int i = k + 1; i < nt; ++i)
-          if (mine(i, k) && !layout.needers(i, k).empty()) {
+          if (mine(i, k) && (bc || !layout.needers(i, k).empty())) {
             xs.push_back(make_int2(i, k));
             xo.push_back(layout.xpos[k][i - k - 1]);
           }
@@ -1354,10 +1404,16 @@ struct Chol {
       SPH_LAUNCH_CHECK();
     }
     SPH_NCCL(ncclGroupStart());
-    for (const Xfer& x : xsends[k])
-      SPH_NCCL(ncclSend(xbuf.get() + x.pos, static_cast<size_t>(x.bytes), ncclUint8, x.peer, comm, s));
-    for (const Xfer& x : xrecvs[k])
-      SPH_NCCL(ncclRecv(xbuf.get() + x.pos, static_cast<size_t>(x.bytes), ncclUint8, x.peer, comm, s));
+    if (xchg_bcast()) {
+      for (const Xfer& x : xroots[k])
+        SPH_NCCL(ncclBroadcast(xbuf.get() + x.pos, xbuf.get() + x.pos, static_cast<size_t>(x.bytes), ncclUint8, x.peer,
+                               comm, s));
+    } else {
+      for (const Xfer& x : xsends[k])
+        SPH_NCCL(ncclSend(xbuf.get() + x.pos, static_cast<size_t>(x.bytes), ncclUint8, x.peer, comm, s));
+      for (const Xfer& x : xrecvs[k])
+        SPH_NCCL(ncclRecv(xbuf.get() + x.pos, static_cast<size_t>(x.bytes), ncclUint8, x.peer, comm, s));
+    }
     SPH_NCCL(ncclGroupEnd());
     note_launch();
     if (ilist_cnt[k]) {
