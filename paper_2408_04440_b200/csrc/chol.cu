@@ -537,7 +537,12 @@ struct Chol {
   DevBuf<char> arena;
   DevBuf<int64_t> d_off;
   DevBuf<uint8_t> d_prec;
-  DevBuf<double> linv_[2], p64_[2];  // double-buffered by step parity (lookahead)
+  // Panel buffers rotate over kSets steps: with lookahead the chain writes
+  // panel k+1 while the bulk reads panel k, and the merged schedule reads
+  // panels k and k+1 while the chain writes k+2.
+  static constexpr int kSets = 3;
+  static int set_of(int k) { return k % kSets; }
+  DevBuf<double> linv_[kSets], p64_[kSets];
   DevBuf<double> dinv, spd_d, spd_pw;
   DevBuf<int> rowexp;  // per-row power-of-two operand scale (FP16x3 SP path)
   DevBuf<int> fail;
@@ -572,11 +577,14 @@ struct Chol {
   // Parts: 0 = the next diagonal tile (k+1, k+1) (feeds POTRF(k+1), the
   // critical chain), 1 = columns >= k+2 (the bulk), 2 = column k+1 below the
   // diagonal (feeds panel(k+1), runs ahead of the bulk on the main stream).
-  static constexpr int kParts = 3;
+  // Merged schedule (pairs of steps k, k+1): part 3 = column k+2 (i >= k+2,
+  // by panel k alone), part 4 = column k+3 and part 5 = columns >= k+4, both
+  // updated by panels k and k+1 in one pass (parts 3+4+5 = part 1).
+  static constexpr int kParts = 6;
   std::vector<int64_t> list_off, list_cnt;  // [(k * kParts + part) * 3 + class]
   DevBuf<int2> plists;                      // panel tiles per step: DP class, then SP/HP
   std::vector<int64_t> plist_off, plist_dp, plist_lo;
-  PanelFormats panel_[2];                   // tensor-core operand mirrors per parity
+  PanelFormats panel_[kSets];               // tensor-core operand mirrors per set
   cudaStream_t stream = nullptr;            // main stream: bulk trailing updates
   cudaStream_t pstream = nullptr;           // high-priority stream: POTRF + panel chain
   std::vector<cudaEvent_t> ev_panel, ev_bulk, ev_colrest, ev_bulkdp;
@@ -1004,10 +1012,10 @@ struct Chol {
     SPH_CUDA(cudaMemcpy(d_off.get(), off.data(), pmap.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     SPH_CUDA(cudaMemcpy(d_prec.get(), sprec.data(), pmap.size(), cudaMemcpyHostToDevice));
     SPH_CUDA(cudaMemset(arena.get(), 0, static_cast<size_t>(o)));
-    for (int p = 0; p < 2; ++p) linv_[p].alloc(static_cast<size_t>(b) * b);
+    for (int p = 0; p < kSets; ++p) linv_[p].alloc(static_cast<size_t>(b) * b);
     dinv.alloc(static_cast<size_t>(b / PC_BLK + 1) * PC_BLK * PC_BLK);
     if (nt > 1)
-      for (int p = 0; p < 2; ++p) p64_[p].alloc(static_cast<size_t>(nt - 1) * b * b);
+      for (int p = 0; p < kSets; ++p) p64_[p].alloc(static_cast<size_t>(nt - 1) * b * b);
     fail.alloc(1);
     sat.alloc(1);
     sched_ctr.alloc(8);  // [stream][class 0..2, 3 = panel]
@@ -1022,7 +1030,10 @@ struct Chol {
         for (int cls = 0; cls < 3; ++cls) {
           const size_t slot = (static_cast<size_t>(k) * kParts + part) * 3 + cls;
           list_off[slot] = static_cast<int64_t>(all.size());
-          const int j_lo = part == 1 ? k + 2 : k + 1, j_hi = part == 1 ? nt : std::min(k + 2, nt);
+          int j_lo = part == 1 ? k + 2 : k + 1, j_hi = part == 1 ? nt : std::min(k + 2, nt);
+          if (part == 3) j_lo = k + 2, j_hi = std::min(k + 3, nt);
+          if (part == 4) j_lo = k + 3, j_hi = std::min(k + 4, nt);
+          if (part == 5) j_lo = k + 4, j_hi = nt;
           for (int j = j_lo; j < j_hi; ++j)
             for (int i = j; i < nt; ++i) {
               if (part == 0 && i != j) continue;
@@ -1110,7 +1121,7 @@ struct Chol {
     rowexp.alloc(n);
     SPH_CUDA(cudaMemset(rowexp.get(), 0, n * sizeof(int)));
     if (cfg.compute == SPHEMU_COMPUTE_TENSOR && nt > 1)
-      for (int p = 0; p < 2; ++p) {
+      for (int p = 0; p < kSets; ++p) {
         panel_[p].alloc(nt, b, pmap, cfg.hp_format, cfg.sp_compute == SPHEMU_SP_F16X3, rowexp.get());
         panel_[p].set_arena(arena.get(), std::max<int64_t>(o, static_cast<int64_t>(128) * b), b);
       }
@@ -1209,7 +1220,7 @@ struct Chol {
   // uncapped: CTAs beyond the SMs the bulk leaves free start as soon as the
   // bulk's CTAs retire (measured faster than a capped panel: C2 62 vs 73 ms).
   void op_panel(int k, cudaStream_t s, int max_ctas = 0) {
-    const int set = k & 1;
+    const int set = set_of(k);
     const int pp = prof_begin(kPanel, s);
     if (cfg.compute == SPHEMU_COMPUTE_TENSOR) {
       const int2* base = plists.get() + plist_off[k];
@@ -1250,7 +1261,9 @@ struct Chol {
   // DP diagonal tiles only.
   void op_update(int k, int part, cudaStream_t s, int max_ctas, const int* yield = nullptr, bool resume = false,
                  cudaEvent_t dp_done = nullptr) {
-    const int set = k & 1;
+    const int set = set_of(k);
+    const bool merged = part == 4 || part == 5;  // panels k and k+1 in one pass
+    const int set2 = set_of(k + 1);
     for (int cls = 0; cls < 3; ++cls) {
       if (cls == 1 && dp_done) SPH_CUDA(cudaEventRecord(dp_done, s));
       const size_t slot = (static_cast<size_t>(k) * kParts + part) * 3 + cls;
@@ -1262,17 +1275,25 @@ struct Chol {
       const int pu = prof_begin(kUpdDp + cls, s);
       if (tensor) {
         tc_update(store(), k, cls, cfg.hp_format, lst, lrows.get() + list_off[slot], cnt, p64_[set].get(),
-                  panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s, cls), yield, resume);
+                  panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s, cls), yield, resume, merged ? k + 1 : -1,
+                  merged ? &panel_[set2] : nullptr);
       } else {
         if (b % D2_BM == 0 && !(part == 0 && chain_small_syrk())) {
           smem_optin(reinterpret_cast<const void*>(k_update_fp64_v2), (int)sizeof(D2Smem));
           const int per = (b / D2_BM) * (b / D2_BN);
           k_update_fp64_v2<<<static_cast<unsigned>(cnt * per), D2_THREADS, sizeof(D2Smem), s>>>(
-              store(), k, lst, p64_[set].get(), fail.get(), sat.get());
+              store(), k, lst, p64_[set].get(), fail.get(), sat.get(), merged ? k + 1 : -1,
+              merged ? p64_[set2].get() : nullptr);
         } else {
           const int per = (b / DG_BM) * (b / DG_BN);
           k_update_fp64<<<static_cast<unsigned>(cnt * per), DG_THREADS, 0, s>>>(store(), k, lst, p64_[set].get(),
                                                                                  fail.get(), sat.get());
+          if (merged) {  // the 64 x 64 kernel has no second K range: the second step as its own pass
+            SPH_LAUNCH_CHECK();
+            k_update_fp64<<<static_cast<unsigned>(cnt * per), DG_THREADS, 0, s>>>(store(), k + 1, lst,
+                                                                                   p64_[set2].get(), fail.get(),
+                                                                                   sat.get());
+          }
         }
         SPH_LAUNCH_CHECK();
       }
@@ -1310,7 +1331,9 @@ struct Chol {
     auto reserve_at = [&](int k) { return (nt - 1 - k > r_tail) ? r_early : kChainCtas; };
     int reserve = kChainCtas;
     potrf_cap = kChainCtas;
-    if (dist()) {
+    if (merge_on() && nt >= 3) {
+      run_merged(reserve_at);
+    } else if (dist()) {
       factor_dist();
     } else if (!cfg.lookahead || nt == 1) {
       for (int k = 0; k < nt; ++k) {
@@ -1372,6 +1395,141 @@ struct Chol {
     factored = true;
   }
 
+  // Merged two-step schedule (default; SPHEMU_MERGE=0 restores one update
+  // pass per step). Steps run in pairs (k, k+1): the chain factors both
+  // diagonal tiles and solves both panels as before, the main stream updates
+  // column k+2 with panel k alone (it feeds the chain's next step), and every
+  // tile right of it receives both steps' updates in ONE pass
+  // (C -= P_k Q_k^T + P_k+1 Q_k+1^T: one C round trip and one storage rounding
+  // for the two steps — halving the trailing matrix's HBM traffic, which the
+  // 16-bit update is bound by). Column k+3 goes first (it feeds the next
+  // pair's chain), then the bulk. Same arithmetic with and without lookahead
+  // and on any P x Q grid (the lists hold each rank's tiles).
+  static bool merge_on() {
+    static const bool on = [] {
+      const char* e = std::getenv("SPHEMU_MERGE");
+      return !(e && e[0] == '0');
+    }();
+    return on;
+  }
+
+  template <class ReserveFn>
+  void run_merged(ReserveFn reserve_at) {
+    const bool D = dist();
+    auto potrf = [&](int k, cudaStream_t s) {
+      if (D) op_potrf_dist(k, s);
+      else op_potrf(k, s);
+    };
+    auto panel = [&](int k, cudaStream_t s) {
+      if (D) op_panel_dist(k, s);
+      else op_panel(k, s);
+    };
+    auto cols = [&](int k, cudaStream_t s) {
+      if (!D) col_out(k, s);
+    };
+    // chain reserve: one GPU as reserve_at; the distributed chain also carries the exchange (factor_dist)
+    const char* env_reserve = std::getenv("SPHEMU_DIST_RESERVE");
+    const int dist_reserve = env_reserve ? std::atoi(env_reserve) : (P * Q >= 4 ? 48 : kChainCtas);
+    auto reserve_for = [&](int k) { return D ? dist_reserve : reserve_at(k); };
+    if (!cfg.lookahead) {
+      potrf(0, stream);
+      panel(0, stream);
+      cols(0, stream);
+      int k = 0;
+      while (k + 1 < nt) {
+        if (k + 2 < nt) {
+          op_update(k, 0, stream, 0);
+          op_update(k, 2, stream, 0);
+          op_update(k, 3, stream, 0);
+          potrf(k + 1, stream);
+          panel(k + 1, stream);
+          cols(k + 1, stream);
+          op_update(k + 1, 0, stream, 0);
+          op_update(k + 1, 2, stream, 0);
+          op_update(k, 4, stream, 0);
+          op_update(k, 5, stream, 0);
+          potrf(k + 2, stream);
+          if (k + 3 < nt) panel(k + 2, stream);
+          cols(k + 2, stream);
+          k += 2;
+        } else {
+          op_update(k, 0, stream, 0);
+          potrf(k + 1, stream);
+          cols(k + 1, stream);
+          k += 1;
+        }
+      }
+    } else {
+      SPH_CUDA(cudaEventRecord(ev_start_p, stream));
+      SPH_CUDA(cudaStreamWaitEvent(pstream, ev_start_p, 0));
+      potrf(0, pstream);
+      panel(0, pstream);
+      SPH_CUDA(cudaEventRecord(ev_panel[0], pstream));
+      cols(0, pstream);
+      cudaEvent_t diag_ready = nullptr;  // diagonal tile (k+1, k+1) has every update of steps < k
+      auto yielding_panel = [&](int k, bool y) {
+        if (y) SPH_CUDA(cudaMemsetAsync(yield_flag.get(), 1, sizeof(int), pstream));
+        panel(k, pstream);
+        if (y) SPH_CUDA(cudaMemsetAsync(yield_flag.get(), 0, sizeof(int), pstream));
+      };
+      int k = 0;
+      while (k + 1 < nt) {
+        const int reserve = reserve_for(k);
+        potrf_cap = std::min(kChainCtas, reserve);
+        const int bulk_ctas = std::max(1, num_sms() - reserve);
+        const bool y = yield_on() && !D;
+        if (diag_ready) SPH_CUDA(cudaStreamWaitEvent(pstream, diag_ready, 0));
+        op_update(k, 0, pstream, 0);
+        potrf(k + 1, pstream);
+        SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k], 0));
+        op_update(k, 2, stream, 0);
+        SPH_CUDA(cudaEventRecord(ev_colrest[k], stream));
+        if (k + 2 >= nt) {  // the last step: no panel below the last diagonal tile
+          SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
+          cols(k + 1, pstream);
+          break;
+        }
+        // ---- step k: panel k+1 on the chain, column k+2 by panel k on the main stream
+        SPH_CUDA(cudaStreamWaitEvent(pstream, ev_colrest[k], 0));
+        yielding_panel(k + 1, y);
+        SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
+        cols(k + 1, pstream);
+        op_update(k, 3, stream, bulk_ctas, y ? yield_flag.get() : nullptr);
+        if (y) {
+          SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k + 1], 0));
+          op_update(k, 3, stream, bulk_ctas, nullptr, true);
+        }
+        SPH_CUDA(cudaEventRecord(ev_bulkdp[k], stream));  // column k+2 done with panel k
+        // ---- step k+1: its diagonal and column k+2, then both steps' updates right of it
+        SPH_CUDA(cudaStreamWaitEvent(pstream, ev_bulkdp[k], 0));
+        op_update(k + 1, 0, pstream, 0);
+        potrf(k + 2, pstream);
+        SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k + 1], 0));
+        op_update(k + 1, 2, stream, 0);
+        SPH_CUDA(cudaEventRecord(ev_colrest[k + 1], stream));
+        const bool more = k + 3 < nt;
+        if (more) {
+          SPH_CUDA(cudaStreamWaitEvent(pstream, ev_colrest[k + 1], 0));
+          yielding_panel(k + 2, y);
+        }
+        SPH_CUDA(cudaEventRecord(ev_panel[k + 2], pstream));
+        cols(k + 2, pstream);
+        op_update(k, 4, stream, 0);  // column k+3: feeds the next pair's chain
+        SPH_CUDA(cudaEventRecord(ev_bulk[k + 1], stream));
+        diag_ready = ev_bulk[k + 1];
+        op_update(k, 5, stream, bulk_ctas, (y && more) ? yield_flag.get() : nullptr);
+        if (y && more) {
+          SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k + 2], 0));
+          op_update(k, 5, stream, bulk_ctas, nullptr, true);
+        }
+        SPH_CUDA(cudaEventRecord(ev_bulk[k], stream));
+        k += 2;
+      }
+      SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[nt - 1], 0));
+    }
+    if (D) SPH_NCCL(ncclAllReduce(sat.get(), sat.get(), 1, ncclUint32, ncclSum, comm, stream));
+  }
+
   // 2D block-cyclic step sequence (PAPER.md:570 pattern): the owner of
   // (k,k) factors it and broadcasts L_kk^{-1} (and the failure flag); the
   // process column k mod Q computes its panel tiles; every panel tile is
@@ -1385,7 +1543,7 @@ struct Chol {
     if (rank == ok) op_potrf(k, s);
     SPH_NCCL(ncclBroadcast(fail.get(), fail.get(), 1, ncclInt32, ok, comm, s));
     if (k + 1 < nt) {
-      const int set = k & 1;
+      const int set = set_of(k);
       SPH_NCCL(ncclBroadcast(linv_[set].get(), linv_[set].get(), static_cast<size_t>(b) * b, ncclFloat64, ok, comm, s));
     }
     note_launch(2);
@@ -1394,7 +1552,7 @@ struct Chol {
   // Panel TRSM on the owned panel tiles, then every panel tile broadcast at
   // its storage precision and imported into the operand mirrors elsewhere.
   void op_panel_dist(int k, cudaStream_t s, int max_ctas = 0) {
-    const int set = k & 1;
+    const int set = set_of(k);
     op_panel(k, s, max_ctas);
     const int px = prof_begin(kPanel, s);
     const unsigned gx = static_cast<unsigned>(std::max(1, b * b / (256 * 16)));
@@ -1496,7 +1654,7 @@ struct Chol {
     const int G = std::max(1, std::min(potrf_cap, nblk * (nblk + 1) / 2));
     double* dkk = reinterpret_cast<double*>(arena.get() + off[tix(k, k)]);
     int bk = rows(k), kk = k, bb = b;
-    double* lp = linv_[k & 1].get();
+    double* lp = linv_[set_of(k)].get();
     double* dp = dinv.get();
     int* fp = fail.get();
     void* args[] = {&dkk, &bb, &bk, &lp, &dp, &fp, &kk};

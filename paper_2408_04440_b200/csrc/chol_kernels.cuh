@@ -490,10 +490,12 @@ static __global__ void __launch_bounds__(DG_THREADS) k_update_fp64(TileStore ts,
 // Same update on 128 x 64 sub-tiles with the cp.async DGEMM (dgemm2.cuh);
 // needs b % 128 == 0. Sub-tiles strictly above the diagonal of SYRK tiles are
 // skipped.
+// k2 >= 0: merged two-step update, C -= P_k Q_k^T + P_k2 Q_k2^T (P64b = step k2's mirror).
 static __global__ void __launch_bounds__(D2_THREADS) k_update_fp64_v2(TileStore ts, int k,
                                                                       const int2* __restrict__ list,
                                                                       const double* __restrict__ P64,
-                                                                      const int* fail, unsigned* sat) {
+                                                                      const int* fail, unsigned* sat, int k2 = -1,
+                                                                      const double* __restrict__ P64b = nullptr) {
   extern __shared__ __align__(16) uint8_t d2_smem[];
   D2Smem& sm = *reinterpret_cast<D2Smem*>(d2_smem);
   if (*(volatile const int*)fail >= 0) return;
@@ -510,6 +512,13 @@ static __global__ void __launch_bounds__(D2_THREADS) k_update_fp64_v2(TileStore 
   D2Op B{Pj + (int64_t)c0 * b, b, D2_BN, b};
   double acc[4][4][2];
   dgemm2_128x64<D2B::kNT, true>(A, B, b, sm, acc);
+  if (k2 >= 0) {
+    const double* Pi2 = P64b + (int64_t)(i - k2 - 1) * b * b;
+    const double* Pj2 = P64b + (int64_t)(j - k2 - 1) * b * b;
+    D2Op A2{Pi2 + (int64_t)r0 * b, b, D2_BM, b};
+    D2Op B2{Pj2 + (int64_t)c0 * b, b, D2_BN, b};
+    dgemm2_128x64<D2B::kNT, true>(A2, B2, b, sm, acc, false);
+  }
   void* tp = ts.tile(i, j);
   const int p = ts.tprec(i, j);
   unsigned local = 0;

@@ -116,14 +116,18 @@ __device__ __forceinline__ void d2_load_stage(const D2Op& A, const D2Op& B, int 
 
 // acc[mi][ni][e]: C(row, col), row = wm*32 + mi*8 + (lane>>2), col = wn*32 + ni*8 + (lane&3)*2 + e,
 // wm = warp >> 1 (0..3), wn = warp & 1.
+// zero = false: acc += A B (a second K range into the same accumulator).
 template <D2B BL, bool V16>
-__device__ void dgemm2_128x64(const D2Op& A, const D2Op& B, int K, D2Smem& sm, double (&acc)[4][4][2]) {
+__device__ void dgemm2_128x64(const D2Op& A, const D2Op& B, int K, D2Smem& sm, double (&acc)[4][4][2],
+                              bool zero = true) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp >> 1, wn = warp & 1;
+  if (zero) {
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+    for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  }
   const int nk = (K + D2_BK - 1) / D2_BK;
   if (nk <= 0) return;
 #pragma unroll

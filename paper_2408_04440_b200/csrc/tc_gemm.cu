@@ -155,6 +155,7 @@ struct TcArgs {
   int* counter;      // non-null: items are claimed dynamically (atomicAdd), zeroed before the launch
   const int* lexp;   // FP16x3 panel: per output column (Linv row) power-of-two exponent
   const int* yield;  // non-null: stop claiming items once *yield != 0 (dynamic scheduling only)
+  int k2;            // update mode: second panel step of a merged two-step update (-1 = none)
 };
 
 template <int OPK>
@@ -233,7 +234,9 @@ template <int BN, int OPK, int MODE, int CG>
 __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
               const __grid_constant__ CUtensorMap mB_hi, const __grid_constant__ CUtensorMap mB_lo,
-              const __grid_constant__ CUtensorMap mC, const TcArgs args) {
+              const __grid_constant__ CUtensorMap mC, const __grid_constant__ CUtensorMap mA2_hi,
+              const __grid_constant__ CUtensorMap mA2_lo, const __grid_constant__ CUtensorMap mB2_hi,
+              const __grid_constant__ CUtensorMap mB2_lo, const TcArgs args) {
   using T = OpTraits<OPK>;
   using Lay = TcLayout<BN, OPK, MODE, CG>;
   static_assert(CG == 1 || MODE == MODE_UPDATE, "CTA pairs run the trailing update only");
@@ -276,6 +279,14 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mA_hi);
     tma_prefetch(&mB_hi);
+    if (MODE == MODE_UPDATE && args.k2 >= 0) {
+      tma_prefetch(&mA2_hi);
+      tma_prefetch(&mB2_hi);
+      if (T::kSplit) {
+        tma_prefetch(&mA2_lo);
+        tma_prefetch(&mB2_lo);
+      }
+    }
     if (MODE == MODE_UPDATE) tma_prefetch(&mC);
     if (T::kSplit) {
       tma_prefetch(&mA_lo);
@@ -293,6 +304,7 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
   const uint32_t tmem_base = *tmem_holder;
 
   const int kblocks = args.b / T::kBK;
+  const int halves = (MODE == MODE_UPDATE && args.k2 >= 0) ? 2 : 1;  // merged two-step update
   const int64_t items = args.items;
   // Work items: statically strided over clusters, or (CG = 1 with a counter)
   // claimed one by one by the producer and handed to the MMA and epilogue
@@ -386,10 +398,19 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
           ij_nxt = args.list[w_next / args.sub_per];
           if (MODE == MODE_UPDATE) crow_nxt = args.crow[w_next / args.sub_per];
         }
-        const int a_row = (i - args.k - 1) * args.b + m0;
-        const int b_row = (MODE == MODE_UPDATE) ? (j - args.k - 1) * args.b + n0 + static_cast<int>(rank) * (BN / CG)
-                                                : n0;
-        for (int kb = 0; kb < kblocks; ++kb) {
+        // Merged update (k2 >= 0): K runs over panel k's b columns, then
+        // panel k2's — C -= [P_k P_k2] [Q_k Q_k2]^T in one accumulator, one
+        // C round trip for two steps.
+        for (int kb2 = 0; kb2 < kblocks * halves; ++kb2) {
+          const int hf = kb2 >= kblocks ? 1 : 0, kb = kb2 - hf * kblocks;
+          const int kk = hf ? args.k2 : args.k;
+          const CUtensorMap* ma_hi = hf ? &mA2_hi : &mA_hi;
+          const CUtensorMap* ma_lo = hf ? &mA2_lo : &mA_lo;
+          const CUtensorMap* mb_hi = hf ? &mB2_hi : &mB_hi;
+          const CUtensorMap* mb_lo = hf ? &mB2_lo : &mB_lo;
+          const int a_row = (i - kk - 1) * args.b + m0;
+          const int b_row = (MODE == MODE_UPDATE) ? (j - kk - 1) * args.b + n0 + static_cast<int>(rank) * (BN / CG)
+                                                  : n0;
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* st = smem + stage * Lay::kStage;
           const int kx = kb * T::kBK;
@@ -399,22 +420,22 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
             // both CTAs' bytes complete on the leader's full barrier
             const uint32_t fb = mapa_shared(&full[stage], 0);
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], CG * Lay::kStage);
-            tma_load_2d_cg2_hint(&mA_hi, fb, st, kx, a_row, keep);
-            tma_load_2d_cg2_hint(&mB_hi, fb, st + Lay::kA, kx, b_row, keep);
+            tma_load_2d_cg2_hint(ma_hi, fb, st, kx, a_row, keep);
+            tma_load_2d_cg2_hint(mb_hi, fb, st + Lay::kA, kx, b_row, keep);
             if (T::kSplit) {
-              tma_load_2d_cg2_hint(&mA_lo, fb, st + Lay::kA + Lay::kB, kx, a_row, keep);
-              tma_load_2d_cg2_hint(&mB_lo, fb, st + 2 * Lay::kA + Lay::kB, kx, b_row, keep);
+              tma_load_2d_cg2_hint(ma_lo, fb, st + Lay::kA + Lay::kB, kx, a_row, keep);
+              tma_load_2d_cg2_hint(mb_lo, fb, st + 2 * Lay::kA + Lay::kB, kx, b_row, keep);
             }
           } else {
             mbar_arrive_expect_tx(&full[stage], Lay::kStage);
-            tma_load_2d_hint(&mA_hi, &full[stage], st, kx, a_row, keep);
-            tma_load_2d_hint(&mB_hi, &full[stage], st + Lay::kA, kx, b_row, keep);
+            tma_load_2d_hint(ma_hi, &full[stage], st, kx, a_row, keep);
+            tma_load_2d_hint(mb_hi, &full[stage], st + Lay::kA, kx, b_row, keep);
             if (T::kSplit) {
-              tma_load_2d_hint(&mA_lo, &full[stage], st + Lay::kA + Lay::kB, kx, a_row, keep);
-              tma_load_2d_hint(&mB_lo, &full[stage], st + 2 * Lay::kA + Lay::kB, kx, b_row, keep);
+              tma_load_2d_hint(ma_lo, &full[stage], st + Lay::kA + Lay::kB, kx, a_row, keep);
+              tma_load_2d_hint(mb_lo, &full[stage], st + 2 * Lay::kA + Lay::kB, kx, b_row, keep);
             }
           }
-          if (kb == 1 && more) prefetch_c(w_next, ij_nxt, crow_nxt);
+          if (kb2 == 1 && more) prefetch_c(w_next, ij_nxt, crow_nxt);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -451,7 +472,7 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + acc * BN;
-      for (int kb = 0; kb < kblocks; ++kb) {
+      for (int kb = 0; kb < kblocks * halves; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0 && args.dbg == 2) {
@@ -1021,10 +1042,19 @@ __global__ void __launch_bounds__(DG_THREADS) k_panel_trsm_fp64_list(TileStore t
 // ---------------------------------------------------------------------------
 namespace {
 
+// The second panel's operand maps of a merged two-step update (unused otherwise).
+struct Maps2 {
+  const CUtensorMap *a_hi = nullptr, *a_lo = nullptr, *b_hi = nullptr, *b_lo = nullptr;
+};
+
 template <int BN, int OPK, int MODE, int CG = 1>
 void launch_tc(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorMap& b_hi,
                const CUtensorMap& b_lo, const CUtensorMap& c_map, TcArgs args, cudaStream_t s, int max_ctas = 0,
-               bool resume = false) {
+               bool resume = false, Maps2 m2 = {}) {
+  const CUtensorMap& a2_hi = m2.a_hi ? *m2.a_hi : a_hi;
+  const CUtensorMap& a2_lo = m2.a_lo ? *m2.a_lo : a_lo;
+  const CUtensorMap& b2_hi = m2.b_hi ? *m2.b_hi : b_hi;
+  const CUtensorMap& b2_lo = m2.b_lo ? *m2.b_lo : b_lo;
   using Lay = TcLayout<BN, OPK, MODE, CG>;
   auto kern = k_tc_gemm<BN, OPK, MODE, CG>;
   smem_optin(reinterpret_cast<const void*>(kern), Lay::kSmem);
@@ -1032,7 +1062,7 @@ void launch_tc(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorM
   const int cap = (max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms()) / CG;
   const int grid = CG * static_cast<int>(std::min<int64_t>(args.items, std::max(1, cap)));
   if constexpr (CG == 1) {
-    kern<<<grid, Lay::kThreads, Lay::kSmem, s>>>(a_hi, a_lo, b_hi, b_lo, c_map, args);
+    kern<<<grid, Lay::kThreads, Lay::kSmem, s>>>(a_hi, a_lo, b_hi, b_lo, c_map, a2_hi, a2_lo, b2_hi, b2_lo, args);
   } else {
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(grid);
@@ -1046,7 +1076,7 @@ void launch_tc(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorM
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    SPH_CUDA(cudaLaunchKernelEx(&lc, kern, a_hi, a_lo, b_hi, b_lo, c_map, args));
+    SPH_CUDA(cudaLaunchKernelEx(&lc, kern, a_hi, a_lo, b_hi, b_lo, c_map, a2_hi, a2_lo, b2_hi, b2_lo, args));
   }
   SPH_LAUNCH_CHECK();
 }
@@ -1089,6 +1119,7 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
   }
   if (n_lo) {
     TcArgs a{};
+    a.k2 = -1;
     a.ts = ts;
     a.list = d_lo;
     a.k = k;
@@ -1120,9 +1151,10 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
 
 void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* list, const int* rows, int64_t cnt,
                const double* p64, PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s,
-               int max_ctas, int* counter, const int* yield, bool resume) {
+               int max_ctas, int* counter, const int* yield, bool resume, int k2, PanelFormats* pf2) {
   (void)p64;
   TcArgs a{};
+  a.k2 = (k2 >= 0 && pf2) ? k2 : -1;
   a.ts = ts;
   a.list = list;
   a.crow = rows;
@@ -1171,13 +1203,17 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
     a.sub_per = (ts.b / (TC_BM * (pair && pf.f16x3 ? 2 : 1))) * a.sub_n;
     a.items = cnt * a.sub_per;
     if (pf.f16x3 && pair)
-      launch_tc<256, OP_F16X3, MODE_UPDATE, 2>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_a, pf.m_hlo_a, pf.m_c32, a, s, max_ctas, resume);
+      launch_tc<256, OP_F16X3, MODE_UPDATE, 2>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_a, pf.m_hlo_a, pf.m_c32, a, s, max_ctas, resume,
+                  Maps2{a.k2 >= 0 ? &pf2->m_hhi_a : nullptr, a.k2 >= 0 ? &pf2->m_hlo_a : nullptr, a.k2 >= 0 ? &pf2->m_hhi_a : nullptr, a.k2 >= 0 ? &pf2->m_hlo_a : nullptr});
     else if (pf.f16x3 && bn_sp == 256)
-      launch_tc<256, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_b, pf.m_hlo_b, pf.m_c32, a, s, max_ctas, resume);
+      launch_tc<256, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_b, pf.m_hlo_b, pf.m_c32, a, s, max_ctas, resume,
+                  Maps2{a.k2 >= 0 ? &pf2->m_hhi_a : nullptr, a.k2 >= 0 ? &pf2->m_hlo_a : nullptr, a.k2 >= 0 ? &pf2->m_hhi_b : nullptr, a.k2 >= 0 ? &pf2->m_hlo_b : nullptr});
     else if (pf.f16x3)  // 128-wide N: B boxes of 128 rows (the A-side maps)
-      launch_tc<128, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_a, pf.m_hlo_a, pf.m_c32, a, s, max_ctas, resume);
+      launch_tc<128, OP_F16X3, MODE_UPDATE>(pf.m_hhi_a, pf.m_hlo_a, pf.m_hhi_a, pf.m_hlo_a, pf.m_c32, a, s, max_ctas, resume,
+                  Maps2{a.k2 >= 0 ? &pf2->m_hhi_a : nullptr, a.k2 >= 0 ? &pf2->m_hlo_a : nullptr, a.k2 >= 0 ? &pf2->m_hhi_a : nullptr, a.k2 >= 0 ? &pf2->m_hlo_a : nullptr});
     else
-      launch_tc<128, OP_TF32X3, MODE_UPDATE>(pf.m_phi_a, pf.m_plo_a, pf.m_phi_b, pf.m_plo_b, pf.m_c32, a, s, max_ctas, resume);
+      launch_tc<128, OP_TF32X3, MODE_UPDATE>(pf.m_phi_a, pf.m_plo_a, pf.m_phi_b, pf.m_plo_b, pf.m_c32, a, s, max_ctas, resume,
+                  Maps2{a.k2 >= 0 ? &pf2->m_phi_a : nullptr, a.k2 >= 0 ? &pf2->m_plo_a : nullptr, a.k2 >= 0 ? &pf2->m_phi_b : nullptr, a.k2 >= 0 ? &pf2->m_plo_b : nullptr});
   } else {
     static const int hp_bn = [] {
       const char* e = std::getenv("SPHEMU_HP_BN");
@@ -1189,19 +1225,25 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
     a.items = cnt * a.sub_per;
     if (pair) {
       if (hp_format == SPHEMU_HP_BF16)
-        launch_tc<256, OP_BF16, MODE_UPDATE, 2>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas, resume);
+        launch_tc<256, OP_BF16, MODE_UPDATE, 2>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas, resume,
+                  Maps2{a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr});
       else
-        launch_tc<256, OP_F16, MODE_UPDATE, 2>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas, resume);
+        launch_tc<256, OP_F16, MODE_UPDATE, 2>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas, resume,
+                  Maps2{a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr});
     } else if (bn_hp == 256) {
       if (hp_format == SPHEMU_HP_BF16)
-        launch_tc<256, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas, resume);
+        launch_tc<256, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas, resume,
+                  Maps2{a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_b : nullptr, a.k2 >= 0 ? &pf2->m_p16_b : nullptr});
       else
-        launch_tc<256, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas, resume);
+        launch_tc<256, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_b, pf.m_p16_b, pf.m_c16, a, s, max_ctas, resume,
+                  Maps2{a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_b : nullptr, a.k2 >= 0 ? &pf2->m_p16_b : nullptr});
     } else {  // 128-wide N: B boxes of 128 rows (the A-side map)
       if (hp_format == SPHEMU_HP_BF16)
-        launch_tc<128, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas, resume);
+        launch_tc<128, OP_BF16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas, resume,
+                  Maps2{a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr});
       else
-        launch_tc<128, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas, resume);
+        launch_tc<128, OP_F16, MODE_UPDATE>(pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_p16_a, pf.m_c16, a, s, max_ctas, resume,
+                  Maps2{a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr, a.k2 >= 0 ? &pf2->m_p16_a : nullptr});
     }
   }
 }

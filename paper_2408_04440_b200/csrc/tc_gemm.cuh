@@ -72,9 +72,13 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
 // claiming work items once *yield != 0 (the chain wants the SMs for the
 // panel); resume = true continues such a launch from its counter (no reset).
 // Statically scheduled launches (CTA pairs) never yield and skip the resume.
+// k2 >= 0 (with pf2 = that step's operand mirrors): merged two-step update,
+// C -= P_k Q_k^T + P_k2 Q_k2^T in one accumulator (one C round trip, one
+// storage rounding for both steps).
 void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* list, const int* rows, int64_t cnt,
                const double* p64, PanelFormats& pf, const int* fail, unsigned* sat, cudaStream_t s,
-               int max_ctas = 0, int* counter = nullptr, const int* yield = nullptr, bool resume = false);
+               int max_ctas = 0, int* counter = nullptr, const int* yield = nullptr, bool resume = false,
+               int k2 = -1, PanelFormats* pf2 = nullptr);
 
 // Host-side inputs of make_spd_test_matrix: d_i = exp(0.6 u_i - 0.3) with the
 // reference's GaussianRng uniform stream, pw[k] = std::pow(rho, k) (rho = 0.9:
