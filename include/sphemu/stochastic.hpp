@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <span>
 #include <stdexcept>
 #include <vector>
@@ -19,7 +20,23 @@
 
 namespace sphemu {
 
+namespace detail {
+// Owner of a device-resident tiled factor (sphemu_chol_t).
+struct CholHandle {
+  sphemu_chol_t h = nullptr;
+  CholHandle() = default;
+  explicit CholHandle(sphemu_chol_t x) : h(x) {}
+  CholHandle(const CholHandle&) = delete;
+  CholHandle& operator=(const CholHandle&) = delete;
+  ~CholHandle() {
+    if (h) sphemu_gpu_chol_destroy(h);
+  }
+};
+}  // namespace detail
+
 // InnovationModel (stochastic.hpp:36-42): u_hat and v are dim x dim row-major.
+// `factor` (when set) is the same V kept on the device as tiles at their
+// storage precision: emulate(EmulatorModel, ...) draws from it directly.
 struct InnovationModel {
   int dim = 0;
   std::vector<double> u_hat;
@@ -27,6 +44,7 @@ struct InnovationModel {
   double nugget = 0.0;
   PrecisionVariant factored_variant = PrecisionVariant::kDp;
   FactorizationStats factor_stats;
+  std::shared_ptr<detail::CholHandle> factor;
 };
 
 // estimate_innovation_covariance (stochastic.cpp:109-172) on the device;
@@ -98,6 +116,30 @@ inline FieldSeries emulate(const ShtPlan& plan, std::span<const double> v, int d
   return out;
 }
 
+// estimate_innovation_covariance keeping V on the device as the tiled factor
+// (the handle train hands to emulate); residuals host or device (where).
+inline InnovationModel estimate_innovation_factor(const double* residuals, int where, std::int64_t rows, int d,
+                                                  int r_len, int t_len, int order, const MpCholConfig& chol_config,
+                                                  bool dense_v = true) {
+  chol_config.validate();
+  const sphemu_chol_config c = chol_config.c_config();
+  InnovationModel m;
+  m.dim = d;
+  m.u_hat.resize(static_cast<std::size_t>(d) * d);
+  sphemu_chol_stats st{};
+  sphemu_chol_t h = nullptr;
+  detail::check(sphemu_gpu_innovation_factor(residuals, where, rows, d, r_len, t_len, order, &c, m.u_hat.data(),
+                                             SPHEMU_HOST, &m.nugget, &st, &h));
+  m.factor = std::make_shared<detail::CholHandle>(h);
+  if (dense_v) {
+    m.v.resize(static_cast<std::size_t>(d) * d);
+    detail::check(sphemu_gpu_chol_store_dense(h, m.v.data(), SPHEMU_HOST, d));
+  }
+  m.factored_variant = chol_config.variant;
+  m.factor_stats = detail::from_c(st);
+  return m;
+}
+
 // VarModel / VarFit (stochastic.hpp:18-37) with the residuals as a dense
 // row-major (rows x d) vector instead of an Eigen matrix.
 struct VarModel {
@@ -134,6 +176,129 @@ inline VarFit fit_var(const CoeffSeries& coeffs, int order) {
                                    fit.model.phi.data(), fit.phi_se.data(), fit.residuals.data(), SPHEMU_HOST,
                                    &fit.model.zeroed_count, &fit.model.unstable_count, &fit.residual_mean_norm));
   return fit;
+}
+
+// NoiseField (stochastic.hpp:60-66) and fit_noise_field (stochastic.cpp:176-196) on the device.
+struct NoiseField {
+  GridSpec spec;
+  std::vector<double> v2;
+};
+
+inline NoiseField fit_noise_field(const FieldSeries& detrended, const FieldSeries& reconstructed) {
+  detrended.validate();
+  reconstructed.validate();
+  if (!(detrended.spec == reconstructed.spec) || detrended.t_len != reconstructed.t_len ||
+      detrended.r_len != reconstructed.r_len)
+    throw std::invalid_argument("detrended and reconstructed series differ in shape");
+  NoiseField n;
+  n.spec = detrended.spec;
+  n.v2.resize(detrended.spec.points());
+  detail::check(sphemu_gpu_noise_field(detrended.values.data(), reconstructed.values.data(), SPHEMU_HOST,
+                                       static_cast<std::int64_t>(detrended.r_len) * detrended.t_len,
+                                       static_cast<std::int64_t>(detrended.spec.points()), n.v2.data(), SPHEMU_HOST));
+  return n;
+}
+
+// EmulatorModel (stochastic.hpp:68-79).
+struct EmulatorModel {
+  GridSpec spec;
+  int band_limit = 0;
+  TrendModel trend;
+  VarModel var;
+  InnovationModel innovation;
+  NoiseField noise;
+
+  void validate() const {  // stochastic.cpp:198-215
+    spec.validate();
+    if (band_limit < 1 || !spec.admissible(band_limit))
+      throw std::invalid_argument("model band limit is not resolved by its grid");
+    const std::size_t d = static_cast<std::size_t>(band_limit) * band_limit;
+    if (!(trend.spec == spec)) throw std::invalid_argument("trend grid differs from model grid");
+    if (trend.values.size() != spec.points() * trend.record_stride())
+      throw std::invalid_argument("trend parameter block has the wrong size");
+    if (var.band_limit != band_limit || var.phi.size() != static_cast<std::size_t>(var.order) * d)
+      throw std::invalid_argument("lag coefficient block has the wrong size");
+    if (innovation.dim != static_cast<int>(d) || innovation.u_hat.size() != d * d ||
+        (innovation.v.size() != d * d && !innovation.factor))
+      throw std::invalid_argument("innovation covariance has the wrong size");
+    if (!(noise.spec == spec) || noise.v2.size() != spec.points())
+      throw std::invalid_argument("noise field has the wrong size");
+  }
+};
+
+// TrainConfig (pipeline.hpp): trend, lag order, band limit, factorization.
+struct TrainConfig {
+  int band_limit = 0;
+  TrendConfig trend;
+  int var_order = 2;
+  MpCholConfig chol;
+  int threads = 1;
+};
+
+// fit_trend(series, {}, config) (trend.cpp:129-250) without forcing, on the device.
+inline TrendModel fit_trend(const FieldSeries& series, const ForcingTrajectory& forcing, TrendConfig config) {
+  if (!forcing.x.empty() || !forcing.history.empty())
+    throw std::invalid_argument("the device trend fit takes no forcing trajectory");
+  series.validate();
+  TrendModel m;
+  m.spec = series.spec;
+  m.config = config;
+  m.values.resize(series.spec.points() * m.record_stride());
+  detail::check(sphemu_gpu_fit_trend(series.values.data(), SPHEMU_HOST, series.r_len, series.t_len,
+                                     static_cast<std::int64_t>(series.spec.points()), config.harmonics, config.period,
+                                     m.values.data(), SPHEMU_HOST));
+  return m;
+}
+
+// train (pipeline.cpp:18-54): trend -> detrend -> forward SHT -> fit_var ->
+// innovation covariance + factor (kept on the device) -> noise field.
+inline EmulatorModel train(const FieldSeries& series, const ForcingTrajectory& forcing, const TrainConfig& config) {
+  series.validate();
+  const int band_limit = config.band_limit > 0 ? config.band_limit : series.spec.max_band_limit();
+  if (!series.spec.admissible(band_limit))
+    throw std::invalid_argument("training grid does not resolve band limit " + std::to_string(band_limit));
+  EmulatorModel model;
+  model.spec = series.spec;
+  model.band_limit = band_limit;
+  model.trend = fit_trend(series, forcing, config.trend);
+  FieldSeries standardized = detrend(series, model.trend, forcing);
+  ShtPlan plan = build_plan(series.spec, band_limit);
+  CoeffSeries coeffs = forward_sht_batch(plan, standardized, config.threads);
+  VarFit vf = fit_var(coeffs, config.var_order);
+  model.var = vf.model;
+  model.innovation = estimate_innovation_factor(vf.residuals.data(), SPHEMU_HOST, vf.residual_rows,
+                                                band_limit * band_limit, series.r_len, series.t_len, config.var_order,
+                                                config.chol);
+  FieldSeries reconstructed = inverse_sht_batch(plan, coeffs, config.threads);
+  model.noise = fit_noise_field(standardized, reconstructed);
+  model.validate();
+  return model;
+}
+
+// emulate(model, plan, forcing, t_out, seed, r_len, threads, t_start)
+// (stochastic.hpp:84-86): from the device-resident factor when the model
+// holds one (sphemu_gpu_emulate_chol_trend), else from the dense V.
+inline FieldSeries emulate(const EmulatorModel& model, const ShtPlan& plan, const ForcingTrajectory& forcing,
+                           int t_out, std::uint64_t seed, int r_len = 1, int threads = 1, std::int64_t t_start = 1,
+                           EmulationRng rng = EmulationRng::kReference) {
+  (void)threads;
+  model.validate();
+  if (!(plan.spec == model.spec) || plan.band_limit != model.band_limit)
+    throw std::invalid_argument("transform plan does not match the model");
+  const int d = model.band_limit * model.band_limit;
+  if (!model.innovation.factor)
+    return emulate(plan, model.innovation.v, d, model.var.phi, model.var.order, model.trend, forcing, model.noise.v2,
+                   t_out, seed, r_len, t_start, rng);
+  FieldSeries out(plan.spec, t_out, r_len);
+  std::vector<double> phi_pad(model.var.phi.begin(), model.var.phi.end());
+  if (phi_pad.empty()) phi_pad.assign(static_cast<std::size_t>(d), 0.0);
+  detail::check(sphemu_gpu_emulate_chol_trend(
+      model.innovation.factor->h, plan.device->h, phi_pad.data(), model.var.order, model.trend.values.data(),
+      model.trend.config.harmonics, model.trend.config.period, forcing.x.data(),
+      static_cast<std::int64_t>(forcing.x.size()), forcing.history.data(),
+      static_cast<std::int64_t>(forcing.history.size()), t_start, model.noise.v2.data(), t_out, seed, 0, r_len,
+      static_cast<int>(rng), out.values.data(), SPHEMU_HOST));
+  return out;
 }
 
 }  // namespace sphemu

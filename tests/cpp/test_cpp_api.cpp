@@ -272,6 +272,45 @@ int main() {
     CHECK(std::fabs(q.values[HarmonicVector::index_im(2, 1)]) < 1e-6 && std::fabs(q.values[HarmonicVector::index_re(2, 1)]) > 0.1);
   }
 
+  {  // train -> emulate (pipeline.cpp:18-54, stochastic.cpp:217-277) through the C++ API, factor kept on the device
+    const int L = 6, t_len = 120, r_len = 2;
+    GridSpec spec = GridSpec::from_band_limit(L);
+    ShtPlan p = build_plan(spec, L);
+    FieldSeries series(spec, t_len, r_len);
+    std::mt19937_64 rng(91);
+    std::normal_distribution<double> nd;
+    for (int r = 0; r < r_len; ++r) {
+      std::vector<double> state(L * L, 0.0);
+      for (int t = 0; t < t_len; ++t) {
+        HarmonicVector c(L);
+        for (int i = 0; i < L * L; ++i) c.values[i] = state[i] = 0.55 * state[i] + 0.3 * nd(rng);
+        EquiangularField f = inverse_sht(p, c);
+        auto sl = series.slice(r, t);
+        for (std::size_t loc = 0; loc < sl.size(); ++loc)
+          sl[loc] = 1.7 + 1.1 * std::cos(2.0 * std::numbers::pi * (t + 1) / 12.0) + f.values[loc] + 0.05 * nd(rng);
+      }
+    }
+    TrainConfig tc;
+    tc.band_limit = L;
+    tc.trend.harmonics = 2;
+    tc.trend.period = 12;
+    tc.var_order = 2;
+    tc.chol.tile_size = 16;
+    EmulatorModel m = train(series, {}, tc);
+    CHECK(m.innovation.factor != nullptr && m.innovation.v.size() == 36u * 36u && m.noise.v2.size() == spec.points());
+    CHECK(std::fabs(m.trend.values[0] - 1.7) < 0.2);  // intercept of the seasonal series
+    FieldSeries a = emulate(m, p, {}, 8, 42, 2);
+    FieldSeries b2 = emulate(p, m.innovation.v, 36, m.var.phi, m.var.order, m.trend, ForcingTrajectory{}, m.noise.v2, 8,
+                             42, 2);
+    double md = 0.0, mx = 0.0;
+    for (std::size_t e = 0; e < a.values.size(); ++e) {
+      md = std::fmax(md, std::fabs(a.values[e] - b2.values[e]));
+      mx = std::fmax(mx, std::fabs(b2.values[e]));
+    }
+    CHECK(md <= 1e-10 * mx);  // the tiled (dp) factor path = the dense-V path
+    CHECK(throws<std::invalid_argument>([&] { fit_trend(series, ForcingTrajectory{{1.0, 2.0}, {}}, tc.trend); }));
+  }
+
   // covariance + nugget (test_stochastic.cpp:159-210)
   {
     const int d = 36, r_len = 2, t_len = 40, order = 2;
