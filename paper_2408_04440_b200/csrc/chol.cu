@@ -33,6 +33,7 @@
 #include "potrf_coop.cuh"
 #include "emulate.cuh"
 #include "hostio.cuh"
+#include "ozaki.cuh"
 #include "tc_gemm.cuh"
 #include "tcgen05.cuh"
 #include "trmm.cuh"
@@ -543,6 +544,27 @@ struct Chol {
   static constexpr int kSets = 3;
   static int set_of(int k) { return k % kSets; }
   DevBuf<double> linv_[kSets], p64_[kSets];
+  // DP-class updates on the INT8 tensor cores (ozaki.cuh): the digit planes
+  // of each panel set. Block 0 (tile k+1, the chain's diagonal SYRK) is cut
+  // on the panel's stream right after the panel; the rest by the main stream
+  // before its first DP-class update of the step (oz_rest[k]).
+  OzSlices oz_[kSets];
+  bool oz = false;
+  std::vector<uint8_t> oz_rest;
+  // SPHEMU_DP_EMU=0: DP-class updates on FP64 DMMA instead.
+  static bool dp_emu_env() {
+    static const bool on = [] {
+      const char* e = std::getenv("SPHEMU_DP_EMU");
+      return !(e && e[0] == '0');
+    }();
+    return on;
+  }
+  void oz_slice_rest(int k, cudaStream_t s) {
+    if (oz_rest[k]) return;
+    oz_rest[k] = 1;
+    oz_slice(store(), k, p64_[set_of(k)].get(), b, static_cast<int64_t>(nt - k - 1) * b, rowexp.get(),
+             oz_[set_of(k)], fail.get(), s);
+  }
   DevBuf<double> dinv, spd_d, spd_pw;
   DevBuf<int> rowexp;  // per-row power-of-two operand scale (FP16x3 SP path)
   DevBuf<int> fail;
@@ -1125,6 +1147,22 @@ struct Chol {
         panel_[p].alloc(nt, b, pmap, cfg.hp_format, cfg.sp_compute == SPHEMU_SP_F16X3, rowexp.get());
         panel_[p].set_arena(arena.get(), std::max<int64_t>(o, static_cast<int64_t>(128) * b), b);
       }
+    {
+      bool any_dp_update = false;
+      for (int i = 1; i < nt && !any_dp_update; ++i)
+        for (int j = 1; j <= i; ++j)
+          if (pmap[tix(i, j)] == SPHEMU_PREC_DP && mine(i, j)) {
+            any_dp_update = true;
+            break;
+          }
+      // Not for the exact modes: the pure-FP64 variant and sp_compute = fp64
+      // keep every FP64-class update on DMMA.
+      oz = dp_emu_env() && cfg.variant != SPHEMU_VARIANT_DP && cfg.sp_compute != SPHEMU_SP_FP64 &&
+           cfg.compute == SPHEMU_COMPUTE_TENSOR && nt > 1 && b % 128 == 0 && !dist() && any_dp_update;
+      if (oz)
+        for (int p = 0; p < kSets; ++p) oz_[p].alloc(static_cast<int64_t>(nt - 1) * b, b);
+      oz_rest.assign(nt, 0);
+    }
     int prio_lo = 0, prio_hi = 0;
     SPH_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     SPH_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, prio_lo));
@@ -1226,6 +1264,8 @@ struct Chol {
       const int2* base = plists.get() + plist_off[k];
       tc_panel_trsm(store(), k, base, plist_dp[k], base + plist_dp[k], plist_lo[k], linv_[set].get(),
                     p64_[set].get(), panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s, 3));
+      if (oz && k + 1 < nt)  // tile k+1's digits: the chain's diagonal SYRK of the next step
+        oz_slice(store(), k, p64_[set].get(), 0, b, rowexp.get(), oz_[set], fail.get(), s);
     } else {
       const int below = nt - k - 1;
       k_panel_trsm_fp64<<<dim3(below * (b / DG_BM), b / DG_BN), DG_THREADS, 0, s>>>(
@@ -1273,7 +1313,14 @@ struct Chol {
       const bool tensor = !fp64_class(cls) && cfg.compute == SPHEMU_COMPUTE_TENSOR;
       if (resume && !tensor) continue;  // only the persistent tcgen05 launches yield
       const int pu = prof_begin(kUpdDp + cls, s);
-      if (tensor) {
+      if (oz && cls == 0) {
+        if (part != 0) {
+          oz_slice_rest(k, s);
+          if (merged) oz_slice_rest(k + 1, s);
+        }
+        oz_update(store(), k, lst, cnt, oz_[set], merged ? k + 1 : -1, merged ? &oz_[set2] : nullptr, rowexp.get(),
+                  fail.get(), s, max_ctas, ctr(s, 0));
+      } else if (tensor) {
         tc_update(store(), k, cls, cfg.hp_format, lst, lrows.get() + list_off[slot], cnt, p64_[set].get(),
                   panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s, cls), yield, resume, merged ? k + 1 : -1,
                   merged ? &panel_[set2] : nullptr);
@@ -1310,6 +1357,7 @@ struct Chol {
   // identical with and without lookahead).
   void factor() {
     factored = false;
+    std::fill(oz_rest.begin(), oz_rest.end(), 0);
     launches_at_start = launch_count();
     t_start = std::chrono::steady_clock::now();
     SPH_CUDA(cudaEventRecord(ev0, stream));

@@ -256,7 +256,15 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(wcache + Lay::kEpi * 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (*(volatile const int*)args.fail >= 0) return;  // an earlier POTRF failed (both CTAs of a pair see it)
+  {
+    // An earlier POTRF failed: read once per CTA (the chain's kernel may set
+    // the flag between two threads' reads) so the CTA leaves as a whole; the
+    // two CTAs of a pair both leave before their first cluster barrier.
+    __shared__ int s_fail;
+    if (threadIdx.x == 0) s_fail = *(volatile const int*)args.fail;
+    __syncthreads();
+    if (s_fail >= 0) return;
+  }
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // 0 = pair leader (issues the MMAs)
   const int64_t cid = blockIdx.x / CG, ncl = gridDim.x / CG;  // work is strided over clusters
 
@@ -1179,15 +1187,18 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
   // CTA pairs (cta_group::2, M = 256) for the 256-wide kinds: bitwise
   // identical results. Default for the HP class, where the pair's smaller
   // operand stages leave room for 16 epilogue warps (update 820 vs 767
-  // TFLOP/s single-CTA at N = 98 304 dpsphp/bf16); the SP class (fp16x3,
-  // 96 KB stages) stays on single CTAs (SPHEMU_TC_CG_SP=2: 247 vs 285).
+  // TFLOP/s single-CTA at N = 98 304 dpsphp/bf16), and for the SP class
+  // (fp16x3): each CTA stages half of the B rows, so the shared-memory
+  // traffic per MMA (TMA writes + operand reads) drops from ~147 to ~98
+  // B/clk (C2 dpsp 51.8 -> 49.3 ms, n = 64 800 dpsp 275 -> 234 ms, C3
+  // 916 -> 891 ms; SPHEMU_TC_CG_SP=1 restores single CTAs).
   static const int cg_env = [] {
     const char* e = std::getenv("SPHEMU_TC_CG");
     return e ? std::atoi(e) : 2;
   }();
   static const int cg_sp = [] {
     const char* e = std::getenv("SPHEMU_TC_CG_SP");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 2;
   }();
   static const int sp_bn = [] {
     const char* e = std::getenv("SPHEMU_SP_BN");
