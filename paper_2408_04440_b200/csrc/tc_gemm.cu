@@ -226,10 +226,6 @@ struct TcLayout {
   static_assert(kSmem <= 232448, "shared memory budget");
 };
 
-#ifndef SPH_TC_CLAIM_AHEAD
-#define SPH_TC_CLAIM_AHEAD 0
-#endif
-
 template <int BN, int OPK, int MODE, int CG>
 __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap mA_hi, const __grid_constant__ CUtensorMap mA_lo,
@@ -256,11 +252,12 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(wcache + Lay::kEpi * 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  {
-    // An earlier POTRF failed: read once per CTA (the chain's kernel may set
-    // the flag between two threads' reads) so the CTA leaves as a whole; the
-    // two CTAs of a pair both leave before their first cluster barrier.
-    __shared__ int s_fail;
+  // An earlier POTRF failed: read once per CTA (the chain's kernel may set
+  // the flag between two threads' reads) so the CTA leaves as a whole; a
+  // pair uses the leader's read for both CTAs (below, after the cluster
+  // barrier that publishes the peer's mbarriers).
+  __shared__ int s_fail;
+  if constexpr (CG == 1) {
     if (threadIdx.x == 0) s_fail = *(volatile const int*)args.fail;
     __syncthreads();
     if (s_fail >= 0) return;
@@ -280,7 +277,9 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
     for (int s = 0; s < Lay::kEpi * Lay::kRing; ++s) mbar_init(&cfull[s], 1);
     for (int s = 0; s < 4; ++s) {
       mbar_init(&sfull[s], 1);
-      mbar_init(&sempty[s], 1 + Lay::kEpi);
+      // consumers: the MMA warp + the epilogue warps; a pair's leader also
+      // counts the peer's producer and epilogue warps (remote arrivals)
+      mbar_init(&sempty[s], CG == 2 ? 2 + 2 * Lay::kEpi : 1 + Lay::kEpi);
     }
     fence_barrier_init();
   }
@@ -310,6 +309,18 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
   if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  if constexpr (CG == 2) {
+    if (rank == 0 && threadIdx.x == 0) {
+      const int f = *(volatile const int*)args.fail;
+      s_fail = f;
+      st_cluster_u32(mapa_shared(&s_fail, 1), static_cast<uint32_t>(f));
+    }
+    cluster_sync_all();
+    if (s_fail >= 0) {
+      if (warp == 2) tmem_dealloc_cg2(tmem_base, Lay::kTmemCols);
+      return;
+    }
+  }
 
   const int kblocks = args.b / T::kBK;
   const int halves = (MODE == MODE_UPDATE && args.k2 >= 0) ? 2 : 1;  // merged two-step update
@@ -318,15 +329,22 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
   // claimed one by one by the producer and handed to the MMA and epilogue
   // warps through a 4-slot ring, so CTAs that start late (SMs still held by a
   // concurrent kernel) simply find less work left.
-  const bool dyn = CG == 1 && args.counter != nullptr;
+  // Dynamic claims: CTAs (or pair leaders) take items from an atomic counter;
+  // a leader hands each item to its peer through the peer's ring slot.
+  const bool dyn = args.counter != nullptr;
   auto static_item = [&](int64_t n) -> int64_t {
     const int64_t w = cid + n * ncl;
     return w < items ? w : -1;
   };
   auto ring_take = [&](int64_t n) -> int64_t {  // consumer side; caller decides who arrives
     const int slot = static_cast<int>(n & 3);
-    mbar_wait(&sfull[slot], static_cast<uint32_t>((n >> 2) & 1));
+    if constexpr (CG == 2) mbar_wait_cluster(&sfull[slot], static_cast<uint32_t>((n >> 2) & 1));
+    else mbar_wait(&sfull[slot], static_cast<uint32_t>((n >> 2) & 1));
     return static_cast<int64_t>(*(volatile int*)&sched[slot]);
+  };
+  auto ring_release = [&](int64_t n) {  // one consumer's arrival on the (leader's) empty slot
+    if constexpr (CG == 2) mbar_arrive_cluster(mapa_shared(&sempty[n & 3], 0));
+    else mbar_arrive(&sempty[n & 3]);
   };
 
   auto decode = [&](int64_t w, int& i, int& j, int& m0, int& n0) {
@@ -371,30 +389,35 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
       };
       auto publish = [&](int64_t n, int64_t v) {
         const int slot = static_cast<int>(n & 3);
-        mbar_wait(&sempty[slot], static_cast<uint32_t>(((n >> 2) & 1) ^ 1));
-        sched[slot] = static_cast<int>(v);
-        mbar_arrive(&sfull[slot]);  // release: the slot write is visible to the consumers
+        if constexpr (CG == 2) {
+          mbar_wait_cluster(&sempty[slot], static_cast<uint32_t>(((n >> 2) & 1) ^ 1));
+          sched[slot] = static_cast<int>(v);
+          st_cluster_u32(mapa_shared(&sched[slot], 1), static_cast<uint32_t>(v));
+          mbar_arrive(&sfull[slot]);
+          mbar_arrive_cluster(mapa_shared(&sfull[slot], 1));  // release.cluster: orders the remote store
+        } else {
+          mbar_wait(&sempty[slot], static_cast<uint32_t>(((n >> 2) & 1) ^ 1));
+          sched[slot] = static_cast<int>(v);
+          mbar_arrive(&sfull[slot]);  // release: the slot write is visible to the consumers
+        }
       };
-      int64_t w = dyn ? fetch() : static_item(0);
-      if (dyn) publish(0, w);
-#if SPH_TC_CLAIM_AHEAD
-      // Claims run one item further ahead: the atomic for item n + 2 is issued
-      // at the top of item n and its result consumed only after item n's
-      // loads, so its round trip never sits between two items' TMA issues.
-      int64_t w_ahead = dyn ? (w >= 0 ? fetch() : -1) : -1;
-      if (dyn) publish(1, w_ahead);
-#endif
+      // A pair's peer producer is a consumer of the leader's claims.
+      auto claim_item = [&](int64_t n) -> int64_t {
+        if (CG == 2 && rank != 0) {
+          const int64_t v = ring_take(n);
+          ring_release(n);
+          return v;
+        }
+        const int64_t v = fetch();
+        publish(n, v);
+        return v;
+      };
+      int64_t w = dyn ? claim_item(0) : static_item(0);
       int2 ij_cur = w >= 0 ? args.list[w / args.sub_per] : make_int2(0, 0);
       int crow_cur = (MODE == MODE_UPDATE && w >= 0) ? args.crow[w / args.sub_per] : 0;
       prefetch_c(w >= 0 ? w : items, ij_cur, crow_cur);
       for (int64_t n = 0; w >= 0; ++n) {
-#if SPH_TC_CLAIM_AHEAD
-        const int64_t w_next = dyn ? w_ahead : static_item(n + 1);
-        const int64_t claim = (dyn && w_next >= 0) ? atomicAdd(args.counter, 1) : -1;
-#else
-        const int64_t w_next = dyn ? fetch() : static_item(n + 1);
-        if (dyn) publish(n + 1, w_next);
-#endif
+        const int64_t w_next = dyn ? claim_item(n + 1) : static_item(n + 1);
         const int sub = static_cast<int>(w % args.sub_per);
         const int i = ij_cur.x, j = ij_cur.y;
         const int m0 = (sub / args.sub_n) * (TC_BM * CG) + static_cast<int>(rank) * TC_BM;
@@ -449,12 +472,6 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
             phase ^= 1;
           }
         }
-#if SPH_TC_CLAIM_AHEAD
-        if (dyn && w_next >= 0) {
-          w_ahead = claim < items ? claim : -1;
-          publish(n + 2, w_ahead);
-        }
-#endif
         ij_cur = ij_nxt;
         crow_cur = crow_nxt;
         w = w_next;
@@ -472,7 +489,7 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
       if (dyn) {
         w = ring_take(n);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sempty[n & 3]);
+        if (lane == 0) ring_release(n);
       } else {
         w = static_item(n);
       }
@@ -563,7 +580,7 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
       if (dyn) {
         for (; rn <= idx; ++rn) {
           wc[rn & 3] = static_cast<int>(ring_take(rn));
-          mbar_arrive(&sempty[rn & 3]);
+          ring_release(rn);
         }
         return wc[idx & 3];
       }
@@ -1205,7 +1222,17 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
     return e ? std::atoi(e) : 256;
   }();
   const bool pair = (cls == SPHEMU_PREC_SP ? cg_sp : cg_env) == 2 && pf.bn == 256;
-  const bool dyn = !pair && counter != nullptr;
+  // Dynamic claims for CTA pairs (the leader claims and hands the item to
+  // its peer through the peer's ring slot): SPHEMU_TC_PAIR_DYN = 1 the SP
+  // class, 2 all, 0 none (default: static striding measured faster — n =
+  // 64 800 dpsp 234 vs 244 ms, C3 906 vs 915 ms; the per-item handoff sits
+  // in front of the peer's TMA issue).
+  static const int pair_dyn = [] {
+    const char* e = std::getenv("SPHEMU_TC_PAIR_DYN");
+    return e ? std::atoi(e) : 0;
+  }();
+  const bool dyn = counter != nullptr && (!pair || pair_dyn >= 2 || (pair_dyn == 1 && cls == SPHEMU_PREC_SP));
+  a.counter = dyn ? counter : nullptr;
   if (resume && !dyn) return;  // statically scheduled launches never yield
   a.yield = dyn ? yield : nullptr;
   if (cls == SPHEMU_PREC_SP) {

@@ -1,0 +1,7 @@
+timeout 300 python tools/ab.py 32400 dpsp fp16 4
+SPHEMU_RESERVE_EARLY=16 timeout 300 python tools/ab.py 32400 dpsp fp16 4
+timeout 300 python tools/ab.py 129600 dpsphp bf16 2
+timeout 300 python tools/ab.py 64800 dpsp fp16 2
+timeout 300 python tools/chol_timeline.py 32400 512 dpsp 2>/dev/null | head -9
+timeout 300 python tools/timeline_gaps.py 32400 dpsp
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
