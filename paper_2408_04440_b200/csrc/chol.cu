@@ -1146,6 +1146,7 @@ struct Chol {
       for (int p = 0; p < kSets; ++p) {
         panel_[p].alloc(nt, b, pmap, cfg.hp_format, cfg.sp_compute == SPHEMU_SP_F16X3, rowexp.get());
         panel_[p].set_arena(arena.get(), std::max<int64_t>(o, static_cast<int64_t>(128) * b), b);
+        panel_[p].pair_dyn_sp = nt < 96;  // see tc_update
       }
     {
       bool any_dp_update = false;
@@ -1363,20 +1364,19 @@ struct Chol {
     SPH_CUDA(cudaEventRecord(ev0, stream));
     // SMs left to the chain while the bulk runs. Early steps, where the bulk
     // is the critical stream (its work shrinks quadratically, the chain's only
-    // linearly), leave the chain 16 SMs; the last 32 steps leave it 32
+    // linearly), leave the chain 8 SMs; the last 32 steps leave it 32
     // (SPHEMU_RESERVE_EARLY / SPHEMU_RESERVE_TAIL). POTRF's cooperative grid
     // follows the reserve so its CTAs stay co-resident. Measured (1 GPU):
     // C2 58.2 -> 56.4 ms, C3 1 246 -> 1 136 ms against a fixed reserve of 32
     // (tools/reserve_sweep*.sh); with the INT8 DP class and the SP pairs
-    // (statically striped, so the panel no longer gets yielded SMs) 16 beats
-    // 8 for short factorizations: C2 (nt = 64) 48.3 vs 49.8 ms, but C3 (nt =
-    // 254) 938 vs 905 ms and n = 64 800 238 vs 234 ms (tools/exp27/28.sh).
+    // 8 stays best once short factorizations run their SP pairs dynamically
+    // (yielding to the panel): C2 47.8 ms (16: 48.5); static pairs would want
+    // 16 on C2 (48.8 vs 50.3) but 8 on C3 (905 vs 938) (tools/exp27/28/35.sh).
     static const int r_early_env = [] {
       const char* e = std::getenv("SPHEMU_RESERVE_EARLY");
       return e ? std::max(8, std::min(kChainCtas, std::atoi(e))) : 0;
     }();
-    // the bulk's share of the work grows with nt (nt^2 tiles against nt chain steps)
-    const int r_early = r_early_env ? r_early_env : (nt < 96 ? 16 : 8);
+    const int r_early = r_early_env ? r_early_env : 8;
     static const int r_tail = [] {
       const char* e = std::getenv("SPHEMU_RESERVE_TAIL");
       return e ? std::atoi(e) : 32;

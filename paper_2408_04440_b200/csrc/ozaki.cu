@@ -31,22 +31,46 @@ constexpr int OZ_BOX_B = OZ_BN * 128;                   // 8 KB
 constexpr int OZ_STAGE = 2 * OZ_BOX_A + 2 * OZ_BOX_B;   // 48 KB
 constexpr int OZ_STAGES = 4;
 constexpr int OZ_SMEM = OZ_STAGES * OZ_STAGE + 1024 /*align*/ + 256 /*barriers, ring, TMEM holder*/;
-constexpr int OZ_THREADS = 256;  // warp 0 TMA, 1 MMA, 2 TMEM owner, 3 idle, 4-7 epilogue
+#ifndef OZ_EPI_WARPS
+#define OZ_EPI_WARPS 8
+#endif
+constexpr int OZ_EPI = OZ_EPI_WARPS;  // per TMEM lane quarter: 1 (64 columns) or 2 (32 columns each)
+constexpr int OZ_THREADS = 32 * (4 + OZ_EPI);  // warp 0 TMA, 1 MMA, 2 TMEM owner, 3 idle, then the epilogue
 
 // S32 accumulate, signed int8 A and B, K-major, M = 128, N = 64.
 constexpr uint32_t kOzIdesc =
     (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(OZ_BN >> 3) << 17) | (static_cast<uint32_t>(OZ_BM >> 4) << 24);
 
+// Executed by the whole (converged) MMA warp: one elected lane issues, so the
+// operands stay warp-uniform and the compiler keeps them in uniform
+// registers (issued from a lane == 0 branch, every MMA paid ~16 extra
+// instructions of per-lane broadcast: N = 64 MMAs are short enough for that
+// to throttle the tensor pipe).
 __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(kOzIdesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_addr(bar))
+      : "memory");
 }
 
 // 2^mu_g bounds |panel row g| with one bit of headroom: rowexp = 14 - E
 // with sqrt(a_gg) < 2^E (k_rowexp), so mu = E + 1.
 __device__ __forceinline__ int oz_mu(const int* rowexp, int g) { return 15 - __ldg(rowexp + g); }
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 __device__ __forceinline__ double pow2(int e) { return __longlong_as_double(static_cast<long long>(1023 + e) << 52); }
 
 __global__ void __launch_bounds__(256) k_oz_slice(TileStore ts, int k, const double* __restrict__ p64, int64_t row_begin,
@@ -115,8 +139,8 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_STAGES * OZ_STAGE);
   uint64_t* empty = full + OZ_STAGES;
   uint64_t* tfull = empty + OZ_STAGES;
-  uint64_t* tempty = tfull + 1;
-  uint64_t* sfull = tempty + 1;
+  uint64_t* tempty = tfull + 1;  // [OZ_DIGITS]: accumulator C_d drained
+  uint64_t* sfull = tempty + OZ_DIGITS;
   uint64_t* sempty = sfull + 4;
   int* sched = reinterpret_cast<int*>(sempty + 4);
   uint32_t* holder = reinterpret_cast<uint32_t*>(sched + 4);
@@ -134,10 +158,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);
+    for (int d = 0; d < OZ_DIGITS; ++d) mbar_init(&tempty[d], OZ_EPI);
     for (int s = 0; s < 4; ++s) {
       mbar_init(&sfull[s], 1);
-      mbar_init(&sempty[s], 5);  // the MMA warp + 4 epilogue warps
+      mbar_init(&sempty[s], 1 + OZ_EPI);  // the MMA warp + the epilogue warps
     }
     fence_barrier_init();
   }
@@ -231,40 +255,50 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sempty[n & 3]);
       if (w < 0) break;
-      mbar_wait(tempty, acc_phase ^ 1);
-      tc_fence_after();
       for (int kb2 = 0; kb2 < kblocks * halves; ++kb2) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        if (lane == 0 && args.dbg == 2) {
-          umma_commit(&empty[stage]);
-        } else if (lane == 0) {
+        if (args.dbg == 2) {
+          if (kb2 == 0)
+            for (int d = 0; d < OZ_DIGITS; ++d) mbar_wait(&tempty[d], acc_phase ^ 1);
+          umma_commit_elect(&empty[stage]);
+        } else {
           uint8_t* st = smem + stage * OZ_STAGE;
           const uint64_t a0 = umma_desc_sw128(st), a1 = umma_desc_sw128(st + OZ_BOX_A);
           const uint64_t b0 = umma_desc_sw128(st + 2 * OZ_BOX_A), b1 = umma_desc_sw128(st + 2 * OZ_BOX_A + OZ_BOX_B);
+          // Digit-major order (consecutive MMAs go to different accumulators:
+          // N = 64 MMAs are too short to hide a same-accumulator dependency).
+          // The first chunk of a block touches C_0, C_1, ..., C_7 first at
+          // s = 0, the order the epilogue drains them: each waits for its
+          // accumulator just before that MMA, so the previous block's
+          // epilogue overlaps these MMAs.
 #pragma unroll
           for (int s = 0; s < OZ_DIGITS; ++s) {
             const uint64_t ad = (s < 4 ? a0 : a1) + 2 * (s & 3);  // 32-byte K offset inside the swizzled row
 #pragma unroll
             for (int t = 0; t + s < OZ_DIGITS; ++t) {
+              if (kb2 == 0 && s == 0) {
+                mbar_wait(&tempty[t], acc_phase ^ 1);
+                tc_fence_after();
+              }
               const uint64_t bd = (t < 4 ? b0 : b1) + 2 * (t & 3);
               umma_i8(tmem + (s + t) * OZ_BN, ad, bd, (kb2 > 0 || s > 0) ? 1u : 0u);
             }
           }
-          umma_commit(&empty[stage]);
+          umma_commit_elect(&empty[stage]);
         }
-        __syncwarp();
         if (++stage == OZ_STAGES) {
           stage = 0;
           phase ^= 1;
         }
       }
-      if (lane == 0) umma_commit(tfull);
-      __syncwarp();
+      umma_commit_elect(tfull);
       acc_phase ^= 1;
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;
+    constexpr int NH = 8 / OZ_EPI;      // 32-column halves per warp
+    const int q = warp & 3;             // TMEM lane quarter (hardware: warp % 4)
+    const int h0 = ((warp - 4) >> 2) * NH;
     const int row = q * 32 + lane;
     uint32_t acc_phase = 0;
     const TileStore& ts = args.ts;
@@ -278,45 +312,54 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       if (w < 0) break;
       int i, j, r0, c0;
       decode(w, i, j, r0, c0);
-      const double si = pow2(oz_mu(args.rowexp, min(i * ts.lb + r0 + row, ts.n - 1)));
-      double* crow = static_cast<double*>(ts.tile(i, j)) + static_cast<int64_t>(r0 + row) * b + c0;
-      mbar_wait(tfull, acc_phase);
+      // the accumulators take a whole block of MMAs: wait politely, the MMA
+      // and TMA warps share these warps' schedulers
+      while (!mbar_try(tfull, acc_phase)) __nanosleep(128);
       tc_fence_after();
+      double v[NH][32];
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[hh][c] = 0.0;
+      // C_0 2^-14, ..., C_7 2^-63 (the MMA warp's first-touch order); each
+      // drained accumulator goes straight back to the MMA warp
 #pragma unroll 1
-      for (int h = 0; h < (args.dbg ? 0 : 2); ++h) {
-        double v[32];
+      for (int d = 0; d < OZ_DIGITS; ++d) {
+        uint32_t x[NH][32];
+        if (!args.dbg) {
 #pragma unroll
-        for (int c = 0; c < 32; ++c) v[c] = 0.0;
-        // smallest weights first: C_7 2^-63, ..., C_0 2^-14
-#pragma unroll 1
-        for (int d = OZ_DIGITS - 1; d >= 0; --d) {
-          uint32_t x[32];
-          tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + d * OZ_BN + h * 32, x);
-          const double wgt = pow2(-7 * (d + 2));
-#pragma unroll
-          for (int c = 0; c < 32; ++c) v[c] = fma(static_cast<double>(static_cast<int>(x[c])), wgt, v[c]);
+          for (int hh = 0; hh < NH; ++hh)
+            tmem_ld32_nowait(tmem + (static_cast<uint32_t>(q * 32) << 16) + d * OZ_BN + (h0 + hh) * 32, x[hh]);
+          tmem_wait_ld();
         }
-        if (h == 1) {  // every accumulator column is in registers: the MMA warp may start the next block
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(tempty);
-        }
-        double2* cp = reinterpret_cast<double2*>(crow + h * 32);
-#pragma unroll
-        for (int c2 = 0; c2 < 16; ++c2) {
-          const int cg = j * ts.lb + c0 + h * 32 + 2 * c2;
-          const double s0 = si * pow2(oz_mu(args.rowexp, min(cg, ts.n - 1)));
-          const double s1 = si * pow2(oz_mu(args.rowexp, min(cg + 1, ts.n - 1)));
-          double2 cur = cp[c2];
-          cur.x -= v[2 * c2] * s0;
-          cur.y -= v[2 * c2 + 1] * s1;
-          cp[c2] = cur;
-        }
-      }
-      if (args.dbg) {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty);
+        if (lane == 0) mbar_arrive(&tempty[d]);
+        if (!args.dbg) {
+          const double wgt = pow2(-7 * (d + 2));
+#pragma unroll
+          for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[hh][c] = fma(static_cast<double>(static_cast<int>(x[hh][c])), wgt, v[hh][c]);
+        }
+      }
+      if (!args.dbg) {
+        const double si = pow2(oz_mu(args.rowexp, min(i * ts.lb + r0 + row, ts.n - 1)));
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh) {
+          const int cb = c0 + (h0 + hh) * 32;
+          double2* cp = reinterpret_cast<double2*>(static_cast<double*>(ts.tile(i, j)) + static_cast<int64_t>(r0 + row) * b + cb);
+#pragma unroll
+          for (int c2 = 0; c2 < 16; ++c2) {
+            const int cg = j * ts.lb + cb + 2 * c2;
+            const double s0 = si * pow2(oz_mu(args.rowexp, min(cg, ts.n - 1)));
+            const double s1 = si * pow2(oz_mu(args.rowexp, min(cg + 1, ts.n - 1)));
+            double2 cur = cp[c2];
+            cur.x -= v[hh][2 * c2] * s0;
+            cur.y -= v[hh][2 * c2 + 1] * s1;
+            cp[c2] = cur;
+          }
+        }
       }
       acc_phase ^= 1;
     }

@@ -412,12 +412,23 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
         publish(n, v);
         return v;
       };
+      // A pair's leader claims one item further ahead, so the peer finds its
+      // next item already published at the top of each item (the claim's
+      // atomic and the cross-CTA handoff stay off the peer's TMA issue).
+      constexpr bool kAhead = CG == 2;
       int64_t w = dyn ? claim_item(0) : static_item(0);
+      int64_t w_ahead = (dyn && kAhead && rank == 0 && w >= 0) ? claim_item(1) : -1;
       int2 ij_cur = w >= 0 ? args.list[w / args.sub_per] : make_int2(0, 0);
       int crow_cur = (MODE == MODE_UPDATE && w >= 0) ? args.crow[w / args.sub_per] : 0;
       prefetch_c(w >= 0 ? w : items, ij_cur, crow_cur);
       for (int64_t n = 0; w >= 0; ++n) {
-        const int64_t w_next = dyn ? claim_item(n + 1) : static_item(n + 1);
+        int64_t w_next;
+        if (dyn && kAhead && rank == 0) {
+          w_next = w_ahead;
+          w_ahead = w_next >= 0 ? claim_item(n + 2) : -1;
+        } else {
+          w_next = dyn ? claim_item(n + 1) : static_item(n + 1);
+        }
         const int sub = static_cast<int>(w % args.sub_per);
         const int i = ij_cur.x, j = ij_cur.y;
         const int m0 = (sub / args.sub_n) * (TC_BM * CG) + static_cast<int>(rank) * TC_BM;
@@ -1222,15 +1233,18 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
     return e ? std::atoi(e) : 256;
   }();
   const bool pair = (cls == SPHEMU_PREC_SP ? cg_sp : cg_env) == 2 && pf.bn == 256;
-  // Dynamic claims for CTA pairs (the leader claims and hands the item to
-  // its peer through the peer's ring slot): SPHEMU_TC_PAIR_DYN = 1 the SP
-  // class, 2 all, 0 none (default: static striding measured faster — n =
-  // 64 800 dpsp 234 vs 244 ms, C3 906 vs 915 ms; the per-item handoff sits
-  // in front of the peer's TMA issue).
-  static const int pair_dyn = [] {
+  // Dynamic claims for CTA pairs (the leader claims one item ahead and hands
+  // it to its peer through the peer's ring slot): they let the pair yield
+  // its SMs to the chain's panel, which pays off on short factorizations
+  // (C2, nt = 64: 47.8 vs 48.8 ms at the best reserve of each) but costs
+  // throughput on long ones (n = 64 800: 237.7 vs 233.9 ms; C3: 910 vs 897
+  // ms). pf.pair_dyn_sp (the handle's choice, nt < 96) selects it for the SP
+  // class; SPHEMU_TC_PAIR_DYN = 0 none, 1 the SP class, 2 all overrides.
+  static const int pair_dyn_env = [] {
     const char* e = std::getenv("SPHEMU_TC_PAIR_DYN");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : -1;
   }();
+  const int pair_dyn = pair_dyn_env >= 0 ? pair_dyn_env : (pf.pair_dyn_sp ? 1 : 0);
   const bool dyn = counter != nullptr && (!pair || pair_dyn >= 2 || (pair_dyn == 1 && cls == SPHEMU_PREC_SP));
   a.counter = dyn ? counter : nullptr;
   if (resume && !dyn) return;  // statically scheduled launches never yield

@@ -56,6 +56,7 @@ struct PanelFormats {
   CUtensorMap m_c16{}, m_c32{};  // C operand: the tile arena as 16-bit / fp32 rows (set_arena)
   void set_arena(const void* base, int64_t bytes, int b_);
   int bn = 256;
+  bool pair_dyn_sp = false;  // SP-class CTA pairs claim items dynamically (and yield); see tc_update
   void alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int hp_format_, bool f16x3_,
              const int* rowexp_);
 };
