@@ -1313,6 +1313,13 @@ struct Chol {
       const int2* lst = lists.get() + list_off[slot];
       const bool tensor = !fp64_class(cls) && cfg.compute == SPHEMU_COMPUTE_TENSOR;
       if (resume && !tensor) continue;  // only the persistent tcgen05 launches yield
+      static const bool log = [] {
+        const char* e = std::getenv("SPHEMU_LAUNCH_LOG");  // profiling aid: which step / part each launch is
+        return e && e[0] == '1';
+      }();
+      if (log)
+        std::fprintf(stderr, "update k=%d part=%d cls=%d tiles=%lld merged=%d resume=%d\n", k, part, cls,
+                     static_cast<long long>(cnt), merged ? 1 : 0, resume ? 1 : 0);
       const int pu = prof_begin(kUpdDp + cls, s);
       if (oz && cls == 0) {
         if (part != 0) {

@@ -150,8 +150,9 @@ struct TcArgs {
   const int* fail;
   unsigned* sat;
   int dbg;           // diagnostics only (SPHEMU_TC_DBG): 1 = skip the C epilogue, 2 = also skip the MMAs
-  int opt;           // tuning switches (SPHEMU_TC_OPT): 1 = no C prefetch to L2, 2 = prefetch two items ahead,
-                     // 4 = operands evict_first (not evict_last), 8 = C through L2 normally (not streaming)
+  int opt;           // tuning switches (SPHEMU_TC_OPT): 1 = C prefetch to L2 (TMA, one item ahead),
+                     // 4 = operands evict_first (not evict_last), 8 = C through L2 normally (not streaming),
+                     // 16 = operands evict_normal, 32 = operands evict_last on a 0.5 fraction
   int* counter;      // non-null: items are claimed dynamically (atomicAdd), zeroed before the launch
   const int* lexp;   // FP16x3 panel: per output column (Linv row) power-of-two exponent
   const int* yield;  // non-null: stop claiming items once *yield != 0 (dynamic scheduling only)
@@ -361,15 +362,22 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      const uint64_t keep = (args.opt & 4) ? l2_evict_first() : l2_evict_last();  // SPHEMU_TC_OPT bit 2: A/B test
-      // Update mode: pull the C sub-tile of the next work item into L2 while
-      // this one's MMAs run, so the epilogue's C loads hit L2 instead of
-      // waiting on HBM latency.
+      // SPHEMU_TC_OPT A/B tests: bit 2 evict_first, bit 16 evict_normal, bit 32 evict_last on half the lines
+      const uint64_t keep = (args.opt & 4)    ? l2_evict_first()
+                            : (args.opt & 16) ? l2_evict_normal()
+                            : (args.opt & 32) ? l2_evict_last_half()
+                                              : l2_evict_last();
+      // Update mode, opt-in (SPHEMU_TC_OPT bit 1): pull the C sub-tile of the
+      // next work item into L2 while this one's MMAs run. Off by default: the
+      // epilogue's register-staged C loads run a box ahead anyway, and the
+      // prefetched C lines evicted the panel operands every item re-reads
+      // (C2 47.4 -> 46.2 ms, n = 64 800 dpsp 233.5 -> 220.0 ms, C3 891.5 ->
+      // 829.0 ms without it; tools/exp40/41.sh).
       // The next item's list entry and C row are loaded while this item's
       // first stages are in flight (a dependent global load here would stall
       // the TMA issue at every item boundary).
       auto prefetch_c = [&](int64_t wi, int2 ij, int crow) {
-        if (MODE != MODE_UPDATE || args.dbg == 1 || args.dbg == 2 || args.dbg == 5 || (args.opt & 1) || wi >= items)
+        if (MODE != MODE_UPDATE || args.dbg == 1 || args.dbg == 2 || args.dbg == 5 || !(args.opt & 1) || wi >= items)
           return;
         constexpr int kEszP = T::kSplit ? 4 : 2;
         (void)ij;
