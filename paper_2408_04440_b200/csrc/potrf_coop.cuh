@@ -18,40 +18,45 @@
 namespace sphemu_gpu {
 
 constexpr int PC_BLK = 64;
+// Row stride of the 64 x 64 operand blocks staged for the DMMA products: 68
+// doubles keeps the m8n8k4 fragment loads conflict-free per half-warp.
+constexpr int PG_LD = 68;
 
 struct PcSmallSmem {
   double T[64][65];
   double Di[64][65];
   double M[32][33];
+  double X[64][PG_LD];  // CTA 0: its phase-A TRSM result X_{s+1,s}, the lookahead SYRK's operand
   double col[17];  // base-case column broadcast
   int bad;
 };
 
-// 16 x 16 base case (warp 0; lanes 0..15 own the rows): right-looking
-// Cholesky with one rsqrt per column, the factored column broadcast through
-// shared memory (s.col), then the inverse by forward substitution (lane j owns
-// column j, reading L from s.T). Small unrolled code: the cooperative kernel
-// is sensitive to instruction-cache pressure.
+// 16 x 16 base case (warp 0; lanes 0..15 own the rows, 16..31 mirror them):
+// right-looking Cholesky with one rsqrt per column. The column values move by
+// shuffles, and the next pivot goes first: lane c+1 forms its updated
+// diagonal from its own l_{c+1,c} and broadcasts it before the other rows'
+// updates, so a column's critical path is rsqrt -> fma -> shuffle (the
+// earlier shared-memory broadcast put a store, a warp barrier and a load in
+// every step). Same arithmetic as the row updates: bitwise the same factor.
+// Then the inverse by forward substitution (lane j owns column j, reading L
+// from s.T). Small unrolled code: the cooperative kernel is sensitive to
+// instruction-cache pressure.
 __device__ __noinline__ void pc_base16(PcSmallSmem& s, int o, int w, int lane) {
   const int row = lane & 15;
   double a[16], rl[16];
 #pragma unroll
   for (int t = 0; t < 16; ++t) a[t] = s.T[o + row][o + t];
   bool ok = true;
+  double piv = __shfl_sync(0xffffffffu, a[0], 0);
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
-    if (lane == c) s.col[16] = a[c];
-    __syncwarp();
-    const double piv = s.col[16];
     if (c < w && !(piv > 0.0)) ok = false;
     rl[c] = rsqrt(piv);
     const double lrc = (row == c) ? piv * rl[c] : a[c] * rl[c];
     a[c] = lrc;
-    if (lane < 16) s.col[row] = lrc;
-    __syncwarp();
+    if (c + 1 < 16) piv = __shfl_sync(0xffffffffu, fma(-lrc, lrc, a[c + 1]), c + 1);
 #pragma unroll
-    for (int j = c + 1; j < 16; ++j) a[j] -= lrc * s.col[j];
-    __syncwarp();
+    for (int j = c + 1; j < 16; ++j) a[j] = fma(-lrc, __shfl_sync(0xffffffffu, lrc, j), a[j]);
   }
   if (!ok) {
     if (lane == 0) s.bad = 1;
@@ -182,14 +187,10 @@ __device__ unsigned long long* g_potrf_trace;
   } while (0)
 #endif
 
-// Factor + invert the 64 x 64 diagonal block at (j0, j0) (w valid rows).
-// Returns false on a bad pivot (not > 0, or NaN) among the first w columns.
 // 64 x 64 x K (K <= 64) FP64 product with both operands staged whole in
 // shared memory by cp.async (every load in flight at once: one memory round
 // trip instead of one per K-chunk), then 16 DMMA k-steps. Same accumulator
-// layout as dgemm_64x64 (dg_for_each). Row stride 68 doubles keeps the
-// m8n8k4 fragment loads conflict-free per half-warp.
-constexpr int PG_LD = 68;
+// layout as dgemm_64x64 (dg_for_each).
 struct PgSmem {
   double a[64 * PG_LD];
   double b[64 * PG_LD];
@@ -209,6 +210,29 @@ __device__ __forceinline__ void pg_stage(const Acc& X, int K, double* s) {
       src = X.base + (int64_t)row * X.ld + col;
     }
     cp_async16(s + row * PG_LD + col, src, bytes);
+  }
+}
+
+// acc = X X^T for a 64 x K block X already in shared memory (row stride
+// PG_LD, zero beyond K): the lookahead SYRK without a memory round trip.
+__device__ __forceinline__ void pg_syrk_smem(const double* X, int K, double (&acc)[4][4][2]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int kq = lane & 3, rq = lane >> 2;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  for (int kk = 0; kk < K; kk += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = X[(wm * 32 + mi * 8 + rq) * PG_LD + kk + kq];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = X[(wn * 32 + ni * 8 + rq) * PG_LD + kk + kq];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma_8x8x4(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
   }
 }
 
@@ -354,6 +378,17 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
     const double* dinv = dinv_all + (int64_t)s * PC_BLK * PC_BLK;
     // ---- phase A ----
     const int n_trsm = nblk - s - 1;
+    if (cta == 0 && n_trsm > 0) {
+      // CTA 0's lookahead operand A_{s+1,s+1} (lower part) streams into
+      // shared memory under this phase's products (waited for in phase B).
+      const int r = s + 1, rr = rows_of(r), j0 = r * PC_BLK;
+      for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+        const int ri = e >> 6, ci = e & 63;
+        const bool in = ri < rr && ci <= ri;
+        cp_async8(&ss.T[ri][ci], in ? A + (int64_t)(j0 + ri) * b + j0 + ci : A, in ? 8 : 0);
+      }
+      cp_async_commit();
+    }
     for (int item = cta; item < n_trsm + s + 1; item += G) {
       if (item < n_trsm) {  // TRSM, in place (one CTA owns each block)
         const int r = s + 1 + item;
@@ -365,6 +400,8 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
         dg_for_each(acc, [&](int i, int j, double v) {
           if (i < rr && j < w) out[(int64_t)i * b + j] = v;
         });
+        if (item == 0)  // CTA 0: X_{s+1,s} stays in shared memory for the lookahead SYRK
+          dg_for_each(acc, [&](int i, int j, double v) { ss.X[i][j] = (i < rr && j < w) ? v : 0.0; });
       } else {  // TRTRI X_sc = Dinv_s R_sc, in place
         const int c = item - n_trsm;
         RowMajorK d{dinv, PC_BLK, w, w};
@@ -385,17 +422,13 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
     // ---- phase B ----
     if (cta == 0) {
       if (s + 1 < nblk) {
-        // Lookahead block: A_rr -= X_rs X_rs^T straight into shared memory
-        // (A_rr staged by cp.async while the SYRK runs), then factor+invert.
+        // Lookahead block: A_rr -= X_rs X_rs^T with both operands already in
+        // shared memory (X from this CTA's phase-A TRSM, A_rr prefetched at
+        // the start of phase A), then factor+invert.
         const int r = s + 1, rr = rows_of(r), j0 = r * PC_BLK;
-        for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
-          const int ri = e >> 6, ci = e & 63;
-          const bool in = ri < rr && ci <= ri;
-          cp_async8(&ss.T[ri][ci], in ? A + (int64_t)(j0 + ri) * b + j0 + ci : A, in ? 8 : 0);
-        }
-        cp_async_commit();
-        RowMajorK x1{blk(A, b, r, s), b, rr, w};
-        pgemm_64(x1, x1, w, sm, acc);  // waits for every cp.async group, incl. the staging
+        cp_async_wait<0>();
+        __syncthreads();
+        pg_syrk_smem(&ss.X[0][0], w, acc);
         dg_for_each(acc, [&](int i, int j, double v) {
           if (i < rr && j <= i) ss.T[i][j] -= v;
         });
