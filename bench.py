@@ -450,7 +450,7 @@ def roofline(h, wl, args, phases, steps, ms):
     if args.sp_compute == "fp16x3":
         p_sp = own.get("fp16_tflops", 1546.6) / 3
         sp_src = "cuBLAS FP16 GEMM measured on this pool / 3 (3 kind::f16 MMAs per product; profiles/peaks_r01.json)"
-        sp_kernel = "k_tc_gemm<128, F16x3, UPDATE, 1> (SP-class trailing update, row-scaled fp16 hi+lo)"
+        sp_kernel = "k_tc_gemm<128, F16x3, UPDATE, 2> (SP-class trailing update, CTA pairs, row-scaled fp16 hi+lo)"
     else:
         p_sp = own.get("tf32x3_effective_tflops", 244.7)
         sp_src = "cuBLAS TF32 GEMM measured on this pool / 3 (profiles/peaks_r01.json)"
@@ -466,7 +466,7 @@ def roofline(h, wl, args, phases, steps, ms):
     sp_kernel = sp_kernel.replace("<128,", f"<{bn},")
     hp_kernel = hp_kernel.replace("<128,", f"<{bn},")
     cls = {"dp": ("update_dp", p_dp, "FP64 DGEMM measured on this pool (profiles/peaks_r01.json)",
-                  "k_update_fp64_v2 (DP-class trailing update, DMMA)"),
+                  "k_oz_update (DP-class trailing update, INT8 tensor-core digits; DMMA for the dp variant)"),
            "sp": ("update_sp", p_sp, sp_src, sp_kernel),
            "hp": ("update_hp", p_hp, hp_src, hp_kernel)}
     dom_c = dominant_class(wl)
@@ -474,13 +474,21 @@ def roofline(h, wl, args, phases, steps, ms):
     t = phases[ph]["ms"] / steps
     ach = cuf[dom_c] / (t * 1e-3) / 1e12 if t > 0 else None
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "r01_traffic.json")
-    if os.path.exists(tf) and dom_c in ("sp", "hp"):
-        tj = json.load(open(tf))[dom_c]
+    for name in ("r02_traffic.json", "r01_traffic.json"):
+        tf = os.path.join(ROOT, "profiles", name)
+        if not os.path.exists(tf):
+            continue
+        tj = json.load(open(tf)).get(dom_c)
+        if tj is None:
+            continue
         traffic = {"dram_bytes_per_launch": tj["dram_read_bytes"] + tj["dram_write_bytes"],
                    "algorithmic_bytes_per_launch": tj["c_bytes"] + tj["panel_operand_bytes"],
-                   "launch": f"{tj['workload']}: {tj['sub_tiles']} sub-tiles of 128x256, K=512",
-                   "source": "profiles/r01_traffic.json (ncu --set full, one launch)"}
+                   "launch": tj["workload"] + (f", {tj['duration_us']} us alone" if "duration_us" in tj else ""),
+                   "source": f"profiles/{name} (ncu --set full, one launch)"}
+        if "flops" in tj and "duration_us" in tj:
+            traffic["isolated_tflops"] = tj["flops"] / (tj["duration_us"] * 1e-6) / 1e12
+            traffic["isolated_frac"] = traffic["isolated_tflops"] / peak
+        break
     # The bulk update runs on SMs - reserve CTAs (the reserve serves the
     # POTRF/panel chain stream concurrently); frac is against the whole GPU.
     import torch
@@ -491,6 +499,9 @@ def roofline(h, wl, args, phases, steps, ms):
     bulk = [n_sm - 8, n_sm - 32] if world == 1 else [n_sm - (32 if world < 4 else 48)]
     dom = {"kernel": kern, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
            "frac": ach / peak if ach else None, "peak_source": src, "traffic": traffic,
+           "peak_mma_issue": {"f16_tflops": 2229.0, "i8_tops": 4577.0,
+                              "source": "profiles/r02_umma_rate.txt (tools/micro/umma_rate.cu: raw tcgen05.mma "
+                                        "rate, M=128 N>=128); the SP class needs 3 f16 MMAs per product"},
            "sms": {"bulk_ctas": bulk, "device_sms": n_sm,
                    "note": "the bulk update runs on these CTAs while the POTRF/panel chain holds the rest"},
            "per_launch_basis": f"{cuf[dom_c]/1e12:.3f} TFLOP of {dom_c.upper()}-class update per step on this rank "

@@ -1159,7 +1159,7 @@ struct Chol {
       // Not for the exact modes: the pure-FP64 variant and sp_compute = fp64
       // keep every FP64-class update on DMMA.
       oz = dp_emu_env() && cfg.variant != SPHEMU_VARIANT_DP && cfg.sp_compute != SPHEMU_SP_FP64 &&
-           cfg.compute == SPHEMU_COMPUTE_TENSOR && nt > 1 && b % 128 == 0 && !dist() && any_dp_update;
+           cfg.compute == SPHEMU_COMPUTE_TENSOR && nt > 1 && b % 128 == 0 && any_dp_update;
       if (oz)
         for (int p = 0; p < kSets; ++p) oz_[p].alloc(static_cast<int64_t>(nt - 1) * b, b);
       oz_rest.assign(nt, 0);
@@ -1265,7 +1265,7 @@ struct Chol {
       const int2* base = plists.get() + plist_off[k];
       tc_panel_trsm(store(), k, base, plist_dp[k], base + plist_dp[k], plist_lo[k], linv_[set].get(),
                     p64_[set].get(), panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s, 3));
-      if (oz && k + 1 < nt)  // tile k+1's digits: the chain's diagonal SYRK of the next step
+      if (oz && k + 1 < nt && !dist())  // tile k+1's digits: the chain's diagonal SYRK of the next step
         oz_slice(store(), k, p64_[set].get(), 0, b, rowexp.get(), oz_[set], fail.get(), s);
     } else {
       const int below = nt - k - 1;
@@ -1644,6 +1644,9 @@ struct Chol {
           rowexp.get(), cfg.hp_format, fail.get());
       SPH_LAUNCH_CHECK();
     }
+    // tile k+1's digits (the chain's diagonal SYRK of the next step), once
+    // its panel rows are here
+    if (oz && k + 1 < nt) oz_slice(store(), k, p64_[set].get(), 0, b, rowexp.get(), oz_[set], fail.get(), s);
     prof_end(px, s);
   }
 
