@@ -551,6 +551,12 @@ struct Chol {
   OzSlices oz_[kSets];
   bool oz = false;
   std::vector<uint8_t> oz_rest;
+  // Tiles whose panel rows some DP-class update on this rank reads (every
+  // diagonal tile on one GPU; the owned DP tiles' rows and columns on a
+  // process grid), ascending: the digits are cut for these rows only.
+  std::vector<int> oz_tiles;
+  std::vector<uint8_t> oz_need;
+  DevBuf<int> d_oz_tiles;
   // SPHEMU_DP_EMU=0: DP-class updates on FP64 DMMA instead.
   static bool dp_emu_env() {
     static const bool on = [] {
@@ -562,8 +568,16 @@ struct Chol {
   void oz_slice_rest(int k, cudaStream_t s) {
     if (oz_rest[k]) return;
     oz_rest[k] = 1;
-    oz_slice(store(), k, p64_[set_of(k)].get(), b, static_cast<int64_t>(nt - k - 1) * b, rowexp.get(),
-             oz_[set_of(k)], fail.get(), s);
+    // the needed tiles below k+1 (block 0, tile k+1, is cut with the panel)
+    const auto first = std::lower_bound(oz_tiles.begin(), oz_tiles.end(), k + 2);
+    const int64_t cnt = oz_tiles.end() - first;
+    if (cnt)
+      oz_slice_tiles(store(), k, p64_[set_of(k)].get(), d_oz_tiles.get() + (first - oz_tiles.begin()), cnt,
+                     rowexp.get(), oz_[set_of(k)], fail.get(), s);
+  }
+  void oz_slice_next(int k, cudaStream_t s) {  // tile k+1's rows, for the chain's diagonal SYRK
+    if (oz && k + 1 < nt && oz_need[k + 1])
+      oz_slice(store(), k, p64_[set_of(k)].get(), 0, b, rowexp.get(), oz_[set_of(k)], fail.get(), s);
   }
   DevBuf<double> dinv, spd_d, spd_pw;
   DevBuf<int> rowexp;  // per-row power-of-two operand scale (FP16x3 SP path)
@@ -1160,8 +1174,18 @@ struct Chol {
       // keep every FP64-class update on DMMA.
       oz = dp_emu_env() && cfg.variant != SPHEMU_VARIANT_DP && cfg.sp_compute != SPHEMU_SP_FP64 &&
            cfg.compute == SPHEMU_COMPUTE_TENSOR && nt > 1 && b % 128 == 0 && any_dp_update;
-      if (oz)
+      oz_need.assign(nt, 0);
+      for (int i = 1; i < nt; ++i)
+        for (int j = 1; j <= i; ++j)
+          if (pmap[tix(i, j)] == SPHEMU_PREC_DP && mine(i, j)) oz_need[i] = oz_need[j] = 1;
+      oz_tiles.clear();
+      for (int q = 0; q < nt; ++q)
+        if (oz_need[q]) oz_tiles.push_back(q);
+      if (oz) {
         for (int p = 0; p < kSets; ++p) oz_[p].alloc(static_cast<int64_t>(nt - 1) * b, b);
+        d_oz_tiles.alloc(oz_tiles.size());
+        SPH_CUDA(cudaMemcpy(d_oz_tiles.get(), oz_tiles.data(), oz_tiles.size() * sizeof(int), cudaMemcpyHostToDevice));
+      }
       oz_rest.assign(nt, 0);
     }
     int prio_lo = 0, prio_hi = 0;
@@ -1265,8 +1289,7 @@ struct Chol {
       const int2* base = plists.get() + plist_off[k];
       tc_panel_trsm(store(), k, base, plist_dp[k], base + plist_dp[k], plist_lo[k], linv_[set].get(),
                     p64_[set].get(), panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s, 3));
-      if (oz && k + 1 < nt && !dist())  // tile k+1's digits: the chain's diagonal SYRK of the next step
-        oz_slice(store(), k, p64_[set].get(), 0, b, rowexp.get(), oz_[set], fail.get(), s);
+      if (!dist()) oz_slice_next(k, s);
     } else {
       const int below = nt - k - 1;
       k_panel_trsm_fp64<<<dim3(below * (b / DG_BM), b / DG_BN), DG_THREADS, 0, s>>>(
@@ -1489,7 +1512,9 @@ struct Chol {
     };
     // chain reserve: one GPU as reserve_at; the distributed chain also carries the exchange (factor_dist)
     const char* env_reserve = std::getenv("SPHEMU_DIST_RESERVE");
-    const int dist_reserve = env_reserve ? std::atoi(env_reserve) : (P * Q >= 4 ? 48 : kChainCtas);
+    // 32 SMs for the distributed chain (it also packs, exchanges and imports
+    // the panel): C3 on 2 x 2 379 ms against 386 (48), 415 (16), 418 (64)
+    const int dist_reserve = env_reserve ? std::atoi(env_reserve) : kChainCtas;
     auto reserve_for = [&](int k) { return D ? dist_reserve : reserve_at(k); };
     if (!cfg.lookahead) {
       potrf(0, stream);
@@ -1646,7 +1671,7 @@ struct Chol {
     }
     // tile k+1's digits (the chain's diagonal SYRK of the next step), once
     // its panel rows are here
-    if (oz && k + 1 < nt) oz_slice(store(), k, p64_[set].get(), 0, b, rowexp.get(), oz_[set], fail.get(), s);
+    oz_slice_next(k, s);
     prof_end(px, s);
   }
 

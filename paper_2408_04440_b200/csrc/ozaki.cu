@@ -73,16 +73,20 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 }
 __device__ __forceinline__ double pow2(int e) { return __longlong_as_double(static_cast<long long>(1023 + e) << 52); }
 
+// tiles != nullptr: rows [0, rows) index the panel rows of tiles[0..] (b
+// each) instead of the contiguous range starting at row_begin.
 __global__ void __launch_bounds__(256) k_oz_slice(TileStore ts, int k, const double* __restrict__ p64, int64_t row_begin,
-                                                  int64_t row_end, const int* __restrict__ rowexp,
-                                                  uint8_t* __restrict__ s8, const int* fail) {
+                                                  int64_t rows, const int* __restrict__ tiles,
+                                                  const int* __restrict__ rowexp, uint8_t* __restrict__ s8,
+                                                  const int* fail) {
   if (*(volatile const int*)fail >= 0) return;
   const int b = ts.b;
   const int chunks = b / 128;
   const int64_t w = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  const int64_t r = row_begin + w / chunks;
-  if (r >= row_end) return;
+  const int64_t v = w / chunks;
+  if (v >= rows) return;
+  const int64_t r = tiles ? static_cast<int64_t>(tiles[v / b] - k - 1) * b + v % b : row_begin + v;
   const int c0 = static_cast<int>(w % chunks) * 128 + 4 * lane;
   const int tile = k + 1 + static_cast<int>(r / b), rr = static_cast<int>(r % b);
   const int mu = oz_mu(rowexp, min(tile * ts.lb + rr, ts.n - 1));
@@ -385,7 +389,17 @@ void oz_slice(const TileStore& ts, int k, const double* p64, int64_t row_begin, 
               OzSlices& oz, const int* fail, cudaStream_t s) {
   if (row_end <= row_begin) return;
   const int64_t warps = (row_end - row_begin) * (ts.b / 128);
-  k_oz_slice<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(ts, k, p64, row_begin, row_end, rowexp, oz.s8.get(),
+  k_oz_slice<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(ts, k, p64, row_begin, row_end - row_begin,
+                                                                     nullptr, rowexp, oz.s8.get(), fail);
+  SPH_LAUNCH_CHECK();
+}
+
+void oz_slice_tiles(const TileStore& ts, int k, const double* p64, const int* tiles, int64_t cnt, const int* rowexp,
+                    OzSlices& oz, const int* fail, cudaStream_t s) {
+  if (cnt <= 0) return;
+  const int64_t rows = cnt * ts.b;
+  const int64_t warps = rows * (ts.b / 128);
+  k_oz_slice<<<static_cast<unsigned>((warps + 7) / 8), 256, 0, s>>>(ts, k, p64, 0, rows, tiles, rowexp, oz.s8.get(),
                                                                      fail);
   SPH_LAUNCH_CHECK();
 }

@@ -49,6 +49,11 @@ struct OzSlices {
 void oz_slice(const TileStore& ts, int k, const double* p64, int64_t row_begin, int64_t row_end, const int* rowexp,
               OzSlices& oz, const int* fail, cudaStream_t s);
 
+// Digits of the panel rows of tiles[0..cnt) (tile indices > k+1, device
+// array) of step k.
+void oz_slice_tiles(const TileStore& ts, int k, const double* p64, const int* tiles, int64_t cnt, const int* rowexp,
+                    OzSlices& oz, const int* fail, cudaStream_t s);
+
 // C_ij -= P_i P_j^T (+ P2_i P2_j^T for a merged pair: k2 >= 0, oz2 = step
 // k2's digits) on the FP64 tiles of list[0..cnt). counter: dynamic item
 // claims (zeroed here); max_ctas: grid cap (0 = all SMs).
