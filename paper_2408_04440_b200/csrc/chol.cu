@@ -1401,7 +1401,7 @@ struct Chol {
     // (tools/reserve_sweep*.sh); with the INT8 DP class and the SP pairs
     // 8 stays best once short factorizations run their SP pairs dynamically
     // (yielding to the panel): C2 47.8 ms (16: 48.5); static pairs would want
-    // 16 on C2 (48.8 vs 50.3) but 8 on C3 (905 vs 938) (tools/exp27/28/35.sh).
+    // 16 on C2 (48.8 vs 50.3) but 8 on C3 (905 vs 938) (tools/gpu_tasks.sh sweep).
     static const int r_early_env = [] {
       const char* e = std::getenv("SPHEMU_RESERVE_EARLY");
       return e ? std::max(8, std::min(kChainCtas, std::atoi(e))) : 0;

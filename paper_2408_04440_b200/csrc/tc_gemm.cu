@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
       // epilogue's register-staged C loads run a box ahead anyway, and the
       // prefetched C lines evicted the panel operands every item re-reads
       // (C2 47.4 -> 46.2 ms, n = 64 800 dpsp 233.5 -> 220.0 ms, C3 891.5 ->
-      // 829.0 ms without it; tools/exp40/41.sh).
+      // 829.0 ms without it; tools/gpu_tasks.sh sweep with SPHEMU_TC_OPT).
       // The next item's list entry and C row are loaded while this item's
       // first stages are in flight (a dependent global load here would stall
       // the TMA issue at every item boundary).

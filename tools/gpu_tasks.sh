@@ -6,7 +6,14 @@
 #   launches         ncu launch list (gpu__time_duration) of a short bench run
 #   ncu <regex> [n]  one --set full capture of the n-th launch of kernels matching regex
 #   epi <args>       tools/epi_probe.py (SPHEMU_TC_DBG / SPHEMU_TC_CG from the env)
-#   sweep <k=v,..>   tools/ab.py under each listed environment assignment
+#   sweep <N> <VARIANT> <HP> <k=v,..>  tools/ab.py at order N under each environment assignment
+#                    (e.g. sweep 32400 dpsp fp16 SPHEMU_RESERVE_EARLY=8,SPHEMU_RESERVE_EARLY=16)
+#   timeline <N> <VARIANT>   chain/bulk stream busy and idle times (tools/chol_timeline.py, timeline_gaps.py)
+#   oz               the INT8 DP-update kernel alone (tools/micro/oz_bench, SPHEMU_OZ_DBG 0/1/2) + tools/oz_check.py
+#   dist <G> <P> [k=v,..]   tools/dist_perf.py on C3 over G GPUs as P x G/P under each assignment
+#   disttl <G> <P>   per-rank phase totals of the distributed factorization (tools/dist_timeline.py)
+# The round-2 experiments behind the numbers in DESIGN.md were these tasks with the
+# settings quoted there.
 set -u
 mkdir -p gpurun_out
 task=${1:-check}; shift || true
@@ -30,6 +37,23 @@ case "$task" in
     timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:$1" -s ${2:-5} -c 1 -o gpurun_out/ncu_${NAME:-kernel} -f python ${SCRIPT:-bench.py} ${SCRIPT_ARGS:---steps 1 --warmup 3} > gpurun_out/ncu_${NAME:-kernel}.log 2>&1; echo "EXIT $?" ;;
   epi)
     python tools/epi_probe.py "$@" ;;
+  sweep)
+    n=$1; v=$2; hp=$3; IFS=',' read -ra sets <<< "${4:-NONE=1}"
+    for kv in "${sets[@]}"; do echo "$kv"; env "$kv" timeout 300 python tools/ab.py "$n" "$v" "$hp" ${REPS:-3} ${TILE:-512}; done ;;
+  timeline)
+    timeout 300 python tools/chol_timeline.py "$1" ${TILE:-512} "$2" 2>/dev/null | head -9
+    timeout 300 python tools/timeline_gaps.py "$1" "$2" ;;
+  oz)
+    tools/micro/build_oz_bench.sh
+    for d in 0 1 2; do echo "SPHEMU_OZ_DBG=$d"; SPHEMU_OZ_DBG=$d timeout 60 ./tools/micro/oz_bench; done
+    timeout 900 python tools/oz_check.py 4096 512 ;;
+  dist|disttl)
+    g=$1; p=$2; IFS=',' read -ra sets <<< "${3:-NONE=1}"
+    script=tools/dist_perf.py; [ "$task" = disttl ] && script=tools/dist_timeline.py
+    for kv in "${sets[@]}"; do echo "$kv"
+      env "$kv" timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$g" --master-addr 127.0.0.1 \
+        --master-port 29533 $script ${N:-129600} 512 ${VARIANT:-dpsphp} ${HP:-bf16} "$p" 2>&1 | grep -v "^W\|Warn\|return func\|\*\*\*"
+    done ;;
   *)
     echo "unknown task $task"; exit 2 ;;
 esac
