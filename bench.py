@@ -447,9 +447,10 @@ def roofline(h, wl, args, phases, steps, ms):
     peaks = load_peaks()
     own = peaks.get("own", {})
     p_dp = own.get("fp64_dgemm_tflops", 35.5)
+    f16_peak = peaks.get("bf16_tflops", 1664.2)  # kind::f16 and bf16 run at one rate
     if args.sp_compute == "fp16x3":
-        p_sp = own.get("fp16_tflops", 1546.6) / 3
-        sp_src = "cuBLAS FP16 GEMM measured on this pool / 3 (3 kind::f16 MMAs per product; profiles/peaks_r01.json)"
+        p_sp = f16_peak / 3
+        sp_src = "MEASURED_PEAKS.json bf16_tflops (burst; kind::f16 runs at the same rate) / 3 (3 MMAs per product)"
         sp_kernel = "k_tc_gemm<128, F16x3, UPDATE, 2> (SP-class trailing update, CTA pairs, row-scaled fp16 hi+lo)"
     else:
         p_sp = own.get("tf32x3_effective_tflops", 244.7)
@@ -459,7 +460,7 @@ def roofline(h, wl, args, phases, steps, ms):
         p_hp, hp_src = peaks.get("bf16_tflops", 1692.6), "MEASURED_PEAKS.json bf16_tflops (burst)"
         hp_kernel = "k_tc_gemm<128, BF16, UPDATE, 2> (HP-class trailing update, CTA pairs, BF16 storage)"
     else:
-        p_hp, hp_src = own.get("fp16_tflops", 1546.6), "cuBLAS FP16 GEMM measured on this pool (profiles/peaks_r01.json)"
+        p_hp, hp_src = f16_peak, "MEASURED_PEAKS.json bf16_tflops (burst; kind::f16 runs at the same rate)"
         hp_kernel = "k_tc_gemm<128, F16, UPDATE, 2> (HP-class trailing update, CTA pairs, FP16 storage)"
     cuf = h.class_update_flops()
     bn = 256 if wl["tile"] % 256 == 0 else 128
