@@ -234,19 +234,27 @@ __global__ void k_rowexp(TileStore ts, int* rowexp) {
 // 2D block-cyclic exchange: a panel tile received at its storage precision
 // (xbuf slot i-k-1) -> FP64 mirror P64 and the tensor-core mirrors, exactly as
 // the owner's panel epilogue writes them. blockIdx.y indexes the import list.
+// need[i] (per panel row block, this rank's consumers): bit 0 the FP64 mirror
+// (FP64-class updates / the INT8 digit cut), bit 1 the 16-bit HP mirror, bit 2
+// the SP class's split; mirrors nobody here reads are not written.
 __global__ void k_panel_import(TileStore ts, int k, const int2* __restrict__ list, const int64_t* __restrict__ xoff,
                                const uint8_t* __restrict__ xbuf, double* p64, float* p_hi, float* p_lo, uint16_t* p16, uint16_t* h_hi, uint16_t* h_lo,
-                               const int* rowexp, int hp_format, const int* fail) {
+                               const int* rowexp, int hp_format, const uint8_t* __restrict__ need, const int* fail) {
   if (*(volatile const int*)fail >= 0) return;
   const int b = ts.b;
   const int64_t bb = (int64_t)b * b;
   const int i = list[blockIdx.y].x;
+  const int nd = need ? need[i] : 7;
+  if (!(nd & 1)) p64 = nullptr;
+  if (!(nd & 2)) p16 = nullptr;
+  if (!(nd & 4)) p_hi = p_lo = nullptr, h_hi = h_lo = nullptr;
+  if (!p64 && !p16 && !p_hi && !h_hi) return;
   const int p = ts.tprec(i, k);
   const int64_t base = (int64_t)(i - k - 1) * bb;
   const void* src = xbuf + xoff[blockIdx.y];
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += (int64_t)gridDim.x * blockDim.x) {
     const double x = load_elem(src, p, e);
-    p64[base + e] = x;
+    if (p64) p64[base + e] = x;
     if (p_hi) {
       float hi, lo;
       tf32_split(__double2float_rn(x), hi, lo);
@@ -584,6 +592,7 @@ struct Chol {
   DevBuf<int> fail;
   DevBuf<unsigned> sat;
   DevBuf<int2> lists;
+  DevBuf<uint8_t> d_import_need;  // distributed: per panel row block, the mirrors this rank reads (k_panel_import)
   DevBuf<int> lrows;  // per update-list entry: the C tile's arena row (see constructor)
   // Dynamic work claiming for the persistent tcgen05 kernels: one counter per
   // (stream, class) (kernels on one stream run in order; the memset precedes
@@ -1149,6 +1158,17 @@ struct Chol {
       };
       upload(ilists, il);
       upload(ioffs, io);
+      // which operand mirrors this rank's updates read, per panel row block
+      std::vector<uint8_t> need(nt, 0);
+      for (int i = 1; i < nt; ++i)
+        for (int j = 1; j <= i; ++j) {
+          if (!mine(i, j)) continue;
+          const int c = pmap[tix(i, j)];
+          const uint8_t bit = (fp64_class(c) || cfg.compute != SPHEMU_COMPUTE_TENSOR) ? 1 : (c == SPHEMU_PREC_HP ? 2 : 4);
+          need[i] |= bit;
+          need[j] |= bit;
+        }
+      upload(d_import_need, need);
       upload(xsend, xs);
       upload(xsoffs, xo);
       if (xmax > 0) xbuf.alloc(static_cast<size_t>(xmax));
@@ -1666,7 +1686,7 @@ struct Chol {
           store(), k, ilists.get() + ilist_off[k], ioffs.get() + ilist_off[k], xbuf.get(), p64_[set].get(), tensor ? pf.tf32_hi() : nullptr,
           tensor ? pf.tf32_lo() : nullptr, tensor ? pf.half16() : nullptr,
           (tensor && pf.f16x3) ? pf.h_hi.get() : nullptr, (tensor && pf.f16x3) ? pf.h_lo.get() : nullptr,
-          rowexp.get(), cfg.hp_format, fail.get());
+          rowexp.get(), cfg.hp_format, d_import_need.get(), fail.get());
       SPH_LAUNCH_CHECK();
     }
     // tile k+1's digits (the chain's diagonal SYRK of the next step), once
