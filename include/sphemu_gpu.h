@@ -173,12 +173,14 @@ int sphemu_gpu_chol_residual_probe_spd_decay(sphemu_chol_t h, uint64_t seed, dou
 int sphemu_gpu_chol_flops(sphemu_chol_t h, double* f_dp, double* f_sp, double* f_hp);
 /* Phase profiling (CUDA events around every phase; off by default). Phases:
  * 0 POTRF+TRTRI, 1 panel TRSM, 2/3/4 trailing update of the DP/SP/HP
- * classes, 5 tile load. ms/counts have 6 entries. on = 1 records every
- * phase; on = 0x100 | mask records only the phases whose bit is set. */
+ * classes, 5 tile load, 6 panel exchange + import (process grids). ms/counts
+ * have 7 entries. on = 1 records every phase; on = 0x100 | mask records only
+ * the phases whose bit is set. */
 int sphemu_gpu_chol_set_profiling(sphemu_chol_t h, int on);
 int sphemu_gpu_chol_phase_times(sphemu_chol_t h, double* ms, int64_t* counts, int reset);
 /* Timeline of the last profiled factorization: one span per phase launch
- * (phase as above; stream 0 = main/bulk, 1 = high-priority chain), times in
+ * (phase as above; stream 0 = main/bulk, 1 = high-priority chain, 2 = the
+ * chunked panel exchange of process grids), times in
  * ms from the factorization's start. Writes min(count, cap) entries. */
 int sphemu_gpu_chol_timeline(sphemu_chol_t h, int* phase, int* stream, double* t0, double* t1, int cap,
                              int* count);

@@ -341,7 +341,7 @@ class Cholesky:
     def stream(self):
         return lib().sphemu_gpu_chol_stream(self.h)
 
-    PHASES = ("potrf", "panel", "update_dp", "update_sp", "update_hp", "load")
+    PHASES = ("potrf", "panel", "update_dp", "update_sp", "update_hp", "load", "exchange")
 
     def set_profiling(self, on=True, phases=None):
         """Record phase times; phases (names of PHASES) limits which."""
@@ -351,8 +351,8 @@ class Cholesky:
         _check(lib().sphemu_gpu_chol_set_profiling(self.h, v))
 
     def phase_times(self, reset=False):
-        ms = np.zeros(6)
-        cnt = np.zeros(6, dtype=np.int64)
+        ms = np.zeros(len(self.PHASES))
+        cnt = np.zeros(len(self.PHASES), dtype=np.int64)
         _check(lib().sphemu_gpu_chol_phase_times(self.h, _ptr(ms), _ptr(cnt), 1 if reset else 0))
         return {p: {"ms": float(ms[i]), "launches": int(cnt[i])} for i, p in enumerate(self.PHASES)}
 

@@ -251,24 +251,78 @@ __global__ void k_panel_import(TileStore ts, int k, const int2* __restrict__ lis
   if (!p64 && !p16 && !p_hi && !h_hi) return;
   const int p = ts.tprec(i, k);
   const int64_t base = (int64_t)(i - k - 1) * bb;
-  const void* src = xbuf + xoff[blockIdx.y];
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += (int64_t)gridDim.x * blockDim.x) {
-    const double x = load_elem(src, p, e);
-    if (p64) p64[base + e] = x;
+  const uint8_t* src = xbuf + xoff[blockIdx.y];
+  // 8 consecutive elements (one row segment) per thread: 16-byte loads of the
+  // packed tile, 16-byte stores of every mirror
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < bb / 8; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = g * 8;
+    double x[8];
+    if (p == kDP) {
+      const double2* q = reinterpret_cast<const double2*>(src) + g * 4;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2 v = q[u];
+        x[2 * u] = v.x;
+        x[2 * u + 1] = v.y;
+      }
+    } else if (p == kSP) {
+      const float4* q = reinterpret_cast<const float4*>(src) + g * 2;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float4 v = q[u];
+        x[4 * u] = v.x;
+        x[4 * u + 1] = v.y;
+        x[4 * u + 2] = v.z;
+        x[4 * u + 3] = v.w;
+      }
+    } else {
+      const uint4 v = reinterpret_cast<const uint4*>(src)[g];
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (p == kHP) {
+          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[u]));
+          x[2 * u] = f.x;
+          x[2 * u + 1] = f.y;
+        } else {
+          x[2 * u] = __uint_as_float(w[u] << 16);
+          x[2 * u + 1] = __uint_as_float(w[u] & 0xffff0000u);
+        }
+      }
+    }
+    if (p64) {
+      double2* q = reinterpret_cast<double2*>(p64 + base + e);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = make_double2(x[2 * u], x[2 * u + 1]);
+    }
     if (p_hi) {
-      float hi, lo;
-      tf32_split(__double2float_rn(x), hi, lo);
-      p_hi[base + e] = hi;
-      p_lo[base + e] = lo;
+      float hi[8], lo[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tf32_split(__double2float_rn(x[u]), hi[u], lo[u]);
+      float4* qh = reinterpret_cast<float4*>(p_hi + base + e);
+      float4* ql = reinterpret_cast<float4*>(p_lo + base + e);
+      qh[0] = make_float4(hi[0], hi[1], hi[2], hi[3]);
+      qh[1] = make_float4(hi[4], hi[5], hi[6], hi[7]);
+      ql[0] = make_float4(lo[0], lo[1], lo[2], lo[3]);
+      ql[1] = make_float4(lo[4], lo[5], lo[6], lo[7]);
     }
     if (p16) {
+      uint16_t h[8];
       unsigned dummy = 0;
-      p16[base + e] = hp_format == SPHEMU_HP_BF16 ? __bfloat16_as_ushort(to_bf16_sat(x, dummy))
-                                                  : __half_as_ushort(to_half_sat(x, dummy));
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        h[u] = hp_format == SPHEMU_HP_BF16 ? __bfloat16_as_ushort(to_bf16_sat(x[u], dummy))
+                                           : __half_as_ushort(to_half_sat(x[u], dummy));
+      *reinterpret_cast<uint4*>(p16 + base + e) = *reinterpret_cast<const uint4*>(h);
     }
     if (h_hi) {
       const int r = (int)(e / b);
-      f16_split(x, rowexp[min(i * ts.lb + r, ts.n - 1)], h_hi[base + e], h_lo[base + e]);
+      const int er = rowexp[min(i * ts.lb + r, ts.n - 1)];
+      uint16_t hh[8], hl[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) f16_split(x[u], er, hh[u], hl[u]);
+      *reinterpret_cast<uint4*>(h_hi + base + e) = *reinterpret_cast<const uint4*>(hh);
+      *reinterpret_cast<uint4*>(h_lo + base + e) = *reinterpret_cast<const uint4*>(hl);
     }
   }
 }
@@ -523,11 +577,37 @@ struct Chol {
   // / received tiles with their byte positions, xsends / xrecvs the
   // point-to-point transfers of each step (BlockCyclic).
   DevBuf<uint8_t> xbuf;
+  // Copy-engine panel exchange ("ipc", the default on a process grid): every
+  // rank maps its peers' exchange buffers and sync words (CUDA IPC); an owner
+  // packs its panel tiles into its own buffer (double-buffered by step
+  // parity) and publishes the step with a stream memory write, readers wait
+  // for it with cuStreamWaitValue32 and pull each owner's block with one
+  // device-to-device copy over NVLink — copy engines, no SMs taken from the
+  // bulk update (the NCCL broadcast kernels had to fit in the chain's reserve
+  // next to a persistent bulk and crawled) — then acknowledge into the
+  // owner's sync words before it reuses that parity.
+  bool xipc = false;
+  int64_t xhalf = 0;                        // bytes per parity half of xbuf
+  DevBuf<uint32_t> xsync;                   // [0] = published step, [1 + r] = acks from rank r
+  DevBuf<int> xbar;                         // device-side barrier word at the start of a factorization
+  std::vector<uint8_t*> peer_xbuf;
+  std::vector<uint32_t*> peer_sync;
+  uint32_t xepoch = 0;                      // advanced by nt per factorization (stream-ordered words never go back)
   DevBuf<int2> ilists, xsend;
   DevBuf<int64_t> ioffs, xsoffs;
   std::vector<int64_t> ilist_off, ilist_cnt, xsend_off, xsend_cnt;
   using Xfer = BlockCyclic::Xfer;
   std::vector<std::vector<Xfer>> xsends, xrecvs, xroots;
+  // Chunked panel exchange (broadcast mode): the panel TRSM runs in xchunks
+  // slices of the column on the chain stream while the previous slice is
+  // packed, broadcast (second communicator) and imported on xstream.
+  ncclComm_t comm2 = nullptr;
+  cudaStream_t xstream = nullptr;
+  std::vector<cudaEvent_t> ev_tr;
+  cudaEvent_t ev_xdone = nullptr;
+  int xchunks = 1;
+  std::vector<std::vector<int64_t>> xpos_h;  // layout.xpos
+  std::vector<int> pl_i, xs_i, il_i;         // host copies of the plist / xsend / ilist tile rows
   // Panel exchange: one grouped ncclBroadcast per owner block to every rank
   // (default), or with SPHEMU_XCHG=p2p point to point to the readers only
   // (BlockCyclic::needers: (P+Q)/(PQ) of the bytes per rank, but the owner
@@ -638,9 +718,9 @@ struct Chol {
   int64_t launches_at_start = 0, launches = 0;
   // Phase profiling (tracing subsystem): CUDA events around every phase
   // launch, folded into per-phase totals at wait().
-  enum Phase { kPotrf = 0, kPanel = 1, kUpdDp = 2, kUpdSp = 3, kUpdHp = 4, kLoad = 5, kNumPhases = 6 };
+  enum Phase { kPotrf = 0, kPanel = 1, kUpdDp = 2, kUpdSp = 3, kUpdHp = 4, kLoad = 5, kXchg = 6, kNumPhases = 7 };
   bool profiling = false;
-  unsigned prof_mask = 0x3f;  // phases recorded while profiling
+  unsigned prof_mask = 0x7f;  // phases recorded while profiling
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, int>> ev_marks;  // (phase, start event index)
   struct Span {
@@ -659,7 +739,7 @@ struct Chol {
       SPH_CUDA(cudaEventCreate(&e));
       ev_pool.push_back(e);
     }
-    ev_marks.push_back({phase | (s == pstream ? 0x100 : 0), static_cast<int>(idx)});
+    ev_marks.push_back({phase | (s == pstream ? 0x100 : (s == xstream && xstream ? 0x200 : 0)), static_cast<int>(idx)});
     SPH_CUDA(cudaEventRecord(ev_pool[idx], s));
     return static_cast<int>(idx);
   }
@@ -675,7 +755,7 @@ struct Chol {
       SPH_CUDA(cudaEventElapsedTime(&ms, ev_pool[m.second], ev_pool[m.second + 1]));
       if (factored && cudaEventElapsedTime(&a, ev0, ev_pool[m.second]) == cudaSuccess &&
           cudaEventElapsedTime(&z, ev0, ev_pool[m.second + 1]) == cudaSuccess)
-        timeline.push_back({phase, (m.first >> 8) & 1, a, z});
+        timeline.push_back({phase, (m.first >> 8) & 3, a, z});
       phase_ms[phase] += ms;
       phase_n[phase] += 1;
     }
@@ -1113,6 +1193,8 @@ struct Chol {
         if (!fp64_class(pmap[tix(i, k)]) && mine(i, k)) pl.push_back(make_int2(i, k));
       plist_lo[k] = static_cast<int64_t>(pl.size()) - plist_off[k] - plist_dp[k];
     }
+    pl_i.resize(pl.size());
+    for (size_t e = 0; e < pl.size(); ++e) pl_i[e] = pl[e].x;
     if (!pl.empty()) {
       plists.alloc(pl.size());
       SPH_CUDA(cudaMemcpy(plists.get(), pl.data(), pl.size() * sizeof(int2), cudaMemcpyHostToDevice));
@@ -1158,6 +1240,11 @@ struct Chol {
       };
       upload(ilists, il);
       upload(ioffs, io);
+      il_i.resize(il.size());
+      for (size_t e = 0; e < il.size(); ++e) il_i[e] = il[e].x;
+      xs_i.resize(xs.size());
+      for (size_t e = 0; e < xs.size(); ++e) xs_i[e] = xs[e].x;
+      xpos_h = layout.xpos;
       // which operand mirrors this rank's updates read, per panel row block
       std::vector<uint8_t> need(nt, 0);
       for (int i = 1; i < nt; ++i)
@@ -1171,7 +1258,14 @@ struct Chol {
       upload(d_import_need, need);
       upload(xsend, xs);
       upload(xsoffs, xo);
-      if (xmax > 0) xbuf.alloc(static_cast<size_t>(xmax));
+      static const int xmode_ipc = [] {
+        const char* e = std::getenv("SPHEMU_XCHG");
+        return !(e && (std::string(e) == "p2p" || std::string(e) == "nccl"));
+      }();
+      xipc = bc && xmode_ipc && xmax > 0;
+      xhalf = (xmax + 255) / 256 * 256;
+      if (xmax > 0) xbuf.alloc(static_cast<size_t>(xipc ? 2 * xhalf : xmax));
+      if (xipc) ipc_setup();
 
     }
     rowexp.alloc(n);
@@ -1212,6 +1306,20 @@ struct Chol {
     SPH_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     SPH_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, prio_lo));
     SPH_CUDA(cudaStreamCreateWithPriority(&pstream, cudaStreamNonBlocking, prio_hi));
+    if (dist() && xchg_bcast()) {
+      static const int env_chunks = [] {
+        const char* e = std::getenv("SPHEMU_XCHG_CHUNKS");
+        return e ? std::max(1, std::atoi(e)) : 1;  // measured slower when chunked (C3 2x2: 1 / 2 / 4 / 8 -> 358 / 374 / 388 / 425 ms)
+      }();
+      xchunks = env_chunks;
+      if (xchunks > 1) {
+        SPH_NCCL(ncclCommSplit(comm, 0, rank, &comm2, nullptr));
+        SPH_CUDA(cudaStreamCreateWithPriority(&xstream, cudaStreamNonBlocking, prio_hi));
+        ev_tr.resize(xchunks);
+        for (auto& e : ev_tr) SPH_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        SPH_CUDA(cudaEventCreateWithFlags(&ev_xdone, cudaEventDisableTiming));
+      }
+    }
     ev_panel.resize(nt);
     ev_bulk.resize(nt);
     ev_colrest.resize(nt);
@@ -1248,6 +1356,11 @@ struct Chol {
     for (auto e : ev_colrest) cudaEventDestroy(e);
     for (auto e : ev_bulkdp) cudaEventDestroy(e);
     if (ev_start_p) cudaEventDestroy(ev_start_p);
+    if (xstream) cudaStreamSynchronize(xstream);
+    for (auto e : ev_tr) cudaEventDestroy(e);
+    if (ev_xdone) cudaEventDestroy(ev_xdone);
+    if (xstream) cudaStreamDestroy(xstream);
+    if (comm2) ncclCommDestroy(comm2);
     if (pstream) cudaStreamDestroy(pstream);
     if (comm) ncclCommDestroy(comm);
     if (ev0) cudaEventDestroy(ev0);
@@ -1408,10 +1521,18 @@ struct Chol {
   // identical with and without lookahead).
   void factor() {
     factored = false;
+    if (xipc) xepoch += static_cast<uint32_t>(nt) + 2;
     std::fill(oz_rest.begin(), oz_rest.end(), 0);
     launches_at_start = launch_count();
     t_start = std::chrono::steady_clock::now();
     SPH_CUDA(cudaEventRecord(ev0, stream));
+    if (xipc) {
+      // every rank's previous factorization (both streams) is done before any
+      // owner refills an exchange half of this one: a device-side barrier
+      SPH_CUDA(cudaEventRecord(ev_start_p, pstream));
+      SPH_CUDA(cudaStreamWaitEvent(stream, ev_start_p, 0));
+      SPH_NCCL(ncclAllReduce(xbar.get(), xbar.get(), 1, ncclInt32, ncclSum, comm, stream));
+    }
     // SMs left to the chain while the bulk runs. Early steps, where the bulk
     // is the critical stream (its work shrinks quadratically, the chain's only
     // linearly), leave the chain 8 SMs; the last 32 steps leave it 32
@@ -1582,7 +1703,11 @@ struct Chol {
         const int reserve = reserve_for(k);
         potrf_cap = std::min(kChainCtas, reserve);
         const int bulk_ctas = std::max(1, num_sms() - reserve);
-        const bool y = yield_on() && !D;
+        static const bool dist_yield = [] {
+          const char* e = std::getenv("SPHEMU_DIST_YIELD");  // A/B: yielding bulk on process grids
+          return e && e[0] == '1';
+        }();
+        const bool y = yield_on() && (!D || dist_yield);
         if (diag_ready) SPH_CUDA(cudaStreamWaitEvent(pstream, diag_ready, 0));
         op_update(k, 0, pstream, 0);
         potrf(k + 1, pstream);
@@ -1656,11 +1781,165 @@ struct Chol {
 
   // Panel TRSM on the owned panel tiles, then every panel tile broadcast at
   // its storage precision and imported into the operand mirrors elsewhere.
+  void ipc_setup() {
+    const int W = P * Q;
+    xbar.alloc(1);
+    SPH_CUDA(cudaMemset(xbar.get(), 0, sizeof(int)));
+    xsync.alloc(1 + W);
+    SPH_CUDA(cudaMemset(xsync.get(), 0, (1 + W) * sizeof(uint32_t)));
+    cudaIpcMemHandle_t mine[2];
+    SPH_CUDA(cudaIpcGetMemHandle(&mine[0], xbuf.get()));
+    SPH_CUDA(cudaIpcGetMemHandle(&mine[1], xsync.get()));
+    DevBuf<uint8_t> all(sizeof(mine) * W);
+    DevBuf<uint8_t> one(sizeof(mine));
+    SPH_CUDA(cudaMemcpy(one.get(), mine, sizeof(mine), cudaMemcpyHostToDevice));
+    SPH_NCCL(ncclAllGather(one.get(), all.get(), sizeof(mine), ncclUint8, comm, stream));
+    SPH_CUDA(cudaStreamSynchronize(stream));
+    std::vector<cudaIpcMemHandle_t> hs(2 * W);
+    SPH_CUDA(cudaMemcpy(hs.data(), all.get(), sizeof(mine) * W, cudaMemcpyDeviceToHost));
+    peer_xbuf.assign(W, nullptr);
+    peer_sync.assign(W, nullptr);
+    for (int r = 0; r < W; ++r) {
+      if (r == rank) {
+        peer_xbuf[r] = xbuf.get();
+        peer_sync[r] = xsync.get();
+        continue;
+      }
+      void* pb = nullptr;
+      void* ps = nullptr;
+      SPH_CUDA(cudaIpcOpenMemHandle(&pb, hs[2 * r], cudaIpcMemLazyEnablePeerAccess));
+      SPH_CUDA(cudaIpcOpenMemHandle(&ps, hs[2 * r + 1], cudaIpcMemLazyEnablePeerAccess));
+      peer_xbuf[r] = static_cast<uint8_t*>(pb);
+      peer_sync[r] = static_cast<uint32_t*>(ps);
+    }
+  }
+  static void stream_write(cudaStream_t s, uint32_t* addr, uint32_t v) {
+    const CUresult r = cuStreamWriteValue32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                                            CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) throw Error(SPHEMU_ERR_CUDA, "cuStreamWriteValue32 failed: " + std::to_string(r));
+  }
+  static void stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t v) {
+    const CUresult r = cuStreamWaitValue32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                                           CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) throw Error(SPHEMU_ERR_CUDA, "cuStreamWaitValue32 failed: " + std::to_string(r));
+  }
+
+  // The copy-engine exchange of step k's panel (see xipc): owners pack and
+  // publish, readers pull every other owner's block, import, acknowledge.
+  void xchg_ipc(int k, cudaStream_t s) {
+    const int W = P * Q;
+    const uint32_t ep = xepoch + static_cast<uint32_t>(k) + 1;
+    const int64_t par = (k & 1) * xhalf;
+    uint8_t* own = xbuf.get() + par;
+    const unsigned gx = static_cast<unsigned>(std::max(1, b * b / (256 * 16)));
+    if (xsend_cnt[k]) {
+      // the half this step packs into was last read by the readers at step k-2
+      if (k >= 2)
+        for (int q = 0; q < W; ++q)
+          if (q != rank) stream_wait_geq(s, xsync.get() + 1 + q, ep - 2);
+      k_panel_pack<<<dim3(gx, static_cast<unsigned>(xsend_cnt[k])), 256, 0, s>>>(
+          store(), k, xsend.get() + xsend_off[k], xsoffs.get() + xsend_off[k], own, fail.get());
+      SPH_LAUNCH_CHECK();
+      stream_write(s, xsync.get(), ep);
+    }
+    for (const Xfer& x : xroots[k]) {
+      if (x.peer == rank) continue;
+      stream_wait_geq(s, peer_sync[x.peer], ep);
+      SPH_CUDA(cudaMemcpyAsync(own + x.pos, peer_xbuf[x.peer] + par + x.pos, static_cast<size_t>(x.bytes),
+                               cudaMemcpyDeviceToDevice, s));
+    }
+    note_launch();
+  }
+
+  // Chunked form of op_panel_dist (broadcast mode, tensor compute): the
+  // column below the diagonal is cut into xchunks slices by tile row; slice c's
+  // TRSM (this rank's tiles of it) runs on the chain stream s while slice c-1
+  // is packed, broadcast per owner on comm2 and imported on xstream, so the
+  // exchange hides behind the TRSM. Slices are a function of the tile index
+  // only, so every rank issues the same collectives in the same order.
+  void op_panel_dist_chunked(int k, cudaStream_t s, int max_ctas) {
+    const int set = set_of(k);
+    const int below = nt - k - 1;
+    const int C = std::min(xchunks, below);
+    auto chunk_of = [&](int i) { return static_cast<int>((static_cast<int64_t>(i - k - 1) * C) / below); };
+    // sub-range [lo, hi) of a tile-row-sorted list segment holding chunk c
+    auto sub = [&](const std::vector<int>& rows, int64_t off, int64_t cnt, int c, int64_t& lo, int64_t& hi) {
+      lo = off;
+      while (lo < off + cnt && chunk_of(rows[lo]) < c) ++lo;
+      hi = lo;
+      while (hi < off + cnt && chunk_of(rows[hi]) == c) ++hi;
+    };
+    PanelFormats& pf = panel_[set];
+    const unsigned gx = static_cast<unsigned>(std::max(1, b * b / (256 * 16)));
+    const int2* pbase = plists.get() + plist_off[k];
+    const int64_t lo_off = plist_off[k] + plist_dp[k];
+    const int pp = prof_begin(kPanel, s);
+    for (int c = 0; c < C; ++c) {
+      int64_t a, z;
+      sub(pl_i, lo_off, plist_lo[k], c, a, z);
+      if (c == 0 || z > a)
+        tc_panel_trsm(store(), k, pbase, c == 0 ? plist_dp[k] : 0, plists.get() + a, z - a, linv_[set].get(),
+                      p64_[set].get(), pf, fail.get(), sat.get(), s, max_ctas, ctr(s, 3));
+      SPH_CUDA(cudaEventRecord(ev_tr[c], s));
+    }
+    prof_end(pp, s);
+    const int px = prof_begin(kXchg, xstream);
+    for (int c = 0; c < C; ++c) {
+      SPH_CUDA(cudaStreamWaitEvent(xstream, ev_tr[c], 0));
+      int64_t a, z;
+      sub(xs_i, xsend_off[k], xsend_cnt[k], c, a, z);
+      if (z > a) {
+        k_panel_pack<<<dim3(gx, static_cast<unsigned>(z - a)), 256, 0, xstream>>>(
+            store(), k, xsend.get() + a, xsoffs.get() + a, xbuf.get(), fail.get());
+        SPH_LAUNCH_CHECK();
+      }
+      bool any = false;
+      for (const Xfer& x : xroots[k]) {
+        int64_t lo = -1, hi = -1;
+        for (int i = k + 1; i < nt; ++i)
+          if (owner(i, k) == x.peer && chunk_of(i) == c) {
+            const int64_t p0 = xpos_h[k][i - k - 1];
+            const int64_t p1 = p0 + static_cast<int64_t>(b) * b * prec_bytes(sprec[tix(i, k)]);
+            lo = lo < 0 ? p0 : std::min(lo, p0);
+            hi = std::max(hi, p1);
+          }
+        if (lo < 0) continue;
+        if (!any) SPH_NCCL(ncclGroupStart());
+        any = true;
+        SPH_NCCL(ncclBroadcast(xbuf.get() + lo, xbuf.get() + lo, static_cast<size_t>(hi - lo), ncclUint8, x.peer,
+                               comm2, xstream));
+      }
+      if (any) SPH_NCCL(ncclGroupEnd());
+      note_launch();
+      sub(il_i, ilist_off[k], ilist_cnt[k], c, a, z);
+      if (z > a) {
+        const bool tensor = cfg.compute == SPHEMU_COMPUTE_TENSOR;
+        k_panel_import<<<dim3(gx, static_cast<unsigned>(z - a)), 256, 0, xstream>>>(
+            store(), k, ilists.get() + a, ioffs.get() + a, xbuf.get(), p64_[set].get(), tensor ? pf.tf32_hi() : nullptr,
+            tensor ? pf.tf32_lo() : nullptr, tensor ? pf.half16() : nullptr,
+            (tensor && pf.f16x3) ? pf.h_hi.get() : nullptr, (tensor && pf.f16x3) ? pf.h_lo.get() : nullptr,
+            rowexp.get(), cfg.hp_format, d_import_need.get(), fail.get());
+        SPH_LAUNCH_CHECK();
+      }
+    }
+    oz_slice_next(k, xstream);
+    prof_end(px, xstream);
+    SPH_CUDA(cudaEventRecord(ev_xdone, xstream));
+    SPH_CUDA(cudaStreamWaitEvent(s, ev_xdone, 0));
+  }
+
   void op_panel_dist(int k, cudaStream_t s, int max_ctas = 0) {
     const int set = set_of(k);
+    if (xchunks > 1 && xstream && cfg.compute == SPHEMU_COMPUTE_TENSOR) {
+      op_panel_dist_chunked(k, s, max_ctas);
+      return;
+    }
     op_panel(k, s, max_ctas);
-    const int px = prof_begin(kPanel, s);
+    const int px = prof_begin(kXchg, s);
     const unsigned gx = static_cast<unsigned>(std::max(1, b * b / (256 * 16)));
+    if (xipc) {
+      xchg_ipc(k, s);
+    } else {
     if (xsend_cnt[k]) {
       k_panel_pack<<<dim3(gx, static_cast<unsigned>(xsend_cnt[k])), 256, 0, s>>>(
           store(), k, xsend.get() + xsend_off[k], xsoffs.get() + xsend_off[k], xbuf.get(), fail.get());
@@ -1679,16 +1958,21 @@ struct Chol {
     }
     SPH_NCCL(ncclGroupEnd());
     note_launch();
+    }
+    const uint8_t* xsrc = xbuf.get() + (xipc ? (k & 1) * xhalf : 0);
     if (ilist_cnt[k]) {
       PanelFormats& pf = panel_[set];
       const bool tensor = cfg.compute == SPHEMU_COMPUTE_TENSOR;
       k_panel_import<<<dim3(gx, static_cast<unsigned>(ilist_cnt[k])), 256, 0, s>>>(
-          store(), k, ilists.get() + ilist_off[k], ioffs.get() + ilist_off[k], xbuf.get(), p64_[set].get(), tensor ? pf.tf32_hi() : nullptr,
+          store(), k, ilists.get() + ilist_off[k], ioffs.get() + ilist_off[k], xsrc, p64_[set].get(), tensor ? pf.tf32_hi() : nullptr,
           tensor ? pf.tf32_lo() : nullptr, tensor ? pf.half16() : nullptr,
           (tensor && pf.f16x3) ? pf.h_hi.get() : nullptr, (tensor && pf.f16x3) ? pf.h_lo.get() : nullptr,
           rowexp.get(), cfg.hp_format, d_import_need.get(), fail.get());
       SPH_LAUNCH_CHECK();
     }
+    if (xipc)  // the pulled blocks are consumed: every owner may refill this parity at step k+2
+      for (int q = 0; q < P * Q; ++q)
+        if (q != rank) stream_write(s, peer_sync[q] + 1 + rank, xepoch + static_cast<uint32_t>(k) + 1);
     // tile k+1's digits (the chain's diagonal SYRK of the next step), once
     // its panel rows are here
     oz_slice_next(k, s);
@@ -2348,7 +2632,7 @@ int sphemu_gpu_chol_residual_probe_spd(sphemu_chol_t h, uint64_t seed, int n_vec
 int sphemu_gpu_chol_set_profiling(sphemu_chol_t h, int on) {
   return guard([&] {
     h->c->profiling = on != 0;
-    h->c->prof_mask = (on & 0x100) ? static_cast<unsigned>(on & 0x3f) : 0x3fu;
+    h->c->prof_mask = (on & 0x100) ? static_cast<unsigned>(on & 0x7f) : 0x7fu;
   });
 }
 
