@@ -21,7 +21,7 @@ case "$task" in
   check)
     timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "PYTEST_EXIT $?" >> gpurun_out/pytest_gpu.log
     timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "SMOKE_EXIT $?" >> gpurun_out/smoke.log
-    tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log ;;
+    tail -n 3 gpurun_out/pytest_gpu.log; tail -n 3 gpurun_out/smoke.log ;;
   bench)
     n=${1:-1}
     if [ "$n" = 1 ]; then
