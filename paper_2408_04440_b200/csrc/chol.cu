@@ -639,6 +639,18 @@ struct Chol {
   OzSlices oz_[kSets];
   bool oz = false;
   std::vector<uint8_t> oz_rest;
+  std::vector<uint8_t> oz_fused;  // step k's digits were written by its panel epilogue
+  // One GPU, opt-in (SPHEMU_OZ_FUSE = fraction): the panel epilogue writes the
+  // digits of steps k < fraction * nt itself instead of the FP64 mirror; the
+  // integer digit work on the chain's few SMs costs more than the bulk's
+  // separate cut saves, so the default is 0.
+  static double oz_fuse_frac() {
+    static const double f = [] {
+      const char* e = std::getenv("SPHEMU_OZ_FUSE");
+      return e ? std::atof(e) : 0.0;  // measured: 0 / 0.25 / 0.5 / 1 -> C2 46.4 / 47.4 / 48.2 / 48.8 ms
+    }();
+    return f;
+  }
   // Tiles whose panel rows some DP-class update on this rank reads (every
   // diagonal tile on one GPU; the owned DP tiles' rows and columns on a
   // process grid), ascending: the digits are cut for these rows only.
@@ -1297,10 +1309,15 @@ struct Chol {
         if (oz_need[q]) oz_tiles.push_back(q);
       if (oz) {
         for (int p = 0; p < kSets; ++p) oz_[p].alloc(static_cast<int64_t>(nt - 1) * b, b);
+        // one GPU: the panel epilogue writes the digits itself (no FP64 mirror
+        // of the SP/HP panel rows, no separate digit cut); process grids cut
+        // them from the imported rows
+        // (decided per step in op_panel: early steps, where the chain has slack)
         d_oz_tiles.alloc(oz_tiles.size());
         SPH_CUDA(cudaMemcpy(d_oz_tiles.get(), oz_tiles.data(), oz_tiles.size() * sizeof(int), cudaMemcpyHostToDevice));
       }
       oz_rest.assign(nt, 0);
+      oz_fused.assign(nt, 0);
     }
     int prio_lo = 0, prio_hi = 0;
     SPH_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
@@ -1419,10 +1436,14 @@ struct Chol {
     const int set = set_of(k);
     const int pp = prof_begin(kPanel, s);
     if (cfg.compute == SPHEMU_COMPUTE_TENSOR) {
+      if (oz && !dist()) {
+        oz_fused[k] = k < oz_fuse_frac() * nt;
+        panel_[set].s8 = oz_fused[k] ? oz_[set].s8.get() : nullptr;
+      }
       const int2* base = plists.get() + plist_off[k];
       tc_panel_trsm(store(), k, base, plist_dp[k], base + plist_dp[k], plist_lo[k], linv_[set].get(),
                     p64_[set].get(), panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s, 3));
-      if (!dist()) oz_slice_next(k, s);
+      if (!dist() && oz && !oz_fused[k]) oz_slice_next(k, s);
     } else {
       const int below = nt - k - 1;
       k_panel_trsm_fp64<<<dim3(below * (b / DG_BM), b / DG_BN), DG_THREADS, 0, s>>>(
@@ -1478,9 +1499,9 @@ struct Chol {
                      static_cast<long long>(cnt), merged ? 1 : 0, resume ? 1 : 0);
       const int pu = prof_begin(kUpdDp + cls, s);
       if (oz && cls == 0) {
-        if (part != 0) {
-          oz_slice_rest(k, s);
-          if (merged) oz_slice_rest(k + 1, s);
+        if (part != 0) {  // unless the panel epilogue wrote them
+          if (!oz_fused[k]) oz_slice_rest(k, s);
+          if (merged && !oz_fused[k + 1]) oz_slice_rest(k + 1, s);
         }
         oz_update(store(), k, lst, cnt, oz_[set], merged ? k + 1 : -1, merged ? &oz_[set2] : nullptr, rowexp.get(),
                   fail.get(), s, max_ctas, ctr(s, 0));

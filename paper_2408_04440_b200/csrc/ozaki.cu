@@ -59,9 +59,7 @@ __device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
       : "memory");
 }
 
-// 2^mu_g bounds |panel row g| with one bit of headroom: rowexp = 14 - E
-// with sqrt(a_gg) < 2^E (k_rowexp), so mu = E + 1.
-__device__ __forceinline__ int oz_mu(const int* rowexp, int g) { return 15 - __ldg(rowexp + g); }
+__device__ __forceinline__ int oz_mu(const int* rowexp, int g) { return oz_mu_of(__ldg(rowexp + g)); }
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -98,25 +96,9 @@ __global__ void __launch_bounds__(256) k_oz_slice(TileStore ts, int k, const dou
   for (int s = 0; s < OZ_DIGITS; ++s) dig[s] = 0;
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
-    // |x| = m 2^(e - 1075); N = floor(|x| 2^(56 - mu)) < 2^56 (saturated beyond)
-    const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(xs[u]));
-    const bool neg = bits >> 63;
-    int e = static_cast<int>((bits >> 52) & 0x7ff);
-    unsigned long long m = bits & ((1ull << 52) - 1);
-    if (e) m |= 1ull << 52;
-    else e = 1;
-    // N = |x| 2^(56 - mu) rounded to nearest (ties up), saturated at 2^56 - 1
-    const int sh = e - 1019 - mu;
-    unsigned long long N;
-    if (sh >= 0) N = (sh > 3 || ((m << sh) >> 56)) ? (1ull << 56) - 1 : (m << sh);
-    else if (-sh >= 64) N = 0ull;
-    else N = min((m >> -sh) + ((m >> (-sh - 1)) & 1ull), (1ull << 56) - 1);
+    const uint64_t d = oz_digits(xs[u], mu);
 #pragma unroll
-    for (int s = 0; s < OZ_DIGITS; ++s) {
-      int d = static_cast<int>((N >> (49 - 7 * s)) & 127);
-      d = neg ? -d : d;
-      dig[s] |= static_cast<uint32_t>(d & 0xff) << (8 * u);
-    }
+    for (int s = 0; s < OZ_DIGITS; ++s) dig[s] |= static_cast<uint32_t>((d >> (8 * s)) & 0xff) << (8 * u);
   }
   uint8_t* rowp = s8 + r * (OZ_DIGITS * static_cast<int64_t>(b)) + (c0 >> 5) * 256 + (c0 & 31);
 #pragma unroll

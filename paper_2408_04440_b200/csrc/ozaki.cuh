@@ -44,6 +44,48 @@ struct OzSlices {
   void alloc(int64_t rows_, int b_);
 };
 
+// The eight signed base-128 digits of x relative to 2^mu (56-bit fixed
+// point, round to nearest, saturated), digit s in byte s: integer shifts only.
+__device__ __forceinline__ uint64_t oz_digits(double x, int mu) {
+  const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(x));
+  const bool neg = bits >> 63;
+  int e = static_cast<int>((bits >> 52) & 0x7ff);
+  unsigned long long m = bits & ((1ull << 52) - 1);
+  if (e) m |= 1ull << 52;
+  else e = 1;
+  const int sh = e - 1019 - mu;
+  unsigned long long N;
+  if (sh >= 0) N = (sh > 3 || ((m << sh) >> 56)) ? (1ull << 56) - 1 : (m << sh);
+  else if (-sh >= 64) N = 0ull;
+  else N = min((m >> -sh) + ((m >> (-sh - 1)) & 1ull), (1ull << 56) - 1);
+  uint64_t out = 0;
+#pragma unroll
+  for (int s = 0; s < OZ_DIGITS; ++s) {
+    int d = static_cast<int>((N >> (49 - 7 * s)) & 127);
+    d = neg ? -d : d;
+    out |= static_cast<uint64_t>(d & 0xff) << (8 * s);
+  }
+  return out;
+}
+// Writes the digits of 8 consecutive row elements x[0..8) at columns c0..c0+7
+// (c0 % 8 == 0) into a digit row (8 b bytes, [c/32][digit][c%32] layout).
+__device__ __forceinline__ void oz_store8(uint8_t* drow, int c0, const double (&x)[8], int mu) {
+  uint64_t d[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) d[u] = oz_digits(x[u], mu);
+  uint8_t* q = drow + (c0 >> 5) * 256 + (c0 & 31);
+#pragma unroll
+  for (int s = 0; s < OZ_DIGITS; ++s) {
+    uint64_t v = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v |= ((d[u] >> (8 * s)) & 0xffull) << (8 * u);
+    *reinterpret_cast<uint64_t*>(q + s * 32) = v;
+  }
+}
+// 2^mu_g bounds |panel row g| with one bit of headroom: rowexp = 14 - E with
+// sqrt(a_gg) < 2^E (k_rowexp), so mu = E + 1.
+__device__ __forceinline__ int oz_mu_of(int rowexp) { return 15 - rowexp; }
+
 // Digits of panel rows [row_begin, row_end) of step k (panel row r belongs
 // to tile k+1+r/b) from the FP64 mirror p64.
 void oz_slice(const TileStore& ts, int k, const double* p64, int64_t row_begin, int64_t row_end, const int* rowexp,

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "tc_gemm.cuh"
+#include "ozaki.cuh"
 #include "tcgen05.cuh"
 
 namespace sphemu_gpu {
@@ -157,6 +158,7 @@ struct TcArgs {
   const int* lexp;   // FP16x3 panel: per output column (Linv row) power-of-two exponent
   const int* yield;  // non-null: stop claiming items once *yield != 0 (dynamic scheduling only)
   int k2;            // update mode: second panel step of a merged two-step update (-1 = none)
+  uint8_t* s8;       // panel mode: INT8 DP digit rows to write (nullptr = none; p64 may then be nullptr)
 };
 
 template <int OPK>
@@ -879,9 +881,14 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
             } else {
               *reinterpret_cast<uint4*>(static_cast<uint16_t*>(tp) + e) = *reinterpret_cast<const uint4*>(h16);
             }
-            double2* pd = reinterpret_cast<double2*>(args.p64 + pe);
+            if (args.p64) {
+              double2* pd = reinterpret_cast<double2*>(args.p64 + pe);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) pd[u] = make_double2(qv[2 * u], qv[2 * u + 1]);
+              for (int u = 0; u < 4; ++u) pd[u] = make_double2(qv[2 * u], qv[2 * u + 1]);
+            }
+            if (args.s8)  // the INT8 DP class's digits of this row, instead of the FP64 mirror
+              oz_store8(args.s8 + prow * (OZ_DIGITS * static_cast<int64_t>(b)), n0 + c0 + t, qv,
+                        oz_mu_of(args.rowexp[min(i * args.lb + r, args.ts.n - 1)]));
             if (args.p_hi) {
               float hi[8], lo[8];
 #pragma unroll
@@ -1029,7 +1036,7 @@ __global__ void k_panel_prep16(TileStore ts, int k, const int2* list, const int*
 // DP-class panel tiles: P64 (already rounded) -> tile storage + mirrors.
 __global__ void k_panel_finish_dp(TileStore ts, int k, const int2* list, const double* __restrict__ p64,
                                   float* p_hi, float* p_lo, uint16_t* p16, int hp_format, const int* fail,
-                                  uint16_t* h_hi, uint16_t* h_lo, const int* rowexp) {
+                                  uint16_t* h_hi, uint16_t* h_lo, const int* rowexp, uint8_t* s8) {
   if (*(volatile const int*)fail >= 0) return;
   const int b = ts.b;
   const int64_t bb = (int64_t)b * b;
@@ -1055,6 +1062,17 @@ __global__ void k_panel_finish_dp(TileStore ts, int k, const int2* list, const d
     if (h_hi) {
       const int r = (int)(e / b);
       f16_split(x, rowexp[min(i * ts.lb + r, ts.n - 1)], h_hi[base + e], h_lo[base + e]);
+    }
+  }
+  if (s8) {  // INT8 DP digits of these rows: 8 consecutive elements per thread
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < bb / 8; g += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t e = g * 8;
+      const int r = (int)(e / b), c = (int)(e % b);
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = p64[base + e + u];
+      oz_store8(s8 + ((int64_t)(i - k - 1) * b + r) * (OZ_DIGITS * (int64_t)b), c, x,
+                oz_mu_of(rowexp[min(i * ts.lb + r, ts.n - 1)]));
     }
   }
 }
@@ -1139,7 +1157,7 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
     SPH_LAUNCH_CHECK();
     k_panel_finish_dp<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(n_dp)), 256, 0, s>>>(
         ts, k, d_dp, p64, pf.tf32_hi(), pf.tf32_lo(), pf.half16(), pf.hp_format, fail,
-        pf.f16x3 ? pf.h_hi.get() : nullptr, pf.h_lo.get(), pf.rowexp);
+        pf.f16x3 ? pf.h_hi.get() : nullptr, pf.h_lo.get(), pf.rowexp, pf.s8);
     SPH_LAUNCH_CHECK();
   }
   static const bool panel16 = [] {
@@ -1171,7 +1189,8 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
     a.sub_n = b / 128;
     a.sub_per = (b / TC_BM) * a.sub_n;
     a.items = n_lo * a.sub_per;
-    a.p64 = p64;
+    a.p64 = pf.s8 ? nullptr : p64;  // with digits written here nothing reads the SP/HP rows' FP64 mirror
+    a.s8 = pf.s8;
     a.p_hi = pf.tf32_hi();
     a.p_lo = pf.tf32_lo();
     a.p16 = pf.half16();

@@ -57,6 +57,7 @@ struct PanelFormats {
   void set_arena(const void* base, int64_t bytes, int b_);
   int bn = 256;
   bool pair_dyn_sp = false;  // SP-class CTA pairs claim items dynamically (and yield); see tc_update
+  uint8_t* s8 = nullptr;     // INT8 DP digit planes of this set, written by the panel epilogue (one GPU)
   void alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int hp_format_, bool f16x3_,
              const int* rowexp_);
 };
