@@ -41,8 +41,8 @@ case "$task" in
     n=$1; v=$2; hp=$3; IFS=',' read -ra sets <<< "${4:-NONE=1}"
     for kv in "${sets[@]}"; do echo "$kv"; env "$kv" timeout 300 python tools/ab.py "$n" "$v" "$hp" ${REPS:-3} ${TILE:-512}; done ;;
   timeline)
-    timeout 300 python tools/chol_timeline.py "$1" ${TILE:-512} "$2" 2>/dev/null | head -9
-    timeout 300 python tools/timeline_gaps.py "$1" "$2" ;;
+    timeout 600 python tools/chol_timeline.py "$1" ${TILE:-512} "$2" ${HP:-fp16} 2>/dev/null | head -9
+    timeout 600 python tools/timeline_gaps.py "$1" "$2" ${HP:-fp16} ;;
   oz)
     tools/micro/build_oz_bench.sh
     for d in 0 1 2; do echo "SPHEMU_OZ_DBG=$d"; SPHEMU_OZ_DBG=$d timeout 60 ./tools/micro/oz_bench; done
