@@ -672,13 +672,18 @@ struct Chol {
     const auto first = std::lower_bound(oz_tiles.begin(), oz_tiles.end(), k + 2);
     const int64_t cnt = oz_tiles.end() - first;
     if (cnt)
-      oz_slice_tiles(store(), k, p64_[set_of(k)].get(), d_oz_tiles.get() + (first - oz_tiles.begin()), cnt,
+      oz_slice_tiles(store(), k, oz_src(k), d_oz_tiles.get() + (first - oz_tiles.begin()), cnt,
                      rowexp.get(), oz_[set_of(k)], fail.get(), s);
   }
   void oz_slice_next(int k, cudaStream_t s) {  // tile k+1's rows, for the chain's diagonal SYRK
     if (oz && k + 1 < nt && oz_need[k + 1])
-      oz_slice(store(), k, p64_[set_of(k)].get(), 0, b, rowexp.get(), oz_[set_of(k)], fail.get(), s);
+      oz_slice(store(), k, oz_src(k), 0, b, rowexp.get(), oz_[set_of(k)], fail.get(), s);
   }
+  // Where the digits are cut from: one GPU reads the panel tiles themselves
+  // (their rounded values at 2-8 bytes; the panel epilogue then skips the FP64
+  // mirror of SP/HP rows, which nothing else reads); process grids read the
+  // FP64 mirror the import rebuilt (imported tiles are not in the arena).
+  const double* oz_src(int k) { return dist() ? p64_[set_of(k)].get() : nullptr; }
   DevBuf<double> dinv, spd_d, spd_pw;
   DevBuf<int> rowexp;  // per-row power-of-two operand scale (FP16x3 SP path)
   DevBuf<int> fail;
@@ -1439,6 +1444,7 @@ struct Chol {
       if (oz && !dist()) {
         oz_fused[k] = k < oz_fuse_frac() * nt;
         panel_[set].s8 = oz_fused[k] ? oz_[set].s8.get() : nullptr;
+        panel_[set].no_p64 = true;
       }
       const int2* base = plists.get() + plist_off[k];
       tc_panel_trsm(store(), k, base, plist_dp[k], base + plist_dp[k], plist_lo[k], linv_[set].get(),

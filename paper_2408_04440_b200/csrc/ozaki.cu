@@ -88,9 +88,37 @@ __global__ void __launch_bounds__(256) k_oz_slice(TileStore ts, int k, const dou
   const int c0 = static_cast<int>(w % chunks) * 128 + 4 * lane;
   const int tile = k + 1 + static_cast<int>(r / b), rr = static_cast<int>(r % b);
   const int mu = oz_mu(rowexp, min(tile * ts.lb + rr, ts.n - 1));
-  const double2 v01 = __ldcg(reinterpret_cast<const double2*>(p64 + r * b + c0));
-  const double2 v23 = __ldcg(reinterpret_cast<const double2*>(p64 + r * b + c0 + 2));
-  const double xs[4] = {v01.x, v01.y, v23.x, v23.y};
+  double xs[4];
+  if (p64) {
+    const double2 v01 = __ldcg(reinterpret_cast<const double2*>(p64 + r * b + c0));
+    const double2 v23 = __ldcg(reinterpret_cast<const double2*>(p64 + r * b + c0 + 2));
+    xs[0] = v01.x, xs[1] = v01.y, xs[2] = v23.x, xs[3] = v23.y;
+  } else {
+    // straight from the panel tile (i, k) at its storage precision: the
+    // rounded panel value the FP64 mirror would hold, at 2-8 bytes instead of 8
+    const int prec = ts.tprec(tile, k);
+    const char* row = static_cast<const char*>(ts.tile(tile, k)) + static_cast<int64_t>(rr) * b * prec_bytes(prec);
+    if (prec == kDP) {
+      const double2 v01 = __ldcg(reinterpret_cast<const double2*>(row) + c0 / 2);
+      const double2 v23 = __ldcg(reinterpret_cast<const double2*>(row) + c0 / 2 + 1);
+      xs[0] = v01.x, xs[1] = v01.y, xs[2] = v23.x, xs[3] = v23.y;
+    } else if (prec == kSP) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(row) + c0 / 4);
+      xs[0] = v.x, xs[1] = v.y, xs[2] = v.z, xs[3] = v.w;
+    } else {
+      const uint2 v = __ldcg(reinterpret_cast<const uint2*>(row) + c0 / 4);
+      const uint32_t w[2] = {v.x, v.y};
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (prec == kHP) {
+          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[u]));
+          xs[2 * u] = f.x, xs[2 * u + 1] = f.y;
+        } else {
+          xs[2 * u] = __uint_as_float(w[u] << 16), xs[2 * u + 1] = __uint_as_float(w[u] & 0xffff0000u);
+        }
+      }
+    }
+  }
   uint32_t dig[OZ_DIGITS];
 #pragma unroll
   for (int s = 0; s < OZ_DIGITS; ++s) dig[s] = 0;

@@ -87,7 +87,8 @@ __device__ __forceinline__ void oz_store8(uint8_t* drow, int c0, const double (&
 __device__ __forceinline__ int oz_mu_of(int rowexp) { return 15 - rowexp; }
 
 // Digits of panel rows [row_begin, row_end) of step k (panel row r belongs
-// to tile k+1+r/b) from the FP64 mirror p64.
+// to tile k+1+r/b) from the FP64 mirror p64, or (p64 == nullptr) straight
+// from the panel tiles at their storage precision.
 void oz_slice(const TileStore& ts, int k, const double* p64, int64_t row_begin, int64_t row_end, const int* rowexp,
               OzSlices& oz, const int* fail, cudaStream_t s);
 

@@ -1189,7 +1189,7 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
     a.sub_n = b / 128;
     a.sub_per = (b / TC_BM) * a.sub_n;
     a.items = n_lo * a.sub_per;
-    a.p64 = pf.s8 ? nullptr : p64;  // with digits written here nothing reads the SP/HP rows' FP64 mirror
+    a.p64 = (pf.s8 || pf.no_p64) ? nullptr : p64;  // nothing reads the SP/HP rows' FP64 mirror then
     a.s8 = pf.s8;
     a.p_hi = pf.tf32_hi();
     a.p_lo = pf.tf32_lo();

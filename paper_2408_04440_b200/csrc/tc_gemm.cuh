@@ -58,6 +58,7 @@ struct PanelFormats {
   int bn = 256;
   bool pair_dyn_sp = false;  // SP-class CTA pairs claim items dynamically (and yield); see tc_update
   uint8_t* s8 = nullptr;     // INT8 DP digit planes of this set, written by the panel epilogue (one GPU)
+  bool no_p64 = false;       // the SP/HP panel rows' FP64 mirror has no reader (one GPU, INT8 DP class)
   void alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int hp_format_, bool f16x3_,
              const int* rowexp_);
 };
