@@ -1840,14 +1840,26 @@ struct Chol {
       peer_sync[r] = static_cast<uint32_t*>(ps);
     }
   }
+  // Stream memory operations through the runtime's driver entry points (the
+  // library does not link libcuda: it must load on hosts without a driver).
+  using StreamValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static StreamValueFn driver_fn(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      throw Error(SPHEMU_ERR_CUDA, std::string(name) + " unavailable");
+    return reinterpret_cast<StreamValueFn>(p);
+  }
   static void stream_write(cudaStream_t s, uint32_t* addr, uint32_t v) {
-    const CUresult r = cuStreamWriteValue32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
-                                            CU_STREAM_WRITE_VALUE_DEFAULT);
+    static const StreamValueFn fn = driver_fn("cuStreamWriteValue32");
+    const CUresult r = fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                          CU_STREAM_WRITE_VALUE_DEFAULT);
     if (r != CUDA_SUCCESS) throw Error(SPHEMU_ERR_CUDA, "cuStreamWriteValue32 failed: " + std::to_string(r));
   }
   static void stream_wait_geq(cudaStream_t s, uint32_t* addr, uint32_t v) {
-    const CUresult r = cuStreamWaitValue32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
-                                           CU_STREAM_WAIT_VALUE_GEQ);
+    static const StreamValueFn fn = driver_fn("cuStreamWaitValue32");
+    const CUresult r = fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v,
+                          CU_STREAM_WAIT_VALUE_GEQ);
     if (r != CUDA_SUCCESS) throw Error(SPHEMU_ERR_CUDA, "cuStreamWaitValue32 failed: " + std::to_string(r));
   }
 
