@@ -725,7 +725,8 @@ struct Chol {
   static constexpr int kParts = 6;
   std::vector<int64_t> list_off, list_cnt;  // [(k * kParts + part) * 3 + class]
   DevBuf<int2> plists;                      // panel tiles per step: DP class, then SP/HP
-  std::vector<int64_t> plist_off, plist_dp, plist_lo;
+  std::vector<int64_t> plist_off, plist_dp, plist_lo, plist_bf;
+  bool panel_bf = false;  // BF16-class panel tiles listed after the others (plist_bf)
   PanelFormats panel_[kSets];               // tensor-core operand mirrors per set
   cudaStream_t stream = nullptr;            // main stream: bulk trailing updates
   cudaStream_t pstream = nullptr;           // high-priority stream: POTRF + panel chain
@@ -1200,16 +1201,31 @@ struct Chol {
     plist_off.assign(nt, 0);
     plist_dp.assign(nt, 0);
     plist_lo.assign(nt, 0);
+    plist_bf.assign(nt, 0);
+    // BF16-class panel tiles go through the bf16 x (hi + lo) panel kernel
+    // (SPHEMU_PANEL_BF16=0: 3xTF32 like the SP class): listed last per step.
+    static const bool panel_bf_env = [] {
+      const char* e = std::getenv("SPHEMU_PANEL_BF16");
+      return !(e && e[0] == '0');
+    }();
+    const bool bf_split = panel_bf_env && cfg.hp_format == SPHEMU_HP_BF16 && cfg.compute == SPHEMU_COMPUTE_TENSOR;
     std::vector<int2> pl;
     for (int k = 0; k < nt; ++k) {
       plist_off[k] = static_cast<int64_t>(pl.size());
       for (int i = k + 1; i < nt; ++i)
         if (fp64_class(pmap[tix(i, k)]) && mine(i, k)) pl.push_back(make_int2(i, k));
       plist_dp[k] = static_cast<int64_t>(pl.size()) - plist_off[k];
-      for (int i = k + 1; i < nt; ++i)
-        if (!fp64_class(pmap[tix(i, k)]) && mine(i, k)) pl.push_back(make_int2(i, k));
+      for (int i = k + 1; i < nt; ++i) {
+        const int c = pmap[tix(i, k)];
+        if (!fp64_class(c) && mine(i, k) && !(bf_split && c == SPHEMU_PREC_HP)) pl.push_back(make_int2(i, k));
+      }
       plist_lo[k] = static_cast<int64_t>(pl.size()) - plist_off[k] - plist_dp[k];
+      if (bf_split)
+        for (int i = k + 1; i < nt; ++i)
+          if (pmap[tix(i, k)] == SPHEMU_PREC_HP && mine(i, k)) pl.push_back(make_int2(i, k));
+      plist_bf[k] = static_cast<int64_t>(pl.size()) - plist_off[k] - plist_dp[k] - plist_lo[k];
     }
+    panel_bf = bf_split;
     pl_i.resize(pl.size());
     for (size_t e = 0; e < pl.size(); ++e) pl_i[e] = pl[e].x;
     if (!pl.empty()) {
@@ -1448,7 +1464,8 @@ struct Chol {
       }
       const int2* base = plists.get() + plist_off[k];
       tc_panel_trsm(store(), k, base, plist_dp[k], base + plist_dp[k], plist_lo[k], linv_[set].get(),
-                    p64_[set].get(), panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s, 3));
+                    p64_[set].get(), panel_[set], fail.get(), sat.get(), s, max_ctas, ctr(s, 3),
+                    base + plist_dp[k] + plist_lo[k], plist_bf[k]);
       if (!dist() && oz && !oz_fused[k]) oz_slice_next(k, s);
     } else {
       const int below = nt - k - 1;
@@ -1969,7 +1986,7 @@ struct Chol {
 
   void op_panel_dist(int k, cudaStream_t s, int max_ctas = 0) {
     const int set = set_of(k);
-    if (xchunks > 1 && xstream && cfg.compute == SPHEMU_COMPUTE_TENSOR) {
+    if (xchunks > 1 && xstream && cfg.compute == SPHEMU_COMPUTE_TENSOR && !panel_bf) {
       op_panel_dist_chunked(k, s, max_ctas);
       return;
     }

@@ -105,7 +105,7 @@ void PanelFormats::alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int 
   m_inlo_a = make_map(in_lo.get(), rows, b, 4, TC_BM);
   m_lhi_b = make_map(l_hi.get(), b, b, 4, bn_tf32);
   m_llo_b = make_map(l_lo.get(), b, b, 4, bn_tf32);
-  if (f16x3) {
+  if (f16x3 || hp_format == SPHEMU_HP_BF16) {  // FP16x3 panel (opt-in) / the BF16x2 panel's operands
     in16_hi.alloc(elems);
     in16_lo.alloc(elems);
     l16_hi.alloc(static_cast<size_t>(b) * b);
@@ -115,6 +115,8 @@ void PanelFormats::alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int 
     m_in16lo_a = make_map(in16_lo.get(), rows, b, 2, TC_BM);
     m_l16hi_b = make_map(l16_hi.get(), b, b, 2, 128);
     m_l16lo_b = make_map(l16_lo.get(), b, b, 2, 128);
+  }
+  if (f16x3) {
     h_hi.alloc(elems);
     h_lo.alloc(elems);
     m_hhi_a = make_map(h_hi.get(), rows, b, 2, TC_BM, 128);
@@ -127,7 +129,8 @@ void PanelFormats::alloc(int nt_, int b_, const std::vector<uint8_t>& pmap, int 
 // ---------------------------------------------------------------------------
 // Device: the persistent warp-specialized GEMM
 // ---------------------------------------------------------------------------
-enum : int { OP_F16 = 0, OP_BF16 = 1, OP_TF32X3 = 2, OP_F16X3 = 3 };
+// OP_BF16X2: A one bf16 operand, B a bf16 hi/lo split (2 MMAs): the BF16-class panel TRSM
+enum : int { OP_F16 = 0, OP_BF16 = 1, OP_TF32X3 = 2, OP_F16X3 = 3, OP_BF16X2 = 4 };
 enum : int { MODE_UPDATE = 0, MODE_PANEL = 1 };
 
 struct TcArgs {
@@ -164,6 +167,7 @@ struct TcArgs {
 template <int OPK>
 struct OpTraits {
   static constexpr bool kSplit = (OPK == OP_TF32X3 || OPK == OP_F16X3);
+  static constexpr bool kBsplit = (OPK == OP_BF16X2);  // only B carries a lo part
   static constexpr bool kTf32 = (OPK == OP_TF32X3);
   static constexpr int kElem = kTf32 ? 4 : 2;
   // smem row of K per stage (swizzle width). 64-byte rows (SWIZZLE_64B, twice
@@ -171,7 +175,7 @@ struct OpTraits {
   static constexpr int kRowBytes = 128;
   static constexpr int kBK = kRowBytes / kElem;  // K elements per stage
   static constexpr int kUK = kTf32 ? 8 : 16;    // K per tcgen05.mma
-  static constexpr int kFmt = (OPK == OP_F16 || OPK == OP_F16X3) ? 0 : (OPK == OP_BF16 ? 1 : 2);
+  static constexpr int kFmt = (OPK == OP_F16 || OPK == OP_F16X3) ? 0 : ((OPK == OP_BF16 || OPK == OP_BF16X2) ? 1 : 2);
 };
 
 // CG = 2: a CTA pair (cluster of 2) runs cta_group::2 MMAs of M = 256: each
@@ -183,7 +187,7 @@ struct TcLayout {
   static constexpr bool kUpd = (MODE == MODE_UPDATE);
   static constexpr int kA = TC_BM * T::kRowBytes;          // bytes of one A buffer
   static constexpr int kB = (BN / CG) * T::kRowBytes;      // bytes of one B buffer (this CTA's rows)
-  static constexpr int kStage = (T::kSplit ? 2 : 1) * (kA + kB);
+  static constexpr int kStage = (T::kSplit ? 2 : 1) * (kA + kB) + (T::kBsplit ? kB : 0);
   // Update mode stages the C tile through shared memory: per epilogue warp
   // a ring of kRing TMA boxes (32 rows x 128 bytes each).
 #ifndef SPH_TC_RING
@@ -486,6 +490,7 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
               tma_load_2d_hint(ma_lo, &full[stage], st + Lay::kA + Lay::kB, kx, a_row, keep);
               tma_load_2d_hint(mb_lo, &full[stage], st + 2 * Lay::kA + Lay::kB, kx, b_row, keep);
             }
+            if (T::kBsplit) tma_load_2d_hint(mb_lo, &full[stage], st + Lay::kA + Lay::kB, kx, b_row, keep);
           }
           if (kb2 == 1 && more) prefetch_c(w_next, ij_nxt, crow_nxt);
           if (++stage == S) {
@@ -549,6 +554,10 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
               const uint64_t b_lo = umma_desc_k<T::kRowBytes>(st + 2 * Lay::kA + Lay::kB);
               umma_f16(d, a_lo + koff, b_hi + koff, idesc, accum);
               umma_f16(d, a_hi + koff, b_lo + koff, idesc, 1u);
+              umma_f16(d, a_hi + koff, b_hi + koff, idesc, 1u);
+            } else if constexpr (T::kBsplit) {
+              const uint64_t b_lo = umma_desc_k<T::kRowBytes>(st + Lay::kA + Lay::kB);
+              umma_f16(d, a_hi + koff, b_lo + koff, idesc, accum);
               umma_f16(d, a_hi + koff, b_hi + koff, idesc, 1u);
             } else if constexpr (CG == 2) {
               umma_f16_cg2(d, a_hi + koff, b_hi + koff, idesc, accum);
@@ -968,6 +977,33 @@ __global__ void k_panel_prep(TileStore ts, int k, const int2* list, const double
   }
 }
 
+// BF16-class panel TRSM inputs (OP_BF16X2): blockIdx.y == 0 splits Linv
+// into bf16 hi + lo (the B operand, ~16 bits), y >= 1 copies each listed
+// tile's bf16 bits into its panel rows (the A operand; the TRSM writes the
+// tile in place, so it cannot read it there). X = B (Linv_hi + Linv_lo)^T
+// carries ~2^-16 relative error before the epilogue rounds it to bf16.
+__global__ void k_panel_prep_bf16x2(TileStore ts, int k, const int2* list, const double* __restrict__ linv,
+                                    uint16_t* in16, uint16_t* l_hi, uint16_t* l_lo, const int* fail) {
+  if (*(volatile const int*)fail >= 0) return;
+  const int b = ts.b;
+  const int64_t bb = (int64_t)b * b;
+  if (blockIdx.y == 0) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < bb; e += (int64_t)gridDim.x * blockDim.x) {
+      const double x = linv[e];
+      const __nv_bfloat16 hi = __double2bfloat16(x);
+      const __nv_bfloat16 lo = __double2bfloat16(x - (double)__bfloat162float(hi));
+      l_hi[e] = __bfloat16_as_ushort(hi);
+      l_lo[e] = __bfloat16_as_ushort(lo);
+    }
+    return;
+  }
+  const int i = list[blockIdx.y - 1].x;
+  const uint4* src = static_cast<const uint4*>(ts.tile(i, k));
+  uint4* dst = reinterpret_cast<uint4*>(in16 + (int64_t)(i - k - 1) * bb);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < bb / 8; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = src[e];
+}
+
 // FP16x3 panel TRSM inputs. With 2^(14 - rowexp[x]) ~ sqrt(A_xx) (k_rowexp):
 //   B_s[r][c]   = B[r][c] 2^(rowexp[R] + rowexp[C] - 14)      |B_s| <~ 2^14
 //   L_s[j][c]   = Linv[j][c] 2^(14 - rowexp[C] + g_j)        g_j: row max -> <= 2^14
@@ -1149,7 +1185,7 @@ void launch_tc(const CUtensorMap& a_hi, const CUtensorMap& a_lo, const CUtensorM
 
 void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, const int2* d_lo,
                    int64_t n_lo, const double* linv, double* p64, PanelFormats& pf, const int* fail,
-                   unsigned* sat, cudaStream_t s, int max_ctas, int* counter) {
+                   unsigned* sat, cudaStream_t s, int max_ctas, int* counter, const int2* d_bf, int64_t n_bf) {
   const int b = ts.b;
   if (n_dp) {
     k_panel_trsm_fp64_list<<<dim3(static_cast<unsigned>(n_dp * (b / DG_BM)), b / DG_BN), DG_THREADS, 0, s>>>(
@@ -1179,16 +1215,16 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
         ts, k, d_lo, linv, pf.in_hi.get(), pf.in_lo.get(), pf.l_hi.get(), pf.l_lo.get(), fail);
     SPH_LAUNCH_CHECK();
   }
-  if (n_lo) {
+  auto panel_args = [&](const int2* list, int64_t cnt) {
     TcArgs a{};
     a.k2 = -1;
     a.ts = ts;
-    a.list = d_lo;
+    a.list = list;
     a.k = k;
     a.b = b;
     a.sub_n = b / 128;
     a.sub_per = (b / TC_BM) * a.sub_n;
-    a.items = n_lo * a.sub_per;
+    a.items = cnt * a.sub_per;
     a.p64 = (pf.s8 || pf.no_p64) ? nullptr : p64;  // nothing reads the SP/HP rows' FP64 mirror then
     a.s8 = pf.s8;
     a.p_hi = pf.tf32_hi();
@@ -1203,12 +1239,24 @@ void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, c
     a.sat = sat;
     a.counter = counter;
     a.lexp = pf.lexp.get();
+    return a;
+  };
+  if (n_lo) {
+    const TcArgs a = panel_args(d_lo, n_lo);
     if (p16)
       launch_tc<128, OP_F16X3, MODE_PANEL>(pf.m_in16hi_a, pf.m_in16lo_a, pf.m_l16hi_b, pf.m_l16lo_b, pf.m_l16hi_b, a, s,
                                            max_ctas);
     else
       launch_tc<128, OP_TF32X3, MODE_PANEL>(pf.m_inhi_a, pf.m_inlo_a, pf.m_lhi_b, pf.m_llo_b, pf.m_lhi_b, a, s,
                                             max_ctas);
+  }
+  if (n_bf) {  // BF16-class panel tiles: one bf16 operand x Linv's bf16 hi/lo, 2 MMAs per K step
+    k_panel_prep_bf16x2<<<dim3(std::max(1, b * b / (256 * 16)), static_cast<unsigned>(n_bf + 1)), 256, 0, s>>>(
+        ts, k, d_bf, linv, pf.in16_hi.get(), pf.l16_hi.get(), pf.l16_lo.get(), fail);
+    SPH_LAUNCH_CHECK();
+    const TcArgs a = panel_args(d_bf, n_bf);
+    launch_tc<128, OP_BF16X2, MODE_PANEL>(pf.m_in16hi_a, pf.m_in16hi_a, pf.m_l16hi_b, pf.m_l16lo_b, pf.m_l16hi_b, a, s,
+                                          max_ctas);
   }
 }
 

@@ -64,11 +64,13 @@ struct PanelFormats {
 };
 
 // Panel TRSM for all i > k: DP-class tiles through FP64 DMMA, SP/HP-class
-// tiles through 3xTF32 tcgen05; writes the rounded P64 mirror, the tensor
-// mirrors, and the tile storage.
+// tiles (d_lo) through 3xTF32 tcgen05, BF16-class tiles (d_bf) through one
+// bf16 operand x Linv's bf16 hi/lo split; writes the rounded P64 mirror, the
+// tensor mirrors, and the tile storage.
 void tc_panel_trsm(const TileStore& ts, int k, const int2* d_dp, int64_t n_dp, const int2* d_lo,
                    int64_t n_lo, const double* linv, double* p64, PanelFormats& pf, const int* fail,
-                   unsigned* sat, cudaStream_t s, int max_ctas = 0, int* counter = nullptr);
+                   unsigned* sat, cudaStream_t s, int max_ctas = 0, int* counter = nullptr,
+                   const int2* d_bf = nullptr, int64_t n_bf = 0);
 
 // Trailing update of the SP (cls 1) or HP (cls 2) output tiles of step k.
 // yield (non-null, dynamically scheduled launches only): the CTAs stop
