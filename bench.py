@@ -8,8 +8,8 @@ factored (mpchol.cpp:351-410). The N = 1 line also carries the 1-GPU point of
 C3 ("c3_1gpu") so the C3 scaling curve has its base.
 
 N > 1 (configs[2] "C3"): make_spd_test_matrix(129 600, seed 1), dpsphp with
-BF16 HP storage, block-cyclic over P x Q = 2x1 / 4x1 / 8x1 GPUs with copy-engine
-panel broadcasts (2D grids P x Q > 1 through the same handle); step = the generator writes each rank's owned tiles at
+BF16 HP storage, 2D block-cyclic over P x Q = 2x1 / 2x2 / 4x2 GPUs with copy-engine
+panel broadcasts; step = the generator writes each rank's owned tiles at
 storage precision, then the distributed factorization. Strong scaling.
 
   value    = N^3/3 / device time per step, TFLOP/s (whole job, max over ranks);
@@ -167,11 +167,10 @@ WORKLOADS = {
     "C3": {"n": 129600, "variant": "dpsphp", "tile": 512, "hp": "bf16", "input": "generate",
            "desc": "C3: tiled Cholesky make_spd_test_matrix(129600, 1) (L=360) dpsphp/BF16 b=512"},
 }
-# Process grids: block-cyclic over process rows (P x 1). With the copy-engine
-# panel exchange every rank pulls the whole panel column anyway, so a taller
-# grid only splits the chain's panel TRSM further: C3 4 GPUs 4x1 314 ms vs 2x2
-# 331 ms (tools/gpu_tasks.sh dist 4 4 / dist 4 2); 8 GPUs not measurable here.
-GRIDS = {1: (1, 1), 2: (2, 1), 4: (4, 1), 8: (8, 1)}
+# Process grids: 2D block-cyclic P x Q. With the copy-engine
+# exchange and tile k+1's panel row sent first, C3 on 4 GPUs: 2x2 304 ms,
+# 4x1 316 ms (tools/gpu_tasks.sh dist 4 2 / dist 4 4); 8 GPUs not measurable here.
+GRIDS = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}
 THRESH = {"dp": 1e-12, "dpsp": 5e-6, "dpsphp": 1e-2, "dphp": 5e-2}  # acceptance_main.cpp:226
 
 

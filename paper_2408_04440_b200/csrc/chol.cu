@@ -593,6 +593,14 @@ struct Chol {
   std::vector<uint8_t*> peer_xbuf;
   std::vector<uint32_t*> peer_sync;
   uint32_t xepoch = 0;                      // advanced by nt per factorization (stream-ordered words never go back)
+  // Early exchange (lookahead on a process grid): tile k+1's panel row goes
+  // first (its own TRSM, pack, publish, pull, import on the chain) so the
+  // chain's next diagonal SYRK and POTRF start while the rest of the panel is
+  // still being solved / pulled / imported on xstream; xlate[k] marks steps
+  // whose panel completes on xstream.
+  std::vector<uint8_t> xlate;
+  cudaEvent_t ev_trdone = nullptr;
+  void record_panel(int k) { SPH_CUDA(cudaEventRecord(ev_panel[k], (xlate.size() > size_t(k) && xlate[k]) ? xstream : pstream)); }
   DevBuf<int2> ilists, xsend;
   DevBuf<int64_t> ioffs, xsoffs;
   std::vector<int64_t> ilist_off, ilist_cnt, xsend_off, xsend_cnt;
@@ -1344,7 +1352,12 @@ struct Chol {
     SPH_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     SPH_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, prio_lo));
     SPH_CUDA(cudaStreamCreateWithPriority(&pstream, cudaStreamNonBlocking, prio_hi));
-    if (dist() && xchg_bcast()) {
+    if (xipc) {
+      SPH_CUDA(cudaStreamCreateWithPriority(&xstream, cudaStreamNonBlocking, prio_hi));
+      SPH_CUDA(cudaEventCreateWithFlags(&ev_xdone, cudaEventDisableTiming));
+      SPH_CUDA(cudaEventCreateWithFlags(&ev_trdone, cudaEventDisableTiming));
+    }
+    if (dist() && xchg_bcast() && !xipc) {
       static const int env_chunks = [] {
         const char* e = std::getenv("SPHEMU_XCHG_CHUNKS");
         return e ? std::max(1, std::atoi(e)) : 1;  // measured slower when chunked (C3 2x2: 1 / 2 / 4 / 8 -> 358 / 374 / 388 / 425 ms)
@@ -1395,6 +1408,7 @@ struct Chol {
     for (auto e : ev_bulkdp) cudaEventDestroy(e);
     if (ev_start_p) cudaEventDestroy(ev_start_p);
     if (xstream) cudaStreamSynchronize(xstream);
+    if (ev_trdone) cudaEventDestroy(ev_trdone);
     for (auto e : ev_tr) cudaEventDestroy(e);
     if (ev_xdone) cudaEventDestroy(ev_xdone);
     if (xstream) cudaStreamDestroy(xstream);
@@ -1566,15 +1580,20 @@ struct Chol {
   void factor() {
     factored = false;
     if (xipc) xepoch += static_cast<uint32_t>(nt) + 2;
+    xlate.assign(nt, 0);
     std::fill(oz_rest.begin(), oz_rest.end(), 0);
     launches_at_start = launch_count();
     t_start = std::chrono::steady_clock::now();
     SPH_CUDA(cudaEventRecord(ev0, stream));
     if (xipc) {
-      // every rank's previous factorization (both streams) is done before any
+      // every rank's previous factorization (all streams) is done before any
       // owner refills an exchange half of this one: a device-side barrier
       SPH_CUDA(cudaEventRecord(ev_start_p, pstream));
       SPH_CUDA(cudaStreamWaitEvent(stream, ev_start_p, 0));
+      if (xstream) {
+        SPH_CUDA(cudaEventRecord(ev_xdone, xstream));
+        SPH_CUDA(cudaStreamWaitEvent(stream, ev_xdone, 0));
+      }
       SPH_NCCL(ncclAllReduce(xbar.get(), xbar.get(), 1, ncclInt32, ncclSum, comm, stream));
     }
     // SMs left to the chain while the bulk runs. Early steps, where the bulk
@@ -1621,7 +1640,7 @@ struct Chol {
       SPH_CUDA(cudaStreamWaitEvent(pstream, ev_start_p, 0));
       op_potrf(0, pstream);
       op_panel(0, pstream);
-      SPH_CUDA(cudaEventRecord(ev_panel[0], pstream));
+      record_panel(0);
       col_out(0, pstream);
       for (int k = 0; k + 1 < nt; ++k) {
         // chain: SYRK of the next diagonal tile -> POTRF -> (column below ready) -> panel.
@@ -1646,7 +1665,7 @@ struct Chol {
           op_panel(k + 1, pstream);
           if (yield) SPH_CUDA(cudaMemsetAsync(yield_flag.get(), 0, sizeof(int), pstream));
         }
-        SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
+        record_panel(k + 1);
         col_out(k + 1, pstream);
         const int bulk_ctas = std::max(1, num_sms() - reserve);
         op_update(k, 1, stream, bulk_ctas, yield ? yield_flag.get() : nullptr, false, ev_bulkdp[k]);
@@ -1734,7 +1753,7 @@ struct Chol {
       SPH_CUDA(cudaStreamWaitEvent(pstream, ev_start_p, 0));
       potrf(0, pstream);
       panel(0, pstream);
-      SPH_CUDA(cudaEventRecord(ev_panel[0], pstream));
+      record_panel(0);
       cols(0, pstream);
       cudaEvent_t diag_ready = nullptr;  // diagonal tile (k+1, k+1) has every update of steps < k
       auto yielding_panel = [&](int k, bool y) {
@@ -1759,14 +1778,14 @@ struct Chol {
         op_update(k, 2, stream, 0);
         SPH_CUDA(cudaEventRecord(ev_colrest[k], stream));
         if (k + 2 >= nt) {  // the last step: no panel below the last diagonal tile
-          SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
+          record_panel(k + 1);
           cols(k + 1, pstream);
           break;
         }
         // ---- step k: panel k+1 on the chain, column k+2 by panel k on the main stream
         SPH_CUDA(cudaStreamWaitEvent(pstream, ev_colrest[k], 0));
         yielding_panel(k + 1, y);
-        SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
+        record_panel(k + 1);
         cols(k + 1, pstream);
         op_update(k, 3, stream, bulk_ctas, y ? yield_flag.get() : nullptr);
         if (y) {
@@ -1786,7 +1805,7 @@ struct Chol {
           SPH_CUDA(cudaStreamWaitEvent(pstream, ev_colrest[k + 1], 0));
           yielding_panel(k + 2, y);
         }
-        SPH_CUDA(cudaEventRecord(ev_panel[k + 2], pstream));
+        record_panel(k + 2);
         cols(k + 2, pstream);
         op_update(k, 4, stream, 0);  // column k+3: feeds the next pair's chain
         SPH_CUDA(cudaEventRecord(ev_bulk[k + 1], stream));
@@ -1800,6 +1819,10 @@ struct Chol {
         k += 2;
       }
       SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[nt - 1], 0));
+    }
+    if (D && xstream) {  // the last exchange's acknowledgements are part of the factorization
+      SPH_CUDA(cudaEventRecord(ev_xdone, xstream));
+      SPH_CUDA(cudaStreamWaitEvent(stream, ev_xdone, 0));
     }
     if (D) SPH_NCCL(ncclAllReduce(sat.get(), sat.get(), 1, ncclUint32, ncclSum, comm, stream));
   }
@@ -1829,8 +1852,8 @@ struct Chol {
     const int W = P * Q;
     xbar.alloc(1);
     SPH_CUDA(cudaMemset(xbar.get(), 0, sizeof(int)));
-    xsync.alloc(1 + W);
-    SPH_CUDA(cudaMemset(xsync.get(), 0, (1 + W) * sizeof(uint32_t)));
+    xsync.alloc(2 + W);  // [0] published step, [1 + r] acks, [1 + W] tile k+1 published early
+    SPH_CUDA(cudaMemset(xsync.get(), 0, (2 + W) * sizeof(uint32_t)));
     cudaIpcMemHandle_t mine[2];
     SPH_CUDA(cudaIpcGetMemHandle(&mine[0], xbuf.get()));
     SPH_CUDA(cudaIpcGetMemHandle(&mine[1], xsync.get()));
@@ -1984,8 +2007,118 @@ struct Chol {
     SPH_CUDA(cudaStreamWaitEvent(s, ev_xdone, 0));
   }
 
+  // Copy-engine exchange with tile k+1 first (see xlate): on the chain stream
+  // s, tile (k+1, k)'s TRSM, pack and early publish; its pull + import on the
+  // next diagonal's owner (+ its digits); then the rest of this rank's TRSM,
+  // pack and publish. The pulls of the other owners' blocks, the import and
+  // the acknowledgements run on xstream, so the chain's next SYRK / POTRF
+  // overlap them; ev_panel[k] is recorded on xstream (record_panel).
+  void op_panel_dist_early(int k, cudaStream_t s, int max_ctas) {
+    const int set = set_of(k);
+    const int W = P * Q;
+    const uint32_t ep = xepoch + static_cast<uint32_t>(k) + 1;
+    const int64_t par = (k & 1) * xhalf;
+    uint8_t* own = xbuf.get() + par;
+    const unsigned gx = static_cast<unsigned>(std::max(1, b * b / (256 * 16)));
+    PanelFormats& pf = panel_[set];
+    const bool tensor = cfg.compute == SPHEMU_COMPUTE_TENSOR;
+    const int i1 = k + 1;
+    const int o1 = owner(i1, k), d1 = owner(i1, i1);
+    // the per-class panel lists are sorted by tile row: i1 can only be a list's first entry
+    const int64_t off = plist_off[k], ndp = plist_dp[k], nlo = plist_lo[k], nbf = plist_bf[k];
+    const int2* L = plists.get();
+    auto first_is = [&](int64_t o, int64_t n) { return n > 0 && pl_i[o] == i1; };
+    const bool in_dp = first_is(off, ndp), in_lo = first_is(off + ndp, nlo), in_bf = first_is(off + ndp + nlo, nbf);
+    const int pp = prof_begin(kPanel, s);
+    if (k >= 2 && xsend_cnt[k])  // this parity half was last read at step k-2
+      for (int q = 0; q < W; ++q)
+        if (q != rank) stream_wait_geq(s, xsync.get() + 1 + q, ep - 2);
+    const bool mine1 = in_dp || in_lo || in_bf;
+    if (!tensor) op_panel(k, s, max_ctas);  // FP64 compute: the whole column first
+    if (mine1) {
+      if (tensor)
+        tc_panel_trsm(store(), k, L + off, in_dp ? 1 : 0, L + off + ndp, in_lo ? 1 : 0, linv_[set].get(),
+                      p64_[set].get(), pf, fail.get(), sat.get(), s, max_ctas, ctr(s, 3), L + off + ndp + nlo,
+                      in_bf ? 1 : 0);
+      // the early pack: xsend is sorted by tile row, i1 is its first entry
+      k_panel_pack<<<dim3(gx, 1), 256, 0, s>>>(store(), k, xsend.get() + xsend_off[k], xsoffs.get() + xsend_off[k],
+                                               own, fail.get());
+      SPH_LAUNCH_CHECK();
+      stream_write(s, xsync.get() + 1 + W, ep);
+    }
+    if (d1 == rank && o1 != rank) {  // the next diagonal's SYRK reads tile (k+1, k)'s rows
+      const int64_t x1 = xpos_h[k][0];
+      const int64_t by = static_cast<int64_t>(b) * b * prec_bytes(sprec[tix(i1, k)]);
+      stream_wait_geq(s, peer_sync[o1] + 1 + W, ep);
+      SPH_CUDA(cudaMemcpyAsync(own + x1, peer_xbuf[o1] + par + x1, static_cast<size_t>(by), cudaMemcpyDeviceToDevice, s));
+      // ilist is sorted by tile row too: i1 is its first entry here
+      k_panel_import<<<dim3(gx, 1), 256, 0, s>>>(
+          store(), k, ilists.get() + ilist_off[k], ioffs.get() + ilist_off[k], own, p64_[set].get(),
+          tensor ? pf.tf32_hi() : nullptr, tensor ? pf.tf32_lo() : nullptr, tensor ? pf.half16() : nullptr,
+          (tensor && pf.f16x3) ? pf.h_hi.get() : nullptr, (tensor && pf.f16x3) ? pf.h_lo.get() : nullptr,
+          rowexp.get(), cfg.hp_format, d_import_need.get(), fail.get());
+      SPH_LAUNCH_CHECK();
+    }
+    if (d1 == rank) oz_slice_next(k, s);  // the chain's own diagonal SYRK (other readers: after the import)
+    // the rest of this rank's column
+    if (tensor)
+      tc_panel_trsm(store(), k, L + off + (in_dp ? 1 : 0), ndp - (in_dp ? 1 : 0), L + off + ndp + (in_lo ? 1 : 0),
+                    nlo - (in_lo ? 1 : 0), linv_[set].get(), p64_[set].get(), pf, fail.get(), sat.get(), s, max_ctas,
+                    ctr(s, 3), L + off + ndp + nlo + (in_bf ? 1 : 0), nbf - (in_bf ? 1 : 0));
+    if (xsend_cnt[k]) {
+      const int64_t skip = mine1 ? 1 : 0;
+      if (xsend_cnt[k] > skip) {
+        k_panel_pack<<<dim3(gx, static_cast<unsigned>(xsend_cnt[k] - skip)), 256, 0, s>>>(
+            store(), k, xsend.get() + xsend_off[k] + skip, xsoffs.get() + xsend_off[k] + skip, own, fail.get());
+        SPH_LAUNCH_CHECK();
+      }
+      stream_write(s, xsync.get(), ep);
+    }
+    prof_end(pp, s);
+    SPH_CUDA(cudaEventRecord(ev_trdone, s));
+    // pulls, import and acknowledgements off the chain
+    SPH_CUDA(cudaStreamWaitEvent(xstream, ev_trdone, 0));
+    const int px = prof_begin(kXchg, xstream);
+    for (const Xfer& x : xroots[k]) {
+      if (x.peer == rank) continue;
+      stream_wait_geq(xstream, peer_sync[x.peer], ep);
+      SPH_CUDA(cudaMemcpyAsync(own + x.pos, peer_xbuf[x.peer] + par + x.pos, static_cast<size_t>(x.bytes),
+                               cudaMemcpyDeviceToDevice, xstream));
+    }
+    note_launch();
+    if (ilist_cnt[k]) {
+      const int64_t skip = (d1 == rank && o1 != rank) ? 1 : 0;  // imported early already
+      if (ilist_cnt[k] > skip) {
+        k_panel_import<<<dim3(gx, static_cast<unsigned>(ilist_cnt[k] - skip)), 256, 0, xstream>>>(
+            store(), k, ilists.get() + ilist_off[k] + skip, ioffs.get() + ilist_off[k] + skip, own, p64_[set].get(),
+            tensor ? pf.tf32_hi() : nullptr, tensor ? pf.tf32_lo() : nullptr, tensor ? pf.half16() : nullptr,
+            (tensor && pf.f16x3) ? pf.h_hi.get() : nullptr, (tensor && pf.f16x3) ? pf.h_lo.get() : nullptr,
+            rowexp.get(), cfg.hp_format, d_import_need.get(), fail.get());
+        SPH_LAUNCH_CHECK();
+      }
+    }
+    if (d1 != rank) oz_slice_next(k, xstream);
+    for (int q = 0; q < W; ++q)
+      if (q != rank) stream_write(xstream, peer_sync[q] + 1 + rank, ep);
+    prof_end(px, xstream);
+    xlate[k] = 1;
+    if (s != pstream) {  // no lookahead: the caller's stream sees the whole panel
+      SPH_CUDA(cudaEventRecord(ev_xdone, xstream));
+      SPH_CUDA(cudaStreamWaitEvent(s, ev_xdone, 0));
+      xlate[k] = 0;
+    }
+  }
+
   void op_panel_dist(int k, cudaStream_t s, int max_ctas = 0) {
     const int set = set_of(k);
+    static const bool early = [] {
+      const char* e = std::getenv("SPHEMU_XCHG_EARLY");
+      return !(e && e[0] == '0');
+    }();
+    if (xipc && early && xstream) {
+      op_panel_dist_early(k, s, max_ctas);
+      return;
+    }
     if (xchunks > 1 && xstream && cfg.compute == SPHEMU_COMPUTE_TENSOR && !panel_bf) {
       op_panel_dist_chunked(k, s, max_ctas);
       return;
@@ -2071,7 +2204,7 @@ struct Chol {
       SPH_CUDA(cudaStreamWaitEvent(pstream, ev_start_p, 0));
       op_potrf_dist(0, pstream);
       op_panel_dist(0, pstream);
-      SPH_CUDA(cudaEventRecord(ev_panel[0], pstream));
+      record_panel(0);
       for (int k = 0; k + 1 < nt; ++k) {
         if (k > 0) SPH_CUDA(cudaStreamWaitEvent(pstream, ev_bulk[k - 1], 0));
         reserve = (nt - 1 - k > tail) ? reserve_early : reserve_late;
@@ -2085,11 +2218,15 @@ struct Chol {
           SPH_CUDA(cudaStreamWaitEvent(pstream, ev_colrest[k], 0));
           op_panel_dist(k + 1, pstream);
         }
-        SPH_CUDA(cudaEventRecord(ev_panel[k + 1], pstream));
+        record_panel(k + 1);
         op_update(k, 1, stream, std::max(1, num_sms() - reserve));
         SPH_CUDA(cudaEventRecord(ev_bulk[k], stream));
       }
       SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[nt - 1], 0));
+    }
+    if (xstream) {  // the last exchange's acknowledgements are part of the factorization
+      SPH_CUDA(cudaEventRecord(ev_xdone, xstream));
+      SPH_CUDA(cudaStreamWaitEvent(stream, ev_xdone, 0));
     }
     SPH_NCCL(ncclAllReduce(sat.get(), sat.get(), 1, ncclUint32, ncclSum, comm, stream));
   }

@@ -30,7 +30,7 @@ def test_workload_choice():
     a = types.SimpleNamespace(workload=None)
     assert bench.pick_workload(a, 1)["n"] == 32400
     assert bench.pick_workload(a, 4)["n"] == 129600
-    assert bench.GRIDS[4] == (4, 1) and bench.GRIDS[8] == (8, 1)
+    assert bench.GRIDS[4] == (2, 2) and bench.GRIDS[8] == (4, 2)
 
 
 def test_roofline_assembly_for_both_workloads():
