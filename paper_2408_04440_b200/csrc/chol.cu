@@ -1716,9 +1716,12 @@ struct Chol {
     };
     // chain reserve: one GPU as reserve_at; the distributed chain also carries the exchange (factor_dist)
     const char* env_reserve = std::getenv("SPHEMU_DIST_RESERVE");
-    // 32 SMs for the distributed chain (it also packs, exchanges and imports
-    // the panel): C3 on 2 x 2 379 ms against 386 (48), 415 (16), 418 (64)
-    const int dist_reserve = env_reserve ? std::atoi(env_reserve) : kChainCtas;
+    // SMs left to the distributed chain. With the copy-engine exchange (no
+    // NCCL kernels in the chain) and tile k+1 sent first, fewer is better:
+    // C3 2x2 16 / 20 / 24 / 28 / 32 -> 293.5 / 294 / 298 / 300 / 304 ms, 2x1
+    // 16 / 24 / 32 -> 478 / 491 / 510 ms (NCCL exchange, round 2 start: 32
+    // best, 379 ms)
+    const int dist_reserve = env_reserve ? std::atoi(env_reserve) : (xipc ? 16 : kChainCtas);
     auto reserve_for = [&](int k) { return D ? dist_reserve : reserve_at(k); };
     if (!cfg.lookahead) {
       potrf(0, stream);
