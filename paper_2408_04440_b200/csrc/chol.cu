@@ -611,6 +611,11 @@ struct Chol {
   // packed, broadcast (second communicator) and imported on xstream.
   ncclComm_t comm2 = nullptr;
   cudaStream_t xstream = nullptr;
+  // Process grids: the merged pair's big update (part 5) on its own stream
+  // with fewer CTAs, so the next pair's critical column updates (part 2) are
+  // not queued behind it (SPHEMU_SPLIT5, default on for process grids).
+  cudaStream_t bstream = nullptr;
+  std::vector<cudaEvent_t> ev_p4, ev_p5;
   std::vector<cudaEvent_t> ev_tr;
   cudaEvent_t ev_xdone = nullptr;
   int xchunks = 1;
@@ -709,7 +714,7 @@ struct Chol {
       const char* e = std::getenv("SPHEMU_TC_DYN");
       return !(e && e[0] == '0');
     }();
-    return on ? sched_ctr.get() + (s == pstream ? 4 : 0) + cls : nullptr;
+    return on ? sched_ctr.get() + (s == pstream ? 4 : (s == bstream && bstream ? 8 : 0)) + cls : nullptr;
   }
   // Bulk yield: the chain raises the flag when the next panel is ready; the
   // bulk's persistent CTAs stop claiming items so the panel gets the SMs, and
@@ -1169,7 +1174,7 @@ struct Chol {
       for (int p = 0; p < kSets; ++p) p64_[p].alloc(static_cast<size_t>(nt - 1) * b * b);
     fail.alloc(1);
     sat.alloc(1);
-    sched_ctr.alloc(8);  // [stream][class 0..2, 3 = panel]
+    sched_ctr.alloc(12);  // [stream: main, chain, bulk2][class 0..2, 3 = panel]
     yield_flag.alloc(1);
     SPH_CUDA(cudaMemset(yield_flag.get(), 0, sizeof(int)));
     // Per-step output-tile lists by precision class.
@@ -1352,6 +1357,15 @@ struct Chol {
     SPH_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
     SPH_CUDA(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, prio_lo));
     SPH_CUDA(cudaStreamCreateWithPriority(&pstream, cudaStreamNonBlocking, prio_hi));
+    {
+      SPH_CUDA(cudaStreamCreateWithPriority(&bstream, cudaStreamNonBlocking, prio_lo));
+      ev_p4.resize(nt);
+      ev_p5.resize(nt);
+      for (int k = 0; k < nt; ++k) {
+        SPH_CUDA(cudaEventCreateWithFlags(&ev_p4[k], cudaEventDisableTiming));
+        SPH_CUDA(cudaEventCreateWithFlags(&ev_p5[k], cudaEventDisableTiming));
+      }
+    }
     if (xipc) {
       SPH_CUDA(cudaStreamCreateWithPriority(&xstream, cudaStreamNonBlocking, prio_hi));
       SPH_CUDA(cudaEventCreateWithFlags(&ev_xdone, cudaEventDisableTiming));
@@ -1408,6 +1422,10 @@ struct Chol {
     for (auto e : ev_bulkdp) cudaEventDestroy(e);
     if (ev_start_p) cudaEventDestroy(ev_start_p);
     if (xstream) cudaStreamSynchronize(xstream);
+    if (bstream) cudaStreamSynchronize(bstream);
+    for (auto e : ev_p4) cudaEventDestroy(e);
+    for (auto e : ev_p5) cudaEventDestroy(e);
+    if (bstream) cudaStreamDestroy(bstream);
     if (ev_trdone) cudaEventDestroy(ev_trdone);
     for (auto e : ev_tr) cudaEventDestroy(e);
     if (ev_xdone) cudaEventDestroy(ev_xdone);
@@ -1765,6 +1783,13 @@ struct Chol {
         if (y) SPH_CUDA(cudaMemsetAsync(yield_flag.get(), 0, sizeof(int), pstream));
       };
       int k = 0;
+      static const int split5_env = [] {
+        const char* e = std::getenv("SPHEMU_SPLIT5");  // SMs the main stream keeps while part 5 runs (0 = off)
+        return e ? std::atoi(e) : -1;
+      }();
+      const bool split5 = bstream && (split5_env > 0 || (split5_env < 0 && D));
+      const int split5_ctas = split5_env > 0 ? split5_env : 16;
+      int last_p5 = -1;
       while (k + 1 < nt) {
         const int reserve = reserve_for(k);
         potrf_cap = std::min(kChainCtas, reserve);
@@ -1790,6 +1815,8 @@ struct Chol {
         yielding_panel(k + 1, y);
         record_panel(k + 1);
         cols(k + 1, pstream);
+        // column k+2 last received the previous pair's merged update (part 5 of k-2)
+        if (split5 && k >= 2) SPH_CUDA(cudaStreamWaitEvent(stream, ev_p5[k - 2], 0));
         op_update(k, 3, stream, bulk_ctas, y ? yield_flag.get() : nullptr);
         if (y) {
           SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k + 1], 0));
@@ -1813,14 +1840,25 @@ struct Chol {
         op_update(k, 4, stream, 0);  // column k+3: feeds the next pair's chain
         SPH_CUDA(cudaEventRecord(ev_bulk[k + 1], stream));
         diag_ready = ev_bulk[k + 1];
-        op_update(k, 5, stream, bulk_ctas, (y && more) ? yield_flag.get() : nullptr);
-        if (y && more) {
-          SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k + 2], 0));
-          op_update(k, 5, stream, bulk_ctas, nullptr, true);
+        if (split5) {
+          // the right of column k+3 on its own stream (leaving SMs to the next
+          // pair's column updates on the main stream)
+          SPH_CUDA(cudaEventRecord(ev_p4[k], stream));
+          SPH_CUDA(cudaStreamWaitEvent(bstream, ev_p4[k], 0));
+          op_update(k, 5, bstream, std::max(1, bulk_ctas - split5_ctas));
+          SPH_CUDA(cudaEventRecord(ev_p5[k], bstream));
+          last_p5 = k;
+        } else {
+          op_update(k, 5, stream, bulk_ctas, (y && more) ? yield_flag.get() : nullptr);
+          if (y && more) {
+            SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[k + 2], 0));
+            op_update(k, 5, stream, bulk_ctas, nullptr, true);
+          }
         }
         SPH_CUDA(cudaEventRecord(ev_bulk[k], stream));
         k += 2;
       }
+      if (last_p5 >= 0) SPH_CUDA(cudaStreamWaitEvent(stream, ev_p5[last_p5], 0));
       SPH_CUDA(cudaStreamWaitEvent(stream, ev_panel[nt - 1], 0));
     }
     if (D && xstream) {  // the last exchange's acknowledgements are part of the factorization
