@@ -183,7 +183,7 @@ def workload_config(wl, args, world):
             "make_spd_test_matrix generated into the tiles at storage precision, factor")
     return {"workload": wl["desc"], "N": n, "tile_size": wl["tile"], "variant": wl["variant"],
             "hp_format": wl["hp"], "sp_compute": args.sp_compute, "lookahead": args.lookahead,
-            "parallelism": f"2D block-cyclic {grid[0]}x{grid[1]} (NCCL panel broadcasts)" if world > 1
+            "parallelism": f"2D block-cyclic {grid[0]}x{grid[1]} (copy-engine panel exchange over NVLink)" if world > 1
             else "single GPU", "step": step,
             "l2": f"tiles {8 * n * n / 2 / 1e9 / world:.1f}+ GB per GPU >> 126 MB L2, no flush needed"}
 
@@ -353,13 +353,16 @@ def time_factor(sph, h, wl, args, world, a_dev=None, steps=None, warmup=None, cl
     warmup = args.warmup if warmup is None else warmup
     lib = sph._sphemu.lib()
 
-    def step():
+    def step(sync=True):
+        # steps are enqueued back to back (the handle orders a factorization
+        # after the previous one on all of its streams); the host waits once
+        # after the loop instead of idling the GPU between steps
         if a_dev is not None:
             h.load(a_dev.data_ptr(), where=sph._sphemu.DEVICE, lda=wl["n"])
         else:
             h.generate_spd(1)
         h.factor()
-        return h.wait()
+        return h.wait() if sync else None
 
     # Inside the timed region only the dominant update class is bracketed by
     # CUDA events (the roofline's achieved rate); the full phase breakdown
@@ -368,8 +371,8 @@ def time_factor(sph, h, wl, args, world, a_dev=None, steps=None, warmup=None, cl
     clocks = ClockSampler(clocks_index) if clocks_index is not None else None
     if clocks:
         clocks.__enter__()
-    for _ in range(warmup):
-        step()
+    for w in range(warmup):
+        step(sync=(w == warmup - 1))
     h.reset_phase_times()
     launches0 = lib.sphemu_gpu_launch_count()
     barrier(world)
@@ -378,8 +381,8 @@ def time_factor(sph, h, wl, args, world, a_dev=None, steps=None, warmup=None, cl
     if clocks:
         clocks.mark_start()
     start.record()
-    for _ in range(steps):
-        st = step()
+    for i in range(steps):
+        st = step(sync=(i == steps - 1))
     end.record()
     torch.cuda.synchronize()
     if clocks:
