@@ -1453,6 +1453,9 @@ struct Chol {
     const int pl = prof_begin(kLoad);
     if (where == SPHEMU_HOST) {
       load_host(a, lda, diag_shift);
+    } else if (n % 8 == 0 && lb % 8 == 0 && lda % 2 == 0 && reinterpret_cast<uintptr_t>(a) % 16 == 0) {
+      k_load_dense8<<<tile_grid(), 256, 0, stream>>>(store(), a, lda, sat.get(), diag_shift);
+      SPH_LAUNCH_CHECK();
     } else {
       k_load_dense<<<tile_grid(), 256, 0, stream>>>(store(), a, lda, sat.get(), 0, 0, diag_shift);
       SPH_LAUNCH_CHECK();
@@ -1461,7 +1464,8 @@ struct Chol {
     SPH_LAUNCH_CHECK();
     if (dist()) SPH_NCCL(ncclAllReduce(rowexp.get(), rowexp.get(), n, ncclInt32, ncclMax, comm, stream));
     prof_end(pl);
-    SPH_CUDA(cudaStreamSynchronize(stream));
+    // device input: stream-ordered with the factorization, no host wait
+    if (where == SPHEMU_HOST) SPH_CUDA(cudaStreamSynchronize(stream));
   }
 
   void generate_spd(uint64_t seed, double rho = 0.9);

@@ -201,3 +201,22 @@ def test_sp_class_compute_modes(sph, O, n, b, sp_compute):
     r_gpu, r_ref = O.relative_residual(a, f), O.relative_residual(a, ref)
     assert r_gpu <= max(2 * r_ref, THRESH["dpsp"]), (r_gpu, r_ref)
     assert np.abs(f - ref).max() < 1e-5
+
+
+@pytest.mark.parametrize("variant,hp,n,b", [("dpsp", "fp16", 1000, 256), ("dpsphp", "bf16", 1536, 512),
+                                            ("dphp", "fp16", 777, 128)])
+def test_device_load_matches_host_load(sph, variant, hp, n, b):
+    """Tiling a device-resident dense input (the vectorized k_load_dense8 when
+    n and the tile size are multiples of 8, the scalar kernel otherwise) stores
+    exactly what the host-buffer path stores, saturation counts included."""
+    import torch
+    rng = np.random.default_rng(4)
+    a = rng.standard_normal((n, n)) * 3e4  # some entries overflow binary16
+    a = 0.5 * (a + a.T)
+    h1 = sph.Cholesky(n, variant, tile_size=b, hp_format=hp)
+    h1.load(a)
+    h2 = sph.Cholesky(n, variant, tile_size=b, hp_format=hp)
+    t = torch.from_numpy(a).cuda()
+    h2.load(t.data_ptr(), where=sph._sphemu.DEVICE, lda=n)
+    torch.cuda.synchronize()
+    assert np.array_equal(h1.factor_dense_unfactored(), h2.factor_dense_unfactored())
