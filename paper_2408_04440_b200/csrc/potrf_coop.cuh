@@ -80,6 +80,48 @@ __device__ __noinline__ void pc_base16(PcSmallSmem& s, int o, int w, int lane) {
     for (int r = 0; r < 16; ++r) s.Di[o + r][o + lane] = x[r];
 }
 
+// 32 x 32 base case on one warp (lane = row): the same right-looking,
+// next-pivot-first shuffle scheme as pc_base16 over 32 columns, then the
+// inverse by forward substitution (lane j owns column j, L read back from
+// s.T with broadcast loads). Replaces the 16-wide recursion level (two 16 x 16
+// bases + four 16-wide products, each behind a CTA barrier): one warp, no
+// barriers, 32 rsqrt-bound column steps.
+__device__ __noinline__ void pc_base32(PcSmallSmem& s, int o, int w, int lane) {
+  double a[32], rl[32];
+#pragma unroll
+  for (int t = 0; t < 32; ++t) a[t] = s.T[o + lane][o + t];
+  bool ok = true;
+  double piv = __shfl_sync(0xffffffffu, a[0], 0);
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    if (c < w && !(piv > 0.0)) ok = false;
+    rl[c] = rsqrt(piv);
+    const double lrc = (lane == c) ? piv * rl[c] : a[c] * rl[c];
+    a[c] = lrc;
+    if (c + 1 < 32) piv = __shfl_sync(0xffffffffu, fma(-lrc, lrc, a[c + 1]), c + 1);
+#pragma unroll
+    for (int j = c + 1; j < 32; ++j) a[j] = fma(-lrc, __shfl_sync(0xffffffffu, lrc, j), a[j]);
+  }
+  if (!ok) {
+    if (lane == 0) s.bad = 1;
+    return;
+  }
+#pragma unroll
+  for (int t = 0; t < 32; ++t) s.T[o + lane][o + t] = t <= lane ? a[t] : 0.0;
+  __syncwarp();
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    x[r] *= rl[r];
+#pragma unroll
+    for (int i = r + 1; i < 32; ++i) x[i] -= s.T[o + i][o + r] * x[r];
+  }
+#pragma unroll
+  for (int r = 0; r < 32; ++r) s.Di[o + r][o + lane] = x[r];
+}
+
 // out(r, c, sum_t a(r, t) b(t, c)) for an N x N product on the whole CTA
 // (128 threads); each thread keeps one row of a in registers. All reads
 // finish (barrier) before any write, so in-place updates are safe.
@@ -139,10 +181,16 @@ __device__ __forceinline__ void pc_mm_t(FA fa, FB fb, FO fo) {
 // L22, inv22 | inv21 = -inv22 (L21 inv11).
 // Not inlined: the two calls per level share one copy of the code (the
 // cooperative kernel is large enough for instruction fetch to matter).
+#ifndef PC_BASE32
+#define PC_BASE32 0  // measured slower: chol_inv<32> 5.65 vs 5.0 us (the per-column shuffle chain is ~250 cycles either way)
+#endif
 template <int H>
 __device__ __noinline__ void pc_chol_inv(PcSmallSmem& s, int o, int w) {
   if constexpr (H == 16) {
     if ((threadIdx.x >> 5) == 0) pc_base16(s, o, w, threadIdx.x & 31);
+    __syncthreads();
+  } else if constexpr (H == 32 && PC_BASE32) {
+    if ((threadIdx.x >> 5) == 0) pc_base32(s, o, w, threadIdx.x & 31);
     __syncthreads();
   } else {
     constexpr int N = H / 2;
