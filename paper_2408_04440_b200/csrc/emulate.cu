@@ -175,7 +175,15 @@ void emulate_core(const EmulArgs& a, const XiFn& xi_fn) {
   // column the normals of every rank (8 d W), the innovations and the
   // tiled product's padded operands (~32 d), the kept draws, fields and eps.
   const int64_t col_bytes = (int64_t)d * (8 * W + 32) + points * 8 * 2;
-  const int64_t budget = a.chunk_bytes > 0 ? a.chunk_bytes : (int64_t{8} << 30);
+  // default chunk budget: half of the free HBM, at most 32 GB (each chunk re-reads the whole factor, and the
+  // TRMM's 256-snapshot blocks fill better with more columns per chunk)
+  int64_t budget = a.chunk_bytes;
+  if (budget <= 0) {
+    size_t fr = 0, tot = 0;
+    budget = (cudaMemGetInfo(&fr, &tot) == cudaSuccess && fr > 0)
+                 ? std::min<int64_t>(int64_t{32} << 30, std::max<int64_t>(int64_t{1} << 30, (int64_t)(fr / 2)))
+                 : (int64_t{8} << 30);
+  }
   const int rc = (int)std::max<int64_t>(1, std::min<int64_t>(cnt_max, budget / std::max<int64_t>(1, col_bytes * steps)));
   const int n_chunks = (cnt_max + rc - 1) / rc;
   const int64_t ymax = (int64_t)rc * a.t_out * points;
