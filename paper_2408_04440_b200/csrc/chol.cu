@@ -698,6 +698,8 @@ struct Chol {
   // FP64 mirror the import rebuilt (imported tiles are not in the arena).
   const double* oz_src(int k) { return dist() ? p64_[set_of(k)].get() : nullptr; }
   DevBuf<double> dinv, spd_d, spd_pw;
+  uint64_t spd_seed = 0;
+  double spd_rho = -1.0;  // (seed, rho) of the factors in spd_d / spd_pw
   DevBuf<int> rowexp;  // per-row power-of-two operand scale (FP16x3 SP path)
   DevBuf<int> fail;
   DevBuf<unsigned> sat;
@@ -2653,19 +2655,28 @@ struct Chol {
 // does (GaussianRng uniform -> exp, std::pow(0.9, k)), matrix built on device.
 void Chol::generate_spd(uint64_t seed, double rho) {
   factored = false;
-  std::vector<double> d(n), pw(n);
-  host_spd_factors(n, seed, d.data(), pw.data(), rho);
-  spd_d.alloc(n);
-  spd_pw.alloc(n);
-  SPH_CUDA(cudaMemcpyAsync(spd_d.get(), d.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream));
-  SPH_CUDA(cudaMemcpyAsync(spd_pw.get(), pw.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream));
+  // d_i and rho^k (host mt19937_64 + exp / pow, as the reference) are
+  // recomputed and uploaded only when (seed, rho) change; the generation
+  // itself is stream-ordered with the factorization (no host wait)
+  if (spd_d.n != static_cast<size_t>(n) || seed != spd_seed || rho != spd_rho) {
+    std::vector<double> d(n), pw(n);
+    host_spd_factors(n, seed, d.data(), pw.data(), rho);
+    if (spd_d.n != static_cast<size_t>(n)) {
+      spd_d.alloc(n);
+      spd_pw.alloc(n);
+    }
+    SPH_CUDA(cudaMemcpyAsync(spd_d.get(), d.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream));
+    SPH_CUDA(cudaMemcpyAsync(spd_pw.get(), pw.data(), n * sizeof(double), cudaMemcpyHostToDevice, stream));
+    SPH_CUDA(cudaStreamSynchronize(stream));  // the host vectors go out of scope
+    spd_seed = seed;
+    spd_rho = rho;
+  }
   reset_flags();
   k_gen_spd<<<tile_grid(), 256, 0, stream>>>(store(), spd_d.get(), spd_pw.get(), sat.get());
   SPH_LAUNCH_CHECK();
   k_rowexp<<<ceil_div(n, 256), 256, 0, stream>>>(store(), rowexp.get());
   SPH_LAUNCH_CHECK();
   if (dist()) SPH_NCCL(ncclAllReduce(rowexp.get(), rowexp.get(), n, ncclInt32, ncclMax, comm, stream));
-  SPH_CUDA(cudaStreamSynchronize(stream));
 }
 
 }  // namespace sphemu_gpu
