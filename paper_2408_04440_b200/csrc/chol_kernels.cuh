@@ -54,9 +54,7 @@ static __global__ void k_gen_spd(TileStore ts, const double* __restrict__ d, con
   const int p = ts.tprec(i, j);
   const int b = ts.b;
   unsigned local = 0;
-  for (int64_t e = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; e < (int64_t)b * b;
-       e += (int64_t)gridDim.y * blockDim.x) {
-    const int r = (int)(e / b), c = (int)(e % b);
+  auto value = [&](int r, int c) {
     const int R = i * ts.lb + r, Cc = j * ts.lb + c;
     double v = 0.0;
     if (r < ts.lb && c < ts.lb && R < ts.n && Cc < ts.n) {
@@ -64,7 +62,37 @@ static __global__ void k_gen_spd(TileStore ts, const double* __restrict__ d, con
       else if (R > Cc) v = __dmul_rn(__dmul_rn(__dmul_rn(d[R], d[Cc]), 0.25), pw[R - Cc]);
       else v = __dmul_rn(__dmul_rn(__dmul_rn(d[Cc], d[R]), 0.25), pw[Cc - R]);
     }
-    store_elem(tp, p, e, v, local);
+    return v;
+  };
+  if ((b & 7) == 0) {
+    // 8 consecutive elements of a row per thread: one 16 / 32 / 64-byte store
+    for (int64_t g = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; g < (int64_t)b * b / 8;
+         g += (int64_t)gridDim.y * blockDim.x) {
+      const int64_t e = g * 8;
+      const int r = (int)(e / b), c = (int)(e % b);
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = value(r, c + u);
+      if (p == kDP) {
+        double2* q = reinterpret_cast<double2*>(static_cast<double*>(tp) + e);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) q[u] = make_double2(v[2 * u], v[2 * u + 1]);
+      } else if (p == kSP) {
+        float4* q = reinterpret_cast<float4*>(static_cast<float*>(tp) + e);
+        q[0] = make_float4(__double2float_rn(v[0]), __double2float_rn(v[1]), __double2float_rn(v[2]), __double2float_rn(v[3]));
+        q[1] = make_float4(__double2float_rn(v[4]), __double2float_rn(v[5]), __double2float_rn(v[6]), __double2float_rn(v[7]));
+      } else {
+        uint16_t h[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          h[u] = p == kHP ? __half_as_ushort(to_half_sat(v[u], local)) : __bfloat16_as_ushort(to_bf16_sat(v[u], local));
+        *reinterpret_cast<uint4*>(static_cast<uint16_t*>(tp) + e) = *reinterpret_cast<const uint4*>(h);
+      }
+    }
+  } else {
+    for (int64_t e = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; e < (int64_t)b * b;
+         e += (int64_t)gridDim.y * blockDim.x)
+      store_elem(tp, p, e, value((int)(e / b), (int)(e % b)), local);
   }
   flush_sat(local, sat);
 }
