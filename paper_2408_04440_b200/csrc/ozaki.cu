@@ -52,6 +52,14 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t a, uint64_t b,
       "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(kOzIdesc), "r"(acc));
 }
+constexpr uint32_t kOzIdesc128 =
+    (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(128 >> 3) << 17) | (static_cast<uint32_t>(OZ_BM >> 4) << 24);
+__device__ __forceinline__ void umma_i8_n128(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kOzIdesc128), "r"(acc));
+}
 __device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
@@ -384,6 +392,231 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   if (warp == 2) tmem_dealloc(tmem, 512);
 }
 
+// Wide form (SPHEMU_OZ_BN=128): 128 x 128 output blocks and N = 128 MMAs
+// (4.58 TOPS against 3.05 at N = 64), the eight diagonals in two passes of
+// four TMEM accumulators (128 columns each): pass 0 folds C_0..C_3 from
+// digits 0-3 only (10 pairs, 32 KB stages), pass 1 C_4..C_7 from all digits
+// (26 pairs, 64 KB stages); each pass's epilogue subtracts its partial sum
+// from the FP64 tile (two read-modify-writes per block, both exact-order
+// FP64). Each accumulator is released as soon as both 32-column halves of
+// its rows are in registers.
+constexpr int OZW_BN = 128;
+constexpr int OZW_BOX = 128 * 128;  // 16 KB: 128 rows x 128 digit bytes
+constexpr int OZW_STAGE = 4 * OZW_BOX;
+constexpr int OZW_STAGES = 3;
+constexpr int OZW_SMEM = OZW_STAGES * OZW_STAGE + 1024 + 256;
+
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    k_oz_update_w(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mA2, const OzArgs args) {
+  extern __shared__ __align__(1024) uint8_t ozw_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ozw_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZW_STAGES * OZW_STAGE);
+  uint64_t* empty = full + OZW_STAGES;
+  uint64_t* tfull = empty + OZW_STAGES;
+  uint64_t* tempty = tfull + 1;  // [4] accumulator slot drained
+  uint64_t* sfull = tempty + 4;
+  uint64_t* sempty = sfull + 4;
+  int* sched = reinterpret_cast<int*>(sempty + 4);
+  uint32_t* holder = reinterpret_cast<uint32_t*>(sched + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ int s_fail;
+  if (threadIdx.x == 0) s_fail = *(volatile const int*)args.fail;
+  __syncthreads();
+  if (s_fail >= 0) return;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZW_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    for (int x = 0; x < 4; ++x) mbar_init(&tempty[x], OZ_EPI);
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&sfull[s], 1);
+      mbar_init(&sempty[s], 1 + OZ_EPI);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mA);
+    if (args.k2 >= 0) tma_prefetch(&mA2);
+  }
+  if (warp == 2) tmem_alloc(holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *holder;
+  const int b = args.ts.b;
+  const int kblocks = b / 32;
+  const int halves = args.k2 >= 0 ? 2 : 1;
+  auto decode = [&](int64_t w, int& i, int& j, int& r0, int& c0) {
+    const int2 ij = args.list[w / args.per];
+    const int sub = static_cast<int>(w % args.per);
+    i = ij.x;
+    j = ij.y;
+    r0 = (sub / args.subn) * OZ_BM;
+    c0 = (sub % args.subn) * OZW_BN;
+  };
+  auto ring_take = [&](int64_t n) -> int64_t {
+    const int slot = static_cast<int>(n & 3);
+    mbar_wait(&sfull[slot], static_cast<uint32_t>((n >> 2) & 1));
+    return static_cast<int64_t>(*(volatile int*)&sched[slot]);
+  };
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t keep = l2_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      int64_t snext = blockIdx.x;
+      auto claim = [&]() -> int64_t {
+        for (;;) {
+          int64_t w;
+          if (args.counter) {
+            w = atomicAdd(args.counter, 1);
+          } else {
+            w = snext;
+            snext += gridDim.x;
+          }
+          if (w >= args.items) return -1;
+          int i, j, r0, c0;
+          decode(w, i, j, r0, c0);
+          if (!(i == j && c0 >= r0 + OZ_BM)) return w;
+        }
+      };
+      for (int64_t n = 0;; ++n) {
+        const int64_t w = claim();
+        const int slot = static_cast<int>(n & 3);
+        mbar_wait(&sempty[slot], static_cast<uint32_t>(((n >> 2) & 1) ^ 1));
+        sched[slot] = static_cast<int>(w);
+        mbar_arrive(&sfull[slot]);
+        if (w < 0) break;
+        int i, j, r0, c0;
+        decode(w, i, j, r0, c0);
+        for (int pass = 0; pass < 2; ++pass)
+          for (int kb2 = 0; kb2 < kblocks * halves; ++kb2) {
+            const int hf = kb2 >= kblocks ? 1 : 0, kb = kb2 - hf * kblocks;
+            const int kk = hf ? args.k2 : args.k;
+            const CUtensorMap* ma = hf ? &mA2 : &mA;
+            const int a_row = (i - kk - 1) * b + r0, b_row = (j - kk - 1) * b + c0;
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* st = smem + stage * OZW_STAGE;
+            mbar_arrive_expect_tx(&full[stage], pass ? OZW_STAGE : 2 * OZW_BOX);
+            const int x = kb * 128;
+            // layout: A digits 0-3, B digits 0-3, A digits 4-7, B digits 4-7
+            tma_load_2d_hint(ma, &full[stage], st, x, a_row, keep);
+            tma_load_2d_hint(ma, &full[stage], st + OZW_BOX, x, b_row, keep);
+            if (pass) {
+              tma_load_2d_hint(ma, &full[stage], st + 2 * OZW_BOX, x + 64, a_row, keep);
+              tma_load_2d_hint(ma, &full[stage], st + 3 * OZW_BOX, x + 64, b_row, keep);
+            }
+            if (++stage == OZW_STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+      }
+    }
+  } else if (warp == 1) {
+    int stage = 0;
+    uint32_t phase = 0, pass_phase = 0;
+    for (int64_t n = 0;; ++n) {
+      const int64_t w = ring_take(n);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[n & 3]);
+      if (w < 0) break;
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int kb2 = 0; kb2 < kblocks * halves; ++kb2) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          uint8_t* st = smem + stage * OZW_STAGE;
+          const uint64_t a0 = umma_desc_sw128(st), b0 = umma_desc_sw128(st + OZW_BOX);
+          const uint64_t a1 = umma_desc_sw128(st + 2 * OZW_BOX), b1 = umma_desc_sw128(st + 3 * OZW_BOX);
+#pragma unroll
+          for (int s = 0; s < OZ_DIGITS; ++s) {
+            const uint64_t ad = (s < 4 ? a0 : a1) + 2 * (s & 3);
+#pragma unroll
+            for (int t = 0; t + s < OZ_DIGITS; ++t) {
+              const int d = s + t;
+              if ((d >> 2) != pass) continue;
+              if (kb2 == 0 && s == 0) {  // first touch of slot d & 3 in this pass
+                mbar_wait(&tempty[d & 3], pass_phase ^ 1);
+                tc_fence_after();
+              }
+              const uint64_t bd = (t < 4 ? b0 : b1) + 2 * (t & 3);
+              umma_i8_n128(tmem + (d & 3) * OZW_BN, ad, bd, (kb2 > 0 || s > 0) ? 1u : 0u);
+            }
+          }
+          umma_commit_elect(&empty[stage]);
+          if (++stage == OZW_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_elect(tfull);
+        pass_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // two warps per TMEM lane quarter, 64 columns each, in two 32-column halves
+    const int q = warp & 3;
+    const int cbase = ((warp - 4) >> 2) * 64;
+    const int row = q * 32 + lane;
+    uint32_t pass_phase = 0;
+    const TileStore& ts = args.ts;
+    for (int64_t n = 0;; ++n) {
+      int64_t w = -1;
+      if (lane == 0) {
+        w = ring_take(n);
+        mbar_arrive(&sempty[n & 3]);
+      }
+      w = __shfl_sync(0xffffffffu, static_cast<int>(w), 0);
+      if (w < 0) break;
+      int i, j, r0, c0;
+      decode(w, i, j, r0, c0);
+      const double si = pow2(oz_mu(args.rowexp, min(i * ts.lb + r0 + row, ts.n - 1)));
+      for (int pass = 0; pass < 2; ++pass) {
+        while (!mbar_try(tfull, pass_phase)) __nanosleep(128);
+        tc_fence_after();
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          double v[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) v[c] = 0.0;
+#pragma unroll 1
+          for (int x = 0; x < 4; ++x) {
+            uint32_t xv[32];
+            tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + x * OZW_BN + cbase + h * 32, xv);
+            if (h == 1) {  // both halves of slot x are read: back to the MMA warp
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tempty[x]);
+            }
+            const double wgt = pow2(-7 * (4 * pass + x + 2));
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] = fma(static_cast<double>(static_cast<int>(xv[c])), wgt, v[c]);
+          }
+          const int cb = c0 + cbase + h * 32;
+          double2* cp = reinterpret_cast<double2*>(static_cast<double*>(ts.tile(i, j)) + static_cast<int64_t>(r0 + row) * b + cb);
+#pragma unroll
+          for (int c2 = 0; c2 < 16; ++c2) {
+            const int cg = j * ts.lb + cb + 2 * c2;
+            const double s0 = si * pow2(oz_mu(args.rowexp, min(cg, ts.n - 1)));
+            const double s1 = si * pow2(oz_mu(args.rowexp, min(cg + 1, ts.n - 1)));
+            double2 cur = cp[c2];
+            cur.x -= v[2 * c2] * s0;
+            cur.y -= v[2 * c2 + 1] * s1;
+            cp[c2] = cur;
+          }
+        }
+        pass_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, 512);
+}
+
 }  // namespace
 
 void OzSlices::alloc(int64_t rows_, int b_) {
@@ -433,12 +666,27 @@ void oz_update(const TileStore& ts, int k, const int2* list, int64_t cnt, const 
     return e ? std::atoi(e) : 0;
   }();
   a.dbg = dbg;
-  smem_optin(reinterpret_cast<const void*>(k_oz_update), OZ_SMEM);
+  static const int bn = [] {
+    const char* e = std::getenv("SPHEMU_OZ_BN");
+    return e ? std::atoi(e) : 64;
+  }();
+  const bool wide = bn == 128 && ts.b % 128 == 0 && dbg == 0;
+  if (wide) {
+    a.subn = ts.b / 128;
+    a.per = (ts.b / OZ_BM) * a.subn;
+    a.items = cnt * a.per;
+  }
   if (counter) SPH_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), s));
   const int cap = max_ctas > 0 ? std::min(max_ctas, num_sms()) : num_sms();
   const int grid = static_cast<int>(std::min<int64_t>(a.items, std::max(1, cap)));
   const OzSlices& o2 = a.k2 >= 0 ? *oz2 : oz;
-  k_oz_update<<<grid, OZ_THREADS, OZ_SMEM, s>>>(oz.m_a, oz.m_b, o2.m_a, o2.m_b, a);
+  if (wide) {
+    smem_optin(reinterpret_cast<const void*>(k_oz_update_w), OZW_SMEM);
+    k_oz_update_w<<<grid, OZ_THREADS, OZW_SMEM, s>>>(oz.m_a, o2.m_a, a);
+  } else {
+    smem_optin(reinterpret_cast<const void*>(k_oz_update), OZ_SMEM);
+    k_oz_update<<<grid, OZ_THREADS, OZ_SMEM, s>>>(oz.m_a, oz.m_b, o2.m_a, o2.m_b, a);
+  }
   SPH_LAUNCH_CHECK();
 }
 
