@@ -1757,7 +1757,18 @@ struct Chol {
     // 16 / 24 / 32 -> 478 / 491 / 510 ms (NCCL exchange, round 2 start: 32
     // best, 379 ms)
     const int dist_reserve = env_reserve ? std::atoi(env_reserve) : (xipc ? 16 : kChainCtas);
-    auto reserve_for = [&](int k) { return D ? dist_reserve : reserve_at(k); };
+    // the last dist_tail steps (chain-bound: the bulk idles behind the panel
+    // and exchange) leave the chain kChainCtas SMs, as on one GPU. C3 2x2:
+    // 0 / 32 / 64 / 128 steps -> 283.6 / 278.6 / 278.0 / 278.7 ms; 2x1: 0 /
+    // 64 -> 471.9 / 476.6 ms, so grids of 4+ ranks only.
+    static const int dist_tail_env = [] {
+      const char* e = std::getenv("SPHEMU_DIST_RESERVE_TAIL");
+      return e ? std::atoi(e) : -1;
+    }();
+    const int dist_tail = dist_tail_env >= 0 ? dist_tail_env : (P * Q >= 4 ? 64 : 0);
+    auto reserve_for = [&](int k) {
+      return D ? (nt - 1 - k > dist_tail ? dist_reserve : std::max(dist_reserve, kChainCtas)) : reserve_at(k);
+    };
     if (!cfg.lookahead) {
       potrf(0, stream);
       panel(0, stream);

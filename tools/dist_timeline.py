@@ -38,8 +38,29 @@ out.append("  stream busy ms: bulk %.1f chain %.1f" % (busy[0], busy[1]))
 for k, x in sorted(agg.items()):
     out.append(f"  {'bulk ' if k[0] == 0 else 'chain'} {k[1]:10s} {x:8.2f} ms")
 rows = sorted(tl, key=lambda x: x[2])
-for i, (ph, s, a, z) in enumerate(rows[w0:w0 + 24]):
-    out.append(f"  {'B' if s == 0 else 'C'} {ph:10s} {a:9.3f} {z:9.3f} {z - a:7.3f}")
+span = max(z for _, _, _, z in tl)
+
+
+def idle_quarters(stream):
+    """Idle ms of `stream` (union of its intervals) in each quarter of the span."""
+    iv = sorted((a, z) for _, s, a, z in tl if s == stream)
+    res = []
+    for q in range(4):
+        lo, hi = span * q / 4, span * (q + 1) / 4
+        cov, cur = 0.0, lo
+        for a, z in iv:
+            a, z = max(a, cur), min(z, hi)
+            if z > a:
+                cov += z - a
+                cur = z
+        res.append(hi - lo - cov)
+    return res
+
+
+out.append("  bulk  idle ms per quarter: " + " ".join("%7.2f" % x for x in idle_quarters(0)))
+out.append("  chain idle ms per quarter: " + " ".join("%7.2f" % x for x in idle_quarters(1)))
+for i, (ph, s, a, z) in enumerate(rows[w0:w0 + 40] if w0 >= 0 else rows[w0:]):
+    out.append(f"  {'BCX'[s]} {ph:10s} {a:9.3f} {z:9.3f} {z - a:7.3f}")
 for r in range(world):
     if r == rank:
         print("\n".join(out), flush=True)

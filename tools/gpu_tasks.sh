@@ -11,6 +11,7 @@
 #   timeline <N> <VARIANT>   chain/bulk stream busy and idle times (tools/chol_timeline.py, timeline_gaps.py)
 #   oz               the INT8 DP-update kernel alone (tools/micro/oz_bench, SPHEMU_OZ_DBG 0/1/2) + tools/oz_check.py
 #   dist <G> <P> [k=v,..]   tools/dist_perf.py on C3 over G GPUs as P x G/P under each assignment
+#                    (k=v+k2=v2 sets several variables for one run)
 #   disttl <G> <P>   per-rank phase totals of the distributed factorization (tools/dist_timeline.py)
 # The round-2 experiments behind the numbers in DESIGN.md were these tasks with the
 # settings quoted there.
@@ -39,7 +40,7 @@ case "$task" in
     python tools/epi_probe.py "$@" ;;
   sweep)
     n=$1; v=$2; hp=$3; IFS=',' read -ra sets <<< "${4:-NONE=1}"
-    for kv in "${sets[@]}"; do echo "$kv"; env "$kv" timeout 300 python tools/ab.py "$n" "$v" "$hp" ${REPS:-3} ${TILE:-512}; done ;;
+    for kv in "${sets[@]}"; do echo "$kv"; env ${kv//+/ } timeout 300 python tools/ab.py "$n" "$v" "$hp" ${REPS:-3} ${TILE:-512}; done ;;
   timeline)
     timeout 600 python tools/chol_timeline.py "$1" ${TILE:-512} "$2" ${HP:-fp16} 2>/dev/null | head -9
     timeout 600 python tools/timeline_gaps.py "$1" "$2" ${HP:-fp16} ;;
@@ -51,8 +52,8 @@ case "$task" in
     g=$1; p=$2; IFS=',' read -ra sets <<< "${3:-NONE=1}"
     script=tools/dist_perf.py; [ "$task" = disttl ] && script=tools/dist_timeline.py
     for kv in "${sets[@]}"; do echo "$kv"
-      env "$kv" timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$g" --master-addr 127.0.0.1 \
-        --master-port 29533 $script ${N:-129600} 512 ${VARIANT:-dpsphp} ${HP:-bf16} "$p" 2>&1 | grep -v "^W\|Warn\|return func\|\*\*\*"
+      env ${kv//+/ } timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$g" --master-addr 127.0.0.1 \
+        --master-port 29533 $script ${N:-129600} 512 ${VARIANT:-dpsphp} ${HP:-bf16} "$p" ${W0:-100} 2>&1 | grep -v "^W\|Warn\|return func\|\*\*\*"
     done ;;
   *)
     echo "unknown task $task"; exit 2 ;;
