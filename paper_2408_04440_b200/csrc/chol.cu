@@ -711,6 +711,7 @@ struct Chol {
   // each launch, a resumed launch continues from its class's counter).
   // SPHEMU_TC_DYN=0 falls back to static striding.
   DevBuf<int> sched_ctr;
+  DevBuf<unsigned> pc_bar;  // k_potrf_coop's split-barrier arrival counter (zero between launches)
   int* ctr(cudaStream_t s, int cls) {
     static const bool on = [] {
       const char* e = std::getenv("SPHEMU_TC_DYN");
@@ -1177,6 +1178,8 @@ struct Chol {
     fail.alloc(1);
     sat.alloc(1);
     sched_ctr.alloc(12);  // [stream: main, chain, bulk2][class 0..2, 3 = panel]
+    pc_bar.alloc(1);
+    SPH_CUDA(cudaMemset(pc_bar.get(), 0, sizeof(unsigned)));
     yield_flag.alloc(1);
     SPH_CUDA(cudaMemset(yield_flag.get(), 0, sizeof(int)));
     // Per-step output-tile lists by precision class.
@@ -2311,7 +2314,8 @@ struct Chol {
     double* lp = linv_[set_of(k)].get();
     double* dp = dinv.get();
     int* fp = fail.get();
-    void* args[] = {&dkk, &bb, &bk, &lp, &dp, &fp, &kk};
+    unsigned* bp = pc_bar.get();
+    void* args[] = {&dkk, &bb, &bk, &lp, &dp, &fp, &kk, &bp};
     SPH_CUDA(cudaLaunchCooperativeKernel((void*)k_potrf_coop, dim3(G), dim3(DG_THREADS), args, smem, s));
     note_launch();
   }

@@ -389,9 +389,17 @@ __device__ __forceinline__ double* blk(double* A, int b, int r, int c) {
 //   phase B: CTA 0 updates block (s+1, s+1) and factors/inverts it (lookahead)
 //            | the rest: A_rc -= X_rs X_cs^T (s < c <= r, not (s+1,s+1))
 //            | TRTRI R_rc -= L_rs X_sc (r > s, c <= s)
+//
+// Barrier A is split: CTA 0 arrives after its phase-A items and goes straight
+// on to the lookahead (it reads nothing the other CTAs write in phase A), so
+// its factor + invert of block (s+1, s+1), the chain's long pole, starts one
+// barrier earlier; the other CTAs wait for every arrival before their
+// trailing updates. *bar counts arrivals (G per step); CTA 0 zeroes it after
+// the last grid.sync, when every CTA is past its last wait.
 __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ A, int b, int bk,
                                                            double* __restrict__ Linv,
-                                                           double* __restrict__ dinv_all, int* fail, int k) {
+                                                           double* __restrict__ dinv_all, int* fail, int k,
+                                                           unsigned* __restrict__ bar) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) uint8_t pc_smem[];
@@ -420,8 +428,14 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
   __threadfence();
   grid.sync();
   PTRACE(2);
+  auto reset_bar = [&] {
+    if (cta == 0 && threadIdx.x == 0) *bar = 0u;
+  };
   for (int s = 0; s < nblk; ++s) {
-    if (*(volatile int*)fail >= 0) return;
+    if (*(volatile int*)fail >= 0) {
+      reset_bar();
+      return;
+    }
     const int w = rows_of(s);
     const double* dinv = dinv_all + (int64_t)s * PC_BLK * PC_BLK;
     // ---- phase A ----
@@ -464,8 +478,18 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
       __syncthreads();
     }
     PTRACE(3 + 4 * s);
-    __threadfence();
-    grid.sync();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(bar, 1u);
+      if (G == 1 || cta > 0) {
+        const unsigned target = static_cast<unsigned>(G) * static_cast<unsigned>(s + 1);
+        while (*(volatile unsigned*)bar < target) {
+        }
+        __threadfence();
+      }
+    }
+    __syncthreads();
     PTRACE(4 + 4 * s);
     // ---- phase B ----
     if (cta == 0) {
@@ -518,6 +542,7 @@ __global__ void __launch_bounds__(DG_THREADS) k_potrf_coop(double* __restrict__ 
     grid.sync();
     PTRACE(6 + 4 * s);
   }
+  reset_bar();
   // Strict upper part to zero (potrf_tile's final loop).
   for (int64_t e = (int64_t)cta * blockDim.x + threadIdx.x; e < (int64_t)b * b; e += (int64_t)G * blockDim.x) {
     const int r = (int)(e / b), c = (int)(e % b);

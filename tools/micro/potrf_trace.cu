@@ -18,6 +18,9 @@ int main() {
   cudaMalloc(&Linv, 8 * b * b);
   cudaMalloc(&dinv, 8 * 64 * 64 * 9);
   cudaMalloc(&fail, 4);
+  unsigned* bar;
+  cudaMalloc(&bar, 4);
+  cudaMemset(bar, 0, 4);
   cudaMalloc(&tr, 8 * 64 * 64);
   cudaMemcpyToSymbol(g_potrf_trace, &tr, sizeof(tr));
   const size_t smem = potrf_coop_smem();
@@ -27,7 +30,7 @@ int main() {
     cudaMemset(fail, 0xff, 4);
     cudaMemset(tr, 0, 8 * 64 * 64);
     int bb = b, bk = b, k = 0;
-    void* args[] = {&A, &bb, &bk, &Linv, &dinv, &fail, &k};
+    void* args[] = {&A, &bb, &bk, &Linv, &dinv, &fail, &k, &bar};
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
