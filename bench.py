@@ -364,10 +364,12 @@ def time_factor(sph, h, wl, args, world, a_dev=None, steps=None, warmup=None, cl
         h.factor()
         return h.wait() if sync else None
 
-    # Inside the timed region only the dominant update class is bracketed by
-    # CUDA events (the roofline's achieved rate); the full phase breakdown
-    # comes from one extra profiled step afterwards.
-    h.set_profiling(True, phases=["update_" + dominant_class(wl)])
+    # Inside the timed region the dominant update class's launches of the
+    # last timed step are bracketed by CUDA events (the roofline's achieved
+    # rate): events around every launch of every step cost 2.4 ms of a 46 ms
+    # C2 step (tools/step_gap.py). The full phase breakdown comes from one
+    # extra profiled step afterwards.
+    h.set_profiling(False)
     clocks = ClockSampler(clocks_index) if clocks_index is not None else None
     if clocks:
         clocks.__enter__()
@@ -382,6 +384,8 @@ def time_factor(sph, h, wl, args, world, a_dev=None, steps=None, warmup=None, cl
         clocks.mark_start()
     start.record()
     for i in range(steps):
+        if i == steps - 1:
+            h.set_profiling(True, phases=["update_" + dominant_class(wl)])
         st = step(sync=(i == steps - 1))
     end.record()
     torch.cuda.synchronize()
@@ -512,7 +516,8 @@ def roofline(h, wl, args, phases, steps, ms):
            "sms": {"bulk_ctas": bulk, "device_sms": n_sm,
                    "note": "the bulk update runs on these CTAs while the POTRF/panel chain holds the rest"},
            "per_launch_basis": f"{cuf[dom_c]/1e12:.3f} TFLOP of {dom_c.upper()}-class update per step on this rank "
-                               f"/ summed launch time {t:.2f} ms (CUDA events on the launching stream)"}
+                               f"/ summed launch time {t:.2f} ms (CUDA events on the launching stream around each "
+                               f"launch of the last timed step)"}
     fl = h.flops()
     t_roof = fl["dp"] / (p_dp * 1e12) + fl["sp"] / (p_sp * 1e12) + fl["hp"] / (p_hp * 1e12)
     world = max(1, args.world)
@@ -845,7 +850,7 @@ def run_ours(args, world, rank, local):
     value = flops / (ms * 1e-3) / 1e12
     phases = h.all_phases
     probe = h.residual_probe(1, 2)
-    dom = roofline(h, wl, args, h.timed_phases, args.steps, ms)
+    dom = roofline(h, wl, args, h.timed_phases, 1, ms)  # the last timed step's launches
     sat = int(st.half_saturations)
     probe_kms = kms_probe(h)
     # emulation from this factor (C2: L = 180; N > 1: the C3 matrix, L = 360)
