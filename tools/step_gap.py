@@ -55,4 +55,7 @@ def run(load=True, factor=True, prof=None):
 
 print("load+factor, no profiling: %.2f ms/step, device_ms %s" % run())
 print("load+factor, update_sp events: %.2f ms/step, device_ms %s" % run(prof=["update_" + ("sp" if v == "dpsp" else "hp")]))
-print("load only: %.2f ms/step" % run(factor=False)[0])
+h.phase_times(reset=True)
+run(prof=["load"])
+pt = h.phase_times()["load"]
+print("load: %.2f ms per call" % (pt["ms"] / max(1, pt["launches"])))
