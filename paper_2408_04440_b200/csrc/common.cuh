@@ -38,6 +38,17 @@ int64_t launch_count();
 // SPHEMU_SYNC_CHECK=1 (debugging): every launch is followed by a device
 // synchronize, so an asynchronous fault is reported at the kernel that raised it.
 bool sync_check();
+// Diagnostic modes (SPHEMU_TC_DBG / SPHEMU_OZ_DBG: skip the MMAs or the
+// epilogue for timing experiments) exist only in a diagnostics build
+// (make DIAG=1); production kernels compile them out.
+#ifdef SPHEMU_DIAG
+#define SPH_DBG(args) ((args).dbg)
+#define SPH_DBG_ENV(name) ([] { const char* e__ = std::getenv(name); return e__ ? std::atoi(e__) : 0; }())
+#else
+#define SPH_DBG(args) 0
+#define SPH_DBG_ENV(name) 0
+#endif
+
 #define SPH_LAUNCH_CHECK()                                                                 \
   do {                                                                                     \
     ::sphemu_gpu::note_launch();                                                           \

@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       for (int kb2 = 0; kb2 < kblocks * halves; ++kb2) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        if (args.dbg == 2) {
+        if (SPH_DBG(args) == 2) {
           if (kb2 == 0)
             for (int d = 0; d < OZ_DIGITS; ++d) mbar_wait(&tempty[d], acc_phase ^ 1);
           umma_commit_elect(&empty[stage]);
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 #pragma unroll 1
       for (int d = 0; d < OZ_DIGITS; ++d) {
         uint32_t x[NH][32];
-        if (!args.dbg) {
+        if (!SPH_DBG(args)) {
 #pragma unroll
           for (int hh = 0; hh < NH; ++hh)
             tmem_ld32_nowait(tmem + (static_cast<uint32_t>(q * 32) << 16) + d * OZ_BN + (h0 + hh) * 32, x[hh]);
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[d]);
-        if (!args.dbg) {
+        if (!SPH_DBG(args)) {
           const double wgt = pow2(-7 * (d + 2));
 #pragma unroll
           for (int hh = 0; hh < NH; ++hh)
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             for (int c = 0; c < 32; ++c) v[hh][c] = fma(static_cast<double>(static_cast<int>(x[hh][c])), wgt, v[hh][c]);
         }
       }
-      if (!args.dbg) {
+      if (!SPH_DBG(args)) {
         const double si = pow2(oz_mu(args.rowexp, min(i * ts.lb + r0 + row, ts.n - 1)));
 #pragma unroll
         for (int hh = 0; hh < NH; ++hh) {
@@ -661,10 +661,7 @@ void oz_update(const TileStore& ts, int k, const int2* list, int64_t cnt, const 
   a.rowexp = rowexp;
   a.fail = fail;
   a.counter = counter;
-  static const int dbg = [] {
-    const char* e = std::getenv("SPHEMU_OZ_DBG");
-    return e ? std::atoi(e) : 0;
-  }();
+  static const int dbg = SPH_DBG_ENV("SPHEMU_OZ_DBG");
   a.dbg = dbg;
   static const int bn = [] {
     const char* e = std::getenv("SPHEMU_OZ_BN");

@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
       // first stages are in flight (a dependent global load here would stall
       // the TMA issue at every item boundary).
       auto prefetch_c = [&](int64_t wi, int2 ij, int crow) {
-        if (MODE != MODE_UPDATE || args.dbg == 1 || args.dbg == 2 || args.dbg == 5 || !(args.opt & 1) || wi >= items)
+        if (MODE != MODE_UPDATE || SPH_DBG(args) == 1 || SPH_DBG(args) == 2 || SPH_DBG(args) == 5 || !(args.opt & 1) || wi >= items)
           return;
         constexpr int kEszP = T::kSplit ? 4 : 2;
         (void)ij;
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
       for (int kb = 0; kb < kblocks * halves; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        if (lane == 0 && args.dbg == 2) {
+        if (lane == 0 && SPH_DBG(args) == 2) {
           if constexpr (CG == 2) umma_commit_cg2(&empty[stage]);
           else umma_commit(&empty[stage]);
         } else if (lane == 0) {
@@ -653,13 +653,13 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
                  (lane & 7) * 16;
 #pragma unroll
       for (int s8 = 0; s8 < 8; ++s8)
-        cpre[s8] = args.dbg == 5 ? make_uint4(0, 0, 0, 0)
+        cpre[s8] = SPH_DBG(args) == 5 ? make_uint4(0, 0, 0, 0)
                                  : ((args.opt & 8) ? __ldcg(reinterpret_cast<const uint4*>(cpre_ptr + s8 * 4 * c_pitch))
                                                    : __ldcs(reinterpret_cast<const uint4*>(cpre_ptr + s8 * 4 * c_pitch)));
     };
     if (MODE == MODE_UPDATE) load_box(0);
 #else
-    if (MODE == MODE_UPDATE && lane == 0 && (args.dbg == 0 || args.dbg >= 3) && args.dbg != 5)
+    if (MODE == MODE_UPDATE && lane == 0 && (SPH_DBG(args) == 0 || SPH_DBG(args) >= 3) && SPH_DBG(args) != 5)
       for (int s = 0; s < R; ++s) issue_c();
 #endif
     for (int64_t n = 0;; ++n) {
@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
 #pragma unroll 1
-        for (int bl = 0; bl < ((args.dbg == 1 || args.dbg == 2) ? 0 : kNBox); ++bl, ++gbox) {
+        for (int bl = 0; bl < ((SPH_DBG(args) == 1 || SPH_DBG(args) == 2) ? 0 : kNBox); ++bl, ++gbox) {
           const int bx = grp + NG * bl;
 #if SPH_TC_REGC
           (void)bx;
@@ -709,11 +709,11 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
           load_box(gbox + 1);
 #else
           const int slot = static_cast<int>(gbox % R);
-          if (args.dbg != 5) mbar_wait(&cf[slot], static_cast<uint32_t>((gbox / R) & 1));
+          if (SPH_DBG(args) != 5) mbar_wait(&cf[slot], static_cast<uint32_t>((gbox / R) & 1));
 #endif
           const uint32_t row_s = smem_addr(cring + slot * Lay::kCBox) + lane * 128;
 #pragma unroll
-          for (int h = 0; h < (args.dbg == 3 ? 0 : kBoxCols / 32); ++h) {
+          for (int h = 0; h < (SPH_DBG(args) == 3 ? 0 : kBoxCols / 32); ++h) {
             uint32_t v[32];
 #if SPH_TC_REGC
             if (h == 0) {
@@ -809,7 +809,7 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
             for (int s8 = 0; s8 < 8; ++s8) {
               const int r = 4 * s8 + (lane >> 3);
               const uint4 v = lds128(sb + r * 128 + (((lane & 7) ^ (r & 7)) << 4));
-              if (args.dbg != 4) {  // the C tile is not read again this step: stream it out
+              if (SPH_DBG(args) != 4) {  // the C tile is not read again this step: stream it out
                 if (args.opt & 8) __stcg(reinterpret_cast<uint4*>(cur_ptr + s8 * 4 * c_pitch), v);
                 else __stcs(reinterpret_cast<uint4*>(cur_ptr + s8 * 4 * c_pitch), v);
               }
@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(TcLayout<BN, OPK, MODE, CG>::kThreads, 1)
           if (lane == 0) {
             int bi, bj, bm, bn;
             decode(w, bi, bj, bm, bn);
-            if (args.dbg != 3 && args.dbg != 4)
+            if (SPH_DBG(args) != 3 && SPH_DBG(args) != 4)
               tma_store_2d(&mC, cring + slot * Lay::kCBox, bn + bx * kBoxCols, c_row(w) + bm + q * 32);
             bulk_commit();
             if (R == 1) {
@@ -1276,10 +1276,7 @@ void tc_update(const TileStore& ts, int k, int cls, int hp_format, const int2* l
   a.sat = sat;
   a.rowexp = pf.rowexp;
   a.lb = ts.lb;
-  static const int dbg = [] {
-    const char* e = std::getenv("SPHEMU_TC_DBG");
-    return e ? std::atoi(e) : 0;
-  }();
+  static const int dbg = SPH_DBG_ENV("SPHEMU_TC_DBG");
   a.dbg = dbg;
   a.counter = counter;
   static const int opt = [] {

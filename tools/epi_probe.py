@@ -1,4 +1,5 @@
-"""Diagnostics for the update kernel (SPHEMU_TC_DBG modes): factor a strongly
+"""Diagnostics for the update kernel (SPHEMU_TC_DBG modes; a diagnostics build,
+make -C paper_2408_04440_b200/csrc DIAG=1 -B): factor a strongly
 diagonally dominant matrix, which stays positive definite even when a
 diagnostic mode skips parts of the C epilogue, and print the busy time of the
 dominant update class (tools/epi_probe.py N VARIANT HP_FORMAT)."""

@@ -36,7 +36,8 @@ case "$task" in
     timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c ${COUNT:-20000} --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 > gpurun_out/ncu_launches.log 2>&1; echo "EXIT $?" ;;
   ncu)
     timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:$1" -s ${2:-5} -c 1 -o gpurun_out/ncu_${NAME:-kernel} -f python ${SCRIPT:-bench.py} ${SCRIPT_ARGS:---steps 1 --warmup 3} > gpurun_out/ncu_${NAME:-kernel}.log 2>&1; echo "EXIT $?" ;;
-  epi)
+  epi)  # the SPHEMU_TC_DBG modes exist only in a diagnostics build
+    make -C paper_2408_04440_b200/csrc DIAG=1 -B -j8 > /dev/null
     python tools/epi_probe.py "$@" ;;
   sweep)
     n=$1; v=$2; hp=$3; IFS=',' read -ra sets <<< "${4:-NONE=1}"
@@ -44,7 +45,8 @@ case "$task" in
   timeline)
     timeout 600 python tools/chol_timeline.py "$1" ${TILE:-512} "$2" ${HP:-fp16} 2>/dev/null | head -9
     timeout 600 python tools/timeline_gaps.py "$1" "$2" ${HP:-fp16} ;;
-  oz)
+  oz)  # the SPHEMU_OZ_DBG modes exist only in a diagnostics build
+    make -C paper_2408_04440_b200/csrc DIAG=1 -B -j8 > /dev/null
     tools/micro/build_oz_bench.sh
     for d in 0 1 2; do echo "SPHEMU_OZ_DBG=$d"; SPHEMU_OZ_DBG=$d timeout 60 ./tools/micro/oz_bench; done
     timeout 900 python tools/oz_check.py 4096 512 ;;
